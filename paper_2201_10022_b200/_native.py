@@ -1,0 +1,348 @@
+"""ctypes binding of the C-ABI in include/abd_b200.h (libabd_b200.so).
+
+There is no CPU fallback: every compute entry goes to the sm_100a kernels,
+and a missing library or GPU raises immediately (RuntimeError).  Status
+codes map back to the reference's exception types.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import weakref
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libabd_b200.so")
+
+ABD_OK, ABD_ERR_ARG, ABD_ERR_CUDA, ABD_ERR_BARRIER_DOMAIN, ABD_ERR_CCD_DOMAIN = 0, 1, 2, 3, 4
+ABD_ERR_FACTORIZATION, ABD_ERR_STEP_FAILURE, ABD_ERR_NO_DEVICE, ABD_ERR_NOT_CONVERGED = 5, 6, 7, 8
+VF, EE = 0, 1
+
+_lib = None
+
+dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+lp = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+ip32 = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+up8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+i64 = C.c_int64
+i32 = C.c_int
+dbl = C.c_double
+vp = C.c_void_p
+
+
+class StepParamsC(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("dt", "d_hat", "kappa_barrier", "mu", "epsilon_v", "newton_tol",
+                                          "ccd_slack", "ccd_step_scale", "pcg_rel_tol")] + \
+               [(n, C.c_int) for n in ("max_newton_iters", "friction_outer_iters", "pcg_max_iters",
+                                      "compute_min_distance")]
+
+
+class StepStatsC(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("iterations", "converged", "nondescent_fallbacks", "pcg_iters_total")] + \
+               [("candidates", C.c_int64)] + \
+               [(n, C.c_double) for n in ("min_distance", "ip_value", "max_ortho_error", "last_dq_over_dt",
+                                          "t_broad", "t_assemble", "t_solve", "t_ccd", "t_line_search", "t_total")]
+
+
+_SIGS = {
+    "abd_last_error": (C.c_char_p, []),
+    "abd_last_error_index": (i64, []),
+    "abd_kernel_launches": (i64, []),
+    "abd_device_info": (i32, [C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
+    "abd_pt_closest_batch": (i32, [i64, dp, dp, ip32, dp]),
+    "abd_ee_closest_batch": (i32, [i64, dp, dp, ip32, dp, dp]),
+    "abd_pair_distance_gradients": (i32, [i32, i64, dp, dp, dp, dp, ip32, dp]),
+    "abd_ee_mollifier_batch": (i32, [i64, dp, dp, dp, vp, vp]),
+    "abd_barrier_batch": (i32, [i64, dp, dbl, dp, dp, dp]),
+    "abd_ortho_batch": (i32, [i64, dp, dp, i32, dp, dp, dp]),
+    "abd_project_psd_batch": (i32, [i64, i32, dp, dp]),
+    "abd_accd_batch": (i32, [i32, i64, dp, dp, dbl, dbl, i32, dp]),
+    "abd_friction_batch": (i32, [i64, lp, lp, dp, dbl, dp, dp, i32, dp, up8, dbl, dbl, i32, vp, vp, vp]),
+    "abd_bsr_matvec": (i32, [i32, i32, dp, i64, lp, dp, dp, dp]),
+    "abd_bsr_pcg": (i32, [i32, i32, dp, i64, lp, dp, dp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
+    "abd_scene_create": (vp, [i32, lp, lp, lp, dp, lp, lp, dp, up8, dp, dp]),
+    "abd_scene_destroy": (None, [vp]),
+    "abd_broad_phase": (i32, [vp, dp, dp, dbl, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+    "abd_get_candidates": (i32, [vp, lp, lp, lp]),
+    "abd_set_candidates": (i32, [vp, i64, lp, i64, lp, i64, lp]),
+    "abd_contact_energy": (i32, [vp, dp, dbl, dbl, C.POINTER(dbl)]),
+    "abd_candidate_min_d2": (i32, [vp, dp, C.POINTER(dbl)]),
+    "abd_global_min_distance": (i32, [vp, dp, C.POINTER(dbl)]),
+    "abd_contact_gradient_hessian": (i32, [vp, dp, dbl, dbl, i32, C.POINTER(i64)]),
+    "abd_get_pair_blocks": (i32, [vp, lp, lp, dp, dp, dp]),
+    "abd_friction_precompute": (i32, [vp, dp, dbl, dbl, dbl, C.POINTER(i64)]),
+    "abd_get_friction": (i32, [vp, lp, lp, dp, dp, dp, dp]),
+    "abd_set_friction": (i32, [vp, i64, lp, lp, dp, dbl, dp, dp]),
+    "abd_step_filter": (i32, [vp, dp, dp, dbl, C.POINTER(dbl)]),
+    "abd_compute_q_tilde": (i32, [vp, dp, dp, dp, dbl, dp]),
+    "abd_ip_value": (i32, [vp, dp, dp, dbl, dbl, dbl, dbl, C.POINTER(dbl)]),
+    "abd_assemble": (i32, [vp, dp, dp, dbl, dbl, dbl, dbl, C.POINTER(i64)]),
+    "abd_get_system": (i32, [vp, dp, dp, lp, dp]),
+    "abd_solve_resident": (i32, [vp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
+    "abd_set_state": (i32, [vp, vp, vp]),
+    "abd_get_state": (i32, [vp, vp, vp]),
+    "abd_advance_step": (i32, [vp, vp, C.POINTER(StepParamsC), C.POINTER(StepStatsC), vp]),
+}
+
+
+def lib():
+    """Load libabd_b200.so (RuntimeError if it is missing: no CPU fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} not found: build the sm_100a kernels first "
+            "(python -m paper_2201_10022_b200.build); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def check(rc):
+    if rc == ABD_OK:
+        return
+    L = lib()
+    msg = L.abd_last_error().decode()
+    idx = int(L.abd_last_error_index())
+    from . import contact, sparse, solver  # exception types live with their reference modules
+    if rc == ABD_ERR_BARRIER_DOMAIN:
+        raise contact.BarrierDomainError(msg)
+    if rc in (ABD_ERR_CCD_DOMAIN, ABD_ERR_ARG):
+        raise ValueError(msg)
+    if rc == ABD_ERR_FACTORIZATION:
+        raise sparse.FactorizationError(idx)
+    if rc == ABD_ERR_STEP_FAILURE:
+        raise solver.StepFailure(msg)
+    if rc == ABD_ERR_NOT_CONVERGED:
+        raise sparse.PcgNotConverged(msg)
+    raise NativeError(msg)
+
+
+def f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if shape is None else a.reshape(shape)
+
+
+def i64a(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    return a if shape is None else a.reshape(shape)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def kernel_launches() -> int:
+    return int(lib().abd_kernel_launches())
+
+
+# ---------------------------------------------------------------------------
+# stateless batch wrappers
+
+def pt_closest(z):
+    z = f64(z).reshape(-1, 4, 3)
+    n = len(z)
+    d2, reg, bary = np.empty(n), np.empty(n, dtype=np.int32), np.empty((n, 3))
+    check(lib().abd_pt_closest_batch(n, z, d2, reg, bary))
+    return d2, reg.astype(np.int64), bary
+
+
+def ee_closest(z):
+    z = f64(z).reshape(-1, 4, 3)
+    n = len(z)
+    d2, reg, s, t = np.empty(n), np.empty(n, dtype=np.int32), np.empty(n), np.empty(n)
+    check(lib().abd_ee_closest_batch(n, z, d2, reg, s, t))
+    return d2, reg.astype(np.int64), s, t
+
+
+def d2_derivatives(kind, z):
+    z = f64(z).reshape(-1, 4, 3)
+    n = len(z)
+    d2, g, h = np.empty(n), np.empty((n, 12)), np.empty((n, 12, 12))
+    reg, gam = np.empty(n, dtype=np.int32), np.empty((n, 4))
+    check(lib().abd_pair_distance_gradients(VF if kind == "vf" else EE, n, z, d2, g, h, reg, gam))
+    return d2, g, h, reg.astype(np.int64), gam
+
+
+def mollifier(z, eps, derivs=True):
+    z = f64(z).reshape(-1, 4, 3)
+    n = len(z)
+    eps = f64(np.broadcast_to(np.asarray(eps, dtype=float), (n,)))
+    val = np.empty(n)
+    g = np.empty((n, 12)) if derivs else None
+    h = np.empty((n, 12, 12)) if derivs else None
+    check(lib().abd_ee_mollifier_batch(n, z, eps, val, _ptr(g), _ptr(h)))
+    return (val, g, h) if derivs else val
+
+
+def barrier_batch(s, d_hat):
+    s = f64(s).reshape(-1)
+    n = len(s)
+    b0, b1, b2 = np.empty(n), np.empty(n), np.empty(n)
+    check(lib().abd_barrier_batch(n, s, float(d_hat), b0, b1, b2))
+    return b0, b1, b2
+
+
+def ortho_batch(q, k, project):
+    q = f64(q).reshape(-1, 12)
+    n = len(q)
+    e, g, h = np.empty(n), np.empty((n, 12)), np.empty((n, 12, 12))
+    check(lib().abd_ortho_batch(n, q, f64(k).reshape(n), int(project), e, g, h))
+    return e, g, h
+
+
+def project_psd_batch(H):
+    H = f64(H)
+    n, k = H.shape[0], H.shape[-1]
+    out = np.empty_like(H)
+    if n:
+        check(lib().abd_project_psd_batch(n, k, H, out))
+    return out
+
+
+def accd_batch(kind, x, dx, slack, t_max, max_iters):
+    x = f64(x).reshape(-1, 4, 3)
+    dx = f64(dx).reshape(-1, 4, 3)
+    n = len(x)
+    t = np.empty(n)
+    if n:
+        check(lib().abd_accd_batch(VF if kind in ("vf", "vertex-face") else EE, n, x, dx, float(slack),
+                                   float(t_max), int(max_iters), t))
+    return t
+
+
+def friction_batch(data, q_all, dynamic, dt, eps_v, project, want_blocks):
+    n = len(data.lam)
+    q = f64(q_all).reshape(-1, 12)
+    nb = len(q)
+    dyn = np.ascontiguousarray(np.asarray(dynamic, dtype=np.uint8).reshape(nb))
+    e = np.empty(1)
+    g = np.empty((n, 24)) if want_blocks else None
+    h = np.empty((n, 24, 24)) if want_blocks else None
+    check(lib().abd_friction_batch(n, i64a(data.body_a), i64a(data.body_b), f64(data.lam), float(data.mu),
+                                   f64(data.tangent_map), f64(data.offset), nb, q, dyn, float(dt), float(eps_v),
+                                   int(project), _ptr(e), _ptr(g), _ptr(h)))
+    return float(e[0]), g, h
+
+
+def bsr_matvec(n, bdim, diag, keys, off, x):
+    y = np.empty(n * bdim)
+    check(lib().abd_bsr_matvec(n, bdim, f64(diag), len(keys), i64a(keys).reshape(-1), f64(off),
+                               f64(x).reshape(-1), y))
+    return y
+
+
+def bsr_pcg(n, bdim, diag, keys, off, rhs, rel_tol=1e-8, max_iters=100000):
+    x = np.empty(n * bdim)
+    it, rel = C.c_int(0), C.c_double(0.0)
+    check(lib().abd_bsr_pcg(n, bdim, f64(diag), len(keys), i64a(keys).reshape(-1), f64(off),
+                            f64(rhs).reshape(-1), float(rel_tol), int(max_iters), x, C.byref(it), C.byref(rel)))
+    return x, it.value, rel.value
+
+
+# ---------------------------------------------------------------------------
+# scene contexts (device-resident geometry), cached per tuple of bodies
+
+class Scene:
+    """Owns an abd_scene*; geometry uploaded once from CollisionBody arrays."""
+
+    def __init__(self, bodies, masses=None, stiffness=None):
+        L = lib()
+        B = len(bodies)
+        self.n_bodies = B
+        v_off = np.cumsum([0] + [len(b.rest) for b in bodies]).astype(np.int64)
+        e_off = np.cumsum([0] + [len(b.edges) for b in bodies]).astype(np.int64)
+        t_off = np.cumsum([0] + [len(b.triangles) for b in bodies]).astype(np.int64)
+        cat = lambda xs, w, dt: (np.concatenate([np.asarray(x, dtype=dt).reshape(-1, w) for x in xs])  # noqa: E731
+                                 if B else np.zeros((0, w), dtype=dt))
+        rest = f64(cat([b.rest for b in bodies], 3, np.float64))
+        edges = i64a(cat([b.edges for b in bodies], 2, np.int64))
+        tris = i64a(cat([b.triangles for b in bodies], 3, np.int64))
+        el2 = f64(np.concatenate([np.asarray(b.edge_rest_len_sq, dtype=float).reshape(-1) for b in bodies])
+                  if B else np.zeros(0))
+        dyn = np.ascontiguousarray(np.array([bool(b.dynamic) for b in bodies], dtype=np.uint8))
+        M = np.zeros((B, 12, 12))
+        K = np.zeros(B)
+        if masses is not None:
+            for i, m in enumerate(masses):
+                if m is not None:
+                    M[i] = m
+        if stiffness is not None:
+            for i, k in enumerate(stiffness):
+                if k is not None:
+                    K[i] = k
+        self.dynamic = dyn.astype(bool)
+        self.ptr = L.abd_scene_create(B, v_off, e_off, t_off, rest, edges, tris, el2, dyn, f64(M), f64(K))
+        if not self.ptr:
+            check(ABD_ERR_CUDA if L.abd_last_error() else ABD_ERR_NO_DEVICE)
+            raise NativeError(L.abd_last_error().decode())
+        self._fin = weakref.finalize(self, L.abd_scene_destroy, self.ptr)
+        self._cand_key = None
+        self._fric_key = None
+
+    def q(self, q):
+        return f64(q).reshape(self.n_bodies, 12)
+
+    # candidate / friction residency
+    def set_candidates(self, cands):
+        key = (id(cands), id(cands.vf), id(cands.ee), id(cands.overlap_pairs))
+        if getattr(cands, "_resident", None) is self and self._cand_key == key:
+            return
+        vf, ee, ov = i64a(cands.vf).reshape(-1, 4), i64a(cands.ee).reshape(-1, 4), i64a(cands.overlap_pairs).reshape(-1, 2)
+        check(lib().abd_set_candidates(self.ptr, len(vf), vf, len(ee), ee, len(ov), ov))
+        self._cand_key = key
+        try:
+            cands._resident = self
+        except AttributeError:
+            pass
+
+    def set_friction(self, fr):
+        key = (id(fr), id(fr.lam), fr.lam.tobytes() if len(fr.lam) < 4096 else id(fr.lam))
+        if self._fric_key == key:
+            return
+        n = len(fr.lam)
+        check(lib().abd_set_friction(self.ptr, n, i64a(fr.body_a), i64a(fr.body_b), f64(fr.lam), float(fr.mu),
+                                     f64(fr.tangent_map).reshape(-1), f64(fr.offset).reshape(-1)))
+        self._fric_key = key
+
+    def broad_phase(self, q0, q1, d_hat):
+        a, b, c = i64(0), i64(0), i64(0)
+        check(lib().abd_broad_phase(self.ptr, self.q(q0), self.q(q1), float(d_hat), C.byref(a), C.byref(b),
+                                    C.byref(c)))
+        vf = np.empty((a.value, 4), dtype=np.int64)
+        ee = np.empty((b.value, 4), dtype=np.int64)
+        ov = np.empty((c.value, 2), dtype=np.int64)
+        check(lib().abd_get_candidates(self.ptr, vf, ee, ov))
+        return vf, ee, ov
+
+
+_SCENES: dict = {}
+
+
+def scene_for(bodies, masses=None, stiffness=None, key_extra=()):
+    """Context cached on the identity of the (immutable) body records."""
+    key = tuple(id(b) for b in bodies) + tuple(key_extra)
+    ent = _SCENES.get(key)
+    if ent is not None and all(r() is b for r, b in zip(ent[1], bodies)):
+        return ent[0]
+    sc = Scene(bodies, masses, stiffness)
+    refs = []
+    for b in bodies:
+        try:
+            refs.append(weakref.ref(b))
+        except TypeError:
+            refs.append(lambda b=b: b)
+    if len(_SCENES) > 16:
+        _SCENES.pop(next(iter(_SCENES)))
+    _SCENES[key] = (sc, refs)
+    return sc

@@ -1,0 +1,712 @@
+// extern "C" boundary (include/abd_b200.h): host buffers in, host buffers
+// out; exceptions mapped to abd_status + thread-local message.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "driver.h"
+
+using namespace abd;
+
+namespace abd {
+extern std::atomic<int64_t> g_launches;
+}
+
+struct abd_scene {
+  Scene s;
+};
+
+static thread_local std::string t_err;
+static thread_local int64_t t_err_idx = -1;
+
+template <class F>
+static int guard(F&& f) {
+  try {
+    f();
+    return ABD_OK;
+  } catch (Error& e) {
+    t_err = e.what();
+    t_err_idx = e.index;
+    return e.code;
+  } catch (std::exception& e) {
+    t_err = e.what();
+    t_err_idx = -1;
+    return ABD_ERR_CUDA;
+  }
+}
+
+static void ensure_device() {
+  static int ok = -1;
+  if (ok == 1) return;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw Error(ABD_ERR_NO_DEVICE, "no CUDA device visible (the sm_100a kernels need a B200)");
+  }
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, 0));
+  if (p.major != 10) throw Error(ABD_ERR_NO_DEVICE, "device is not sm_100 (Blackwell B200 required)");
+  ok = 1;
+}
+
+// RAII device staging buffer
+template <class T>
+struct Dev {
+  DVec<T> v;
+  cudaStream_t st;
+  explicit Dev(cudaStream_t s) : st(s) {}
+  T* up(const T* h, size_t n) {
+    v.upload(h, std::max<size_t>(n, 0), st);
+    if (!n) v.resize(1);
+    return v.p;
+  }
+  T* alloc(size_t n) {
+    v.resize(std::max<size_t>(n, 1));
+    return v.p;
+  }
+  void down(T* h, size_t n) {
+    if (h && n) v.download(h, n, st);
+  }
+};
+
+static cudaStream_t g_stream() {
+  static cudaStream_t s = nullptr;
+  if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+static void sync(cudaStream_t s) { CK(cudaStreamSynchronize(s)); }
+
+static void check_flag(Dev<int>& f, cudaStream_t st, int code, const char* msg) {
+  int h = 0;
+  f.down(&h, 1);
+  sync(st);
+  if (h) throw Error(code, msg);
+}
+
+extern "C" {
+
+const char* abd_last_error(void) { return t_err.c_str(); }
+int64_t abd_last_error_index(void) { return t_err_idx; }
+int64_t abd_kernel_launches(void) { return g_launches.load(); }
+
+int abd_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  return guard([&] {
+    ensure_device();
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, 0));
+    if (sm_count) *sm_count = p.multiProcessorCount;
+    if (cc_major) *cc_major = p.major;
+    if (cc_minor) *cc_minor = p.minor;
+  });
+}
+
+int abd_pt_closest_batch(int64_t n, const double* z, double* d2, int32_t* region, double* bary) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> dz(st), dd(st), db(st);
+    Dev<int> dr(st);
+    launch_pt_closest(st, n, dz.up(z, 12 * n), dd.alloc(n), dr.alloc(n), db.alloc(3 * n));
+    dd.down(d2, n);
+    dr.down(region, n);
+    db.down(bary, 3 * n);
+    sync(st);
+  });
+}
+
+int abd_ee_closest_batch(int64_t n, const double* z, double* d2, int32_t* region, double* s, double* t) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> dz(st), dd(st), ds(st), dt(st);
+    Dev<int> dr(st);
+    launch_ee_closest(st, n, dz.up(z, 12 * n), dd.alloc(n), dr.alloc(n), ds.alloc(n), dt.alloc(n));
+    dd.down(d2, n);
+    dr.down(region, n);
+    ds.down(s, n);
+    dt.down(t, n);
+    sync(st);
+  });
+}
+
+int abd_pair_distance_gradients(int kind, int64_t n, const double* z, double* d2, double* grad, double* hess,
+                                int32_t* region, double* gamma) {
+  return guard([&] {
+    ensure_device();
+    if (kind != ABD_VF && kind != ABD_EE) throw Error(ABD_ERR_ARG, "unknown pair kind");
+    cudaStream_t st = g_stream();
+    Dev<double> dz(st), dd(st), dg(st), dh(st), dga(st);
+    Dev<int> dr(st);
+    launch_d2_derivs(st, kind, n, dz.up(z, 12 * n), dd.alloc(n), dg.alloc(12 * n), dh.alloc(144 * n), dr.alloc(n),
+                     dga.alloc(4 * n));
+    dd.down(d2, n);
+    dg.down(grad, 12 * n);
+    dh.down(hess, 144 * n);
+    dr.down(region, n);
+    dga.down(gamma, 4 * n);
+    sync(st);
+  });
+}
+
+int abd_ee_mollifier_batch(int64_t n, const double* z, const double* eps_x, double* val, double* grad, double* hess) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> dz(st), de(st), dv(st), dg(st), dh(st);
+    bool full = grad && hess;
+    launch_mollifier(st, n, dz.up(z, 12 * n), de.up(eps_x, n), dv.alloc(n), full ? dg.alloc(12 * n) : nullptr,
+                     full ? dh.alloc(144 * n) : nullptr);
+    dv.down(val, n);
+    if (full) {
+      dg.down(grad, 12 * n);
+      dh.down(hess, 144 * n);
+    }
+    sync(st);
+  });
+}
+
+int abd_barrier_batch(int64_t n, const double* d_sq, double d_hat, double* b0, double* b1, double* b2) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> ds(st), o0(st), o1(st), o2(st);
+    Dev<int> err(st);
+    err.alloc(1);
+    err.v.zero(st);
+    launch_barrier(st, n, ds.up(d_sq, n), d_hat, o0.alloc(n), o1.alloc(n), o2.alloc(n), err.v.p);
+    check_flag(err, st, ABD_ERR_BARRIER_DOMAIN,
+               "barrier evaluated at non-positive squared distance (intersection reached; CCD filtering must "
+               "prevent this)");
+    o0.down(b0, n);
+    o1.down(b1, n);
+    o2.down(b2, n);
+    sync(st);
+  });
+}
+
+int abd_ortho_batch(int64_t n, const double* q, const double* stiffness, int project, double* energy, double* grad,
+                    double* hess) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> dq(st), dk(st), de(st), dg(st), dh(st);
+    launch_ortho(st, n, dq.up(q, 12 * n), dk.up(stiffness, n), project, de.alloc(n), dg.alloc(12 * n),
+                 dh.alloc(144 * n));
+    de.down(energy, n);
+    dg.down(grad, 12 * n);
+    dh.down(hess, 144 * n);
+    sync(st);
+  });
+}
+
+int abd_project_psd_batch(int64_t n, int k, const double* H, double* out) {
+  return guard([&] {
+    ensure_device();
+    if (k < 1 || k > 24) throw Error(ABD_ERR_ARG, "project_psd supports 1 <= k <= 24");
+    cudaStream_t st = g_stream();
+    Dev<double> di(st), dout(st);
+    launch_psd(st, n, k, di.up(H, (size_t)n * k * k), dout.alloc((size_t)n * k * k));
+    dout.down(out, (size_t)n * k * k);
+    sync(st);
+  });
+}
+
+int abd_accd_batch(int kind, int64_t n, const double* x, const double* dx, double slack, double t_max, int max_iters,
+                   double* t) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> dxv(st), ddx(st), dt(st);
+    Dev<int> err(st);
+    err.alloc(1);
+    err.v.zero(st);
+    launch_accd(st, kind, n, dxv.up(x, 12 * n), ddx.up(dx, 12 * n), slack, t_max, max_iters, dt.alloc(n), err.v.p);
+    check_flag(err, st, ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
+    dt.down(t, n);
+    sync(st);
+  });
+}
+
+static void pack_friction(int64_t n, const int64_t* ba, const int64_t* bb, const double* lam, const double* tmap,
+                          const double* off, std::vector<int2>& hb, std::vector<double>& hr) {
+  hb.resize(std::max<int64_t>(n, 1));
+  hr.resize(std::max<int64_t>(n, 1) * FRIC_STRIDE);
+  for (int64_t i = 0; i < n; ++i) {
+    hb[i] = make_int2((int)ba[i], (int)bb[i]);
+    std::memcpy(&hr[i * FRIC_STRIDE], tmap + 48 * i, 48 * sizeof(double));
+    hr[i * FRIC_STRIDE + 48] = off[2 * i];
+    hr[i * FRIC_STRIDE + 49] = off[2 * i + 1];
+    hr[i * FRIC_STRIDE + 50] = lam[i];
+  }
+}
+
+int abd_friction_batch(int64_t n, const int64_t* body_a, const int64_t* body_b, const double* lam, double mu,
+                       const double* tangent_map, const double* offset, int n_bodies, const double* q,
+                       const uint8_t* dynamic, double dt, double eps_v, int project, double* energy, double* grad24,
+                       double* hess24) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    std::vector<int2> hb;
+    std::vector<double> hr;
+    pack_friction(n, body_a, body_b, lam, tangent_map, offset, hb, hr);
+    Dev<int2> db(st);
+    Dev<double> dr(st), dq(st), part(st), dg(st), dh(st);
+    Dev<unsigned char> dd(st);
+    db.up(hb.data(), hb.size());
+    dr.up(hr.data(), hr.size());
+    dq.up(q, 12 * (size_t)n_bodies);
+    dd.up(dynamic, n_bodies);
+    bool want = grad24 && hess24;
+    launch_friction(st, n, db.v.p, dr.v.p, mu, dq.v.p, dd.v.p, dt, eps_v, project, part.alloc(RED_BLOCKS),
+                    want ? dg.alloc(24 * n) : nullptr, want ? dh.alloc(576 * n) : nullptr, nullptr);
+    if (energy) {
+      Dev<double> one(st);
+      one.alloc(1);
+      reduce_fixed_stream(st, part.v.p, RED_BLOCKS, one.v.p);  // deterministic fixed-order sum
+      one.down(energy, 1);
+    }
+    if (want) {
+      dg.down(grad24, 24 * n);
+      dh.down(hess24, 576 * n);
+    }
+    sync(st);
+  });
+}
+
+static Scene& bsr_scene() {
+  static thread_local Scene* s = nullptr;
+  if (!s) s = new Scene();
+  return *s;
+}
+
+static void pad_vec(int n, int bdim, const double* in, std::vector<double>& out) {
+  out.assign(12 * (size_t)n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < bdim; ++c) out[12 * (size_t)i + c] = in[(size_t)bdim * i + c];
+}
+
+int abd_bsr_matvec(int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off,
+                   const double* x, double* y) {
+  return guard([&] {
+    ensure_device();
+    if (bdim < 1 || bdim > 12) throw Error(ABD_ERR_ARG, "block_dim must be in [1, 12]");
+    Scene& s = bsr_scene();
+    load_bsr(s, n, bdim, diag, n_off, keys, off);
+    std::vector<double> xp;
+    pad_vec(n, bdim, x, xp);
+    DVec<double> dx, dy;
+    dx.upload(xp.data(), xp.size(), s.stream);
+    dy.resize(std::max<size_t>(xp.size(), 1));
+    spmv(s, dx.p, dy.p);
+    std::vector<double> yp(xp.size());
+    dy.download(yp.data(), yp.size(), s.stream);
+    sync(s.stream);
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < bdim; ++c) y[(size_t)bdim * i + c] = yp[12 * (size_t)i + c];
+  });
+}
+
+int abd_bsr_pcg(int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off,
+                const double* rhs, double rel_tol, int max_iters, double* x, int* iters, double* rel_res) {
+  return guard([&] {
+    ensure_device();
+    if (bdim < 1 || bdim > 12) throw Error(ABD_ERR_ARG, "block_dim must be in [1, 12]");
+    Scene& s = bsr_scene();
+    load_bsr(s, n, bdim, diag, n_off, keys, off);
+    std::vector<double> bp;
+    pad_vec(n, bdim, rhs, bp);
+    DVec<double> db, dx;
+    db.upload(bp.data(), bp.size(), s.stream);
+    dx.resize(std::max<size_t>(bp.size(), 1));
+    double rel = 0.0;
+    int it = pcg_solve(s, db.p, dx.p, rel_tol, max_iters, rel);
+    std::vector<double> xp(bp.size());
+    dx.download(xp.data(), xp.size(), s.stream);
+    sync(s.stream);
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < bdim; ++c) x[(size_t)bdim * i + c] = xp[12 * (size_t)i + c];
+    if (iters) *iters = it;
+    if (rel_res) *rel_res = rel;
+  });
+}
+
+// ---------------------------------------------------------------------------
+abd_scene* abd_scene_create(int n_bodies, const int64_t* v_off, const int64_t* e_off, const int64_t* t_off,
+                            const double* rest, const int64_t* edges, const int64_t* tris, const double* edge_len_sq,
+                            const uint8_t* dynamic, const double* mass, const double* stiffness) {
+  abd_scene* out = nullptr;
+  int rc = guard([&] {
+    ensure_device();
+    if (n_bodies < 0) throw Error(ABD_ERR_ARG, "n_bodies < 0");
+    auto* h = new abd_scene();
+    Scene& s = h->s;
+    int B = n_bodies;
+    s.B = B;
+    s.V = v_off[B];
+    s.E = e_off[B];
+    s.T = t_off[B];
+    if (s.V >= (1ll << 31) || s.E >= (1ll << 31) || s.T >= (1ll << 31)) throw Error(ABD_ERR_ARG, "scene too large");
+    std::vector<int> vo(B + 1), eo(B + 1), to(B + 1), vb(s.V), eb(s.E), tb(s.T);
+    std::vector<int> ge(2 * s.E), gt(3 * s.T);
+    for (int b = 0; b <= B; ++b) {
+      vo[b] = (int)v_off[b];
+      eo[b] = (int)e_off[b];
+      to[b] = (int)t_off[b];
+    }
+    for (int b = 0; b < B; ++b) {
+      s.max_v = std::max(s.max_v, vo[b + 1] - vo[b]);
+      s.max_e = std::max(s.max_e, eo[b + 1] - eo[b]);
+      s.max_t = std::max(s.max_t, to[b + 1] - to[b]);
+      for (int v = vo[b]; v < vo[b + 1]; ++v) vb[v] = b;
+      for (int e = eo[b]; e < eo[b + 1]; ++e) {
+        eb[e] = b;
+        for (int k = 0; k < 2; ++k) {
+          int64_t lv = edges[2 * e + k];
+          if (lv < 0 || lv >= vo[b + 1] - vo[b]) throw Error(ABD_ERR_ARG, "edge index out of range");
+          ge[2 * e + k] = vo[b] + (int)lv;
+        }
+      }
+      for (int t = to[b]; t < to[b + 1]; ++t) {
+        tb[t] = b;
+        for (int k = 0; k < 3; ++k) {
+          int64_t lv = tris[3 * t + k];
+          if (lv < 0 || lv >= vo[b + 1] - vo[b]) throw Error(ABD_ERR_ARG, "triangle index out of range");
+          gt[3 * t + k] = vo[b] + (int)lv;
+        }
+      }
+    }
+    cudaStream_t st = s.stream;
+    s.v_off.upload(vo.data(), B + 1, st);
+    s.e_off.upload(eo.data(), B + 1, st);
+    s.t_off.upload(to.data(), B + 1, st);
+    s.rest.upload(rest, 3 * s.V, st);
+    s.edges.upload(ge.data(), 2 * s.E, st);
+    s.tris.upload(gt.data(), 3 * s.T, st);
+    s.elen2.upload(edge_len_sq, s.E, st);
+    s.vert_body.upload(vb.data(), s.V, st);
+    s.edge_body.upload(eb.data(), s.E, st);
+    s.tri_body.upload(tb.data(), s.T, st);
+    s.h_dyn.assign(dynamic, dynamic + B);
+    s.dyn.upload(s.h_dyn.data(), B, st);
+    s.h_slot.assign(B, -1);
+    s.h_dyn_body.clear();
+    for (int b = 0; b < B; ++b)
+      if (dynamic[b]) {
+        s.h_slot[b] = (int)s.h_dyn_body.size();
+        s.h_dyn_body.push_back(b);
+      }
+    s.n_dyn = (int)s.h_dyn_body.size();
+    s.slot.upload(s.h_slot.data(), B, st);
+    s.dyn_body.upload(s.h_dyn_body.data(), std::max(s.n_dyn, 0), st);
+    if (s.n_dyn == 0) s.dyn_body.resize(1);
+    s.mass.upload(mass, 144 * (size_t)B, st);
+    s.stiff.upload(stiffness, B, st);
+    s.q.resize(12 * (size_t)B);
+    s.q.zero(st);
+    s.q_dot.resize(12 * (size_t)B);
+    s.q_dot.zero(st);
+    CK(cudaStreamSynchronize(st));
+    out = h;
+  });
+  (void)rc;
+  return out;
+}
+
+void abd_scene_destroy(abd_scene* s) { delete s; }
+
+#define SC(h) Scene& s = (h)->s
+
+int abd_broad_phase(abd_scene* h, const double* q0, const double* q1, double d_hat, int64_t* n_vf, int64_t* n_ee,
+                    int64_t* n_ov) {
+  return guard([&] {
+    SC(h);
+    s.q.upload(q0, 12 * (size_t)s.B, s.stream);
+    s.q_trial.upload(q1, 12 * (size_t)s.B, s.stream);
+    broad_phase(s, s.q.p, s.q_trial.p, d_hat);
+    sync(s.stream);
+    *n_vf = s.cands.n_vf;
+    *n_ee = s.cands.n_ee;
+    *n_ov = s.cands.n_ov;
+  });
+}
+
+int abd_get_candidates(abd_scene* h, int64_t* vf, int64_t* ee, int64_t* ov) {
+  return guard([&] {
+    SC(h);
+    std::vector<int4> a(s.cands.n_vf), b(s.cands.n_ee);
+    std::vector<int2> c(s.cands.n_ov);
+    s.cands.vf.download(a.data(), a.size(), s.stream);
+    s.cands.ee.download(b.data(), b.size(), s.stream);
+    s.cands.ov.download(c.data(), c.size(), s.stream);
+    sync(s.stream);
+    for (size_t i = 0; i < a.size(); ++i) {
+      vf[4 * i] = a[i].x; vf[4 * i + 1] = a[i].y; vf[4 * i + 2] = a[i].z; vf[4 * i + 3] = a[i].w;
+    }
+    for (size_t i = 0; i < b.size(); ++i) {
+      ee[4 * i] = b[i].x; ee[4 * i + 1] = b[i].y; ee[4 * i + 2] = b[i].z; ee[4 * i + 3] = b[i].w;
+    }
+    for (size_t i = 0; i < c.size(); ++i) {
+      ov[2 * i] = c[i].x;
+      ov[2 * i + 1] = c[i].y;
+    }
+  });
+}
+
+int abd_set_candidates(abd_scene* h, int64_t n_vf, const int64_t* vf, int64_t n_ee, const int64_t* ee, int64_t n_ov,
+                       const int64_t* ov) {
+  return guard([&] {
+    SC(h);
+    std::vector<int4> a(n_vf), b(n_ee);
+    std::vector<int2> c(n_ov);
+    for (int64_t i = 0; i < n_vf; ++i) a[i] = make_int4((int)vf[4 * i], (int)vf[4 * i + 1], (int)vf[4 * i + 2], (int)vf[4 * i + 3]);
+    for (int64_t i = 0; i < n_ee; ++i) b[i] = make_int4((int)ee[4 * i], (int)ee[4 * i + 1], (int)ee[4 * i + 2], (int)ee[4 * i + 3]);
+    for (int64_t i = 0; i < n_ov; ++i) c[i] = make_int2((int)ov[2 * i], (int)ov[2 * i + 1]);
+    s.cands.vf.upload(a.data(), n_vf, s.stream);
+    s.cands.ee.upload(b.data(), n_ee, s.stream);
+    s.cands.ov.upload(c.data(), n_ov, s.stream);
+    s.cands.n_vf = n_vf;
+    s.cands.n_ee = n_ee;
+    s.cands.n_ov = n_ov;
+    sync(s.stream);
+  });
+}
+
+static const double* up_q(Scene& s, DVec<double>& buf, const double* q) {
+  buf.upload(q, 12 * (size_t)s.B, s.stream);
+  return buf.p;
+}
+
+int abd_contact_energy(abd_scene* h, const double* q, double kappa, double d_hat, double* energy) {
+  return guard([&] {
+    SC(h);
+    *energy = contact_energy(s, up_q(s, s.q_trial, q), kappa, d_hat);
+  });
+}
+
+int abd_candidate_min_d2(abd_scene* h, const double* q, double* d2) {
+  return guard([&] {
+    SC(h);
+    *d2 = candidate_min_d2(s, up_q(s, s.q_trial, q));
+  });
+}
+
+int abd_global_min_distance(abd_scene* h, const double* q, double* dist) {
+  return guard([&] {
+    SC(h);
+    *dist = global_min_distance(s, up_q(s, s.q_trial, q));
+  });
+}
+
+int abd_contact_gradient_hessian(abd_scene* h, const double* q, double kappa, double d_hat, int project,
+                                 int64_t* n_active) {
+  return guard([&] {
+    SC(h);
+    *n_active = contact_blocks(s, up_q(s, s.q_trial, q), kappa, d_hat, project);
+  });
+}
+
+int abd_get_pair_blocks(abd_scene* h, int64_t* body_a, int64_t* body_b, double* grad, double* hess, double* d_sq) {
+  return guard([&] {
+    SC(h);
+    int64_t n = s.pblk.n;
+    std::vector<int2> b(n);
+    std::vector<double> blk((size_t)n * PB_STRIDE), d2(n);
+    s.pblk.bodies.download(b.data(), n, s.stream);
+    s.pblk.blk.download(blk.data(), (size_t)n * PB_STRIDE, s.stream);
+    s.pblk.d2.download(d2.data(), n, s.stream);
+    sync(s.stream);
+    for (int64_t i = 0; i < n; ++i) {
+      if (body_a) body_a[i] = b[i].x;
+      if (body_b) body_b[i] = b[i].y;
+      if (d_sq) d_sq[i] = d2[i];
+      const double* o = &blk[(size_t)i * PB_STRIDE];
+      if (grad) std::memcpy(grad + 24 * i, o, 24 * sizeof(double));
+      if (hess) {
+        double* H = hess + 576 * i;
+        for (int r = 0; r < 12; ++r)
+          for (int c = 0; c < 12; ++c) {
+            H[r * 24 + c] = o[24 + r * 12 + c];
+            H[(r + 12) * 24 + c + 12] = o[24 + 144 + r * 12 + c];
+            H[r * 24 + c + 12] = o[24 + 288 + r * 12 + c];
+            H[(c + 12) * 24 + r] = o[24 + 288 + r * 12 + c];
+          }
+      }
+    }
+  });
+}
+
+int abd_friction_precompute(abd_scene* h, const double* q_prev, double kappa, double d_hat, double mu, int64_t* n) {
+  return guard([&] {
+    SC(h);
+    static thread_local DVec<double>* basis = nullptr;
+    if (!basis) basis = new DVec<double>();
+    *n = friction_precompute(s, up_q(s, s.q_trial, q_prev), kappa, d_hat, mu, basis);
+    s.red.resize(std::max<int64_t>(*n, 1) * 6);
+    CK(cudaMemcpyAsync(s.red.p, basis->p, std::max<int64_t>(*n, 1) * 6 * sizeof(double), cudaMemcpyDeviceToDevice,
+                       s.stream));
+    sync(s.stream);
+  });
+}
+
+int abd_get_friction(abd_scene* h, int64_t* body_a, int64_t* body_b, double* lam, double* tangent_map, double* offset,
+                     double* basis) {
+  return guard([&] {
+    SC(h);
+    int64_t n = s.fric.n;
+    std::vector<int2> b(n);
+    std::vector<double> rec((size_t)n * FRIC_STRIDE), bs((size_t)n * 6);
+    s.fric.bodies.download(b.data(), n, s.stream);
+    s.fric.rec.download(rec.data(), (size_t)n * FRIC_STRIDE, s.stream);
+    if (basis && n) CK(cudaMemcpyAsync(bs.data(), s.red.p, n * 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+    sync(s.stream);
+    for (int64_t i = 0; i < n; ++i) {
+      body_a[i] = b[i].x;
+      body_b[i] = b[i].y;
+      const double* r = &rec[(size_t)i * FRIC_STRIDE];
+      std::memcpy(tangent_map + 48 * i, r, 48 * sizeof(double));
+      offset[2 * i] = r[48];
+      offset[2 * i + 1] = r[49];
+      lam[i] = r[50];
+      if (basis) std::memcpy(basis + 6 * i, &bs[6 * i], 6 * sizeof(double));
+    }
+  });
+}
+
+int abd_set_friction(abd_scene* h, int64_t n, const int64_t* body_a, const int64_t* body_b, const double* lam, double mu,
+                     const double* tangent_map, const double* offset) {
+  return guard([&] {
+    SC(h);
+    std::vector<int2> hb;
+    std::vector<double> hr;
+    pack_friction(n, body_a, body_b, lam, tangent_map, offset, hb, hr);
+    s.fric.bodies.upload(hb.data(), hb.size(), s.stream);
+    s.fric.rec.upload(hr.data(), hr.size(), s.stream);
+    s.fric.n = n;
+    s.fric.mu = mu;
+    sync(s.stream);
+  });
+}
+
+int abd_step_filter(abd_scene* h, const double* q, const double* dq, double slack, double* alpha) {
+  return guard([&] {
+    SC(h);
+    const double* dqq = up_q(s, s.q_trial, q);
+    s.dq.upload(dq, 12 * (size_t)s.B, s.stream);
+    *alpha = step_filter(s, dqq, s.dq.p, slack);
+  });
+}
+
+int abd_compute_q_tilde(abd_scene* h, const double* q, const double* q_dot, const double* forces, double dt,
+                        double* q_tilde) {
+  return guard([&] {
+    SC(h);
+    size_t NB = 12 * (size_t)s.B;
+    DVec<double> a, b, c, o;
+    a.upload(q, NB, s.stream);
+    b.upload(q_dot, NB, s.stream);
+    c.upload(forces, NB, s.stream);
+    o.resize(NB);
+    launch_q_tilde(s, a.p, b.p, c.p, dt, o.p);
+    o.download(q_tilde, NB, s.stream);
+    sync(s.stream);
+  });
+}
+
+int abd_ip_value(abd_scene* h, const double* q, const double* q_tilde, double dt, double kappa, double d_hat,
+                 double eps_v, double* value) {
+  return guard([&] {
+    SC(h);
+    s.q_tilde.upload(q_tilde, 12 * (size_t)s.B, s.stream);
+    *value = ip_value(s, up_q(s, s.q_trial, q), s.q_tilde.p, dt, kappa, d_hat, eps_v);
+  });
+}
+
+int abd_assemble(abd_scene* h, const double* q, const double* q_tilde, double dt, double kappa, double d_hat,
+                 double eps_v, int64_t* n_off) {
+  return guard([&] {
+    SC(h);
+    s.q_tilde.upload(q_tilde, 12 * (size_t)s.B, s.stream);
+    assemble(s, up_q(s, s.q_trial, q), s.q_tilde.p, dt, kappa, d_hat, eps_v);
+    *n_off = s.H.n_off;
+  });
+}
+
+int abd_get_system(abd_scene* h, double* grad, double* diag, int64_t* off_keys, double* off_blocks) {
+  return guard([&] {
+    SC(h);
+    Bsr& H = s.H;
+    int n = H.n;
+    std::vector<double> val((size_t)H.nnzb * 144);
+    std::vector<int> dpos(n), upos(H.n_off);
+    std::vector<int2> keys(H.n_off);
+    H.val.download(val.data(), val.size(), s.stream);
+    H.diag_pos.download(dpos.data(), n, s.stream);
+    H.upper_pos.download(upos.data(), H.n_off, s.stream);
+    H.upper_keys.download(keys.data(), H.n_off, s.stream);
+    if (grad) s.grad.download(grad, 12 * (size_t)n, s.stream);
+    sync(s.stream);
+    for (int i = 0; i < n; ++i)
+      if (diag) std::memcpy(diag + 144 * (size_t)i, &val[144 * (size_t)dpos[i]], 144 * sizeof(double));
+    for (int64_t k = 0; k < H.n_off; ++k) {
+      if (off_keys) {
+        off_keys[2 * k] = keys[k].x;
+        off_keys[2 * k + 1] = keys[k].y;
+      }
+      if (off_blocks) std::memcpy(off_blocks + 144 * k, &val[144 * (size_t)upos[k]], 144 * sizeof(double));
+    }
+  });
+}
+
+int abd_solve_resident(abd_scene* h, double rel_tol, int max_iters, double* dx, int* iters, double* rel_res) {
+  return guard([&] {
+    SC(h);
+    int64_t N = 12 * (int64_t)s.H.n;
+    DVec<double> neg, x;
+    neg.resize(std::max<int64_t>(N, 1));
+    x.resize(std::max<int64_t>(N, 1));
+    std::vector<double> g(N);
+    s.grad.download(g.data(), N, s.stream);
+    sync(s.stream);
+    for (auto& v : g) v = -v;
+    neg.upload(g.data(), N, s.stream);
+    double rel = 0.0;
+    int it = pcg_solve(s, neg.p, x.p, rel_tol, max_iters, rel);
+    x.download(dx, N, s.stream);
+    sync(s.stream);
+    if (iters) *iters = it;
+    if (rel_res) *rel_res = rel;
+  });
+}
+
+int abd_set_state(abd_scene* h, const double* q, const double* q_dot) {
+  return guard([&] {
+    SC(h);
+    if (q) s.q.upload(q, 12 * (size_t)s.B, s.stream);
+    if (q_dot) s.q_dot.upload(q_dot, 12 * (size_t)s.B, s.stream);
+    sync(s.stream);
+  });
+}
+
+int abd_get_state(abd_scene* h, double* q, double* q_dot) {
+  return guard([&] {
+    SC(h);
+    if (q) s.q.download(q, 12 * (size_t)s.B, s.stream);
+    if (q_dot) s.q_dot.download(q_dot, 12 * (size_t)s.B, s.stream);
+    sync(s.stream);
+  });
+}
+
+int abd_advance_step(abd_scene* h, const double* forces, const abd_step_params* p, abd_step_stats* st,
+                     double* energy_trace) {
+  return guard([&] {
+    SC(h);
+    advance_step(s, forces, *p, *st, energy_trace);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,30 @@
+#pragma once
+#include "abd_pair.cuh"
+#include "kernels.h"
+
+namespace abd {
+
+// k_broad.cu
+void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat);
+// k_solve.cu
+void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f);
+void reduce_system(Scene& s, const double* diag0, const double* grad0);
+int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_iters, double& rel_res);
+void spmv(Scene& s, const double* x, double* y);
+void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off);
+// k_stats.cu
+double global_min_distance(Scene& s, const double* q);
+// driver.cu
+int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project);
+void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, int project);
+int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, double mu, DVec<double>* basis);
+double contact_energy(Scene& s, const double* q, double kappa, double dh);
+double friction_energy(Scene& s, const double* q, double dt, double eps_v);
+double body_energy(Scene& s, const double* q, const double* qt, double dt);
+double ip_value(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v);
+double step_filter(Scene& s, const double* q, const double* dq, double slack);
+double candidate_min_d2(Scene& s, const double* q);
+void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v);
+void advance_step(Scene& s, const double* forces_host, const abd_step_params& P, abd_step_stats& st, double* trace);
+
+}  // namespace abd

@@ -1,0 +1,391 @@
+// Scene narrow phase: activity filter, per-pair contact blocks (K3 first
+// pass), contact energy (K6), friction precompute (K7), CCD (K5), per-body
+// inertia + orthogonality terms (K1).
+#include "abd_misc.cuh"
+#include "kernels.h"
+
+namespace abd {
+
+SceneView view(const Scene& s) {
+  SceneView v;
+  v.v_off = s.v_off.p;
+  v.e_off = s.e_off.p;
+  v.t_off = s.t_off.p;
+  v.rest = s.rest.p;
+  v.edges = s.edges.p;
+  v.tris = s.tris.p;
+  v.elen2 = s.elen2.p;
+  v.dyn = s.dyn.p;
+  v.slot = s.slot.p;
+  v.B = s.B;
+  return v;
+}
+
+// global vertex ids and owning bodies of a candidate's 4 stacked points
+struct PairIds {
+  int vid[4];
+  int body[4];
+  double eps;
+};
+
+__device__ __forceinline__ PairIds pair_ids(const SceneView& sv, int kind, int4 r) {
+  PairIds p;
+  if (kind == KIND_VF) {
+    p.vid[0] = sv.v_off[r.x] + r.y;
+    int t = sv.t_off[r.z] + r.w;
+    p.vid[1] = sv.tris[3 * t];
+    p.vid[2] = sv.tris[3 * t + 1];
+    p.vid[3] = sv.tris[3 * t + 2];
+    p.body[0] = r.x;
+    p.body[1] = p.body[2] = p.body[3] = r.z;
+    p.eps = 0.0;
+  } else {
+    int ea = sv.e_off[r.x] + r.y, eb = sv.e_off[r.z] + r.w;
+    p.vid[0] = sv.edges[2 * ea];
+    p.vid[1] = sv.edges[2 * ea + 1];
+    p.vid[2] = sv.edges[2 * eb];
+    p.vid[3] = sv.edges[2 * eb + 1];
+    p.body[0] = p.body[1] = r.x;
+    p.body[2] = p.body[3] = r.z;
+    // DEFAULT_MOLLIFIER_SCALE * la * lb  (contact.py:462)
+    p.eps = xmul(xmul(1e-3, sv.elen2[ea]), sv.elen2[eb]);
+  }
+  return p;
+}
+
+__device__ __forceinline__ void pair_points(const SceneView& sv, const PairIds& ids, const double* q, V3* z, V3* xb) {
+  for (int k = 0; k < 4; ++k) {
+    xb[k] = ld3(sv.rest + 3 * (int64_t)ids.vid[k]);
+    z[k] = world_pos(q + 12 * (int64_t)ids.body[k], xb[k]);
+  }
+}
+
+__global__ void k_pair_flags(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                             const double* __restrict__ q, double dh2, int* flags, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  PairIds ids = pair_ids(sv, kind, rows[i]);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  double d2 = pair_d2(kind, z);
+  int on = d2 < dh2;
+  flags[i] = on;
+  if (on && !(d2 > 0.0)) atomicExch(err, 1);
+}
+
+// K3 first pass: one thread per candidate, active ones write g24 | haa | hbb | hab
+__global__ void __launch_bounds__(64) k_pair_blocks(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                                                     const double* __restrict__ q, double kappa, double dh,
+                                                     int project, const int* __restrict__ flags,
+                                                     const int* __restrict__ pos, int64_t base, int2* out_bodies,
+                                                     double* out_blk, double* out_d2) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  int4 r = rows[i];
+  PairIds ids = pair_ids(sv, kind, r);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  Closest c = closest(kind, z);
+  double g12[12], tg[12];
+  double H12[144], T1[144], V[144];
+  contact_point_terms(kind, z, c, ids.eps, kappa, dh, g12, H12, tg, T1);
+  int64_t o = base + pos[i];
+  double* blk = out_blk + o * PB_STRIDE;
+  map_to_bodies(kind, xb, g12, H12, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0, T1, V, blk, blk + 24,
+                blk + 24 + 144, blk + 24 + 288);
+  out_bodies[o] = make_int2(r.x, r.z);
+  out_d2[o] = c.d2;
+}
+
+__global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                                 const double* __restrict__ q, double kappa, double dh, double* partials, int* err) {
+  __shared__ double sh[RED_THREADS];
+  double acc = 0.0;
+  double dh2 = dh * dh;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    PairIds ids = pair_ids(sv, kind, rows[i]);
+    V3 z[4], xb[4];
+    pair_points(sv, ids, q, z, xb);
+    double d2 = pair_d2(kind, z);
+    if (!(d2 < dh2)) continue;
+    if (!(d2 > 0.0)) atomicExch(err, 1);
+    double b = kappa * barrier_terms(d2, dh).b0;
+    if (kind == KIND_EE) b = mollifier_value(z, ids.eps) * b;
+    acc += b;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+__global__ void k_cand_min_d2(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                              const double* __restrict__ q, unsigned long long* best) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double d2 = INFINITY;
+  if (i < n) {
+    PairIds ids = pair_ids(sv, kind, rows[i]);
+    V3 z[4], xb[4];
+    pair_points(sv, ids, q, z, xb);
+    d2 = pair_d2(kind, z);
+  }
+  for (int o = 16; o > 0; o >>= 1) d2 = fmin(d2, __shfl_xor_sync(0xffffffffu, d2, o));
+  if ((threadIdx.x & 31) == 0 && d2 < INFINITY) atomicMin(best, (unsigned long long)__double_as_longlong(d2));
+}
+
+// K7: lagged friction records at q_prev for active candidates (contact.py:722-790)
+__global__ void k_friction_pre(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                               const double* __restrict__ q, double kappa, double dh, const int* __restrict__ flags,
+                               const int* __restrict__ pos, int64_t base, int2* out_bodies, double* out_rec,
+                               double* out_basis) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  int4 r = rows[i];
+  PairIds ids = pair_ids(sv, kind, r);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  Closest c = closest(kind, z);
+  double d = sqrt(c.d2);
+  double lam = -kappa * 2.0 * d * barrier_terms(c.d2, dh).b1;
+  if (kind == KIND_EE) lam = lam * mollifier_value(z, ids.eps);
+  V3 rr = c.gamma[0] * z[0];
+  rr = rr + c.gamma[1] * z[1];
+  rr = rr + c.gamma[2] * z[2];
+  rr = rr + c.gamma[3] * z[3];
+  V3 nrm = V3{rr.x / d, rr.y / d, rr.z / d};
+  double ax = fabs(nrm.x), ay = fabs(nrm.y), az = fabs(nrm.z);
+  int pick = (ax <= ay && ax <= az) ? 0 : ((ay <= az) ? 1 : 2);
+  V3 helper = V3{pick == 0 ? 1.0 : 0.0, pick == 1 ? 1.0 : 0.0, pick == 2 ? 1.0 : 0.0};
+  V3 t1 = xcross(nrm, helper);
+  double tn = xnorm_seq(t1);
+  t1 = V3{t1.x / tn, t1.y / tn, t1.z / tn};
+  V3 t2 = xcross(nrm, t1);
+  double T[3][2] = {{t1.x, t2.x}, {t1.y, t2.y}, {t1.z, t2.z}};
+  // c_s[j] = sum_{k in side s} gamma_k w_k[j]
+  double cs[2][4];
+  for (int s = 0; s < 2; ++s) {
+    for (int j = 0; j < 4; ++j) cs[s][j] = 0.0;
+    int k0 = side_begin(kind, s), nk = side_count(kind, s);
+    for (int k = 0; k < nk; ++k) {
+      double gk = c.gamma[k0 + k];
+      cs[s][0] += gk;
+      cs[s][1] += gk * xb[k0 + k].x;
+      cs[s][2] += gk * xb[k0 + k].y;
+      cs[s][3] += gk * xb[k0 + k].z;
+    }
+  }
+  int64_t o = base + pos[i];
+  double* rec = out_rec + o * FRIC_STRIDE;
+  const double* qa = q + 12 * (int64_t)r.x;
+  const double* qb = q + 12 * (int64_t)r.z;
+  for (int m = 0; m < 2; ++m) {
+    double off = 0.0;
+    for (int col = 0; col < 24; ++col) {
+      int s = col / 12, rem = col % 12;
+      int a = rem < 3 ? rem : (rem - 3) / 3;
+      int j = rem < 3 ? 0 : 1 + (rem - 3) % 3;
+      double v = T[a][m] * cs[s][j];
+      rec[m * 24 + col] = v;
+      off += v * (s == 0 ? qa[rem] : qb[rem]);
+    }
+    rec[48 + m] = off;
+  }
+  rec[50] = lam;
+  out_bodies[o] = make_int2(r.x, r.z);
+  if (out_basis) {
+    double* bs = out_basis + o * 6;
+    for (int a = 0; a < 3; ++a) {
+      bs[2 * a] = T[a][0];
+      bs[2 * a + 1] = T[a][1];
+    }
+  }
+}
+
+// K5: ACCD over candidates with a global min (ccd.py:130-153)
+__global__ void k_ccd(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows, const double* __restrict__ q,
+                      const double* __restrict__ dq, double slack, unsigned long long* tmin, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  PairIds ids = pair_ids(sv, kind, rows[i]);
+  V3 x[4], xb[4], dx[4];
+  pair_points(sv, ids, q, x, xb);
+  for (int k = 0; k < 4; ++k) {
+    int b = ids.body[k];
+    dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+  }
+  bool bad = false;
+  double t = accd_query(kind, x, dx, slack, 1.0, 512, tmin, bad);
+  if (bad) atomicExch(err, 1);
+  atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
+}
+
+// K1: inertia + orthogonality per dynamic slot (solver.py:197-200, :283-296)
+__global__ void k_body_terms(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ mass,
+                             const double* __restrict__ stiff, const double* __restrict__ q,
+                             const double* __restrict__ qt, double dt, double* grad0, double* diag0,
+                             double* partials, int want) {
+  __shared__ double sh[RED_THREADS];
+  double acc = 0.0;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_dyn; s += gridDim.x * blockDim.x) {
+    int b = dyn_body[s];
+    const double* M = mass + 144 * (int64_t)b;
+    double qq[12], diff[12], Md[12];
+    for (int c = 0; c < 12; ++c) {
+      qq[c] = q[12 * (int64_t)b + c];
+      diff[c] = qq[c] - qt[12 * (int64_t)b + c];
+    }
+    double quad = 0.0;
+    for (int r = 0; r < 12; ++r) {
+      double a = 0.0;
+      for (int c = 0; c < 12; ++c) a += M[r * 12 + c] * diff[c];
+      Md[r] = a;
+      quad += diff[r] * a;
+    }
+    double dt2 = dt * dt;
+    double k = stiff[b];
+    acc += 0.5 * quad + dt2 * ortho_energy_dev(qq, k);
+    if (!want) continue;
+    double g[12], H[144], V[144];
+    ortho_derivs_dev(qq, k, g, H);
+    psd_project_jacobi<12>(H + 3 * 12 + 3, V, 9);
+    for (int c = 0; c < 12; ++c) grad0[12 * (int64_t)s + c] = Md[c] + dt2 * g[c];
+    for (int c = 0; c < 144; ++c) diag0[144 * (int64_t)s + c] = M[c] + dt2 * H[c];
+  }
+  if (!partials) return;
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+// q_tilde = q + dt qdot + dt^2 M^{-1} f (solver.py:179-190), Cholesky per body
+__global__ void k_q_tilde(int B, const unsigned char* __restrict__ dyn, const double* __restrict__ mass,
+                          const double* __restrict__ q, const double* __restrict__ qd, const double* __restrict__ f,
+                          double dt, double* qt) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double* qb = q + 12 * (int64_t)b;
+  if (!dyn[b]) {
+    for (int c = 0; c < 12; ++c) qt[12 * (int64_t)b + c] = qb[c];
+    return;
+  }
+  double L[144], y[12];
+  const double* M = mass + 144 * (int64_t)b;
+  for (int r = 0; r < 144; ++r) L[r] = M[r];
+  for (int j = 0; j < 12; ++j) {
+    double d = L[j * 12 + j];
+    for (int k = 0; k < j; ++k) d -= L[j * 12 + k] * L[j * 12 + k];
+    d = sqrt(d);
+    L[j * 12 + j] = d;
+    for (int i = j + 1; i < 12; ++i) {
+      double v = L[i * 12 + j];
+      for (int k = 0; k < j; ++k) v -= L[i * 12 + k] * L[j * 12 + k];
+      L[i * 12 + j] = v / d;
+    }
+  }
+  for (int i = 0; i < 12; ++i) {
+    double v = f[12 * (int64_t)b + i];
+    for (int k = 0; k < i; ++k) v -= L[i * 12 + k] * y[k];
+    y[i] = v / L[i * 12 + i];
+  }
+  for (int i = 11; i >= 0; --i) {
+    double v = y[i];
+    for (int k = i + 1; k < 12; ++k) v -= L[k * 12 + i] * y[k];
+    y[i] = v / L[i * 12 + i];
+  }
+  double dt2 = dt * dt;
+  for (int c = 0; c < 12; ++c) qt[12 * (int64_t)b + c] = qb[c] + dt * qd[12 * (int64_t)b + c] + dt2 * y[c];
+}
+
+// trial = q + alpha * dq  (numpy: multiply then add, no FMA)
+__global__ void k_axpy_q(int64_t n, const double* __restrict__ q, double alpha, const double* __restrict__ dq,
+                         double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = xadd(q[i], xmul(alpha, dq[i]));
+}
+
+// ---------------------------------------------------------------------------
+static const int4* rows_of(const Scene& s, int kind, int64_t& n) {
+  n = kind == KIND_VF ? s.cands.n_vf : s.cands.n_ee;
+  return kind == KIND_VF ? s.cands.vf.p : s.cands.ee.p;
+}
+
+void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err) {
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  if (!n) return;
+  k_pair_flags<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dh2, flags, err);
+  note_launch("k_pair_flags");
+}
+
+void launch_pair_blocks(Scene& s, int kind, const double* q, double kappa, double dh, int project, const int* flags,
+                        const int* pos, int64_t base, int* err) {
+  (void)err;
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  if (!n) return;
+  k_pair_blocks<<<grid_for(n, 64), 64, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, project, flags, pos,
+                                                      base, s.pblk.bodies.p, s.pblk.blk.p, s.pblk.d2.p);
+  note_launch("k_pair_blocks");
+}
+
+void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, double dh, double* partials, int* err) {
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  k_contact_energy<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, partials, err);
+  note_launch("k_contact_energy");
+}
+
+void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best) {
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  if (!n) return;
+  k_cand_min_d2<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, best);
+  note_launch("k_cand_min_d2");
+}
+
+void launch_friction_pre(Scene& s, int kind, const double* q, double kappa, double dh, const int* flags,
+                         const int* pos, int64_t base, double* basis_out) {
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  if (!n) return;
+  k_friction_pre<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, flags, pos, base,
+                                                         s.fric.bodies.p, s.fric.rec.p, basis_out);
+  note_launch("k_friction_pre");
+}
+
+void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack, unsigned long long* tmin,
+                int* err) {
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  if (!n) return;
+  k_ccd<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dq, slack, tmin, err);
+  note_launch("k_ccd");
+}
+
+void launch_body_terms(Scene& s, const double* q, const double* qt, double dt, double* grad0, double* diag0,
+                       double* partials, int want) {
+  k_body_terms<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p, s.stiff.p, q, qt, dt, grad0,
+                                                         diag0, partials, want);
+  note_launch("k_body_terms");
+}
+
+void launch_q_tilde(Scene& s, const double* q, const double* qd, const double* f, double dt, double* qt) {
+  if (!s.B) return;
+  k_q_tilde<<<grid_for(s.B, 64), 64, 0, s.stream>>>(s.B, s.dyn.p, s.mass.p, q, qd, f, dt, qt);
+  note_launch("k_q_tilde");
+}
+
+void launch_axpy_q(Scene& s, const double* q, double alpha, const double* dq, double* out, int64_t n) {
+  if (!n) return;
+  k_axpy_q<<<grid_for(n, 256), 256, 0, s.stream>>>(n, q, alpha, dq, out);
+  note_launch("k_axpy_q");
+}
+
+}  // namespace abd

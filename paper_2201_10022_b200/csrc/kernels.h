@@ -1,0 +1,68 @@
+// Host-side launchers of the sm_100a kernels (device pointers in/out).
+#pragma once
+#include "abd_math.cuh"
+#include "scene.h"
+
+namespace abd {
+
+void note_launch(const char* name);
+void reduce_fixed_device(Scene& s, const double* partials, int n, double* out_dev);
+void reduce_fixed_stream(cudaStream_t st, const double* partials, int n, double* out_dev);
+
+// plain-data view of the scene geometry passed to kernels by value
+struct SceneView {
+  const int* v_off;
+  const int* e_off;
+  const int* t_off;
+  const double* rest;
+  const int* edges;
+  const int* tris;
+  const double* elen2;
+  const unsigned char* dyn;
+  const int* slot;
+  int B;
+};
+SceneView view(const Scene& s);
+
+constexpr int FRIC_STRIDE = 51;  // tmap (48) | offset (2) | lam (1)
+constexpr int RED_BLOCKS = 592;  // fixed grid for deterministic reductions (4 x 148)
+constexpr int RED_THREADS = 256;
+
+// ---- stateless batch launchers (k_batch.cu) ----
+void launch_pt_closest(cudaStream_t st, int64_t n, const double* z, double* d2, int* region, double* bary);
+void launch_ee_closest(cudaStream_t st, int64_t n, const double* z, double* d2, int* region, double* s,
+                       double* t);
+void launch_d2_derivs(cudaStream_t st, int kind, int64_t n, const double* z, double* d2, double* grad,
+                      double* hess, int* region, double* gamma);
+void launch_mollifier(cudaStream_t st, int64_t n, const double* z, const double* eps, double* val, double* grad,
+                      double* hess);
+void launch_barrier(cudaStream_t st, int64_t n, const double* s, double dh, double* b0, double* b1, double* b2,
+                    int* err);
+void launch_ortho(cudaStream_t st, int64_t n, const double* q, const double* k, int project, double* e,
+                  double* g, double* h);
+void launch_psd(cudaStream_t st, int64_t n, int k, const double* H, double* out);
+void launch_accd(cudaStream_t st, int kind, int64_t n, const double* x, const double* dx, double slack,
+                 double tmax, int max_iters, double* t, int* err);
+void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const double* rec, double mu,
+                     const double* q, const unsigned char* dyn, double dt, double eps_v, int project,
+                     double* energy_partials, double* grad24, double* hess24, double* pblk_out);
+
+// ---- scene narrow phase (k_narrow.cu) ----
+// activity flags d^2 < d_hat^2 for the resident candidates of `kind`
+void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err);
+void launch_pair_blocks(Scene& s, int kind, const double* q, double kappa, double dh, int project,
+                        const int* flags, const int* pos, int64_t base, int* err);
+void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, double dh, double* partials,
+                           int* err);
+void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best_bits);
+void launch_friction_pre(Scene& s, int kind, const double* q, double kappa, double dh, const int* flags,
+                         const int* pos, int64_t base, double* basis_out);
+void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack,
+                unsigned long long* tmin_bits, int* err);
+// per-body inertia + orthogonality terms (K1): grad0/diag0 per dynamic slot, energy partials
+void launch_body_terms(Scene& s, const double* q, const double* q_tilde, double dt, double* grad0,
+                       double* diag0, double* energy_partials, int want_derivs);
+void launch_q_tilde(Scene& s, const double* q, const double* q_dot, const double* f, double dt, double* qt);
+void launch_axpy_q(Scene& s, const double* q, double alpha, const double* dq, double* out, int64_t n);
+
+}  // namespace abd

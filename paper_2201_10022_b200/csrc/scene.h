@@ -1,0 +1,156 @@
+// Device-resident scene context: geometry SoA, per-step state, work buffers.
+// Host-side C++ (no torch types); see DESIGN.md "Data layout in HBM".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/abd_b200.h"
+
+namespace abd {
+
+// ---------------------------------------------------------------------------
+// errors: C++ exceptions inside the library, mapped to status codes at the
+// C-ABI boundary (capi.cu) together with a thread-local message.
+struct Error : std::runtime_error {
+  int code;
+  int64_t index;
+  Error(int c, const std::string& m, int64_t idx = -1) : std::runtime_error(m), code(c), index(idx) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define CK(x) ::abd::cuda_check((x), #x)
+
+// growable device vector (never shrinks; contents undefined after grow)
+template <class T>
+struct DVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  DVec() = default;
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  ~DVec() {
+    if (p) cudaFree(p);
+  }
+  void resize(size_t m) {
+    if (m > cap) {
+      if (p) CK(cudaFree(p));
+      size_t c = m + m / 4 + 16;
+      CK(cudaMalloc(&p, c * sizeof(T)));
+      cap = c;
+    }
+    n = m;
+  }
+  void upload(const T* h, size_t m, cudaStream_t s) {
+    resize(m);
+    if (m) CK(cudaMemcpyAsync(p, h, m * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void download(T* h, size_t m, cudaStream_t s) const {
+    if (m) CK(cudaMemcpyAsync(h, p, m * sizeof(T), cudaMemcpyDeviceToHost, s));
+  }
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+};
+
+struct Cands {
+  DVec<int4> vf, ee;  // (body_a, prim_a, body_b, prim_b) in canonical order
+  DVec<int2> ov;      // overlapping body pairs (i < j)
+  int64_t n_vf = 0, n_ee = 0, n_ov = 0;
+};
+
+// lagged friction records (compact form of contact.py:687-708)
+struct FrictionSet {
+  DVec<int2> bodies;      // (body_a, body_b)
+  DVec<double> rec;       // 17 doubles per pair: T(6) c(8) off(2) lam(1)
+  int64_t n = 0;
+  double mu = 0.0;
+};
+
+// per-active-pair local blocks (PairBlocks restated): g24 | haa | hbb | hab
+constexpr int PB_STRIDE = 24 + 3 * 144;
+struct PairBlockSet {
+  DVec<int2> bodies;
+  DVec<double> blk;  // PB_STRIDE per pair
+  DVec<double> d2;
+  int64_t n = 0;
+};
+
+// symmetric BSR over dynamic slots, stored in full (both triangles) CSR
+struct Bsr {
+  int n = 0;                 // block rows
+  int64_t nnzb = 0;          // stored blocks (diag + 2 * n_off)
+  int64_t n_off = 0;         // upper off-diagonal blocks
+  DVec<int> row_ptr;         // n + 1
+  DVec<int> col;             // nnzb
+  DVec<double> val;          // nnzb * 144
+  DVec<int> diag_pos;        // n: position of the diagonal block
+  DVec<int2> upper_keys;     // n_off (i < j) sorted
+  DVec<int> upper_pos;       // position of (i,j)
+  DVec<int> lower_pos;       // position of (j,i)
+};
+
+struct Stats;  // driver statistics (driver.cu)
+
+struct Scene {
+  int B = 0, n_dyn = 0;
+  int64_t V = 0, E = 0, T = 0;
+  int max_v = 0, max_e = 0, max_t = 0;  // per-body primitive maxima (sort key widths)
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+
+  // geometry (immutable after create)
+  DVec<int> v_off, e_off, t_off;  // B + 1
+  DVec<double> rest;              // V * 3
+  DVec<int> edges;                // E * 2 (global vertex ids)
+  DVec<int> tris;                 // T * 3 (global vertex ids)
+  DVec<double> elen2;             // E
+  DVec<int> vert_body, edge_body, tri_body;
+  DVec<unsigned char> dyn;        // B
+  DVec<int> slot;                 // B (dynamic slot or -1)
+  DVec<int> dyn_body;             // n_dyn
+  DVec<double> mass;              // B * 144 (full 12x12, zero for kinematic)
+  DVec<double> stiff;             // B
+  std::vector<int> h_slot, h_dyn_body;
+  std::vector<unsigned char> h_dyn;
+
+  // state
+  DVec<double> q, q0, q_dot, q_tilde, dq, q_trial, forces;
+
+  // broad / narrow phase
+  Cands cands;
+  FrictionSet fric;
+  PairBlockSet pblk;
+
+  // assembly / solve
+  Bsr H;
+  DVec<double> grad, dx;  // n_dyn * 12
+
+  // scratch
+  DVec<unsigned char> tmp_bytes;
+  DVec<int> tmp_i0, tmp_i1, tmp_i2, tmp_i3;
+  DVec<int64_t> tmp_l0, tmp_l1, tmp_l2, tmp_l3;
+  DVec<double> tmp_d0, tmp_d1, tmp_d2, tmp_d3;
+  DVec<double> red;  // reduction partials
+  double* h_pinned = nullptr;  // small pinned staging for scalars
+  DVec<double> vbox;  // V * 6 vertex boxes (broad phase)
+  DVec<double> bbox;  // B * 6 body boxes
+
+  Scene();
+  ~Scene();
+};
+
+// ---------------------------------------------------------------------------
+// cub wrappers (scene.cu)
+void scan_exclusive_i32(Scene& s, const int* in, int* out, int64_t n);
+void sort_pairs_u64(Scene& s, uint64_t* keys, uint64_t* keys_alt, int* vals, int* vals_alt, int64_t n,
+                    int end_bit, bool& result_in_alt);
+double reduce_sum_det(Scene& s, const double* partials, int n);  // deterministic
+
+inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
+int bits_for(int64_t maxval);
+
+}  // namespace abd

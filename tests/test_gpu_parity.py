@@ -1,0 +1,336 @@
+"""Parity of the sm_100a path (through the C-ABI) against reference goldens and the oracle."""
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from golden_io import oracle_bodies, unpack_meshes
+from oracle import abd_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+P = pytest.importorskip("paper_2201_10022_b200")
+from paper_2201_10022_b200 import _native  # noqa: E402
+
+
+def test_library_loaded_and_device():
+    import ctypes as C
+    sm, a, b = C.c_int(), C.c_int(), C.c_int()
+    _native.check(_native.lib().abd_device_info(C.byref(sm), C.byref(a), C.byref(b)))
+    assert a.value == 10 and sm.value >= 100
+
+
+def test_pt_closest_bitwise(golden):
+    g = golden("kernels.npz")
+    z = g["pt_z"]
+    d2, reg, bary = P.point_triangle_closest(z[:, 0], z[:, 1], z[:, 2], z[:, 3])
+    assert np.array_equal(reg, g["pt_region"])
+    assert np.array_equal(d2, g["pt_d2"])
+    assert np.array_equal(bary, g["pt_bary"])
+
+
+def test_ee_closest_bitwise(golden):
+    g = golden("kernels.npz")
+    z = g["ee_z"]
+    d2, reg, s, t = P.edge_edge_closest(z[:, 0], z[:, 1], z[:, 2], z[:, 3])
+    assert np.array_equal(reg, g["ee_region"])
+    assert np.array_equal(d2, g["ee_d2"])
+    assert np.array_equal(s, g["ee_s"]) and np.array_equal(t, g["ee_t"])
+
+
+@pytest.mark.parametrize("kind", ["vf", "ee"])
+def test_d2_derivatives(golden, kind):
+    g = golden("kernels.npz")
+    d2, gr, h, reg, gam = P.pair_distance_gradients(kind, g[f"g{kind}_z"])
+    assert np.array_equal(reg, g[f"g{kind}_region"])
+    assert np.array_equal(d2, g[f"g{kind}_d2"])
+    for k in range(len(d2)):
+        assert rel_err(gr[k], g[f"g{kind}_grad"][k]) <= TOL
+        assert rel_err(h[k], g[f"g{kind}_hess"][k]) <= TOL
+
+
+def test_mollifier(golden):
+    g = golden("kernels.npz")
+    v, gr, h = P.ee_mollifier_grad_hess(g["mol_z"], g["mol_eps"])
+    assert np.allclose(v, g["mol_val"], rtol=1e-12, atol=0)
+    z = g["mol_z"]
+    assert np.array_equal(P.ee_mollifier(z[:, 0], z[:, 1], z[:, 2], z[:, 3], g["mol_eps"]), g["mol_val2"])
+    for k in range(len(v)):
+        ref_g, ref_h = g["mol_grad"][k], g["mol_hess"][k]
+        if np.abs(ref_g).max() > 0:
+            assert rel_err(gr[k], ref_g) <= TOL
+            assert rel_err(h[k], ref_h) <= TOL
+
+
+def test_barrier(golden):
+    g = golden("kernels.npz")
+    s, dh = g["bar_s"], float(g["bar_dhat"])
+    for f, key in ((P.barrier, "bar_b0"), (P.barrier_d1, "bar_b1"), (P.barrier_d2, "bar_b2")):
+        assert np.allclose(f(s, dh), g[key], rtol=1e-13, atol=0)
+    with pytest.raises(P.BarrierDomainError):
+        P.barrier(0.0, 1e-3)
+    with pytest.raises(P.BarrierDomainError):
+        P.barrier_d1(-1.0, 1e-3)
+
+
+def test_barrier_known_answer():
+    d_hat = 1e-3
+    assert float(P.barrier(0.25 * d_hat ** 2, d_hat)) == pytest.approx((d_hat ** 2 / 4) * np.log(2.0), rel=1e-12)
+    assert float(P.barrier(d_hat ** 2, d_hat)) == 0.0
+
+
+def test_ortho(golden):
+    g = golden("kernels.npz")
+    k = float(g["orth_k"])
+    mat = P.BodyMaterial(1000.0, 1e8, k / 1e8)
+    qs = g["orth_q"]
+    e, gr, h = _native.ortho_batch(qs, np.full(len(qs), mat.stiffness_scale), False)
+    _, _, hp = _native.ortho_batch(qs, np.full(len(qs), mat.stiffness_scale), True)
+    for i in range(len(qs)):
+        assert e[i] == pytest.approx(g["orth_e"][i], rel=1e-12, abs=1e-300)
+        if i > 0:
+            assert rel_err(gr[i], g["orth_g"][i], tiny=1e-300) <= TOL
+        assert rel_err(h[i], g["orth_h"][i]) <= TOL
+        assert rel_err(hp[i], g["orth_hp"][i]) <= TOL
+    assert P.ortho_energy(P.BodyCoords.from_parts(np.zeros(3), np.diag([2.0, 1, 1])), P.BodyMaterial(1.0, 1.0, 1.0)) \
+        == pytest.approx(9.0)
+
+
+@pytest.mark.parametrize("k", [2, 12, 24])
+def test_project_psd(golden, k):
+    g = golden("kernels.npz")
+    out = P.project_psd(g[f"psd{k}_in"])
+    for i in range(len(out)):
+        assert rel_err(out[i], g[f"psd{k}_out"][i]) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["vf", "ee"])
+def test_accd_bitwise(golden, kind):
+    g = golden("kernels.npz")
+    name = "vertex-face" if kind == "vf" else "edge-edge"
+    t = P.accd_toi_batch(name, g[f"ccd_{kind}_x"], g[f"ccd_{kind}_dx"], slack=0.1)
+    assert np.array_equal(t, g[f"ccd_{kind}_t"])
+    t3 = P.accd_toi_batch(name, g[f"ccd_{kind}_x"], g[f"ccd_{kind}_dx"], slack=0.3, t_max=0.7)
+    assert np.array_equal(t3, g[f"ccd_{kind}_t3"])
+
+
+def test_accd_known_answers():
+    x = np.array([[0.2, 0.2, 1.0], [0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    dx = np.zeros((4, 3))
+    dx[0] = [0, 0, -2.0]
+    assert P.accd_toi(P.CcdQuery("vertex-face", x, dx, slack=0.1)) <= 0.5
+    dx[0] = [0, 0, 2.0]
+    assert P.accd_toi(P.CcdQuery("vertex-face", x, dx)) == 1.0
+    with pytest.raises(ValueError):
+        P.accd_toi_batch("vertex-face", np.zeros((1, 4, 3)), np.ones((1, 4, 3)))
+
+
+# ---------------------------------------------------------------------------
+CASES = ["twocube", "aligned", "floor", "ico"]
+
+
+def _bodies(g, p):
+    out = []
+    for v, t, e, dyn in unpack_meshes(p, g):
+        out.append(P.CollisionBody.from_mesh(P.SurfaceMesh(v, t, e), dynamic=dyn))
+    return out
+
+
+def _case(golden, tag):
+    g = golden("contact.npz")
+    p = tag + "_"
+    d_hat, kappa, mu, density, kappa_o, dt = g[p + "params"]
+    return g, p, _bodies(g, p), d_hat, kappa, mu, dt
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_broad_phase_bit_exact(golden, tag):
+    g, p, bodies, d_hat, *_ = _case(golden, tag)
+    q0, dq = g[p + "q0"], g[p + "dq"]
+    for nm, q1 in (("c0", q0), ("c1", q0 + dq)):
+        c = P.broad_phase(bodies, q0, q1, d_hat)
+        assert np.array_equal(c.vf, g[p + nm + "_vf"])
+        assert np.array_equal(c.ee, g[p + nm + "_ee"])
+        assert np.array_equal(c.overlap_pairs, g[p + nm + "_ov"])
+
+
+def _cands(g, p, nm="c0"):
+    return P.CandidateSet(g[p + nm + "_vf"], g[p + nm + "_ee"], g[p + nm + "_ov"])
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_contact_energy_and_blocks(golden, tag):
+    g, p, bodies, d_hat, kappa, mu, dt = _case(golden, tag)
+    q0 = g[p + "q0"]
+    c = _cands(g, p)
+    e = P.contact_energy(bodies, q0, c, kappa, d_hat)
+    assert e == pytest.approx(float(g[p + "energy"]), rel=1e-12, abs=0)
+    for s, proj in (("P", True), ("U", False)):
+        blk = P.contact_gradient_hessian(bodies, q0, c, kappa, d_hat, project=proj)
+        assert np.array_equal(blk.body_a, g[p + f"blk{s}_a"])
+        assert np.array_equal(blk.body_b, g[p + f"blk{s}_b"])
+        assert np.array_equal(blk.d_sq, g[p + f"blk{s}_d2"])
+        for k in range(len(blk.body_a)):
+            assert rel_err(blk.grad[k], g[p + f"blk{s}_g"][k]) <= TOL
+            assert rel_err(blk.hess[k], g[p + f"blk{s}_h"][k]) <= TOL
+            if proj:
+                w = np.linalg.eigvalsh(blk.hess[k])
+                assert w.min() >= -1e-10 * max(1.0, abs(w).max())
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_friction(golden, tag):
+    g, p, bodies, d_hat, kappa, mu, dt = _case(golden, tag)
+    q0 = g[p + "q0"]
+    fr = P.friction_precompute(bodies, q0, _cands(g, p), kappa, d_hat, mu)
+    assert np.array_equal(fr.body_a, g[p + "fr_a"]) and np.array_equal(fr.body_b, g[p + "fr_b"])
+    assert np.allclose(fr.lam, g[p + "fr_lam"], rtol=1e-12, atol=0)
+    assert np.allclose(fr.tangent_map, g[p + "fr_tmap"], rtol=1e-12, atol=1e-15)
+    assert np.allclose(fr.offset, g[p + "fr_off"], rtol=1e-11, atol=1e-13)
+    for k in range(len(fr)):
+        T = fr.basis[k]
+        assert np.allclose(T.T @ T, np.eye(2), atol=1e-12)
+    # evaluate on the reference's own lagged data (exact inputs)
+    ref = P.FrictionData(g[p + "fr_a"], g[p + "fr_b"], g[p + "fr_lam"], mu, g[p + "fr_tmap"], g[p + "fr_off"],
+                         g[p + "fr_basis"])
+    qp = g[p + "qp"]
+    assert P.friction_energy(qp, ref, dt, 1e-3) == pytest.approx(float(g[p + "fr_energy"]), rel=1e-11)
+    dyn = np.array([b.dynamic for b in bodies])
+    for s, proj in (("P", True), ("U", False)):
+        fb = P.friction_gradient_hessian(qp, ref, dt, 1e-3, dyn, project=proj)
+        for k in range(len(ref)):
+            rg = g[p + f"frb{s}_g"][k]
+            if np.abs(rg).max() > 1e-14:
+                assert rel_err(fb.grad[k], rg) <= 1e-8
+            assert rel_err(fb.hess[k], g[p + f"frb{s}_h"][k]) <= TOL
+
+
+@pytest.mark.parametrize("tag", CASES)
+def test_step_filter_assembly_solve(golden, tag):
+    g, p, bodies, d_hat, kappa, mu, dt = _case(golden, tag)
+    q0, dq = g[p + "q0"], g[p + "dq"]
+    a = P.step_filter(bodies, q0, dq, _cands(g, p, "c1"), slack=0.1)
+    assert a == float(g[p + "alpha"])
+    # model with the reference masses
+    gms, mats = [], []
+    for b, M, k in zip(bodies, g[p + "masses"], g[p + "stiff"]):
+        if b.dynamic:
+            gms.append(P.GeneralizedMass.from_moments(M[0, 0], M[0, 3:6], M[3:6, 3:6]))
+            mats.append(P.BodyMaterial(1.0, k, 1.0))
+        else:
+            gms.append(None)
+            mats.append(None)
+    model = P.SystemModel(bodies, gms, mats)
+    ref_fr = P.FrictionData(g[p + "fr_a"], g[p + "fr_b"], g[p + "fr_lam"], mu, g[p + "fr_tmap"],
+                            g[p + "fr_off"], g[p + "fr_basis"])
+    ip = P.IncrementalPotentialState(q0, g[p + "qdot"], g[p + "qtilde"], ref_fr, _cands(g, p), model)
+    prm = P.StepParams(dt=dt, d_hat=d_hat, kappa_barrier=kappa, mu=mu)
+    qp = g[p + "qp"]
+    grad, H = P.assemble(qp, ip, prm)
+    assert rel_err(grad, g[p + "asm_g"]) <= TOL
+    for s in range(len(H.diag)):
+        assert rel_err(H.diag[s], g[p + "asm_diag"][s]) <= TOL
+    keys = [tuple(k) for k in g[p + "asm_off_keys"]]
+    assert sorted(H.off.keys()) == keys
+    for k, blk in zip(keys, g[p + "asm_off_blocks"]):
+        if np.abs(blk).max() > 0:
+            assert rel_err(H.off[k], blk) <= TOL
+    assert P.ip_value(qp, ip, prm) == pytest.approx(float(g[p + "ip"]), rel=1e-12)
+    dx = P.solve_newton_system(H, grad)
+    assert np.linalg.norm(H.matvec(dx) + grad) <= 1e-8 * np.linalg.norm(grad) * 1.0001
+    assert rel_err(dx, g[p + "solve_dx"]) <= 1e-6
+
+
+def test_sparse_solver_and_errors():
+    rng = np.random.default_rng(6)
+    A = P.BlockSparseMatrix(10, [(i, i + 1) for i in range(9)], block_dim=12)
+    for i in range(10):
+        G = rng.normal(size=(12, 12))
+        A.add_diag(i, G @ G.T + 12 * np.eye(12))
+    for i in range(9):
+        A.add_off(i, i + 1, 0.1 * rng.normal(size=(12, 12)))
+    A.add_diag(3, 1e9 * np.eye(12))
+    gvec = rng.normal(size=A.shape[0])
+    x = A.factor().solve_refined(-gvec, rel_tol=1e-8)
+    assert np.linalg.norm(A.matvec(x) + gvec) <= 1e-8 * np.linalg.norm(gvec)
+    assert np.allclose(A.matvec(x), A.to_dense() @ x, rtol=1e-13, atol=1e-9)
+    B = P.BlockSparseMatrix(3, [(0, 1)], block_dim=4)
+    B.add_diag(0, np.eye(4))
+    B.add_diag(1, np.eye(4))
+    B.add_diag(2, -np.eye(4))
+    with pytest.raises(P.FactorizationError) as err:
+        B.factor()
+    assert err.value.block == 2
+    C_ = P.BlockSparseMatrix(5, [], block_dim=12)
+    for i in range(5):
+        G = rng.normal(size=(12, 12))
+        C_.add_diag(i, G @ G.T + 12 * np.eye(12))
+    b = rng.normal(size=60)
+    x = C_.factor().solve(b)
+    for i in range(5):
+        assert np.allclose(x[12 * i:12 * i + 12], np.linalg.solve(C_.diag[i], b[12 * i:12 * i + 12]),
+                           rtol=1e-12, atol=1e-12)
+
+
+def _box_stack_model(g):
+    from paper_2201_10022_b200 import scenes
+    spec = scenes.box_stack(seed=0)
+    model, state, params = spec.build()
+    for mb, (v, t, e, dyn) in zip(model.bodies, unpack_meshes("scene_", g)):
+        assert np.array_equal(mb.rest, v) and np.array_equal(mb.edges, e)
+    return model, state, params
+
+
+def test_box_stack_trajectory(golden):
+    """100-step box stack: per-step DOFs within 1e-6 relative, intersection-free, same Newton counts."""
+    g = golden("box_stack.npz")
+    model, state, params = _box_stack_model(g)
+    iters = []
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for s in range(len(g["iterations"])):
+            state, st = P.advance_step(model, state, params)
+            ref = g["q"][s + 1]
+            err = np.abs(state.q - ref).max() / np.abs(ref).max()
+            assert err <= 1e-6, (s, err)
+            assert st.min_distance > 0.0
+            assert st.min_distance == pytest.approx(g["min_distance"][s], rel=1e-6)
+            assert st.ip_value == pytest.approx(g["ip_value"][s], rel=1e-6, abs=1e-12)
+            iters.append(st.iterations)
+    assert sum(iters) == pytest.approx(int(g["iterations"].sum()), rel=0.05)
+
+
+def test_ico_pile_trajectory(golden):
+    g = golden("ico_pile.npz")
+    from paper_2201_10022_b200 import scenes
+    spec = scenes.icosphere_pile(seed=3, nx=2, ny=2, nz=2, mu=0.5, subdiv=1)
+    model, state, params = spec.build()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for s in range(len(g["iterations"])):
+            state, st = P.advance_step(model, state, params)
+            ref = g["q"][s + 1]
+            assert np.abs(state.q - ref).max() / np.abs(ref).max() <= 1e-6, s
+            assert st.min_distance > 0.0
+
+
+def test_free_body_exact_translation():
+    mesh = P.box_mesh(0.5)
+    gm, vol = P.mass_matrix(mesh, 1000.0)
+    model = P.SystemModel([P.CollisionBody.from_mesh(mesh)], [gm], [P.BodyMaterial(1000.0, 1e11, vol)])
+    params = P.StepParams(dt=0.01)
+    state = P.SimState(q=np.tile(P.BodyCoords.identity().q, (1, 1)), q_dot=np.zeros((1, 12)))
+    state.q_dot[0, :3] = [0.3, -0.1, 0.2]
+    for _ in range(5):
+        new, st = P.advance_step(model, state, params)
+        assert np.abs(new.q[0] - (state.q[0] + params.dt * state.q_dot[0])).max() <= 1e-12
+        assert st.iterations == 1 and st.converged
+        state = new
+
+
+def test_kernel_launch_counter_moves():
+    n0 = _native.kernel_launches()
+    P.point_triangle_closest(np.zeros(3), [0, 0, 1.0], [1.0, 0, 1], [0, 1.0, 1])
+    assert _native.kernel_launches() > n0
