@@ -65,6 +65,12 @@ int abd_project_psd_batch(int64_t n, int k, const double* H, double* out);
 /* accd_toi_batch  ccd.py:59-104.  x, dx: (n,4,3). */
 int abd_accd_batch(int kind, int64_t n, const double* x, const double* dx, double slack, double t_max,
                    int max_iters, double* t);
+/* per-pair contact terms on explicit points (contact.py:486-538 + :646-675 for one pair each):
+ * z, rest (n,4,3) world / rest points, eps_x (n) (EE), dyn (n,2) uint8 side flags.
+ * g12 (n,12), h12 (n,12,12) point-space barrier derivatives; g24 (n,24), h24 (n,24,24). */
+int abd_contact_pair_batch(int kind, int64_t n, const double* z, const double* rest, const double* eps_x,
+                           double kappa, double d_hat, const uint8_t* dyn, int project, double* g12, double* h12,
+                           double* g24, double* h24);
 /* friction_energy / friction_gradient_hessian  contact.py:815-853.
  * pairs: body ids (n), lam (n), tangent_map (n,2,24), offset (n,2); q: (n_bodies,12);
  * dynamic: (n_bodies) uint8.  energy may be NULL; grad24 (n,24)/hess24 (n,24,24) may be NULL. */

@@ -13,7 +13,9 @@ import weakref
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libabd_b200.so")
+LIB_PATH = os.path.join(HERE, "libabd_b200_dbg.so" if os.environ.get("ABD_DEVICE_DEBUG") else
+                        ("libabd_b200_o" + os.environ["ABD_PTXAS_O"] + ".so") if os.environ.get("ABD_PTXAS_O")
+                        else "libabd_b200.so")
 
 ABD_OK, ABD_ERR_ARG, ABD_ERR_CUDA, ABD_ERR_BARRIER_DOMAIN, ABD_ERR_CCD_DOMAIN = 0, 1, 2, 3, 4
 ABD_ERR_FACTORIZATION, ABD_ERR_STEP_FAILURE, ABD_ERR_NO_DEVICE, ABD_ERR_NOT_CONVERGED = 5, 6, 7, 8
@@ -58,7 +60,8 @@ _SIGS = {
     "abd_ortho_batch": (i32, [i64, dp, dp, i32, dp, dp, dp]),
     "abd_project_psd_batch": (i32, [i64, i32, dp, dp]),
     "abd_accd_batch": (i32, [i32, i64, dp, dp, dbl, dbl, i32, dp]),
-    "abd_friction_batch": (i32, [i64, lp, lp, dp, dbl, dp, dp, i32, dp, up8, dbl, dbl, i32, vp, vp, vp]),
+    "abd_contact_pair_batch": (i32, [i32, i64, dp, dp, dp, dbl, dbl, up8, i32, dp, dp, dp, dp]),
+    "abd_friction_batch":(i32, [i64, lp, lp, dp, dbl, dp, dp, i32, dp, up8, dbl, dbl, i32, vp, vp, vp]),
     "abd_bsr_matvec": (i32, [i32, i32, dp, i64, lp, dp, dp, dp]),
     "abd_bsr_pcg": (i32, [i32, i32, dp, i64, lp, dp, dp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
     "abd_scene_create": (vp, [i32, lp, lp, lp, dp, lp, lp, dp, up8, dp, dp]),
@@ -219,6 +222,17 @@ def accd_batch(kind, x, dx, slack, t_max, max_iters):
         check(lib().abd_accd_batch(VF if kind in ("vf", "vertex-face") else EE, n, x, dx, float(slack),
                                    float(t_max), int(max_iters), t))
     return t
+
+
+def contact_pair_batch(kind, z, rest, eps, kappa, d_hat, dyn_ab, project=True):
+    z = f64(z).reshape(-1, 4, 3)
+    n = len(z)
+    out = (np.empty((n, 12)), np.empty((n, 12, 12)), np.empty((n, 24)), np.empty((n, 24, 24)))
+    check(lib().abd_contact_pair_batch(VF if kind == "vf" else EE, n, z, f64(rest).reshape(-1, 4, 3),
+                                       f64(np.broadcast_to(np.asarray(eps, dtype=float), (n,))), float(kappa),
+                                       float(d_hat), np.ascontiguousarray(np.asarray(dyn_ab, dtype=np.uint8).reshape(n, 2)),
+                                       int(project), *out))
+    return out
 
 
 def friction_batch(data, q_all, dynamic, dt, eps_v, project, want_blocks):

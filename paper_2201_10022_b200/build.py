@@ -21,6 +21,14 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                 "-Xptxas", "-warn-spills"]
+if os.environ.get("ABD_PTXAS_O"):
+    BUILD = os.path.join(HERE, "_build_o" + os.environ["ABD_PTXAS_O"])
+    LIB = os.path.join(HERE, "libabd_b200_o" + os.environ["ABD_PTXAS_O"] + ".so")
+    FLAGS = FLAGS + ["-Xptxas", "-O" + os.environ["ABD_PTXAS_O"]]
+if os.environ.get("ABD_DEVICE_DEBUG"):
+    BUILD = os.path.join(HERE, "_build_dbg")
+    LIB = os.path.join(HERE, "libabd_b200_dbg.so")
+    FLAGS = ARCH + ["-G", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 
 
 def _sources():

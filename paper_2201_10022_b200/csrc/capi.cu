@@ -49,6 +49,9 @@ static void ensure_device() {
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
   if (p.major != 10) throw Error(ABD_ERR_NO_DEVICE, "device is not sm_100 (Blackwell B200 required)");
+  size_t cur = 0;
+  CK(cudaDeviceGetLimit(&cur, cudaLimitStackSize));
+  if (cur < 16384) CK(cudaDeviceSetLimit(cudaLimitStackSize, 16384));
   ok = 1;
 }
 
@@ -227,6 +230,25 @@ int abd_accd_batch(int kind, int64_t n, const double* x, const double* dx, doubl
     launch_accd(st, kind, n, dxv.up(x, 12 * n), ddx.up(dx, 12 * n), slack, t_max, max_iters, dt.alloc(n), err.v.p);
     check_flag(err, st, ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
     dt.down(t, n);
+    sync(st);
+  });
+}
+
+int abd_contact_pair_batch(int kind, int64_t n, const double* z, const double* rest, const double* eps_x,
+                           double kappa, double d_hat, const uint8_t* dyn, int project, double* g12, double* h12,
+                           double* g24, double* h24) {
+  return guard([&] {
+    ensure_device();
+    cudaStream_t st = g_stream();
+    Dev<double> dz(st), dr(st), de(st), o1(st), o2(st), o3(st), o4(st);
+    Dev<unsigned char> dd(st);
+    launch_contact_pairs(st, kind, n, dz.up(z, 12 * n), dr.up(rest, 12 * n), de.up(eps_x, n), kappa, d_hat,
+                         dd.up(dyn, 2 * n), project, o1.alloc(12 * n), o2.alloc(144 * n), o3.alloc(24 * n),
+                         o4.alloc(576 * n));
+    o1.down(g12, 12 * n);
+    o2.down(h12, 144 * n);
+    o3.down(g24, 24 * n);
+    o4.down(h24, 576 * n);
     sync(st);
   });
 }

@@ -1,5 +1,6 @@
 // Stateless batch kernels behind the per-function drop-in API
 // (distance.py, contact.py barrier, body.py ortho/project_psd, ccd.py).
+#include "abd_contact.cuh"
 #include "abd_misc.cuh"
 #include "kernels.h"
 
@@ -162,8 +163,41 @@ __global__ void k_friction(int64_t n, const int2* __restrict__ bodies, const dou
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// per-pair contact terms on explicit points (K3 arithmetic without the scene gather)
+__global__ void __launch_bounds__(64) k_contact_pairs(int kind, int64_t n, const double* __restrict__ z,
+                                                      const double* __restrict__ xb, const double* __restrict__ eps,
+                                                      double kappa, double dh, const unsigned char* __restrict__ dyn,
+                                                      int project, double* g12o, double* h12o, double* g24o,
+                                                      double* h24o) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  V3 p[4], r[4];
+  ldz(z, i, p);
+  ldz(xb, i, r);
+  double blk[PB_STRIDE];
+  contact_pair_eval(kind, p, r, eps[i], kappa, dh, dyn[2 * i] != 0, dyn[2 * i + 1] != 0, project != 0, blk,
+                    g12o + 12 * i, h12o + 144 * i);
+  for (int k = 0; k < 24; ++k) g24o[24 * i + k] = blk[k];
+  double* H = h24o + 576 * i;
+  for (int rr = 0; rr < 12; ++rr)
+    for (int cc = 0; cc < 12; ++cc) {
+      H[rr * 24 + cc] = blk[24 + rr * 12 + cc];
+      H[(rr + 12) * 24 + cc + 12] = blk[168 + rr * 12 + cc];
+      H[rr * 24 + cc + 12] = blk[312 + rr * 12 + cc];
+      H[(cc + 12) * 24 + rr] = blk[312 + rr * 12 + cc];
+    }
+}
+
 // ---------------------------------------------------------------------------
 #define GRID(n, b) dim3(grid_for((n), (b))), dim3(b), 0
+
+void launch_contact_pairs(cudaStream_t st, int kind, int64_t n, const double* z, const double* xb, const double* eps,
+                          double kappa, double dh, const unsigned char* dyn, int project, double* g12, double* h12,
+                          double* g24, double* h24) {
+  if (!n) return;
+  k_contact_pairs<<<GRID(n, 64), st>>>(kind, n, z, xb, eps, kappa, dh, dyn, project, g12, h12, g24, h24);
+  note_launch("k_contact_pairs");
+}
 
 void launch_pt_closest(cudaStream_t st, int64_t n, const double* z, double* d2, int* region, double* bary) {
   if (!n) return;

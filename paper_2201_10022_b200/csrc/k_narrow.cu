@@ -1,6 +1,7 @@
 // Scene narrow phase: activity filter, per-pair contact blocks (K3 first
 // pass), contact energy (K6), friction precompute (K7), CCD (K5), per-body
 // inertia + orthogonality terms (K1).
+#include "abd_contact.cuh"
 #include "abd_misc.cuh"
 #include "kernels.h"
 
@@ -85,16 +86,12 @@ __global__ void __launch_bounds__(64) k_pair_blocks(SceneView sv, int kind, int6
   PairIds ids = pair_ids(sv, kind, r);
   V3 z[4], xb[4];
   pair_points(sv, ids, q, z, xb);
-  Closest c = closest(kind, z);
-  double g12[12], tg[12];
-  double H12[144], T1[144], V[144];
-  contact_point_terms(kind, z, c, ids.eps, kappa, dh, g12, H12, tg, T1);
   int64_t o = base + pos[i];
   double* blk = out_blk + o * PB_STRIDE;
-  map_to_bodies(kind, xb, g12, H12, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0, T1, V, blk, blk + 24,
-                blk + 24 + 144, blk + 24 + 288);
+  PairEval ev = contact_pair_eval(kind, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0,
+                                  blk);
   out_bodies[o] = make_int2(r.x, r.z);
-  out_d2[o] = c.d2;
+  out_d2[o] = ev.d2;
 }
 
 __global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
@@ -151,10 +148,12 @@ __global__ void k_friction_pre(SceneView sv, int kind, int64_t n, const int4* __
   double d = sqrt(c.d2);
   double lam = -kappa * 2.0 * d * barrier_terms(c.d2, dh).b1;
   if (kind == KIND_EE) lam = lam * mollifier_value(z, ids.eps);
-  V3 rr = c.gamma[0] * z[0];
-  rr = rr + c.gamma[1] * z[1];
-  rr = rr + c.gamma[2] * z[2];
-  rr = rr + c.gamma[3] * z[3];
+  // r = einsum("ni,nik->nk", gamma, z): sequential order, no FMA (the tangent
+  // helper axis below is picked by argmin |n|, so n must match numpy bitwise)
+  V3 rr = xscale(c.gamma[0], z[0]);
+  rr = xadd3(rr, xscale(c.gamma[1], z[1]));
+  rr = xadd3(rr, xscale(c.gamma[2], z[2]));
+  rr = xadd3(rr, xscale(c.gamma[3], z[3]));
   V3 nrm = V3{rr.x / d, rr.y / d, rr.z / d};
   double ax = fabs(nrm.x), ay = fabs(nrm.y), az = fabs(nrm.z);
   int pick = (ax <= ay && ax <= az) ? 0 : ((ay <= az) ? 1 : 2);

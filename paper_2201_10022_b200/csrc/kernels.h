@@ -43,6 +43,9 @@ void launch_ortho(cudaStream_t st, int64_t n, const double* q, const double* k, 
 void launch_psd(cudaStream_t st, int64_t n, int k, const double* H, double* out);
 void launch_accd(cudaStream_t st, int kind, int64_t n, const double* x, const double* dx, double slack,
                  double tmax, int max_iters, double* t, int* err);
+void launch_contact_pairs(cudaStream_t st, int kind, int64_t n, const double* z, const double* xb, const double* eps,
+                          double kappa, double dh, const unsigned char* dyn, int project, double* g12, double* h12,
+                          double* g24, double* h24);
 void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const double* rec, double mu,
                      const double* q, const unsigned char* dyn, double dt, double eps_v, int project,
                      double* energy_partials, double* grad24, double* hess24, double* pblk_out);

@@ -187,9 +187,18 @@ def test_friction(golden, tag):
     fr = P.friction_precompute(bodies, q0, _cands(g, p), kappa, d_hat, mu)
     assert np.array_equal(fr.body_a, g[p + "fr_a"]) and np.array_equal(fr.body_b, g[p + "fr_b"])
     assert np.allclose(fr.lam, g[p + "fr_lam"], rtol=1e-12, atol=0)
-    assert np.allclose(fr.tangent_map, g[p + "fr_tmap"], rtol=1e-12, atol=1e-15)
-    assert np.allclose(fr.offset, g[p + "fr_off"], rtol=1e-11, atol=1e-13)
+    # the tangent frame is defined up to an in-plane rotation when |n| has tied
+    # small components (rounding noise picks the helper axis); energies and
+    # blocks only see T T^T, so compare the rotation-invariant tmap^T tmap and
+    # tmap^T offset (norm-relative)
     for k in range(len(fr)):
+        A, Ar = fr.tangent_map[k], g[p + "fr_tmap"][k]
+        assert rel_err(A.T @ A, Ar.T @ Ar) <= 1e-12
+        # offset = tmap . q_pair(q_prev): a cancellation-limited quantity, compare
+        # against the scale of its terms
+        qp = np.concatenate([q0[fr.body_a[k]], q0[fr.body_b[k]]])
+        scale = np.linalg.norm(A) * np.linalg.norm(qp)
+        assert np.linalg.norm(A.T @ fr.offset[k] - Ar.T @ g[p + "fr_off"][k]) <= 1e-12 * scale
         T = fr.basis[k]
         assert np.allclose(T.T @ T, np.eye(2), atol=1e-12)
     # evaluate on the reference's own lagged data (exact inputs)
