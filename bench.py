@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 ABD Newton steps on the 10k-body icosphere pile (BASELINE config 4).
+
+    python bench.py [--gpus N --steps K --warmup W --start S]
+    python bench.py --impl reference ...        (CPU oracle arm)
+
+A "step" is one implicit time step (`advance_step`: broad phase, friction
+precompute, Newton loop with assembly / PCG / CCD / line search, stats).
+Timed steps are [S + W, S + W + K) of the pile simulation from its seeded
+initial state.  `value` is measured on the device-resident C-ABI path;
+`e2e` repeats the same window through the Python API (`advance_step`) with
+host numpy state (H2D q, q_dot, forces and D2H q, q_dot every step).
+Prints one JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+import warnings
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": HBM_FALLBACK}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.path = f"/tmp/abd_clocks_{os.getpid()}.csv"
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if len(r) > 5 + k and "Active" in r[5 + k]
+                          and "Not" not in r[5 + k]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def oracle_sample_rate(spec_kw, start_steps, budget_s, threads_note):
+    """Oracle advance_step steps/s on a 8x8x2 sub-pile (same generator), scaled to 10k bodies."""
+    from oracle import abd_oracle as O
+    from paper_2201_10022_b200 import scenes
+    from paper_2201_10022_b200.body import mass_matrix
+
+    spec = scenes.icosphere_pile(seed=0, nx=8, ny=8, nz=2, **spec_kw)
+    from types import SimpleNamespace
+    bodies, masses, stiff = [], [], []
+    cache = {}
+    for m, dyn in zip(spec.meshes, spec.dynamic):
+        d = m.vertices[m.edges[:, 1]] - m.vertices[m.edges[:, 0]]
+        bodies.append(SimpleNamespace(rest=m.vertices, triangles=m.triangles, edges=m.edges,
+                                      edge_rest_len_sq=np.einsum("ij,ij->i", d, d), dynamic=bool(dyn)))
+        if dyn:
+            if id(m) not in cache:
+                cache[id(m)] = mass_matrix(m, spec.density)
+            gm, vol = cache[id(m)]
+            masses.append(gm.matrix)
+            stiff.append(spec.kappa_ortho * vol)
+        else:
+            masses.append(None)
+            stiff.append(None)
+    model = O.OracleModel(bodies, masses, stiff)
+    prm = O.OracleParams(**spec.params)
+    f = np.zeros((len(bodies), 12))
+    g = np.array(spec.gravity)
+    for b in model.dyn:
+        f[b, :3] = masses[b][0, 0] * g
+        f[b, 3:] = np.kron(g, masses[b][0, 3:6])
+    q, qd = spec.q0.copy(), spec.q_dot0.copy()
+    warnings.simplefilter("ignore")
+    for _ in range(start_steps):
+        q, qd, _ = O.advance_step(model, q, qd, f, prm, min_distance=False)
+    n = 0
+    t0 = time.perf_counter()
+    iters = 0
+    while True:
+        q, qd, st = O.advance_step(model, q, qd, f, prm, min_distance=True)
+        n += 1
+        iters += st.iterations
+        el = time.perf_counter() - t0
+        if el >= budget_s or n >= 200:
+            break
+    nb = int(model.dynamic.sum())
+    scale = nb / 10000.0
+    return {"rate_sample": n / el, "steps": n, "seconds": el, "iters": iters, "bodies": nb,
+            "value": n / el * scale, "scale": scale, "note": threads_note}
+
+
+def run_reference(args):
+    """--impl reference: the oracle restatement of the reference path on the host CPU."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = oracle_sample_rate({}, args.warmup, args.steps * 4.0, f"numpy, {cores} host threads available")
+    line = {
+        "impl": "reference", "metric": "sim steps/s (10k-body icosphere pile, fp64 ABD)", "value": r["value"],
+        "unit": "steps/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
+        "ms_per_step": 1e3 / r["value"] if r["value"] else None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
+        "config": {"workload": "icosphere_pile 20x20x25 (10,001 bodies) -- CPU sample 4x4x2 scaled",
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": r["value"], "unit": "steps/s", "cores": cores, "kind": "port",
+                         "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} "
+                                   f"icospheres + ground, same generator) from step {args.warmup}, "
+                                   f"{r['steps']} steps in {r['seconds']:.1f}s, x{r['scale']:.4f} linear "
+                                   "body scaling to 10k (optimistic for the CPU)"},
+        "e2e": {"value": r["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=45)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--start", type=int, default=0, help="untimed steps before warm-up")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=20)
+    ap.add_argument("--nz", type=int, default=25)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_mod
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+
+    import paper_2201_10022_b200 as P
+    from paper_2201_10022_b200 import _native, scenes
+    from paper_2201_10022_b200.solver import step_params_c
+
+    spec = scenes.icosphere_pile(seed=0, nx=args.nx, ny=args.nx, nz=args.nz)
+    model, state, params = spec.build()
+    B = len(model.bodies)
+    L = _native.lib()
+    sc = model.gpu_scene()
+    forces = np.ascontiguousarray(model.forces(0, params.dt, state.q), dtype=np.float64)
+    q = np.ascontiguousarray(state.q, dtype=np.float64)
+    qd = np.ascontiguousarray(state.q_dot, dtype=np.float64)
+    _native.check(L.abd_set_state(sc.ptr, q.ctypes.data, qd.ctypes.data))
+    cp = step_params_c(params)
+    st = _native.StepStatsC()
+    warnings.simplefilter("ignore")
+
+    def step(first=False):
+        _native.check(L.abd_advance_step(sc.ptr, forces.ctypes.data if first else None, C.byref(cp), C.byref(st),
+                                         None))
+        return st.iterations
+
+    step(first=True)
+    for _ in range(args.start + args.warmup - 1):
+        step()
+    # snapshot the window's initial state for the e2e pass
+    q_start = np.empty((B, 12))
+    qd_start = np.empty((B, 12))
+    _native.check(L.abd_get_state(sc.ptr, q_start.ctypes.data, qd_start.ctypes.data))
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    _native.check(L.abd_kernel_stats_reset(sc.ptr))
+    n_launch0 = _native.kernel_launches()
+    barrier()
+    iters = 0
+    pcg_total = 0
+    with ClockSampler(local) as clk:
+        _native.check(L.abd_timer_start(sc.ptr))
+        for _ in range(args.steps):
+            iters += step()
+            pcg_total += st.pcg_iters_total
+        ms = C.c_double(0.0)
+        _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
+    barrier()
+    launches = _native.kernel_launches() - n_launch0
+    elapsed_ms = max_over_ranks(ms.value)
+    iters_all = max_over_ranks(float(iters))
+    value = world * args.steps / (elapsed_ms * 1e-3)
+    # dominant kernel: the PCG solve (k_pcg); stats on this rank
+    kst = {}
+    for which, name in ((0, "k_pcg"), (1, "k_pair_blocks"), (2, "k_ccd"), (3, "k_prim_pairs")):
+        n_, t_, b_, u_ = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
+        _native.check(L.abd_kernel_stats(sc.ptr, which, C.byref(n_), C.byref(t_), C.byref(b_), C.byref(u_)))
+        kst[name] = {"launches": n_.value, "ms": t_.value, "bytes": b_.value, "units": u_.value}
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", HBM_FALLBACK))
+    pc = kst["k_pcg"]
+    achieved = (pc["bytes"] / pc["launches"]) / (pc["ms"] / pc["launches"] * 1e-3) / 1e9 if pc["launches"] else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "pcg_dram_bytes_per_launch.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "k_pcg (block-Jacobi PCG, one cooperative launch per solve)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
+                "traffic": traffic, "peak_source": pk_kind,
+                "bytes_model": "per PCG iteration 1152*(nnzb + n) + 13*96*n (SURVEY 8(d) K4)",
+                "share_of_step": pc["ms"] / elapsed_ms if elapsed_ms else None,
+                "other_kernels": {k: v for k, v in kst.items() if k != "k_pcg"}}
+
+    # e2e through the public Python API with host numpy state
+    e2e = None
+    if not args.no_e2e:
+        state2 = P.SimState(q=q_start.copy(), q_dot=qd_start.copy(), time=0.0, step_index=args.start + args.warmup)
+        barrier()
+        _native.check(L.abd_timer_start(sc.ptr))
+        for _ in range(args.steps):
+            state2, _st = P.advance_step(model, state2, params)
+        ms2 = C.c_double(0.0)
+        _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms2)))
+        barrier()
+        e_ms = max_over_ranks(ms2.value)
+        e2e = {"value": world * args.steps / (e_ms * 1e-3), "unit": "steps/s",
+               "h2d_bytes_per_step": 3 * 96 * B, "d2h_bytes_per_step": 2 * 96 * B,
+               "path": "paper_2201_10022_b200.advance_step (Python API, host numpy q/q_dot/forces)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        r = oracle_sample_rate({}, args.start + args.warmup, args.cpu_budget, "1 thread")
+        cpu = {"value": r["value"], "unit": "steps/s", "cores": 1, "kind": "port",
+               "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} icospheres + "
+                         f"ground, same generator) from step {args.start + args.warmup}: {r['steps']} steps in "
+                         f"{r['seconds']:.1f}s ({r['rate_sample']:.3f} steps/s), x{r['scale']:.4f} linear body "
+                         "scaling to the 10k pile (optimistic for the CPU)"}
+
+    if rank == 0:
+        line = {
+            "metric": "sim steps/s (10k-body icosphere pile, fp64 ABD)", "value": value, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
+            "config": {"workload": f"icosphere_pile {args.nx}x{args.nx}x{args.nz} ({B} bodies, seed 0), "
+                                   f"steps [{args.start + args.warmup}, {args.start + args.warmup + args.steps})",
+                       "newton_iters": int(iters_all), "newton_it_per_s": world * iters_all / (elapsed_ms * 1e-3),
+                       "pcg_iters": pcg_total,
+                       "l2": "per-step working set exceeds L2 (rest+topology+vertex boxes > 126 MB); no flush",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -163,6 +163,16 @@ typedef struct abd_step_stats {
   double t_broad, t_assemble, t_solve, t_ccd, t_line_search, t_total; /* ms, CUDA events */
 } abd_step_stats;
 
+/* per-kernel instrumentation accumulated by the driver (CUDA events on the scene stream):
+ * which = 0: block-Jacobi PCG solve (k_pcg), 1: pair assembly (k_pair_blocks),
+ * 2: CCD (k_ccd), 3: broad phase primitive pairs (k_prim_pairs).
+ * launches, total device ms, total algorithmic bytes (SURVEY §8(d) per-unit figures). */
+int abd_kernel_stats(abd_scene* s, int which, int64_t* launches, double* ms, double* bytes, int64_t* units);
+int abd_kernel_stats_reset(abd_scene* s);
+/* device timer on the scene stream: start records an event, stop syncs and returns ms */
+int abd_timer_start(abd_scene* s);
+int abd_timer_stop(abd_scene* s, double* ms);
+
 int abd_set_state(abd_scene* s, const double* q, const double* q_dot);
 int abd_get_state(abd_scene* s, double* q, double* q_dot);
 /* forces (n_bodies,12) host; NULL = reuse the last uploaded forces. energy_trace may be NULL

@@ -274,26 +274,44 @@ def barrier_terms(d_sq, d_hat):
 # ---------------------------------------------------------------------------
 # gathers (contact.py:419-463) and Jacobians (contact.py:466-483)
 
+_FLAT: dict = {}
+
+
+def _flat(bodies):
+    """Concatenated geometry with per-body offsets (cached per body list)."""
+    key = tuple(id(b) for b in bodies)
+    ent = _FLAT.get(key)
+    if ent is not None:
+        return ent
+    vo = np.cumsum([0] + [len(b.rest) for b in bodies])
+    rest = np.concatenate([b.rest for b in bodies])
+    tris = np.concatenate([np.asarray(b.triangles, dtype=np.int64) + vo[i] for i, b in enumerate(bodies)])
+    edges = np.concatenate([np.asarray(b.edges, dtype=np.int64) + vo[i] for i, b in enumerate(bodies)])
+    to = np.cumsum([0] + [len(b.triangles) for b in bodies])
+    eo = np.cumsum([0] + [len(b.edges) for b in bodies])
+    el2 = np.concatenate([np.asarray(b.edge_rest_len_sq, dtype=float) for b in bodies])
+    ent = (vo, to, eo, rest, tris, edges, el2)
+    if len(_FLAT) > 8:
+        _FLAT.clear()
+    _FLAT[key] = ent
+    return ent
+
+
 def gather(kind, bodies, X, rows):
-    """World points z (N,4,3), rest points (N,4,3), eps_x (EE) for rows."""
+    """World points z (N,4,3), rest points (N,4,3), eps_x (EE) for rows (contact.py:419-463)."""
     rows = np.asarray(rows, dtype=np.int64).reshape(-1, 4)
-    n = len(rows)
-    z = np.empty((n, 4, 3))
-    rp = np.empty((n, 4, 3))
-    eps = np.ones(n)
-    for k in range(n):
-        ba, pa, bb, pb = (int(x) for x in rows[k])
-        A, B = bodies[ba], bodies[bb]
-        if kind == "vf":
-            ids = [(ba, pa)] + [(bb, int(v)) for v in B.triangles[pb]]
-        else:
-            ea, eb = A.edges[pa], B.edges[pb]
-            ids = [(ba, int(ea[0])), (ba, int(ea[1])), (bb, int(eb[0])), (bb, int(eb[1]))]
-            eps[k] = MOLLIFIER_SCALE * A.edge_rest_len_sq[pa] * B.edge_rest_len_sq[pb]
-        for m, (b, v) in enumerate(ids):
-            z[k, m] = X[b][v]
-            rp[k, m] = bodies[b].rest[v]
-    return z, rp, eps
+    vo, to, eo, rest, tris, edges, el2 = _flat(bodies)
+    Xall = np.concatenate(X) if len(X) else np.zeros((0, 3))
+    if kind == "vf":
+        vid = np.stack([vo[rows[:, 0]] + rows[:, 1]] + [tris[to[rows[:, 2]] + rows[:, 3], k] for k in range(3)],
+                       axis=1)
+        eps = np.ones(len(rows))
+    else:
+        ea = eo[rows[:, 0]] + rows[:, 1]
+        eb = eo[rows[:, 2]] + rows[:, 3]
+        vid = np.stack([edges[ea, 0], edges[ea, 1], edges[eb, 0], edges[eb, 1]], axis=1)
+        eps = MOLLIFIER_SCALE * el2[ea] * el2[eb]
+    return Xall[vid].reshape(-1, 4, 3), rest[vid].reshape(-1, 4, 3), eps
 
 
 SIDES = {"vf": (0, 1, 1, 1), "ee": (0, 0, 1, 1)}

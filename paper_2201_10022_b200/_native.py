@@ -83,6 +83,10 @@ _SIGS = {
     "abd_assemble": (i32, [vp, dp, dp, dbl, dbl, dbl, dbl, C.POINTER(i64)]),
     "abd_get_system": (i32, [vp, dp, dp, lp, dp]),
     "abd_solve_resident": (i32, [vp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
+    "abd_kernel_stats": (i32, [vp, i32, C.POINTER(i64), C.POINTER(dbl), C.POINTER(dbl), C.POINTER(i64)]),
+    "abd_kernel_stats_reset": (i32, [vp]),
+    "abd_timer_start": (i32, [vp]),
+    "abd_timer_stop": (i32, [vp, C.POINTER(dbl)]),
     "abd_set_state": (i32, [vp, vp, vp]),
     "abd_get_state": (i32, [vp, vp, vp]),
     "abd_advance_step": (i32, [vp, vp, C.POINTER(StepParamsC), C.POINTER(StepStatsC), vp]),

@@ -100,6 +100,134 @@ ABD_D void ortho_derivs_dev(const double* q, double k, double* g, double* H) {
         }
 }
 
+// symmetric 3x3 eigen-decomposition (cyclic Jacobi): S = V diag(w) V^T, columns V[:][i]
+ABD_D void sym3_eig(double S[3][3], double w[3], double V[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) V[i][j] = i == j ? 1.0 : 0.0;
+  double fro = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) fro += S[i][j] * S[i][j];
+  for (int sweep = 0; sweep < 30 && fro > 0.0; ++sweep) {
+    double off = S[0][1] * S[0][1] + S[0][2] * S[0][2] + S[1][2] * S[1][2];
+    if (off <= 1e-36 * fro) break;
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int q = p + 1; q < 3; ++q) {
+        double apq = S[p][q];
+        if (apq == 0.0) continue;
+        double theta = (S[q][q] - S[p][p]) / (2.0 * apq);
+        double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c, tau = s / (1.0 + c);
+        S[p][p] -= t * apq;
+        S[q][q] += t * apq;
+        S[p][q] = S[q][p] = 0.0;
+        int r = 3 - p - q;
+        double g = S[r][p], h = S[r][q];
+        S[r][p] = S[p][r] = g - s * (h + g * tau);
+        S[r][q] = S[q][r] = h + s * (g - h * tau);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double g2 = V[k][p], h2 = V[k][q];
+          V[k][p] = g2 - s * (h2 + g2 * tau);
+          V[k][q] = h2 + s * (g2 - h2 * tau);
+        }
+      }
+  }
+  w[0] = S[0][0];
+  w[1] = S[1][1];
+  w[2] = S[2][2];
+}
+
+// PSD projection of the orthogonality Hessian in closed form.  With
+// A = U diag(s) V^T, the Hessian acts on dA = U X V^T as
+//   H[X]_ij = 4k ((s_i^2 + s_j^2 - 1) X_ij + s_i s_j X_ji)
+// so its 9 eigenpairs are 4k(3 s_i^2 - 1) on u_i v_i^T and
+// 4k(s_i^2 + s_j^2 - 1 +- s_i s_j) on (u_i v_j^T +- u_j v_i^T)/sqrt2.
+// proj(H) = H - sum_{lambda < 0} lambda vec(dA) vec(dA)^T  (equals the
+// reference's eigh-clamp of body.py:281-296 applied at solver.py:292-294).
+ABD_D void ortho_project_closed(const double* q, double k, double* H) {
+  const double* A = q + 3;  // A[r][c] = A[3 r + c]
+  double S[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) S[a][b] = A[a] * A[b] + A[3 + a] * A[3 + b] + A[6 + a] * A[6 + b];
+  double w[3], V[3][3];
+  sym3_eig(S, w, V);
+  // order by descending singular value
+  int o0 = 0, o1 = 1, o2 = 2;
+  if (w[o0] < w[o1]) { int t = o0; o0 = o1; o1 = t; }
+  if (w[o1] < w[o2]) { int t = o1; o1 = o2; o2 = t; }
+  if (w[o0] < w[o1]) { int t = o0; o0 = o1; o1 = t; }
+  int ord[3] = {o0, o1, o2};
+  double s[3], v[3][3], u[3][3];  // v[i], u[i]: i-th singular vectors
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    s[i] = sqrt(fmax(w[ord[i]], 0.0));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[i][c] = V[c][ord[i]];
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) u[i][r] = A[3 * r] * v[i][0] + A[3 * r + 1] * v[i][1] + A[3 * r + 2] * v[i][2];
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      double d = u[i][0] * u[j][0] + u[i][1] * u[j][1] + u[i][2] * u[j][2];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) u[i][r] -= d * u[j][r];
+    }
+    double nn = sqrt(u[i][0] * u[i][0] + u[i][1] * u[i][1] + u[i][2] * u[i][2]);
+    if (nn > 1e-12 * (s[0] > 0.0 ? s[0] : 1.0)) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) u[i][r] /= nn;
+    } else if (i == 2) {
+      u[2][0] = u[0][1] * u[1][2] - u[0][2] * u[1][1];
+      u[2][1] = u[0][2] * u[1][0] - u[0][0] * u[1][2];
+      u[2][2] = u[0][0] * u[1][1] - u[0][1] * u[1][0];
+    } else {
+      // degenerate: any unit vector orthogonal to the previous ones
+      double e[3] = {1.0, 0.0, 0.0};
+      for (int tries = 0; tries < 3; ++tries) {
+        e[0] = tries == 0; e[1] = tries == 1; e[2] = tries == 2;
+        for (int j = 0; j < i; ++j) {
+          double d = e[0] * u[j][0] + e[1] * u[j][1] + e[2] * u[j][2];
+          for (int r = 0; r < 3; ++r) e[r] -= d * u[j][r];
+        }
+        double ne = sqrt(e[0] * e[0] + e[1] * e[1] + e[2] * e[2]);
+        if (ne > 0.5) {
+          for (int r = 0; r < 3; ++r) u[i][r] = e[r] / ne;
+          break;
+        }
+      }
+    }
+  }
+  const double k4 = 4.0 * k;
+  const double r2 = 0.70710678118654752440;
+  // negative modes only
+  for (int m = 0; m < 9; ++m) {
+    int i, j;
+    double sg;
+    if (m < 3) { i = j = m; sg = 0.0; }
+    else { int p = (m - 3) >> 1; i = p == 2 ? 1 : 0; j = p == 0 ? 1 : 2; sg = ((m - 3) & 1) ? -1.0 : 1.0; }
+    double lam = (m < 3) ? k4 * (3.0 * s[i] * s[i] - 1.0) : k4 * (s[i] * s[i] + s[j] * s[j] - 1.0 + sg * s[i] * s[j]);
+    if (!(lam < 0.0)) continue;
+    double dA[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        dA[3 * r + c] = (m < 3) ? u[i][r] * v[i][c] : r2 * (u[i][r] * v[j][c] + sg * u[j][r] * v[i][c]);
+    for (int a = 0; a < 9; ++a)
+      for (int b = 0; b < 9; ++b) H[(3 + a) * 12 + 3 + b] -= lam * dA[a] * dA[b];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // friction on one lagged pair (contact.py:805-853).  rec: tmap(48) off(2) lam(1)
 struct FricEval {

@@ -705,6 +705,44 @@ int abd_solve_resident(abd_scene* h, double rel_tol, int max_iters, double* dx, 
   });
 }
 
+int abd_kernel_stats(abd_scene* h, int which, int64_t* launches, double* ms, double* bytes, int64_t* units) {
+  return guard([&] {
+    SC(h);
+    if (which < 0 || which > 3) throw Error(ABD_ERR_ARG, "kernel stats index out of range");
+    Scene::KStat& k = s.kstat[which];
+    if (launches) *launches = k.launches;
+    if (ms) *ms = k.ms;
+    if (bytes) *bytes = k.bytes;
+    if (units) *units = k.units;
+  });
+}
+
+int abd_kernel_stats_reset(abd_scene* h) {
+  return guard([&] {
+    SC(h);
+    for (auto& k : s.kstat) k = Scene::KStat{};
+  });
+}
+
+int abd_timer_start(abd_scene* h) {
+  return guard([&] {
+    SC(h);
+    CK(cudaStreamSynchronize(s.stream));
+    CK(cudaEventRecord(s.tev0, s.stream));
+  });
+}
+
+int abd_timer_stop(abd_scene* h, double* ms) {
+  return guard([&] {
+    SC(h);
+    CK(cudaEventRecord(s.tev1, s.stream));
+    CK(cudaEventSynchronize(s.tev1));
+    float m = 0.f;
+    CK(cudaEventElapsedTime(&m, s.tev0, s.tev1));
+    *ms = m;
+  });
+}
+
 int abd_set_state(abd_scene* h, const double* q, const double* q_dot) {
   return guard([&] {
     SC(h);

@@ -1,6 +1,7 @@
 // Scene-level operations and the Newton driver (solver.py:179-628) with
-// device-resident state; only scalars (alpha, energies, |dq|, g.dq) cross
-// to the host per iteration.
+// device-resident state.  Per Newton iteration only a handful of scalars
+// cross to the host (candidate counts, |dq|_inf and g.dq, alpha_max, one
+// energy per line-search trial); all buffers are persistent workspaces.
 #include <chrono>
 #include <cmath>
 #include <vector>
@@ -11,20 +12,16 @@ namespace abd {
 
 // ---------------------------------------------------------------------------
 // small helper kernels
-__global__ void k_absmax(int64_t n, const double* __restrict__ x, unsigned long long* out) {
-  double m = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = fmax(m, fabs(x[i]));
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
-}
-
-__global__ void k_dot_partials(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
-                               double* partials) {
+__global__ void k_absmax_dot(int64_t n, const double* __restrict__ x, const double* __restrict__ g,
+                             unsigned long long* amax, double* partials) {
   __shared__ double sh[RED_THREADS];
-  double acc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    acc += a[i] * b[i];
+  double m = 0.0, acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    m = fmax(m, fabs(x[i]));
+    acc += g[i] * x[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax, (unsigned long long)__double_as_longlong(m));
   sh[threadIdx.x] = acc;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -75,71 +72,82 @@ __global__ void k_ortho_err(int n_dyn, const int* __restrict__ dyn_body, const d
 }
 
 // ---------------------------------------------------------------------------
-static double absmax(Scene& s, const double* x, int64_t n) {
-  DVec<unsigned long long> m;
-  m.resize(1);
-  m.zero(s.stream);
-  if (n) {
-    k_absmax<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(n, x, m.p);
-    note_launch("k_absmax");
+static double bits_to_d(unsigned long long b) { return __builtin_bit_cast(double, b); }
+static unsigned long long d_to_bits(double d) { return (unsigned long long)__builtin_bit_cast(long long, d); }
+
+struct EventTimer {
+  Scene& s;
+  int which;
+  bool on;
+  EventTimer(Scene& sc, int w) : s(sc), which(w), on(sc.instrument) {
+    if (on) CK(cudaEventRecord(s.ev0, s.stream));
   }
-  unsigned long long h = 0;
-  CK(cudaMemcpyAsync(&h, m.p, sizeof(h), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
-  return __builtin_bit_cast(double, h);
-}
+  // call after the host has synchronised the stream
+  void done(int64_t units, double bytes) {
+    if (!on) return;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+    Scene::KStat& k = s.kstat[which];
+    k.launches += 1;
+    k.units += units;
+    k.ms += ms;
+    k.bytes += bytes;
+  }
+  void stop() {
+    if (on) CK(cudaEventRecord(s.ev1, s.stream));
+  }
+};
 
-static double dot_det(Scene& s, const double* a, const double* b, int64_t n) {
-  s.red.resize(RED_BLOCKS);
-  k_dot_partials<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(n, a, b, s.red.p);
-  note_launch("k_dot_partials");
-  return reduce_sum_det(s, s.red.p, RED_BLOCKS);
-}
-
-static void check_err_flag(Scene& s, DVec<int>& err, int code, const char* msg) {
-  int h = 0;
-  CK(cudaMemcpyAsync(&h, err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
-  if (h) throw Error(code, msg);
-}
-
-// ---------------------------------------------------------------------------
-int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project) {
+// flags + exclusive scan of candidate activity (d^2 < d_hat^2) into s.w.flags/pos;
+// returns the active count (one host sync, also checks the barrier domain)
+static int active_scan(Scene& s, const double* q, double dh) {
   int64_t n_vf = s.cands.n_vf, n_ee = s.cands.n_ee;
   int64_t n = n_vf + n_ee;
-  DVec<int> flags, pos, err;
-  flags.resize(n + 1);
-  pos.resize(n + 1);
-  err.resize(1);
-  err.zero(s.stream);
+  Scene::Work& w = s.w;
+  w.flags.resize(n + 1);
+  w.pos.resize(n + 1);
+  w.err.resize(2);
+  w.err.zero(s.stream);
   double dh2 = dh * dh;
-  launch_pair_flags(s, KIND_VF, q, dh2, flags.p, err.p);
-  launch_pair_flags(s, KIND_EE, q, dh2, flags.p + n_vf, err.p);
-  CK(cudaMemsetAsync(flags.p + n, 0, sizeof(int), s.stream));
-  scan_exclusive_i32(s, flags.p, pos.p, n + 1);
-  int total = 0, n_vf_act = 0;
-  CK(cudaMemcpyAsync(&total, pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaMemcpyAsync(&n_vf_act, pos.p + n_vf, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  check_err_flag(s, err, ABD_ERR_BARRIER_DOMAIN,
-                 "barrier evaluated at non-positive squared distance (intersection reached)");
+  launch_pair_flags(s, KIND_VF, q, dh2, w.flags.p, w.err.p);
+  launch_pair_flags(s, KIND_EE, q, dh2, w.flags.p + n_vf, w.err.p);
+  CK(cudaMemsetAsync(w.flags.p + n, 0, sizeof(int), s.stream));
+  scan_exclusive_i32(s, w.flags.p, w.pos.p, n + 1);
+  int* hp = reinterpret_cast<int*>(s.h_pinned);
+  CK(cudaMemcpyAsync(hp, w.pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaMemcpyAsync(hp + 1, w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  if (hp[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
+                                                 "(intersection reached; CCD filtering must prevent this)");
+  return hp[0];
+}
+
+int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project) {
+  int64_t n_vf = s.cands.n_vf;
+  int total = active_scan(s, q, dh);
   s.pblk.bodies.resize(std::max(total, 1));
   s.pblk.blk.resize((int64_t)std::max(total, 1) * PB_STRIDE);
   s.pblk.d2.resize(std::max(total, 1));
   s.pblk.n = total;
-  launch_pair_blocks(s, KIND_VF, q, kappa, dh, project, flags.p, pos.p, 0, err.p);
-  launch_pair_blocks(s, KIND_EE, q, kappa, dh, project, flags.p + n_vf, pos.p + n_vf, 0, err.p);
+  EventTimer tm(s, 1);
+  launch_pair_blocks(s, KIND_VF, q, kappa, dh, project, s.w.flags.p, s.w.pos.p, 0, s.w.err.p);
+  launch_pair_blocks(s, KIND_EE, q, kappa, dh, project, s.w.flags.p + n_vf, s.w.pos.p + n_vf, 0, s.w.err.p);
+  tm.stop();
   CK(cudaStreamSynchronize(s.stream));
-  (void)n_vf_act;
+  // algorithmic bytes (scene form): candidate record 16 B + 4 rest points 96 B
+  // (+ eps 8 B for EE) per candidate, one PB_STRIDE record written per active pair
+  double bytes = 112.0 * (double)(s.cands.n_vf + s.cands.n_ee) + 8.0 * (double)s.cands.n_ee +
+                 8.0 * PB_STRIDE * (double)total;
+  tm.done(total, bytes);
   return total;
 }
 
-// append friction blocks of the resident friction set after n_c contact blocks
+// append friction blocks of the resident friction set after the contact blocks
 void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, int project) {
   int64_t nc = s.pblk.n, nf = s.fric.n;
   if (nf == 0) return;
-  // grow keeping the contact part
   int64_t tot = nc + nf;
-  if ((size_t)tot > s.pblk.bodies.cap || (size_t)tot * PB_STRIDE > s.pblk.blk.cap) {
+  if ((size_t)tot > s.pblk.bodies.cap || (size_t)tot * PB_STRIDE > s.pblk.blk.cap || (size_t)tot > s.pblk.d2.cap) {
     DVec<int2> b2;
     DVec<double> k2, d2;
     b2.resize(tot);
@@ -158,6 +166,7 @@ void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, 
     std::swap(s.pblk.d2.p, d2.p);
     std::swap(s.pblk.d2.cap, d2.cap);
   }
+  s.pblk.bodies.n = tot;
   CK(cudaMemcpyAsync(s.pblk.bodies.p + nc, s.fric.bodies.p, nf * sizeof(int2), cudaMemcpyDeviceToDevice, s.stream));
   launch_friction(s.stream, nf, s.fric.bodies.p, s.fric.rec.p, s.fric.mu, q, s.dyn.p, dt, eps_v, project, nullptr,
                   nullptr, nullptr, s.pblk.blk.p + nc * PB_STRIDE);
@@ -166,22 +175,9 @@ void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, 
 
 int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, double mu, DVec<double>* basis) {
   if (mu < 0) throw Error(ABD_ERR_ARG, "friction coefficient must be >= 0");
-  int64_t n_vf = s.cands.n_vf, n_ee = s.cands.n_ee;
-  int64_t n = n_vf + n_ee;
+  int64_t n_vf = s.cands.n_vf;
   s.fric.mu = mu;
-  DVec<int> flags, pos, err;
-  flags.resize(n + 1);
-  pos.resize(n + 1);
-  err.resize(1);
-  err.zero(s.stream);
-  double dh2 = dh * dh;
-  launch_pair_flags(s, KIND_VF, q, dh2, flags.p, err.p);
-  launch_pair_flags(s, KIND_EE, q, dh2, flags.p + n_vf, err.p);
-  CK(cudaMemsetAsync(flags.p + n, 0, sizeof(int), s.stream));
-  scan_exclusive_i32(s, flags.p, pos.p, n + 1);
-  int total = 0;
-  CK(cudaMemcpyAsync(&total, pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  check_err_flag(s, err, ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance");
+  int total = active_scan(s, q, dh);
   s.fric.n = total;
   s.fric.bodies.resize(std::max(total, 1));
   s.fric.rec.resize((int64_t)std::max(total, 1) * FRIC_STRIDE);
@@ -190,24 +186,48 @@ int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, 
     basis->resize((int64_t)std::max(total, 1) * 6);
     bp = basis->p;
   }
-  launch_friction_pre(s, KIND_VF, q, kappa, dh, flags.p, pos.p, 0, bp);
-  launch_friction_pre(s, KIND_EE, q, kappa, dh, flags.p + n_vf, pos.p + n_vf, 0, bp);
-  CK(cudaStreamSynchronize(s.stream));
+  launch_friction_pre(s, KIND_VF, q, kappa, dh, s.w.flags.p, s.w.pos.p, 0, bp);
+  launch_friction_pre(s, KIND_EE, q, kappa, dh, s.w.flags.p + n_vf, s.w.pos.p + n_vf, 0, bp);
   return total;
 }
 
+// energy pieces as 4 fixed-order sums: body | contact VF | contact EE | friction
+static void energy_terms(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh,
+                         double eps_v, double out[4]) {
+  s.red.resize(4 * RED_BLOCKS);
+  s.w.err.resize(2);
+  s.w.err.zero(s.stream);
+  s.w.scal.resize(4);
+  launch_body_terms(s, q, qt, dt, nullptr, nullptr, s.red.p, 0);
+  launch_contact_energy(s, KIND_VF, q, kappa, dh, s.red.p + RED_BLOCKS, s.w.err.p);
+  launch_contact_energy(s, KIND_EE, q, kappa, dh, s.red.p + 2 * RED_BLOCKS, s.w.err.p);
+  if (s.fric.n)
+    launch_friction(s.stream, s.fric.n, s.fric.bodies.p, s.fric.rec.p, s.fric.mu, q, s.dyn.p, dt, eps_v, 0,
+                    s.red.p + 3 * RED_BLOCKS, nullptr, nullptr, nullptr);
+  else
+    CK(cudaMemsetAsync(s.red.p + 3 * RED_BLOCKS, 0, RED_BLOCKS * sizeof(double), s.stream));
+  reduce_fixed_multi(s.stream, s.red.p, RED_BLOCKS, 4, s.w.scal.p);
+  CK(cudaMemcpyAsync(s.h_pinned, s.w.scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  int* he = reinterpret_cast<int*>(s.h_pinned + 8);
+  CK(cudaMemcpyAsync(he, s.w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  if (he[0]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
+                                                 "(intersection reached; CCD filtering must prevent this)");
+  for (int k = 0; k < 4; ++k) out[k] = s.h_pinned[k];
+}
+
 double contact_energy(Scene& s, const double* q, double kappa, double dh) {
-  DVec<int> err;
-  err.resize(1);
-  err.zero(s.stream);
-  s.red.resize(2 * RED_BLOCKS);
-  launch_contact_energy(s, KIND_VF, q, kappa, dh, s.red.p, err.p);
-  launch_contact_energy(s, KIND_EE, q, kappa, dh, s.red.p + RED_BLOCKS, err.p);
-  check_err_flag(s, err, ABD_ERR_BARRIER_DOMAIN,
-                 "barrier evaluated at non-positive squared distance (intersection reached)");
-  double vf = reduce_sum_det(s, s.red.p, RED_BLOCKS);
-  double ee = reduce_sum_det(s, s.red.p + RED_BLOCKS, RED_BLOCKS);
-  return (0.0 + vf) + ee;
+  double e[4];
+  int64_t nf = s.fric.n;
+  s.fric.n = 0;  // contact only
+  try {
+    energy_terms(s, q, q, 1.0, kappa, dh, 0.0, e);
+  } catch (...) {
+    s.fric.n = nf;
+    throw;
+  }
+  s.fric.n = nf;
+  return (0.0 + e[1]) + e[2];
 }
 
 double friction_energy(Scene& s, const double* q, double dt, double eps_v) {
@@ -224,52 +244,58 @@ double body_energy(Scene& s, const double* q, const double* qt, double dt) {
   return reduce_sum_det(s, s.red.p, RED_BLOCKS);
 }
 
+// ip_value (solver.py:193-205): ((sum_b body_b) + ((0 + E_vf) + E_ee)) + E_f
 double ip_value(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v) {
-  double e = body_energy(s, q, qt, dt);
-  e += contact_energy(s, q, kappa, dh);
-  e += friction_energy(s, q, dt, eps_v);
-  return e;
+  double e[4];
+  energy_terms(s, q, qt, dt, kappa, dh, eps_v, e);
+  double total = e[0];
+  total += (0.0 + e[1]) + e[2];
+  total += e[3];
+  return total;
 }
 
 double step_filter(Scene& s, const double* q, const double* dq, double slack) {
-  DVec<unsigned long long> tmin;
-  DVec<int> err;
-  tmin.resize(1);
-  err.resize(1);
-  err.zero(s.stream);
-  unsigned long long one = (unsigned long long)__builtin_bit_cast(long long, 1.0);
-  CK(cudaMemcpyAsync(tmin.p, &one, sizeof(one), cudaMemcpyHostToDevice, s.stream));
-  launch_ccd(s, KIND_VF, q, dq, slack, tmin.p, err.p);
-  launch_ccd(s, KIND_EE, q, dq, slack, tmin.p, err.p);
-  unsigned long long h = 0;
-  CK(cudaMemcpyAsync(&h, tmin.p, sizeof(h), cudaMemcpyDeviceToHost, s.stream));
-  check_err_flag(s, err, ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
-  return std::fmin(1.0, __builtin_bit_cast(double, h));
+  unsigned long long* tmin = s.w.ull.p;
+  s.w.err.resize(2);
+  s.w.err.zero(s.stream);
+  unsigned long long one = d_to_bits(1.0);
+  CK(cudaMemcpyAsync(tmin, &one, sizeof(one), cudaMemcpyHostToDevice, s.stream));
+  EventTimer tm(s, 2);
+  launch_ccd(s, KIND_VF, q, dq, slack, tmin, s.w.err.p);
+  launch_ccd(s, KIND_EE, q, dq, slack, tmin, s.w.err.p);
+  tm.stop();
+  unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
+  CK(cudaMemcpyAsync(hb, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
+  int* he = reinterpret_cast<int*>(s.h_pinned + 2);
+  CK(cudaMemcpyAsync(he, s.w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  if (he[0]) throw Error(ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
+  int64_t nq = s.cands.n_vf + s.cands.n_ee;
+  tm.done(nq, 112.0 * (double)nq + 192.0 * s.B);
+  return std::fmin(1.0, bits_to_d(hb[0]));
 }
 
 double candidate_min_d2(Scene& s, const double* q) {
-  DVec<unsigned long long> best;
-  best.resize(1);
-  unsigned long long inf = (unsigned long long)__builtin_bit_cast(long long, (double)INFINITY);
-  CK(cudaMemcpyAsync(best.p, &inf, sizeof(inf), cudaMemcpyHostToDevice, s.stream));
-  launch_cand_min_d2(s, KIND_VF, q, best.p);
-  launch_cand_min_d2(s, KIND_EE, q, best.p);
-  unsigned long long h = 0;
-  CK(cudaMemcpyAsync(&h, best.p, sizeof(h), cudaMemcpyDeviceToHost, s.stream));
+  unsigned long long* best = s.w.ull.p + 1;
+  unsigned long long inf = d_to_bits(INFINITY);
+  CK(cudaMemcpyAsync(best, &inf, sizeof(inf), cudaMemcpyHostToDevice, s.stream));
+  launch_cand_min_d2(s, KIND_VF, q, best);
+  launch_cand_min_d2(s, KIND_EE, q, best);
+  unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
+  CK(cudaMemcpyAsync(hb, best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaStreamSynchronize(s.stream));
-  return __builtin_bit_cast(double, h);
+  return bits_to_d(hb[0]);
 }
 
 void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v) {
   int n = s.n_dyn;
-  DVec<double> grad0, diag0;
-  grad0.resize(std::max(12 * n, 1));
-  diag0.resize(std::max(144 * n, 1));
-  launch_body_terms(s, q, qt, dt, grad0.p, diag0.p, nullptr, 1);
+  s.w.grad0.resize(std::max(12 * n, 1));
+  s.w.diag0.resize(std::max(144 * n, 1));
+  launch_body_terms(s, q, qt, dt, s.w.grad0.p, s.w.diag0.p, nullptr, 1);
   contact_blocks(s, q, kappa, dh, 1);
   append_friction_blocks(s, q, dt, eps_v, 1);
   build_pattern(s, s.cands.ov.p, s.cands.n_ov, s.fric.bodies.p, s.fric.n);
-  reduce_system(s, diag0.p, grad0.p);
+  reduce_system(s, s.w.diag0.p, s.w.grad0.p);
 }
 
 // ---------------------------------------------------------------------------
@@ -294,6 +320,8 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   s.dq.resize(NB);
   s.q_trial.resize(NB);
   s.dx.resize(std::max<int64_t>(ND, 1));
+  s.w.neg.resize(std::max<int64_t>(ND, 1));
+  s.red.resize(4 * RED_BLOCKS);
   CK(cudaMemcpyAsync(s.q0.p, s.q.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   launch_q_tilde(s, s.q0.p, s.q_dot.p, s.forces.p, P.dt, s.q_tilde.p);
 
@@ -302,8 +330,6 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   st.t_broad += ms(t0, clk::now());
   friction_precompute(s, s.q.p, P.kappa_barrier, P.d_hat, P.mu, nullptr);
   int64_t max_c = s.cands.n_vf + s.cands.n_ee;
-  DVec<double> neg;
-  neg.resize(std::max<int64_t>(ND, 1));
   double last_dq = 0.0;
   int n_trace = 0;
   int outer_n = std::max(1, P.friction_outer_iters);
@@ -320,26 +346,31 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       assemble(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
       st.t_assemble += ms(t0, clk::now());
       t0 = clk::now();
+      double amax = 0.0, gd = 0.0;
       if (ND) {
-        k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, neg.p);
+        k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
         note_launch("k_neg");
         double rel = 0.0;
-        int its = 0;
-        try {
-          its = pcg_solve(s, neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
-        } catch (Error& e) {
-          throw;
-        }
-        st.pcg_iters_total += its;
+        st.pcg_iters_total += pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
+        // |dx|_inf and g.dx in one pass, one sync
+        unsigned long long* am = s.w.ull.p + 2;
+        CK(cudaMemsetAsync(am, 0, sizeof(unsigned long long), stream));
+        k_absmax_dot<<<RED_BLOCKS, RED_THREADS, 0, stream>>>(ND, s.dx.p, s.grad.p, am, s.red.p);
+        note_launch("k_absmax_dot");
+        s.w.scal.resize(4);
+        reduce_fixed_stream(stream, s.red.p, RED_BLOCKS, s.w.scal.p);
+        CK(cudaMemcpyAsync(s.h_pinned, am, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(s.h_pinned + 1, s.w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        amax = bits_to_d(*reinterpret_cast<unsigned long long*>(s.h_pinned));
+        gd = s.h_pinned[1];
       }
       st.t_solve += ms(t0, clk::now());
-      double amax = ND ? absmax(s, s.dx.p, ND) : 0.0;
       last_dq = amax / P.dt;
       if (ND == 0 || amax / P.dt < P.newton_tol) {
         converged = true;
         break;
       }
-      double gd = dot_det(s, s.grad.p, s.dx.p, ND);
       double sign = 1.0;
       const double* dsrc = s.dx.p;
       if (gd >= 0.0) {
@@ -350,9 +381,9 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       s.dq.zero(stream);
       k_expand_dq<<<grid_for(ND, 256), 256, 0, stream>>>(s.n_dyn, s.dyn_body.p, dsrc, sign, s.dq.p);
       note_launch("k_expand_dq");
-      // candidates over the proposed interval
+      // candidates over the proposed interval [q, q + dq]
       t0 = clk::now();
-      launch_axpy_q(s, s.q.p, 1.0, s.dq.p, s.q_trial.p, NB);  // q + dq (alpha = 1: exact add)
+      launch_axpy_q(s, s.q.p, 1.0, s.dq.p, s.q_trial.p, NB);  // q + dq (exact add)
       broad_phase(s, s.q.p, s.q_trial.p, P.d_hat);
       st.t_broad += ms(t0, clk::now());
       max_c = std::max<int64_t>(max_c, s.cands.n_vf + s.cands.n_ee);
@@ -369,9 +400,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         e = ip_value(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
         if (e < e0) break;
         alpha *= 0.5;
-        if (alpha < 1e-12) {
-          throw Error(ABD_ERR_STEP_FAILURE, "line search underflow (no descent below alpha = 1e-12)");
-        }
+        if (alpha < 1e-12) throw Error(ABD_ERR_STEP_FAILURE, "line search underflow (no descent below alpha = 1e-12)");
       }
       CK(cudaMemcpyAsync(s.q.p, s.q_trial.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
       st.t_line_search += ms(tls, clk::now());
@@ -383,7 +412,6 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   }
   st.last_dq_over_dt = last_dq;
   st.candidates = max_c;
-  // q_dot
   k_qdot<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.dyn.p, s.q.p, s.q0.p, P.dt, s.q_dot.p);
   note_launch("k_qdot");
   // stats (solver.py:604-627)
@@ -395,17 +423,16 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   }
   st.ip_value = ip_value(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
   {
-    DVec<unsigned long long> m;
-    m.resize(1);
-    m.zero(stream);
+    unsigned long long* m = s.w.ull.p + 3;
+    CK(cudaMemsetAsync(m, 0, sizeof(unsigned long long), stream));
     if (s.n_dyn) {
-      k_ortho_err<<<grid_for(s.n_dyn, 256), 256, 0, stream>>>(s.n_dyn, s.dyn_body.p, s.q.p, m.p);
+      k_ortho_err<<<grid_for(s.n_dyn, 256), 256, 0, stream>>>(s.n_dyn, s.dyn_body.p, s.q.p, m);
       note_launch("k_ortho_err");
     }
-    unsigned long long h = 0;
-    CK(cudaMemcpyAsync(&h, m.p, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
+    CK(cudaMemcpyAsync(hb, m, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    st.max_ortho_error = __builtin_bit_cast(double, h);
+    st.max_ortho_error = bits_to_d(hb[0]);
   }
   st.t_total = ms(t_start, clk::now());
 }

@@ -89,7 +89,8 @@ __global__ void k_ortho(int64_t n, const double* __restrict__ q, const double* _
   for (int c = 0; c < 12; ++c) qq[c] = q[12 * i + c];
   e[i] = ortho_energy_dev(qq, k[i]);
   ortho_derivs_dev(qq, k[i], gg, H);
-  if (project) psd_project_jacobi<12>(H + 3 * 12 + 3, V, 9);
+  (void)V;
+  if (project) ortho_project_closed(qq, k[i], H);
   for (int c = 0; c < 12; ++c) g[12 * i + c] = gg[c];
   for (int c = 0; c < 144; ++c) h[144 * i + c] = H[c];
 }

@@ -247,9 +247,9 @@ __global__ void k_body_terms(int n_dyn, const int* __restrict__ dyn_body, const 
     double k = stiff[b];
     acc += 0.5 * quad + dt2 * ortho_energy_dev(qq, k);
     if (!want) continue;
-    double g[12], H[144], V[144];
+    double g[12], H[144];
     ortho_derivs_dev(qq, k, g, H);
-    psd_project_jacobi<12>(H + 3 * 12 + 3, V, 9);
+    ortho_project_closed(qq, k, H);  // closed-form eigen-clamp via the 3x3 SVD of A
     for (int c = 0; c < 12; ++c) grad0[12 * (int64_t)s + c] = Md[c] + dt2 * g[c];
     for (int c = 0; c < 144; ++c) diag0[144 * (int64_t)s + c] = M[c] + dt2 * H[c];
   }

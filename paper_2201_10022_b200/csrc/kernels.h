@@ -8,6 +8,7 @@ namespace abd {
 void note_launch(const char* name);
 void reduce_fixed_device(Scene& s, const double* partials, int n, double* out_dev);
 void reduce_fixed_stream(cudaStream_t st, const double* partials, int n, double* out_dev);
+void reduce_fixed_multi(cudaStream_t st, const double* partials, int n, int count, double* out_dev);
 
 // plain-data view of the scene geometry passed to kernels by value
 struct SceneView {

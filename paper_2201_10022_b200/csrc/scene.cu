@@ -35,11 +35,18 @@ Scene::Scene() {
   CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   CK(cudaMallocHost(&h_pinned, 64 * sizeof(double)));
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventCreate(&tev0));
+  CK(cudaEventCreate(&tev1));
+  w.ull.resize(16);
 }
 
 Scene::~Scene() {
   if (stream) cudaStreamDestroy(stream);
   if (h_pinned) cudaFreeHost(h_pinned);
+  for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
+    if (e) cudaEventDestroy(e);
 }
 
 void scan_exclusive_i32(Scene& s, const int* in, int* out, int64_t n) {
@@ -63,9 +70,24 @@ void sort_pairs_u64(Scene& s, uint64_t* keys, uint64_t* keys_alt, int* vals, int
   result_in_alt = (k.Current() == keys_alt);
 }
 
+void sort_pairs_u32(Scene& s, uint32_t* keys, uint32_t* keys_alt, int* vals, int* vals_alt, int64_t n, int end_bit,
+                    bool& result_in_alt) {
+  result_in_alt = false;
+  if (n <= 1) return;
+  cub::DoubleBuffer<uint32_t> k(keys, keys_alt);
+  cub::DoubleBuffer<int> v(vals, vals_alt);
+  size_t bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k, v, (int)n, 0, end_bit, s.stream));
+  s.tmp_bytes.resize(bytes);
+  CK(cub::DeviceRadixSort::SortPairs(s.tmp_bytes.p, bytes, k, v, (int)n, 0, end_bit, s.stream));
+  result_in_alt = (k.Current() == keys_alt);
+}
+
 // fixed-order tree reduction of a partials array (one CTA, deterministic)
 __global__ void k_reduce_fixed(const double* __restrict__ in, int n, double* __restrict__ out) {
   __shared__ double sh[1024];
+  in += (int64_t)blockIdx.x * n;  // one CTA per partials array
+  out += blockIdx.x;
   double acc = 0.0;
   // each thread sums a contiguous strided slice in index order
   for (int i = threadIdx.x; i < n; i += blockDim.x) acc += in[i];
@@ -89,6 +111,12 @@ void reduce_fixed_stream(cudaStream_t st, const double* partials, int n, double*
 
 void reduce_fixed_device(Scene& s, const double* partials, int n, double* out_dev) {
   reduce_fixed_stream(s.stream, partials, n, out_dev);
+}
+
+// `count` consecutive partial arrays of length n -> count sums (deterministic)
+void reduce_fixed_multi(cudaStream_t st, const double* partials, int n, int count, double* out_dev) {
+  k_reduce_fixed<<<count, 1024, 0, st>>>(partials, n, out_dev);
+  note_launch("k_reduce_fixed");
 }
 
 double reduce_sum_det(Scene& s, const double* partials, int n) {

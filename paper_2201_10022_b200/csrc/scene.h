@@ -139,6 +139,26 @@ struct Scene {
   DVec<double> vbox;  // V * 6 vertex boxes (broad phase)
   DVec<double> bbox;  // B * 6 body boxes
 
+  // persistent workspaces (grown, never shrunk: no cudaMalloc in steady state)
+  struct Work {
+    DVec<int> flags, pos, err, order, cnt, off, seg_s, seg_e, row_of, nsel, bad, iters;
+    DVec<uint64_t> k0, k1, e0, e1;
+    DVec<uint32_t> ka, kb;
+    DVec<int> va, vb;
+    DVec<int4> rows_tmp;
+    DVec<int2> pairs_tmp;
+    DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
+    DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
+  } w;
+
+  // per-kernel instrumentation (CUDA events on `stream`)
+  struct KStat {
+    int64_t launches = 0, units = 0;
+    double ms = 0.0, bytes = 0.0;
+  } kstat[4];
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
+  bool instrument = true;
+
   Scene();
   ~Scene();
 };
@@ -148,6 +168,8 @@ struct Scene {
 void scan_exclusive_i32(Scene& s, const int* in, int* out, int64_t n);
 void sort_pairs_u64(Scene& s, uint64_t* keys, uint64_t* keys_alt, int* vals, int* vals_alt, int64_t n,
                     int end_bit, bool& result_in_alt);
+void sort_pairs_u32(Scene& s, uint32_t* keys, uint32_t* keys_alt, int* vals, int* vals_alt, int64_t n, int end_bit,
+                    bool& result_in_alt);
 double reduce_sum_det(Scene& s, const double* partials, int n);  // deterministic
 
 inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
