@@ -1,31 +1,12 @@
-// K4: block-Jacobi PCG on the resident symmetric BSR (replaces the reference's
-// BlockCholesky.solve_refined, sparse.py:90-161, to the same ||Ax-b|| <=
-// rel_tol ||b|| contract).
-//
-// One persistent cooperative launch per solve.  Each CTA owns whole block
-// rows (16 block rows x 12 scalar rows = 192 threads), so the 12x12
-// block-Jacobi apply needs only __syncthreads, and an iteration costs two
-// grid-wide reductions:
-//   phase A: p_new = z + beta p_old fused into the SpMV gather (double-
-//            buffered p), Ap = A p_new, partial p_new.Ap        -> grid sync
-//   phase B: x += alpha p, r -= alpha Ap, z = P^-1 r,
-//            partials r.z and r.r                              -> grid sync
-// Dot products are reduced in a fixed order by every CTA (deterministic).
-// On convergence of the recursive residual the true residual b - A x is
-// checked and CG restarts from x if it fails.
-#include <cooperative_groups.h>
-
+// Block-Jacobi preconditioner setup for K4 (the PCG itself is k_cg.cu), the
+// standalone BSR SpMV (BlockSparseMatrix.matvec, sparse.py:77-84) and the
+// stateless BSR loader used by the sparse.py drop-in.
 #include <algorithm>
 #include <vector>
 
 #include "driver.h"
 
-namespace cg = cooperative_groups;
-
 namespace abd {
-
-constexpr int PCG_ROWS = 16;               // block rows per CTA
-constexpr int PCG_THREADS = PCG_ROWS * 12;  // 192
 
 // block-Jacobi preconditioner: inverse of each 12x12 diagonal block.  16 lanes
 // per block (two blocks per warp): right-looking Cholesky with lane t owning
@@ -85,357 +66,10 @@ __global__ void __launch_bounds__(128) k_jacobi_inv(int n, const int* __restrict
   for (int i = 0; i < 12; ++i) P[i * 12 + t] = y[i];
 }
 
-struct PcgArgs {
-  int n;
-  const int* row_ptr;
-  const int* col;
-  const double* val;
-  const double* pinv;
-  const int* bad;
-  const double* b;
-  double* x;
-  double* r;
-  double* z;
-  double* pa;
-  double* pb;
-  double* Ap;
-  double* part;  // 4 * gridDim.x: two alternating (A | B) banks of 2 values per CTA
-  double rel_tol;
-  int max_iters;
-  int* out_iters;
-  double* out_rel;
-};
 
-__device__ __forceinline__ double cta_sum(double v, double* sh) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh[wid] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < PCG_THREADS / 32; ++w) t += sh[w];
-  return t;
-}
-
-// every CTA reduces the per-CTA partials in the same fixed order
-__device__ __forceinline__ double grid_total(const double* part, int which, double* sh) {
-  double v = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += part[2 * i + which];
-  return cta_sum(v, sh);
-}
-
-__device__ __forceinline__ void cta_sum2(double& a, double& b, double* sh) {
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xffffffffu, a, o);
-    b += __shfl_xor_sync(0xffffffffu, b, o);
-  }
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) {
-    sh[wid] = a;
-    sh[8 + wid] = b;
-  }
-  __syncthreads();
-  double ta = 0.0, tb = 0.0;
-#pragma unroll
-  for (int w = 0; w < PCG_THREADS / 32; ++w) {
-    ta += sh[w];
-    tb += sh[8 + w];
-  }
-  a = ta;
-  b = tb;
-}
-
-__device__ __forceinline__ void grid_total2(const double* part, double& a, double& b, double* sh) {
-  double va = 0.0, vb = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
-    va += part[2 * i];
-    vb += part[2 * i + 1];
-  }
-  cta_sum2(va, vb, sh);
-  a = va;
-  b = vb;
-}
-
-// row (br, rr) of A (z + beta p_old); beta == 0 reads only z
-__device__ __forceinline__ double spmv_fused(const PcgArgs& a, int br, int rr, const double* __restrict__ zv,
-                                             const double* __restrict__ po, double beta) {
-  double acc = 0.0;
-  int k1 = a.row_ptr[br + 1];
-  for (int k = a.row_ptr[br]; k < k1; ++k) {
-    const double2* blk = reinterpret_cast<const double2*>(a.val + 144 * (int64_t)k + 12 * rr);
-    int c = a.col[k];
-    const double* zc = zv + 12 * (int64_t)c;
-    const double* pc = po + 12 * (int64_t)c;
-#pragma unroll
-    for (int h = 0; h < 6; ++h) {
-      double2 m = __ldg(blk + h);
-      acc += m.x * (zc[2 * h] + beta * pc[2 * h]) + m.y * (zc[2 * h + 1] + beta * pc[2 * h + 1]);
-    }
-  }
-  return acc;
-}
-
-__device__ __forceinline__ double spmv_plain(const PcgArgs& a, int br, int rr, const double* __restrict__ xv) {
-  double acc = 0.0;
-  int k1 = a.row_ptr[br + 1];
-  for (int k = a.row_ptr[br]; k < k1; ++k) {
-    const double2* blk = reinterpret_cast<const double2*>(a.val + 144 * (int64_t)k + 12 * rr);
-    const double* xc = xv + 12 * (int64_t)a.col[k];
-#pragma unroll
-    for (int h = 0; h < 6; ++h) {
-      double2 m = __ldg(blk + h);
-      acc += m.x * xc[2 * h] + m.y * xc[2 * h + 1];
-    }
-  }
-  return acc;
-}
-
-__device__ __forceinline__ double prec_row(const PcgArgs& a, int br, int rr, const double* __restrict__ r) {
-  const double2* P = reinterpret_cast<const double2*>(a.pinv + 144 * (int64_t)br + 12 * rr);
-  const double* rv = r + 12 * (int64_t)br;
-  double acc = 0.0;
-#pragma unroll
-  for (int h = 0; h < 6; ++h) {
-    double2 m = __ldg(P + h);
-    acc += m.x * rv[2 * h] + m.y * rv[2 * h + 1];
-  }
-  return acc;
-}
-
-__global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double sh[16];
-  if (*a.bad != 0x7fffffff) return;  // non-SPD preconditioner block: host raises
-  const int lb = threadIdx.x / 12, rr = threadIdx.x % 12;
-  const int groups = (a.n + PCG_ROWS - 1) / PCG_ROWS;
-  // x = 0, r = b, p = 0
-  double bb = 0.0;
-  for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-    int br = g * PCG_ROWS + lb;
-    if (br >= a.n) continue;
-    int64_t t = 12 * (int64_t)br + rr;
-    a.x[t] = 0.0;
-    double bt = a.b[t];
-    a.r[t] = bt;
-    a.pa[t] = 0.0;
-    bb += bt * bt;
-  }
-  double dummy = 0.0;
-  cta_sum2(bb, dummy, sh);
-  double* partA = a.part;
-  double* partB = a.part + 2 * gridDim.x;
-  if (threadIdx.x == 0) {
-    partA[2 * blockIdx.x] = bb;
-    partA[2 * blockIdx.x + 1] = 0.0;
-  }
-  grid.sync();
-  double bn2, d2_;
-  grid_total2(partA, bn2, d2_, sh);
-  const double bnorm = sqrt(bn2);
-  if (bnorm == 0.0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      *a.out_iters = 0;
-      *a.out_rel = 0.0;
-    }
-    return;
-  }
-  const double tol = a.rel_tol * bnorm;
-  double* po = a.pa;
-  double* pn = a.pb;
-  int it = 0;
-  double rel = 1.0;
-  for (int restart = 0; restart < 4; ++restart) {
-    // z = P^-1 r (CTA-local block rows), rz
-    double rz = 0.0;
-    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-      int br = g * PCG_ROWS + lb;
-      if (br >= a.n) continue;
-      int64_t t = 12 * (int64_t)br + rr;
-      double zt = prec_row(a, br, rr, a.r);
-      a.z[t] = zt;
-      rz += a.r[t] * zt;
-    }
-    double rr0 = 0.0;
-    cta_sum2(rz, rr0, sh);
-    if (threadIdx.x == 0) {
-      partB[2 * blockIdx.x] = rz;
-      partB[2 * blockIdx.x + 1] = 0.0;
-    }
-    grid.sync();
-    grid_total2(partB, rz, rr0, sh);
-    double beta = 0.0;
-    bool conv = false;
-    while (it < a.max_iters) {
-      // phase A: p_new = z + beta p_old ; Ap = A p_new
-      double pap = 0.0;
-      for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-        int br = g * PCG_ROWS + lb;
-        if (br >= a.n) continue;
-        int64_t t = 12 * (int64_t)br + rr;
-        double v = spmv_fused(a, br, rr, a.z, po, beta);
-        double pt = a.z[t] + beta * po[t];
-        pn[t] = pt;
-        a.Ap[t] = v;
-        pap += pt * v;
-      }
-      double zero = 0.0;
-      cta_sum2(pap, zero, sh);
-      if (threadIdx.x == 0) {
-        partA[2 * blockIdx.x] = pap;
-        partA[2 * blockIdx.x + 1] = 0.0;
-      }
-      grid.sync();
-      grid_total2(partA, pap, zero, sh);
-      double alpha = rz / pap;
-      // phase B
-      double rzn = 0.0, rrn = 0.0;
-      for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-        int br = g * PCG_ROWS + lb;
-        bool live = br < a.n;
-        int64_t t = 12 * (int64_t)br + rr;
-        if (live) {
-          a.x[t] += alpha * pn[t];
-          double rt = a.r[t] - alpha * a.Ap[t];
-          a.r[t] = rt;
-          rrn += rt * rt;
-        }
-        __syncthreads();  // whole block row of r written (same CTA)
-        if (live) {
-          double zt = prec_row(a, br, rr, a.r);
-          a.z[t] = zt;
-          rzn += a.r[t] * zt;
-        }
-      }
-      cta_sum2(rzn, rrn, sh);
-      if (threadIdx.x == 0) {
-        partB[2 * blockIdx.x] = rzn;
-        partB[2 * blockIdx.x + 1] = rrn;
-      }
-      grid.sync();
-      grid_total2(partB, rzn, rrn, sh);
-      ++it;
-      double rn = sqrt(rrn);
-      rel = rn / bnorm;
-      double* tmp = po;
-      po = pn;
-      pn = tmp;
-      if (rn <= tol || !(pap > 0.0)) {
-        conv = rn <= tol;
-        break;
-      }
-      beta = rzn / rz;
-      rz = rzn;
-    }
-    // true residual r = b - A x
-    grid.sync();
-    double tr = 0.0;
-    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-      int br = g * PCG_ROWS + lb;
-      if (br >= a.n) continue;
-      int64_t t = 12 * (int64_t)br + rr;
-      double v = a.b[t] - spmv_plain(a, br, rr, a.x);
-      a.r[t] = v;
-      tr += v * v;
-    }
-    double z0 = 0.0;
-    cta_sum2(tr, z0, sh);
-    if (threadIdx.x == 0) {
-      partA[2 * blockIdx.x] = tr;
-      partA[2 * blockIdx.x + 1] = 0.0;
-    }
-    grid.sync();
-    grid_total2(partA, tr, z0, sh);
-    rel = sqrt(tr) / bnorm;
-    (void)conv;
-    if (sqrt(tr) <= tol || it >= a.max_iters) break;
-    // restart: reset p
-    for (int g = blockIdx.x; g < groups; g += gridDim.x) {
-      int br = g * PCG_ROWS + lb;
-      if (br >= a.n) continue;
-      po[12 * (int64_t)br + rr] = 0.0;
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *a.out_iters = it;
-    *a.out_rel = rel;
-  }
-}
-
-// solve H x = rhs on the resident BSR; returns iterations, rel residual
-int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_iters, double& rel_res) {
-  Bsr& H = s.H;
-  cudaStream_t st = s.stream;
-  int n = H.n;
-  if (n == 0) {
-    rel_res = 0.0;
-    return 0;
-  }
-  int64_t N = 12 * (int64_t)n;
-  Scene::Work& w = s.w;
-  w.pinv.resize(144 * (int64_t)n);
-  w.r.resize(N);
-  w.z.resize(N);
-  w.p.resize(N);
-  w.p2.resize(N);
-  w.Ap.resize(N);
-  w.bad.resize(1);
-  w.iters.resize(1);
-  w.scal.resize(4);
-  int big = 0x7fffffff;
-  CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-  k_jacobi_inv<<<grid_for(n, JI_BLOCKS), 128, 0, st>>>(n, H.diag_pos.p, H.val.p, w.pinv.p, w.bad.p);
+void launch_jacobi_inv(Scene& s, int n, const int* diag_pos, const double* val, double* pinv, int* bad) {
+  k_jacobi_inv<<<grid_for(n, JI_BLOCKS), 128, 0, s.stream>>>(n, diag_pos, val, pinv, bad);
   note_launch("k_jacobi_inv");
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_pcg, PCG_THREADS, 0));
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  int groups = (n + PCG_ROWS - 1) / PCG_ROWS;
-  int grid = std::max(1, std::min(groups, blocks_per_sm * s.num_sms));
-  w.part.resize(4 * (int64_t)grid);
-  PcgArgs a;
-  a.n = n;
-  a.row_ptr = H.row_ptr.p;
-  a.col = H.col.p;
-  a.val = H.val.p;
-  a.pinv = w.pinv.p;
-  a.bad = w.bad.p;
-  a.b = rhs;
-  a.x = x;
-  a.r = w.r.p;
-  a.z = w.z.p;
-  a.pa = w.p.p;
-  a.pb = w.p2.p;
-  a.Ap = w.Ap.p;
-  a.part = w.part.p;
-  a.rel_tol = rel_tol;
-  a.max_iters = max_iters;
-  a.out_iters = w.iters.p;
-  a.out_rel = w.scal.p;
-  void* args[] = {&a};
-  if (s.instrument) CK(cudaEventRecord(s.ev0, st));
-  CK(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(grid), dim3(PCG_THREADS), args, 0, st));
-  note_launch("k_pcg");
-  if (s.instrument) CK(cudaEventRecord(s.ev1, st));
-  int hit = 0, hbad = 0;
-  CK(cudaMemcpyAsync(&hit, w.iters.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&rel_res, w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&hbad, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (hbad != big) throw Error(ABD_ERR_FACTORIZATION, "non-SPD diagonal block in block-Jacobi PCG", hbad);
-  if (s.instrument) {
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
-    Scene::KStat& k = s.kstat[0];
-    k.launches += 1;
-    k.units += hit;
-    k.ms += ms;
-    // algorithmic bytes per iteration: 1152 (nnzb + n) + 13 * 96 * n
-    k.bytes += (double)hit * (1152.0 * (double)(H.nnzb + n) + 13.0 * 96.0 * n);
-  }
-  return hit;
 }
 
 // y = H x on the resident BSR (thread per scalar row)

@@ -149,6 +149,7 @@ struct Scene {
     DVec<int2> pairs_tmp;
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
+    DVec<double> cg_u, cg_w, cg_m, cg_q;
   } w;
 
   // per-kernel instrumentation (CUDA events on `stream`)
