@@ -427,6 +427,317 @@ __global__ void __launch_bounds__(RES_THREADS, 1) k_cg_res(CgArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster block-Jacobi preconditioner.  The body-coupling graph of a contact
+// step is mostly tiny connected components (isolated bodies, stacked pairs
+// and short columns; see profiles/): block-Jacobi over single bodies leaves
+// CG resolving every component's spectrum at once (~10^3 iterations).  Here
+// each connected component of <= CL_SMALL bodies becomes ONE dense block
+// (exact inverse: CG converges on it in one step) and larger components are
+// cut into BFS-contiguous clusters of <= CL_BIG bodies.  Single-body
+// clusters are exactly the 12x12 block-Jacobi of the north star.
+constexpr int CL_MAX = 8;  // rows per cluster upper bound (dense size 96)
+
+struct ClusterArgs {
+  const int* slot_row;      // G * R: block row of each CTA slot (-1 = empty)
+  const int* slot_base;     // G * R: CTA-local slot of the cluster's first row
+  const int* slot_k;        // G * R: cluster size (rows)
+  const long long* slot_off;  // G * R: offset of the cluster's (12K)^2 inverse
+  const double* minv;
+};
+
+__global__ void __launch_bounds__(RES_THREADS, 1) k_cg_cluster(CgArgs a, ClusterArgs c) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double dsm[];
+  double* vsh = dsm;                  // RES_ROWS * 12 (cluster exchange)
+  double* sh = vsh + RES_ROWS * 12;   // 256 reduction scratch
+  if (*a.bad != 0x7fffffff) return;
+  const int lb = threadIdx.x / 12, rr = threadIdx.x % 12;
+  const int slot = blockIdx.x * RES_ROWS + lb;
+  const int br = c.slot_row[slot];
+  const bool live = br >= 0;
+  const int64_t t = 12 * (int64_t)(live ? br : 0) + rr;
+  const int cbase = c.slot_base[slot];
+  const int ck = c.slot_k[slot];
+  const int dim = 12 * ck;
+  const double* Mrow = c.minv + c.slot_off[slot] + (int64_t)(12 * (lb - cbase) + rr) * dim;
+  auto prec = [&](double v) -> double {  // (M^-1 v)_row over the row's cluster
+    __syncthreads();
+    vsh[threadIdx.x] = v;
+    __syncthreads();
+    if (!live) return 0.0;
+    const double* vv = vsh + 12 * cbase;
+    double acc0 = 0.0, acc1 = 0.0;
+    int j = 0;
+    for (; j + 1 < dim; j += 2) {
+      double2 mm = __ldg(reinterpret_cast<const double2*>(Mrow + j));
+      acc0 += mm.x * vv[j];
+      acc1 += mm.y * vv[j + 1];
+    }
+    if (j < dim) acc0 += Mrow[j] * vv[j];
+    return acc0 + acc1;
+  };
+  double* bankA = a.part;
+  double* bankB = a.part + 4 * gridDim.x;
+  const double bt = live ? a.b[t] : 0.0;
+  double x = 0.0, r = bt;
+  double u = prec(r);
+  if (live) a.u[t] = u;
+  double v1[1] = {bt * bt};
+  cta_partials<1, RES_WARPS>(v1, sh, bankA);
+  grid.sync();
+  double tb[1];
+  grid_totals<1, RES_WARPS>(bankA, sh, tb);
+  const double bnorm = sqrt(tb[0]);
+  if (bnorm == 0.0) {
+    if (live) a.x[t] = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *a.out_iters = 0;
+      *a.out_rel = 0.0;
+    }
+    return;
+  }
+  const double tol = a.rel_tol * bnorm;
+  int it = 0;
+  double rel = 1.0;
+  double w = 0.0, m = 0.0, z = 0.0, q = 0.0, s = 0.0, p = 0.0;
+  for (int restart = 0; restart < 6; ++restart) {
+    w = live ? spmv_row(a, br, rr, a.u) : 0.0;
+    m = prec(w);
+    double* mc = a.m;
+    double* mn = a.m2;
+    if (live) mc[t] = m;
+    double pv[3] = {r * u, w * u, r * r};
+    cta_partials<3, RES_WARPS>(pv, sh, bankB);
+    grid.sync();
+    double* cur = bankB;
+    double* nxt = bankA;
+    double gamma_old = 0.0, alpha_old = 1.0;
+    bool first = true;
+    while (true) {
+      double tot[3];
+      grid_totals<3, RES_WARPS>(cur, sh, tot);
+      double gam = tot[0], del = tot[1], rn = sqrt(fmax(tot[2], 0.0));
+      rel = rn / bnorm;
+      if (rn <= tol) break;
+      if (it >= a.max_iters || !(gam > 0.0)) break;
+      double beta = first ? 0.0 : gam / gamma_old;
+      double denom = first ? del : del - beta * gam / alpha_old;
+      if (!(denom > 0.0)) break;
+      double alpha = gam / denom;
+      double nt = live ? spmv_row(a, br, rr, mc) : 0.0;
+      z = nt + beta * z;
+      q = m + beta * q;
+      s = w + beta * s;
+      p = u + beta * p;
+      x += alpha * p;
+      r -= alpha * s;
+      u -= alpha * q;
+      w -= alpha * z;
+      m = prec(w);
+      if (live) mn[t] = m;
+      double pv2[3] = {r * u, w * u, r * r};
+      cta_partials<3, RES_WARPS>(pv2, sh, nxt);
+      grid.sync();
+      ++it;
+      gamma_old = gam;
+      alpha_old = alpha;
+      first = false;
+      double* tmp = cur;
+      cur = nxt;
+      nxt = tmp;
+      tmp = mc;
+      mc = mn;
+      mn = tmp;
+    }
+    if (live) a.x[t] = x;
+    grid.sync();
+    r = live ? bt - spmv_row(a, br, rr, a.x) : 0.0;
+    u = prec(r);
+    if (live) a.u[t] = u;
+    double tv[1] = {r * r};
+    cta_partials<1, RES_WARPS>(tv, sh, bankA);
+    grid.sync();
+    double tt[1];
+    grid_totals<1, RES_WARPS>(bankA, sh, tt);
+    rel = sqrt(tt[0]) / bnorm;
+    if (sqrt(tt[0]) <= tol || it >= a.max_iters) break;
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.out_iters = it;
+    *a.out_rel = rel;
+  }
+}
+
+// dense inverse of each cluster's diagonal block (one CTA of 96 threads per
+// cluster): gather the cluster's BSR blocks, Cholesky with lane i owning row i,
+// then lane j solves column j of the inverse.
+__global__ void __launch_bounds__(96) k_cluster_inv(int ncl, const int* __restrict__ cl_off,
+                                                    const int* __restrict__ cl_rows,
+                                                    const long long* __restrict__ cl_minv, const int* __restrict__ row_ptr,
+                                                    const int* __restrict__ col, const double* __restrict__ val,
+                                                    double* minv, int* bad) {
+  extern __shared__ double Ls[];  // dim x (dim + 1)
+  const int cidx = blockIdx.x;
+  if (cidx >= ncl) return;
+  const int r0 = cl_off[cidx], K = cl_off[cidx + 1] - r0;
+  const int dim = 12 * K, ld = dim + 1;
+  for (int e = threadIdx.x; e < dim * ld; e += blockDim.x) Ls[e] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < K; ++i) {
+    int row = cl_rows[r0 + i];
+    for (int k = row_ptr[row]; k < row_ptr[row + 1]; ++k) {
+      int cc = col[k], j = -1;
+      for (int q = 0; q < K; ++q)
+        if (cl_rows[r0 + q] == cc) j = q;
+      if (j < 0) continue;
+      for (int e = threadIdx.x; e < 144; e += blockDim.x)
+        Ls[(12 * i + e / 12) * ld + 12 * j + e % 12] = val[144 * (int64_t)k + e];
+    }
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  bool ok = true;
+  for (int j = 0; j < dim; ++j) {
+    double d = Ls[j * ld + j];
+    ok = ok && (d > 0.0);
+    double sd = sqrt(fmax(d, 1e-300));
+    __syncthreads();
+    if (tid > j && tid < dim) Ls[tid * ld + j] /= sd;
+    if (tid == j) Ls[j * ld + j] = sd;
+    __syncthreads();
+    if (tid > j && tid < dim) {
+      double ltj = Ls[tid * ld + j];
+      for (int k = j + 1; k <= tid; ++k) Ls[tid * ld + k] -= ltj * Ls[k * ld + j];
+    }
+    __syncthreads();
+  }
+  if (!ok) {
+    if (tid == 0) atomicMin(bad, cl_rows[r0]);
+    return;
+  }
+  if (tid >= dim) return;
+  // column tid of L^-T L^-1, written row-major (symmetric)
+  double* out = minv + cl_minv[cidx];
+  double y[96];
+  for (int i = 0; i < dim; ++i) {
+    double v = (i == tid) ? 1.0 : 0.0;
+    for (int k = 0; k < i; ++k) v -= Ls[i * ld + k] * y[k];
+    y[i] = v / Ls[i * ld + i];
+  }
+  for (int i = dim - 1; i >= 0; --i) {
+    double v = y[i];
+    for (int k = i + 1; k < dim; ++k) v -= Ls[k * ld + i] * y[k];
+    y[i] = v / Ls[i * ld + i];
+  }
+  for (int i = 0; i < dim; ++i) out[(int64_t)i * dim + tid] = y[i];
+}
+
+// host: components + clusters + CTA packing for the resident BSR; returns the
+// number of CTAs (0 if the packing does not fit one cooperative wave)
+static int build_clusters(Scene& s, int max_ctas, int ksmall, int kbig, int& ncl, int64_t& minv_total) {
+  Bsr& H = s.H;
+  int n = H.n;
+  cudaStream_t st = s.stream;
+  std::vector<int2> keys(H.n_off);
+  H.upper_keys.download(keys.data(), H.n_off, st);
+  CK(cudaStreamSynchronize(st));
+  std::vector<int> deg(n + 1, 0);
+  for (auto& k : keys) {
+    deg[k.x]++;
+    deg[k.y]++;
+  }
+  std::vector<int> adj_off(n + 1, 0);
+  for (int i = 0; i < n; ++i) adj_off[i + 1] = adj_off[i] + deg[i];
+  std::vector<int> adj(adj_off[n]), fill(adj_off.begin(), adj_off.end() - 1);
+  for (auto& k : keys) {
+    adj[fill[k.x]++] = k.y;
+    adj[fill[k.y]++] = k.x;
+  }
+  std::vector<int> seen(n, 0), comp, clust_off{0}, clust_rows;
+  clust_rows.reserve(n);
+  std::vector<int> queue;
+  for (int s0 = 0; s0 < n; ++s0) {
+    if (seen[s0]) continue;
+    comp.clear();
+    queue.clear();
+    queue.push_back(s0);
+    seen[s0] = 1;
+    for (size_t h = 0; h < queue.size(); ++h) {
+      int v = queue[h];
+      comp.push_back(v);
+      for (int e = adj_off[v]; e < adj_off[v + 1]; ++e)
+        if (!seen[adj[e]]) {
+          seen[adj[e]] = 1;
+          queue.push_back(adj[e]);
+        }
+    }
+    int kk = (int)comp.size() <= ksmall ? (int)comp.size() : kbig;  // BFS-contiguous chunks
+    for (size_t b = 0; b < comp.size(); b += kk) {
+      size_t e = std::min(comp.size(), b + kk);
+      std::vector<int> chunk(comp.begin() + b, comp.begin() + e);
+      std::sort(chunk.begin(), chunk.end());
+      clust_rows.insert(clust_rows.end(), chunk.begin(), chunk.end());
+      clust_off.push_back((int)clust_rows.size());
+    }
+  }
+  ncl = (int)clust_off.size() - 1;
+  // pack clusters into CTAs of RES_ROWS slots, round-robin for load balance
+  int G = std::max(1, (n + RES_ROWS - 1) / RES_ROWS);
+  std::vector<int> used;
+  std::vector<int> cl_cta(ncl), cl_slot(ncl);
+  for (;;) {
+    if (G > max_ctas) return 0;
+    used.assign(G, 0);
+    bool fit = true;
+    int cur = 0;
+    for (int ci = 0; ci < ncl && fit; ++ci) {
+      int K = clust_off[ci + 1] - clust_off[ci];
+      int tries = 0;
+      while (used[cur] + K > RES_ROWS && tries < G) {
+        cur = (cur + 1) % G;
+        ++tries;
+      }
+      if (used[cur] + K > RES_ROWS) {
+        fit = false;
+        break;
+      }
+      cl_cta[ci] = cur;
+      cl_slot[ci] = used[cur];
+      used[cur] += K;
+      cur = (cur + 1) % G;
+    }
+    if (fit) break;
+    ++G;
+  }
+  std::vector<int> slot_row(G * RES_ROWS, -1), slot_base(G * RES_ROWS, 0), slot_k(G * RES_ROWS, 1);
+  std::vector<long long> slot_off(G * RES_ROWS, 0), cl_minv(ncl);
+  long long off = 0;
+  for (int ci = 0; ci < ncl; ++ci) {
+    int K = clust_off[ci + 1] - clust_off[ci];
+    cl_minv[ci] = off;
+    for (int q = 0; q < K; ++q) {
+      int sl = cl_cta[ci] * RES_ROWS + cl_slot[ci] + q;
+      slot_row[sl] = clust_rows[clust_off[ci] + q];
+      slot_base[sl] = cl_slot[ci];
+      slot_k[sl] = K;
+      slot_off[sl] = off;
+    }
+    off += (long long)(12 * K) * (12 * K);
+  }
+  minv_total = off;
+  Scene::Work& w = s.w;
+  w.cl_slot_row.upload(slot_row.data(), slot_row.size(), st);
+  w.cl_slot_base.upload(slot_base.data(), slot_base.size(), st);
+  w.cl_slot_k.upload(slot_k.data(), slot_k.size(), st);
+  w.cl_slot_off.upload(slot_off.data(), slot_off.size(), st);
+  w.cl_off.upload(clust_off.data(), clust_off.size(), st);
+  w.cl_rows.upload(clust_rows.data(), clust_rows.size(), st);
+  w.cl_minv.upload(cl_minv.data(), cl_minv.size(), st);
+  return G;
+}
+
 void launch_jacobi_inv(Scene& s, int n, const int* diag_pos, const double* val, double* pinv, int* bad);
 
 // solve H x = rhs on the resident BSR; returns iterations, rel residual
@@ -501,7 +812,32 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
   a.out_rel = w.scal.p;
   void* args[] = {&a};
   if (s.instrument) CK(cudaEventRecord(s.ev0, st));
-  if (use_res) {
+  static const bool no_cluster = getenv("ABD_CG_NO_CLUSTER") != nullptr;
+  static const int ksmall = getenv("ABD_CL_SMALL") ? atoi(getenv("ABD_CL_SMALL")) : CL_MAX;
+  static const int kbig = getenv("ABD_CL_BIG") ? atoi(getenv("ABD_CL_BIG")) : 4;
+  static int cl_bps = -1;
+  const size_t cl_smem = (size_t)(RES_ROWS * 12 + 256) * sizeof(double);
+  if (cl_bps < 0) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cl_bps, k_cg_cluster, RES_THREADS, cl_smem));
+    CK(cudaFuncSetAttribute((void*)k_cluster_inv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            96 * 97 * (int)sizeof(double)));
+  }
+  int G = 0, ncl = 0;
+  int64_t minv_total = 0;
+  if (use_res && !no_cluster && cl_bps >= 1)
+    G = build_clusters(s, cl_bps * s.num_sms, std::min(ksmall, CL_MAX), std::min(kbig, CL_MAX), ncl, minv_total);
+  if (G > 0) {
+    w.minv.resize(std::max<int64_t>(minv_total, 1));
+    w.part.resize(8 * (int64_t)std::max(grid, G));
+    a.part = w.part.p;
+    k_cluster_inv<<<ncl, 96, 96 * 97 * sizeof(double), st>>>(ncl, w.cl_off.p, w.cl_rows.p, w.cl_minv.p, H.row_ptr.p,
+                                                            H.col.p, H.val.p, w.minv.p, w.bad.p);
+    note_launch("k_cluster_inv");
+    ClusterArgs ca{w.cl_slot_row.p, w.cl_slot_base.p, w.cl_slot_k.p, w.cl_slot_off.p, w.minv.p};
+    void* cargs[] = {&a, &ca};
+    grid = G;
+    CK(cudaLaunchCooperativeKernel((void*)k_cg_cluster, dim3(G), dim3(RES_THREADS), cargs, cl_smem, st));
+  } else if (use_res) {
     grid = res_groups;
     CK(cudaLaunchCooperativeKernel((void*)k_cg_res, dim3(grid), dim3(RES_THREADS), args, res_smem, st));
   } else {

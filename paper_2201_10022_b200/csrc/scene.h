@@ -150,6 +150,10 @@ struct Scene {
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
     DVec<double> cg_u, cg_w, cg_m, cg_q;
+    // cluster block-Jacobi preconditioner (k_cg.cu)
+    DVec<int> cl_slot_row, cl_slot_base, cl_slot_k, cl_off, cl_rows;
+    DVec<long long> cl_slot_off, cl_minv;
+    DVec<double> minv;
   } w;
 
   // per-kernel instrumentation (CUDA events on `stream`)
