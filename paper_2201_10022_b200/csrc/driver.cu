@@ -2,6 +2,8 @@
 // device-resident state.  Per Newton iteration only a handful of scalars
 // cross to the host (candidate counts, |dq|_inf and g.dq, alpha_max, one
 // energy per line-search trial); all buffers are persistent workspaces.
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <vector>
@@ -306,6 +308,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
     return std::chrono::duration<double, std::milli>(b - a).count();
   };
   auto t_start = clk::now();
+  static const bool trace_newton = getenv("ABD_TRACE_NEWTON") != nullptr;
   st = abd_step_stats{};
   cudaStream_t stream = s.stream;
   int64_t NB = 12 * (int64_t)s.B;
@@ -346,12 +349,13 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       assemble(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
       st.t_assemble += ms(t0, clk::now());
       t0 = clk::now();
-      double amax = 0.0, gd = 0.0;
+      double amax = 0.0, gd = 0.0, rel = 0.0;
+      int pcg_it = 0;
       if (ND) {
         k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
         note_launch("k_neg");
-        double rel = 0.0;
-        st.pcg_iters_total += pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
+        pcg_it = pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
+        st.pcg_iters_total += pcg_it;
         // |dx|_inf and g.dx in one pass, one sync
         unsigned long long* am = s.w.ull.p + 2;
         CK(cudaMemsetAsync(am, 0, sizeof(unsigned long long), stream));
@@ -403,6 +407,10 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         if (alpha < 1e-12) throw Error(ABD_ERR_STEP_FAILURE, "line search underflow (no descent below alpha = 1e-12)");
       }
       CK(cudaMemcpyAsync(s.q.p, s.q_trial.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+      if (trace_newton)
+        fprintf(stderr, "newton it=%d dq/dt=%.3e gd=%.3e pcg=%d rel=%.2e ccd=%.3e alpha=%.3e e0=%.10e de=%.3e ncand=%lld\n",
+                it, amax / P.dt, gd, pcg_it, rel, amax_ccd, alpha, e0, e - e0,
+                (long long)(s.cands.n_vf + s.cands.n_ee));
       st.t_line_search += ms(tls, clk::now());
       if (trace) trace[n_trace] = e;
       ++n_trace;
