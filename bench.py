@@ -165,9 +165,11 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=45)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--start", type=int, default=0, help="untimed steps before warm-up")
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--start", type=int, default=0, help="untimed steps before warm-up (no checkpoint)")
+    ap.add_argument("--ckpt", default=os.path.join(ROOT, "bench_data", "pile_step150.npz"),
+                    help="start state (q, q_dot, step) of the 20x20x25 pile; 'none' = step 0")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nx", type=int, default=20)
     ap.add_argument("--nz", type=int, default=25)
@@ -199,7 +201,15 @@ def main():
     B = len(model.bodies)
     L = _native.lib()
     sc = model.gpu_scene()
-    forces = np.ascontiguousarray(model.forces(0, params.dt, state.q), dtype=np.float64)
+    step0, time0 = 0, 0.0
+    use_ckpt = args.ckpt.lower() != "none" and (args.nx, args.nz) == (20, 25)
+    if use_ckpt:
+        ck = np.load(args.ckpt)
+        assert int(ck["seed"]) == 0 and ck["q"].shape == state.q.shape
+        state.q, state.q_dot = ck["q"].copy(), ck["q_dot"].copy()
+        step0, time0 = int(ck["step"]), float(ck["time"])
+        args.start = 0
+    forces = np.ascontiguousarray(model.forces(step0, time0 + params.dt, state.q), dtype=np.float64)
     q = np.ascontiguousarray(state.q, dtype=np.float64)
     qd = np.ascontiguousarray(state.q_dot, dtype=np.float64)
     _native.check(L.abd_set_state(sc.ptr, q.ctypes.data, qd.ctypes.data))
@@ -266,17 +276,20 @@ def main():
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_pcg (block-Jacobi PCG, one cooperative launch per solve)",
+    roofline = {"bound": "hbm", "kernel": "k_cg_cluster (pipelined cluster-block-Jacobi PCG, one cooperative "
+                                          "launch per Newton solve)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
                 "traffic": traffic, "peak_source": pk_kind,
-                "bytes_model": "per PCG iteration 1152*(nnzb + n) + 13*96*n (SURVEY 8(d) K4)",
+                "bytes_model": "per PCG iteration 1152*nnzb (BSR SpMV) + 8*sum_c (12 k_c)^2 (cluster inverses) "
+                               "+ 13*96*n (vectors), summed over the launch's iterations (SURVEY 8(d) K4)",
                 "share_of_step": pc["ms"] / elapsed_ms if elapsed_ms else None,
                 "other_kernels": {k: v for k, v in kst.items() if k != "k_pcg"}}
 
     # e2e through the public Python API with host numpy state
     e2e = None
     if not args.no_e2e:
-        state2 = P.SimState(q=q_start.copy(), q_dot=qd_start.copy(), time=0.0, step_index=args.start + args.warmup)
+        w0 = step0 + args.start + args.warmup
+        state2 = P.SimState(q=q_start.copy(), q_dot=qd_start.copy(), time=w0 * params.dt, step_index=w0)
         barrier()
         _native.check(L.abd_timer_start(sc.ptr))
         for _ in range(args.steps):
@@ -292,10 +305,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        r = oracle_sample_rate({}, args.start + args.warmup, args.cpu_budget, "1 thread")
+        r = oracle_sample_rate({}, args.warmup, args.cpu_budget, "1 thread")
         cpu = {"value": r["value"], "unit": "steps/s", "cores": 1, "kind": "port",
                "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} icospheres + "
-                         f"ground, same generator) from step {args.start + args.warmup}: {r['steps']} steps in "
+                         f"ground, same generator) from step {args.warmup}: {r['steps']} steps in "
                          f"{r['seconds']:.1f}s ({r['rate_sample']:.3f} steps/s), x{r['scale']:.4f} linear body "
                          "scaling to the 10k pile (optimistic for the CPU)"}
 
@@ -306,7 +319,9 @@ def main():
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
             "config": {"workload": f"icosphere_pile {args.nx}x{args.nx}x{args.nz} ({B} bodies, seed 0), "
-                                   f"steps [{args.start + args.warmup}, {args.start + args.warmup + args.steps})",
+                                   f"steps [{step0 + args.start + args.warmup}, {step0 + args.start + args.warmup + args.steps})"
+                                   + (f" from checkpoint {os.path.relpath(args.ckpt, ROOT)} (step {step0} of the "
+                                      "200-step run; late, contact-dense phase)" if use_ckpt else ""),
                        "newton_iters": int(iters_all), "newton_it_per_s": world * iters_all / (elapsed_ms * 1e-3),
                        "pcg_iters": pcg_total,
                        "l2": "per-step working set exceeds L2 (rest+topology+vertex boxes > 126 MB); no flush",

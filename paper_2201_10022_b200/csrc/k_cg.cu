@@ -811,7 +811,6 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
   a.out_iters = w.iters.p;
   a.out_rel = w.scal.p;
   void* args[] = {&a};
-  if (s.instrument) CK(cudaEventRecord(s.ev0, st));
   static const bool no_cluster = getenv("ABD_CG_NO_CLUSTER") != nullptr;
   static const int ksmall = getenv("ABD_CL_SMALL") ? atoi(getenv("ABD_CL_SMALL")) : CL_MAX;
   static const int kbig = getenv("ABD_CL_BIG") ? atoi(getenv("ABD_CL_BIG")) : 4;
@@ -833,14 +832,17 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
     k_cluster_inv<<<ncl, 96, 96 * 97 * sizeof(double), st>>>(ncl, w.cl_off.p, w.cl_rows.p, w.cl_minv.p, H.row_ptr.p,
                                                             H.col.p, H.val.p, w.minv.p, w.bad.p);
     note_launch("k_cluster_inv");
+    if (s.instrument) CK(cudaEventRecord(s.ev0, st));
     ClusterArgs ca{w.cl_slot_row.p, w.cl_slot_base.p, w.cl_slot_k.p, w.cl_slot_off.p, w.minv.p};
     void* cargs[] = {&a, &ca};
     grid = G;
     CK(cudaLaunchCooperativeKernel((void*)k_cg_cluster, dim3(G), dim3(RES_THREADS), cargs, cl_smem, st));
   } else if (use_res) {
+    if (s.instrument) CK(cudaEventRecord(s.ev0, st));
     grid = res_groups;
     CK(cudaLaunchCooperativeKernel((void*)k_cg_res, dim3(grid), dim3(RES_THREADS), args, res_smem, st));
   } else {
+    if (s.instrument) CK(cudaEventRecord(s.ev0, st));
     CK(cudaLaunchCooperativeKernel(kfun, dim3(grid), dim3(threads), args, 0, st));
   }
   note_launch("k_cg");
@@ -860,8 +862,10 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
     k.launches += 1;
     k.units += hit;
     k.ms += ms;
-    // algorithmic bytes per iteration: 1152 (nnzb + n) + 13 * 96 * n
-    k.bytes += (double)hit * (1152.0 * (double)(H.nnzb + n) + 13.0 * 96.0 * n);
+    // algorithmic bytes per iteration: BSR SpMV 1152 nnzb, preconditioner
+    // (1152 n block-Jacobi, or 8 * sum k_c^2 * 144 for the dense cluster inverses), 13 vectors.
+    const double prec_bytes = G > 0 ? 8.0 * (double)minv_total : 1152.0 * n;
+    k.bytes += (double)hit * (1152.0 * (double)H.nnzb + prec_bytes + 13.0 * 96.0 * n);
     static const bool trace = getenv("ABD_TRACE_PCG") != nullptr;
     if (trace) {
       // connected components of the block graph (diagnostic)
