@@ -89,6 +89,12 @@ int abd_bsr_matvec(int n, int bdim, const double* diag, int64_t n_off, const int
  * block) when a diagonal block is not SPD. */
 int abd_bsr_pcg(int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off,
                 const double* rhs, double rel_tol, int max_iters, double* x, int* iters, double* rel_res);
+/* x = A^-1 rhs by the device sparse block Cholesky (minimum-degree order, elimination-tree
+ * levels) with up to max_refine refinement steps until |A x - rhs| <= rel_tol |rhs|:
+ * BlockCholesky(A).solve_refined (sparse.py:90-161).  rel_tol = 0, max_refine = 0 is the plain
+ * BlockCholesky.solve (sparse.py:131-147).  Non-SPD pivot: ABD_ERR_FACTORIZATION, index = block. */
+int abd_bsr_cholesky(int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off,
+                     const double* rhs, double rel_tol, int max_refine, double* x, int* solves, double* rel_res);
 
 /* ---------------- scene context (device-resident geometry) -------------- */
 
@@ -147,6 +153,10 @@ int abd_assemble(abd_scene* s, const double* q, const double* q_tilde, double dt
 int abd_get_system(abd_scene* s, double* grad, double* diag, int64_t* off_keys, double* off_blocks);
 /* solve the resident system H dx = -grad (block-Jacobi PCG) */
 int abd_solve_resident(abd_scene* s, double rel_tol, int max_iters, double* dx, int* iters, double* rel_res);
+/* dx = -H^-1 g of the resident system by the device sparse block Cholesky with refinement
+ * (BlockCholesky(H).solve_refined(-g, rel_tol), sparse.py:90-161 / solver.py:345-348);
+ * solves = triangular solves performed (1 + corrections, at most 3 corrections). */
+int abd_solve_resident_cholesky(abd_scene* s, double rel_tol, double* dx, int* solves, double* rel_res);
 
 /* advance_step  solver.py:493-628 with device-resident state. */
 typedef struct abd_step_params {
@@ -154,10 +164,14 @@ typedef struct abd_step_params {
   double pcg_rel_tol;
   int max_newton_iters, friction_outer_iters, pcg_max_iters;
   int compute_min_distance; /* 1: StepStats.min_distance semantics (solver.py:604-611) */
+  /* Newton linear solve: 0 = sparse block Cholesky + refinement (BlockCholesky.solve_refined,
+   * sparse.py:90-161; the reference's solver), 1 = pipelined block-Jacobi PCG to pcg_rel_tol */
+  int linear_solver;
 } abd_step_params;
 
 typedef struct abd_step_stats {
-  int iterations, converged, nondescent_fallbacks, pcg_iters_total;
+  int iterations, converged, nondescent_fallbacks;
+  int pcg_iters_total;     /* PCG iterations, or triangular solves of the Cholesky path */
   int64_t candidates;      /* max candidate count over the step (StepStats.candidates) */
   double min_distance, ip_value, max_ortho_error, last_dq_over_dt;
   double t_broad, t_assemble, t_solve, t_ccd, t_line_search, t_total; /* ms, CUDA events */

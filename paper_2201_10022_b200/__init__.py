@@ -73,7 +73,7 @@ from .solver import (
     line_search,
     solve_newton_system,
 )
-from .sparse import BlockJacobiPCG, BlockSparseMatrix, FactorizationError
+from .sparse import BlockCholesky, BlockJacobiPCG, BlockSparseMatrix, FactorizationError
 
 __all__ = [n for n in dir() if not n.startswith("_")]
 __version__ = "0.1.0"

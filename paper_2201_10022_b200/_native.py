@@ -37,7 +37,7 @@ class StepParamsC(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("dt", "d_hat", "kappa_barrier", "mu", "epsilon_v", "newton_tol",
                                           "ccd_slack", "ccd_step_scale", "pcg_rel_tol")] + \
                [(n, C.c_int) for n in ("max_newton_iters", "friction_outer_iters", "pcg_max_iters",
-                                      "compute_min_distance")]
+                                      "compute_min_distance", "linear_solver")]
 
 
 class StepStatsC(C.Structure):
@@ -64,6 +64,7 @@ _SIGS = {
     "abd_friction_batch":(i32, [i64, lp, lp, dp, dbl, dp, dp, i32, dp, up8, dbl, dbl, i32, vp, vp, vp]),
     "abd_bsr_matvec": (i32, [i32, i32, dp, i64, lp, dp, dp, dp]),
     "abd_bsr_pcg": (i32, [i32, i32, dp, i64, lp, dp, dp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
+    "abd_bsr_cholesky": (i32, [i32, i32, dp, i64, lp, dp, dp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
     "abd_scene_create": (vp, [i32, lp, lp, lp, dp, lp, lp, dp, up8, dp, dp]),
     "abd_scene_destroy": (None, [vp]),
     "abd_broad_phase": (i32, [vp, dp, dp, dbl, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
@@ -83,6 +84,7 @@ _SIGS = {
     "abd_assemble": (i32, [vp, dp, dp, dbl, dbl, dbl, dbl, C.POINTER(i64)]),
     "abd_get_system": (i32, [vp, dp, dp, lp, dp]),
     "abd_solve_resident": (i32, [vp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
+    "abd_solve_resident_cholesky": (i32, [vp, dbl, dp, C.POINTER(i32), C.POINTER(dbl)]),
     "abd_kernel_stats": (i32, [vp, i32, C.POINTER(i64), C.POINTER(dbl), C.POINTER(dbl), C.POINTER(i64)]),
     "abd_kernel_stats_reset": (i32, [vp]),
     "abd_timer_start": (i32, [vp]),
@@ -266,6 +268,15 @@ def bsr_pcg(n, bdim, diag, keys, off, rhs, rel_tol=1e-8, max_iters=100000):
     check(lib().abd_bsr_pcg(n, bdim, f64(diag), len(keys), i64a(keys).reshape(-1), f64(off),
                             f64(rhs).reshape(-1), float(rel_tol), int(max_iters), x, C.byref(it), C.byref(rel)))
     return x, it.value, rel.value
+
+
+def bsr_cholesky(n, bdim, diag, keys, off, rhs, rel_tol=1e-8, max_refine=3):
+    x = np.empty(n * bdim)
+    ns, rel = C.c_int(0), C.c_double(0.0)
+    check(lib().abd_bsr_cholesky(n, bdim, f64(diag), len(keys), i64a(keys).reshape(-1), f64(off),
+                                 f64(rhs).reshape(-1), float(rel_tol), int(max_refine), x, C.byref(ns),
+                                 C.byref(rel)))
+    return x, ns.value, rel.value
 
 
 # ---------------------------------------------------------------------------

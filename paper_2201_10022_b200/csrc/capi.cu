@@ -357,6 +357,31 @@ int abd_bsr_pcg(int n, int bdim, const double* diag, int64_t n_off, const int64_
   });
 }
 
+int abd_bsr_cholesky(int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off,
+                     const double* rhs, double rel_tol, int max_refine, double* x, int* solves, double* rel_res) {
+  return guard([&] {
+    ensure_device();
+    if (bdim < 1 || bdim > 12) throw Error(ABD_ERR_ARG, "block_dim must be in [1, 12]");
+    if (max_refine < 0) throw Error(ABD_ERR_ARG, "max_refine < 0");
+    Scene& s = bsr_scene();
+    load_bsr(s, n, bdim, diag, n_off, keys, off);
+    std::vector<double> bp;
+    pad_vec(n, bdim, rhs, bp);
+    DVec<double> db, dx;
+    db.upload(bp.data(), bp.size(), s.stream);
+    dx.resize(std::max<size_t>(bp.size(), 1));
+    double rel = 0.0;
+    int ns = chol_solve(s, db.p, dx.p, rel_tol, rel, max_refine);
+    std::vector<double> xp(bp.size());
+    dx.download(xp.data(), xp.size(), s.stream);
+    sync(s.stream);
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < bdim; ++c) x[(size_t)bdim * i + c] = xp[12 * (size_t)i + c];
+    if (solves) *solves = ns;
+    if (rel_res) *rel_res = rel;
+  });
+}
+
 // ---------------------------------------------------------------------------
 abd_scene* abd_scene_create(int n_bodies, const int64_t* v_off, const int64_t* e_off, const int64_t* t_off,
                             const double* rest, const int64_t* edges, const int64_t* tris, const double* edge_len_sq,
@@ -701,6 +726,27 @@ int abd_solve_resident(abd_scene* h, double rel_tol, int max_iters, double* dx, 
     x.download(dx, N, s.stream);
     sync(s.stream);
     if (iters) *iters = it;
+    if (rel_res) *rel_res = rel;
+  });
+}
+
+int abd_solve_resident_cholesky(abd_scene* h, double rel_tol, double* dx, int* solves, double* rel_res) {
+  return guard([&] {
+    SC(h);
+    int64_t N = 12 * (int64_t)s.H.n;
+    DVec<double> neg, x;
+    neg.resize(std::max<int64_t>(N, 1));
+    x.resize(std::max<int64_t>(N, 1));
+    std::vector<double> g(N);
+    s.grad.download(g.data(), N, s.stream);
+    sync(s.stream);
+    for (auto& v : g) v = -v;
+    neg.upload(g.data(), N, s.stream);
+    double rel = 0.0;
+    int ns = chol_solve(s, neg.p, x.p, rel_tol, rel);
+    x.download(dx, N, s.stream);
+    sync(s.stream);
+    if (solves) *solves = ns;
     if (rel_res) *rel_res = rel;
   });
 }

@@ -354,7 +354,8 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       if (ND) {
         k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
         note_launch("k_neg");
-        pcg_it = pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
+        pcg_it = P.linear_solver == 1 ? pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel)
+                                      : chol_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, rel);
         st.pcg_iters_total += pcg_it;
         // |dx|_inf and g.dx in one pass, one sync
         unsigned long long* am = s.w.ull.p + 2;

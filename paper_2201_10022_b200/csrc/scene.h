@@ -154,6 +154,11 @@ struct Scene {
     DVec<int> cl_slot_row, cl_slot_base, cl_slot_k, cl_off, cl_rows;
     DVec<long long> cl_slot_off, cl_minv;
     DVec<double> minv;
+    // sparse block Cholesky plan and factor (k_chol.cu)
+    DVec<int> ch_flags, ch_nodes, ch_lvl_ptr, ch_cta_lvl, ch_cta_nlvl, ch_diag_blk, ch_col_cnt, ch_blk_row,
+        ch_blk_apos, ch_row_ptr, ch_row_blk, ch_row_col, ch_upd_ptr;
+    DVec<int2> ch_upd;
+    DVec<double> ch_L;
   } w;
 
   // per-kernel instrumentation (CUDA events on `stream`)

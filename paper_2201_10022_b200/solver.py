@@ -52,12 +52,17 @@ class StepParams:
     ccd_step_scale: float = 0.9
     workers: int = 1  # accepted for API compatibility; the GPU path has no host pool
     audit_iterates: bool = False
+    # Newton linear solve: "cholesky" = device sparse block Cholesky + refinement (the
+    # reference's BlockCholesky.solve_refined), "pcg" = block-Jacobi PCG to 1e-8 residual
+    linear_solver: str = "cholesky"
 
     def __post_init__(self):
         if self.dt <= 0 or self.d_hat <= 0 or self.newton_tol <= 0:
             raise ValueError("dt, d_hat and newton_tol must be positive")
         if self.mu < 0:
             raise ValueError("friction coefficient must be >= 0")
+        if self.linear_solver not in ("cholesky", "pcg"):
+            raise ValueError("linear_solver must be 'cholesky' or 'pcg'")
 
 
 @dataclass
@@ -227,7 +232,8 @@ def step_params_c(params: StepParams, min_distance=True, pcg_rel_tol=1e-8,
         epsilon_v=params.epsilon_v, newton_tol=params.newton_tol, ccd_slack=params.ccd_slack,
         ccd_step_scale=params.ccd_step_scale, pcg_rel_tol=pcg_rel_tol,
         max_newton_iters=params.max_newton_iters, friction_outer_iters=params.friction_outer_iters,
-        pcg_max_iters=pcg_max_iters, compute_min_distance=1 if min_distance else 0)
+        pcg_max_iters=pcg_max_iters, compute_min_distance=1 if min_distance else 0,
+        linear_solver=1 if params.linear_solver == "pcg" else 0)
 
 
 def advance_step(model: SystemModel, state: SimState, params: StepParams):

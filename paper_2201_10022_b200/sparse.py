@@ -2,10 +2,11 @@
 
 `BlockSparseMatrix` keeps the reference's host container semantics
 (fixed pattern, upper off-diagonal storage, out-of-pattern adds raise).
-`matvec` and `factor().solve*` run on the GPU: the reference's block
-Cholesky is replaced by a block-Jacobi PCG (kernel K4, csrc/k_solve.cu)
-to the same 1e-8 relative residual contract.  Blocks smaller
-than 12 are padded to 12 on the device.
+`matvec` and `factor().solve*` run on the GPU: `factor()` is the device
+sparse block Cholesky (kernel K4, csrc/k_chol.cu: minimum-degree order,
+elimination-tree levels, refinement as solve_refined); `BlockJacobiPCG`
+keeps the iterative alternative under the same 1e-8 relative residual
+contract.  Blocks smaller than 12 are padded to 12 on the device.
 """
 from __future__ import annotations
 
@@ -15,7 +16,7 @@ import numpy as np
 
 from . import _native
 
-__all__ = ["BlockSparseMatrix", "BlockJacobiPCG", "FactorizationError", "PcgNotConverged"]
+__all__ = ["BlockSparseMatrix", "BlockCholesky", "BlockJacobiPCG", "FactorizationError", "PcgNotConverged"]
 
 
 class FactorizationError(RuntimeError):
@@ -84,8 +85,40 @@ class BlockSparseMatrix:
         k, off = self._packed()
         return _native.bsr_matvec(self.n, self.b, self.diag, k, off, np.asarray(x, dtype=float))
 
-    def factor(self) -> "BlockJacobiPCG":
-        return BlockJacobiPCG(self)
+    def factor(self) -> "BlockCholesky":
+        return BlockCholesky(self)
+
+
+class BlockCholesky:
+    """L L^T = A on the GPU (sparse.py:87-161).
+
+    Construction factors once (raising FactorizationError(block) on a non-SPD
+    pivot); the solves re-run the device factor + triangular solves on the
+    current contents of A (the container is host-side and mutable).
+    """
+
+    def __init__(self, A: BlockSparseMatrix):
+        self._A = A
+        self.last_solves = 0
+        self.last_rel_residual = 0.0
+        if A.n:
+            k, off = A._packed()
+            _native.bsr_cholesky(A.n, A.b, A.diag, k, off, np.zeros(A.n * A.b), 0.0, 0)
+
+    def solve(self, rhs: np.ndarray) -> np.ndarray:
+        """One forward/backward substitution (sparse.py:131-147)."""
+        return self.solve_refined(rhs, rel_tol=0.0, max_refine=0)
+
+    def solve_refined(self, rhs: np.ndarray, rel_tol: float = 1e-8, max_refine: int = 3) -> np.ndarray:
+        """Iterative refinement until |A x - rhs| <= rel_tol |rhs| (sparse.py:149-161)."""
+        A = self._A
+        rhs = np.asarray(rhs, dtype=float).reshape(-1)
+        if A.n == 0:
+            return np.zeros(0)
+        k, off = A._packed()
+        x, ns, rel = _native.bsr_cholesky(A.n, A.b, A.diag, k, off, rhs, rel_tol, max_refine)
+        self.last_solves, self.last_rel_residual = ns, rel
+        return x
 
 
 class BlockJacobiPCG:

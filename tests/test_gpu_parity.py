@@ -286,6 +286,53 @@ def test_sparse_solver_and_errors():
                            rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("seed,n,deg", [(0, 60, 3), (1, 300, 5), (2, 1000, 2)])
+def test_block_cholesky_random_graph(seed, n, deg):
+    """Device block Cholesky (fill-in, multi-level elimination trees, several
+    components, isolated blocks) against a dense numpy solve."""
+    rng = np.random.default_rng(seed)
+    pairs = set()
+    for i in range(n):
+        for _ in range(rng.integers(0, deg + 1)):
+            j = int(rng.integers(0, n))
+            if j != i:
+                pairs.add((min(i, j), max(i, j)))
+    pairs = sorted(pairs)
+    A = P.BlockSparseMatrix(n, pairs, block_dim=12)
+    deg_of = np.zeros(n)
+    for i, j in pairs:
+        blk = rng.normal(size=(12, 12))
+        A.add_off(i, j, blk)
+        deg_of[i] += np.linalg.norm(blk, 2)
+        deg_of[j] += np.linalg.norm(blk, 2)
+    for i in range(n):
+        G = rng.normal(size=(12, 12))
+        A.add_diag(i, G @ G.T + (deg_of[i] + 1.0) * np.eye(12))  # block diagonally dominant
+    # a few pattern blocks left exactly zero (dropped by the analysis)
+    for k in pairs[::7]:
+        A.off[k][:] = 0.0
+    b = rng.normal(size=12 * n)
+    F = A.factor()
+    x = F.solve(b)
+    ref = np.linalg.solve(A.to_dense(), b)
+    assert np.linalg.norm(x - ref) <= 1e-11 * np.linalg.norm(ref)
+    xr = F.solve_refined(b, rel_tol=1e-14)
+    assert np.linalg.norm(A.matvec(xr) - b) <= 1e-13 * np.linalg.norm(b) or F.last_solves == 4
+
+
+def test_cholesky_and_pcg_steps_agree(golden):
+    """Both Newton linear solvers give the same box-stack steps to solver precision."""
+    g = golden("box_stack.npz")
+    model, state, params = _box_stack_model(g)
+    prm_p = P.StepParams(**{**params.__dict__, "linear_solver": "pcg"})
+    s1, s2 = state, state
+    for _ in range(10):
+        s1, st1 = P.advance_step(model, s1, params)
+        s2, st2 = P.advance_step(model, s2, prm_p)
+        assert st1.iterations == st2.iterations
+    assert rel_err(s1.q, s2.q) <= 1e-9
+
+
 def _box_stack_model(g):
     from paper_2201_10022_b200 import scenes
     spec = scenes.box_stack(seed=0)
