@@ -20,6 +20,7 @@
 // A failed pivot raises ABD_ERR_FACTORIZATION with the smallest failing
 // dynamic slot (sparse.py:18-26 semantics).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -35,20 +36,22 @@ namespace abd {
 constexpr int CH_THREADS = 256;
 constexpr int CH_HW = CH_THREADS / 16;  // half-warps per CTA
 
+// Plan layout (one packed int buffer uploaded per analysis).  L holds the n
+// diagonal blocks first (L_jj at index j), then the off-diagonal blocks.
 struct CholView {
-  const int* nodes;     // node ids, CTA-major then level-major
+  int n;
+  const int* nodes;     // node ids, CTA-major then level-major (isolated nodes last)
   const int* lvl_ptr;   // per CTA: nlvl + 1 offsets into nodes (absolute)
   const int* cta_lvl;   // per CTA: start index into lvl_ptr
   const int* cta_nlvl;  // per CTA: number of levels
-  const int* diag_blk;  // per node: L block index of L_jj (column blocks follow)
-  const int* col_cnt;   // per node: number of off-diagonal blocks in column j
-  const int* blk_row;   // per L block: row node i (off-diagonal blocks)
-  const int* blk_apos;  // per L block: position of A(i, j) in the BSR (-1: fill)
-  const int* row_ptr;   // per node: range into row_blk (blocks L_jk, k before j)
-  const int* row_blk;
+  const int* col_ptr;   // n + 1: off-diagonal blocks of column j (index k -> L block n + k)
+  const int* blk_row;   // per off block: row node i
+  const int* blk_apos;  // per off block: position of A(i, j) in the BSR (-1: fill)
+  const int* row_ptr;   // n + 1: range into row_blk (blocks L_jk, k eliminated before j)
+  const int* row_blk;   // L block index
   const int* row_col;   // column node k of each row_blk entry
-  const int* upd_ptr;   // per L block: range into upd (pairs (L_ik, L_jk))
-  const int2* upd;
+  const int* upd_ptr;   // per off block: range into upd
+  const int2* upd;      // (L_ik, L_jk) block index pairs
   const int* diag_pos;  // BSR diagonal block positions
   const double* val;    // BSR values
   double* L;            // L blocks, 144 doubles each (row-major)
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor(CholView v) {
     const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
     for (int idx = lo + hw; idx < hi; idx += CH_HW) {
       const int j = v.nodes[idx];
-      const int dblk = v.diag_blk[j];
+      const int dblk = j;
       // D = A_jj - sum_k L_jk L_jk^T (row t), then symmetrised (sparse.py:117)
       double d[12];
       if (t < 12) {
@@ -129,12 +132,11 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor(CholView v) {
         }
       }
       // off-diagonal blocks of column j: L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
-      const int nb = v.col_cnt[j];
-      for (int b = 1; b <= nb; ++b) {
-        const int blk = dblk + b;
+      for (int b = v.col_ptr[j]; b < v.col_ptr[j + 1]; ++b) {
+        const int blk = v.n + b;
         if (t < 12) {
           double bt[12];
-          const int ap = v.blk_apos[blk];
+          const int ap = v.blk_apos[b];
           if (ap >= 0) {
             const double* A = v.val + 144 * (int64_t)ap + 12 * t;
 #pragma unroll
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor(CholView v) {
 #pragma unroll
             for (int c = 0; c < 12; ++c) bt[c] = 0.0;
           }
-          for (int u = v.upd_ptr[blk]; u < v.upd_ptr[blk + 1]; ++u) {
+          for (int u = v.upd_ptr[b]; u < v.upd_ptr[b + 1]; ++u) {
             const int2 pq = v.upd[u];
             const double* Li = v.L + 144 * (int64_t)pq.x;  // L_ik
             const double* Lj = v.L + 144 * (int64_t)pq.y;  // L_jk
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_solve(CholView v, const dou
           for (int m = 0; m < 12; ++m) s = fma(Lk[m], yk[m], s);
           acc -= s;
         }
-        const double* Ld = v.L + 144 * (int64_t)v.diag_blk[j] + 12 * tt;
+        const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
 #pragma unroll
         for (int m = 0; m < 12; ++m) lrow[m] = Ld[m];
       } else {
@@ -231,17 +233,15 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_solve(CholView v, const dou
       double acc = 0.0, lcol[12];
       if (live) {
         acc = x[12 * (int64_t)j + tt];
-        const int dblk = v.diag_blk[j];
-        const int nb = v.col_cnt[j];
-        for (int bb = 1; bb <= nb; ++bb) {
-          const double* Lb = v.L + 144 * (int64_t)(dblk + bb) + tt;  // column tt of L_ij
-          const double* xi = x + 12 * (int64_t)v.blk_row[dblk + bb];
+        for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
+          const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;  // column tt of L_ij
+          const double* xi = x + 12 * (int64_t)v.blk_row[bb];
           double s = 0.0;
 #pragma unroll
           for (int r = 0; r < 12; ++r) s = fma(Lb[12 * r], xi[r], s);
           acc -= s;
         }
-        const double* Ld = v.L + 144 * (int64_t)dblk + tt;
+        const double* Ld = v.L + 144 * (int64_t)j + tt;
 #pragma unroll
         for (int m = 0; m < 12; ++m) lcol[m] = Ld[12 * m];  // L_jj[m][tt]
       } else {
@@ -323,29 +323,26 @@ __global__ void k_add_inplace(int64_t n, double* x, const double* d) {
 namespace {
 
 struct Analysis {
-  int n_cta = 0;
+  int n_cta = 0, n_coupled = 0;
   int64_t n_blk = 0, n_upd = 0, n_edges = 0;
   int max_level = 0, largest = 0;
+  double ms_sync = 0, ms_order = 0, ms_plan = 0;
+  CholView view{};
 };
 
-// minimum-degree elimination on the block graph; returns struct(v) (later
-// neighbours at elimination) per node and the elimination order.
-void min_degree(int n, std::vector<std::vector<int>>& adj, std::vector<int>& order,
+// minimum-degree elimination on a (local) graph; colstruct[v] = neighbours
+// still alive when v is eliminated (its L column structure), order = elimination order.
+void min_degree(int m, std::vector<std::vector<int>>& adj, std::vector<int>& order,
                 std::vector<std::vector<int>>& colstruct) {
   order.clear();
-  order.reserve(n);
-  colstruct.assign(n, {});
-  std::vector<char> done(n, 0);
+  order.reserve(m);
+  colstruct.assign(m, {});
+  std::vector<char> done(m, 0);
   typedef std::pair<int, int> DI;
-  std::priority_queue<DI, std::vector<DI>, std::greater<DI>> heap;
-  for (int v = 0; v < n; ++v) {
-    if (adj[v].empty()) {
-      order.push_back(v);  // isolated: eliminated first, no structure
-      done[v] = 1;
-    } else {
-      heap.push({(int)adj[v].size(), v});
-    }
-  }
+  std::vector<DI> hv;
+  hv.reserve(2 * m);
+  for (int v = 0; v < m; ++v) hv.push_back({(int)adj[v].size(), v});
+  std::priority_queue<DI, std::vector<DI>, std::greater<DI>> heap(std::greater<DI>(), std::move(hv));
   std::vector<int> merged;
   while (!heap.empty()) {
     DI top = heap.top();
@@ -354,10 +351,9 @@ void min_degree(int n, std::vector<std::vector<int>>& adj, std::vector<int>& ord
     if (done[v] || top.first != (int)adj[v].size()) continue;
     done[v] = 1;
     order.push_back(v);
-    std::vector<int> nb = adj[v];  // sorted, alive neighbours
-    colstruct[v] = nb;
+    std::vector<int>& nb = colstruct[v];
+    nb.swap(adj[v]);
     for (int a : nb) {
-      // adj[a] = (adj[a] U nb) \ {a, v}
       merged.clear();
       std::set_union(adj[a].begin(), adj[a].end(), nb.begin(), nb.end(), std::back_inserter(merged));
       std::vector<int>& out = adj[a];
@@ -366,202 +362,257 @@ void min_degree(int n, std::vector<std::vector<int>>& adj, std::vector<int>& ord
         if (u != a && u != v) out.push_back(u);
       heap.push({(int)out.size(), a});
     }
-    adj[v].clear();
   }
+}
+
+double ms_since(std::chrono::steady_clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
 }
 
 }  // namespace
 
 static Analysis chol_analyze(Scene& s) {
+  using clk = std::chrono::steady_clock;
   Bsr& H = s.H;
   Scene::Work& w = s.w;
   cudaStream_t st = s.stream;
   const int n = H.n;
   const int64_t n_off = H.n_off;
   Analysis an;
-  std::vector<int> flags(n_off), upos(n_off), lpos(n_off), dpos(n);
-  std::vector<int2> keys(n_off);
+  auto t0 = clk::now();
+  // flags | upper_pos | lower_pos | keys (2 ints) per pattern block, one pinned staging buffer
+  int* hm = w.h_meta.reserve(5 * (size_t)std::max<int64_t>(n_off, 1));
+  int *flags = hm, *upos = hm + n_off, *lpos = hm + 2 * n_off, *keys = hm + 3 * n_off;
   if (n_off) {
     w.ch_flags.resize(n_off);
     k_block_nz<<<grid_for(n_off * 32, 256), 256, 0, st>>>(n_off, H.upper_pos.p, H.val.p, w.ch_flags.p);
     note_launch("k_block_nz");
-    w.ch_flags.download(flags.data(), n_off, st);
-    H.upper_pos.download(upos.data(), n_off, st);
-    H.lower_pos.download(lpos.data(), n_off, st);
-    H.upper_keys.download(keys.data(), n_off, st);
+    CK(cudaMemcpyAsync(flags, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(upos, H.upper_pos.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lpos, H.lower_pos.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(keys, H.upper_keys.p, n_off * sizeof(int2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   }
-  H.diag_pos.download(dpos.data(), n, st);
-  CK(cudaStreamSynchronize(st));
+  an.ms_sync = ms_since(t0);
+  t0 = clk::now();
 
-  // graph of nonzero couplings (keys are (i < j) sorted)
-  std::vector<std::vector<int>> adj(n);
+  // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order
+  std::vector<int> loc(n, -1), glob;
   for (int64_t k = 0; k < n_off; ++k)
     if (flags[k]) {
-      adj[keys[k].x].push_back(keys[k].y);
-      adj[keys[k].y].push_back(keys[k].x);
+      loc[keys[2 * k]] = 0;
+      loc[keys[2 * k + 1]] = 0;
       ++an.n_edges;
     }
-  for (auto& a : adj) std::sort(a.begin(), a.end());
-  // (row, col) -> BSR position of the original coupling, for L block sources
-  auto apos_of = [&](int i, int j) -> int {
-    int a = std::min(i, j), b = std::max(i, j);
-    // binary search in the sorted upper keys
+  for (int v = 0; v < n; ++v)
+    if (loc[v] == 0) {
+      loc[v] = (int)glob.size();
+      glob.push_back(v);
+    }
+  const int m = (int)glob.size();
+  an.n_coupled = m;
+  // adjacency in key order is already sorted per node (keys sorted by (i, j))
+  std::vector<std::vector<int>> adj(m);
+  for (int64_t k = 0; k < n_off; ++k)
+    if (flags[k]) {
+      int a = loc[keys[2 * k]], b = loc[keys[2 * k + 1]];
+      adj[a].push_back(b);
+      adj[b].push_back(a);
+    }
+  std::vector<int> order;
+  std::vector<std::vector<int>> cs;
+  min_degree(m, adj, order, cs);
+  std::vector<int> pos(m);
+  for (int i = 0; i < m; ++i) pos[order[i]] = i;
+  for (auto& c : cs)
+    if (c.size() > 1) std::sort(c.begin(), c.end(), [&](int a, int b) { return pos[a] < pos[b]; });
+  an.ms_order = ms_since(t0);
+  t0 = clk::now();
+
+  auto apos_of = [&](int gi, int gj) -> int {  // BSR position of A(gi, gj) (nonzero coupling)
+    int a = std::min(gi, gj), b = std::max(gi, gj);
     int64_t lo = 0, hi = n_off - 1;
     while (lo <= hi) {
-      int64_t m = (lo + hi) >> 1;
-      int2 km = keys[m];
-      if (km.x < a || (km.x == a && km.y < b)) lo = m + 1;
-      else if (km.x == a && km.y == b) return flags[m] ? (i < j ? upos[m] : lpos[m]) : -1;
-      else hi = m - 1;
+      int64_t mm = (lo + hi) >> 1;
+      int kx = keys[2 * mm], ky = keys[2 * mm + 1];
+      if (kx < a || (kx == a && ky < b)) lo = mm + 1;
+      else if (kx == a && ky == b) return flags[mm] ? (gi < gj ? upos[mm] : lpos[mm]) : -1;
+      else hi = mm - 1;
     }
     return -1;
   };
-
-  std::vector<int> order;
-  std::vector<std::vector<int>> cs;
-  min_degree(n, adj, order, cs);
-  std::vector<int> pos(n);
-  for (int i = 0; i < n; ++i) pos[order[i]] = i;
-  for (auto& c : cs) std::sort(c.begin(), c.end(), [&](int a, int b) { return pos[a] < pos[b]; });
-
-  // L blocks: per node the diagonal then its column structure
-  std::vector<int> diag_blk(n), col_cnt(n);
-  int64_t nb = 0;
-  for (int j = 0; j < n; ++j) {
-    diag_blk[j] = (int)nb;
-    col_cnt[j] = (int)cs[j].size();
-    nb += 1 + cs[j].size();
-  }
-  an.n_blk = nb;
-  std::vector<int> blk_row(nb, -1), blk_apos(nb, -1);
-  // row lists: for node i, blocks L_ik (k eliminated before i), ordered by pos[k]
-  std::vector<std::vector<std::pair<int, int>>> rows(n);  // (k, blk)
-  for (int k : order) {
+  // off-diagonal L blocks: column (local) v owns [col_off[v], col_off[v+1])
+  std::vector<int> col_off(m + 1, 0);
+  for (int v = 0; v < m; ++v) col_off[v + 1] = col_off[v] + (int)cs[v].size();
+  const int nbo = col_off[m];
+  an.n_blk = n + (int64_t)nbo;
+  // row lists (local i): (k, off block) for k eliminated before i, in elimination order of k
+  std::vector<int> rcnt(m + 1, 0);
+  for (int v = 0; v < m; ++v)
+    for (int i : cs[v]) rcnt[i + 1]++;
+  for (int v = 0; v < m; ++v) rcnt[v + 1] += rcnt[v];
+  std::vector<int> rfill(rcnt.begin(), rcnt.end() - 1), r_k(nbo), r_b(nbo);
+  for (int k : order)
     for (size_t q = 0; q < cs[k].size(); ++q) {
       int i = cs[k][q];
-      int blk = diag_blk[k] + 1 + (int)q;
-      blk_row[blk] = i;
-      blk_apos[blk] = apos_of(i, k);
-      rows[i].push_back({k, blk});
+      r_k[rfill[i]] = k;
+      r_b[rfill[i]] = col_off[k] + (int)q;
+      rfill[i]++;
     }
-  }
-  std::vector<int> row_ptr(n + 1, 0), row_blk, row_col;
-  for (int i = 0; i < n; ++i) {
-    row_ptr[i + 1] = row_ptr[i] + (int)rows[i].size();
-    for (auto& pr : rows[i]) {
-      row_col.push_back(pr.first);
-      row_blk.push_back(pr.second);
-    }
-  }
-  // update lists for off-diagonal blocks (i, j): k in rows[j] with i in cs[k]
-  std::vector<int> upd_ptr(nb + 1, 0);
-  std::vector<int2> upd;
-  for (int j = 0; j < n; ++j) {
-    for (int bq = 0; bq <= col_cnt[j]; ++bq) {
-      int blk = diag_blk[j] + bq;
-      if (bq > 0) {
-        int i = blk_row[blk];
-        for (auto& pr : rows[j]) {
-          int k = pr.first;
-          const std::vector<int>& ck = cs[k];
-          auto it = std::find(ck.begin(), ck.end(), i);
-          if (it != ck.end()) upd.push_back(make_int2(diag_blk[k] + 1 + (int)(it - ck.begin()), pr.second));
+  // update pairs for off block (i, j): k in rows(j) with i in cs[k]
+  std::vector<int> upd_ptr(nbo + 1, 0), upd;
+  for (int j = 0; j < m; ++j)
+    for (size_t q = 0; q < cs[j].size(); ++q) {
+      int b = col_off[j] + (int)q, i = cs[j][q];
+      for (int e = rcnt[j]; e < rcnt[j + 1]; ++e) {
+        const std::vector<int>& ck = cs[r_k[e]];
+        auto it = std::find(ck.begin(), ck.end(), i);
+        if (it != ck.end()) {
+          upd.push_back(n + col_off[r_k[e]] + (int)(it - ck.begin()));
+          upd.push_back(n + r_b[e]);
         }
       }
-      upd_ptr[blk + 1] = (int)upd.size();
+      upd_ptr[b + 1] = (int)(upd.size() / 2);
     }
-  }
-  an.n_upd = (int64_t)upd.size();
-  // elimination tree levels (height above the leaves) and component roots
-  std::vector<int> level(n, 0), root(n);
+  an.n_upd = (int64_t)upd.size() / 2;
+  // elimination-tree levels and component roots (local)
+  std::vector<int> level(m, 0), root(m);
   for (int v : order)
-    if (!cs[v].empty()) {
-      int p = cs[v][0];
-      level[p] = std::max(level[p], level[v] + 1);
-    }
-  for (int q = n - 1; q >= 0; --q) {
+    if (!cs[v].empty()) level[cs[v][0]] = std::max(level[cs[v][0]], level[v] + 1);
+  for (int q = m - 1; q >= 0; --q) {
     int v = order[q];
     root[v] = cs[v].empty() ? v : root[cs[v][0]];
   }
-  // components -> CTAs (largest first onto the least loaded CTA)
-  std::vector<int> csize(n, 0), cdepth(n, 0);
-  for (int v = 0; v < n; ++v) {
+  std::vector<int> csize(m, 0), cdepth(m, 0), comps;
+  for (int v = 0; v < m; ++v) {
     csize[root[v]]++;
     cdepth[root[v]] = std::max(cdepth[root[v]], level[v] + 1);
+    an.max_level = std::max(an.max_level, level[v] + 1);
   }
-  std::vector<int> comps;
-  for (int v = 0; v < n; ++v)
+  for (int v = 0; v < m; ++v)
     if (root[v] == v) comps.push_back(v);
-  std::sort(comps.begin(), comps.end(), [&](int a, int b) {
-    return csize[a] != csize[b] ? csize[a] > csize[b] : a < b;
-  });
+  std::sort(comps.begin(), comps.end(),
+            [&](int a, int b) { return csize[a] != csize[b] ? csize[a] > csize[b] : a < b; });
   an.largest = comps.empty() ? 0 : csize[comps[0]];
-  const int n_cta = std::max(1, std::min((int)comps.size(), 4 * s.num_sms));
+  // CTAs: components (largest first onto the least loaded), then isolated nodes
+  const int n_iso = n - m;
+  const int iso_per_cta = 4 * CH_HW;
+  const int n_ccta = std::min((int)comps.size(), 2 * s.num_sms);
+  const int n_icta = (n_iso + iso_per_cta - 1) / iso_per_cta;
+  const int n_cta = std::max(1, n_ccta + n_icta);
   an.n_cta = n_cta;
-  std::vector<int> cta_of_root(n, -1);
+  std::vector<int> cta_of(m, -1), cta_nlvl(n_cta, 0);
   {
     typedef std::pair<int64_t, int> LI;
     std::priority_queue<LI, std::vector<LI>, std::greater<LI>> load;
-    for (int c = 0; c < n_cta; ++c) load.push({0, c});
+    for (int c = 0; c < n_ccta; ++c) load.push({0, c});
     for (int r : comps) {
       LI top = load.top();
       load.pop();
-      cta_of_root[r] = top.second;
-      // cost: nodes spread over the CTA's half-warps plus the level latency
+      cta_of[r] = top.second;
+      cta_nlvl[top.second] = std::max(cta_nlvl[top.second], cdepth[r]);
       top.first += (int64_t)csize[r] + 8 * (int64_t)cdepth[r];
       load.push(top);
     }
   }
-  std::vector<int> cta_nlvl(n_cta, 0);
-  for (int v = 0; v < n; ++v) {
-    int c = cta_of_root[root[v]];
-    cta_nlvl[c] = std::max(cta_nlvl[c], level[v] + 1);
-    an.max_level = std::max(an.max_level, level[v] + 1);
-  }
-  std::vector<int> cta_lvl(n_cta + 1, 0);
-  for (int c = 0; c < n_cta; ++c) cta_lvl[c + 1] = cta_lvl[c] + cta_nlvl[c] + 1;
-  std::vector<int> cnt(cta_lvl[n_cta], 0);
-  for (int v = 0; v < n; ++v) cnt[cta_lvl[cta_of_root[root[v]]] + level[v]]++;
-  std::vector<int> lvl_ptr(cta_lvl[n_cta], 0);
+  for (int c = n_ccta; c < n_cta; ++c) cta_nlvl[c] = (n_iso > 0) ? 1 : 0;
+
+  // packed plan: nodes | lvl_ptr | cta_lvl | cta_nlvl | col_ptr | blk_row | blk_apos | row_ptr |
+  //              row_blk | row_col | upd_ptr | (pad) | upd pairs
+  int n_lvl_entries = 0;
+  for (int c = 0; c < n_cta; ++c) n_lvl_entries += cta_nlvl[c] + 1;
+  size_t off_nodes = 0, off_lvl = off_nodes + n, off_ctal = off_lvl + n_lvl_entries, off_ctan = off_ctal + n_cta,
+         off_colp = off_ctan + n_cta, off_brow = off_colp + n + 1, off_bapos = off_brow + nbo,
+         off_rowp = off_bapos + nbo, off_rowb = off_rowp + n + 1, off_rowc = off_rowb + nbo,
+         off_updp = off_rowc + nbo, off_upd = off_updp + nbo + 1;
+  off_upd += off_upd & 1;  // int2 alignment
+  const size_t total = off_upd + upd.size() + 2;
+  int* hp = w.h_plan.reserve(total);
+  int* nodes = hp + off_nodes;
+  int* lvl_ptr = hp + off_lvl;
+  int* cta_lvl = hp + off_ctal;
+  int* cta_nl = hp + off_ctan;
   {
-    int run = 0;
+    // count nodes per (cta, level), then prefix offsets
+    int e = 0;
     for (int c = 0; c < n_cta; ++c) {
+      cta_lvl[c] = e;
+      cta_nl[c] = cta_nlvl[c];
+      e += cta_nlvl[c] + 1;
+    }
+    std::vector<int> cnt(n_lvl_entries + 1, 0);
+    for (int v = 0; v < m; ++v) cnt[cta_lvl[cta_of[root[v]]] + level[v]]++;
+    int run = 0;
+    for (int c = 0; c < n_ccta; ++c)
       for (int l = 0; l <= cta_nlvl[c]; ++l) {
-        int e = cta_lvl[c] + l;
-        lvl_ptr[e] = run;
-        if (l < cta_nlvl[c]) run += cnt[e];
+        int ix = cta_lvl[c] + l;
+        lvl_ptr[ix] = run;
+        if (l < cta_nlvl[c]) run += cnt[ix];
+      }
+    std::vector<int> fillp(lvl_ptr, lvl_ptr + n_lvl_entries);
+    for (int v = 0; v < m; ++v) nodes[fillp[cta_lvl[cta_of[root[v]]] + level[v]]++] = glob[v];
+    // isolated nodes, iso_per_cta per CTA in node order
+    int iso = m;
+    for (int c = n_ccta; c < n_cta; ++c) {
+      lvl_ptr[cta_lvl[c]] = iso;
+      iso = std::min(n, iso + iso_per_cta);
+      lvl_ptr[cta_lvl[c] + 1] = iso;
+    }
+    int q = m;
+    for (int v = 0; v < n; ++v)
+      if (loc[v] < 0) nodes[q++] = v;
+  }
+  int* col_ptr = hp + off_colp;
+  int* row_ptr = hp + off_rowp;
+  {
+    // per global node column/row ranges (empty for isolated nodes)
+    int c = 0, r = 0;
+    for (int v = 0; v < n; ++v) {
+      col_ptr[v] = c;
+      row_ptr[v] = r;
+      int l = loc[v];
+      if (l >= 0) {
+        for (size_t q = 0; q < cs[l].size(); ++q) {
+          int b = col_off[l] + (int)q;  // == c + q since locals follow global order
+          hp[off_brow + b] = glob[cs[l][q]];
+          hp[off_bapos + b] = apos_of(glob[cs[l][q]], v);
+        }
+        c += (int)cs[l].size();
+        for (int e2 = rcnt[l]; e2 < rcnt[l + 1]; ++e2) {
+          hp[off_rowb + r] = r_b[e2] + n;
+          hp[off_rowc + r] = glob[r_k[e2]];
+          ++r;
+        }
       }
     }
+    col_ptr[n] = c;
+    row_ptr[n] = r;
   }
-  std::vector<int> fillp(lvl_ptr), nodes(n);
-  for (int v = 0; v < n; ++v) nodes[fillp[cta_lvl[cta_of_root[root[v]]] + level[v]]++] = v;
-
-  auto up = [&](DVec<int>& d, const std::vector<int>& h) { d.upload(h.data(), std::max<size_t>(h.size(), 1), st); };
-  up(w.ch_nodes, nodes);
-  up(w.ch_lvl_ptr, lvl_ptr);
-  up(w.ch_cta_lvl, cta_lvl);
-  up(w.ch_cta_nlvl, cta_nlvl);
-  up(w.ch_diag_blk, diag_blk);
-  up(w.ch_col_cnt, col_cnt);
-  up(w.ch_blk_row, blk_row);
-  up(w.ch_blk_apos, blk_apos);
-  up(w.ch_row_ptr, row_ptr);
-  if (row_blk.empty()) row_blk.push_back(0), row_col.push_back(0);
-  up(w.ch_row_blk, row_blk);
-  up(w.ch_row_col, row_col);
-  up(w.ch_upd_ptr, upd_ptr);
-  if (upd.empty()) upd.push_back(make_int2(0, 0));
-  w.ch_upd.upload(upd.data(), upd.size(), st);
-  w.ch_L.resize(144 * std::max<int64_t>(nb, 1));
+  std::copy(upd_ptr.begin(), upd_ptr.end(), hp + off_updp);
+  std::copy(upd.begin(), upd.end(), hp + off_upd);
+  w.ch_plan.resize(total);
+  CK(cudaMemcpyAsync(w.ch_plan.p, hp, total * sizeof(int), cudaMemcpyHostToDevice, st));
+  w.ch_L.resize(144 * std::max<int64_t>(an.n_blk, 1));
+  const int* dp = w.ch_plan.p;
+  an.view = CholView{n,
+                     dp + off_nodes,
+                     dp + off_lvl,
+                     dp + off_ctal,
+                     dp + off_ctan,
+                     dp + off_colp,
+                     dp + off_brow,
+                     dp + off_bapos,
+                     dp + off_rowp,
+                     dp + off_rowb,
+                     dp + off_rowc,
+                     dp + off_updp,
+                     reinterpret_cast<const int2*>(dp + off_upd),
+                     H.diag_pos.p,
+                     H.val.p,
+                     w.ch_L.p,
+                     w.bad.p};
+  an.ms_plan = ms_since(t0);
   return an;
-}
-
-static CholView chol_view(Scene& s) {
-  Scene::Work& w = s.w;
-  return CholView{w.ch_nodes.p,    w.ch_lvl_ptr.p, w.ch_cta_lvl.p, w.ch_cta_nlvl.p, w.ch_diag_blk.p,
-                  w.ch_col_cnt.p,  w.ch_blk_row.p, w.ch_blk_apos.p, w.ch_row_ptr.p, w.ch_row_blk.p,
-                  w.ch_row_col.p,  w.ch_upd_ptr.p, w.ch_upd.p,      s.H.diag_pos.p, s.H.val.p,
-                  w.ch_L.p,        w.bad.p};
 }
 
 // Direct solve of the resident system H x = rhs with refinement (sparse.py:149-161).
@@ -574,9 +625,11 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
   const int64_t N = 12 * (int64_t)n;
   rel_res = 0.0;
   if (n == 0) return 0;
-  Analysis an = chol_analyze(s);
-  CholView v = chol_view(s);
+  auto th0 = std::chrono::steady_clock::now();
   w.bad.resize(1);
+  Analysis an = chol_analyze(s);
+  const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+  CholView v = an.view;
   const int big = 0x7fffffff;
   CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   if (s.instrument) CK(cudaEventRecord(s.ev0, st));
@@ -625,9 +678,9 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
     if (trace)
       fprintf(stderr,
               "[abd chol] n=%d edges=%lld L_blocks=%lld updates=%lld levels=%d largest=%d ctas=%d solves=%d "
-              "rel=%.2e factor+solve_ms=%.3f\n",
+              "rel=%.2e factor+solve_ms=%.3f analysis_ms=%.3f (sync %.3f order %.3f plan %.3f) coupled=%d\n",
               n, (long long)an.n_edges, (long long)an.n_blk, (long long)an.n_upd, an.max_level, an.largest,
-              an.n_cta, solves, rel_res, ms);
+              an.n_cta, solves, rel_res, ms, host_ms, an.ms_sync, an.ms_order, an.ms_plan, an.n_coupled);
   }
   return solves;
 }

@@ -56,6 +56,28 @@ struct DVec {
   }
 };
 
+// growable pinned host buffer (never shrinks)
+template <class T>
+struct HostPinned {
+  T* p = nullptr;
+  size_t cap = 0;
+  HostPinned() = default;
+  HostPinned(const HostPinned&) = delete;
+  HostPinned& operator=(const HostPinned&) = delete;
+  ~HostPinned() {
+    if (p) cudaFreeHost(p);
+  }
+  T* reserve(size_t m) {
+    if (m > cap) {
+      if (p) CK(cudaFreeHost(p));
+      size_t c = m + m / 4 + 64;
+      CK(cudaMallocHost(&p, c * sizeof(T)));
+      cap = c;
+    }
+    return p;
+  }
+};
+
 struct Cands {
   DVec<int4> vf, ee;  // (body_a, prim_a, body_b, prim_b) in canonical order
   DVec<int2> ov;      // overlapping body pairs (i < j)
@@ -154,11 +176,10 @@ struct Scene {
     DVec<int> cl_slot_row, cl_slot_base, cl_slot_k, cl_off, cl_rows;
     DVec<long long> cl_slot_off, cl_minv;
     DVec<double> minv;
-    // sparse block Cholesky plan and factor (k_chol.cu)
-    DVec<int> ch_flags, ch_nodes, ch_lvl_ptr, ch_cta_lvl, ch_cta_nlvl, ch_diag_blk, ch_col_cnt, ch_blk_row,
-        ch_blk_apos, ch_row_ptr, ch_row_blk, ch_row_col, ch_upd_ptr;
-    DVec<int2> ch_upd;
+    // sparse block Cholesky plan (one packed int buffer) and factor (k_chol.cu)
+    DVec<int> ch_flags, ch_plan;
     DVec<double> ch_L;
+    HostPinned<int> h_plan, h_meta;
   } w;
 
   // per-kernel instrumentation (CUDA events on `stream`)

@@ -24,4 +24,5 @@ for _ in range(K):
     t0 = time.time()
     state, st = P.advance_step(model, state, params)
     print(f"step {st.step} it={st.iterations} conv={st.converged} pcg={st.pcg_iterations} "
-          f"mind={st.min_distance:.3e} wall={time.time() - t0:.3f}s", file=sys.stderr, flush=True)
+          f"mind={st.min_distance:.3e} wall={time.time() - t0:.3f}s "
+          + " ".join(f"{k}={v * 1e3:.1f}ms" for k, v in st.timings.items()), file=sys.stderr, flush=True)
