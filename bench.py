@@ -85,7 +85,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def oracle_sample_rate(spec_kw, start_steps, budget_s, threads_note):
+def oracle_sample_rate(spec_kw, start_steps, budget_s, threads_note, threads=None):
     """Oracle advance_step steps/s on a 8x8x2 sub-pile (same generator), scaled to 10k bodies."""
     from oracle import abd_oracle as O
     from paper_2201_10022_b200 import scenes
@@ -117,6 +117,8 @@ def oracle_sample_rate(spec_kw, start_steps, budget_s, threads_note):
         f[b, 3:] = np.kron(g, masses[b][0, 3:6])
     q, qd = spec.q0.copy(), spec.q_dot0.copy()
     warnings.simplefilter("ignore")
+    from threadpoolctl import threadpool_limits
+    limiter = threadpool_limits(limits=threads) if threads else None
     for _ in range(start_steps):
         q, qd, _ = O.advance_step(model, q, qd, f, prm, min_distance=False)
     n = 0
@@ -129,6 +131,8 @@ def oracle_sample_rate(spec_kw, start_steps, budget_s, threads_note):
         el = time.perf_counter() - t0
         if el >= budget_s or n >= 200:
             break
+    if limiter is not None:
+        limiter.restore_original_limits()
     nb = int(model.dynamic.sum())
     scale = nb / 10000.0
     return {"rate_sample": n / el, "steps": n, "seconds": el, "iters": iters, "bodies": nb,
@@ -259,31 +263,42 @@ def main():
     elapsed_ms = max_over_ranks(ms.value)
     iters_all = max_over_ranks(float(iters))
     value = world * args.steps / (elapsed_ms * 1e-3)
-    # dominant kernel: the PCG solve (k_pcg); stats on this rank
+    # per-kernel live stats (CUDA events on the scene stream, this rank); the roofline
+    # is reported for the instrumented kernel with the largest share of the timed region
+    names = {0: ("k_chol", "k_chol_factor + k_chol_solve (K4 sparse block Cholesky, one factor + solve "
+                           "per Newton iteration; PCG iterations when linear_solver='pcg')",
+                 "A blocks read + L written (1152 B each), 2x1152 B per update pair, L read twice by the "
+                 "solve, 4 vectors of 96 B per body"),
+             1: ("k_pair_blocks", "k_pair_blocks (K3 contact pair gradient/Hessian, VF + EE launches)",
+                 "SURVEY 8(d) K3: 112 P_vf + 120 P_ee + 96 B + 1152 N_blk + 96 B_d"),
+             2: ("k_ccd", "k_ccd (K5 additive CCD, VF + EE launches)", "SURVEY 8(d) K5: 112 (P_vf + P_ee) + 192 B"),
+             3: ("k_prim_pairs", "k_prim_pairs (K2 broad phase primitive pairs)",
+                 "SURVEY 8(d) K2: 24 V + 8 E + 12 T + 192 B + 16 (P_vf + P_ee)")}
     kst = {}
-    for which, name in ((0, "k_pcg"), (1, "k_pair_blocks"), (2, "k_ccd"), (3, "k_prim_pairs")):
+    for which, (name, _, _) in names.items():
         n_, t_, b_, u_ = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
         _native.check(L.abd_kernel_stats(sc.ptr, which, C.byref(n_), C.byref(t_), C.byref(b_), C.byref(u_)))
-        kst[name] = {"launches": n_.value, "ms": t_.value, "bytes": b_.value, "units": u_.value}
+        kst[name] = {"launches": n_.value, "ms": t_.value, "bytes": b_.value, "units": u_.value,
+                     "share_of_step": t_.value / elapsed_ms if elapsed_ms else None,
+                     "achieved_gbs": (b_.value / (t_.value * 1e-3) / 1e9) if t_.value else None}
+    top = max(names, key=lambda k: kst[names[k][0]]["ms"])
+    tname, tdesc, tmodel = names[top]
     pk, pk_kind = peaks()
     hbm = float(pk.get("hbm_gbs", HBM_FALLBACK))
-    pc = kst["k_pcg"]
+    pc = kst[tname]
     achieved = (pc["bytes"] / pc["launches"]) / (pc["ms"] / pc["launches"] * 1e-3) / 1e9 if pc["launches"] else 0.0
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "pcg_dram_bytes_per_launch.json")
+    tpath = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tpath)).get(tname)
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_cg_cluster (pipelined cluster-block-Jacobi PCG, one cooperative "
-                                          "launch per Newton solve)",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm if hbm else None,
-                "traffic": traffic, "peak_source": pk_kind,
-                "bytes_model": "per PCG iteration 1152*nnzb (BSR SpMV) + 8*sum_c (12 k_c)^2 (cluster inverses) "
-                               "+ 13*96*n (vectors), summed over the launch's iterations (SURVEY 8(d) K4)",
-                "share_of_step": pc["ms"] / elapsed_ms if elapsed_ms else None,
-                "other_kernels": {k: v for k, v in kst.items() if k != "k_pcg"}}
+    roofline = {"bound": "hbm", "kernel": tdesc, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm if hbm else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": pc["bytes"] / pc["launches"] if pc["launches"] else None,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})", "bytes_model": tmodel,
+                "share_of_step": pc["share_of_step"], "kernels": kst}
 
     # e2e through the public Python API with host numpy state
     e2e = None
@@ -304,8 +319,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-        r = oracle_sample_rate({}, args.warmup, args.cpu_budget, "1 thread")
+        r = oracle_sample_rate({}, args.warmup, args.cpu_budget, "1 thread", threads=1)
         cpu = {"value": r["value"], "unit": "steps/s", "cores": 1, "kind": "port",
                "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} icospheres + "
                          f"ground, same generator) from step {args.warmup}: {r['steps']} steps in "

@@ -594,7 +594,9 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
       k.launches += 1;
       k.units += n_ov;
       k.ms += ms;
-      k.bytes += 16.0 * (double)(hc[0] + hc[1]);
+      // rest xyz, int32 edges/tris, q0+q1 per body, int4 candidate rows
+      k.bytes += 24.0 * (double)s.V + 8.0 * (double)s.E + 12.0 * (double)s.T + 192.0 * (double)s.B +
+                 16.0 * (double)(hc[0] + hc[1]);
     }
     if (hc[0] <= c.vf.cap && hc[1] <= c.ee.cap) break;
     if (hc[0] > c.vf.cap) c.vf.resize(hc[0]);
