@@ -940,26 +940,45 @@ def line_search(model, q_all, dq, ip, prm, e0=None):
 
 
 def global_min_distance(bodies, q_all):
-    """solver.py:396-473 restated as an exhaustive box-pruned search."""
+    """solver.py:396-473 restated: body pairs in ascending box-gap order with an
+    early exit once the gap reaches the best distance (solver.py:407-420);
+    primitive pairs whose box gap is already >= best are skipped (exact: the
+    box gap is a lower bound of the primitive distance)."""
     X = all_world_points(bodies, q_all)
-    best = np.inf
     n = len(bodies)
+    lo = np.array([x.min(axis=0) for x in X])
+    hi = np.array([x.max(axis=0) for x in X])
+    gaps = []
     for i in range(n):
         for j in range(i + 1, n):
             if not (bodies[i].dynamic or bodies[j].dynamic):
                 continue
-            for a, b in ((i, j), (j, i)):
-                V = X[a]
-                T = X[b][bodies[b].triangles]
-                P = np.repeat(V, len(T), axis=0)
-                TT = np.tile(T, (len(V), 1, 1))
-                d2 = pt_closest(P, TT[:, 0], TT[:, 1], TT[:, 2])[0]
+            g = np.maximum(0.0, np.maximum(lo[i] - hi[j], lo[j] - hi[i]))
+            gaps.append((float(np.linalg.norm(g)), i, j))
+    gaps.sort()
+
+    def box_gap(alo, ahi, blo, bhi):
+        g = np.maximum(0.0, np.maximum(alo - bhi, blo - ahi))
+        return np.sqrt(np.einsum("...i,...i->...", g, g))
+
+    best = np.inf
+    for gap, i, j in gaps:
+        if gap >= best:
+            break
+        for a, b in ((i, j), (j, i)):
+            V = X[a]
+            T = X[b][bodies[b].triangles]
+            g = box_gap(V[:, None, :], V[:, None, :], T.min(axis=1)[None], T.max(axis=1)[None])
+            vi, ti = np.nonzero(g < best)
+            if len(vi):
+                d2 = pt_closest(V[vi], T[ti, 0], T[ti, 1], T[ti, 2])[0]
                 best = min(best, float(np.sqrt(d2.min())))
-            Ea = X[i][bodies[i].edges]
-            Eb = X[j][bodies[j].edges]
-            A = np.repeat(Ea, len(Eb), axis=0)
-            B = np.tile(Eb, (len(Ea), 1, 1))
-            d2 = ee_closest(A[:, 0], A[:, 1], B[:, 0], B[:, 1])[0]
+        Ea = X[i][bodies[i].edges]
+        Eb = X[j][bodies[j].edges]
+        g = box_gap(Ea.min(axis=1)[:, None], Ea.max(axis=1)[:, None], Eb.min(axis=1)[None], Eb.max(axis=1)[None])
+        ei, ej = np.nonzero(g < best)
+        if len(ei):
+            d2 = ee_closest(Ea[ei, 0], Ea[ei, 1], Eb[ej, 0], Eb[ej, 1])[0]
             best = min(best, float(np.sqrt(d2.min())))
     return best
 
