@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.h"
@@ -170,19 +171,50 @@ __device__ __forceinline__ int prim_count(const PrimGeo& g, int kind, int body) 
   return o[body + 1] - o[body];
 }
 
-constexpr int BP_THREADS = 256;
-constexpr int BP_TILE = 256;
+constexpr int BP_THREADS = 512;
+constexpr int BP_TILE = 512;
+constexpr int BP_VCAP = 256;  // vertex boxes cached in shared memory per body (else on the fly)
+
+// primitive box from the body's cached vertex boxes (vb != nullptr) or recomputed
+__device__ __forceinline__ void prim_box_c(const PrimGeo& g, int kind, int body, int local, const double* vb,
+                                           double* bx) {
+  if (vb == nullptr) {
+    prim_box(g, kind, body, local, bx);
+    return;
+  }
+  const int v0 = g.v_off[body];
+  if (kind == 0) {
+    const double* s = vb + 6 * local;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) bx[k] = s[k];
+    return;
+  }
+  const int nv = kind == 1 ? 2 : 3;
+  const int* ids =
+      kind == 1 ? g.edges + 2 * (int64_t)(g.e_off[body] + local) : g.tris + 3 * (int64_t)(g.t_off[body] + local);
+  const double* s0 = vb + 6 * (ids[0] - v0);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) bx[k] = s0[k];
+  for (int m = 1; m < nv; ++m) {
+    const double* sm = vb + 6 * (ids[m] - v0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      bx[k] = fmin(bx[k], sm[k]);
+      bx[3 + k] = fmax(bx[3 + k], sm[3 + k]);
+    }
+  }
+}
 
 // block-wide cull of primitives [start, start+TILE) of (kind, body) against the
 // overlap box into shared lists; returns the culled count
-__device__ int cull_tile(const PrimGeo& g, int kind, int body, int start, int count, const double* obox, int* ids,
-                         double* boxes, int* warp_tot) {
+__device__ int cull_tile(const PrimGeo& g, int kind, int body, int start, int count, const double* obox,
+                         const double* vb, int* ids, double* boxes, int* warp_tot) {
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int local = start + threadIdx.x;
   bool keep = false;
   double bx[6];
   if (threadIdx.x < BP_TILE && local < count) {
-    prim_box(g, kind, body, local, bx);
+    prim_box_c(g, kind, body, local, vb, bx);
     keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] && bx[2] <= obox[5] &&
            obox[2] <= bx[5];
   }
@@ -203,13 +235,21 @@ __device__ int cull_tile(const PrimGeo& g, int kind, int body, int start, int co
   return total;
 }
 
-// one CTA per overlapping body pair
+constexpr size_t BP_SMEM = sizeof(double) * (2 * 6 * BP_VCAP + 2 * 6 * BP_TILE) + sizeof(int) * 2 * BP_TILE;
+
+// one CTA per overlapping body pair; the vertex boxes of both bodies are computed
+// once per pair into shared memory (edge / triangle boxes are their min/max)
 __global__ void __launch_bounds__(BP_THREADS) k_prim_pairs(PrimGeo g, int64_t n_ov, const int2* __restrict__ ov,
                                                              const double* __restrict__ bbox,
                                                              unsigned long long* counters, int64_t cap_vf,
                                                              int64_t cap_ee, int4* out_vf, int4* out_ee) {
-  __shared__ int ida[BP_TILE], idb[BP_TILE];
-  __shared__ double bxa[6 * BP_TILE], bxb[6 * BP_TILE];
+  extern __shared__ double bp_sm[];
+  double* vbi = bp_sm;                      // BP_VCAP x 6
+  double* vbj = vbi + 6 * BP_VCAP;          // BP_VCAP x 6
+  double* bxa = vbj + 6 * BP_VCAP;          // BP_TILE x 6
+  double* bxb = bxa + 6 * BP_TILE;          // BP_TILE x 6
+  int* ida = reinterpret_cast<int*>(bxb + 6 * BP_TILE);
+  int* idb = ida + BP_TILE;
   __shared__ int warp_tot[BP_THREADS / 32];
   __shared__ double obox[6];
   for (int64_t pi = blockIdx.x; pi < n_ov; pi += gridDim.x) {
@@ -219,41 +259,70 @@ __global__ void __launch_bounds__(BP_THREADS) k_prim_pairs(PrimGeo g, int64_t n_
       obox[threadIdx.x] = fmax(bbox[6 * i + threadIdx.x], bbox[6 * j + threadIdx.x]);
       obox[3 + threadIdx.x] = fmin(bbox[6 * i + 3 + threadIdx.x], bbox[6 * j + 3 + threadIdx.x]);
     }
+    const int nvi = prim_count(g, 0, i), nvj = prim_count(g, 0, j);
+    const bool ci = nvi <= BP_VCAP, cj = nvj <= BP_VCAP;
+    for (int t = threadIdx.x; t < 2 * BP_VCAP; t += BP_THREADS) {
+      const int side = t / BP_VCAP, lv = t % BP_VCAP;
+      const int body = side ? j : i;
+      if ((side ? cj : ci) && lv < (side ? nvj : nvi)) {
+        double* o = (side ? vbj : vbi) + 6 * lv;
+        vertex_box(g.rest, g.v_off[body] + lv, g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h, o);
+      }
+    }
     __syncthreads();
     // products: (vertex of i, tri of j) -> vf(i,.,j,.); (vertex of j, tri of i) -> vf(j,.,i,.); (edge i, edge j)
     for (int prod = 0; prod < 3; ++prod) {
       int ka = prod == 2 ? 1 : 0, kb = prod == 2 ? 1 : 2;
       int ba = prod == 1 ? j : i, bb = prod == 1 ? i : j;
+      const double* vba = (prod == 1 ? cj : ci) ? (prod == 1 ? vbj : vbi) : nullptr;
+      const double* vbb = (prod == 1 ? ci : cj) ? (prod == 1 ? vbi : vbj) : nullptr;
       int na = prim_count(g, ka, ba), nb = prim_count(g, kb, bb);
       bool is_vf = prod < 2;
       for (int sa = 0; sa < na; sa += BP_TILE) {
-        int ca = cull_tile(g, ka, ba, sa, na, obox, ida, bxa, warp_tot);
+        int ca = cull_tile(g, ka, ba, sa, na, obox, vba, ida, bxa, warp_tot);
         if (ca == 0) continue;
         for (int sb = 0; sb < nb; sb += BP_TILE) {
-          int cb = cull_tile(g, kb, bb, sb, nb, obox, idb, bxb, warp_tot);
+          int cb = cull_tile(g, kb, bb, sb, nb, obox, vbb, idb, bxb, warp_tot);
           if (cb == 0) continue;
-          int64_t tot = (int64_t)ca * cb;
-          for (int64_t k0 = 0; k0 < tot; k0 += BP_THREADS) {
-            int64_t k = k0 + threadIdx.x;
-            bool hit = false;
-            int x = 0, y = 0;
-            if (k < tot) {
-              x = (int)(k / cb);
-              y = (int)(k % cb);
-              hit = box_overlap(bxa + 6 * x, bxb + 6 * y);
-            }
-            unsigned m = __ballot_sync(0xffffffffu, hit);
-            if (m) {
-              int lane = threadIdx.x & 31;
-              unsigned long long base = 0;
-              if (lane == __ffs(m) - 1) base = atomicAdd(counters + (is_vf ? 0 : 1), (unsigned long long)__popc(m));
-              base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-              if (hit) {
-                unsigned long long at = base + __popc(m & ((1u << lane) - 1));
-                if (is_vf) {
-                  if ((int64_t)at < cap_vf) out_vf[at] = make_int4(ba, ida[x], bb, idb[y]);
-                } else {
-                  if ((int64_t)at < cap_ee) out_ee[at] = make_int4(ba, ida[x], bb, idb[y]);
+          // each thread keeps one box of the larger side in registers and sweeps a
+          // chunk of the other side (same smem address across the warp: broadcast)
+          const bool a_thr = ca >= cb;
+          const int nt = a_thr ? ca : cb, nl = a_thr ? cb : ca;
+          const int G = nt >= BP_THREADS ? 1 : BP_THREADS / nt;
+          const int Lc = (nl + G - 1) / G;
+          const double* own_box = a_thr ? bxa : bxb;
+          const double* oth_box = a_thr ? bxb : bxa;
+          for (int base = 0; base < nt * G; base += BP_THREADS) {
+            const int idx = base + threadIdx.x;
+            const int own = idx % nt, chunk = idx / nt;
+            const bool live = idx < nt * G;
+            double ob[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) ob[k] = live ? own_box[6 * own + k] : 0.0;
+            const int y0 = chunk * Lc;
+            for (int yy = 0; yy < Lc; ++yy) {
+              const int y = y0 + yy;
+              bool hit = false;
+              if (live && y < nl) {
+                const double* b2 = oth_box + 6 * y;
+                hit = ob[0] <= b2[3] && b2[0] <= ob[3] && ob[1] <= b2[4] && b2[1] <= ob[4] && ob[2] <= b2[5] &&
+                      b2[2] <= ob[5];
+              }
+              unsigned m = __ballot_sync(0xffffffffu, hit);
+              if (m) {
+                int lane = threadIdx.x & 31;
+                unsigned long long base2 = 0;
+                if (lane == __ffs(m) - 1)
+                  base2 = atomicAdd(counters + (is_vf ? 0 : 1), (unsigned long long)__popc(m));
+                base2 = __shfl_sync(0xffffffffu, base2, __ffs(m) - 1);
+                if (hit) {
+                  unsigned long long at = base2 + __popc(m & ((1u << lane) - 1));
+                  const int x = a_thr ? own : y, yb = a_thr ? y : own;
+                  if (is_vf) {
+                    if ((int64_t)at < cap_vf) out_vf[at] = make_int4(ba, ida[x], bb, idb[yb]);
+                  } else {
+                    if ((int64_t)at < cap_ee) out_ee[at] = make_int4(ba, ida[x], bb, idb[yb]);
+                  }
                 }
               }
             }
@@ -263,6 +332,208 @@ __global__ void __launch_bounds__(BP_THREADS) k_prim_pairs(PrimGeo g, int64_t n_
       }
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_prim_pairs2: one CTA per overlapping body pair, few barriers per pair.
+//   1. per-pair metadata (offsets, counts, overlap box) and the vertex boxes of
+//      both bodies into shared memory;
+//   2. ONE pass culls all six primitive lists (verts/edges/tris of i and j)
+//      against the overlap box into shared id lists (smem atomics; the final
+//      canonical sort makes the output order deterministic);
+//   3. per product (VF i->j, VF j->i, EE): the larger side stays in registers
+//      (one box per thread), the other side's boxes are materialised once in
+//      shared memory and swept with broadcast reads.
+// Requires max_v <= P2_VCAP; larger meshes use k_prim_pairs.
+constexpr int P2_THREADS = 256;
+constexpr int P2_VCAP = 256;
+
+// box of a primitive from packed local vertex ids (8 bits each, P2_VCAP = 256)
+__device__ __forceinline__ void box_from_packed(int kind, unsigned pk, const double* vb, double* bx) {
+  const double* s0 = vb + 6 * (pk & 0xffu);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) bx[k] = s0[k];
+  const int nv = kind == 0 ? 1 : (kind == 1 ? 2 : 3);
+  for (int m = 1; m < nv; ++m) {
+    const double* sm = vb + 6 * ((pk >> (8 * m)) & 0xffu);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      bx[k] = fmin(bx[k], sm[k]);
+      bx[3 + k] = fmax(bx[3 + k], sm[3 + k]);
+    }
+  }
+}
+
+__device__ __forceinline__ void box_from_cache(const PrimGeo& g, int kind, int gid, int v0, const double* vb,
+                                               double* bx) {
+  if (kind == 0) {
+    const double* s0 = vb + 6 * (gid - v0);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) bx[k] = s0[k];
+    return;
+  }
+  const int nv = kind == 1 ? 2 : 3;
+  const int* ids = kind == 1 ? g.edges + 2 * (int64_t)gid : g.tris + 3 * (int64_t)gid;
+  const double* s0 = vb + 6 * (ids[0] - v0);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) bx[k] = s0[k];
+  for (int m = 1; m < nv; ++m) {
+    const double* sm = vb + 6 * (ids[m] - v0);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      bx[k] = fmin(bx[k], sm[k]);
+      bx[3 + k] = fmax(bx[3 + k], sm[3 + k]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(P2_THREADS, 3)
+    k_prim_pairs2(PrimGeo g, int64_t n_ov, const int2* __restrict__ ov, const double* __restrict__ bbox,
+                  unsigned long long* counters, int64_t cap_vf, int64_t cap_ee, int4* out_vf, int4* out_ee,
+                  int cap_list) {
+  extern __shared__ double p2_sm[];
+  double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
+  double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
+  int* lists = reinterpret_cast<int*>(obx + 6 * (size_t)cap_list);  // [6][cap_list] local ids
+  unsigned* lpk = reinterpret_cast<unsigned*>(lists + 6 * (size_t)cap_list);  // packed local vertex ids
+  __shared__ int meta[16];  // v0,e0,t0 (i) | v0,e0,t0 (j) | nv,ne,nt (i) | nv,ne,nt (j)
+  __shared__ int lcount[6];
+  __shared__ double obox[6];
+  for (int64_t pi = blockIdx.x; pi < n_ov; pi += gridDim.x) {
+    const int2 pr = ov[pi];
+    const int bi = pr.x, bj = pr.y;
+    if (threadIdx.x < 6) {
+      const int side = threadIdx.x / 3, kind = threadIdx.x % 3;
+      const int body = side ? bj : bi;
+      const int* o = kind == 0 ? g.v_off : (kind == 1 ? g.e_off : g.t_off);
+      const int a = o[body], b = o[body + 1];
+      meta[3 * side + kind] = a;
+      meta[6 + 3 * side + kind] = b - a;
+      lcount[threadIdx.x] = 0;
+    } else if (threadIdx.x >= 32 && threadIdx.x < 35) {
+      const int k = threadIdx.x - 32;
+      obox[k] = fmax(bbox[6 * bi + k], bbox[6 * bj + k]);
+      obox[3 + k] = fmin(bbox[6 * bi + 3 + k], bbox[6 * bj + 3 + k]);
+    }
+    __syncthreads();
+    // vertex boxes of both bodies
+    for (int t = threadIdx.x; t < 2 * P2_VCAP; t += P2_THREADS) {
+      const int side = t / P2_VCAP, lv = t % P2_VCAP;
+      if (lv < meta[6 + 3 * side]) {
+        const int body = side ? bj : bi;
+        vertex_box(g.rest, meta[3 * side] + lv, g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h,
+                   vb + 6 * (side * P2_VCAP + lv));
+      }
+    }
+    __syncthreads();
+    // one cull pass over the six lists (list id = 3 * side + kind); topology is
+    // prefetched 4 primitives per thread, survivors keep id + packed local vertex ids
+    {
+      const int tot = meta[6] + meta[7] + meta[8] + meta[9] + meta[10] + meta[11];
+      for (int t0 = threadIdx.x; t0 < tot; t0 += 4 * P2_THREADS) {
+        unsigned pk[4];
+        int lst[4], loc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int t = t0 + u * P2_THREADS;
+          lst[u] = -1;
+          loc[u] = 0;
+          pk[u] = 0;
+          if (t < tot) {
+            int l = 0, r = t;
+            while (r >= meta[6 + l]) {
+              r -= meta[6 + l];
+              ++l;
+            }
+            const int side = l / 3, kind = l % 3, v0 = meta[3 * side];
+            lst[u] = l;
+            loc[u] = r;
+            if (kind == 0) {
+              pk[u] = (unsigned)r;
+            } else if (kind == 1) {
+              const int2 e = *reinterpret_cast<const int2*>(g.edges + 2 * (int64_t)(meta[l] + r));
+              pk[u] = (unsigned)(e.x - v0) | ((unsigned)(e.y - v0) << 8);
+            } else {
+              const int* tr = g.tris + 3 * (int64_t)(meta[l] + r);
+              pk[u] = (unsigned)(tr[0] - v0) | ((unsigned)(tr[1] - v0) << 8) | ((unsigned)(tr[2] - v0) << 16);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (lst[u] < 0) continue;
+          const int l = lst[u], side = l / 3, kind = l % 3;
+          double bx[6];
+          box_from_packed(kind, pk[u], vb + 6 * side * P2_VCAP, bx);
+          const bool keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] &&
+                            bx[2] <= obox[5] && obox[2] <= bx[5];
+          if (keep) {
+            const int at = atomicAdd(&lcount[l], 1);
+            lists[l * cap_list + at] = loc[u];
+            lpk[l * cap_list + at] = pk[u];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // products: (verts i, tris j) -> vf(i,.,j,.); (verts j, tris i) -> vf(j,.,i,.); (edges i, edges j)
+    for (int prod = 0; prod < 3; ++prod) {
+      const int la = prod == 0 ? 0 : (prod == 1 ? 3 : 1);  // list of side a
+      const int lb = prod == 0 ? 5 : (prod == 1 ? 2 : 4);  // list of side b
+      const int ca = lcount[la], cb = lcount[lb];
+      if (ca == 0 || cb == 0) continue;  // uniform across the CTA
+      const int ka = la % 3, kb = lb % 3, sa = la / 3, sb = lb / 3;
+      const bool a_thr = ca >= cb;  // thread side = a
+      const int nt = a_thr ? ca : cb, nl = a_thr ? cb : ca;
+      const int lt = a_thr ? la : lb, ll = a_thr ? lb : la;
+      const int kt = a_thr ? ka : kb, kl = a_thr ? kb : ka;
+      const int st_ = a_thr ? sa : sb, sl = a_thr ? sb : sa;
+      // materialise the loop side's boxes
+      for (int t = threadIdx.x; t < nl; t += P2_THREADS)
+        box_from_packed(kl, lpk[ll * cap_list + t], vb + 6 * sl * P2_VCAP, obx + 6 * t);
+      __syncthreads();
+      const bool is_vf = prod < 2;
+      const int body_a = prod == 1 ? bj : bi, body_b = prod == 1 ? bi : bj;
+      const int G = nt >= P2_THREADS ? 1 : P2_THREADS / nt;
+      const int Lc = (nl + G - 1) / G;
+      for (int base = 0; base < nt * G; base += P2_THREADS) {
+        const int idx = base + threadIdx.x;
+        const bool live = idx < nt * G;
+        const int own = live ? idx % nt : 0, chunk = idx / nt;
+        double ob[6];
+        const int own_local = live ? lists[lt * cap_list + own] : 0;
+        if (live) box_from_packed(kt, lpk[lt * cap_list + own], vb + 6 * st_ * P2_VCAP, ob);
+        const int y0 = chunk * Lc;
+        for (int yy = 0; yy < Lc; ++yy) {
+          const int y = y0 + yy;
+          bool hit = false;
+          if (live && y < nl) {
+            const double* b2 = obx + 6 * y;
+            hit = ob[0] <= b2[3] && b2[0] <= ob[3] && ob[1] <= b2[4] && b2[1] <= ob[4] && ob[2] <= b2[5] &&
+                  b2[2] <= ob[5];
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (m) {
+            const int lane = threadIdx.x & 31;
+            unsigned long long base2 = 0;
+            if (lane == __ffs(m) - 1) base2 = atomicAdd(counters + (is_vf ? 0 : 1), (unsigned long long)__popc(m));
+            base2 = __shfl_sync(0xffffffffu, base2, __ffs(m) - 1);
+            if (hit) {
+              const unsigned long long at = base2 + __popc(m & ((1u << lane) - 1));
+              const int yl = lists[ll * cap_list + y];
+              const int pa = a_thr ? own_local : yl, pb = a_thr ? yl : own_local;
+              if (is_vf) {
+                if ((int64_t)at < cap_vf) out_vf[at] = make_int4(body_a, pa, body_b, pb);
+              } else {
+                if ((int64_t)at < cap_ee) out_ee[at] = make_int4(body_a, pa, body_b, pb);
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -396,6 +667,67 @@ __global__ void k_cell_keys(int B, const double* __restrict__ bbox, const uint32
   keys[b] = cell_key((long long)floor(x[0] / cell), (long long)floor(x[1] / cell), (long long)floor(x[2] / cell));
 }
 
+// cell size in one CTA: median of up to 2048 strided extent samples (bitonic
+// sort in shared memory), then the largest extent <= 4x that median, next float
+// up (outliers such as ground slabs and walls become "large").  The cell only
+// steers the binning; overlap decisions are exact box tests.
+__global__ void __launch_bounds__(1024) k_cell_size(int B, const uint32_t* __restrict__ ext, double* cell_out) {
+  __shared__ uint32_t sk[2048];
+  __shared__ uint32_t red[32];
+  const int ns = min(B, 2048);
+  for (int t = threadIdx.x; t < 2048; t += 1024)
+    sk[t] = t < ns ? ext[(int64_t)t * B / ns] : 0xffffffffu;
+  __syncthreads();
+  for (int k = 2; k <= 2048; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < 2048; t += 1024) {
+        int u = t ^ j;
+        if (u > t) {
+          bool up = (t & k) == 0;
+          uint32_t a = sk[t], b = sk[u];
+          if ((a > b) == up) {
+            sk[t] = b;
+            sk[u] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  const uint32_t lim = __float_as_uint(4.0f * __uint_as_float(sk[(ns - 1) / 2]));
+  uint32_t best = 0;
+  for (int b = threadIdx.x; b < B; b += 1024) {
+    uint32_t e = ext[b];
+    if (e <= lim && e > best) best = e;
+  }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = red[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (threadIdx.x == 0) {
+      double cell = (double)__uint_as_float(best + 1u);
+      if (!(cell > 0.0)) cell = 1.0;
+      *cell_out = cell;
+    }
+  }
+}
+
+__global__ void k_cell_keys2(int B, const double* __restrict__ bbox, const double* __restrict__ cell_p,
+                             uint32_t* keys, int* vals) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double cell = *cell_p;
+  const double* x = bbox + 6 * b;
+  double e = fmax(fmax(x[3] - x[0], x[4] - x[1]), x[5] - x[2]);
+  vals[b] = b;
+  if (e > cell) {
+    keys[b] = 0xffffffffu;  // large: not binned
+    return;
+  }
+  keys[b] = cell_key((long long)floor(x[0] / cell), (long long)floor(x[1] / cell), (long long)floor(x[2] / cell));
+}
+
 __device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t k) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -406,21 +738,18 @@ __device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_
   return lo;
 }
 
-// one thread per body: emit (min, max) overlapping pairs exactly once
+// one thread per (body, x column of cells): emit (min, max) overlapping pairs
+// exactly once (an overlapping body's low corner lies in exactly one cell)
+constexpr int GP_COLS = 4;  // x columns per body: floor(hi/c) - floor(lo/c - 1 - eps) <= 3 for extent <= c
 __global__ void k_grid_pairs(int B, const double* __restrict__ bbox, const unsigned char* __restrict__ dyn,
                              const uint32_t* __restrict__ skeys, const int* __restrict__ sbody, int n_small,
                              const double* __restrict__ cell_p, unsigned long long* count, int64_t cap, int2* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= B) return;
+  const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (item >= (int64_t)B * GP_COLS) return;
+  const int i = (int)(item / GP_COLS), dxc = (int)(item % GP_COLS);
   const double cell = *cell_p;
   const double* a = bbox + 6 * i;
   double e = fmax(fmax(a[3] - a[0], a[4] - a[1]), a[5] - a[2]);
-  auto emit = [&](int j) {
-    if (!(dyn[i] || dyn[j])) return;
-    if (!box_overlap(a, bbox + 6 * j)) return;
-    unsigned long long at = atomicAdd(count, 1ull);
-    if ((int64_t)at < cap) out[at] = make_int2(min(i, j), max(i, j));
-  };
   // pairs involving a large body come from k_large_pairs
   if (e > cell) return;
   // an overlapping small body has lo_j in [lo_i - cell, hi_i]; floor(lo/cell) is
@@ -428,16 +757,29 @@ __global__ void k_grid_pairs(int B, const double* __restrict__ bbox, const unsig
   long long x0 = (long long)floor(a[0] / cell - 1.0 - 1e-9), x1 = (long long)floor(a[3] / cell);
   long long y0 = (long long)floor(a[1] / cell - 1.0 - 1e-9), y1 = (long long)floor(a[4] / cell);
   long long z0 = (long long)floor(a[2] / cell - 1.0 - 1e-9), z1 = (long long)floor(a[5] / cell);
-  for (long long cx = x0; cx <= x1; ++cx)
-    for (long long cy = y0; cy <= y1; ++cy)
-      for (long long cz = z0; cz <= z1; ++cz) {
-        uint32_t k = cell_key(cx, cy, cz);
-        int p = lower_bound_u32(skeys, n_small, k);
-        for (; p < n_small && skeys[p] == k; ++p) {
-          int j = sbody[p];
-          if (j > i) emit(j);  // small-small pairs once, from the lower index
+  const long long cx = x0 + dxc;
+  const bool last = dxc == GP_COLS - 1;
+  if (cx > x1) return;
+  const long long cx_end = last ? x1 : cx;  // (never more than GP_COLS columns; kept exact)
+  const unsigned char di = dyn[i];
+  for (long long xx = cx; xx <= cx_end; ++xx)
+    for (long long cy = y0; cy <= y1; ++cy) {
+      // z is the fastest key field: one search per (x, y) column unless z wraps
+      const uint32_t k0 = cell_key(xx, cy, z0), k1 = cell_key(xx, cy, z1);
+      const bool contiguous = k1 - k0 == (uint32_t)(z1 - z0);
+      for (long long cz = z0; cz <= (contiguous ? z0 : z1); ++cz) {
+        const uint32_t lo = contiguous ? k0 : cell_key(xx, cy, cz), hi = contiguous ? k1 : lo;
+        int p = lower_bound_u32(skeys, n_small, lo);
+        for (; p < n_small && skeys[p] <= hi; ++p) {
+          const int j = sbody[p];
+          if (j <= i) continue;  // small-small pairs once, from the lower index
+          if (!(di || dyn[j])) continue;
+          if (!box_overlap(a, bbox + 6 * j)) continue;
+          unsigned long long at = atomicAdd(count, 1ull);
+          if ((int64_t)at < cap) out[at] = make_int2(i, j);
         }
       }
+    }
 }
 
 // every (large body, body) pair: thread per body j over the few large bodies
@@ -517,20 +859,12 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   w.vb.resize(s.B + 1);
   w.ka.resize(s.B);
   w.kb.resize(s.B);
-  uint32_t* ext_sorted = reinterpret_cast<uint32_t*>(w.e0.p);
-  w.e0.resize(s.B);
   k_extent_keys<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.ka.p);
   note_launch("k_extent_keys");
-  ext_sorted = reinterpret_cast<uint32_t*>(w.e0.p);
-  {
-    size_t bytes = 0;
-    CK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, w.ka.p, ext_sorted, s.B, 0, 32, st));
-    s.tmp_bytes.resize(bytes);
-    CK(cub::DeviceRadixSort::SortKeys(s.tmp_bytes.p, bytes, w.ka.p, ext_sorted, s.B, 0, 32, st));
-  }
   w.scal.resize(4);
-  int pct = (int)((int64_t)(s.B - 1) * 9 / 10);
-  k_cell_keys<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, ext_sorted, pct, w.ka.p, w.va.p, w.scal.p);
+  k_cell_size<<<1, 1024, 0, st>>>(s.B, w.ka.p, w.scal.p);
+  note_launch("k_cell_size");
+  k_cell_keys2<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.scal.p, w.ka.p, w.va.p);
   note_launch("k_cell_keys");
   sort_pairs_u32(s, w.ka.p, w.kb.p, w.va.p, w.vb.p, s.B, 32, alt);
   const uint32_t* skeys = alt ? w.kb.p : w.ka.p;
@@ -541,7 +875,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   if (c.ov.cap < 256) c.ov.resize(256);
   for (int attempt = 0; attempt < 3; ++attempt) {
     CK(cudaMemsetAsync(ovc, 0, sizeof(unsigned long long), st));
-    k_grid_pairs<<<grid_for(s.B, 128), 128, 0, st>>>(s.B, s.bbox.p, s.dyn.p, skeys, sbody, n_small, w.scal.p, ovc,
+    k_grid_pairs<<<grid_for((int64_t)s.B * GP_COLS, 128), 128, 0, st>>>(s.B, s.bbox.p, s.dyn.p, skeys, sbody, n_small, w.scal.p, ovc,
                                                      (int64_t)c.ov.cap, c.ov.p);
     note_launch("k_grid_pairs");
     k_large_pairs<<<grid_for(s.B, 128), 128, 0, st>>>(s.B, s.bbox.p, s.dyn.p, skeys, sbody, w.scal.p, ovc,
@@ -579,10 +913,26 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   unsigned long long* hc = reinterpret_cast<unsigned long long*>(s.h_pinned);
   for (int attempt = 0; attempt < 3; ++attempt) {
     CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
-    int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 8);
+    static bool attr = false;
+    const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
+    const size_t p2_smem =
+        sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) + 2 * sizeof(int) * 6 * (size_t)cap_list;
+    const bool use2 = s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1");
+    if (!attr) {
+      CK(cudaFuncSetAttribute((void*)k_prim_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM));
+      CK(cudaFuncSetAttribute((void*)k_prim_pairs2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      attr = true;
+    }
     if (s.instrument) CK(cudaEventRecord(s.ev0, st));
-    k_prim_pairs<<<grid, BP_THREADS, 0, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
-                                              (int64_t)c.ee.cap, c.vf.p, c.ee.p);
+    if (use2) {
+      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 3);
+      k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
+                                                       (int64_t)c.ee.cap, c.vf.p, c.ee.p, cap_list);
+    } else {
+      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
+      k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
+                                                      (int64_t)c.ee.cap, c.vf.p, c.ee.p);
+    }
     note_launch("k_prim_pairs");
     if (s.instrument) CK(cudaEventRecord(s.ev1, st));
     CK(cudaMemcpyAsync(hc, counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));

@@ -9,12 +9,15 @@
 //     tree and its levels are built, and connected components are packed onto
 //     CTAs.  Contact graphs of piles are forests of short chains, so the fill
 //     is ~0 and the tree height is tens of levels.
-//   * factor (k_chol_factor): one CTA walks the levels of its components with
+//   * factor + solve (k_chol_factor_solve): one CTA walks the levels of its components with
 //     __syncthreads between levels; a half-warp (lane t = row t) owns one node:
 //     D = A_jj - sum_k L_jk L_jk^T, 12x12 Cholesky, then L_ij = (A_ij -
 //     sum_k L_ik L_jk^T) L_jj^-T for every block of the column.  Left-looking
 //     with fixed update order: deterministic, no atomics.
-//   * solve (k_chol_solve): forward levels ascending, backward descending.
+//     The forward substitution of node j runs right after its factor; the
+//     backward sweep follows in the same kernel (levels descending).  The
+//     12x12 pivots are in-register Cholesky factors (shuffles, rsqrt per pivot).
+//   * refinement solves (k_chol_solve) reuse the factor and 1 / L_cc.
 //   * refinement exactly as solve_refined: r = b - A x over the resident BSR,
 //     stop when |r| <= rel_tol |b|, at most 3 corrections.
 // A failed pivot raises ABD_ERR_FACTORIZATION with the smallest failing
@@ -55,209 +58,294 @@ struct CholView {
   const int* diag_pos;  // BSR diagonal block positions
   const double* val;    // BSR values
   double* L;            // L blocks, 144 doubles each (row-major)
+  double* dinv;         // n x 12: 1 / L_jj[c][c]
   int* bad;
 };
 
 __device__ __forceinline__ unsigned half_mask(int half) { return 0xffffu << (16 * half); }
 
-__global__ void __launch_bounds__(CH_THREADS) k_chol_factor(CholView v) {
-  __shared__ double Ss[CH_HW][12][13];
+__device__ __forceinline__ double hshfl(unsigned mask, double v, int src) { return __shfl_sync(mask, v, src, 16); }
+
+// 1/sqrt(x) without the libdevice slow-path call (whose register saves would put
+// the in-register factor on the stack): MUFU seed + 3 Newton steps (>= 53 bits)
+// for pivots in [1e-36, 1e36]; others take the exact division path.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  if (!(x > 1e-36 && x < 1e36)) return 1.0 / sqrt(x);
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x, r * r, 1.5);
+  r = r * fma(-0.5 * x, r * r, 1.5);
+  r = r * fma(-0.5 * x, r * r, 1.5);
+  return r;
+}
+
+// In-register 12x12 Cholesky on a 16-lane group: lane t < 12 holds row t of the
+// symmetric matrix in d[]; on exit d[] is row t of L (zeros above the diagonal)
+// and every lane holds rinv[c] = 1 / L_cc.  Division-free (rsqrt per pivot).
+__device__ __forceinline__ bool chol12(unsigned mask, int t, double d[12], double rinv[12]) {
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    const double p = hshfl(mask, d[c], c);
+    ok = ok && (p > 0.0);
+    const double pp = p > 0.0 ? p : 1.0;
+    const double r = rsqrt_nr(pp);
+    rinv[c] = r;
+    if (t == c) d[c] = pp * r;
+    else if (t > c) d[c] *= r;
+#pragma unroll
+    for (int k = c + 1; k < 12; ++k) {
+      const double lkc = hshfl(mask, d[c], k);
+      if (t >= k) d[k] = fma(-d[c], lkc, d[k]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 12; ++c)
+    if (c > t) d[c] = 0.0;
+  return ok;
+}
+
+// lane t: acc <- row t of (L^-1 acc) for lower-triangular L whose row t is lrow
+__device__ __forceinline__ double lower_solve12(unsigned mask, int t, double acc, const double lrow[12],
+                                                const double rinv[12]) {
+  double y = 0.0;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    const double yc = hshfl(mask, acc, c) * rinv[c];
+    if (t == c) y = yc;
+    if (t > c) acc = fma(-lrow[c], yc, acc);
+  }
+  return y;
+}
+
+// lane t: row t of (L^-T acc); lcol = column t of L (lcol[c] = L[c][t])
+__device__ __forceinline__ double upper_solve12(unsigned mask, int t, double acc, const double lcol[12],
+                                                const double rinv[12]) {
+  double x = 0.0;
+#pragma unroll
+  for (int c = 11; c >= 0; --c) {
+    const double xc = hshfl(mask, acc, c) * rinv[c];
+    if (t == c) x = xc;
+    if (t < c) acc = fma(-lcol[c], xc, acc);
+  }
+  return x;
+}
+
+// Factor + forward substitution (levels ascending), then backward substitution
+// (levels descending), one CTA per group of components.  x receives y, then x.
+__global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, const double* __restrict__ b,
+                                                                   double* x) {
+  __shared__ double Ss[CH_HW][12][13];  // per half-warp: staged L_jk / symmetrisation / L_jj
+  __shared__ double Ts[CH_HW][12][13];  // per half-warp: staged L_jk of update pairs
   const int hw = threadIdx.x >> 4, t = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
+  const int tt = t < 12 ? t : 0;
   const unsigned mask = half_mask(half);
   double (*S)[13] = Ss[hw];
+  double (*T)[13] = Ts[hw];
   const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
   for (int l = 0; l < nl; ++l) {
     const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
     for (int idx = lo + hw; idx < hi; idx += CH_HW) {
       const int j = v.nodes[idx];
-      const int dblk = j;
-      // D = A_jj - sum_k L_jk L_jk^T (row t), then symmetrised (sparse.py:117)
       double d[12];
-      if (t < 12) {
-        const double* A = v.val + 144 * (int64_t)v.diag_pos[j] + 12 * t;
+      {
+        const double* A = v.val + 144 * (int64_t)v.diag_pos[j] + 12 * tt;
 #pragma unroll
         for (int c = 0; c < 12; ++c) d[c] = A[c];
-        for (int e = v.row_ptr[j]; e < v.row_ptr[j + 1]; ++e) {
-          const double* Lk = v.L + 144 * (int64_t)v.row_blk[e];
-          double lr[12];
+      }
+      double acc = b[12 * (int64_t)j + tt];
+      // D = A_jj - sum_k L_jk L_jk^T and b_j - sum_k L_jk y_k over the row list of j
+      for (int e = v.row_ptr[j]; e < v.row_ptr[j + 1]; ++e) {
+        const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
+        const double* yk = x + 12 * (int64_t)v.row_col[e];
+        double lr[12];
 #pragma unroll
-          for (int m = 0; m < 12; ++m) lr[m] = Lk[12 * t + m];
+        for (int m = 0; m < 12; ++m) lr[m] = Lk[m];
+        __syncwarp(mask);
+        if (t < 12) {
 #pragma unroll
-          for (int c = 0; c < 12; ++c) {
-            double s = 0.0;
-#pragma unroll
-            for (int m = 0; m < 12; ++m) s = fma(lr[m], Lk[12 * c + m], s);
-            d[c] -= s;
-          }
+          for (int m = 0; m < 12; ++m) S[t][m] = lr[m];
         }
+        __syncwarp(mask);
+        double s2 = 0.0;
+#pragma unroll
+        for (int m = 0; m < 12; ++m) s2 = fma(lr[m], yk[m], s2);
+        acc -= s2;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < 12; ++m) s = fma(lr[m], S[c][m], s);
+          d[c] -= s;
+        }
+      }
+      // symmetrise (sparse.py:117: cholesky(0.5 (D + D^T)))
+      __syncwarp(mask);
+      if (t < 12) {
 #pragma unroll
         for (int c = 0; c < 12; ++c) S[t][c] = d[c];
       }
       __syncwarp(mask);
-      double e[12];
-      if (t < 12) {
 #pragma unroll
-        for (int c = 0; c < 12; ++c) e[c] = S[c][t];
-      }
-      __syncwarp(mask);
-      if (t < 12) {
-#pragma unroll
-        for (int c = 0; c < 12; ++c) S[t][c] = 0.5 * (d[c] + e[c]);
-      }
-      __syncwarp(mask);
-      // right-looking 12x12 Cholesky, lane t owns row t
-      bool ok = true;
-      for (int c = 0; c < 12; ++c) {
-        double p = S[c][c];
-        ok = ok && (p > 0.0);
-        double sp = sqrt(fmax(p, 1e-300));
-        __syncwarp(mask);
-        if (t > c && t < 12) S[t][c] /= sp;
-        if (t == c) S[c][c] = sp;
-        __syncwarp(mask);
-        if (t > c && t < 12) {
-          double ltc = S[t][c];
-          for (int k = c + 1; k <= t; ++k) S[t][k] -= ltc * S[k][c];
-        }
-        __syncwarp(mask);
-      }
+      for (int c = 0; c < 12; ++c) d[c] = 0.5 * (d[c] + S[c][tt]);
+      double rinv[12];
+      const bool ok = chol12(mask, t, d, rinv);
       if (!ok && t == 0) atomicMin(v.bad, j);
-      double lrow[12];
+      __syncwarp(mask);
       if (t < 12) {
-        double* Ld = v.L + 144 * (int64_t)dblk + 12 * t;
+        double* Ld = v.L + 144 * (int64_t)j + 12 * t;
 #pragma unroll
         for (int c = 0; c < 12; ++c) {
-          lrow[c] = c <= t ? S[t][c] : 0.0;
-          Ld[c] = lrow[c];
+          Ld[c] = d[c];
+          S[t][c] = d[c];  // L_jj rows for the off-diagonal solves below
         }
+        double mine = rinv[0];
+#pragma unroll
+        for (int c = 1; c < 12; ++c)
+          if (c == t) mine = rinv[c];
+        v.dinv[12 * (int64_t)j + t] = mine;
       }
+      // forward substitution for node j
+      const double y = lower_solve12(mask, t, acc, d, rinv);
+      if (t < 12) x[12 * (int64_t)j + t] = y;
+      __syncwarp(mask);
       // off-diagonal blocks of column j: L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
-      for (int b = v.col_ptr[j]; b < v.col_ptr[j + 1]; ++b) {
-        const int blk = v.n + b;
-        if (t < 12) {
-          double bt[12];
-          const int ap = v.blk_apos[b];
-          if (ap >= 0) {
-            const double* A = v.val + 144 * (int64_t)ap + 12 * t;
+      for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
+        double bt[12];
+        const int ap = v.blk_apos[bb];
+        if (ap >= 0) {
+          const double* A = v.val + 144 * (int64_t)ap + 12 * tt;
 #pragma unroll
-            for (int c = 0; c < 12; ++c) bt[c] = A[c];
-          } else {
+          for (int c = 0; c < 12; ++c) bt[c] = A[c];
+        } else {
 #pragma unroll
-            for (int c = 0; c < 12; ++c) bt[c] = 0.0;
+          for (int c = 0; c < 12; ++c) bt[c] = 0.0;
+        }
+        for (int u = v.upd_ptr[bb]; u < v.upd_ptr[bb + 1]; ++u) {
+          const int2 pq = v.upd[u];
+          const double* Li = v.L + 144 * (int64_t)pq.x + 12 * tt;  // row t of L_ik
+          const double* Lj = v.L + 144 * (int64_t)pq.y + 12 * tt;  // row t of L_jk (staged)
+          double lr[12];
+#pragma unroll
+          for (int m = 0; m < 12; ++m) lr[m] = Li[m];
+          __syncwarp(mask);
+          if (t < 12) {
+#pragma unroll
+            for (int m = 0; m < 12; ++m) T[t][m] = Lj[m];
           }
-          for (int u = v.upd_ptr[b]; u < v.upd_ptr[b + 1]; ++u) {
-            const int2 pq = v.upd[u];
-            const double* Li = v.L + 144 * (int64_t)pq.x;  // L_ik
-            const double* Lj = v.L + 144 * (int64_t)pq.y;  // L_jk
-            double lr[12];
-#pragma unroll
-            for (int m = 0; m < 12; ++m) lr[m] = Li[12 * t + m];
-#pragma unroll
-            for (int c = 0; c < 12; ++c) {
-              double s = 0.0;
-#pragma unroll
-              for (int m = 0; m < 12; ++m) s = fma(lr[m], Lj[12 * c + m], s);
-              bt[c] -= s;
-            }
-          }
-          // row t of X with X L_jj^T = B: forward substitution against L_jj rows
-          double x[12];
+          __syncwarp(mask);
 #pragma unroll
           for (int c = 0; c < 12; ++c) {
-            double s = bt[c];
+            double s = 0.0;
 #pragma unroll
-            for (int m = 0; m < c; ++m) s -= S[c][m] * x[m];
-            x[c] = s / S[c][c];
+            for (int m = 0; m < 12; ++m) s = fma(lr[m], T[c][m], s);
+            bt[c] -= s;
           }
-          double* Lo = v.L + 144 * (int64_t)blk + 12 * t;
+        }
+        // row t of X with X L_jj^T = B (forward substitution against L_jj rows)
+        double xr[12];
 #pragma unroll
-          for (int c = 0; c < 12; ++c) Lo[c] = x[c];
+        for (int c = 0; c < 12; ++c) {
+          double s = bt[c];
+#pragma unroll
+          for (int m = 0; m < c; ++m) s = fma(-S[c][m], xr[m], s);
+          xr[c] = s * rinv[c];
+        }
+        if (t < 12) {
+          double* Lo = v.L + 144 * (int64_t)(v.n + bb) + 12 * t;
+#pragma unroll
+          for (int c = 0; c < 12; ++c) Lo[c] = xr[c];
         }
       }
       __syncwarp(mask);
-    }
-    __syncthreads();
-  }
-}
-
-// x = A^-1 b via the factor (x may alias nothing; y is stored in x).
-__global__ void __launch_bounds__(CH_THREADS) k_chol_solve(CholView v, const double* __restrict__ b, double* x) {
-  const int hw = threadIdx.x >> 4, t = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
-  const unsigned mask = half_mask(half);
-  const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
-  const int tt = t < 12 ? t : 0;
-  // forward: L y = b, levels ascending
-  for (int l = 0; l < nl; ++l) {
-    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
-    for (int base = lo; base < hi; base += CH_HW) {
-      const int idx = base + hw;
-      const bool live = idx < hi;
-      const int j = live ? v.nodes[idx] : 0;
-      double acc = 0.0, lrow[12];
-      if (live) {
-        acc = b[12 * (int64_t)j + tt];
-        for (int e = v.row_ptr[j]; e < v.row_ptr[j + 1]; ++e) {
-          const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
-          const double* yk = x + 12 * (int64_t)v.row_col[e];
-          double s = 0.0;
-#pragma unroll
-          for (int m = 0; m < 12; ++m) s = fma(Lk[m], yk[m], s);
-          acc -= s;
-        }
-        const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
-#pragma unroll
-        for (int m = 0; m < 12; ++m) lrow[m] = Ld[m];
-      } else {
-#pragma unroll
-        for (int m = 0; m < 12; ++m) lrow[m] = (m == tt) ? 1.0 : 0.0;
-      }
-      double y = 0.0;
-#pragma unroll
-      for (int c = 0; c < 12; ++c) {
-        double dcc = __shfl_sync(mask, lrow[c], c, 16);
-        double yc = __shfl_sync(mask, acc, c, 16) / dcc;
-        if (t == c) y = yc;
-        if (t > c) acc -= lrow[c] * yc;
-      }
-      if (live && t < 12) x[12 * (int64_t)j + t] = y;
     }
     __syncthreads();
   }
   // backward: L^T x = y, levels descending
   for (int l = nl - 1; l >= 0; --l) {
     const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
-    for (int base = lo; base < hi; base += CH_HW) {
-      const int idx = base + hw;
-      const bool live = idx < hi;
-      const int j = live ? v.nodes[idx] : 0;
-      double acc = 0.0, lcol[12];
-      if (live) {
-        acc = x[12 * (int64_t)j + tt];
-        for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
-          const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;  // column tt of L_ij
-          const double* xi = x + 12 * (int64_t)v.blk_row[bb];
-          double s = 0.0;
+    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
+      const int j = v.nodes[idx];
+      double acc = x[12 * (int64_t)j + tt];
+      for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
+        const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;  // column tt of L_ij
+        const double* xi = x + 12 * (int64_t)v.blk_row[bb];
+        double s = 0.0;
 #pragma unroll
-          for (int r = 0; r < 12; ++r) s = fma(Lb[12 * r], xi[r], s);
-          acc -= s;
-        }
-        const double* Ld = v.L + 144 * (int64_t)j + tt;
-#pragma unroll
-        for (int m = 0; m < 12; ++m) lcol[m] = Ld[12 * m];  // L_jj[m][tt]
-      } else {
-#pragma unroll
-        for (int m = 0; m < 12; ++m) lcol[m] = (m == tt) ? 1.0 : 0.0;
+        for (int r = 0; r < 12; ++r) s = fma(Lb[12 * r], xi[r], s);
+        acc -= s;
       }
-      double xv = 0.0;
+      double lcol[12], rinv[12];
+      const double* Ld = v.L + 144 * (int64_t)j + tt;
+      const double* di = v.dinv + 12 * (int64_t)j;
 #pragma unroll
-      for (int c = 11; c >= 0; --c) {
-        double dcc = __shfl_sync(mask, lcol[c], c, 16);
-        double xc = __shfl_sync(mask, acc, c, 16) / dcc;
-        if (t == c) xv = xc;
-        if (t < c) acc -= lcol[c] * xc;
+      for (int m = 0; m < 12; ++m) {
+        lcol[m] = Ld[12 * m];
+        rinv[m] = di[m];
       }
+      const double xv = upper_solve12(mask, t, acc, lcol, rinv);
       __syncwarp(mask);
-      if (live && t < 12) x[12 * (int64_t)j + t] = xv;
+      if (t < 12) x[12 * (int64_t)j + t] = xv;
+    }
+    __syncthreads();
+  }
+}
+
+// x = A^-1 b with the resident factor (refinement corrections)
+__global__ void __launch_bounds__(CH_THREADS) k_chol_solve(CholView v, const double* __restrict__ b, double* x) {
+  const int hw = threadIdx.x >> 4, t = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
+  const unsigned mask = half_mask(half);
+  const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
+  const int tt = t < 12 ? t : 0;
+  for (int l = 0; l < nl; ++l) {
+    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
+    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
+      const int j = v.nodes[idx];
+      double acc = b[12 * (int64_t)j + tt];
+      for (int e = v.row_ptr[j]; e < v.row_ptr[j + 1]; ++e) {
+        const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
+        const double* yk = x + 12 * (int64_t)v.row_col[e];
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < 12; ++m) s = fma(Lk[m], yk[m], s);
+        acc -= s;
+      }
+      double lrow[12], rinv[12];
+      const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
+      const double* di = v.dinv + 12 * (int64_t)j;
+#pragma unroll
+      for (int m = 0; m < 12; ++m) {
+        lrow[m] = Ld[m];
+        rinv[m] = di[m];
+      }
+      const double y = lower_solve12(mask, t, acc, lrow, rinv);
+      if (t < 12) x[12 * (int64_t)j + t] = y;
+    }
+    __syncthreads();
+  }
+  for (int l = nl - 1; l >= 0; --l) {
+    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
+    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
+      const int j = v.nodes[idx];
+      double acc = x[12 * (int64_t)j + tt];
+      for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
+        const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;
+        const double* xi = x + 12 * (int64_t)v.blk_row[bb];
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < 12; ++r) s = fma(Lb[12 * r], xi[r], s);
+        acc -= s;
+      }
+      double lcol[12], rinv[12];
+      const double* Ld = v.L + 144 * (int64_t)j + tt;
+      const double* di = v.dinv + 12 * (int64_t)j;
+#pragma unroll
+      for (int m = 0; m < 12; ++m) {
+        lcol[m] = Ld[12 * m];
+        rinv[m] = di[m];
+      }
+      const double xv = upper_solve12(mask, t, acc, lcol, rinv);
+      __syncwarp(mask);
+      if (t < 12) x[12 * (int64_t)j + t] = xv;
     }
     __syncthreads();
   }
@@ -327,6 +415,7 @@ struct Analysis {
   int64_t n_blk = 0, n_upd = 0, n_edges = 0;
   int max_level = 0, largest = 0;
   double ms_sync = 0, ms_order = 0, ms_plan = 0;
+  bool cached = false;
   CholView view{};
 };
 
@@ -395,6 +484,44 @@ static Analysis chol_analyze(Scene& s) {
   }
   an.ms_sync = ms_since(t0);
   t0 = clk::now();
+  Scene::Work::CholCache& cc = w.ch_cache;
+  auto make_view = [&](const size_t* o) {
+    const int* dp = w.ch_plan.p;
+    return CholView{n,
+                    dp + o[0],
+                    dp + o[1],
+                    dp + o[2],
+                    dp + o[3],
+                    dp + o[4],
+                    dp + o[5],
+                    dp + o[6],
+                    dp + o[7],
+                    dp + o[8],
+                    dp + o[9],
+                    dp + o[10],
+                    reinterpret_cast<const int2*>(dp + o[11]),
+                    H.diag_pos.p,
+                    H.val.p,
+                    w.ch_L.p,
+                    w.ch_dinv.p,
+                    w.bad.p};
+  };
+  if (cc.valid && cc.n == n && cc.n_off == n_off &&
+      std::equal(flags, flags + n_off, cc.meta.begin()) &&
+      std::equal(keys, keys + 2 * n_off, cc.meta.begin() + n_off)) {
+    an.n_cta = (int)cc.stats[0];
+    an.n_coupled = (int)cc.stats[1];
+    an.n_blk = cc.stats[2];
+    an.n_upd = cc.stats[3];
+    an.n_edges = cc.stats[4];
+    an.max_level = (int)cc.stats[5];
+    an.largest = (int)cc.stats[6];
+    an.view = make_view(cc.offs);
+    an.cached = true;
+    ++cc.hits;
+    return an;
+  }
+  ++cc.misses;
 
   // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order
   std::vector<int> loc(n, -1), glob;
@@ -411,21 +538,94 @@ static Analysis chol_analyze(Scene& s) {
     }
   const int m = (int)glob.size();
   an.n_coupled = m;
-  // adjacency in key order is already sorted per node (keys sorted by (i, j))
-  std::vector<std::vector<int>> adj(m);
+  // adjacency (CSR) in key order is already sorted per node (keys sorted by (i, j))
+  std::vector<int> adj_ptr(m + 1, 0), adj_idx(2 * an.n_edges);
   for (int64_t k = 0; k < n_off; ++k)
     if (flags[k]) {
-      int a = loc[keys[2 * k]], b = loc[keys[2 * k + 1]];
-      adj[a].push_back(b);
-      adj[b].push_back(a);
+      adj_ptr[loc[keys[2 * k]] + 1]++;
+      adj_ptr[loc[keys[2 * k + 1]] + 1]++;
     }
+  for (int v = 0; v < m; ++v) adj_ptr[v + 1] += adj_ptr[v];
+  {
+    std::vector<int> fp(adj_ptr.begin(), adj_ptr.end() - 1);
+    for (int64_t k = 0; k < n_off; ++k)
+      if (flags[k]) {
+        int a2 = loc[keys[2 * k]], b2 = loc[keys[2 * k + 1]];
+        adj_idx[fp[a2]++] = b2;
+        adj_idx[fp[b2]++] = a2;
+      }
+  }
+  // Elimination order: peel degree <= 1 nodes first (no fill: contact graphs are
+  // mostly forests of chains), then minimum degree on the remaining 2-core.
+  // Column structures (later neighbours at elimination) as CSR csp/csi.
   std::vector<int> order;
-  std::vector<std::vector<int>> cs;
-  min_degree(m, adj, order, cs);
+  order.reserve(m);
+  std::vector<int> deg(m), one(m, -1);
+  std::vector<char> gone(m, 0), queued(m, 0);
+  std::vector<int> queue;
+  queue.reserve(m);
+  for (int v = 0; v < m; ++v) {
+    deg[v] = adj_ptr[v + 1] - adj_ptr[v];
+    if (deg[v] <= 1) {
+      queue.push_back(v);
+      queued[v] = 1;
+    }
+  }
+  for (size_t qi = 0; qi < queue.size(); ++qi) {
+    int v = queue[qi];
+    gone[v] = 1;
+    order.push_back(v);
+    for (int e = adj_ptr[v]; e < adj_ptr[v + 1]; ++e) {
+      int u = adj_idx[e];
+      if (gone[u]) continue;
+      one[v] = u;  // the single live neighbour
+      if (--deg[u] <= 1 && !queued[u]) {
+        queued[u] = 1;
+        queue.push_back(u);
+      }
+      break;
+    }
+  }
+  std::vector<int> csp(m + 1, 0), csi;
+  std::vector<std::vector<int>> core_cs;
+  std::vector<int> core_glob;  // local id of each 2-core node
+  if ((int)order.size() < m) {
+    std::vector<int> core_id(m, -1);
+    for (int v = 0; v < m; ++v)
+      if (!gone[v]) {
+        core_id[v] = (int)core_glob.size();
+        core_glob.push_back(v);
+      }
+    const int mc = (int)core_glob.size();
+    std::vector<std::vector<int>> cadj(mc);
+    for (int c = 0; c < mc; ++c) {
+      int v = core_glob[c];
+      for (int e = adj_ptr[v]; e < adj_ptr[v + 1]; ++e)
+        if (core_id[adj_idx[e]] >= 0) cadj[c].push_back(core_id[adj_idx[e]]);
+    }
+    std::vector<int> corder;
+    min_degree(mc, cadj, corder, core_cs);
+    for (int c : corder) order.push_back(core_glob[c]);
+  }
   std::vector<int> pos(m);
   for (int i = 0; i < m; ++i) pos[order[i]] = i;
-  for (auto& c : cs)
-    if (c.size() > 1) std::sort(c.begin(), c.end(), [&](int a, int b) { return pos[a] < pos[b]; });
+  {
+    std::vector<int> core_of(m, -1);
+    for (size_t c = 0; c < core_glob.size(); ++c) core_of[core_glob[c]] = (int)c;
+    for (int v = 0; v < m; ++v)
+      csp[v + 1] = csp[v] + (core_of[v] >= 0 ? (int)core_cs[core_of[v]].size() : (one[v] >= 0 ? 1 : 0));
+    csi.resize(csp[m]);
+    for (int v = 0; v < m; ++v) {
+      if (core_of[v] >= 0) {
+        std::vector<int>& c = core_cs[core_of[v]];
+        for (int& x : c) x = core_glob[x];
+        std::sort(c.begin(), c.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
+        std::copy(c.begin(), c.end(), csi.begin() + csp[v]);
+      } else if (one[v] >= 0) {
+        csi[csp[v]] = one[v];
+      }
+    }
+  }
   an.ms_order = ms_since(t0);
   t0 = clk::now();
 
@@ -442,35 +642,34 @@ static Analysis chol_analyze(Scene& s) {
     return -1;
   };
   // off-diagonal L blocks: column (local) v owns [col_off[v], col_off[v+1])
-  std::vector<int> col_off(m + 1, 0);
-  for (int v = 0; v < m; ++v) col_off[v + 1] = col_off[v] + (int)cs[v].size();
-  const int nbo = col_off[m];
+  const std::vector<int>& col_off = csp;
+  const int nbo = csp[m];
   an.n_blk = n + (int64_t)nbo;
   // row lists (local i): (k, off block) for k eliminated before i, in elimination order of k
   std::vector<int> rcnt(m + 1, 0);
-  for (int v = 0; v < m; ++v)
-    for (int i : cs[v]) rcnt[i + 1]++;
+  for (int e = 0; e < nbo; ++e) rcnt[csi[e] + 1]++;
   for (int v = 0; v < m; ++v) rcnt[v + 1] += rcnt[v];
   std::vector<int> rfill(rcnt.begin(), rcnt.end() - 1), r_k(nbo), r_b(nbo);
   for (int k : order)
-    for (size_t q = 0; q < cs[k].size(); ++q) {
-      int i = cs[k][q];
+    for (int e = csp[k]; e < csp[k + 1]; ++e) {
+      int i = csi[e];
       r_k[rfill[i]] = k;
-      r_b[rfill[i]] = col_off[k] + (int)q;
+      r_b[rfill[i]] = e;
       rfill[i]++;
     }
   // update pairs for off block (i, j): k in rows(j) with i in cs[k]
   std::vector<int> upd_ptr(nbo + 1, 0), upd;
   for (int j = 0; j < m; ++j)
-    for (size_t q = 0; q < cs[j].size(); ++q) {
-      int b = col_off[j] + (int)q, i = cs[j][q];
+    for (int b = csp[j]; b < csp[j + 1]; ++b) {
+      const int i = csi[b];
       for (int e = rcnt[j]; e < rcnt[j + 1]; ++e) {
-        const std::vector<int>& ck = cs[r_k[e]];
-        auto it = std::find(ck.begin(), ck.end(), i);
-        if (it != ck.end()) {
-          upd.push_back(n + col_off[r_k[e]] + (int)(it - ck.begin()));
-          upd.push_back(n + r_b[e]);
-        }
+        const int k = r_k[e];
+        for (int f = csp[k]; f < csp[k + 1]; ++f)
+          if (csi[f] == i) {
+            upd.push_back(n + f);
+            upd.push_back(n + r_b[e]);
+            break;
+          }
       }
       upd_ptr[b + 1] = (int)(upd.size() / 2);
     }
@@ -478,10 +677,10 @@ static Analysis chol_analyze(Scene& s) {
   // elimination-tree levels and component roots (local)
   std::vector<int> level(m, 0), root(m);
   for (int v : order)
-    if (!cs[v].empty()) level[cs[v][0]] = std::max(level[cs[v][0]], level[v] + 1);
+    if (csp[v + 1] > csp[v]) level[csi[csp[v]]] = std::max(level[csi[csp[v]]], level[v] + 1);
   for (int q = m - 1; q >= 0; --q) {
     int v = order[q];
-    root[v] = cs[v].empty() ? v : root[cs[v][0]];
+    root[v] = csp[v + 1] == csp[v] ? v : root[csi[csp[v]]];
   }
   std::vector<int> csize(m, 0), cdepth(m, 0), comps;
   for (int v = 0; v < m; ++v) {
@@ -572,12 +771,11 @@ static Analysis chol_analyze(Scene& s) {
       row_ptr[v] = r;
       int l = loc[v];
       if (l >= 0) {
-        for (size_t q = 0; q < cs[l].size(); ++q) {
-          int b = col_off[l] + (int)q;  // == c + q since locals follow global order
-          hp[off_brow + b] = glob[cs[l][q]];
-          hp[off_bapos + b] = apos_of(glob[cs[l][q]], v);
+        for (int b = csp[l]; b < csp[l + 1]; ++b) {  // b == c + q: locals follow global order
+          hp[off_brow + b] = glob[csi[b]];
+          hp[off_bapos + b] = apos_of(glob[csi[b]], v);
         }
-        c += (int)cs[l].size();
+        c += csp[l + 1] - csp[l];
         for (int e2 = rcnt[l]; e2 < rcnt[l + 1]; ++e2) {
           hp[off_rowb + r] = r_b[e2] + n;
           hp[off_rowc + r] = glob[r_k[e2]];
@@ -593,24 +791,18 @@ static Analysis chol_analyze(Scene& s) {
   w.ch_plan.resize(total);
   CK(cudaMemcpyAsync(w.ch_plan.p, hp, total * sizeof(int), cudaMemcpyHostToDevice, st));
   w.ch_L.resize(144 * std::max<int64_t>(an.n_blk, 1));
-  const int* dp = w.ch_plan.p;
-  an.view = CholView{n,
-                     dp + off_nodes,
-                     dp + off_lvl,
-                     dp + off_ctal,
-                     dp + off_ctan,
-                     dp + off_colp,
-                     dp + off_brow,
-                     dp + off_bapos,
-                     dp + off_rowp,
-                     dp + off_rowb,
-                     dp + off_rowc,
-                     dp + off_updp,
-                     reinterpret_cast<const int2*>(dp + off_upd),
-                     H.diag_pos.p,
-                     H.val.p,
-                     w.ch_L.p,
-                     w.bad.p};
+  w.ch_dinv.resize(12 * std::max<int64_t>(n, 1));
+  const size_t offs[13] = {off_nodes, off_lvl,  off_ctal, off_ctan, off_colp, off_brow, off_bapos,
+                           off_rowp,  off_rowb, off_rowc, off_updp, off_upd,  total};
+  an.view = make_view(offs);
+  cc.valid = true;
+  cc.n = n;
+  cc.n_off = n_off;
+  cc.meta.assign(flags, flags + n_off);
+  cc.meta.insert(cc.meta.end(), keys, keys + 2 * n_off);
+  const int64_t st8[8] = {an.n_cta, an.n_coupled, an.n_blk, an.n_upd, an.n_edges, an.max_level, an.largest, 0};
+  std::copy(st8, st8 + 8, cc.stats);
+  std::copy(offs, offs + 13, cc.offs);
   an.ms_plan = ms_since(t0);
   return an;
 }
@@ -633,10 +825,8 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
   const int big = 0x7fffffff;
   CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   if (s.instrument) CK(cudaEventRecord(s.ev0, st));
-  k_chol_factor<<<an.n_cta, CH_THREADS, 0, st>>>(v);
-  note_launch("k_chol_factor");
-  k_chol_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, rhs, x);
-  note_launch("k_chol_solve");
+  k_chol_factor_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, rhs, x);
+  note_launch("k_chol_factor_solve");
   if (s.instrument) CK(cudaEventRecord(s.ev1, st));
   w.r.resize(N);
   w.z.resize(N);
@@ -678,9 +868,11 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
     if (trace)
       fprintf(stderr,
               "[abd chol] n=%d edges=%lld L_blocks=%lld updates=%lld levels=%d largest=%d ctas=%d solves=%d "
-              "rel=%.2e factor+solve_ms=%.3f analysis_ms=%.3f (sync %.3f order %.3f plan %.3f) coupled=%d\n",
+              "rel=%.2e factor+solve_ms=%.3f analysis_ms=%.3f (sync %.3f order %.3f plan %.3f) coupled=%d "
+              "cached=%d hits=%lld misses=%lld\n",
               n, (long long)an.n_edges, (long long)an.n_blk, (long long)an.n_upd, an.max_level, an.largest,
-              an.n_cta, solves, rel_res, ms, host_ms, an.ms_sync, an.ms_order, an.ms_plan, an.n_coupled);
+              an.n_cta, solves, rel_res, ms, host_ms, an.ms_sync, an.ms_order, an.ms_plan, an.n_coupled,
+              (int)an.cached, (long long)w.ch_cache.hits, (long long)w.ch_cache.misses);
   }
   return solves;
 }

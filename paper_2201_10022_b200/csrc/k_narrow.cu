@@ -207,18 +207,22 @@ __global__ void k_friction_pre(SceneView sv, int kind, int64_t n, const int4* __
 __global__ void k_ccd(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows, const double* __restrict__ q,
                       const double* __restrict__ dq, double slack, unsigned long long* tmin, int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  PairIds ids = pair_ids(sv, kind, rows[i]);
-  V3 x[4], xb[4], dx[4];
-  pair_points(sv, ids, q, x, xb);
-  for (int k = 0; k < 4; ++k) {
-    int b = ids.body[k];
-    dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+  double t = INFINITY;
+  if (i < n) {
+    PairIds ids = pair_ids(sv, kind, rows[i]);
+    V3 x[4], xb[4], dx[4];
+    pair_points(sv, ids, q, x, xb);
+    for (int k = 0; k < 4; ++k) {
+      int b = ids.body[k];
+      dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+    }
+    bool bad = false;
+    t = accd_query(kind, x, dx, slack, 1.0, 512, tmin, bad);
+    if (bad) atomicExch(err, 1);
   }
-  bool bad = false;
-  double t = accd_query(kind, x, dx, slack, 1.0, 512, tmin, bad);
-  if (bad) atomicExch(err, 1);
-  atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
+  // one ordered-bits atomic per warp (t >= 0, so the bit patterns order like the values)
+  for (int o = 16; o > 0; o >>= 1) t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
+  if ((threadIdx.x & 31) == 0 && t < INFINITY) atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
 }
 
 // K1: inertia + orthogonality per dynamic slot (solver.py:197-200, :283-296)

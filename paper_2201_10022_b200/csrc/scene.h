@@ -178,8 +178,19 @@ struct Scene {
     DVec<double> minv;
     // sparse block Cholesky plan (one packed int buffer) and factor (k_chol.cu)
     DVec<int> ch_flags, ch_plan;
-    DVec<double> ch_L;
+    DVec<double> ch_L, ch_dinv;
     HostPinned<int> h_plan, h_meta;
+    // last analysed pattern (nonzero flags + keys) and its plan: Newton iterations
+    // whose coupling pattern is unchanged reuse the resident plan
+    struct CholCache {
+      bool valid = false;
+      int n = 0;
+      int64_t n_off = 0;
+      std::vector<int> meta;
+      int64_t stats[8] = {};
+      size_t offs[13] = {};
+      int64_t hits = 0, misses = 0;
+    } ch_cache;
   } w;
 
   // per-kernel instrumentation (CUDA events on `stream`)
