@@ -164,6 +164,39 @@ __global__ void k_friction(int64_t n, const int2* __restrict__ bodies, const dou
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// lean variants used by the Newton driver: energy-only partials, and pair blocks
+// written straight into the PairBlocks records (no per-thread 24x24 staging)
+__global__ void k_friction_energy(int64_t n, const int2* __restrict__ bodies, const double* __restrict__ rec,
+                                  double mu, const double* __restrict__ q, double eh, double* partials) {
+  __shared__ double sh[RED_THREADS];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int2 b = bodies[i];
+    const double* r = rec + i * FRIC_STRIDE;
+    FricEval e = friction_eval(r, q + 12 * b.x, q + 12 * b.y, eh);
+    acc += mu * r[50] * e.f0;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+__global__ void k_friction_pblk(int64_t n, const int2* __restrict__ bodies, const double* __restrict__ rec,
+                                double mu, const double* __restrict__ q, const unsigned char* __restrict__ dyn,
+                                double eh, int project, double* pblk) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int2 b = bodies[i];
+    const double* r = rec + i * FRIC_STRIDE;
+    FricEval e = friction_eval(r, q + 12 * b.x, q + 12 * b.y, eh);
+    double* o = pblk + i * PB_STRIDE;
+    friction_blocks_dev(r, e, mu, dyn[b.x] != 0, dyn[b.y] != 0, project != 0, o, o + 24, o + 168, o + 312);
+  }
+}
+
 // per-pair contact terms on explicit points (K3 arithmetic without the scene gather)
 __global__ void __launch_bounds__(64) k_contact_pairs(int kind, int64_t n, const double* __restrict__ z,
                                                       const double* __restrict__ xb, const double* __restrict__ eps,
@@ -249,9 +282,17 @@ void launch_accd(cudaStream_t st, int kind, int64_t n, const double* x, const do
 void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const double* rec, double mu, const double* q,
                      const unsigned char* dyn, double dt, double eps_v, int project, double* partials,
                      double* grad24, double* hess24, double* pblk) {
-  k_friction<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, bodies, rec, mu, q, dyn, eps_v * dt, project, partials, grad24,
-                                                 hess24, pblk);
-  note_launch("k_friction");
+  if (partials && !grad24 && !pblk) {
+    k_friction_energy<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, bodies, rec, mu, q, eps_v * dt, partials);
+    note_launch("k_friction_energy");
+  } else if (pblk && !partials && !grad24) {
+    k_friction_pblk<<<grid_for(n, 128), 128, 0, st>>>(n, bodies, rec, mu, q, dyn, eps_v * dt, project, pblk);
+    note_launch("k_friction_pblk");
+  } else {
+    k_friction<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, bodies, rec, mu, q, dyn, eps_v * dt, project, partials,
+                                                   grad24, hess24, pblk);
+    note_launch("k_friction");
+  }
 }
 
 }  // namespace abd

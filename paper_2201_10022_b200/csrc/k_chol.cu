@@ -10,7 +10,7 @@
 //     CTAs.  Contact graphs of piles are forests of short chains, so the fill
 //     is ~0 and the tree height is tens of levels.
 //   * factor + solve (k_chol_factor_solve): one CTA walks the levels of its components with
-//     __syncthreads between levels; a half-warp (lane t = row t) owns one node:
+//     __syncthreads between levels; a warp (lane t = row t) owns one node:
 //     D = A_jj - sum_k L_jk L_jk^T, 12x12 Cholesky, then L_ij = (A_ij -
 //     sum_k L_ik L_jk^T) L_jj^-T for every block of the column.  Left-looking
 //     with fixed update order: deterministic, no atomics.
@@ -36,8 +36,8 @@
 
 namespace abd {
 
-constexpr int CH_THREADS = 256;
-constexpr int CH_HW = CH_THREADS / 16;  // half-warps per CTA
+constexpr int CH_THREADS = 384;
+constexpr int CH_HW = CH_THREADS / 32;  // warps per CTA (one node per warp, lane t = row t)
 
 // Plan layout (one packed int buffer uploaded per analysis).  L holds the n
 // diagonal blocks first (L_jj at index j), then the off-diagonal blocks.
@@ -60,11 +60,13 @@ struct CholView {
   double* L;            // L blocks, 144 doubles each (row-major)
   double* dinv;         // n x 12: 1 / L_jj[c][c]
   int* bad;
+  long long* dbg;       // optional per-node phase clocks of CTA 0 (ABD_CHOL_CLOCK)
 };
 
-__device__ __forceinline__ unsigned half_mask(int half) { return 0xffffu << (16 * half); }
 
-__device__ __forceinline__ double hshfl(unsigned mask, double v, int src) { return __shfl_sync(mask, v, src, 16); }
+// full-warp shuffles: every lane of a warp runs the same node, so no partial-mask
+// convergence checks are generated
+__device__ __forceinline__ double hshfl(unsigned mask, double v, int src) { return __shfl_sync(mask, v, src); }
 
 // 1/sqrt(x) without the libdevice slow-path call (whose register saves would put
 // the in-register factor on the stack): MUFU seed + 3 Newton steps (>= 53 bits)
@@ -78,7 +80,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return r;
 }
 
-// In-register 12x12 Cholesky on a 16-lane group: lane t < 12 holds row t of the
+// In-register 12x12 Cholesky on a warp: lane t < 12 holds row t of the
 // symmetric matrix in d[]; on exit d[] is row t of L (zeros above the diagonal)
 // and every lane holds rinv[c] = 1 / L_cc.  Division-free (rsqrt per pivot).
 __device__ __forceinline__ bool chol12(unsigned mask, int t, double d[12], double rinv[12]) {
@@ -92,10 +94,14 @@ __device__ __forceinline__ bool chol12(unsigned mask, int t, double d[12], doubl
     rinv[c] = r;
     if (t == c) d[c] = pp * r;
     else if (t > c) d[c] *= r;
+    // constant trip counts (k > c as a predicate) so both loops fully unroll and
+    // d[] stays in registers
 #pragma unroll
-    for (int k = c + 1; k < 12; ++k) {
-      const double lkc = hshfl(mask, d[c], k);
-      if (t >= k) d[k] = fma(-d[c], lkc, d[k]);
+    for (int k = 0; k < 12; ++k) {
+      if (k > c) {
+        const double lkc = hshfl(mask, d[c], k);
+        if (t >= k) d[k] = fma(-d[c], lkc, d[k]);
+      }
     }
   }
 #pragma unroll
@@ -134,11 +140,11 @@ __device__ __forceinline__ double upper_solve12(unsigned mask, int t, double acc
 // (levels descending), one CTA per group of components.  x receives y, then x.
 __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, const double* __restrict__ b,
                                                                    double* x) {
-  __shared__ double Ss[CH_HW][12][13];  // per half-warp: staged L_jk / symmetrisation / L_jj
-  __shared__ double Ts[CH_HW][12][13];  // per half-warp: staged L_jk of update pairs
-  const int hw = threadIdx.x >> 4, t = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
+  __shared__ double Ss[CH_HW][12][13];  // per warp: staged L_jk / symmetrisation / L_jj
+  __shared__ double Ts[CH_HW][12][13];  // per warp: staged L_jk of update pairs
+  const int hw = threadIdx.x >> 5, t = threadIdx.x & 31;
   const int tt = t < 12 ? t : 0;
-  const unsigned mask = half_mask(half);
+  const unsigned mask = 0xffffffffu;
   double (*S)[13] = Ss[hw];
   double (*T)[13] = Ts[hw];
   const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
@@ -146,6 +152,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
     const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
     for (int idx = lo + hw; idx < hi; idx += CH_HW) {
       const int j = v.nodes[idx];
+      long long ck0 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
       double d[12];
       {
         const double* A = v.val + 144 * (int64_t)v.diag_pos[j] + 12 * tt;
@@ -188,7 +195,9 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
 #pragma unroll
       for (int c = 0; c < 12; ++c) d[c] = 0.5 * (d[c] + S[c][tt]);
       double rinv[12];
+      long long ck1 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
       const bool ok = chol12(mask, t, d, rinv);
+      long long ck2 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
       if (!ok && t == 0) atomicMin(v.bad, j);
       __syncwarp(mask);
       if (t < 12) {
@@ -208,6 +217,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
       const double y = lower_solve12(mask, t, acc, d, rinv);
       if (t < 12) x[12 * (int64_t)j + t] = y;
       __syncwarp(mask);
+      long long ck3 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
       // off-diagonal blocks of column j: L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
       for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
         double bt[12];
@@ -247,7 +257,8 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
         for (int c = 0; c < 12; ++c) {
           double s = bt[c];
 #pragma unroll
-          for (int m = 0; m < c; ++m) s = fma(-S[c][m], xr[m], s);
+          for (int m = 0; m < 12; ++m)
+            if (m < c) s = fma(-S[c][m], xr[m], s);
           xr[c] = s * rinv[c];
         }
         if (t < 12) {
@@ -257,6 +268,17 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
         }
       }
       __syncwarp(mask);
+      if (v.dbg && blockIdx.x == 0 && t == 0 && idx - v.lvl_ptr[c0] < 256) {
+        long long* o = v.dbg + 8 * (idx - v.lvl_ptr[c0]);
+        o[0] = j;
+        o[1] = l;
+        o[2] = ck0;
+        o[3] = ck1;
+        o[4] = ck2;
+        o[5] = ck3;
+        o[6] = clock64();
+        o[7] = v.col_ptr[j + 1] - v.col_ptr[j];
+      }
     }
     __syncthreads();
   }
@@ -292,8 +314,8 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
 
 // x = A^-1 b with the resident factor (refinement corrections)
 __global__ void __launch_bounds__(CH_THREADS) k_chol_solve(CholView v, const double* __restrict__ b, double* x) {
-  const int hw = threadIdx.x >> 4, t = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
-  const unsigned mask = half_mask(half);
+  const int hw = threadIdx.x >> 5, t = threadIdx.x & 31;
+  const unsigned mask = 0xffffffffu;
   const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
   const int tt = t < 12 ? t : 0;
   for (int l = 0; l < nl; ++l) {
@@ -693,6 +715,15 @@ static Analysis chol_analyze(Scene& s) {
   std::sort(comps.begin(), comps.end(),
             [&](int a, int b) { return csize[a] != csize[b] ? csize[a] > csize[b] : a < b; });
   an.largest = comps.empty() ? 0 : csize[comps[0]];
+  static const bool trace_lv = getenv("ABD_TRACE_CHOL") != nullptr;
+  if (trace_lv && !comps.empty()) {
+    std::vector<int> h(cdepth[comps[0]], 0);
+    for (int v = 0; v < m; ++v)
+      if (root[v] == comps[0]) h[level[v]]++;
+    fprintf(stderr, "[abd chol] largest component levels:");
+    for (int x : h) fprintf(stderr, " %d", x);
+    fprintf(stderr, "\n");
+  }
   // CTAs: components (largest first onto the least loaded), then isolated nodes
   const int n_iso = n - m;
   const int iso_per_cta = 4 * CH_HW;
@@ -825,8 +856,28 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
   const int big = 0x7fffffff;
   CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
   if (s.instrument) CK(cudaEventRecord(s.ev0, st));
+  static const bool clk_dbg = getenv("ABD_CHOL_CLOCK") != nullptr;
+  static DVec<long long> dbgbuf;
+  if (clk_dbg) {
+    dbgbuf.resize(8 * 256);
+    dbgbuf.zero(st);
+    v.dbg = dbgbuf.p;
+  }
   k_chol_factor_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, rhs, x);
   note_launch("k_chol_factor_solve");
+  if (clk_dbg) {
+    std::vector<long long> hb(8 * 256);
+    dbgbuf.download(hb.data(), hb.size(), st);
+    CK(cudaStreamSynchronize(st));
+    long long t0c = hb[2];
+    fprintf(stderr, "[abd chol clock] node level start D_done chol_done fwd_done end n_off (cycles from first)\n");
+    for (int q = 0; q < 256; ++q) {
+      long long* o = &hb[8 * q];
+      if (o[2] == 0) continue;
+      fprintf(stderr, "  %6lld %3lld %8lld %6lld %6lld %6lld %6lld %lld\n", o[0], o[1], o[2] - t0c, o[3] - o[2],
+              o[4] - o[3], o[5] - o[4], o[6] - o[5], o[7]);
+    }
+  }
   if (s.instrument) CK(cudaEventRecord(s.ev1, st));
   w.r.resize(N);
   w.z.resize(N);

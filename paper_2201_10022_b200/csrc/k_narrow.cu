@@ -267,6 +267,40 @@ __global__ void k_body_terms(int n_dyn, const int* __restrict__ dyn_body, const 
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// K1 energy only (line-search trials): 0.5 dq^T M dq + dt^2 V_perp per dynamic slot
+__global__ void k_body_energy(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ mass,
+                              const double* __restrict__ stiff, const double* __restrict__ q,
+                              const double* __restrict__ qt, double dt, double* partials) {
+  __shared__ double sh[RED_THREADS];
+  double acc = 0.0;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_dyn; s += gridDim.x * blockDim.x) {
+    int b = dyn_body[s];
+    const double* M = mass + 144 * (int64_t)b;
+    double qq[12], diff[12];
+#pragma unroll
+    for (int c = 0; c < 12; ++c) {
+      qq[c] = q[12 * (int64_t)b + c];
+      diff[c] = qq[c] - qt[12 * (int64_t)b + c];
+    }
+    double quad = 0.0;
+#pragma unroll
+    for (int r = 0; r < 12; ++r) {
+      double a = 0.0;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) a += M[r * 12 + c] * diff[c];
+      quad += diff[r] * a;
+    }
+    acc += 0.5 * quad + (dt * dt) * ortho_energy_dev(qq, stiff[b]);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
 // q_tilde = q + dt qdot + dt^2 M^{-1} f (solver.py:179-190), Cholesky per body
 __global__ void k_q_tilde(int B, const unsigned char* __restrict__ dyn, const double* __restrict__ mass,
                           const double* __restrict__ q, const double* __restrict__ qd, const double* __restrict__ f,
@@ -374,6 +408,12 @@ void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double sl
 
 void launch_body_terms(Scene& s, const double* q, const double* qt, double dt, double* grad0, double* diag0,
                        double* partials, int want) {
+  if (!want) {
+    k_body_energy<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p, s.stiff.p, q, qt, dt,
+                                                            partials);
+    note_launch("k_body_energy");
+    return;
+  }
   k_body_terms<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p, s.stiff.p, q, qt, dt, grad0,
                                                          diag0, partials, want);
   note_launch("k_body_terms");
