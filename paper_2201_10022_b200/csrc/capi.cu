@@ -755,6 +755,7 @@ int abd_kernel_stats(abd_scene* h, int which, int64_t* launches, double* ms, dou
   return guard([&] {
     SC(h);
     if (which < 0 || which > 3) throw Error(ABD_ERR_ARG, "kernel stats index out of range");
+    kstat_flush(s, which);
     Scene::KStat& k = s.kstat[which];
     if (launches) *launches = k.launches;
     if (ms) *ms = k.ms;
@@ -766,7 +767,11 @@ int abd_kernel_stats(abd_scene* h, int which, int64_t* launches, double* ms, dou
 int abd_kernel_stats_reset(abd_scene* h) {
   return guard([&] {
     SC(h);
-    for (auto& k : s.kstat) k = Scene::KStat{};
+    for (auto& k : s.kstat) {
+      k.launches = k.units = 0;
+      k.ms = k.bytes = 0.0;
+      k.pending = false;
+    }
   });
 }
 

@@ -33,6 +33,17 @@ __global__ void k_absmax_dot(int64_t n, const double* __restrict__ x, const doub
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// trial q + alpha0 dq with alpha0 from the device CCD minimum (solver.py:375-376):
+// alpha_max = min(1, t_min); alpha0 = 1 if alpha_max >= 1 else min(1, scale alpha_max)
+__global__ void k_alpha_trial(int64_t n, const double* __restrict__ q, const double* __restrict__ dq,
+                              const unsigned long long* __restrict__ tmin, double scale, double* out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double amax = fmin(1.0, __longlong_as_double((long long)*tmin));
+  const double alpha = amax >= 1.0 ? 1.0 : fmin(1.0, scale * amax);
+  out[i] = xadd(q[i], xmul(alpha, dq[i]));
+}
+
 __global__ void k_expand_dq(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ dx, double sign,
                             double* dq) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -77,26 +88,26 @@ __global__ void k_ortho_err(int n_dyn, const int* __restrict__ dyn_body, const d
 static double bits_to_d(unsigned long long b) { return __builtin_bit_cast(double, b); }
 static unsigned long long d_to_bits(double d) { return (unsigned long long)__builtin_bit_cast(long long, d); }
 
+// per-kernel event timing on the scene stream, resolved lazily (kstat_flush) at
+// the next use of the same slot or when the stats are read: no extra host sync
 struct EventTimer {
   Scene& s;
   int which;
   bool on;
   EventTimer(Scene& sc, int w) : s(sc), which(w), on(sc.instrument) {
-    if (on) CK(cudaEventRecord(s.ev0, s.stream));
+    if (!on) return;
+    kstat_flush(s, which);
+    CK(cudaEventRecord(s.kstat[which].e0, s.stream));
   }
-  // call after the host has synchronised the stream
   void done(int64_t units, double bytes) {
     if (!on) return;
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
     Scene::KStat& k = s.kstat[which];
-    k.launches += 1;
-    k.units += units;
-    k.ms += ms;
-    k.bytes += bytes;
+    k.pending = true;
+    k.p_units = units;
+    k.p_bytes = bytes;
   }
   void stop() {
-    if (on) CK(cudaEventRecord(s.ev1, s.stream));
+    if (on) CK(cudaEventRecord(s.kstat[which].e1, s.stream));
   }
 };
 
@@ -135,7 +146,6 @@ int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int p
   launch_pair_blocks(s, KIND_VF, q, kappa, dh, project, s.w.flags.p, s.w.pos.p, 0, s.w.err.p);
   launch_pair_blocks(s, KIND_EE, q, kappa, dh, project, s.w.flags.p + n_vf, s.w.pos.p + n_vf, 0, s.w.err.p);
   tm.stop();
-  CK(cudaStreamSynchronize(s.stream));
   // algorithmic bytes (scene form): candidate record 16 B + 4 rest points 96 B
   // (+ eps 8 B for EE) per candidate, one PB_STRIDE record written per active pair
   double bytes = 112.0 * (double)(s.cands.n_vf + s.cands.n_ee) + 8.0 * (double)s.cands.n_ee +
@@ -256,6 +266,78 @@ double ip_value(Scene& s, const double* q, const double* qt, double dt, double k
   return total;
 }
 
+// energy pieces launched without a host sync: partials into red4 (4 x RED_BLOCKS),
+// fixed-order sums into scal4[0..3], barrier-domain flag into err
+static void launch_energy(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh,
+                          double eps_v, double* red4, double* scal4, int* err) {
+  launch_body_terms(s, q, qt, dt, nullptr, nullptr, red4, 0);
+  launch_contact_energy(s, KIND_VF, q, kappa, dh, red4 + RED_BLOCKS, err);
+  launch_contact_energy(s, KIND_EE, q, kappa, dh, red4 + 2 * RED_BLOCKS, err);
+  if (s.fric.n)
+    launch_friction(s.stream, s.fric.n, s.fric.bodies.p, s.fric.rec.p, s.fric.mu, q, s.dyn.p, dt, eps_v, 0,
+                    red4 + 3 * RED_BLOCKS, nullptr, nullptr, nullptr);
+  else
+    CK(cudaMemsetAsync(red4 + 3 * RED_BLOCKS, 0, RED_BLOCKS * sizeof(double), s.stream));
+  reduce_fixed_multi(s.stream, red4, RED_BLOCKS, 4, scal4);
+}
+
+static double ip_combine(const double* e) {  // ((body + ((0 + vf) + ee)) + fric), solver.py:193-205
+  double total = e[0];
+  total += (0.0 + e[1]) + e[2];
+  total += e[3];
+  return total;
+}
+
+// CCD step bound, e0 = ip_value(q) and the first trial energy in ONE host sync
+// (ccd.py:130-153, solver.py:358-393); returns alpha_max, alpha0, e0, e(alpha0)
+struct LsFirst {
+  double amax, alpha, e0, e, ccd_ms;
+};
+static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB) {
+  cudaStream_t st = s.stream;
+  Scene::Work& w = s.w;
+  unsigned long long* tmin = w.ull.p;
+  w.lsred.resize(8 * RED_BLOCKS);
+  w.lsscal.resize(8);
+  w.lserr.resize(2);
+  w.lserr.zero(st);
+  unsigned long long one = d_to_bits(1.0);
+  CK(cudaMemcpyAsync(tmin, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+  EventTimer tm(s, 2);
+  launch_ccd(s, KIND_VF, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
+  launch_ccd(s, KIND_EE, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
+  tm.stop();
+  launch_energy(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v, w.lsred.p, w.lsscal.p,
+                w.lserr.p + 1);
+  k_alpha_trial<<<grid_for(NB, 256), 256, 0, st>>>(NB, s.q.p, s.dq.p, tmin, P.ccd_step_scale, s.q_trial.p);
+  note_launch("k_alpha_trial");
+  launch_energy(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v,
+                w.lsred.p + 4 * RED_BLOCKS, w.lsscal.p + 4, w.lserr.p + 1);
+  double* hp = s.h_pinned + 32;
+  CK(cudaMemcpyAsync(hp, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hp + 1, w.lsscal.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hp + 9, w.lserr.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int* he = reinterpret_cast<const int*>(hp + 9);
+  if (he[0]) throw Error(ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
+  if (he[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
+                                                 "(intersection reached; CCD filtering must prevent this)");
+  int64_t nq = s.cands.n_vf + s.cands.n_ee;
+  LsFirst r;
+  r.ccd_ms = 0.0;
+  if (s.instrument) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s.kstat[2].e0, s.kstat[2].e1));
+    r.ccd_ms = ms;
+  }
+  tm.done(nq, 112.0 * (double)nq + 192.0 * s.B);
+  r.amax = std::fmin(1.0, bits_to_d(*reinterpret_cast<const unsigned long long*>(hp)));
+  r.alpha = r.amax >= 1.0 ? 1.0 : std::fmin(1.0, P.ccd_step_scale * r.amax);
+  r.e0 = ip_combine(hp + 1);
+  r.e = ip_combine(hp + 5);
+  return r;
+}
+
 double step_filter(Scene& s, const double* q, const double* dq, double slack) {
   unsigned long long* tmin = s.w.ull.p;
   s.w.err.resize(2);
@@ -354,19 +436,28 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       if (ND) {
         k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
         note_launch("k_neg");
-        pcg_it = P.linear_solver == 1 ? pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel)
-                                      : chol_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, rel);
+        const bool chol = P.linear_solver != 1;
+        if (chol) chol_begin(s, s.w.neg.p, s.dx.p);
+        else pcg_it = pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
+        // |dx|_inf and g.dx in one pass; the Cholesky residual check shares the host sync
+        auto absmax_dot = [&]() {
+          unsigned long long* am = s.w.ull.p + 2;
+          CK(cudaMemsetAsync(am, 0, sizeof(unsigned long long), stream));
+          k_absmax_dot<<<RED_BLOCKS, RED_THREADS, 0, stream>>>(ND, s.dx.p, s.grad.p, am, s.red.p);
+          note_launch("k_absmax_dot");
+          s.w.scal.resize(8);
+          reduce_fixed_stream(stream, s.red.p, RED_BLOCKS, s.w.scal.p);
+          CK(cudaMemcpyAsync(s.h_pinned, am, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+          CK(cudaMemcpyAsync(s.h_pinned + 1, s.w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+          CK(cudaStreamSynchronize(stream));
+        };
+        absmax_dot();
+        if (chol) {
+          bool changed = false;
+          pcg_it = chol_finish(s, P.pcg_rel_tol, rel, 3, changed);
+          if (changed) absmax_dot();
+        }
         st.pcg_iters_total += pcg_it;
-        // |dx|_inf and g.dx in one pass, one sync
-        unsigned long long* am = s.w.ull.p + 2;
-        CK(cudaMemsetAsync(am, 0, sizeof(unsigned long long), stream));
-        k_absmax_dot<<<RED_BLOCKS, RED_THREADS, 0, stream>>>(ND, s.dx.p, s.grad.p, am, s.red.p);
-        note_launch("k_absmax_dot");
-        s.w.scal.resize(4);
-        reduce_fixed_stream(stream, s.red.p, RED_BLOCKS, s.w.scal.p);
-        CK(cudaMemcpyAsync(s.h_pinned, am, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(s.h_pinned + 1, s.w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
         amax = bits_to_d(*reinterpret_cast<unsigned long long*>(s.h_pinned));
         gd = s.h_pinned[1];
       }
@@ -394,18 +485,15 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       max_c = std::max<int64_t>(max_c, s.cands.n_vf + s.cands.n_ee);
       // line search (solver.py:358-393)
       auto tls = clk::now();
-      t0 = clk::now();
-      double amax_ccd = step_filter(s, s.q.p, s.dq.p, P.ccd_slack);
-      st.t_ccd += ms(t0, clk::now());
-      double alpha = amax_ccd >= 1.0 ? 1.0 : std::fmin(1.0, P.ccd_step_scale * amax_ccd);
-      double e0 = ip_value(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
-      double e = 0.0;
-      while (true) {
-        launch_axpy_q(s, s.q.p, alpha, s.dq.p, s.q_trial.p, NB);
-        e = ip_value(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
-        if (e < e0) break;
+      LsFirst lf = line_search_first(s, P, NB);
+      st.t_ccd += lf.ccd_ms;
+      const double amax_ccd = lf.amax, e0 = lf.e0;
+      double alpha = lf.alpha, e = lf.e;
+      while (!(e < e0)) {
         alpha *= 0.5;
         if (alpha < 1e-12) throw Error(ABD_ERR_STEP_FAILURE, "line search underflow (no descent below alpha = 1e-12)");
+        launch_axpy_q(s, s.q.p, alpha, s.dq.p, s.q_trial.p, NB);
+        e = ip_value(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
       }
       CK(cudaMemcpyAsync(s.q.p, s.q_trial.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
       if (trace_newton)

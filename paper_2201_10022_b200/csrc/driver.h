@@ -12,6 +12,8 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0);
 int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_iters, double& rel_res);
 // k_chol.cu: sparse block Cholesky + refinement; returns the number of triangular solves
 int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine = 3);
+void chol_begin(Scene& s, const double* rhs, double* x);
+int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed);
 void spmv(Scene& s, const double* x, double* y);
 void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off);
 // k_stats.cu

@@ -838,24 +838,80 @@ static Analysis chol_analyze(Scene& s) {
   return an;
 }
 
-// Direct solve of the resident system H x = rhs with refinement (sparse.py:149-161).
-// Returns the number of triangular solves (1 + corrections).
-int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine) {
+// Direct solve of the resident system H x = rhs with refinement (sparse.py:149-161),
+// split so the driver can fold the residual check into its own host sync:
+//   chol_begin  : analysis + factor/solve + residual + async copies (no sync)
+//   chol_finish : after a stream sync, pivot check, residual test, corrections
+static CholView plan_view(Scene& s) {
+  Scene::Work& w = s.w;
+  const size_t* o = w.ch_cache.offs;
+  const int* dp = w.ch_plan.p;
+  return CholView{s.H.n,
+                  dp + o[0],
+                  dp + o[1],
+                  dp + o[2],
+                  dp + o[3],
+                  dp + o[4],
+                  dp + o[5],
+                  dp + o[6],
+                  dp + o[7],
+                  dp + o[8],
+                  dp + o[9],
+                  dp + o[10],
+                  reinterpret_cast<const int2*>(dp + o[11]),
+                  s.H.diag_pos.p,
+                  s.H.val.p,
+                  w.ch_L.p,
+                  w.ch_dinv.p,
+                  w.bad.p,
+                  nullptr};
+}
+
+static void launch_resid(Scene& s, const double* rhs, const double* x) {
+  Scene::Work& w = s.w;
+  cudaStream_t st = s.stream;
+  k_resid<<<RED_BLOCKS, RED_THREADS, 0, st>>>(s.H.n, s.H.row_ptr.p, s.H.col.p, s.H.val.p, x, rhs, w.r.p, w.part.p);
+  note_launch("k_resid");
+  reduce_fixed_multi(st, w.part.p, RED_BLOCKS, 2, w.scal.p + 4);
+  CK(cudaMemcpyAsync(s.h_pinned + 24, w.scal.p + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(reinterpret_cast<int*>(s.h_pinned + 28), w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+}
+
+void chol_begin(Scene& s, const double* rhs, double* x) {
   Bsr& H = s.H;
   Scene::Work& w = s.w;
   cudaStream_t st = s.stream;
   const int n = H.n;
   const int64_t N = 12 * (int64_t)n;
-  rel_res = 0.0;
-  if (n == 0) return 0;
+  Scene::Work::CholRun& run = w.ch_run;
+  run = Scene::Work::CholRun{};
+  if (n == 0) return;
   auto th0 = std::chrono::steady_clock::now();
   w.bad.resize(1);
   Analysis an = chol_analyze(s);
-  const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+  run.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+  run.active = true;
+  run.rhs = rhs;
+  run.x = x;
+  run.n_cta = an.n_cta;
+  run.stats[0] = an.n_edges;
+  run.stats[1] = an.n_blk;
+  run.stats[2] = an.n_upd;
+  run.stats[3] = an.max_level;
+  run.stats[4] = an.largest;
+  run.stats[5] = an.n_coupled;
+  run.stats[6] = an.cached ? 1 : 0;
+  run.ms3[0] = an.ms_sync;
+  run.ms3[1] = an.ms_order;
+  run.ms3[2] = an.ms_plan;
   CholView v = an.view;
   const int big = 0x7fffffff;
   CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
-  if (s.instrument) CK(cudaEventRecord(s.ev0, st));
+  Scene::KStat& ks = s.kstat[0];
+  if (s.instrument) {
+    kstat_flush(s, 0);
+    CK(cudaEventRecord(ks.e0, st));
+  }
   static const bool clk_dbg = getenv("ABD_CHOL_CLOCK") != nullptr;
   static DVec<long long> dbgbuf;
   if (clk_dbg) {
@@ -865,6 +921,7 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
   }
   k_chol_factor_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, rhs, x);
   note_launch("k_chol_factor_solve");
+  if (s.instrument) CK(cudaEventRecord(ks.e1, st));
   if (clk_dbg) {
     std::vector<long long> hb(8 * 256);
     dbgbuf.download(hb.data(), hb.size(), st);
@@ -878,54 +935,74 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
               o[4] - o[3], o[5] - o[4], o[6] - o[5], o[7]);
     }
   }
-  if (s.instrument) CK(cudaEventRecord(s.ev1, st));
   w.r.resize(N);
   w.z.resize(N);
   w.part.resize(2 * RED_BLOCKS);
-  w.scal.resize(4);
-  int solves = 1;
+  w.scal.resize(8);
+  launch_resid(s, rhs, x);
+}
+
+int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed) {
+  Scene::Work& w = s.w;
+  Scene::Work::CholRun& run = w.ch_run;
+  cudaStream_t st = s.stream;
+  changed = false;
+  rel_res = 0.0;
+  if (!run.active) return 0;
+  run.active = false;
+  const int n = s.H.n;
+  const int64_t N = 12 * (int64_t)n;
+  const int big = 0x7fffffff;
   double* hp = s.h_pinned + 24;
   int* hb = reinterpret_cast<int*>(s.h_pinned + 28);
+  int solves = 1;
   for (int refine = 0;; ++refine) {
-    k_resid<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, H.row_ptr.p, H.col.p, H.val.p, x, rhs, w.r.p, w.part.p);
-    note_launch("k_resid");
-    reduce_fixed_multi(st, w.part.p, RED_BLOCKS, 2, w.scal.p);
-    CK(cudaMemcpyAsync(hp, w.scal.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hb, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    if (refine > 0) CK(cudaStreamSynchronize(st));
     if (*hb != big) throw Error(ABD_ERR_FACTORIZATION, "non-SPD pivot in the block Cholesky", *hb);
     const double rn = std::sqrt(hp[0]), bn = std::sqrt(hp[1]);
     rel_res = bn > 0.0 ? rn / bn : 0.0;
     if (bn == 0.0 || rn <= rel_tol * bn || refine >= max_refine) break;
-    k_chol_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, w.r.p, w.z.p);
+    CholView v = plan_view(s);
+    k_chol_solve<<<run.n_cta, CH_THREADS, 0, st>>>(v, w.r.p, w.z.p);
     note_launch("k_chol_solve");
-    k_add_inplace<<<grid_for(N, 256), 256, 0, st>>>(N, x, w.z.p);
+    k_add_inplace<<<grid_for(N, 256), 256, 0, st>>>(N, run.x, w.z.p);
     note_launch("k_add_inplace");
+    changed = true;
     ++solves;
+    launch_resid(s, run.rhs, run.x);
   }
   if (s.instrument) {
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
     Scene::KStat& k = s.kstat[0];
-    k.launches += 1;
-    k.units += solves;
-    k.ms += ms;
     // algorithmic bytes of factor + one solve: A blocks read and L written once,
     // L_ik/L_jk read per update pair, L read twice by the solve, vectors.
     const double blk = 1152.0;
-    k.bytes += blk * (double)an.n_blk * 2.0 + blk * 2.0 * (double)an.n_upd + blk * 2.0 * (double)an.n_blk +
-               4.0 * 96.0 * n;
+    k.pending = true;
+    k.p_units = solves;
+    k.p_bytes = blk * (double)run.stats[1] * 2.0 + blk * 2.0 * (double)run.stats[2] +
+                blk * 2.0 * (double)run.stats[1] + 4.0 * 96.0 * n;
     static const bool trace = getenv("ABD_TRACE_CHOL") != nullptr;
-    if (trace)
+    if (trace) {
+      float ms = 0.f;
+      CK(cudaEventSynchronize(k.e1));
+      CK(cudaEventElapsedTime(&ms, k.e0, k.e1));
       fprintf(stderr,
-              "[abd chol] n=%d edges=%lld L_blocks=%lld updates=%lld levels=%d largest=%d ctas=%d solves=%d "
-              "rel=%.2e factor+solve_ms=%.3f analysis_ms=%.3f (sync %.3f order %.3f plan %.3f) coupled=%d "
-              "cached=%d hits=%lld misses=%lld\n",
-              n, (long long)an.n_edges, (long long)an.n_blk, (long long)an.n_upd, an.max_level, an.largest,
-              an.n_cta, solves, rel_res, ms, host_ms, an.ms_sync, an.ms_order, an.ms_plan, an.n_coupled,
-              (int)an.cached, (long long)w.ch_cache.hits, (long long)w.ch_cache.misses);
+              "[abd chol] n=%d edges=%lld L_blocks=%lld updates=%lld levels=%lld largest=%lld ctas=%d solves=%d "
+              "rel=%.2e factor+solve_ms=%.3f analysis_ms=%.3f (sync %.3f order %.3f plan %.3f) coupled=%lld "
+              "cached=%lld hits=%lld misses=%lld\n",
+              n, (long long)run.stats[0], (long long)run.stats[1], (long long)run.stats[2], (long long)run.stats[3],
+              (long long)run.stats[4], run.n_cta, solves, rel_res, ms, run.host_ms, run.ms3[0], run.ms3[1],
+              run.ms3[2], (long long)run.stats[5], (long long)run.stats[6], (long long)w.ch_cache.hits,
+              (long long)w.ch_cache.misses);
+    }
   }
   return solves;
+}
+
+int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine) {
+  chol_begin(s, rhs, x);
+  CK(cudaStreamSynchronize(s.stream));
+  bool changed = false;
+  return chol_finish(s, rel_tol, rel_res, max_refine, changed);
 }
 
 }  // namespace abd

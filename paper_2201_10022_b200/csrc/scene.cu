@@ -39,6 +39,10 @@ Scene::Scene() {
   CK(cudaEventCreate(&ev1));
   CK(cudaEventCreate(&tev0));
   CK(cudaEventCreate(&tev1));
+  for (auto& k : kstat) {
+    CK(cudaEventCreate(&k.e0));
+    CK(cudaEventCreate(&k.e1));
+  }
   w.ull.resize(16);
 }
 
@@ -47,6 +51,10 @@ Scene::~Scene() {
   if (h_pinned) cudaFreeHost(h_pinned);
   for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
     if (e) cudaEventDestroy(e);
+  for (auto& k : kstat) {
+    if (k.e0) cudaEventDestroy(k.e0);
+    if (k.e1) cudaEventDestroy(k.e1);
+  }
 }
 
 void scan_exclusive_i32(Scene& s, const int* in, int* out, int64_t n) {
@@ -98,6 +106,19 @@ __global__ void k_reduce_fixed(const double* __restrict__ in, int n, double* __r
     __syncthreads();
   }
   if (threadIdx.x == 0) *out = sh[0];
+}
+
+void kstat_flush(Scene& s, int which) {
+  Scene::KStat& k = s.kstat[which];
+  if (!k.pending) return;
+  float ms = 0.f;
+  CK(cudaEventSynchronize(k.e1));
+  CK(cudaEventElapsedTime(&ms, k.e0, k.e1));
+  k.launches += 1;
+  k.units += k.p_units;
+  k.ms += ms;
+  k.bytes += k.p_bytes;
+  k.pending = false;
 }
 
 void reduce_fixed_stream(cudaStream_t st, const double* partials, int n, double* out_dev) {

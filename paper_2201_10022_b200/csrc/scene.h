@@ -171,6 +171,8 @@ struct Scene {
     DVec<int2> pairs_tmp;
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
+    DVec<double> lsred, lsscal;  // merged CCD + e0 + first-trial line-search reductions
+    DVec<int> lserr;
     DVec<double> cg_u, cg_w, cg_m, cg_q;
     // cluster block-Jacobi preconditioner (k_cg.cu)
     DVec<int> cl_slot_row, cl_slot_base, cl_slot_k, cl_off, cl_rows;
@@ -191,12 +193,26 @@ struct Scene {
       size_t offs[13] = {};
       int64_t hits = 0, misses = 0;
     } ch_cache;
+    // an in-flight chol_begin awaiting chol_finish
+    struct CholRun {
+      bool active = false;
+      const double* rhs = nullptr;
+      double* x = nullptr;
+      int n_cta = 0;
+      int64_t stats[8] = {};
+      double host_ms = 0.0, ms3[3] = {};
+    } ch_run;
   } w;
 
   // per-kernel instrumentation (CUDA events on `stream`)
   struct KStat {
     int64_t launches = 0, units = 0;
     double ms = 0.0, bytes = 0.0;
+    // lazily resolved timing of the last launch (its own event pair, no extra sync)
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    bool pending = false;
+    int64_t p_units = 0;
+    double p_bytes = 0.0;
   } kstat[4];
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
   bool instrument = true;
@@ -213,6 +229,7 @@ void sort_pairs_u64(Scene& s, uint64_t* keys, uint64_t* keys_alt, int* vals, int
 void sort_pairs_u32(Scene& s, uint32_t* keys, uint32_t* keys_alt, int* vals, int* vals_alt, int64_t n, int end_bit,
                     bool& result_in_alt);
 double reduce_sum_det(Scene& s, const double* partials, int n);  // deterministic
+void kstat_flush(Scene& s, int which);  // resolve a pending lazily-timed launch
 
 inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
 int bits_for(int64_t maxval);
