@@ -43,7 +43,10 @@ ABD_D double accd_query(int kind, V3* x, const V3* dx, double slack, double tmax
     t = reached ? tmax : tn;
     if (stalled || reached) break;
     for (int k = 0; k < 4; ++k) x[k] = xadd3(x[k], xscale(tl, p[k]));
-    if (t_cut_bits) {
+    // early exit once this query can no longer lower the global minimum; the
+    // shared bound lives in L2, so it is polled every 8 iterations (returning any
+    // t >= the bound leaves the minimum unchanged)
+    if (t_cut_bits && (it & 7) == 7) {
       unsigned long long cb = *t_cut_bits;
       if (t >= __longlong_as_double((long long)cb)) break;
     }

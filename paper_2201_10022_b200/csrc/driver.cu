@@ -111,6 +111,8 @@ struct EventTimer {
   }
 };
 
+static void mark_structure(Scene& s);
+
 // flags + exclusive scan of candidate activity (d^2 < d_hat^2) into s.w.flags/pos;
 // returns the active count (one host sync, also checks the barrier domain)
 static int active_scan(Scene& s, const double* q, double dh) {
@@ -135,9 +137,10 @@ static int active_scan(Scene& s, const double* q, double dh) {
   return hp[0];
 }
 
-int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project) {
+int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark) {
   int64_t n_vf = s.cands.n_vf;
   int total = active_scan(s, q, dh);
+  if (mark) mark_structure(s);
   s.pblk.bodies.resize(std::max(total, 1));
   s.pblk.blk.resize((int64_t)std::max(total, 1) * PB_STRIDE);
   s.pblk.d2.resize(std::max(total, 1));
@@ -371,14 +374,90 @@ double candidate_min_d2(Scene& s, const double* q) {
   return bits_to_d(hb[0]);
 }
 
+// coupling structure for the Cholesky analysis: pattern blocks touched by an
+// active contact or a friction pair between two dynamic bodies (a superset of
+// the nonzero blocks), marked by binary search in the sorted upper keys
+__global__ void k_mark_active(int64_t n, const int2* __restrict__ bodies, const int* __restrict__ slot,
+                              int64_t n_off, const int2* __restrict__ keys, int* flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int2 b = bodies[i];
+  int sa = slot[b.x], sb = slot[b.y];
+  if (sa < 0 || sb < 0 || sa == sb) return;
+  int a = min(sa, sb), c = max(sa, sb);
+  int64_t lo = 0, hi = n_off - 1;
+  while (lo <= hi) {
+    int64_t m = (lo + hi) >> 1;
+    int2 k = keys[m];
+    if (k.x < a || (k.x == a && k.y < c)) lo = m + 1;
+    else if (k.x == a && k.y == c) {
+      flags[m] = 1;
+      return;
+    } else hi = m - 1;
+  }
+}
+
+__global__ void k_mark_active_rows(int64_t n, const int4* __restrict__ rows, const int* __restrict__ act,
+                                   const int* __restrict__ slot, int64_t n_off, const int2* __restrict__ keys,
+                                   int* flags) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || !act[i]) return;
+  int4 r = rows[i];
+  int sa = slot[r.x], sb = slot[r.z];
+  if (sa < 0 || sb < 0 || sa == sb) return;
+  int a = min(sa, sb), c = max(sa, sb);
+  int64_t lo = 0, hi = n_off - 1;
+  while (lo <= hi) {
+    int64_t m = (lo + hi) >> 1;
+    int2 k = keys[m];
+    if (k.x < a || (k.x == a && k.y < c)) lo = m + 1;
+    else if (k.x == a && k.y == c) {
+      flags[m] = 1;
+      return;
+    } else hi = m - 1;
+  }
+}
+
+// structure flags (active contact candidates + friction pairs) copied to the host
+// right after the activity scan, so the host analysis overlaps the pair blocks
+static void mark_structure(Scene& s) {
+  Scene::Work& w = s.w;
+  const int64_t n_off = s.H.n_off;
+  w.ch_flags.resize(std::max<int64_t>(n_off, 1));
+  if (n_off) {
+    w.ch_flags.zero(s.stream);
+    const int64_t n_vf = s.cands.n_vf, n_ee = s.cands.n_ee;
+    if (n_vf)
+      k_mark_active_rows<<<grid_for(n_vf, 256), 256, 0, s.stream>>>(n_vf, s.cands.vf.p, w.flags.p, s.slot.p, n_off,
+                                                                    s.H.upper_keys.p, w.ch_flags.p);
+    if (n_ee)
+      k_mark_active_rows<<<grid_for(n_ee, 256), 256, 0, s.stream>>>(n_ee, s.cands.ee.p, w.flags.p + n_vf, s.slot.p,
+                                                                    n_off, s.H.upper_keys.p, w.ch_flags.p);
+    note_launch("k_mark_active_rows");
+    if (s.fric.n) {
+      k_mark_active<<<grid_for(s.fric.n, 256), 256, 0, s.stream>>>(s.fric.n, s.fric.bodies.p, s.slot.p, n_off,
+                                                                   s.H.upper_keys.p, w.ch_flags.p);
+      note_launch("k_mark_active");
+    }
+    int* hm = w.h_meta.reserve(3 * (size_t)n_off);
+    CK(cudaMemcpyAsync(hm, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaMemcpyAsync(hm + n_off, s.H.upper_keys.p, n_off * sizeof(int2), cudaMemcpyDeviceToHost, s.stream));
+  }
+  if (!w.ch_pre_ev) CK(cudaEventCreateWithFlags(&w.ch_pre_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(w.ch_pre_ev, s.stream));
+  w.ch_pre = true;
+}
+
 void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v) {
   int n = s.n_dyn;
   s.w.grad0.resize(std::max(12 * n, 1));
   s.w.diag0.resize(std::max(144 * n, 1));
   launch_body_terms(s, q, qt, dt, s.w.grad0.p, s.w.diag0.p, nullptr, 1);
-  contact_blocks(s, q, kappa, dh, 1);
-  append_friction_blocks(s, q, dt, eps_v, 1);
+  // the pattern depends only on the overlap and friction pairs: build it first so
+  // the Cholesky analysis inputs can be copied out while the values are reduced
   build_pattern(s, s.cands.ov.p, s.cands.n_ov, s.fric.bodies.p, s.fric.n);
+  contact_blocks(s, q, kappa, dh, 1, /*mark=*/true);
+  append_friction_blocks(s, q, dt, eps_v, 1);
   reduce_system(s, s.w.diag0.p, s.w.grad0.p);
 }
 
@@ -400,6 +479,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
     s.forces.resize(NB);
     s.forces.zero(stream);
   }
+  s.w.ch_cache.valid = false;  // Cholesky plans are reused within a step only
   s.q0.resize(NB);
   s.q_tilde.resize(NB);
   s.dq.resize(NB);

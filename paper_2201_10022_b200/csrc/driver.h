@@ -19,7 +19,7 @@ void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, cons
 // k_stats.cu
 double global_min_distance(Scene& s, const double* q);
 // driver.cu
-int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project);
+int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark = false);
 void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, int project);
 int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, double mu, DVec<double>* basis);
 double contact_energy(Scene& s, const double* q, double kappa, double dh);

@@ -49,7 +49,8 @@ struct CholView {
   const int* cta_nlvl;  // per CTA: number of levels
   const int* col_ptr;   // n + 1: off-diagonal blocks of column j (index k -> L block n + k)
   const int* blk_row;   // per off block: row node i
-  const int* blk_apos;  // per off block: position of A(i, j) in the BSR (-1: fill)
+  const int* bsr_row;   // BSR row_ptr / col: A(i, j) found by binary search in row i (absent: fill)
+  const int* bsr_col;
   const int* row_ptr;   // n + 1: range into row_blk (blocks L_jk, k eliminated before j)
   const int* row_blk;   // L block index
   const int* row_col;   // column node k of each row_blk entry
@@ -66,6 +67,19 @@ struct CholView {
 
 // full-warp shuffles: every lane of a warp runs the same node, so no partial-mask
 // convergence checks are generated
+// position of block (r, c) in the sorted-column CSR, or -1
+__device__ __forceinline__ int bsr_find(const int* __restrict__ row_ptr, const int* __restrict__ col, int r, int c) {
+  int lo = row_ptr[r], hi = row_ptr[r + 1] - 1;
+  while (lo <= hi) {
+    const int m = (lo + hi) >> 1;
+    const int cm = col[m];
+    if (cm == c) return m;
+    if (cm < c) lo = m + 1;
+    else hi = m - 1;
+  }
+  return -1;
+}
+
 __device__ __forceinline__ double hshfl(unsigned mask, double v, int src) { return __shfl_sync(mask, v, src); }
 
 // 1/sqrt(x) without the libdevice slow-path call (whose register saves would put
@@ -221,7 +235,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
       // off-diagonal blocks of column j: L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
       for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
         double bt[12];
-        const int ap = v.blk_apos[bb];
+        const int ap = bsr_find(v.bsr_row, v.bsr_col, v.blk_row[bb], j);
         if (ap >= 0) {
           const double* A = v.val + 144 * (int64_t)ap + 12 * tt;
 #pragma unroll
@@ -436,7 +450,7 @@ struct Analysis {
   int n_cta = 0, n_coupled = 0;
   int64_t n_blk = 0, n_upd = 0, n_edges = 0;
   int max_level = 0, largest = 0;
-  double ms_sync = 0, ms_order = 0, ms_plan = 0;
+  double ms_sync = 0, ms_order = 0, ms_plan = 0, ms_sub[6] = {};
   bool cached = false;
   CholView view{};
 };
@@ -491,16 +505,18 @@ static Analysis chol_analyze(Scene& s) {
   const int64_t n_off = H.n_off;
   Analysis an;
   auto t0 = clk::now();
-  // flags | upper_pos | lower_pos | keys (2 ints) per pattern block, one pinned staging buffer
-  int* hm = w.h_meta.reserve(5 * (size_t)std::max<int64_t>(n_off, 1));
-  int *flags = hm, *upos = hm + n_off, *lpos = hm + 2 * n_off, *keys = hm + 3 * n_off;
-  if (n_off) {
+  // flags | keys (2 ints) per pattern block, one pinned staging buffer
+  int* hm = w.h_meta.reserve(3 * (size_t)std::max<int64_t>(n_off, 1));
+  int *flags = hm, *keys = hm + n_off;
+  if (w.ch_pre) {
+    // structure from the active pairs, already on its way to the host (assemble)
+    w.ch_pre = false;
+    CK(cudaEventSynchronize(w.ch_pre_ev));
+  } else if (n_off) {
     w.ch_flags.resize(n_off);
     k_block_nz<<<grid_for(n_off * 32, 256), 256, 0, st>>>(n_off, H.upper_pos.p, H.val.p, w.ch_flags.p);
     note_launch("k_block_nz");
     CK(cudaMemcpyAsync(flags, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(upos, H.upper_pos.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(lpos, H.lower_pos.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(keys, H.upper_keys.p, n_off * sizeof(int2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
@@ -516,7 +532,8 @@ static Analysis chol_analyze(Scene& s) {
                     dp + o[3],
                     dp + o[4],
                     dp + o[5],
-                    dp + o[6],
+                    H.row_ptr.p,
+                    H.col.p,
                     dp + o[7],
                     dp + o[8],
                     dp + o[9],
@@ -528,9 +545,13 @@ static Analysis chol_analyze(Scene& s) {
                     w.ch_dinv.p,
                     w.bad.p};
   };
-  if (cc.valid && cc.n == n && cc.n_off == n_off &&
-      std::equal(flags, flags + n_off, cc.meta.begin()) &&
-      std::equal(keys, keys + 2 * n_off, cc.meta.begin() + n_off)) {
+  // nonzero couplings (keys are sorted (i < j)); the cached plan is reused when
+  // they are a subset of the cached graph (extra blocks then hold exact zeros)
+  std::vector<uint64_t>& cur = w.ch_edges_cur;
+  cur.clear();
+  for (int64_t k = 0; k < n_off; ++k)
+    if (flags[k]) cur.push_back(((uint64_t)(uint32_t)keys[2 * k] << 32) | (uint32_t)keys[2 * k + 1]);
+  if (cc.valid && cc.n == n && std::includes(cc.edges.begin(), cc.edges.end(), cur.begin(), cur.end())) {
     an.n_cta = (int)cc.stats[0];
     an.n_coupled = (int)cc.stats[1];
     an.n_blk = cc.stats[2];
@@ -544,15 +565,24 @@ static Analysis chol_analyze(Scene& s) {
     return an;
   }
   ++cc.misses;
+  // Build the plan for the union with the previously analysed graph of this step
+  // (contacts come and go across Newton iterations; the union keeps later
+  // iterations on the resident plan).  ch_cache.valid is reset per time step.
+  static const bool no_union = getenv("ABD_CHOL_NO_UNION") != nullptr;
+  if (cc.valid && cc.n == n && !no_union) {
+    std::vector<uint64_t> un;
+    un.reserve(cur.size() + cc.edges.size());
+    std::set_union(cur.begin(), cur.end(), cc.edges.begin(), cc.edges.end(), std::back_inserter(un));
+    cur.swap(un);
+  }
 
   // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order
   std::vector<int> loc(n, -1), glob;
-  for (int64_t k = 0; k < n_off; ++k)
-    if (flags[k]) {
-      loc[keys[2 * k]] = 0;
-      loc[keys[2 * k + 1]] = 0;
-      ++an.n_edges;
-    }
+  for (uint64_t e : cur) {
+    loc[(int)(e >> 32)] = 0;
+    loc[(int)(e & 0xffffffffu)] = 0;
+    ++an.n_edges;
+  }
   for (int v = 0; v < n; ++v)
     if (loc[v] == 0) {
       loc[v] = (int)glob.size();
@@ -562,20 +592,18 @@ static Analysis chol_analyze(Scene& s) {
   an.n_coupled = m;
   // adjacency (CSR) in key order is already sorted per node (keys sorted by (i, j))
   std::vector<int> adj_ptr(m + 1, 0), adj_idx(2 * an.n_edges);
-  for (int64_t k = 0; k < n_off; ++k)
-    if (flags[k]) {
-      adj_ptr[loc[keys[2 * k]] + 1]++;
-      adj_ptr[loc[keys[2 * k + 1]] + 1]++;
-    }
+  for (uint64_t e : cur) {
+    adj_ptr[loc[(int)(e >> 32)] + 1]++;
+    adj_ptr[loc[(int)(e & 0xffffffffu)] + 1]++;
+  }
   for (int v = 0; v < m; ++v) adj_ptr[v + 1] += adj_ptr[v];
   {
     std::vector<int> fp(adj_ptr.begin(), adj_ptr.end() - 1);
-    for (int64_t k = 0; k < n_off; ++k)
-      if (flags[k]) {
-        int a2 = loc[keys[2 * k]], b2 = loc[keys[2 * k + 1]];
-        adj_idx[fp[a2]++] = b2;
-        adj_idx[fp[b2]++] = a2;
-      }
+    for (uint64_t e : cur) {
+      int a2 = loc[(int)(e >> 32)], b2 = loc[(int)(e & 0xffffffffu)];
+      adj_idx[fp[a2]++] = b2;
+      adj_idx[fp[b2]++] = a2;
+    }
   }
   // Elimination order: peel degree <= 1 nodes first (no fill: contact graphs are
   // mostly forests of chains), then minimum degree on the remaining 2-core.
@@ -651,22 +679,11 @@ static Analysis chol_analyze(Scene& s) {
   an.ms_order = ms_since(t0);
   t0 = clk::now();
 
-  auto apos_of = [&](int gi, int gj) -> int {  // BSR position of A(gi, gj) (nonzero coupling)
-    int a = std::min(gi, gj), b = std::max(gi, gj);
-    int64_t lo = 0, hi = n_off - 1;
-    while (lo <= hi) {
-      int64_t mm = (lo + hi) >> 1;
-      int kx = keys[2 * mm], ky = keys[2 * mm + 1];
-      if (kx < a || (kx == a && ky < b)) lo = mm + 1;
-      else if (kx == a && ky == b) return flags[mm] ? (gi < gj ? upos[mm] : lpos[mm]) : -1;
-      else hi = mm - 1;
-    }
-    return -1;
-  };
   // off-diagonal L blocks: column (local) v owns [col_off[v], col_off[v+1])
   const std::vector<int>& col_off = csp;
   const int nbo = csp[m];
   an.n_blk = n + (int64_t)nbo;
+  an.ms_sub[0] = ms_since(t0);
   // row lists (local i): (k, off block) for k eliminated before i, in elimination order of k
   std::vector<int> rcnt(m + 1, 0);
   for (int e = 0; e < nbo; ++e) rcnt[csi[e] + 1]++;
@@ -679,6 +696,7 @@ static Analysis chol_analyze(Scene& s) {
       r_b[rfill[i]] = e;
       rfill[i]++;
     }
+  an.ms_sub[1] = ms_since(t0);
   // update pairs for off block (i, j): k in rows(j) with i in cs[k]
   std::vector<int> upd_ptr(nbo + 1, 0), upd;
   for (int j = 0; j < m; ++j)
@@ -696,6 +714,7 @@ static Analysis chol_analyze(Scene& s) {
       upd_ptr[b + 1] = (int)(upd.size() / 2);
     }
   an.n_upd = (int64_t)upd.size() / 2;
+  an.ms_sub[2] = ms_since(t0);
   // elimination-tree levels and component roots (local)
   std::vector<int> level(m, 0), root(m);
   for (int v : order)
@@ -724,6 +743,7 @@ static Analysis chol_analyze(Scene& s) {
     for (int x : h) fprintf(stderr, " %d", x);
     fprintf(stderr, "\n");
   }
+  an.ms_sub[3] = ms_since(t0);
   // CTAs: components (largest first onto the least loaded), then isolated nodes
   const int n_iso = n - m;
   const int iso_per_cta = 4 * CH_HW;
@@ -747,6 +767,7 @@ static Analysis chol_analyze(Scene& s) {
   }
   for (int c = n_ccta; c < n_cta; ++c) cta_nlvl[c] = (n_iso > 0) ? 1 : 0;
 
+  an.ms_sub[4] = ms_since(t0);
   // packed plan: nodes | lvl_ptr | cta_lvl | cta_nlvl | col_ptr | blk_row | blk_apos | row_ptr |
   //              row_blk | row_col | upd_ptr | (pad) | upd pairs
   int n_lvl_entries = 0;
@@ -804,7 +825,6 @@ static Analysis chol_analyze(Scene& s) {
       if (l >= 0) {
         for (int b = csp[l]; b < csp[l + 1]; ++b) {  // b == c + q: locals follow global order
           hp[off_brow + b] = glob[csi[b]];
-          hp[off_bapos + b] = apos_of(glob[csi[b]], v);
         }
         c += csp[l + 1] - csp[l];
         for (int e2 = rcnt[l]; e2 < rcnt[l + 1]; ++e2) {
@@ -817,6 +837,7 @@ static Analysis chol_analyze(Scene& s) {
     col_ptr[n] = c;
     row_ptr[n] = r;
   }
+  an.ms_sub[5] = ms_since(t0);
   std::copy(upd_ptr.begin(), upd_ptr.end(), hp + off_updp);
   std::copy(upd.begin(), upd.end(), hp + off_upd);
   w.ch_plan.resize(total);
@@ -829,12 +850,16 @@ static Analysis chol_analyze(Scene& s) {
   cc.valid = true;
   cc.n = n;
   cc.n_off = n_off;
-  cc.meta.assign(flags, flags + n_off);
-  cc.meta.insert(cc.meta.end(), keys, keys + 2 * n_off);
+  cc.edges.swap(cur);
   const int64_t st8[8] = {an.n_cta, an.n_coupled, an.n_blk, an.n_upd, an.n_edges, an.max_level, an.largest, 0};
   std::copy(st8, st8 + 8, cc.stats);
   std::copy(offs, offs + 13, cc.offs);
   an.ms_plan = ms_since(t0);
+  static const bool trace_sub = getenv("ABD_TRACE_CHOL") != nullptr;
+  if (trace_sub)
+    fprintf(stderr, "[abd chol plan] cum ms: %.3f %.3f %.3f %.3f %.3f %.3f end %.3f (m=%d nbo=%d total=%zu)\n",
+            an.ms_sub[0], an.ms_sub[1], an.ms_sub[2], an.ms_sub[3], an.ms_sub[4], an.ms_sub[5], an.ms_plan, m, nbo,
+            total);
   return an;
 }
 
@@ -853,7 +878,8 @@ static CholView plan_view(Scene& s) {
                   dp + o[3],
                   dp + o[4],
                   dp + o[5],
-                  dp + o[6],
+                  s.H.row_ptr.p,
+                  s.H.col.p,
                   dp + o[7],
                   dp + o[8],
                   dp + o[9],

@@ -209,6 +209,7 @@ __global__ void k_row_of(int n, const int* __restrict__ row_ptr, int* row_of) {
 // build pattern + CSR from overlap pairs and friction pairs (dyn-dyn only)
 void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f) {
   Bsr& H = s.H;
+  s.w.ch_pre = false;  // any structure copied out for the Cholesky belongs to the old pattern
   cudaStream_t st = s.stream;
   int n = s.n_dyn;
   H.n = n;

@@ -51,6 +51,7 @@ Scene::~Scene() {
   if (h_pinned) cudaFreeHost(h_pinned);
   for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
     if (e) cudaEventDestroy(e);
+  if (w.ch_pre_ev) cudaEventDestroy(w.ch_pre_ev);
   for (auto& k : kstat) {
     if (k.e0) cudaEventDestroy(k.e0);
     if (k.e1) cudaEventDestroy(k.e1);

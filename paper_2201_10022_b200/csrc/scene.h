@@ -188,11 +188,15 @@ struct Scene {
       bool valid = false;
       int n = 0;
       int64_t n_off = 0;
-      std::vector<int> meta;
+      std::vector<uint64_t> edges;  // (i << 32 | j) nonzero couplings the plan was built for
       int64_t stats[8] = {};
       size_t offs[13] = {};
       int64_t hits = 0, misses = 0;
     } ch_cache;
+    std::vector<uint64_t> ch_edges_cur;
+    // structure flags + keys copied out by assemble() (event-ordered); consumed once
+    bool ch_pre = false;
+    cudaEvent_t ch_pre_ev = nullptr;
     // an in-flight chol_begin awaiting chol_finish
     struct CholRun {
       bool active = false;
