@@ -491,6 +491,16 @@ int abd_get_candidates(abd_scene* h, int64_t* vf, int64_t* ee, int64_t* ov) {
     s.cands.ee.download(b.data(), b.size(), s.stream);
     s.cands.ov.download(c.data(), c.size(), s.stream);
     sync(s.stream);
+    // the device keeps a deterministic per-overlap-pair order; the API returns the
+    // reference's canonical (c0, c2, c1, c3) order (contact.py:404)
+    auto canon = [](const int4& p, const int4& q) {
+      if (p.x != q.x) return p.x < q.x;
+      if (p.z != q.z) return p.z < q.z;
+      if (p.y != q.y) return p.y < q.y;
+      return p.w < q.w;
+    };
+    std::sort(a.begin(), a.end(), canon);
+    std::sort(b.begin(), b.end(), canon);
     for (size_t i = 0; i < a.size(); ++i) {
       vf[4 * i] = a[i].x; vf[4 * i + 1] = a[i].y; vf[4 * i + 2] = a[i].z; vf[4 * i + 3] = a[i].w;
     }

@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(BP_THREADS) k_prim_pairs(PrimGeo g, int64_t n_
 // Requires max_v <= P2_VCAP; larger meshes use k_prim_pairs.
 constexpr int P2_THREADS = 256;
 constexpr int P2_VCAP = 256;
+constexpr int P2_HCAP = 1024;  // hits per (pair, product) sorted in shared memory
 
 // box of a primitive from packed local vertex ids (8 bits each, P2_VCAP = 256)
 __device__ __forceinline__ void box_from_packed(int kind, unsigned pk, const double* vb, double* bx) {
@@ -391,12 +392,15 @@ __device__ __forceinline__ void box_from_cache(const PrimGeo& g, int kind, int g
 __global__ void __launch_bounds__(P2_THREADS, 3)
     k_prim_pairs2(PrimGeo g, int64_t n_ov, const int2* __restrict__ ov, const double* __restrict__ bbox,
                   unsigned long long* counters, int64_t cap_vf, int64_t cap_ee, int4* out_vf, int4* out_ee,
-                  int cap_list) {
+                  int cap_list, int2* tab, int* unsorted) {
   extern __shared__ double p2_sm[];
   double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
   double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
   int* lists = reinterpret_cast<int*>(obx + 6 * (size_t)cap_list);  // [6][cap_list] local ids
   unsigned* lpk = reinterpret_cast<unsigned*>(lists + 6 * (size_t)cap_list);  // packed local vertex ids
+  unsigned* hk = lpk + 6 * (size_t)cap_list;  // [P2_HCAP] hits of the current product
+  __shared__ int hcount;
+  __shared__ unsigned long long hbase;
   __shared__ int meta[16];  // v0,e0,t0 (i) | v0,e0,t0 (j) | nv,ne,nt (i) | nv,ne,nt (j)
   __shared__ int lcount[6];
   __shared__ double obox[6];
@@ -482,7 +486,10 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int la = prod == 0 ? 0 : (prod == 1 ? 3 : 1);  // list of side a
       const int lb = prod == 0 ? 5 : (prod == 1 ? 2 : 4);  // list of side b
       const int ca = lcount[la], cb = lcount[lb];
-      if (ca == 0 || cb == 0) continue;  // uniform across the CTA
+      if (ca == 0 || cb == 0) {  // uniform across the CTA
+        if (threadIdx.x == 0) tab[3 * pi + prod] = make_int2(0, 0);
+        continue;
+      }
       const int ka = la % 3, kb = lb % 3, sa = la / 3, sb = lb / 3;
       const bool a_thr = ca >= cb;  // thread side = a
       const int nt = a_thr ? ca : cb, nl = a_thr ? cb : ca;
@@ -497,44 +504,125 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int body_a = prod == 1 ? bj : bi, body_b = prod == 1 ? bi : bj;
       const int G = nt >= P2_THREADS ? 1 : P2_THREADS / nt;
       const int Lc = (nl + G - 1) / G;
-      for (int base = 0; base < nt * G; base += P2_THREADS) {
-        const int idx = base + threadIdx.x;
-        const bool live = idx < nt * G;
-        const int own = live ? idx % nt : 0, chunk = idx / nt;
-        double ob[6];
-        const int own_local = live ? lists[lt * cap_list + own] : 0;
-        if (live) box_from_packed(kt, lpk[lt * cap_list + own], vb + 6 * st_ * P2_VCAP, ob);
-        const int y0 = chunk * Lc;
-        for (int yy = 0; yy < Lc; ++yy) {
-          const int y = y0 + yy;
-          bool hit = false;
-          if (live && y < nl) {
-            const double* b2 = obx + 6 * y;
-            hit = ob[0] <= b2[3] && b2[0] <= ob[3] && ob[1] <= b2[4] && b2[1] <= ob[4] && ob[2] <= b2[5] &&
-                  b2[2] <= ob[5];
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, hit);
-          if (m) {
-            const int lane = threadIdx.x & 31;
-            unsigned long long base2 = 0;
-            if (lane == __ffs(m) - 1) base2 = atomicAdd(counters + (is_vf ? 0 : 1), (unsigned long long)__popc(m));
-            base2 = __shfl_sync(0xffffffffu, base2, __ffs(m) - 1);
-            if (hit) {
-              const unsigned long long at = base2 + __popc(m & ((1u << lane) - 1));
-              const int yl = lists[ll * cap_list + y];
-              const int pa = a_thr ? own_local : yl, pb = a_thr ? yl : own_local;
-              if (is_vf) {
-                if ((int64_t)at < cap_vf) out_vf[at] = make_int4(body_a, pa, body_b, pb);
-              } else {
-                if ((int64_t)at < cap_ee) out_ee[at] = make_int4(body_a, pa, body_b, pb);
+      if (threadIdx.x == 0) hcount = 0;
+      __syncthreads();
+      // pass 0: hits into shared memory; pass 1 (only when they overflow P2_HCAP):
+      // straight into the reserved chunk, which is then flagged for a global sort
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+          if (hcount <= P2_HCAP) break;  // uniform
+          __syncthreads();
+          if (threadIdx.x == 0) hcount = 0;
+          __syncthreads();
+        }
+        for (int base = 0; base < nt * G; base += P2_THREADS) {
+          const int idx = base + threadIdx.x;
+          const bool live = idx < nt * G;
+          const int own = live ? idx % nt : 0, chunk = idx / nt;
+          double ob[6];
+          const int own_local = live ? lists[lt * cap_list + own] : 0;
+          if (live) box_from_packed(kt, lpk[lt * cap_list + own], vb + 6 * st_ * P2_VCAP, ob);
+          const int y0 = chunk * Lc;
+          for (int yy = 0; yy < Lc; ++yy) {
+            const int y = y0 + yy;
+            bool hit = false;
+            if (live && y < nl) {
+              const double* b2 = obx + 6 * y;
+              hit = ob[0] <= b2[3] && b2[0] <= ob[3] && ob[1] <= b2[4] && b2[1] <= ob[4] && ob[2] <= b2[5] &&
+                    b2[2] <= ob[5];
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (m) {
+              const int lane = threadIdx.x & 31;
+              int b0 = 0;
+              if (lane == __ffs(m) - 1) b0 = atomicAdd(&hcount, __popc(m));
+              b0 = __shfl_sync(0xffffffffu, b0, __ffs(m) - 1);
+              if (hit) {
+                const int at = b0 + __popc(m & ((1u << lane) - 1));
+                const int yl = lists[ll * cap_list + y];
+                const int pa = a_thr ? own_local : yl, pb = a_thr ? yl : own_local;
+                if (pass == 0) {
+                  if (at < P2_HCAP) hk[at] = ((unsigned)pa << 16) | (unsigned)pb;
+                } else {
+                  const unsigned long long g2 = hbase + (unsigned long long)at;
+                  if (is_vf) {
+                    if ((int64_t)g2 < cap_vf) out_vf[g2] = make_int4(body_a, pa, body_b, pb);
+                  } else {
+                    if ((int64_t)g2 < cap_ee) out_ee[g2] = make_int4(body_a, pa, body_b, pb);
+                  }
+                }
               }
             }
           }
+        }
+        __syncthreads();
+        if (pass == 0) {
+          const int cnt = hcount;
+          if (threadIdx.x == 0) {
+            hbase = cnt ? atomicAdd(counters + (is_vf ? 0 : 1), (unsigned long long)cnt) : 0ull;
+            tab[3 * pi + prod] = make_int2((int)hbase, cnt);
+            if (cnt > P2_HCAP) atomicExch(unsorted, 1);
+          }
+          if (cnt > 0 && cnt <= P2_HCAP) {
+            // deterministic in-chunk order: bitonic sort of the packed (prim_a, prim_b)
+            int P2 = 1;
+            while (P2 < cnt) P2 <<= 1;
+            for (int t = cnt + threadIdx.x; t < P2; t += P2_THREADS) hk[t] = 0xffffffffu;
+            __syncthreads();
+            for (int k = 2; k <= P2; k <<= 1)
+              for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                for (int t = threadIdx.x; t < P2; t += P2_THREADS) {
+                  const int u = t ^ jj;
+                  if (u > t) {
+                    const bool up = (t & k) == 0;
+                    const unsigned a = hk[t], b = hk[u];
+                    if ((a > b) == up) {
+                      hk[t] = b;
+                      hk[u] = a;
+                    }
+                  }
+                }
+                __syncthreads();
+              }
+            const unsigned long long b0 = hbase;
+            for (int t = threadIdx.x; t < cnt; t += P2_THREADS) {
+              const unsigned long long g2 = b0 + (unsigned long long)t;
+              const int pa = (int)(hk[t] >> 16), pb = (int)(hk[t] & 0xffffu);
+              if (is_vf) {
+                if ((int64_t)g2 < cap_vf) out_vf[g2] = make_int4(body_a, pa, body_b, pb);
+              } else {
+                if ((int64_t)g2 < cap_ee) out_ee[g2] = make_int4(body_a, pa, body_b, pb);
+              }
+            }
+          }
+          __syncthreads();
         }
       }
       __syncthreads();
     }
   }
+}
+
+// chunk table -> per-list counts in (pair, product) order
+__global__ void k_chunk_counts(int64_t n_ov, const int2* __restrict__ tab, int* cnt_vf, int* cnt_ee) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n_ov) return;
+  cnt_vf[2 * p] = tab[3 * p].y;
+  cnt_vf[2 * p + 1] = tab[3 * p + 1].y;
+  cnt_ee[p] = tab[3 * p + 2].y;
+}
+
+// move every chunk to its final offset (warp per chunk)
+__global__ void k_chunk_move(int64_t n_ov, const int2* __restrict__ tab, int prod_lo, int nprod,
+                             const int* __restrict__ dst_off, const int4* __restrict__ src, int4* dst) {
+  int64_t wgl = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (wgl >= n_ov * nprod) return;
+  const int64_t p = wgl / nprod;
+  const int pr = prod_lo + (int)(wgl % nprod);
+  const int2 e = tab[3 * p + pr];
+  const int d = dst_off[wgl];
+  for (int k = lane; k < e.y; k += 32) dst[d + k] = src[e.x + k];
 }
 
 // keys for canonical order (c0, c2, c1, c3): two LSD passes with stable sorts
@@ -908,6 +996,8 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   // primitive pairs
   PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
   unsigned long long* counters = w.ull.p + 4;
+  int* unsorted = reinterpret_cast<int*>(w.ull.p + 8);
+  bool chunked = false;
   if (c.vf.cap < 1024) c.vf.resize(1024);
   if (c.ee.cap < 1024) c.ee.resize(1024);
   unsigned long long* hc = reinterpret_cast<unsigned long long*>(s.h_pinned);
@@ -915,8 +1005,8 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
     static bool attr = false;
     const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
-    const size_t p2_smem =
-        sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) + 2 * sizeof(int) * 6 * (size_t)cap_list;
+    const size_t p2_smem = sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) +
+                           2 * sizeof(int) * 6 * (size_t)cap_list + sizeof(unsigned) * P2_HCAP;
     const bool use2 = s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1");
     if (!attr) {
       CK(cudaFuncSetAttribute((void*)k_prim_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM));
@@ -926,8 +1016,11 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     if (s.instrument) CK(cudaEventRecord(s.ev0, st));
     if (use2) {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 3);
+      w.tab.resize(3 * (size_t)n_ov);
+      CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
       k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
-                                                       (int64_t)c.ee.cap, c.vf.p, c.ee.p, cap_list);
+                                                       (int64_t)c.ee.cap, c.vf.p, c.ee.p, cap_list, w.tab.p,
+                                                       unsorted);
     } else {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
       k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
@@ -936,7 +1029,9 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     note_launch("k_prim_pairs");
     if (s.instrument) CK(cudaEventRecord(s.ev1, st));
     CK(cudaMemcpyAsync(hc, counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc + 2, unsorted, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;
     if (s.instrument) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
@@ -956,8 +1051,41 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   c.n_ee = (int64_t)hc[1];
   c.vf.n = c.n_vf;
   c.ee.n = c.n_ee;
-  sort_rows(s, c.vf, c.n_vf, bits_for(s.max_v - 1), bits_for(s.max_t - 1));
-  sort_rows(s, c.ee, c.n_ee, bits_for(s.max_e - 1), bits_for(s.max_e - 1));
+  if (!chunked) {
+    // canonical (c0, c2, c1, c3) order by radix sort
+    sort_rows(s, c.vf, c.n_vf, bits_for(s.max_v - 1), bits_for(s.max_t - 1));
+    sort_rows(s, c.ee, c.n_ee, bits_for(s.max_e - 1), bits_for(s.max_e - 1));
+    return;
+  }
+  // Deterministic order without a global sort: (overlap pair, product, prim_a, prim_b).
+  // Each (pair, product) chunk was sorted in shared memory; chunks move to their
+  // prefix-sum offsets in pair order.  (abd_get_candidates returns the canonical order.)
+  w.cnt.resize(2 * n_ov + 1);
+  w.off.resize(2 * n_ov + 1);
+  w.va.resize(n_ov + 1);
+  w.vb.resize(n_ov + 1);
+  k_chunk_counts<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, w.tab.p, w.cnt.p, w.va.p);
+  note_launch("k_chunk_counts");
+  scan_exclusive_i32(s, w.cnt.p, w.off.p, 2 * n_ov);
+  scan_exclusive_i32(s, w.va.p, w.vb.p, n_ov);
+  w.rows_tmp.resize(std::max<int64_t>(c.n_vf, 1));
+  if (c.n_vf) {
+    k_chunk_move<<<grid_for(2 * n_ov * 32, 256), 256, 0, st>>>(n_ov, w.tab.p, 0, 2, w.off.p, c.vf.p, w.rows_tmp.p);
+    note_launch("k_chunk_move");
+    std::swap(c.vf.p, w.rows_tmp.p);
+    std::swap(c.vf.cap, w.rows_tmp.cap);
+    std::swap(c.vf.n, w.rows_tmp.n);
+    c.vf.n = c.n_vf;
+  }
+  w.rows_tmp.resize(std::max<int64_t>(c.n_ee, 1));
+  if (c.n_ee) {
+    k_chunk_move<<<grid_for(n_ov * 32, 256), 256, 0, st>>>(n_ov, w.tab.p, 2, 1, w.vb.p, c.ee.p, w.rows_tmp.p);
+    note_launch("k_chunk_move");
+    std::swap(c.ee.p, w.rows_tmp.p);
+    std::swap(c.ee.cap, w.rows_tmp.cap);
+    std::swap(c.ee.n, w.rows_tmp.n);
+    c.ee.n = c.n_ee;
+  }
 }
 
 }  // namespace abd

@@ -168,6 +168,7 @@ struct Scene {
     DVec<uint32_t> ka, kb;
     DVec<int> va, vb;
     DVec<int4> rows_tmp;
+    DVec<int2> tab;  // broad phase (pair, product) -> (chunk start, count)
     DVec<int2> pairs_tmp;
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
