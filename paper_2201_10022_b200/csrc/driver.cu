@@ -128,12 +128,17 @@ static int active_scan(Scene& s, const double* q, double dh) {
   launch_pair_flags(s, KIND_EE, q, dh2, w.flags.p + n_vf, w.err.p);
   CK(cudaMemsetAsync(w.flags.p + n, 0, sizeof(int), s.stream));
   scan_exclusive_i32(s, w.flags.p, w.pos.p, n + 1);
+  // compacted active list: act[pos[i]] = i (VF slots first, then EE)
+  w.act.resize(n + 1);
+  launch_scatter_active(s, n, w.flags.p, w.pos.p, w.act.p);
   int* hp = reinterpret_cast<int*>(s.h_pinned);
   CK(cudaMemcpyAsync(hp, w.pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaMemcpyAsync(hp + 1, w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaMemcpyAsync(hp + 2, w.pos.p + n_vf, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaStreamSynchronize(s.stream));
   if (hp[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
                                                  "(intersection reached; CCD filtering must prevent this)");
+  w.n_act_vf = hp[2];
   return hp[0];
 }
 
@@ -146,8 +151,9 @@ int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int p
   s.pblk.d2.resize(std::max(total, 1));
   s.pblk.n = total;
   EventTimer tm(s, 1);
-  launch_pair_blocks(s, KIND_VF, q, kappa, dh, project, s.w.flags.p, s.w.pos.p, 0, s.w.err.p);
-  launch_pair_blocks(s, KIND_EE, q, kappa, dh, project, s.w.flags.p + n_vf, s.w.pos.p + n_vf, 0, s.w.err.p);
+  (void)n_vf;
+  launch_pair_blocks_act(s, KIND_VF, q, kappa, dh, project, s.w.act.p, 0, s.w.n_act_vf);
+  launch_pair_blocks_act(s, KIND_EE, q, kappa, dh, project, s.w.act.p, s.w.n_act_vf, total - s.w.n_act_vf);
   tm.stop();
   // algorithmic bytes (scene form): candidate record 16 B + 4 rest points 96 B
   // (+ eps 8 B for EE) per candidate, one PB_STRIDE record written per active pair

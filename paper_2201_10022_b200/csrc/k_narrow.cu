@@ -94,6 +94,32 @@ __global__ void __launch_bounds__(64) k_pair_blocks(SceneView sv, int kind, int6
   out_d2[o] = ev.d2;
 }
 
+// same over the compacted active list: full warps instead of ~1/4 active lanes
+__global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind, int64_t count,
+                                                         const int* __restrict__ act, int64_t cand_off,
+                                                         const int4* __restrict__ rows, const double* __restrict__ q,
+                                                         double kappa, double dh, int project, int64_t slot_off,
+                                                         int2* out_bodies, double* out_blk, double* out_d2) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int64_t slot = slot_off + t;
+  const int64_t i = act[slot] - cand_off;
+  int4 r = rows[i];
+  PairIds ids = pair_ids(sv, kind, r);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  double* blk = out_blk + slot * PB_STRIDE;
+  PairEval ev = contact_pair_eval(kind, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0,
+                                  blk);
+  out_bodies[slot] = make_int2(r.x, r.z);
+  out_d2[slot] = ev.d2;
+}
+
+__global__ void k_scatter_active(int64_t n, const int* __restrict__ flags, const int* __restrict__ pos, int* act) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n && flags[i]) act[pos[i]] = (int)i;
+}
+
 __global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
                                  const double* __restrict__ q, double kappa, double dh, double* partials, int* err) {
   __shared__ double sh[RED_THREADS];
@@ -369,6 +395,24 @@ void launch_pair_blocks(Scene& s, int kind, const double* q, double kappa, doubl
   if (!n) return;
   k_pair_blocks<<<grid_for(n, 64), 64, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, project, flags, pos,
                                                       base, s.pblk.bodies.p, s.pblk.blk.p, s.pblk.d2.p);
+  note_launch("k_pair_blocks");
+}
+
+void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act) {
+  if (!n) return;
+  k_scatter_active<<<grid_for(n, 256), 256, 0, s.stream>>>(n, flags, pos, act);
+  note_launch("k_scatter_active");
+}
+
+void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, double dh, int project,
+                            const int* act, int64_t slot_off, int64_t count) {
+  if (count <= 0) return;
+  int64_t n;
+  const int4* rows = rows_of(s, kind, n);
+  const int64_t cand_off = kind == KIND_VF ? 0 : s.cands.n_vf;
+  k_pair_blocks_act<<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q, kappa, dh,
+                                                             project, slot_off, s.pblk.bodies.p, s.pblk.blk.p,
+                                                             s.pblk.d2.p);
   note_launch("k_pair_blocks");
 }
 

@@ -56,6 +56,9 @@ void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const doubl
 void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err);
 void launch_pair_blocks(Scene& s, int kind, const double* q, double kappa, double dh, int project,
                         const int* flags, const int* pos, int64_t base, int* err);
+void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act);
+void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, double dh, int project,
+                            const int* act, int64_t slot_off, int64_t count);
 void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, double dh, double* partials,
                            int* err);
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best_bits);

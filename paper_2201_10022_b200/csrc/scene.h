@@ -163,6 +163,8 @@ struct Scene {
 
   // persistent workspaces (grown, never shrunk: no cudaMalloc in steady state)
   struct Work {
+    DVec<int> act;      // compacted active candidate indices (VF then EE)
+    int64_t n_act_vf = 0;
     DVec<int> flags, pos, err, order, cnt, off, seg_s, seg_e, row_of, nsel, bad, iters;
     DVec<uint64_t> k0, k1, e0, e1;
     DVec<uint32_t> ka, kb;
