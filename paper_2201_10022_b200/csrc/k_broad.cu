@@ -563,8 +563,25 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
             tab[3 * pi + prod] = make_int2((int)hbase, cnt);
             if (cnt > P2_HCAP) atomicExch(unsorted, 1);
           }
-          if (cnt > 0 && cnt <= P2_HCAP) {
-            // deterministic in-chunk order: bitonic sort of the packed (prim_a, prim_b)
+          __syncthreads();  // hbase visible to the whole CTA
+          if (cnt > 0 && cnt <= 256) {
+            // deterministic in-chunk order by rank (keys are unique (prim_a, prim_b)):
+            // one pass, broadcast smem reads, no barrier ladder
+            const unsigned long long b0 = hbase;
+            for (int t = threadIdx.x; t < cnt; t += P2_THREADS) {
+              const unsigned key = hk[t];
+              int rank = 0;
+              for (int u = 0; u < cnt; ++u) rank += hk[u] < key;
+              const unsigned long long g2 = b0 + (unsigned long long)rank;
+              const int pa = (int)(key >> 16), pb = (int)(key & 0xffffu);
+              if (is_vf) {
+                if ((int64_t)g2 < cap_vf) out_vf[g2] = make_int4(body_a, pa, body_b, pb);
+              } else {
+                if ((int64_t)g2 < cap_ee) out_ee[g2] = make_int4(body_a, pa, body_b, pb);
+              }
+            }
+          } else if (cnt > 256 && cnt <= P2_HCAP) {
+            // larger chunks: bitonic sort in shared memory
             int P2 = 1;
             while (P2 < cnt) P2 <<= 1;
             for (int t = cnt + threadIdx.x; t < P2; t += P2_THREADS) hk[t] = 0xffffffffu;
