@@ -153,8 +153,8 @@ ABD_D void sym3_eig(double S[3][3], double w[3], double V[3][3]) {
 // 4k(s_i^2 + s_j^2 - 1 +- s_i s_j) on (u_i v_j^T +- u_j v_i^T)/sqrt2.
 // proj(H) = H - sum_{lambda < 0} lambda vec(dA) vec(dA)^T  (equals the
 // reference's eigh-clamp of body.py:281-296 applied at solver.py:292-294).
-ABD_D void ortho_project_closed(const double* q, double k, double* H) {
-  const double* A = q + 3;  // A[r][c] = A[3 r + c]
+// singular values (descending) and vectors of the 3x3 A (u[i], v[i]: i-th pair)
+ABD_D void ortho_svd3(const double* A, double s[3], double u[3][3], double v[3][3]) {
   double S[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -168,7 +168,6 @@ ABD_D void ortho_project_closed(const double* q, double k, double* H) {
   if (w[o1] < w[o2]) { int t = o1; o1 = o2; o2 = t; }
   if (w[o0] < w[o1]) { int t = o0; o0 = o1; o1 = t; }
   int ord[3] = {o0, o1, o2};
-  double s[3], v[3][3], u[3][3];  // v[i], u[i]: i-th singular vectors
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     s[i] = sqrt(fmax(w[ord[i]], 0.0));
@@ -210,6 +209,12 @@ ABD_D void ortho_project_closed(const double* q, double k, double* H) {
       }
     }
   }
+}
+
+ABD_D void ortho_project_closed(const double* q, double k, double* H) {
+  const double* A = q + 3;  // A[r][c] = A[3 r + c]
+  double s[3], v[3][3], u[3][3];  // v[i], u[i]: i-th singular vectors
+  ortho_svd3(A, s, u, v);
   const double k4 = 4.0 * k;
   const double r2 = 0.70710678118654752440;
   // negative modes only

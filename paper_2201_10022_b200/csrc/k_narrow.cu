@@ -293,6 +293,142 @@ __global__ void k_body_terms(int n_dyn, const int* __restrict__ dyn_body, const 
   if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// K1 gradient + projected diagonal block, one warp per dynamic body: the 3x3 SVD
+// of A is computed redundantly by the lanes, lanes 0..8 publish the negative
+// modes of the closed-form projection (ortho_project_closed) in shared memory,
+// and the 144 block entries are written coalesced (no per-thread 12x12 array)
+constexpr int BT_WARPS = 8;
+__global__ void __launch_bounds__(32 * BT_WARPS) k_body_derivs(int n_dyn, const int* __restrict__ dyn_body,
+                                                               const double* __restrict__ mass,
+                                                               const double* __restrict__ stiff,
+                                                               const double* __restrict__ q,
+                                                               const double* __restrict__ qt, double dt,
+                                                               double* grad0, double* diag0) {
+  __shared__ double modes[BT_WARPS][9][10];  // lambda (or 0 = inactive) | dA[9]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sidx = blockIdx.x * BT_WARPS + w;
+  if (sidx >= n_dyn) return;
+  const int b = dyn_body[sidx];
+  const double* M = mass + 144 * (int64_t)b;
+  const double* qb = q + 12 * (int64_t)b;
+  double qq[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) qq[c] = qb[c];
+  const double k = stiff[b];
+  const double dt2 = dt * dt;
+  const double* A = qq + 3;
+  // closed-form eigenpairs (abd_misc.cuh ortho_project_closed), redundant per lane
+  double S3[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) S3[a][c] = A[a] * A[c] + A[3 + a] * A[3 + c] + A[6 + a] * A[6 + c];
+  if (lane == 0) {
+    // all nine modes with compile-time indices (registers, no local memory)
+    double sv[3], uu[3][3], vv[3][3];
+    ortho_svd3(A, sv, uu, vv);
+    const double k4 = 4.0 * k;
+    const double r2 = 0.70710678118654752440;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+      const int pp = m < 3 ? 0 : (m - 3) >> 1;
+      const int i = m < 3 ? m : (pp == 2 ? 1 : 0);
+      const int j = m < 3 ? m : (pp == 0 ? 1 : 2);
+      const double sg = m < 3 ? 0.0 : (((m - 3) & 1) ? -1.0 : 1.0);
+      const double lam = (m < 3) ? k4 * (3.0 * sv[i] * sv[i] - 1.0)
+                                 : k4 * (sv[i] * sv[i] + sv[j] * sv[j] - 1.0 + sg * sv[i] * sv[j]);
+      double* o = modes[w][m];
+      o[0] = lam < 0.0 ? lam : 0.0;
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          o[1 + 3 * r + c] = (m < 3) ? uu[i][r] * vv[i][c] : r2 * (uu[i][r] * vv[j][c] + sg * uu[j][r] * vv[i][c]);
+    }
+  }
+  __syncwarp();
+  double G[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) G[i][j] = A[3 * i] * A[3 * j] + A[3 * i + 1] * A[3 * j + 1] + A[3 * i + 2] * A[3 * j + 2];
+  const double s4 = 4.0 * k;
+  double* D = diag0 + 144 * (int64_t)sidx;
+  for (int e = lane; e < 144; e += 32) {
+    const int r = e / 12, c = e % 12;
+    double h = 0.0;
+    if (r >= 3 && c >= 3) {
+      const int i = (r - 3) / 3, a = (r - 3) % 3, j = (c - 3) / 3, bb = (c - 3) % 3;
+      double v;
+      if (i == j) {
+        const double aa = A[3 * i + a] * A[3 * i + bb];
+        v = 2.0 * aa + (a == bb ? G[i][i] - 1.0 : 0.0) + (S3[a][bb] - aa);
+      } else {
+        v = A[3 * j + a] * A[3 * i + bb] + (a == bb ? G[i][j] : 0.0);
+      }
+      h = s4 * v;
+      for (int m = 0; m < 9; ++m) {
+        const double lam = modes[w][m][0];
+        if (lam < 0.0) h -= lam * modes[w][m][1 + (r - 3)] * modes[w][m][1 + (c - 3)];
+      }
+    }
+    D[e] = M[e] + dt2 * h;
+  }
+  if (lane < 12) {
+    double g[12];
+    ortho_derivs_dev(qq, k, g, nullptr);
+    const double* qtb = qt + 12 * (int64_t)b;
+    double gr = 0.0;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) gr += M[lane * 12 + c] * (qq[c] - qtb[c]);
+    double gl = g[0];
+#pragma unroll
+    for (int c = 1; c < 12; ++c)
+      if (c == lane) gl = g[c];
+    grad0[12 * (int64_t)sidx + lane] = gr + dt2 * gl;
+  }
+}
+
+// K1 energy only (line-search trials), one warp per dynamic slot: coalesced reads
+// of the 12x12 mass block, fixed-order warp and block sums
+__global__ void __launch_bounds__(RED_THREADS) k_body_energy_w(int n_dyn, const int* __restrict__ dyn_body,
+                                                               const double* __restrict__ mass,
+                                                               const double* __restrict__ stiff,
+                                                               const double* __restrict__ q,
+                                                               const double* __restrict__ qt, double dt,
+                                                               double* partials) {
+  __shared__ double sh[RED_THREADS / 32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (RED_THREADS / 32);
+  double acc = 0.0;  // lane 0: this warp's bodies in slot order
+  for (int sidx = blockIdx.x * (RED_THREADS / 32) + w; sidx < n_dyn; sidx += nw) {
+    const int b = dyn_body[sidx];
+    const double* M = mass + 144 * (int64_t)b;
+    const double* qb = q + 12 * (int64_t)b;
+    const double* qtb = qt + 12 * (int64_t)b;
+    double part = 0.0;
+    for (int e = lane; e < 144; e += 32) {
+      const int r = e / 12, c = e % 12;
+      part += (qb[r] - qtb[r]) * M[e] * (qb[c] - qtb[c]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if (lane == 0) {
+      double qq[12];
+#pragma unroll
+      for (int c = 0; c < 12; ++c) qq[c] = qb[c];
+      acc += 0.5 * part + (dt * dt) * ortho_energy_dev(qq, stiff[b]);
+    }
+  }
+  if (lane == 0) sh[w] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k2 = 0; k2 < RED_THREADS / 32; ++k2) t += sh[k2];
+    partials[blockIdx.x] = t;
+  }
+}
+
 // K1 energy only (line-search trials): 0.5 dq^T M dq + dt^2 V_perp per dynamic slot
 __global__ void k_body_energy(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ mass,
                               const double* __restrict__ stiff, const double* __restrict__ q,
@@ -453,9 +589,15 @@ void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double sl
 void launch_body_terms(Scene& s, const double* q, const double* qt, double dt, double* grad0, double* diag0,
                        double* partials, int want) {
   if (!want) {
-    k_body_energy<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p, s.stiff.p, q, qt, dt,
-                                                            partials);
+    k_body_energy_w<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p, s.stiff.p, q, qt, dt,
+                                                              partials);
     note_launch("k_body_energy");
+    return;
+  }
+  if (!partials && s.n_dyn) {
+    k_body_derivs<<<grid_for(s.n_dyn, BT_WARPS), 32 * BT_WARPS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p,
+                                                                               s.stiff.p, q, qt, dt, grad0, diag0);
+    note_launch("k_body_derivs");
     return;
   }
   k_body_terms<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(s.n_dyn, s.dyn_body.p, s.mass.p, s.stiff.p, q, qt, dt, grad0,
