@@ -187,6 +187,18 @@ int abd_kernel_stats_reset(abd_scene* s);
 int abd_timer_start(abd_scene* s);
 int abd_timer_stop(abd_scene* s, double* ms);
 
+/* ---------------- multi-GPU: one process per GPU ----------------
+ * Per-pair work (primitive pairs, pair blocks, CCD, contact/friction energy) is split
+ * across ranks by overlap body pair; the assembled system, energies and the CCD bound
+ * are all-reduced; factorisation and the Newton update run replicated.  A scene starts
+ * single-rank.  dtype: 0 f64, 1 i32, 2 i64; op: 0 sum, 1 min, 2 max.  The callback
+ * receives a device pointer after the scene stream has been synchronised and must
+ * complete the in-place reduction before returning (0 = success). */
+typedef int (*abd_allreduce_fn)(void* user, void* device_ptr, int64_t count, int dtype, int op);
+int abd_nccl_unique_id(uint8_t* out128);
+int abd_scene_set_comm_nccl(abd_scene* s, const uint8_t* id128, int rank, int world);
+int abd_scene_set_comm_callback(abd_scene* s, int rank, int world, abd_allreduce_fn fn, void* user);
+
 int abd_set_state(abd_scene* s, const double* q, const double* q_dot);
 int abd_get_state(abd_scene* s, double* q, double* q_dot);
 /* forces (n_bodies,12) host; NULL = reuse the last uploaded forces. energy_trace may be NULL

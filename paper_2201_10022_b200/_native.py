@@ -85,6 +85,9 @@ _SIGS = {
     "abd_get_system": (i32, [vp, dp, dp, lp, dp]),
     "abd_solve_resident": (i32, [vp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
     "abd_solve_resident_cholesky": (i32, [vp, dbl, dp, C.POINTER(i32), C.POINTER(dbl)]),
+    "abd_nccl_unique_id": (i32, [C.c_char_p]),
+    "abd_scene_set_comm_nccl": (i32, [vp, C.c_char_p, i32, i32]),
+    "abd_scene_set_comm_callback": (i32, [vp, i32, i32, vp, vp]),
     "abd_kernel_stats": (i32, [vp, i32, C.POINTER(i64), C.POINTER(dbl), C.POINTER(dbl), C.POINTER(i64)]),
     "abd_kernel_stats_reset": (i32, [vp]),
     "abd_timer_start": (i32, [vp]),

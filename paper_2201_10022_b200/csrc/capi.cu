@@ -464,7 +464,14 @@ abd_scene* abd_scene_create(int n_bodies, const int64_t* v_off, const int64_t* e
   return out;
 }
 
-void abd_scene_destroy(abd_scene* s) { delete s; }
+void abd_scene_destroy(abd_scene* s) {
+  if (!s) return;
+  try {
+    comm_destroy(s->s);
+  } catch (...) {
+  }
+  delete s;
+}
 
 #define SC(h) Scene& s = (h)->s
 
@@ -801,6 +808,27 @@ int abd_timer_stop(abd_scene* h, double* ms) {
     float m = 0.f;
     CK(cudaEventElapsedTime(&m, s.tev0, s.tev1));
     *ms = m;
+  });
+}
+
+int abd_nccl_unique_id(uint8_t* out128) {
+  return guard([&] {
+    ensure_device();
+    comm_get_nccl_id(out128);
+  });
+}
+
+int abd_scene_set_comm_nccl(abd_scene* h, const uint8_t* id128, int rank, int world) {
+  return guard([&] {
+    SC(h);
+    comm_init_nccl(s, id128, rank, world);
+  });
+}
+
+int abd_scene_set_comm_callback(abd_scene* h, int rank, int world, abd_allreduce_fn fn, void* user) {
+  return guard([&] {
+    SC(h);
+    comm_init_callback(s, rank, world, fn, user);
   });
 }
 

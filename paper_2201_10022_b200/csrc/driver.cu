@@ -131,6 +131,7 @@ static int active_scan(Scene& s, const double* q, double dh) {
   // compacted active list: act[pos[i]] = i (VF slots first, then EE)
   w.act.resize(n + 1);
   launch_scatter_active(s, n, w.flags.p, w.pos.p, w.act.p);
+  comm_allreduce(s, w.err.p, 1, 1, 2);  // a domain error on any rank stops every rank
   int* hp = reinterpret_cast<int*>(s.h_pinned);
   CK(cudaMemcpyAsync(hp, w.pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaMemcpyAsync(hp + 1, w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
@@ -209,7 +210,23 @@ int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, 
   }
   launch_friction_pre(s, KIND_VF, q, kappa, dh, s.w.flags.p, s.w.pos.p, 0, bp);
   launch_friction_pre(s, KIND_EE, q, kappa, dh, s.w.flags.p + n_vf, s.w.pos.p + n_vf, 0, bp);
+  if (s.comm.world > 1) {
+    // every rank's friction body pairs enter the (replicated) BSR pattern
+    static_assert(sizeof(int2) == sizeof(int64_t), "int2 packs into int64");
+    s.fric.n_pattern = comm_allgather_i64(s, reinterpret_cast<const int64_t*>(s.fric.bodies.p), total,
+                                          s.w.fric_keys_all);
+  }
   return total;
+}
+
+// friction pairs entering the BSR pattern (all ranks' pairs when partitioned)
+static const int2* fric_pattern(Scene& s, int64_t& n) {
+  if (s.comm.world > 1) {
+    n = s.fric.n_pattern;
+    return reinterpret_cast<const int2*>(s.w.fric_keys_all.p);
+  }
+  n = s.fric.n;
+  return s.fric.bodies.p;
 }
 
 // energy pieces as 4 fixed-order sums: body | contact VF | contact EE | friction
@@ -219,7 +236,8 @@ static void energy_terms(Scene& s, const double* q, const double* qt, double dt,
   s.w.err.resize(2);
   s.w.err.zero(s.stream);
   s.w.scal.resize(4);
-  launch_body_terms(s, q, qt, dt, nullptr, nullptr, s.red.p, 0);
+  if (s.comm.rank == 0) launch_body_terms(s, q, qt, dt, nullptr, nullptr, s.red.p, 0);
+  else CK(cudaMemsetAsync(s.red.p, 0, RED_BLOCKS * sizeof(double), s.stream));
   launch_contact_energy(s, KIND_VF, q, kappa, dh, s.red.p + RED_BLOCKS, s.w.err.p);
   launch_contact_energy(s, KIND_EE, q, kappa, dh, s.red.p + 2 * RED_BLOCKS, s.w.err.p);
   if (s.fric.n)
@@ -228,6 +246,8 @@ static void energy_terms(Scene& s, const double* q, const double* qt, double dt,
   else
     CK(cudaMemsetAsync(s.red.p + 3 * RED_BLOCKS, 0, RED_BLOCKS * sizeof(double), s.stream));
   reduce_fixed_multi(s.stream, s.red.p, RED_BLOCKS, 4, s.w.scal.p);
+  comm_allreduce(s, s.w.scal.p, 4, 0, 0);
+  comm_allreduce(s, s.w.err.p, 1, 1, 2);
   CK(cudaMemcpyAsync(s.h_pinned, s.w.scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
   int* he = reinterpret_cast<int*>(s.h_pinned + 8);
   CK(cudaMemcpyAsync(he, s.w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
@@ -279,7 +299,8 @@ double ip_value(Scene& s, const double* q, const double* qt, double dt, double k
 // fixed-order sums into scal4[0..3], barrier-domain flag into err
 static void launch_energy(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh,
                           double eps_v, double* red4, double* scal4, int* err) {
-  launch_body_terms(s, q, qt, dt, nullptr, nullptr, red4, 0);
+  if (s.comm.rank == 0) launch_body_terms(s, q, qt, dt, nullptr, nullptr, red4, 0);
+  else CK(cudaMemsetAsync(red4, 0, RED_BLOCKS * sizeof(double), s.stream));
   launch_contact_energy(s, KIND_VF, q, kappa, dh, red4 + RED_BLOCKS, err);
   launch_contact_energy(s, KIND_EE, q, kappa, dh, red4 + 2 * RED_BLOCKS, err);
   if (s.fric.n)
@@ -322,6 +343,11 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   note_launch("k_alpha_trial");
   launch_energy(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v,
                 w.lsred.p + 4 * RED_BLOCKS, w.lsscal.p + 4, w.lserr.p + 1);
+  // partitioned: global CCD bound (t >= 0: min of the bit patterns == min of the values),
+  // energies and error flags over all ranks
+  comm_allreduce(s, tmin, 1, 0, 1);
+  comm_allreduce(s, w.lsscal.p, 8, 0, 0);
+  comm_allreduce(s, w.lserr.p, 2, 1, 2);
   double* hp = s.h_pinned + 32;
   CK(cudaMemcpyAsync(hp, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hp + 1, w.lsscal.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -357,6 +383,8 @@ double step_filter(Scene& s, const double* q, const double* dq, double slack) {
   launch_ccd(s, KIND_VF, q, dq, slack, tmin, s.w.err.p);
   launch_ccd(s, KIND_EE, q, dq, slack, tmin, s.w.err.p);
   tm.stop();
+  comm_allreduce(s, tmin, 1, 0, 1);
+  comm_allreduce(s, s.w.err.p, 1, 1, 2);
   unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
   CK(cudaMemcpyAsync(hb, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
   int* he = reinterpret_cast<int*>(s.h_pinned + 2);
@@ -374,6 +402,7 @@ double candidate_min_d2(Scene& s, const double* q) {
   CK(cudaMemcpyAsync(best, &inf, sizeof(inf), cudaMemcpyHostToDevice, s.stream));
   launch_cand_min_d2(s, KIND_VF, q, best);
   launch_cand_min_d2(s, KIND_EE, q, best);
+  comm_allreduce(s, best, 1, 0, 1);  // d2 >= 0 (inf when empty): bit order == value order
   unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
   CK(cudaMemcpyAsync(hb, best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaStreamSynchronize(s.stream));
@@ -445,6 +474,7 @@ static void mark_structure(Scene& s) {
                                                                    s.H.upper_keys.p, w.ch_flags.p);
       note_launch("k_mark_active");
     }
+    comm_allreduce(s, w.ch_flags.p, n_off, 1, 2);  // union of the ranks' couplings
     int* hm = w.h_meta.reserve(3 * (size_t)n_off);
     CK(cudaMemcpyAsync(hm, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
     CK(cudaMemcpyAsync(hm + n_off, s.H.upper_keys.p, n_off * sizeof(int2), cudaMemcpyDeviceToHost, s.stream));
@@ -458,13 +488,26 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   int n = s.n_dyn;
   s.w.grad0.resize(std::max(12 * n, 1));
   s.w.diag0.resize(std::max(144 * n, 1));
-  launch_body_terms(s, q, qt, dt, s.w.grad0.p, s.w.diag0.p, nullptr, 1);
+  // body terms enter once (rank 0); pair terms are split across ranks
+  if (s.comm.rank == 0) {
+    launch_body_terms(s, q, qt, dt, s.w.grad0.p, s.w.diag0.p, nullptr, 1);
+  } else {
+    s.w.grad0.zero(s.stream);
+    s.w.diag0.zero(s.stream);
+  }
   // the pattern depends only on the overlap and friction pairs: build it first so
   // the Cholesky analysis inputs can be copied out while the values are reduced
-  build_pattern(s, s.cands.ov.p, s.cands.n_ov, s.fric.bodies.p, s.fric.n);
+  int64_t nfp = 0;
+  const int2* fp = fric_pattern(s, nfp);
+  build_pattern(s, s.cands.ov.p, s.cands.n_ov, fp, nfp);
   contact_blocks(s, q, kappa, dh, 1, /*mark=*/true);
   append_friction_blocks(s, q, dt, eps_v, 1);
   reduce_system(s, s.w.diag0.p, s.w.grad0.p);
+  if (s.comm.world > 1) {
+    // the replicated system: sum of the ranks' partial assemblies
+    comm_allreduce(s, s.H.val.p, 144 * s.H.nnzb, 0, 0);
+    comm_allreduce(s, s.grad.p, 12 * (int64_t)n, 0, 0);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -16,6 +16,13 @@ void chol_begin(Scene& s, const double* rhs, double* x);
 int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed);
 void spmv(Scene& s, const double* x, double* y);
 void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off);
+// comm.cu
+void comm_get_nccl_id(void* out128);
+void comm_init_nccl(Scene& s, const void* id128, int rank, int world);
+void comm_init_callback(Scene& s, int rank, int world, abd_allreduce_fn fn, void* user);
+void comm_destroy(Scene& s);
+void comm_allreduce(Scene& s, void* dptr, int64_t count, int dtype, int op);
+int64_t comm_allgather_i64(Scene& s, const int64_t* local, int64_t n_local, DVec<int64_t>& out);
 // k_stats.cu
 double global_min_distance(Scene& s, const double* q);
 // driver.cu

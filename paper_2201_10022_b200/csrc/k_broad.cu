@@ -392,7 +392,7 @@ __device__ __forceinline__ void box_from_cache(const PrimGeo& g, int kind, int g
 __global__ void __launch_bounds__(P2_THREADS, 3)
     k_prim_pairs2(PrimGeo g, int64_t n_ov, const int2* __restrict__ ov, const double* __restrict__ bbox,
                   unsigned long long* counters, int64_t cap_vf, int64_t cap_ee, int4* out_vf, int4* out_ee,
-                  int cap_list, int2* tab, int* unsorted) {
+                  int cap_list, int2* tab, int* unsorted, int rank, int world) {
   extern __shared__ double p2_sm[];
   double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
   double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   __shared__ int meta[16];  // v0,e0,t0 (i) | v0,e0,t0 (j) | nv,ne,nt (i) | nv,ne,nt (j)
   __shared__ int lcount[6];
   __shared__ double obox[6];
-  for (int64_t pi = blockIdx.x; pi < n_ov; pi += gridDim.x) {
+  // multi-GPU: this rank takes overlap pairs rank, rank + world, ... (table rows of the others stay 0)
+  for (int64_t pi = rank + (int64_t)blockIdx.x * world; pi < n_ov; pi += (int64_t)gridDim.x * world) {
     const int2 pr = ov[pi];
     const int bi = pr.x, bj = pr.y;
     if (threadIdx.x < 6) {
@@ -1024,7 +1025,9 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
     const size_t p2_smem = sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) +
                            2 * sizeof(int) * 6 * (size_t)cap_list + sizeof(unsigned) * P2_HCAP;
-    const bool use2 = s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1");
+    const bool use2 = (s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1")) || s.comm.world > 1;
+    if (s.comm.world > 1 && !(s.max_v <= P2_VCAP && p2_smem <= 100 * 1024))
+      throw Error(ABD_ERR_ARG, "partitioned broad phase needs <= 256 vertices per body");
     if (!attr) {
       CK(cudaFuncSetAttribute((void*)k_prim_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM));
       CK(cudaFuncSetAttribute((void*)k_prim_pairs2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
@@ -1034,10 +1037,11 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     if (use2) {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 3);
       w.tab.resize(3 * (size_t)n_ov);
+      if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_ov * sizeof(int2), st));
       CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
       k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
                                                        (int64_t)c.ee.cap, c.vf.p, c.ee.p, cap_list, w.tab.p,
-                                                       unsorted);
+                                                       unsorted, s.comm.rank, s.comm.world);
     } else {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
       k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,

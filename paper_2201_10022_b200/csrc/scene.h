@@ -89,6 +89,7 @@ struct FrictionSet {
   DVec<int2> bodies;      // (body_a, body_b)
   DVec<double> rec;       // 17 doubles per pair: T(6) c(8) off(2) lam(1)
   int64_t n = 0;
+  int64_t n_pattern = 0;  // all ranks' pairs (multi-GPU BSR pattern)
   double mu = 0.0;
 };
 
@@ -116,6 +117,14 @@ struct Bsr {
 };
 
 struct Stats;  // driver statistics (driver.cu)
+
+// multi-GPU communicator (comm.cu): kind 0 = single process, 1 = NCCL, 2 = host callback
+struct Comm {
+  int rank = 0, world = 1, kind = 0;
+  void* nccl = nullptr;
+  abd_allreduce_fn cb = nullptr;
+  void* user = nullptr;
+};
 
 struct Scene {
   int B = 0, n_dyn = 0;
@@ -163,6 +172,7 @@ struct Scene {
 
   // persistent workspaces (grown, never shrunk: no cudaMalloc in steady state)
   struct Work {
+    DVec<int64_t> comm_cnt, comm_buf, fric_keys, fric_keys_all;  // multi-GPU scratch
     DVec<int> act;      // compacted active candidate indices (VF then EE)
     int64_t n_act_vf = 0;
     DVec<int> flags, pos, err, order, cnt, off, seg_s, seg_e, row_of, nsel, bad, iters;
@@ -210,6 +220,8 @@ struct Scene {
       double host_ms = 0.0, ms3[3] = {};
     } ch_run;
   } w;
+
+  Comm comm;
 
   // per-kernel instrumentation (CUDA events on `stream`)
   struct KStat {
