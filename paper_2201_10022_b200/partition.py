@@ -1,4 +1,15 @@
-"""Body-slab partitioning for multi-GPU steps, host-side logic.
+"""Partitioning for multi-GPU steps, host-side logic.
+
+Implemented on the device (csrc/comm.cu, csrc/k_broad.cu): the per-pair work is
+split by OVERLAP BODY PAIR -- the sorted overlap list is identical on every
+rank and rank r takes pairs r, r + W, r + 2W, ... (`pair_owner` /
+`rows_of_owned_pairs` restate it for the CPU tests); the system, energies and
+CCD bound are all-reduced, the solve is replicated.  Every candidate belongs to
+exactly one overlap pair, so the ranks' candidate sets are disjoint and their
+union is the single-GPU set.
+
+The body-slab helpers below are the alternative SURVEY §8(e) sketches (slab
+ownership with halo bodies); they are kept for slab-sharded scenes.
 
 One process per GPU.  Each step, dynamic bodies are sorted by centroid along
 the longest scene axis and cut into contiguous slabs balanced by primitive
@@ -21,7 +32,23 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["slab_partition", "halo_bodies", "owned_rows", "counted_rows", "dedup_union", "ordered_sum"]
+__all__ = ["pair_owner", "rows_of_owned_pairs", "slab_partition", "halo_bodies", "owned_rows", "counted_rows",
+           "dedup_union", "ordered_sum"]
+
+
+def pair_owner(n_pairs, world):
+    """Owning rank of each overlap pair (index order of the sorted overlap list)."""
+    return np.arange(n_pairs, dtype=np.int64) % max(int(world), 1)
+
+
+def rows_of_owned_pairs(rows, overlap_pairs, rank, world):
+    """Candidate rows (body_a, prim_a, body_b, prim_b) whose overlap pair `rank` owns."""
+    r = np.asarray(rows, dtype=np.int64).reshape(-1, 4)
+    ov = np.asarray(overlap_pairs, dtype=np.int64).reshape(-1, 2)
+    owner = pair_owner(len(ov), world)
+    index = {(int(a), int(b)): k for k, (a, b) in enumerate(ov)}
+    keep = [owner[index[(min(int(x[0]), int(x[2])), max(int(x[0]), int(x[2])))]] == rank for x in r]
+    return r[np.array(keep, dtype=bool)] if len(r) else r
 
 
 def slab_partition(centroids, weights, dynamic, n_parts, axis=None):

@@ -63,6 +63,19 @@ def _worker(rank, world, port, out):
     parts = [None] * world
     dist.all_gather_object(parts, e_part)
     total = PT.ordered_sum(parts)
+    # the implemented split: by overlap pair (disjoint sets, union = full set)
+    pvf = PT.rows_of_owned_pairs(full.vf, full.overlap_pairs, rank, world)
+    pee = PT.rows_of_owned_pairs(full.ee, full.overlap_pairs, rank, world)
+    gp = [None] * world
+    dist.all_gather_object(gp, (pvf.tolist(), pee.tolist(),
+                                O.contact_energy(bodies, q0, pvf, pee, kappa, d_hat)))
+    n_pvf = sum(len(x[0]) for x in gp)
+    n_pee = sum(len(x[1]) for x in gp)
+    uvf2 = PT.dedup_union([np.array(x[0], dtype=np.int64).reshape(-1, 4) for x in gp])
+    uee2 = PT.dedup_union([np.array(x[1], dtype=np.int64).reshape(-1, 4) for x in gp])
+    e_pairs = PT.ordered_sum([x[2] for x in gp])
+    pair_ok = (n_pvf == len(full.vf) and n_pee == len(full.ee) and np.array_equal(uvf2, full.vf)
+               and np.array_equal(uee2, full.ee))
     # global min CCD step: min over ranks of the owned-row minima
     a_part = O.step_filter(bodies, q0, dq, mine_vf, mine_ee, 0.1)
     t = torch.tensor([a_part], dtype=torch.float64)
@@ -71,7 +84,7 @@ def _worker(rank, world, port, out):
         out.put((np.array_equal(uvf, full.vf), np.array_equal(uee, full.ee), total,
                  O.contact_energy(bodies, q0, full.vf, full.ee, kappa, d_hat), float(t.item()),
                  O.step_filter(bodies, q0, dq, full.vf, full.ee, 0.1), int((owner >= 0).sum()),
-                 sorted(set(owner[owner >= 0].tolist()))))
+                 sorted(set(owner[owner >= 0].tolist())), pair_ok, e_pairs))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -88,8 +101,10 @@ def test_slab_sharding_gloo(world):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    vf_ok, ee_ok, total, ref, amin, aref, n_owned, parts = res
+    vf_ok, ee_ok, total, ref, amin, aref, n_owned, parts, pair_ok, e_pairs = res
     assert vf_ok and ee_ok
+    assert pair_ok  # pair-partitioned candidate sets are disjoint and complete
+    assert e_pairs == pytest.approx(ref, rel=1e-12, abs=0)
     assert total == pytest.approx(ref, rel=1e-12, abs=0)
     assert amin == aref
     assert parts == list(range(world))
