@@ -94,8 +94,10 @@ __global__ void __launch_bounds__(64) k_pair_blocks(SceneView sv, int kind, int6
   out_d2[o] = ev.d2;
 }
 
-// same over the compacted active list: full warps instead of ~1/4 active lanes
-__global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind, int64_t count,
+// same over the compacted active list: full warps instead of ~1/4 active lanes;
+// specialised per kind so the VF kernel carries none of the mollified-EE state
+template <int KIND>
+__global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_unused, int64_t count,
                                                          const int* __restrict__ act, int64_t cand_off,
                                                          const int4* __restrict__ rows, const double* __restrict__ q,
                                                          double kappa, double dh, int project, int64_t slot_off,
@@ -105,11 +107,12 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind, 
   const int64_t slot = slot_off + t;
   const int64_t i = act[slot] - cand_off;
   int4 r = rows[i];
-  PairIds ids = pair_ids(sv, kind, r);
+  (void)kind_unused;
+  PairIds ids = pair_ids(sv, KIND, r);
   V3 z[4], xb[4];
   pair_points(sv, ids, q, z, xb);
   double* blk = out_blk + slot * PB_STRIDE;
-  PairEval ev = contact_pair_eval(kind, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0,
+  PairEval ev = contact_pair_eval(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0,
                                   blk);
   out_bodies[slot] = make_int2(r.x, r.z);
   out_d2[slot] = ev.d2;
@@ -546,9 +549,14 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
   int64_t n;
   const int4* rows = rows_of(s, kind, n);
   const int64_t cand_off = kind == KIND_VF ? 0 : s.cands.n_vf;
-  k_pair_blocks_act<<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q, kappa, dh,
-                                                             project, slot_off, s.pblk.bodies.p, s.pblk.blk.p,
-                                                             s.pblk.d2.p);
+  if (kind == KIND_VF)
+    k_pair_blocks_act<KIND_VF><<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q,
+                                                                        kappa, dh, project, slot_off, s.pblk.bodies.p,
+                                                                        s.pblk.blk.p, s.pblk.d2.p);
+  else
+    k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q,
+                                                                        kappa, dh, project, slot_off, s.pblk.bodies.p,
+                                                                        s.pblk.blk.p, s.pblk.d2.p);
   note_launch("k_pair_blocks");
 }
 
