@@ -651,6 +651,7 @@ int abd_set_friction(abd_scene* h, int64_t n, const int64_t* body_a, const int64
     s.fric.bodies.upload(hb.data(), hb.size(), s.stream);
     s.fric.rec.upload(hr.data(), hr.size(), s.stream);
     s.fric.n = n;
+    s.fric.gen += 1;
     s.fric.mu = mu;
     sync(s.stream);
   });

@@ -201,6 +201,7 @@ int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, 
   s.fric.mu = mu;
   int total = active_scan(s, q, dh);
   s.fric.n = total;
+  s.fric.gen += 1;
   s.fric.bodies.resize(std::max(total, 1));
   s.fric.rec.resize((int64_t)std::max(total, 1) * FRIC_STRIDE);
   double* bp = nullptr;
@@ -499,7 +500,7 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   // the Cholesky analysis inputs can be copied out while the values are reduced
   int64_t nfp = 0;
   const int2* fp = fric_pattern(s, nfp);
-  build_pattern(s, s.cands.ov.p, s.cands.n_ov, fp, nfp);
+  build_pattern(s, s.cands.ov.p, s.cands.n_ov, fp, nfp, /*from_cands=*/true);
   contact_blocks(s, q, kappa, dh, 1, /*mark=*/true);
   append_friction_blocks(s, q, dt, eps_v, 1);
   reduce_system(s, s.w.diag0.p, s.w.grad0.p);
@@ -529,6 +530,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
     s.forces.zero(stream);
   }
   s.w.ch_cache.valid = false;  // Cholesky plans are reused within a step only
+  s.w.pat_valid = false;       // and so is the (superset) BSR pattern
   s.q0.resize(NB);
   s.q_tilde.resize(NB);
   s.dq.resize(NB);

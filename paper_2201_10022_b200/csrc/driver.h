@@ -7,7 +7,7 @@ namespace abd {
 // k_broad.cu
 void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat);
 // k_solve.cu
-void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f);
+void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f, bool from_cands = false);
 void reduce_system(Scene& s, const double* diag0, const double* grad0);
 int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_iters, double& rel_res);
 // k_chol.cu: sparse block Cholesky + refinement; returns the number of triangular solves

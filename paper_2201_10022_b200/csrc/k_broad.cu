@@ -621,6 +621,24 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   }
 }
 
+__global__ void k_ov_in_pattern(int64_t n, const int2* __restrict__ ov, const int* __restrict__ slot, int64_t n_off,
+                                const int2* __restrict__ keys, int* inside) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int sa = slot[ov[i].x], sb = slot[ov[i].y];
+  if (sa < 0 || sb < 0 || sa == sb) return;  // no block for pairs with a kinematic body
+  const int a = min(sa, sb), b = max(sa, sb);
+  int64_t lo = 0, hi = n_off - 1;
+  while (lo <= hi) {
+    int64_t m = (lo + hi) >> 1;
+    const int2 k = keys[m];
+    if (k.x < a || (k.x == a && k.y < b)) lo = m + 1;
+    else if (k.x == a && k.y == b) return;
+    else hi = m - 1;
+  }
+  *inside = 0;
+}
+
 // chunk table -> per-list counts in (pair, product) order
 __global__ void k_chunk_counts(int64_t n_ov, const int2* __restrict__ tab, int* cnt_vf, int* cnt_ee) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -995,7 +1013,11 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   int n_ov = (int)hov[0];
   c.n_ov = n_ov;
   c.ov.n = n_ov;
-  if (n_ov == 0) return;
+  c.ov_matches_pattern = false;
+  if (n_ov == 0) {
+    c.ov_matches_pattern = w.pat_n_ov == 0;
+    return;
+  }
   // canonical (i, j) order of overlap pairs
   {
     int bB = bits_for(s.B - 1);
@@ -1010,6 +1032,19 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     k_gather<int2><<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, alt ? w.vb.p : w.va.p, c.ov.p, w.pairs_tmp.p);
     note_launch("k_gather");
     CK(cudaMemcpyAsync(c.ov.p, w.pairs_tmp.p, n_ov * sizeof(int2), cudaMemcpyDeviceToDevice, st));
+  }
+  // is every dynamic overlap pair already a block of the resident BSR pattern?
+  // (read back with the primitive-pair counts below; build_pattern then keeps the
+  // pattern -- extra blocks just hold zeros -- instead of re-sorting it)
+  int* ov_same = reinterpret_cast<int*>(w.ull.p + 9);
+  if (w.pat_valid && s.H.n == s.n_dyn) {
+    const int one = 1;
+    CK(cudaMemcpyAsync(ov_same, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    k_ov_in_pattern<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, c.ov.p, s.slot.p, s.H.n_off, s.H.upper_keys.p,
+                                                         ov_same);
+    note_launch("k_ov_in_pattern");
+  } else {
+    CK(cudaMemsetAsync(ov_same, 0, sizeof(int), st));
   }
   // primitive pairs
   PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
@@ -1051,7 +1086,9 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     if (s.instrument) CK(cudaEventRecord(s.ev1, st));
     CK(cudaMemcpyAsync(hc, counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hc + 2, unsorted, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc + 3, ov_same, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    c.ov_matches_pattern = *reinterpret_cast<int*>(hc + 3) != 0;
     chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;
     if (s.instrument) {
       float ms = 0.f;

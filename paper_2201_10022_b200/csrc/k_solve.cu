@@ -207,9 +207,16 @@ __global__ void k_row_of(int n, const int* __restrict__ row_ptr, int* row_of) {
 
 // ---------------------------------------------------------------------------
 // build pattern + CSR from overlap pairs and friction pairs (dyn-dyn only)
-void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f) {
+void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f, bool from_cands) {
   Bsr& H = s.H;
+  Scene::Work& wk = s.w;
+  // overlap pairs all inside the resident pattern and the same friction set: the
+  // pattern (row_ptr, col, positions) is reused -- no sorts, no host sync
+  if (from_cands && wk.pat_valid && s.cands.ov_matches_pattern && wk.pat_n_f == n_f &&
+      wk.pat_fric_gen == s.fric.gen && H.n == s.n_dyn)
+    return;
   s.w.ch_pre = false;  // any structure copied out for the Cholesky belongs to the old pattern
+  wk.pat_valid = false;
   cudaStream_t st = s.stream;
   int n = s.n_dyn;
   H.n = n;
@@ -273,6 +280,13 @@ void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64
   k_csr_positions<<<grid_for(mx, 256), 256, 0, st>>>(n, n_off, k0.p, bS, H.row_ptr.p, H.col.p, H.diag_pos.p,
                                                      H.upper_pos.p, H.lower_pos.p, H.upper_keys.p);
   note_launch("k_csr_positions");
+  if (from_cands) {
+    wk.pat_n_ov = n_ov;
+    wk.pat_n_f = n_f;
+    wk.pat_fric_gen = s.fric.gen;
+    wk.pat_valid = true;
+    s.cands.ov_matches_pattern = true;
+  }
 }
 
 // reduce resident pair blocks (s.pblk, n_pairs) + per-body diag0/grad0 into H, grad

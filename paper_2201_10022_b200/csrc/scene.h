@@ -82,6 +82,7 @@ struct Cands {
   DVec<int4> vf, ee;  // (body_a, prim_a, body_b, prim_b) in canonical order
   DVec<int2> ov;      // overlapping body pairs (i < j)
   int64_t n_vf = 0, n_ee = 0, n_ov = 0;
+  bool ov_matches_pattern = false;  // ov equals the overlap list of the resident BSR pattern
 };
 
 // lagged friction records (compact form of contact.py:687-708)
@@ -90,6 +91,7 @@ struct FrictionSet {
   DVec<double> rec;       // 17 doubles per pair: T(6) c(8) off(2) lam(1)
   int64_t n = 0;
   int64_t n_pattern = 0;  // all ranks' pairs (multi-GPU BSR pattern)
+  int64_t gen = 0;        // bumped whenever the friction set changes
   double mu = 0.0;
 };
 
@@ -181,6 +183,10 @@ struct Scene {
     DVec<int> va, vb;
     DVec<int4> rows_tmp;
     DVec<int2> tab;  // broad phase (pair, product) -> (chunk start, count)
+    // overlap list / friction generation of the resident BSR pattern (build_pattern reuse)
+    DVec<int2> pat_ov;
+    int64_t pat_n_ov = -1, pat_n_f = -1, pat_fric_gen = -1;
+    bool pat_valid = false;
     DVec<int2> pairs_tmp;
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
