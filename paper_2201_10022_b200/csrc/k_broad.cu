@@ -759,9 +759,12 @@ __global__ void k_extent_keys(int B, const double* __restrict__ bbox, uint32_t* 
   keys[b] = __float_as_uint((float)fmax(e, 0.0));
 }
 
-// 10 bits per axis (wraps every 1024 cells: collisions only add box tests)
+// 7 bits per axis (wraps every 128 cells: aliased cells only add exact box tests);
+// "large" bodies get CELL_LARGE, so the keys fit 22 bits (3 radix passes)
+constexpr uint32_t CELL_LARGE = 1u << 21;
+constexpr int CELL_KEY_BITS = 22;
 __device__ __forceinline__ uint32_t cell_key(long long ix, long long iy, long long iz) {
-  return (((uint32_t)ix & 1023u) << 20) | (((uint32_t)iy & 1023u) << 10) | ((uint32_t)iz & 1023u);
+  return (((uint32_t)ix & 127u) << 14) | (((uint32_t)iy & 127u) << 7) | ((uint32_t)iz & 127u);
 }
 
 __global__ void k_cell_keys(int B, const double* __restrict__ bbox, const uint32_t* __restrict__ sorted_ext,
@@ -785,7 +788,7 @@ __global__ void k_cell_keys(int B, const double* __restrict__ bbox, const uint32
   double e = fmax(fmax(x[3] - x[0], x[4] - x[1]), x[5] - x[2]);
   vals[b] = b;
   if (e > cell) {
-    keys[b] = 0xffffffffu;  // large: not binned
+    keys[b] = CELL_LARGE;  // large: not binned
     return;
   }
   keys[b] = cell_key((long long)floor(x[0] / cell), (long long)floor(x[1] / cell), (long long)floor(x[2] / cell));
@@ -846,7 +849,7 @@ __global__ void k_cell_keys2(int B, const double* __restrict__ bbox, const doubl
   double e = fmax(fmax(x[3] - x[0], x[4] - x[1]), x[5] - x[2]);
   vals[b] = b;
   if (e > cell) {
-    keys[b] = 0xffffffffu;  // large: not binned
+    keys[b] = CELL_LARGE;  // large: not binned
     return;
   }
   keys[b] = cell_key((long long)floor(x[0] / cell), (long long)floor(x[1] / cell), (long long)floor(x[2] / cell));
@@ -907,14 +910,14 @@ __global__ void k_grid_pairs(int B, const double* __restrict__ bbox, const unsig
 }
 
 // every (large body, body) pair: thread per body j over the few large bodies
-// (the ~0-keyed tail of the sorted cell keys); large-large pairs once (j > i)
+// (the CELL_LARGE-keyed tail of the sorted cell keys); large-large pairs once (j > i)
 __global__ void k_large_pairs(int B, const double* __restrict__ bbox, const unsigned char* __restrict__ dyn,
                               const uint32_t* __restrict__ skeys, const int* __restrict__ sbody,
                               const double* __restrict__ cell_p, unsigned long long* count, int64_t cap, int2* out) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= B) return;
   const double cell = *cell_p;
-  int first = lower_bound_u32(skeys, B, 0xffffffffu);
+  int first = lower_bound_u32(skeys, B, CELL_LARGE);
   if (first >= B) return;
   const double* b = bbox + 6 * j;
   double ej = fmax(fmax(b[3] - b[0], b[4] - b[1]), b[5] - b[2]);
@@ -990,10 +993,10 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   note_launch("k_cell_size");
   k_cell_keys2<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.scal.p, w.ka.p, w.va.p);
   note_launch("k_cell_keys");
-  sort_pairs_u32(s, w.ka.p, w.kb.p, w.va.p, w.vb.p, s.B, 32, alt);
+  sort_pairs_u32(s, w.ka.p, w.kb.p, w.va.p, w.vb.p, s.B, CELL_KEY_BITS, alt);
   const uint32_t* skeys = alt ? w.kb.p : w.ka.p;
   const int* sbody = alt ? w.vb.p : w.va.p;
-  int n_small = s.B;  // large bodies carry key ~0 and sort last; the lookups never match them
+  int n_small = s.B;  // large bodies carry CELL_LARGE and sort last; the lookups never match them
   unsigned long long* ovc = w.ull.p + 6;
   unsigned long long* hov = reinterpret_cast<unsigned long long*>(s.h_pinned);
   if (c.ov.cap < 256) c.ov.resize(256);
