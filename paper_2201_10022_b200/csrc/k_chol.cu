@@ -51,6 +51,7 @@ struct CholView {
   const int* blk_row;   // per off block: row node i
   const int* bsr_row;   // BSR row_ptr / col: A(i, j) found by binary search in row i (absent: fill)
   const int* bsr_col;
+  int* apos;            // per off block: BSR position of A(i, j) or -1, filled by k_chol_apos
   const int* row_ptr;   // n + 1: range into row_blk (blocks L_jk, k eliminated before j)
   const int* row_blk;   // L block index
   const int* row_col;   // column node k of each row_blk entry
@@ -157,6 +158,14 @@ __device__ __forceinline__ double upper_solve12(unsigned mask, int t, double acc
 
 // Factor + forward substitution (levels ascending), then backward substitution
 // (levels descending), one CTA per group of components.  x receives y, then x.
+// BSR positions of the factor's off-diagonal source blocks, all nodes in parallel
+// (takes the binary searches off the level-serial critical path)
+__global__ void k_chol_apos(CholView v) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= v.n) return;
+  for (int b = v.col_ptr[j]; b < v.col_ptr[j + 1]; ++b) v.apos[b] = bsr_find(v.bsr_row, v.bsr_col, v.blk_row[b], j);
+}
+
 __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, const double* __restrict__ b,
                                                                    double* x) {
   __shared__ double Ss[CH_HW][12][13];  // per warp: staged L_jk / symmetrisation / L_jj
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, co
       // off-diagonal blocks of column j: L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
       for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
         double bt[12];
-        const int ap = bsr_find(v.bsr_row, v.bsr_col, v.blk_row[bb], j);
+        const int ap = v.apos[bb];
         if (ap >= 0) {
           const double* A = v.val + 144 * (int64_t)ap + 12 * tt;
 #pragma unroll
@@ -539,6 +548,7 @@ static Analysis chol_analyze(Scene& s) {
                     dp + o[5],
                     H.row_ptr.p,
                     H.col.p,
+                    w.ch_apos.p,
                     dp + o[7],
                     dp + o[8],
                     dp + o[9],
@@ -849,6 +859,7 @@ static Analysis chol_analyze(Scene& s) {
   CK(cudaMemcpyAsync(w.ch_plan.p, hp, total * sizeof(int), cudaMemcpyHostToDevice, st));
   w.ch_L.resize(144 * std::max<int64_t>(an.n_blk, 1));
   w.ch_dinv.resize(12 * std::max<int64_t>(n, 1));
+  w.ch_apos.resize(std::max<int64_t>(an.n_blk - n, 1));
   const size_t offs[13] = {off_nodes, off_lvl,  off_ctal, off_ctan, off_colp, off_brow, off_bapos,
                            off_rowp,  off_rowb, off_rowc, off_updp, off_upd,  total};
   an.view = make_view(offs);
@@ -885,6 +896,7 @@ static CholView plan_view(Scene& s) {
                   dp + o[5],
                   s.H.row_ptr.p,
                   s.H.col.p,
+                  w.ch_apos.p,
                   dp + o[7],
                   dp + o[8],
                   dp + o[9],
@@ -950,6 +962,8 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
     dbgbuf.zero(st);
     v.dbg = dbgbuf.p;
   }
+  k_chol_apos<<<grid_for(n, 128), 128, 0, st>>>(v);
+  note_launch("k_chol_apos");
   k_chol_factor_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, rhs, x);
   note_launch("k_chol_factor_solve");
   if (s.instrument) CK(cudaEventRecord(ks.e1, st));

@@ -198,7 +198,7 @@ struct Scene {
     DVec<long long> cl_slot_off, cl_minv;
     DVec<double> minv;
     // sparse block Cholesky plan (one packed int buffer) and factor (k_chol.cu)
-    DVec<int> ch_flags, ch_plan;
+    DVec<int> ch_flags, ch_plan, ch_apos;
     DVec<double> ch_L, ch_dinv;
     HostPinned<int> h_plan, h_meta;
     // last analysed pattern (nonzero flags + keys) and its plan: Newton iterations
