@@ -185,16 +185,19 @@ def chainmail(seed=0, n_chains=200, links=50, steps=400, chains_x=20, spacing=0.
     """Config 5: hanging chains of interlocked tori (R=0.1, r=0.02, 24x8).
 
     Link k lies in the xz plane (k even) or yz plane (k odd), centres
-    0.1 m apart along -z (interlock clearance 0.06 m, SURVEY §7 item 7);
+    0.14 m apart along -z: each link passes through its neighbours' holes
+    (0.02 m clearance) and same-plane links k, k+2 keep 0.04 m apart (a 0.1 m
+    pitch would make them overlap; SURVEY §7 item 7 only bounds the pitch
+    below 2R - 2r = 0.16 m);
     the top link of every chain is kinematic.  Each chain gets one seeded
     lateral velocity ~ N(0, 0.5) m/s on its dynamic links.
     """
     rng = np.random.default_rng(seed)
-    R, r, s = 0.1, 0.02, 0.1
+    R, r, s = 0.1, 0.02, 0.14
     base = torus_mesh(R, r, 24, 8)
     # torus_mesh lies in the xy plane; rotate into xz (about x) / yz (about y)
-    rx = np.array([[1.0, 0, 0], [0, 0, -1.0], [0, 1.0, 0]])
-    ry = np.array([[0, 0, 1.0], [0, 1.0, 0], [-1.0, 0, 0]]) @ rx
+    rx = np.array([[1.0, 0, 0], [0, 0, -1.0], [0, 1.0, 0]])  # xy -> xz plane
+    ry = np.array([[0, -1.0, 0], [1.0, 0, 0], [0, 0, 1.0]]) @ rx  # then about z: xz -> yz plane
     meshes, q0, qd, dyn = [], [], [], []
     chains_y = int(np.ceil(n_chains / chains_x))
     for cidx in range(n_chains):

@@ -337,8 +337,39 @@ def gen_ico_pile(steps=40):
     save("ico_pile.npz", out)
 
 
+def gen_trajectory(name, spec, steps):
+    """Reference trajectory of a small version of a BASELINE scene (q per step, iterations, min distance)."""
+    model = ref_model(spec.meshes, spec.dynamic, spec.density, spec.kappa_ortho)
+    params = rs.StepParams(**spec.params)
+    state = rs.SimState(q=spec.q0.copy(), q_dot=spec.q_dot0.copy())
+    qs, its, mind = [spec.q0.copy()], [], []
+    t0 = time.perf_counter()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for _ in range(steps):
+            state, st = rs.advance_step(model, state, params)
+            qs.append(state.q.copy())
+            its.append(st.iterations)
+            mind.append(st.min_distance)
+    el = time.perf_counter() - t0
+    out = dict(q=np.array(qs), iterations=np.array(its), min_distance=np.array(mind), seconds=np.array(el))
+    pack_bodies("scene_", model.bodies, out)
+    print(f"{name} {steps} steps: {el:.2f}s, {np.sum(its)} Newton iterations")
+    save(name + ".npz", out)
+
+
+def gen_cube_drop(steps=70):
+    """Config 3 in small: 2x2x2 unit cubes (1.2 m pitch, random rotations) into the open container, mu=0.2."""
+    gen_trajectory("cube_drop", scenes.cube_drop(seed=0, n=2, steps=steps), steps)
+
+
+def gen_chainmail(steps=40):
+    """Config 5 in small: 2 chains of 3 interlocked tori (top link fixed), mu=0.3, dt=0.005, d_hat=1e-4."""
+    gen_trajectory("chainmail", scenes.chainmail(seed=0, n_chains=2, links=3, chains_x=2, steps=steps), steps)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["kernels", "contact", "box_stack", "ico_pile"]
+    which = sys.argv[1:] or ["kernels", "contact", "box_stack", "ico_pile", "cube_drop", "chainmail"]
     if "kernels" in which:
         gen_kernels()
     if "contact" in which:
@@ -347,3 +378,7 @@ if __name__ == "__main__":
         gen_box_stack()
     if "ico_pile" in which:
         gen_ico_pile()
+    if "cube_drop" in which:
+        gen_cube_drop()
+    if "chainmail" in which:
+        gen_chainmail()
