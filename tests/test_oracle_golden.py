@@ -208,3 +208,37 @@ def test_box_stack_trajectory(golden):
         ref = g["q"][s + 1]
         assert np.abs(q - ref).max() / np.abs(ref).max() <= 1e-6
         assert st.iterations == g["iterations"][s]
+
+
+@pytest.mark.parametrize("name,steps", [("chainmail", 40), ("cube_drop", 35)])
+def test_small_config_trajectories(golden, name, steps):
+    """Oracle advance_step reproduces the reference on small configs 3 and 5
+    (friction, kinematic walls / anchors, tori with mollified edge-edge contact)."""
+    g = golden(name + ".npz")
+    bodies = oracle_bodies("scene_", g)
+    from paper_2201_10022_b200 import scenes
+    from paper_2201_10022_b200.body import mass_matrix
+    spec = (scenes.cube_drop(seed=0, n=2) if name == "cube_drop"
+            else scenes.chainmail(seed=0, n_chains=2, links=3, chains_x=2))
+    masses, stiff = [], []
+    for m, dyn in zip(spec.meshes, spec.dynamic):
+        if dyn:
+            gm, vol = mass_matrix(m, spec.density)
+            masses.append(gm.matrix)
+            stiff.append(spec.kappa_ortho * vol)
+        else:
+            masses.append(None)
+            stiff.append(None)
+    model = O.OracleModel(bodies, masses, stiff)
+    prm = O.OracleParams(**{k: v for k, v in spec.params.items()})
+    f = np.zeros((len(bodies), 12))
+    grav = np.array([0, 0, -9.8])
+    for b in model.dyn:
+        f[b, :3] = masses[b][0, 0] * grav
+        f[b, 3:] = np.kron(grav, masses[b][0, 3:6])
+    q, qd = g["q"][0].copy(), spec.q_dot0.copy()
+    for s in range(steps):
+        q, qd, st = O.advance_step(model, q, qd, f, prm, min_distance=False)
+        ref = g["q"][s + 1]
+        assert np.abs(q - ref).max() / np.abs(ref).max() <= 1e-6, (name, s)
+        assert st.iterations == g["iterations"][s]
