@@ -37,8 +37,10 @@ struct DVec {
   }
   void resize(size_t m) {
     if (m > cap) {
+      // 2x headroom: workspaces grow in a handful of steps and then stay put
+      // (cudaFree synchronises the device, so steady-state regrowth would stall)
       if (p) CK(cudaFree(p));
-      size_t c = m + m / 4 + 16;
+      size_t c = 2 * m + 16;
       CK(cudaMalloc(&p, c * sizeof(T)));
       cap = c;
     }
@@ -70,7 +72,7 @@ struct HostPinned {
   T* reserve(size_t m) {
     if (m > cap) {
       if (p) CK(cudaFreeHost(p));
-      size_t c = m + m / 4 + 64;
+      size_t c = 2 * m + 64;
       CK(cudaMallocHost(&p, c * sizeof(T)));
       cap = c;
     }
