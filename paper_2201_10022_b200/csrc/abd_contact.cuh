@@ -121,6 +121,9 @@ struct PairEval {
 
 // Full per-pair evaluation.  out: g24 (24) | haa (144) | hbb (144) | hab (144).
 // h12/g12 (optional, may be null): point-space derivatives for testing.
+// COMPACT: `out` receives a compact pair record (abd_pblk.cuh: g24 | type |
+// low-rank factors) instead of the dense g24 | H_aa | H_bb | H_ab blocks.
+template <bool COMPACT = false>
 ABD_D PairEval contact_pair_eval(int kind, const V3* z, const V3* xb, double eps, double kappa, double dh,
                                  bool dyn_a, bool dyn_b, bool project, double* out, double* g12o = nullptr,
                                  double* h12o = nullptr) {
@@ -292,6 +295,21 @@ ABD_D PairEval contact_pair_eval(int kind, const V3* z, const V3* xb, double eps
         M[i][j] = acc;
       }
     if (project) jacobi_psd_reg<5>(M);
+    if (COMPACT) {
+      out[24] = 0.0;  // type: 5-column (ch (x) I3 | fq0 | fq1)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) out[25 + q] = ch[q];
+#pragma unroll
+      for (int q = 0; q < 24; ++q) {
+        out[33 + q] = fq[0][q];
+        out[57 + q] = fq[1][q];
+      }
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int j = 0; j < 5; ++j) out[81 + 5 * i + j] = M[i][j];
+      return res;
+    }
     // H24 = Q M Q^T with Q = [ch (x) e_0..2 | fq0 | fq1]
     // U[(sj,a)][beta] = ch[sj] M[a][beta] + fq0[sja] M[3][beta] + fq1[sja] M[4][beta]
 #pragma unroll
@@ -496,6 +514,18 @@ ABD_D PairEval contact_pair_eval(int kind, const V3* z, const V3* xb, double eps
           M[3 * be + a][3 * ga + b] = acc;
         }
   if (project) jacobi_psd_reg<9>(M);
+  if (COMPACT) {
+    out[24] = 1.0;  // type: 9-column Kronecker (Qx (x) I3)
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) out[25 + 3 * q + k] = Qx[q][k];
+#pragma unroll
+    for (int i = 0; i < 9; ++i)
+#pragma unroll
+      for (int j = 0; j < 9; ++j) out[49 + 9 * i + j] = M[i][j];
+    return res;
+  }
   // H24[(sj,a),(tl,b)] = sum_{be,ga} Qx[sj][be] M[(be,a),(ga,b)] Qx[tl][ga]
 #pragma unroll 1
   for (int sj = 0; sj < 8; ++sj)

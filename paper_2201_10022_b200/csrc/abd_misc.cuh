@@ -259,6 +259,30 @@ ABD_D FricEval friction_eval(const double* rec, const double* qa, const double* 
 }
 
 // g24 and H24 (full 24x24 into out, row-major) with kinematic zeroing
+// compact friction record (abd_pblk.cuh type 2): g24 | 2 | G0 | G1 | h00 h01 h11
+ABD_D void friction_compact_dev(const double* rec, const FricEval& e, double mu, bool dyn_a, bool dyn_b,
+                                bool project, double* out) {
+  double sc = mu * rec[50];
+  double gu0 = sc * e.f1y * e.u[0], gu1 = sc * e.f1y * e.u[1];
+  double an = e.y > 0.0 ? (e.f1p - e.f1y) / (e.y * e.y) : 0.0;
+  double h00 = sc * (e.f1y + an * e.u[0] * e.u[0]);
+  double h01 = sc * (an * e.u[0] * e.u[1]);
+  double h11 = sc * (e.f1y + an * e.u[1] * e.u[1]);
+  if (project) psd_project_2x2(h00, h01, h11);
+  const double* G0 = rec;
+  const double* G1 = rec + 24;
+  out[24] = 2.0;
+  for (int c = 0; c < 24; ++c) {
+    bool dc = c < 12 ? dyn_a : dyn_b;
+    out[c] = dc ? G0[c] * gu0 + G1[c] * gu1 : 0.0;
+    out[25 + c] = dc ? G0[c] : 0.0;
+    out[49 + c] = dc ? G1[c] : 0.0;
+  }
+  out[73] = h00;
+  out[74] = h01;
+  out[75] = h11;
+}
+
 ABD_D void friction_blocks_dev(const double* rec, const FricEval& e, double mu, bool dyn_a, bool dyn_b,
                                bool project, double* g24, double* haa, double* hbb, double* hab) {
   double sc = mu * rec[50];

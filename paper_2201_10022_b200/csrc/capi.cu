@@ -579,16 +579,20 @@ int abd_get_pair_blocks(abd_scene* h, int64_t* body_a, int64_t* body_b, double* 
     SC(h);
     int64_t n = s.pblk.n;
     std::vector<int2> b(n);
-    std::vector<double> blk((size_t)n * PB_STRIDE), d2(n);
+    std::vector<double> blk((size_t)n * PB_DENSE), d2(n);
     s.pblk.bodies.download(b.data(), n, s.stream);
-    s.pblk.blk.download(blk.data(), (size_t)n * PB_STRIDE, s.stream);
+    // compact records -> dense g24 | H_aa | H_bb | H_ab for readout
+    DVec<double> dense;
+    dense.resize(std::max<size_t>((size_t)n * PB_DENSE, 1));
+    launch_pblk_dense(s.stream, n, s.pblk.blk.p, dense.p);
+    dense.download(blk.data(), (size_t)n * PB_DENSE, s.stream);
     s.pblk.d2.download(d2.data(), n, s.stream);
     sync(s.stream);
     for (int64_t i = 0; i < n; ++i) {
       if (body_a) body_a[i] = b[i].x;
       if (body_b) body_b[i] = b[i].y;
       if (d_sq) d_sq[i] = d2[i];
-      const double* o = &blk[(size_t)i * PB_STRIDE];
+      const double* o = &blk[(size_t)i * PB_DENSE];
       if (grad) std::memcpy(grad + 24 * i, o, 24 * sizeof(double));
       if (hess) {
         double* H = hess + 576 * i;

@@ -157,7 +157,7 @@ int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int p
   launch_pair_blocks_act(s, KIND_EE, q, kappa, dh, project, s.w.act.p, s.w.n_act_vf, total - s.w.n_act_vf);
   tm.stop();
   // algorithmic bytes (scene form): candidate record 16 B + 4 rest points 96 B
-  // (+ eps 8 B for EE) per candidate, one PB_STRIDE record written per active pair
+  // (+ eps 8 B for EE) per candidate, one compact PB_STRIDE record written per active pair
   double bytes = 112.0 * (double)(s.cands.n_vf + s.cands.n_ee) + 8.0 * (double)s.cands.n_ee +
                  8.0 * PB_STRIDE * (double)total;
   tm.done(total, bytes);

@@ -2,6 +2,7 @@
 // (distance.py, contact.py barrier, body.py ortho/project_psd, ccd.py).
 #include "abd_contact.cuh"
 #include "abd_misc.cuh"
+#include "abd_pblk.cuh"
 #include "kernels.h"
 
 namespace abd {
@@ -143,15 +144,7 @@ __global__ void k_friction(int64_t n, const int2* __restrict__ bodies, const dou
             H[(cc + 12) * 24 + rr] = hab[rr * 12 + cc];
           }
       }
-      if (pblk) {
-        double* o = pblk + i * PB_STRIDE;
-        for (int c = 0; c < 24; ++c) o[c] = g[c];
-        for (int c = 0; c < 144; ++c) {
-          o[24 + c] = haa[c];
-          o[24 + 144 + c] = hbb[c];
-          o[24 + 288 + c] = hab[c];
-        }
-      }
+      if (pblk) friction_compact_dev(r, e, mu, dyn[b.x] != 0, dyn[b.y] != 0, project != 0, pblk + i * PB_STRIDE);
     }
   }
   if (!partials) return;
@@ -192,8 +185,7 @@ __global__ void k_friction_pblk(int64_t n, const int2* __restrict__ bodies, cons
     int2 b = bodies[i];
     const double* r = rec + i * FRIC_STRIDE;
     FricEval e = friction_eval(r, q + 12 * b.x, q + 12 * b.y, eh);
-    double* o = pblk + i * PB_STRIDE;
-    friction_blocks_dev(r, e, mu, dyn[b.x] != 0, dyn[b.y] != 0, project != 0, o, o + 24, o + 168, o + 312);
+    friction_compact_dev(r, e, mu, dyn[b.x] != 0, dyn[b.y] != 0, project != 0, pblk + i * PB_STRIDE);
   }
 }
 
@@ -208,7 +200,7 @@ __global__ void __launch_bounds__(64) k_contact_pairs(int kind, int64_t n, const
   V3 p[4], r[4];
   ldz(z, i, p);
   ldz(xb, i, r);
-  double blk[PB_STRIDE];
+  double blk[PB_DENSE];
   contact_pair_eval(kind, p, r, eps[i], kappa, dh, dyn[2 * i] != 0, dyn[2 * i + 1] != 0, project != 0, blk,
                     g12o + 12 * i, h12o + 144 * i);
   for (int k = 0; k < 24; ++k) g24o[24 * i + k] = blk[k];
@@ -279,6 +271,30 @@ void launch_accd(cudaStream_t st, int kind, int64_t n, const double* x, const do
   k_accd<<<GRID(n, 128), st>>>(kind, n, x, dx, slack, tmax, max_iters, t, err);
   note_launch("k_accd");
 }
+// compact pair records -> dense g24 | H_aa | H_bb | H_ab (readout / tests)
+__global__ void k_pblk_dense(int64_t n, const double* __restrict__ pblk, double* dense) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * PB_DENSE) return;
+  const int64_t p = t / PB_DENSE;
+  const int e = (int)(t % PB_DENSE);
+  const double* rec = pblk + p * PB_STRIDE;
+  double v;
+  if (e < 24) {
+    v = rec[e];
+  } else {
+    const int blk = (e - 24) / 144, idx = (e - 24) % 144, i = idx / 12, k = idx % 12;
+    const int R = 12 * (blk == 1) + i, C = 12 * (blk >= 1) + k;
+    v = pb_entry(rec, R, C);
+  }
+  dense[t] = v;
+}
+
+void launch_pblk_dense(cudaStream_t st, int64_t n, const double* pblk, double* dense) {
+  if (n <= 0) return;
+  k_pblk_dense<<<grid_for(n * PB_DENSE, 256), 256, 0, st>>>(n, pblk, dense);
+  note_launch("k_pblk_dense");
+}
+
 void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const double* rec, double mu, const double* q,
                      const unsigned char* dyn, double dt, double eps_v, int project, double* partials,
                      double* grad24, double* hess24, double* pblk) {

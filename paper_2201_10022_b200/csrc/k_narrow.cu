@@ -75,25 +75,6 @@ __global__ void k_pair_flags(SceneView sv, int kind, int64_t n, const int4* __re
 }
 
 // K3 first pass: one thread per candidate, active ones write g24 | haa | hbb | hab
-__global__ void __launch_bounds__(64) k_pair_blocks(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
-                                                     const double* __restrict__ q, double kappa, double dh,
-                                                     int project, const int* __restrict__ flags,
-                                                     const int* __restrict__ pos, int64_t base, int2* out_bodies,
-                                                     double* out_blk, double* out_d2) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n || !flags[i]) return;
-  int4 r = rows[i];
-  PairIds ids = pair_ids(sv, kind, r);
-  V3 z[4], xb[4];
-  pair_points(sv, ids, q, z, xb);
-  int64_t o = base + pos[i];
-  double* blk = out_blk + o * PB_STRIDE;
-  PairEval ev = contact_pair_eval(kind, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0,
-                                  blk);
-  out_bodies[o] = make_int2(r.x, r.z);
-  out_d2[o] = ev.d2;
-}
-
 // same over the compacted active list: full warps instead of ~1/4 active lanes;
 // specialised per kind so the VF kernel carries none of the mollified-EE state
 template <int KIND>
@@ -112,7 +93,8 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
   V3 z[4], xb[4];
   pair_points(sv, ids, q, z, xb);
   double* blk = out_blk + slot * PB_STRIDE;
-  PairEval ev = contact_pair_eval(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0, project != 0,
+  PairEval ev = contact_pair_eval<true>(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0,
+                                        project != 0,
                                   blk);
   out_bodies[slot] = make_int2(r.x, r.z);
   out_d2[slot] = ev.d2;
@@ -526,16 +508,6 @@ void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* fla
   note_launch("k_pair_flags");
 }
 
-void launch_pair_blocks(Scene& s, int kind, const double* q, double kappa, double dh, int project, const int* flags,
-                        const int* pos, int64_t base, int* err) {
-  (void)err;
-  int64_t n;
-  const int4* rows = rows_of(s, kind, n);
-  if (!n) return;
-  k_pair_blocks<<<grid_for(n, 64), 64, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, project, flags, pos,
-                                                      base, s.pblk.bodies.p, s.pblk.blk.p, s.pblk.d2.p);
-  note_launch("k_pair_blocks");
-}
 
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act) {
   if (!n) return;

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "abd_pblk.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -164,13 +165,16 @@ __global__ void k_reduce_blocks(int n, const int* __restrict__ row_ptr, const in
     int64_t p = v >> 2;
     int which = v & 3;
     const double* blk = pblk + p * PB_STRIDE;
-    const double* h = blk + 24 + 144 * (which == 0 ? 0 : (which == 1 ? 1 : 2));
+    // target entry (i, k) = H24(12 s_r + i, 12 s_c + k) for the aa / bb / ab blocks;
+    // which 3 is the transposed ab block: H24(k, 12 + i)
 #pragma unroll
     for (int e = 0; e < 5; ++e) {
       int idx = lane + 32 * e;
       if (idx < 144) {
-        int src = which == 3 ? (idx % 12) * 12 + idx / 12 : idx;
-        acc[e] += h[src];
+        const int i = idx / 12, k = idx % 12;
+        const int R = which == 3 ? k : 12 * (which == 1) + i;
+        const int Cc = which == 3 ? 12 + i : 12 * (which >= 1) + k;
+        acc[e] += pb_entry(blk, R, Cc);
       }
     }
     if (which < 2 && lane < 12) gacc += blk[12 * which + lane];

@@ -47,6 +47,7 @@ void launch_accd(cudaStream_t st, int kind, int64_t n, const double* x, const do
 void launch_contact_pairs(cudaStream_t st, int kind, int64_t n, const double* z, const double* xb, const double* eps,
                           double kappa, double dh, const unsigned char* dyn, int project, double* g12, double* h12,
                           double* g24, double* h24);
+void launch_pblk_dense(cudaStream_t st, int64_t n, const double* pblk, double* dense);
 void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const double* rec, double mu,
                      const double* q, const unsigned char* dyn, double dt, double eps_v, int project,
                      double* energy_partials, double* grad24, double* hess24, double* pblk_out);
@@ -54,8 +55,6 @@ void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const doubl
 // ---- scene narrow phase (k_narrow.cu) ----
 // activity flags d^2 < d_hat^2 for the resident candidates of `kind`
 void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err);
-void launch_pair_blocks(Scene& s, int kind, const double* q, double kappa, double dh, int project,
-                        const int* flags, const int* pos, int64_t base, int* err);
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act);
 void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, double dh, int project,
                             const int* act, int64_t slot_off, int64_t count);

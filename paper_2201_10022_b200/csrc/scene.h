@@ -97,8 +97,10 @@ struct FrictionSet {
   double mu = 0.0;
 };
 
-// per-active-pair local blocks (PairBlocks restated): g24 | haa | hbb | hab
-constexpr int PB_STRIDE = 24 + 3 * 144;
+// per-active-pair records (PairBlocks restated): compact g24 | type | low-rank
+// factors (abd_pblk.cuh); PB_DENSE = g24 | haa | hbb | hab for dense readout
+constexpr int PB_STRIDE = 136;
+constexpr int PB_DENSE = 24 + 3 * 144;
 struct PairBlockSet {
   DVec<int2> bodies;
   DVec<double> blk;  // PB_STRIDE per pair

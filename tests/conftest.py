@@ -3,6 +3,11 @@ import sys
 
 import numpy as np
 import pytest
+from threadpoolctl import threadpool_limits
+
+# single-threaded BLAS/LAPACK for the oracle: multi-threaded eigh/solve reductions
+# change rounding with machine load, which can flip near-zero PSD clamps
+_BLAS_LIMIT = threadpool_limits(limits=1)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
