@@ -34,7 +34,8 @@ ABD_D double accd_query(int kind, V3* x, const V3* dx, double slack, double tmax
   double t = 0.0;
   double stall_eps = xmul(1e-12, d0);
   for (int it = 0; it < max_iters; ++it) {
-    double d = sqrt(pair_d2(kind, x));
+    // the first iterate is x itself: reuse d0 (bitwise the same value)
+    double d = it == 0 ? d0 : sqrt(pair_d2(kind, x));
     double adv = xsub(d, gap);
     bool stalled = adv < stall_eps;
     double tl = stalled ? 0.0 : adv / lp;
