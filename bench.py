@@ -156,8 +156,9 @@ def run_reference(args):
         "unit": "steps/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": 1e3 / r["value"] if r["value"] else None, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
-        "config": {"workload": "icosphere_pile 20x20x25 (10,001 bodies) -- CPU sample 4x4x2 scaled",
-                   "parallelism": "cpu"},
+        "config": {"workload": "icosphere_pile 20x20x25 (10,001 bodies, seed 0): CPU sample = 8x8x2 sub-pile "
+                               "of the same generator, scaled linearly by body count",
+                   "parallelism": f"cpu ({cores} host threads)"},
         "cpu_baseline": {"value": r["value"], "unit": "steps/s", "cores": cores, "kind": "port",
                          "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} "
                                    f"icospheres + ground, same generator) from step {args.warmup}, "
