@@ -42,18 +42,21 @@ ABD_D void jacobi_psd_reg(double (&a)[N][N]) {
     for (int i = 0; i < N; ++i)
 #pragma unroll
       for (int j = i + 1; j < N; ++j) off += a[i][j] * a[i][j];
-    if (off <= 1e-34 * fro) break;
+    if (off <= 1e-32 * fro) break;
 #pragma unroll
     for (int p = 0; p < N - 1; ++p) {
 #pragma unroll
       for (int q = p + 1; q < N; ++q) {
         double apq = a[p][q];
         if (apq * apq > 1e-40 * fro) {
-          double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
-          double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-          double c = 1.0 / sqrt(t * t + 1.0);
+          // rotation with MUFU-seeded reciprocals (no IEEE div/sqrt sequences)
+          double theta = (a[q][q] - a[p][p]) * rcp_fast(2.0 * apq);
+          const double th2 = theta * theta + 1.0;
+          const double sq = th2 * rsqrt_fast(th2);  // sqrt(theta^2 + 1)
+          double t = (theta >= 0.0 ? 1.0 : -1.0) * rcp_fast(fabs(theta) + sq);
+          double c = rsqrt_fast(t * t + 1.0);
           double s = t * c;
-          double tau = s / (1.0 + c);
+          double tau = s * rcp_fast(1.0 + c);
           a[p][p] -= t * apq;
           a[q][q] += t * apq;
           a[p][q] = 0.0;

@@ -17,6 +17,24 @@
 
 namespace abd {
 
+// fast reciprocal / reciprocal square root for the small eigen-solvers (not on
+// the bit-exact paths): MUFU seed + Newton steps, no libdevice slow-path call
+// (whose register saves spill the callers' register-resident matrices)
+ABD_D double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+ABD_D double rsqrt_fast(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-0.5 * x, r * r, 1.5);
+  return r * fma(-0.5 * x, r * r, 1.5);
+}
+
 ABD_D double xadd(double a, double b) { return __dadd_rn(a, b); }
 ABD_D double xsub(double a, double b) { return __dsub_rn(a, b); }
 ABD_D double xmul(double a, double b) { return __dmul_rn(a, b); }

@@ -124,9 +124,10 @@ ABD_D void sym3_eig(double S[3][3], double w[3], double V[3][3]) {
       for (int q = p + 1; q < 3; ++q) {
         double apq = S[p][q];
         if (apq == 0.0) continue;
-        double theta = (S[q][q] - S[p][p]) / (2.0 * apq);
-        double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-        double c = 1.0 / sqrt(t * t + 1.0), s = t * c, tau = s / (1.0 + c);
+        double theta = (S[q][q] - S[p][p]) * rcp_fast(2.0 * apq);
+        const double th2 = theta * theta + 1.0;
+        double t = (theta >= 0.0 ? 1.0 : -1.0) * rcp_fast(fabs(theta) + th2 * rsqrt_fast(th2));
+        double c = rsqrt_fast(t * t + 1.0), s = t * c, tau = s * rcp_fast(1.0 + c);
         S[p][p] -= t * apq;
         S[q][q] += t * apq;
         S[p][q] = S[q][p] = 0.0;
