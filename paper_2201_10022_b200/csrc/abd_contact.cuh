@@ -126,7 +126,9 @@ struct PairEval {
 // h12/g12 (optional, may be null): point-space derivatives for testing.
 // COMPACT: `out` receives a compact pair record (abd_pblk.cuh: g24 | type |
 // low-rank factors) instead of the dense g24 | H_aa | H_bb | H_ab blocks.
-template <bool COMPACT = false>
+// MOLL: 0 = either path, 1 = caller guarantees an unmollified pair (the 9-column
+// code is compiled out), 2 = caller guarantees a mollified EE pair.
+template <bool COMPACT = false, int MOLL = 0>
 ABD_D PairEval contact_pair_eval(int kind, const V3* z, const V3* xb, double eps, double kappa, double dh,
                                  bool dyn_a, bool dyn_b, bool project, double* out, double* g12o = nullptr,
                                  double* h12o = nullptr) {
@@ -197,7 +199,7 @@ ABD_D PairEval contact_pair_eval(int kind, const V3* z, const V3* xb, double eps
   double* hab = out + 24 + 288;
   PairEval res;
   res.d2 = cl.d2;
-  if (!moll) {
+  if (MOLL == 1 || (MOLL == 0 && !moll)) {
     res.value = b0;
     // ---------------- 5-column path ----------------
     // g24 = 2 b1 c (x) r

@@ -76,28 +76,165 @@ __global__ void k_pair_flags(SceneView sv, int kind, int64_t n, const int4* __re
 
 // K3 first pass: one thread per candidate, active ones write g24 | haa | hbb | hab
 // same over the compacted active list: full warps instead of ~1/4 active lanes;
-// specialised per kind so the VF kernel carries none of the mollified-EE state
+// specialised per kind so the VF kernel carries none of the mollified-EE state.
+// EE pairs whose mollifier is active (near-parallel edges) are deferred to
+// k_pair_blocks_moll, so the common EE pairs also run the lean 5-column kernel.
+ABD_D bool ee_mollified(const V3* z, double eps) {
+  V3 u = z[1] - z[0], v = z[3] - z[2];
+  V3 cr = cross(u, v);
+  double cc = dot(cr, cr);
+  double ratio = eps > 0.0 ? cc / eps : 1.0;
+  return ratio < 1.0;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_unused, int64_t count,
                                                          const int* __restrict__ act, int64_t cand_off,
                                                          const int4* __restrict__ rows, const double* __restrict__ q,
                                                          double kappa, double dh, int project, int64_t slot_off,
-                                                         int2* out_bodies, double* out_blk, double* out_d2) {
+                                                         int2* out_bodies, double* out_blk, double* out_d2,
+                                                         int* moll_list, int* moll_count) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= count) return;
+  (void)kind_unused;
   const int64_t slot = slot_off + t;
   const int64_t i = act[slot] - cand_off;
   int4 r = rows[i];
-  (void)kind_unused;
   PairIds ids = pair_ids(sv, KIND, r);
   V3 z[4], xb[4];
   pair_points(sv, ids, q, z, xb);
-  double* blk = out_blk + slot * PB_STRIDE;
-  PairEval ev = contact_pair_eval<true>(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0,
-                                        project != 0,
-                                  blk);
   out_bodies[slot] = make_int2(r.x, r.z);
+  if (KIND == KIND_EE && ee_mollified(z, ids.eps)) {
+    moll_list[atomicAdd(moll_count, 1)] = (int)slot;
+    return;
+  }
+  double* blk = out_blk + slot * PB_STRIDE;
+  PairEval ev = contact_pair_eval<true, 1>(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0,
+                                           project != 0, blk);
   out_d2[slot] = ev.d2;
+}
+
+// Warp-parallel PSD clamp of a symmetric 9x9 (padded to 10) in shared memory:
+// parallel-ordered cyclic Jacobi (round-robin tournament, 5 disjoint rotations
+// per round, 9 rounds per sweep), then M <- V max(w, 0) V^T.
+__device__ void warp_psd9(double (*A)[11], double (*V)[11], double4* rot, int lane) {
+  for (int e = lane; e < 110; e += 32) {
+    const int i = e / 11, j = e % 11;
+    if (j < 10) V[i][j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  double fro = 0.0;
+  for (int e = lane; e < 81; e += 32) fro += A[e / 9][e % 9] * A[e / 9][e % 9];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  if (fro == 0.0) return;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    double off = 0.0;
+    for (int e = lane; e < 81; e += 32) {
+      const int i = e / 9, j = e % 9;
+      if (j > i) off += A[i][j] * A[i][j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xffffffffu, off, o);
+    if (off <= 1e-32 * fro) break;
+    for (int round = 0; round < 9; ++round) {
+      // circle-method pairing: round r pairs (r, 9) and ((r + k) % 9, (r - k) % 9),
+      // k = 1..4 -- every pair of 0..8 exactly once per sweep; 9 = zero padding
+      if (lane < 5) {
+        const int a = lane == 0 ? round : (round + lane) % 9;
+        const int b = lane == 0 ? 9 : (round - lane + 9) % 9;
+        const int p = min(a, b), q = max(a, b);
+        double c = 1.0, sn = 0.0;
+        const double apq = A[p][q];
+        if (apq * apq > 1e-40 * fro) {
+          const double theta = (A[q][q] - A[p][p]) * rcp_fast(2.0 * apq);
+          const double th2 = theta * theta + 1.0;
+          const double t = (theta >= 0.0 ? 1.0 : -1.0) * rcp_fast(fabs(theta) + th2 * rsqrt_fast(th2));
+          c = rsqrt_fast(t * t + 1.0);
+          sn = t * c;
+        }
+        rot[lane] = make_double4((double)p, (double)q, c, sn);
+      }
+      __syncwarp();
+      // rows: B = J^T A (rows p, q of each rotation)
+      for (int e = lane; e < 50; e += 32) {
+        const int k = e / 10, j = e % 10;
+        const double4 r = rot[k];
+        const int p = (int)r.x, q = (int)r.y;
+        const double ap = A[p][j], aq = A[q][j];
+        A[p][j] = r.z * ap - r.w * aq;
+        A[q][j] = r.w * ap + r.z * aq;
+      }
+      __syncwarp();
+      // columns: A = B J, and V = V J
+      for (int e = lane; e < 100; e += 32) {
+        const int k = (e % 50) / 10, i = e % 10;
+        const double4 r = rot[k];
+        const int p = (int)r.x, q = (int)r.y;
+        double (*X)[11] = e < 50 ? A : V;
+        const double xp = X[i][p], xq = X[i][q];
+        X[i][p] = r.z * xp - r.w * xq;
+        X[i][q] = r.w * xp + r.z * xq;
+      }
+      __syncwarp();
+    }
+  }
+  // M = V diag(max(w, 0)) V^T (w = diag A), written into A's upper triangle first
+  double res[3];
+  int n_res = 0;
+  for (int e = lane; e < 81; e += 32) {
+    const int i = e / 9, j = e % 9;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc += V[i][k] * fmax(A[k][k], 0.0) * V[j][k];
+    res[n_res++] = acc;
+  }
+  __syncwarp();
+  n_res = 0;
+  for (int e = lane; e < 81; e += 32) A[e / 9][e % 9] = res[n_res++];
+  __syncwarp();
+}
+
+// the deferred mollified EE pairs (9-column path), one warp per pair: lane 0
+// builds the record with the unprojected 9x9 core, the warp clamps it
+constexpr int MOLL_WARPS = 4;
+__global__ void __launch_bounds__(32 * MOLL_WARPS) k_pair_blocks_moll(SceneView sv, const int* __restrict__ moll_list,
+                                                                       const int* __restrict__ moll_count,
+                                                                       const int* __restrict__ act, int64_t cand_off,
+                                                                       const int4* __restrict__ rows,
+                                                                       const double* __restrict__ q, double kappa,
+                                                                       double dh, int project, double* out_blk,
+                                                                       double* out_d2) {
+  __shared__ double As[MOLL_WARPS][10][11], Vs[MOLL_WARPS][10][11];
+  __shared__ double4 rots[MOLL_WARPS][5];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = *moll_count;
+  for (int t = blockIdx.x * MOLL_WARPS + w; t < n; t += gridDim.x * MOLL_WARPS) {
+    const int64_t slot = moll_list[t];
+    double* blk = out_blk + slot * PB_STRIDE;
+    if (lane == 0) {
+      const int64_t i = act[slot] - cand_off;
+      int4 r = rows[i];
+      PairIds ids = pair_ids(sv, KIND_EE, r);
+      V3 z[4], xb[4];
+      pair_points(sv, ids, q, z, xb);
+      PairEval ev = contact_pair_eval<true, 2>(KIND_EE, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0,
+                                               sv.dyn[r.z] != 0, false, blk);
+      out_d2[slot] = ev.d2;
+    }
+    __syncwarp();
+    if (project) {
+      double (*A)[11] = As[w];
+      for (int e = lane; e < 110; e += 32) {
+        const int i = e / 11, j = e % 11;
+        if (j < 10) A[i][j] = (i < 9 && j < 9) ? blk[49 + 9 * i + j] : 0.0;
+      }
+      __syncwarp();
+      warp_psd9(A, Vs[w], rots[w], lane);
+      for (int e = lane; e < 81; e += 32) blk[49 + e] = A[e / 9][e % 9];
+    }
+    __syncwarp();
+  }
 }
 
 __global__ void k_scatter_active(int64_t n, const int* __restrict__ flags, const int* __restrict__ pos, int* act) {
@@ -521,14 +658,23 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
   int64_t n;
   const int4* rows = rows_of(s, kind, n);
   const int64_t cand_off = kind == KIND_VF ? 0 : s.cands.n_vf;
-  if (kind == KIND_VF)
+  int* moll_count = reinterpret_cast<int*>(s.w.ull.p + 10);
+  if (kind == KIND_VF) {
     k_pair_blocks_act<KIND_VF><<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q,
                                                                         kappa, dh, project, slot_off, s.pblk.bodies.p,
-                                                                        s.pblk.blk.p, s.pblk.d2.p);
-  else
+                                                                        s.pblk.blk.p, s.pblk.d2.p, nullptr, nullptr);
+  } else {
+    s.w.moll.resize(std::max<int64_t>(count, 1));
+    CK(cudaMemsetAsync(moll_count, 0, sizeof(int), s.stream));
     k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q,
                                                                         kappa, dh, project, slot_off, s.pblk.bodies.p,
-                                                                        s.pblk.blk.p, s.pblk.d2.p);
+                                                                        s.pblk.blk.p, s.pblk.d2.p, s.w.moll.p,
+                                                                        moll_count);
+    const int grid = (int)std::min<int64_t>(grid_for(count, MOLL_WARPS), 16 * (int64_t)s.num_sms);
+    k_pair_blocks_moll<<<grid, 32 * MOLL_WARPS, 0, s.stream>>>(view(s), s.w.moll.p, moll_count, act, cand_off, rows,
+                                                               q, kappa, dh, project, s.pblk.blk.p, s.pblk.d2.p);
+    note_launch("k_pair_blocks_moll");
+  }
   note_launch("k_pair_blocks");
 }
 

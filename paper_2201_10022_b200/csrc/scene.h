@@ -180,6 +180,7 @@ struct Scene {
   struct Work {
     DVec<int64_t> comm_cnt, comm_buf, fric_keys, fric_keys_all;  // multi-GPU scratch
     DVec<int> act;      // compacted active candidate indices (VF then EE)
+    DVec<int> moll;     // active EE slots with an active mollifier (deferred 9-column path)
     int64_t n_act_vf = 0;
     DVec<int> flags, pos, err, order, cnt, off, seg_s, seg_e, row_of, nsel, bad, iters;
     DVec<uint64_t> k0, k1, e0, e1;
