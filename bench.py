@@ -171,6 +171,120 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def run_micro(args):
+    """--workload micro: BASELINE config 2 (SURVEY §8(d) kernel microbenchmark).
+
+    One step = `assemble` (K1 + K3 + BSR reduction) over 10M VF + 10M EE synthetic
+    pairs on 100k bodies, then the block-Jacobi PCG to 1e-8 relative residual.
+    """
+    from paper_2201_10022_b200 import _native, microbench, scenes
+
+    t0 = time.perf_counter()
+    data = scenes.microbench_pairs(seed=0, n_bodies=args.micro_bodies, n_vf=args.micro_pairs,
+                                   n_ee=args.micro_pairs)
+    sysm = microbench.PairSystem(data)
+    setup_s = time.perf_counter() - t0
+    L = _native.lib()
+    sc = sysm.scene
+    for _ in range(args.warmup):
+        sysm.assemble()
+        sysm.solve()
+    _native.check(L.abd_kernel_stats_reset(sc.ptr))
+    n_launch0 = _native.kernel_launches()
+    asm_ms, sol_ms, iters, rels = [], [], [], []
+    ms = C.c_double(0.0)
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            _native.check(L.abd_timer_start(sc.ptr))
+            sysm.assemble()
+            _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
+            asm_ms.append(ms.value)
+            _native.check(L.abd_timer_start(sc.ptr))
+            _, it, rel = sysm.solve()
+            _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
+            sol_ms.append(ms.value)
+            iters.append(it)
+            rels.append(rel)
+    launches = _native.kernel_launches() - n_launch0
+    P_all = sysm.n_vf + sysm.n_ee
+    B = sysm.B
+    n_blk = B + 2 * sysm.n_off
+    tot_ms = float(np.sum(asm_ms) + np.sum(sol_ms))
+    kst = {}
+    for which, name in ((0, "k_cg"), (1, "k_pair_blocks")):
+        n_, t_, b_, u_ = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
+        _native.check(L.abd_kernel_stats(sc.ptr, which, C.byref(n_), C.byref(t_), C.byref(b_), C.byref(u_)))
+        kst[name] = {"launches": n_.value, "ms": t_.value, "bytes": b_.value, "units": u_.value}
+    pk, pk_kind = peaks()
+    hbm = float(pk.get("hbm_gbs", HBM_FALLBACK))
+    # K4 per PCG iteration (SURVEY §8(d)): 1152 (N_blk + B_d) + 13 x 96 B_d
+    it_bytes = 1152.0 * (n_blk + B) + 13 * 96.0 * B
+    it_ms = float(np.sum(sol_ms)) / max(1, int(np.sum(iters)))
+    # K3 per call, pre-gathered form (SURVEY §8(d)): 104 P_vf + 112 P_ee + 1152 N_blk + 192 B
+    k3_bytes = 104.0 * sysm.n_vf + 112.0 * sysm.n_ee + 1152.0 * n_blk + 192.0 * B
+    k3_ms = float(np.mean(asm_ms))
+    cpu = None
+    if not args.no_cpu:
+        cpu = micro_cpu_rate(args.cpu_budget)
+    line = {
+        "metric": "microbench assemble + PCG time (100k bodies, 10M VF + 10M EE pairs, fp64)",
+        "value": tot_ms / args.steps, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, scenes.microbench_pairs)",
+        "config": {"workload": f"BASELINE config 2: {B} bodies, {sysm.n_vf} VF + {sysm.n_ee} EE pairs, "
+                               f"Morton +-1..4 body graph ({sysm.n_off} off-diagonal blocks), all pairs active",
+                   "assemble_ms": float(np.mean(asm_ms)), "pcg_ms": float(np.mean(sol_ms)),
+                   "pcg_iters": iters, "pcg_rel_res": rels, "pcg_ms_per_iter": it_ms,
+                   "pairs_per_s_assemble": P_all / (k3_ms * 1e-3), "setup_s": setup_s,
+                   "l2": "inputs (~2 GB rest + 22 GB pair records) exceed L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": "K4 PCG iteration (k_cg) / K3 assemble",
+                     "achieved": it_bytes / (it_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": it_bytes / (it_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                     "algorithmic_bytes_per_launch": it_bytes,
+                     "bytes_model": "K4: 1152 (N_blk + B_d) + 13 x 96 B_d per PCG iteration",
+                     "assemble": {"achieved": k3_bytes / (k3_ms * 1e-3) / 1e9, "bytes": k3_bytes,
+                                  "frac": k3_bytes / (k3_ms * 1e-3) / 1e9 / hbm,
+                                  "bytes_model": "K3 pre-gathered: 104 P_vf + 112 P_ee + 1152 N_blk + 192 B"},
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})", "kernels": kst},
+        "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def micro_cpu_rate(budget_s):
+    """Oracle per-pair pipeline (contact_blocks: distance, barrier, J^T H J, 24x24 PSD), pairs/s, 1 thread,
+    on a sample drawn by the same generator (2,000 bodies, equal VF / EE counts)."""
+    from types import SimpleNamespace
+
+    from threadpoolctl import threadpool_limits
+
+    from oracle import abd_oracle as O
+    from paper_2201_10022_b200 import microbench, scenes
+    lim = threadpool_limits(limits=1)
+    n, el, seed = 0, 0.0, 1
+    while el < budget_s:
+        d = scenes.microbench_pairs(seed=seed, n_bodies=2000, n_vf=2000, n_ee=2000)
+        a = microbench.soup_arrays(d)
+        bodies = []
+        for b in range(len(d["q"])):
+            v0, v1 = a["v_off"][b], a["v_off"][b + 1]
+            e0, e1 = a["e_off"][b], a["e_off"][b + 1]
+            t0, t1 = a["t_off"][b], a["t_off"][b + 1]
+            bodies.append(SimpleNamespace(rest=a["rest"][v0:v1], edges=a["edges"][e0:e1], triangles=a["tris"][t0:t1],
+                                          edge_rest_len_sq=a["el2"][e0:e1], dynamic=True))
+        ts = time.perf_counter()
+        O.contact_blocks(bodies, d["q"], a["vf"], a["ee"], 1e4, d["d_hat"])
+        el += time.perf_counter() - ts
+        n += len(a["vf"]) + len(a["ee"])
+        seed += 1
+    lim.restore_original_limits()
+    return {"value": n / el, "unit": "pairs/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/abd_oracle.py contact_blocks (distance, barrier, J^T H J, PSD projection) on {n} "
+                      f"pairs of the config-2 generator (2,000-body draws, half VF, half EE) in {el:.1f}s; the GPU "
+                      "rate to compare is config.pairs_per_s_assemble"}
+
+
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -185,7 +299,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--workload", default="pile", choices=["pile", "micro"],
+                    help="pile = BASELINE config 4 (headline); micro = config 2 kernel microbenchmark")
+    ap.add_argument("--micro-bodies", type=int, default=100_000)
+    ap.add_argument("--micro-pairs", type=int, default=10_000_000, help="VF pairs = EE pairs")
     args = ap.parse_args()
+    if args.workload == "micro":
+        if args.impl == "reference" or int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_micro(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return

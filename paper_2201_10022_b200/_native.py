@@ -289,7 +289,6 @@ class Scene:
     """Owns an abd_scene*; geometry uploaded once from CollisionBody arrays."""
 
     def __init__(self, bodies, masses=None, stiffness=None):
-        L = lib()
         B = len(bodies)
         self.n_bodies = B
         v_off = np.cumsum([0] + [len(b.rest) for b in bodies]).astype(np.int64)
@@ -313,6 +312,22 @@ class Scene:
             for i, k in enumerate(stiffness):
                 if k is not None:
                     K[i] = k
+        self._create(v_off, e_off, t_off, rest, edges, tris, el2, dyn, M, K)
+
+    @classmethod
+    def from_arrays(cls, v_off, e_off, t_off, rest, edges, tris, edge_len_sq, dynamic, mass, stiffness):
+        """Scene from flat SystemModel arrays (the abd_scene_create layout: per-body
+        LOCAL vertex indices in edges/tris, (n_bodies+1) prefix offsets)."""
+        self = cls.__new__(cls)
+        self.n_bodies = len(v_off) - 1
+        self._create(i64a(v_off), i64a(e_off), i64a(t_off), f64(rest).reshape(-1, 3), i64a(edges).reshape(-1, 2),
+                     i64a(tris).reshape(-1, 3), f64(edge_len_sq), np.ascontiguousarray(dynamic, dtype=np.uint8),
+                     mass, stiffness)
+        return self
+
+    def _create(self, v_off, e_off, t_off, rest, edges, tris, el2, dyn, M, K):
+        L = lib()
+        B = self.n_bodies
         self.dynamic = dyn.astype(bool)
         self.ptr = L.abd_scene_create(B, v_off, e_off, t_off, rest, edges, tris, el2, dyn, f64(M), f64(K))
         if not self.ptr:
