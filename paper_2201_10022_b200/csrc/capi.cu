@@ -801,6 +801,7 @@ int abd_timer_start(abd_scene* h) {
   return guard([&] {
     SC(h);
     CK(cudaStreamSynchronize(s.stream));
+    host_prof_reset();
     CK(cudaEventRecord(s.tev0, s.stream));
   });
 }
@@ -810,6 +811,7 @@ int abd_timer_stop(abd_scene* h, double* ms) {
     SC(h);
     CK(cudaEventRecord(s.tev1, s.stream));
     CK(cudaEventSynchronize(s.tev1));
+    host_prof_dump();
     float m = 0.f;
     CK(cudaEventElapsedTime(&m, s.tev0, s.tev1));
     *ms = m;

@@ -120,7 +120,7 @@ void comm_allreduce(Scene& s, void* dptr, int64_t count, int dtype, int op) {
     nccl_check(nccl().all_reduce(dptr, dptr, (size_t)count, nd, no, s.comm.nccl, s.stream), "ncclAllReduce");
     return;
   }
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   int rc = s.comm.cb(s.comm.user, dptr, count, dtype, op);
   if (rc != 0) throw Error(ABD_ERR_CUDA, "collective callback failed");
 }
@@ -144,11 +144,11 @@ int64_t comm_allgather_i64(Scene& s, const int64_t* local, int64_t n_local, DVec
   DVec<int64_t>& cnt = s.w.comm_cnt;
   cnt.resize(W);
   cnt.zero(s.stream);
-  CK(cudaMemcpyAsync(cnt.p + s.comm.rank, &n_local, sizeof(int64_t), cudaMemcpyHostToDevice, s.stream));
+  dev_set_i64(s.stream, cnt.p + s.comm.rank, n_local);
   comm_allreduce(s, cnt.p, W, 2, 0);
   std::vector<int64_t> hc(W);
   cnt.download(hc.data(), W, s.stream);
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   int64_t mx = 0, tot = 0;
   for (int64_t c : hc) mx = std::max(mx, c), tot += c;
   DVec<int64_t>& buf = s.w.comm_buf;

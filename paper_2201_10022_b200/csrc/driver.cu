@@ -136,7 +136,7 @@ static int active_scan(Scene& s, const double* q, double dh) {
   CK(cudaMemcpyAsync(hp, w.pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaMemcpyAsync(hp + 1, w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
   CK(cudaMemcpyAsync(hp + 2, w.pos.p + n_vf, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   if (hp[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
                                                  "(intersection reached; CCD filtering must prevent this)");
   w.n_act_vf = hp[2];
@@ -180,7 +180,7 @@ void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, 
       CK(cudaMemcpyAsync(k2.p, s.pblk.blk.p, nc * PB_STRIDE * sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
       CK(cudaMemcpyAsync(d2.p, s.pblk.d2.p, nc * sizeof(double), cudaMemcpyDeviceToDevice, s.stream));
     }
-    CK(cudaStreamSynchronize(s.stream));
+    SSYNC(s.stream);
     std::swap(s.pblk.bodies.p, b2.p);
     std::swap(s.pblk.bodies.cap, b2.cap);
     std::swap(s.pblk.blk.p, k2.p);
@@ -252,7 +252,7 @@ static void energy_terms(Scene& s, const double* q, const double* qt, double dt,
   CK(cudaMemcpyAsync(s.h_pinned, s.w.scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
   int* he = reinterpret_cast<int*>(s.h_pinned + 8);
   CK(cudaMemcpyAsync(he, s.w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   if (he[0]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
                                                  "(intersection reached; CCD filtering must prevent this)");
   for (int k = 0; k < 4; ++k) out[k] = s.h_pinned[k];
@@ -333,7 +333,7 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   w.lserr.resize(2);
   w.lserr.zero(st);
   unsigned long long one = d_to_bits(1.0);
-  CK(cudaMemcpyAsync(tmin, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+  dev_set_u64(st, tmin, one);
   EventTimer tm(s, 2);
   launch_ccd(s, KIND_VF, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
   launch_ccd(s, KIND_EE, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
@@ -353,7 +353,7 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   CK(cudaMemcpyAsync(hp, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hp + 1, w.lsscal.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hp + 9, w.lserr.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  SSYNC(st);
   const int* he = reinterpret_cast<const int*>(hp + 9);
   if (he[0]) throw Error(ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
   if (he[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
@@ -379,7 +379,7 @@ double step_filter(Scene& s, const double* q, const double* dq, double slack) {
   s.w.err.resize(2);
   s.w.err.zero(s.stream);
   unsigned long long one = d_to_bits(1.0);
-  CK(cudaMemcpyAsync(tmin, &one, sizeof(one), cudaMemcpyHostToDevice, s.stream));
+  dev_set_u64(s.stream, tmin, one);
   EventTimer tm(s, 2);
   launch_ccd(s, KIND_VF, q, dq, slack, tmin, s.w.err.p);
   launch_ccd(s, KIND_EE, q, dq, slack, tmin, s.w.err.p);
@@ -390,7 +390,7 @@ double step_filter(Scene& s, const double* q, const double* dq, double slack) {
   CK(cudaMemcpyAsync(hb, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
   int* he = reinterpret_cast<int*>(s.h_pinned + 2);
   CK(cudaMemcpyAsync(he, s.w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   if (he[0]) throw Error(ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
   int64_t nq = s.cands.n_vf + s.cands.n_ee;
   tm.done(nq, 112.0 * (double)nq + 192.0 * s.B);
@@ -400,13 +400,13 @@ double step_filter(Scene& s, const double* q, const double* dq, double slack) {
 double candidate_min_d2(Scene& s, const double* q) {
   unsigned long long* best = s.w.ull.p + 1;
   unsigned long long inf = d_to_bits(INFINITY);
-  CK(cudaMemcpyAsync(best, &inf, sizeof(inf), cudaMemcpyHostToDevice, s.stream));
+  dev_set_u64(s.stream, best, inf);
   launch_cand_min_d2(s, KIND_VF, q, best);
   launch_cand_min_d2(s, KIND_EE, q, best);
   comm_allreduce(s, best, 1, 0, 1);  // d2 >= 0 (inf when empty): bit order == value order
   unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
   CK(cudaMemcpyAsync(hb, best, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   return bits_to_d(hb[0]);
 }
 
@@ -501,9 +501,12 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   int64_t nfp = 0;
   const int2* fp = fric_pattern(s, nfp);
   build_pattern(s, s.cands.ov.p, s.cands.n_ov, fp, nfp, /*from_cands=*/true);
+  HMARK();
   contact_blocks(s, q, kappa, dh, 1, /*mark=*/true);
+  HMARK();
   append_friction_blocks(s, q, dt, eps_v, 1);
   reduce_system(s, s.w.diag0.p, s.w.grad0.p);
+  HMARK();
   if (s.comm.world > 1) {
     // the replicated system: sum of the ranks' partial assemblies
     comm_allreduce(s, s.H.val.p, 144 * s.H.nnzb, 0, 0);
@@ -570,6 +573,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         const bool chol = P.linear_solver != 1;
         if (chol) chol_begin(s, s.w.neg.p, s.dx.p);
         else pcg_it = pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
+        HMARK();
         // |dx|_inf and g.dx in one pass; the Cholesky residual check shares the host sync
         auto absmax_dot = [&]() {
           unsigned long long* am = s.w.ull.p + 2;
@@ -580,7 +584,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
           reduce_fixed_stream(stream, s.red.p, RED_BLOCKS, s.w.scal.p);
           CK(cudaMemcpyAsync(s.h_pinned, am, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
           CK(cudaMemcpyAsync(s.h_pinned + 1, s.w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
-          CK(cudaStreamSynchronize(stream));
+          SSYNC(stream);
         };
         absmax_dot();
         if (chol) {
@@ -611,6 +615,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       // candidates over the proposed interval [q, q + dq]
       t0 = clk::now();
       launch_axpy_q(s, s.q.p, 1.0, s.dq.p, s.q_trial.p, NB);  // q + dq (exact add)
+      HMARK();
       broad_phase(s, s.q.p, s.q_trial.p, P.d_hat);
       st.t_broad += ms(t0, clk::now());
       max_c = std::max<int64_t>(max_c, s.cands.n_vf + s.cands.n_ee);
@@ -659,7 +664,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
     }
     unsigned long long* hb = reinterpret_cast<unsigned long long*>(s.h_pinned);
     CK(cudaMemcpyAsync(hb, m, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
+    SSYNC(stream);
     st.max_ortho_error = bits_to_d(hb[0]);
   }
   st.t_total = ms(t_start, clk::now());

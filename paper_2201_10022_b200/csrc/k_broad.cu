@@ -1009,7 +1009,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
                                                       (int64_t)c.ov.cap, c.ov.p);
     note_launch("k_large_pairs");
     CK(cudaMemcpyAsync(hov, ovc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    SSYNC(st);
     if (hov[0] <= c.ov.cap) break;
     c.ov.resize(hov[0]);
   }
@@ -1042,7 +1042,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   int* ov_same = reinterpret_cast<int*>(w.ull.p + 9);
   if (w.pat_valid && s.H.n == s.n_dyn) {
     const int one = 1;
-    CK(cudaMemcpyAsync(ov_same, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+    dev_set_i32(st, ov_same, one);
     k_ov_in_pattern<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, c.ov.p, s.slot.p, s.H.n_off, s.H.upper_keys.p,
                                                          ov_same);
     note_launch("k_ov_in_pattern");
@@ -1090,7 +1090,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     CK(cudaMemcpyAsync(hc, counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hc + 2, unsorted, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(hc + 3, ov_same, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    SSYNC(st);
     c.ov_matches_pattern = *reinterpret_cast<int*>(hc + 3) != 0;
     chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;
     if (s.instrument) {

@@ -642,7 +642,7 @@ static int build_clusters(Scene& s, int max_ctas, int ksmall, int kbig, int& ncl
   cudaStream_t st = s.stream;
   std::vector<int2> keys(H.n_off);
   H.upper_keys.download(keys.data(), H.n_off, st);
-  CK(cudaStreamSynchronize(st));
+  SSYNC(st);
   std::vector<int> deg(n + 1, 0);
   for (auto& k : keys) {
     deg[k.x]++;
@@ -757,7 +757,7 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
   w.iters.resize(1);
   w.scal.resize(4);
   int big = 0x7fffffff;
-  CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  dev_set_i32(st, w.bad.p, big);
   launch_jacobi_inv(s, n, H.diag_pos.p, H.val.p, w.pinv.p, w.bad.p);
   // single-pass systems: register-resident solver
   const size_t res_smem = (size_t)(RES_ROWS * 144 + RES_ROWS * 12 + 256) * sizeof(double);
@@ -851,7 +851,7 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
   CK(cudaMemcpyAsync(hp, w.iters.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hp + 1, w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(s.h_pinned + 20, w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  SSYNC(st);
   int hit = hp[0];
   rel_res = s.h_pinned[20];
   if (hp[1] != big) throw Error(ABD_ERR_FACTORIZATION, "non-SPD diagonal block in block-Jacobi PCG", hp[1]);
@@ -871,7 +871,7 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
       // connected components of the block graph (diagnostic)
       std::vector<int2> keys(H.n_off);
       H.upper_keys.download(keys.data(), H.n_off, st);
-      CK(cudaStreamSynchronize(st));
+      SSYNC(st);
       std::vector<int> par(n);
       for (int i = 0; i < n; ++i) par[i] = i;
       auto find = [&](int v) {

@@ -525,14 +525,16 @@ static Analysis chol_analyze(Scene& s) {
   if (w.ch_pre) {
     // structure from the active pairs, already on its way to the host (assemble)
     w.ch_pre = false;
+    HMARK();
     CK(cudaEventSynchronize(w.ch_pre_ev));
+    HMARK();
   } else if (n_off) {
     w.ch_flags.resize(n_off);
     k_block_nz<<<grid_for(n_off * 32, 256), 256, 0, st>>>(n_off, H.upper_pos.p, H.val.p, w.ch_flags.p);
     note_launch("k_block_nz");
     CK(cudaMemcpyAsync(flags, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(keys, H.upper_keys.p, n_off * sizeof(int2), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    SSYNC(st);
   }
   an.ms_sync = ms_since(t0);
   t0 = clk::now();
@@ -566,6 +568,7 @@ static Analysis chol_analyze(Scene& s) {
   cur.clear();
   for (int64_t k = 0; k < n_off; ++k)
     if (flags[k]) cur.push_back(((uint64_t)(uint32_t)keys[2 * k] << 32) | (uint32_t)keys[2 * k + 1]);
+  HMARK();
   if (cc.valid && cc.n == n && std::includes(cc.edges.begin(), cc.edges.end(), cur.begin(), cur.end())) {
     an.n_cta = (int)cc.stats[0];
     an.n_coupled = (int)cc.stats[1];
@@ -929,9 +932,11 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   Scene::Work::CholRun& run = w.ch_run;
   run = Scene::Work::CholRun{};
   if (n == 0) return;
+  HMARK();
   auto th0 = std::chrono::steady_clock::now();
   w.bad.resize(1);
   Analysis an = chol_analyze(s);
+  HMARK();
   run.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
   run.active = true;
   run.rhs = rhs;
@@ -949,7 +954,7 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   run.ms3[2] = an.ms_plan;
   CholView v = an.view;
   const int big = 0x7fffffff;
-  CK(cudaMemcpyAsync(w.bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+  dev_set_i32(st, w.bad.p, big);
   Scene::KStat& ks = s.kstat[0];
   if (s.instrument) {
     kstat_flush(s, 0);
@@ -970,7 +975,7 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   if (clk_dbg) {
     std::vector<long long> hb(8 * 256);
     dbgbuf.download(hb.data(), hb.size(), st);
-    CK(cudaStreamSynchronize(st));
+    SSYNC(st);
     long long t0c = hb[2];
     fprintf(stderr, "[abd chol clock] node level start D_done chol_done fwd_done end n_off (cycles from first)\n");
     for (int q = 0; q < 256; ++q) {
@@ -1002,7 +1007,7 @@ int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool&
   int* hb = reinterpret_cast<int*>(s.h_pinned + 28);
   int solves = 1;
   for (int refine = 0;; ++refine) {
-    if (refine > 0) CK(cudaStreamSynchronize(st));
+    if (refine > 0) SSYNC(st);
     if (*hb != big) throw Error(ABD_ERR_FACTORIZATION, "non-SPD pivot in the block Cholesky", *hb);
     const double rn = std::sqrt(hp[0]), bn = std::sqrt(hp[1]);
     rel_res = bn > 0.0 ? rn / bn : 0.0;
@@ -1045,7 +1050,7 @@ int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool&
 
 int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine) {
   chol_begin(s, rhs, x);
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   bool changed = false;
   return chol_finish(s, rel_tol, rel_res, max_refine, changed);
 }

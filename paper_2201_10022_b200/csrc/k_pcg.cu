@@ -157,7 +157,7 @@ void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, cons
   k_fill_bsr<<<grid_for(tot, 256), 256, 0, st>>>(n, bdim, dd.p, n_off, dkeys.p, doff.p, s.H.row_ptr.p, s.H.col.p,
                                                 s.H.val.p);
   note_launch("k_fill_bsr");
-  CK(cudaStreamSynchronize(st));
+  SSYNC(st);
 }
 
 }  // namespace abd

@@ -249,7 +249,7 @@ void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64
     note_launch("k_drop_sentinel");
     int hn = 0;
     CK(cudaMemcpyAsync(&hn, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    SSYNC(st);
     n_off = hn;
   }
   H.n_off = n_off;

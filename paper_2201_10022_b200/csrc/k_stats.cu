@@ -113,13 +113,13 @@ double global_min_distance(Scene& s, const double* q) {
   DVec<unsigned long long> mg;
   mg.resize(1);
   unsigned long long inf = (unsigned long long)__builtin_bit_cast(long long, (double)INFINITY);
-  CK(cudaMemcpyAsync(mg.p, &inf, sizeof(inf), cudaMemcpyHostToDevice, st));
+  dev_set_u64(st, mg.p, inf);
   int grid = s.num_sms * 8;
   k_pair_gaps<<<grid, 256, 0, st>>>(s.B, s.dyn.p, s.bbox.p, 0.0, mg.p, nullptr, nullptr, 0);
   note_launch("k_pair_gaps");
   unsigned long long hg = 0;
   CK(cudaMemcpyAsync(&hg, mg.p, sizeof(hg), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  SSYNC(st);
   double gmin = __builtin_bit_cast(double, hg);
   if (!(gmin < INFINITY)) return INFINITY;
   // bound: exact distance over all pairs whose gap equals the minimum gap
@@ -137,20 +137,20 @@ double global_min_distance(Scene& s, const double* q) {
       note_launch("k_pair_gaps");
       int hc = 0;
       CK(cudaMemcpyAsync(&hc, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      SSYNC(st);
       if (hc <= cap) return hc;
       cap = hc;
     }
   };
   auto exact = [&](int n) -> double {
-    CK(cudaMemcpyAsync(best.p, &inf, sizeof(inf), cudaMemcpyHostToDevice, st));
+    dev_set_u64(st, best.p, inf);
     if (n) {
       k_pair_min_d2<<<std::min(n, s.num_sms * 8), 256, 0, st>>>(view(s), nullptr, q, list.p, n, best.p);
       note_launch("k_pair_min_d2");
     }
     unsigned long long h = 0;
     CK(cudaMemcpyAsync(&h, best.p, sizeof(h), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    SSYNC(st);
     return std::sqrt(__builtin_bit_cast(double, h));
   };
   int n0 = collect(std::nextafter(gmin, INFINITY));

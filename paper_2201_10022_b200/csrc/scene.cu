@@ -2,7 +2,11 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
 
 #include "kernels.h"
 #include "scene.h"
@@ -109,6 +113,80 @@ __global__ void k_reduce_fixed(const double* __restrict__ in, int n, double* __r
   if (threadIdx.x == 0) *out = sh[0];
 }
 
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+__global__ void k_set_i32(int* p, int v) { *p = v; }
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+void dev_set_u64(cudaStream_t st, unsigned long long* p, unsigned long long v) {
+  k_set_u64<<<1, 1, 0, st>>>(p, v);
+  note_launch("k_set");
+}
+void dev_set_i32(cudaStream_t st, int* p, int v) {
+  k_set_i32<<<1, 1, 0, st>>>(p, v);
+  note_launch("k_set");
+}
+void dev_set_i64(cudaStream_t st, int64_t* p, int64_t v) {
+  k_set_i64<<<1, 1, 0, st>>>(p, v);
+  note_launch("k_set");
+}
+
+static const bool g_prof_on = getenv("ABD_HOST_PROF") != nullptr;
+struct ProfSite {
+  int64_t n = 0;
+  double host_ms = 0.0, blocked_ms = 0.0;
+};
+static std::map<std::string, ProfSite> g_sites;
+static std::chrono::steady_clock::time_point g_last;
+static bool g_last_set = false;
+
+void host_sync(cudaStream_t st, const char* site) {
+  if (!g_prof_on) {
+    CK(cudaStreamSynchronize(st));
+    return;
+  }
+  using clk = std::chrono::steady_clock;
+  auto t0 = clk::now();
+  CK(cudaStreamSynchronize(st));
+  auto t1 = clk::now();
+  const char* base = strrchr(site, '/');
+  ProfSite& p = g_sites[base ? base + 1 : site];
+  p.n += 1;
+  if (g_last_set) p.host_ms += std::chrono::duration<double, std::milli>(t0 - g_last).count();
+  p.blocked_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+  g_last = t1;
+  g_last_set = true;
+}
+
+void host_mark(const char* site) {
+  if (!g_prof_on) return;
+  auto t = std::chrono::steady_clock::now();
+  const char* base = strrchr(site, '/');
+  ProfSite& p = g_sites[std::string("mark ") + (base ? base + 1 : site)];
+  p.n += 1;
+  if (g_last_set) p.host_ms += std::chrono::duration<double, std::milli>(t - g_last).count();
+  g_last = t;
+  g_last_set = true;
+}
+
+void host_prof_reset() {
+  g_sites.clear();
+  g_last_set = false;
+}
+
+void host_prof_dump() {
+  if (!g_prof_on) return;
+  double h = 0.0, b = 0.0;
+  int64_t n = 0;
+  for (auto& kv : g_sites) {
+    fprintf(stderr, "[host_prof] %-22s n=%7lld host=%9.2fms blocked=%9.2fms\n", kv.first.c_str(),
+            (long long)kv.second.n, kv.second.host_ms, kv.second.blocked_ms);
+    h += kv.second.host_ms;
+    b += kv.second.blocked_ms;
+    n += kv.second.n;
+  }
+  fprintf(stderr, "[host_prof] total syncs=%lld host=%.2fms blocked=%.2fms\n", (long long)n, h, b);
+}
+
 void kstat_flush(Scene& s, int which) {
   Scene::KStat& k = s.kstat[which];
   if (!k.pending) return;
@@ -145,7 +223,7 @@ double reduce_sum_det(Scene& s, const double* partials, int n) {
   s.tmp_d3.resize(1);
   reduce_fixed_device(s, partials, n, s.tmp_d3.p);
   CK(cudaMemcpyAsync(s.h_pinned, s.tmp_d3.p, sizeof(double), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
+  SSYNC(s.stream);
   return s.h_pinned[0];
 }
 

@@ -24,6 +24,23 @@ struct Error : std::runtime_error {
 void cuda_check(cudaError_t e, const char* what);
 #define CK(x) ::abd::cuda_check((x), #x)
 
+// stream sync through one choke point: with ABD_HOST_PROF set, the host time
+// since the previous sync (issue + host work) and the time blocked in the sync
+// are accumulated per call site and printed by host_prof_dump()
+void host_sync(cudaStream_t st, const char* site);
+// store one scalar on the device in stream order (a kernel argument: no pageable
+// host->device copy, which may serialise with the stream)
+void dev_set_u64(cudaStream_t st, unsigned long long* p, unsigned long long v);
+void dev_set_i32(cudaStream_t st, int* p, int v);
+void dev_set_i64(cudaStream_t st, int64_t* p, int64_t v);
+void host_prof_dump();
+void host_prof_reset();
+#define ABD_STR2(x) #x
+#define ABD_STR(x) ABD_STR2(x)
+#define SSYNC(st) ::abd::host_sync((st), __FILE__ ":" ABD_STR(__LINE__))
+void host_mark(const char* site);  // host time since the previous sync / mark (ABD_HOST_PROF)
+#define HMARK() ::abd::host_mark(__FILE__ ":" ABD_STR(__LINE__))
+
 // growable device vector (never shrinks; contents undefined after grow)
 template <class T>
 struct DVec {
