@@ -9,7 +9,7 @@ namespace abd {
 // reproducing numpy's arithmetic order bit-for-bit.  t_cut: early exit once
 // t >= t_cut (t only grows, so a global minimum is unchanged).
 ABD_D double accd_query(int kind, V3* x, const V3* dx, double slack, double tmax, int max_iters,
-                        volatile const unsigned long long* t_cut_bits, bool& domain_err) {
+                        volatile const unsigned long long* t_cut_bits, bool& domain_err, int* it_out = nullptr) {
   V3 mean;
   mean.x = xadd(xadd(xadd(dx[0].x, dx[1].x), dx[2].x), dx[3].x) / 4.0;
   mean.y = xadd(xadd(xadd(dx[0].y, dx[1].y), dx[2].y), dx[3].y) / 4.0;
@@ -33,7 +33,8 @@ ABD_D double accd_query(int kind, V3* x, const V3* dx, double slack, double tmax
   if (!(lp > 0.0)) return tmax;
   double t = 0.0;
   double stall_eps = xmul(1e-12, d0);
-  for (int it = 0; it < max_iters; ++it) {
+  int it = 0;
+  for (; it < max_iters; ++it) {
     // the first iterate is x itself: reuse d0 (bitwise the same value)
     double d = it == 0 ? d0 : sqrt(pair_d2(kind, x));
     double adv = xsub(d, gap);
@@ -52,6 +53,7 @@ ABD_D double accd_query(int kind, V3* x, const V3* dx, double slack, double tmax
       if (t >= __longlong_as_double((long long)cb)) break;
     }
   }
+  if (it_out) *it_out = it;
   return fmin(t, tmax);
 }
 

@@ -334,12 +334,19 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   w.lserr.zero(st);
   unsigned long long one = d_to_bits(1.0);
   dev_set_u64(st, tmin, one);
-  EventTimer tm(s, 2);
-  launch_ccd(s, KIND_VF, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
-  launch_ccd(s, KIND_EE, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
-  tm.stop();
+  // e0 = ip_value(q) on the side stream, overlapping the CCD (whose runtime is a
+  // heavy tail of a few long ACCD queries)
+  CK(cudaEventRecord(s.fork_ev, st));
+  CK(cudaStreamWaitEvent(s.side, s.fork_ev, 0));
+  std::swap(s.stream, s.side);
   launch_energy(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v, w.lsred.p, w.lsscal.p,
                 w.lserr.p + 1);
+  std::swap(s.stream, s.side);
+  CK(cudaEventRecord(s.join_ev, s.side));
+  EventTimer tm(s, 2);
+  launch_ccd_both(s, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
+  tm.stop();
+  CK(cudaStreamWaitEvent(st, s.join_ev, 0));
   k_alpha_trial<<<grid_for(NB, 256), 256, 0, st>>>(NB, s.q.p, s.dq.p, tmin, P.ccd_step_scale, s.q_trial.p);
   note_launch("k_alpha_trial");
   launch_energy(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v,
@@ -381,8 +388,7 @@ double step_filter(Scene& s, const double* q, const double* dq, double slack) {
   unsigned long long one = d_to_bits(1.0);
   dev_set_u64(s.stream, tmin, one);
   EventTimer tm(s, 2);
-  launch_ccd(s, KIND_VF, q, dq, slack, tmin, s.w.err.p);
-  launch_ccd(s, KIND_EE, q, dq, slack, tmin, s.w.err.p);
+  launch_ccd_both(s, q, dq, slack, tmin, s.w.err.p);
   tm.stop();
   comm_allreduce(s, tmin, 1, 0, 1);
   comm_allreduce(s, s.w.err.p, 1, 1, 2);

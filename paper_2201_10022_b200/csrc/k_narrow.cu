@@ -5,6 +5,11 @@
 #include "abd_misc.cuh"
 #include "kernels.h"
 
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 namespace abd {
 
 SceneView view(const Scene& s) {
@@ -373,6 +378,49 @@ __global__ void k_ccd(SceneView sv, int kind, int64_t n, const int4* __restrict_
   if ((threadIdx.x & 31) == 0 && t < INFINITY) atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
 }
 
+// K5 over both candidate lists in one launch (VF rows first, then EE): the
+// heavy-tailed ACCD queries of the two kinds share one tail instead of two
+__global__ void k_ccd_both(SceneView sv, int64_t n_vf, const int4* __restrict__ vf, int64_t n_ee,
+                           const int4* __restrict__ ee, const double* __restrict__ q, const double* __restrict__ dq,
+                           double slack, unsigned long long* tmin, int* err) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  double t = INFINITY;
+  if (i < n_vf + n_ee) {
+    const int kind = i < n_vf ? KIND_VF : KIND_EE;
+    PairIds ids = pair_ids(sv, kind, kind == KIND_VF ? vf[i] : ee[i - n_vf]);
+    V3 x[4], xb[4], dx[4];
+    pair_points(sv, ids, q, x, xb);
+    for (int k = 0; k < 4; ++k) {
+      int b = ids.body[k];
+      dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+    }
+    bool bad = false;
+    t = accd_query(kind, x, dx, slack, 1.0, 512, tmin, bad);
+    if (bad) atomicExch(err, 1);
+  }
+  for (int o = 16; o > 0; o >>= 1) t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
+  if ((threadIdx.x & 31) == 0 && t < INFINITY) atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
+}
+
+// diagnostic (ABD_CCD_STATS): per query iterations and t without the shared cut
+__global__ void k_ccd_dbg(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                          const double* __restrict__ q, const double* __restrict__ dq, double slack, int* its,
+                          double* ts) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  PairIds ids = pair_ids(sv, kind, rows[i]);
+  V3 x[4], xb[4], dx[4];
+  pair_points(sv, ids, q, x, xb);
+  for (int k = 0; k < 4; ++k) {
+    int b = ids.body[k];
+    dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+  }
+  bool bad = false;
+  int it = 0;
+  ts[i] = accd_query(kind, x, dx, slack, 1.0, 512, nullptr, bad, &it);
+  its[i] = it;
+}
+
 // K1: inertia + orthogonality per dynamic slot (solver.py:197-200, :283-296)
 __global__ void k_body_terms(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ mass,
                              const double* __restrict__ stiff, const double* __restrict__ q,
@@ -709,6 +757,46 @@ void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double sl
   const int4* rows = rows_of(s, kind, n);
   if (!n) return;
   k_ccd<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dq, slack, tmin, err);
+  note_launch("k_ccd");
+  static const bool stats = getenv("ABD_CCD_STATS") != nullptr;
+  if (stats) {
+    DVec<int> its;
+    DVec<double> ts;
+    its.resize(n);
+    ts.resize(n);
+    k_ccd_dbg<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dq, slack, its.p, ts.p);
+    std::vector<int> hi(n);
+    std::vector<double> ht(n);
+    its.download(hi.data(), n, s.stream);
+    ts.download(ht.data(), n, s.stream);
+    SSYNC(s.stream);
+    double tmn = 1.0;
+    for (int64_t i = 0; i < n; ++i) tmn = std::fmin(tmn, ht[i]);
+    int64_t h[6] = {0, 0, 0, 0, 0, 0}, below2 = 0, sum_it = 0;
+    int mx = 0, mx_it_t_lo = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      int it = hi[i];
+      sum_it += it;
+      mx = std::max(mx, it);
+      h[it <= 1 ? 0 : it <= 4 ? 1 : it <= 16 ? 2 : it <= 64 ? 3 : it <= 256 ? 4 : 5]++;
+      if (ht[i] < 2.0 * tmn) {
+        ++below2;
+        mx_it_t_lo = std::max(mx_it_t_lo, it);
+      }
+    }
+    fprintf(stderr, "[ccd] kind=%d n=%lld tmin=%.4e mean_it=%.2f max_it=%d hist(<=1,4,16,64,256,>)=%lld %lld %lld %lld %lld %lld "
+            "t<2tmin: %lld (max it %d)\n", kind, (long long)n, tmn, (double)sum_it / n, mx, (long long)h[0],
+            (long long)h[1], (long long)h[2], (long long)h[3], (long long)h[4], (long long)h[5], (long long)below2,
+            mx_it_t_lo);
+  }
+}
+
+void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, unsigned long long* tmin,
+                     int* err) {
+  const int64_t n = s.cands.n_vf + s.cands.n_ee;
+  if (!n) return;
+  k_ccd_both<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), s.cands.n_vf, s.cands.vf.p, s.cands.n_ee, s.cands.ee.p,
+                                                    q, dq, slack, tmin, err);
   note_launch("k_ccd");
 }
 

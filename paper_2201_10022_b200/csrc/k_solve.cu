@@ -137,14 +137,24 @@ __global__ void k_seg_bounds(int64_t m, const uint32_t* __restrict__ keys, int64
   if (i == m - 1 || keys[i + 1] != k) end[k] = (int)i + 1;
 }
 
-// one warp per CSR position that is a diagonal or an upper block
-__global__ void k_reduce_blocks(int n, const int* __restrict__ row_ptr, const int* __restrict__ col,
-                                const int* __restrict__ seg_start, const int* __restrict__ seg_end,
-                                const int* __restrict__ cvals, const double* __restrict__ pblk,
-                                const double* __restrict__ diag0, const double* __restrict__ grad0, double* val,
-                                double* grad, const int* __restrict__ row_of) {
+// one warp per CSR position that is a diagonal or an upper block; each
+// contribution's compact record (PB_STRIDE doubles) is staged in shared memory
+// by one coalesced warp load (the next record prefetched into registers while the
+// current one is evaluated), so the ~60 per-entry reads hit shared memory
+constexpr int RB_WARPS = 8;
+constexpr int RB_PER_LANE = (PB_STRIDE + 31) / 32;
+__global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const int* __restrict__ row_ptr,
+                                                                 const int* __restrict__ col,
+                                                                 const int* __restrict__ seg_start,
+                                                                 const int* __restrict__ seg_end,
+                                                                 const int* __restrict__ cvals,
+                                                                 const double* __restrict__ pblk,
+                                                                 const double* __restrict__ diag0,
+                                                                 const double* __restrict__ grad0, double* val,
+                                                                 double* grad, const int* __restrict__ row_of) {
+  __shared__ double srec[RB_WARPS][RB_PER_LANE * 32];
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int64_t nnzb = row_ptr[n];
   if (w >= nnzb) return;
   int r = row_of[w];
@@ -159,12 +169,31 @@ __global__ void k_reduce_blocks(int n, const int* __restrict__ row_ptr, const in
     acc[e] = (is_diag && idx < 144) ? diag0[144 * (int64_t)r + idx] : 0.0;
   }
   if (is_diag && lane < 12) gacc = grad0[12 * (int64_t)r + lane];
-  int s0 = seg_start[w], s1 = seg_end[w];
+  const int s0 = seg_start[w], s1 = seg_end[w];
+  double* sr = srec[wid];
+  double nxt[RB_PER_LANE];
+  int vnext = 0;
+  if (s0 < s1) {
+    vnext = cvals[s0];
+    const double* blk = pblk + (int64_t)(vnext >> 2) * PB_STRIDE;
+#pragma unroll
+    for (int j = 0; j < RB_PER_LANE; ++j)
+      if (lane + 32 * j < PB_STRIDE) nxt[j] = blk[lane + 32 * j];
+  }
   for (int t = s0; t < s1; ++t) {
-    int v = cvals[t];
-    int64_t p = v >> 2;
-    int which = v & 3;
-    const double* blk = pblk + p * PB_STRIDE;
+    const int which = vnext & 3;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < RB_PER_LANE; ++j)
+      if (lane + 32 * j < PB_STRIDE) sr[lane + 32 * j] = nxt[j];
+    __syncwarp();
+    if (t + 1 < s1) {
+      vnext = cvals[t + 1];
+      const double* blk = pblk + (int64_t)(vnext >> 2) * PB_STRIDE;
+#pragma unroll
+      for (int j = 0; j < RB_PER_LANE; ++j)
+        if (lane + 32 * j < PB_STRIDE) nxt[j] = blk[lane + 32 * j];
+    }
     // target entry (i, k) = H24(12 s_r + i, 12 s_c + k) for the aa / bb / ab blocks;
     // which 3 is the transposed ab block: H24(k, 12 + i)
 #pragma unroll
@@ -174,10 +203,10 @@ __global__ void k_reduce_blocks(int n, const int* __restrict__ row_ptr, const in
         const int i = idx / 12, k = idx % 12;
         const int R = which == 3 ? k : 12 * (which == 1) + i;
         const int Cc = which == 3 ? 12 + i : 12 * (which >= 1) + k;
-        acc[e] += pb_entry(blk, R, Cc);
+        acc[e] += pb_entry(sr, R, Cc);
       }
     }
-    if (which < 2 && lane < 12) gacc += blk[12 * which + lane];
+    if (which < 2 && lane < 12) gacc += sr[12 * which + lane];
   }
   double* out = val + 144 * w;
 #pragma unroll
@@ -337,7 +366,7 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
     cv = dv.Current();
   }
   s.grad.resize(12 * (int64_t)n);
-  k_reduce_blocks<<<grid_for(H.nnzb * 32, 256), 256, 0, st>>>(n, H.row_ptr.p, H.col.p, seg_s.p, seg_e.p, cv,
+  k_reduce_blocks<<<grid_for(H.nnzb * 32, 32 * RB_WARPS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, seg_s.p, seg_e.p, cv,
                                                               s.pblk.blk.p, diag0, grad0, H.val.p, s.grad.p,
                                                               row_of.p);
   note_launch("k_reduce_blocks");

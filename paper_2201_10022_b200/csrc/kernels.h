@@ -63,6 +63,8 @@ void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, do
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best_bits);
 void launch_friction_pre(Scene& s, int kind, const double* q, double kappa, double dh, const int* flags,
                          const int* pos, int64_t base, double* basis_out);
+void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, unsigned long long* tmin,
+                     int* err);
 void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack,
                 unsigned long long* tmin_bits, int* err);
 // per-body inertia + orthogonality terms (K1): grad0/diag0 per dynamic slot, energy partials

@@ -38,6 +38,9 @@ Scene::Scene() {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
   CK(cudaMallocHost(&h_pinned, 64 * sizeof(double)));
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
@@ -52,6 +55,9 @@ Scene::Scene() {
 
 Scene::~Scene() {
   if (stream) cudaStreamDestroy(stream);
+  if (side) cudaStreamDestroy(side);
+  if (fork_ev) cudaEventDestroy(fork_ev);
+  if (join_ev) cudaEventDestroy(join_ev);
   if (h_pinned) cudaFreeHost(h_pinned);
   for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
     if (e) cudaEventDestroy(e);

@@ -154,6 +154,8 @@ struct Scene {
   int64_t V = 0, E = 0, T = 0;
   int max_v = 0, max_e = 0, max_t = 0;  // per-body primitive maxima (sort key widths)
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;            // forked work that overlaps the main stream (event-joined)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   int num_sms = 148;
 
   // geometry (immutable after create)
