@@ -299,8 +299,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--workload", default="pile", choices=["pile", "micro"],
-                    help="pile = BASELINE config 4 (headline); micro = config 2 kernel microbenchmark")
+    ap.add_argument("--workload", default="pile", choices=["pile", "micro", "chainmail", "cubes", "boxstack"],
+                    help="pile = BASELINE config 4 (headline); micro = config 2 kernel microbenchmark; "
+                         "chainmail = config 5; cubes = config 3 (1000-cube drop); boxstack = config 1")
     ap.add_argument("--micro-bodies", type=int, default=100_000)
     ap.add_argument("--micro-pairs", type=int, default=10_000_000, help="VF pairs = EE pairs")
     args = ap.parse_args()
@@ -328,7 +329,14 @@ def main():
     from paper_2201_10022_b200 import _native, scenes
     from paper_2201_10022_b200.solver import step_params_c
 
-    spec = scenes.icosphere_pile(seed=0, nx=args.nx, ny=args.nx, nz=args.nz)
+    if args.workload == "pile":
+        spec = scenes.icosphere_pile(seed=0, nx=args.nx, ny=args.nx, nz=args.nz)
+    elif args.workload == "chainmail":
+        spec = scenes.chainmail(seed=0)
+    elif args.workload == "cubes":
+        spec = scenes.cube_drop(seed=0)
+    else:
+        spec = scenes.box_stack(seed=0)
     model, state, params = spec.build()
     B = len(model.bodies)
     L = _native.lib()
@@ -339,7 +347,7 @@ def main():
         from paper_2201_10022_b200.dist import attach_nccl
         attach_nccl(model)
     step0, time0 = 0, 0.0
-    use_ckpt = args.ckpt.lower() != "none" and (args.nx, args.nz) == (20, 25)
+    use_ckpt = args.workload == "pile" and args.ckpt.lower() != "none" and (args.nx, args.nz) == (20, 25)
     if use_ckpt:
         ck = np.load(args.ckpt)
         assert int(ck["seed"]) == 0 and ck["q"].shape == state.q.shape
@@ -384,13 +392,32 @@ def main():
     barrier()
     iters = 0
     pcg_total = 0
+    # small scenes (configs 1 and 3) fit in L2: flush it (write 512 MB) before every
+    # timed step and time the steps one by one so the flush stays outside the sum
+    flush = args.workload in ("cubes", "boxstack")
+    fbuf = None
+    if flush:
+        import torch
+        fbuf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    ms = C.c_double(0.0)
     with ClockSampler(local) as clk:
-        _native.check(L.abd_timer_start(sc.ptr))
-        for _ in range(args.steps):
-            iters += step()
-            pcg_total += st.pcg_iters_total
-        ms = C.c_double(0.0)
-        _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
+        if flush:
+            tot = 0.0
+            for _ in range(args.steps):
+                fbuf.fill_(1.0)
+                torch.cuda.synchronize()
+                _native.check(L.abd_timer_start(sc.ptr))
+                iters += step()
+                pcg_total += st.pcg_iters_total
+                _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
+                tot += ms.value
+            ms.value = tot
+        else:
+            _native.check(L.abd_timer_start(sc.ptr))
+            for _ in range(args.steps):
+                iters += step()
+                pcg_total += st.pcg_iters_total
+            _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
     barrier()
     launches = _native.kernel_launches() - n_launch0
     elapsed_ms = max_over_ranks(ms.value)
@@ -451,7 +478,7 @@ def main():
                "path": "paper_2201_10022_b200.advance_step (Python API, host numpy q/q_dot/forces)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload == "pile":
         r = oracle_sample_rate({}, args.warmup, args.cpu_budget, "1 thread", threads=1)
         cpu = {"value": r["value"], "unit": "steps/s", "cores": 1, "kind": "port",
                "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} icospheres + "
@@ -460,19 +487,28 @@ def main():
                          "scaling to the 10k pile (optimistic for the CPU)"}
 
     if rank == 0:
+        metric = {"pile": "sim steps/s (10k-body icosphere pile, fp64 ABD)",
+                  "chainmail": "sim steps/s (10k-link chainmail, fp64 ABD)",
+                  "cubes": "sim steps/s (1000-cube drop, fp64 ABD)",
+                  "boxstack": "sim steps/s (4-cube box stack, fp64 ABD)"}[args.workload]
+        wl = (f"icosphere_pile {args.nx}x{args.nx}x{args.nz} ({B} bodies, seed 0)" if args.workload == "pile"
+              else f"{spec.name} ({B} bodies, seed 0; BASELINE config "
+                   f"{ {'chainmail': 5, 'cubes': 3, 'boxstack': 1}[args.workload]})")
         line = {
-            "metric": "sim steps/s (10k-body icosphere pile, fp64 ABD)", "value": value, "unit": "steps/s",
+            "metric": metric, "value": value, "unit": "steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
-            "config": {"workload": f"icosphere_pile {args.nx}x{args.nx}x{args.nz} ({B} bodies, seed 0), "
+            "config": {"workload": f"{wl}, "
                                    f"steps [{step0 + args.start + args.warmup}, {step0 + args.start + args.warmup + args.steps})"
                                    + (f" from checkpoint {os.path.relpath(args.ckpt, ROOT)} (step {step0} of the "
                                       "200-step run; late, contact-dense phase)" if use_ckpt else ""),
                        "newton_iters": int(iters_all), "newton_it_per_s": iters_all / (elapsed_ms * 1e-3),
                        "pcg_iters": pcg_total,
-                       "l2": "per-step working set exceeds L2 (rest+topology+vertex boxes > 126 MB); no flush",
+                       "l2": ("L2 flushed (512 MB write) before every timed step; steps timed one by one"
+                              if flush else "per-step working set exceeds L2 (rest+topology+vertex boxes "
+                              "> 126 MB); no flush"),
                        "parallelism": (f"pair-partitioned over {world} GPUs (NCCL all-reduce of the system, "
                                        "replicated solve)") if world > 1 else "single"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

@@ -133,9 +133,7 @@ static int active_scan(Scene& s, const double* q, double dh) {
   launch_scatter_active(s, n, w.flags.p, w.pos.p, w.act.p);
   comm_allreduce(s, w.err.p, 1, 1, 2);  // a domain error on any rank stops every rank
   int* hp = reinterpret_cast<int*>(s.h_pinned);
-  CK(cudaMemcpyAsync(hp, w.pos.p + n, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaMemcpyAsync(hp + 1, w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
-  CK(cudaMemcpyAsync(hp + 2, w.pos.p + n_vf, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  pack_to_host(s.stream, hp, {{w.pos.p + n, 4, 0}, {w.err.p, 4, 4}, {w.pos.p + n_vf, 4, 8}});
   SSYNC(s.stream);
   if (hp[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
                                                  "(intersection reached; CCD filtering must prevent this)");
@@ -249,9 +247,8 @@ static void energy_terms(Scene& s, const double* q, const double* qt, double dt,
   reduce_fixed_multi(s.stream, s.red.p, RED_BLOCKS, 4, s.w.scal.p);
   comm_allreduce(s, s.w.scal.p, 4, 0, 0);
   comm_allreduce(s, s.w.err.p, 1, 1, 2);
-  CK(cudaMemcpyAsync(s.h_pinned, s.w.scal.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
   int* he = reinterpret_cast<int*>(s.h_pinned + 8);
-  CK(cudaMemcpyAsync(he, s.w.err.p, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  pack_to_host(s.stream, s.h_pinned, {{s.w.scal.p, 32, 0}, {s.w.err.p, 4, 64}});
   SSYNC(s.stream);
   if (he[0]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
                                                  "(intersection reached; CCD filtering must prevent this)");
@@ -357,9 +354,7 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   comm_allreduce(s, w.lsscal.p, 8, 0, 0);
   comm_allreduce(s, w.lserr.p, 2, 1, 2);
   double* hp = s.h_pinned + 32;
-  CK(cudaMemcpyAsync(hp, tmin, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hp + 1, w.lsscal.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hp + 9, w.lserr.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  pack_to_host(st, hp, {{tmin, 8, 0}, {w.lsscal.p, 64, 8}, {w.lserr.p, 8, 72}});
   SSYNC(st);
   const int* he = reinterpret_cast<const int*>(hp + 9);
   if (he[0]) throw Error(ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
@@ -588,8 +583,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
           note_launch("k_absmax_dot");
           s.w.scal.resize(8);
           reduce_fixed_stream(stream, s.red.p, RED_BLOCKS, s.w.scal.p);
-          CK(cudaMemcpyAsync(s.h_pinned, am, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
-          CK(cudaMemcpyAsync(s.h_pinned + 1, s.w.scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+          pack_to_host(stream, s.h_pinned, {{am, 8, 0}, {s.w.scal.p, 8, 8}});
           SSYNC(stream);
         };
         absmax_dot();

@@ -1087,9 +1087,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     }
     note_launch("k_prim_pairs");
     if (s.instrument) CK(cudaEventRecord(s.ev1, st));
-    CK(cudaMemcpyAsync(hc, counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hc + 2, unsorted, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(hc + 3, ov_same, sizeof(int), cudaMemcpyDeviceToHost, st));
+    pack_to_host(st, hc, {{counters, 16, 0}, {unsorted, 4, 16}, {ov_same, 4, 24}});
     SSYNC(st);
     c.ov_matches_pattern = *reinterpret_cast<int*>(hc + 3) != 0;
     chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;

@@ -623,76 +623,96 @@ static Analysis chol_analyze(Scene& s) {
       adj_idx[fp[b2]++] = a2;
     }
   }
-  // Elimination order: peel degree <= 1 nodes first (no fill: contact graphs are
-  // mostly forests of chains), then minimum degree on the remaining 2-core.
-  // Column structures (later neighbours at elimination) as CSR csp/csi.
+  // Elimination order by tree contraction (contact graphs of piles are forests of
+  // stacked chains): rounds of rake (every node of degree <= 1 at the start of the
+  // round; no fill) and compress (an independent set of degree-2 nodes; the fill
+  // edge joins the two neighbours), so a chain of L bodies is eliminated in
+  // O(log L) elimination-tree levels instead of L / 2.  What remains (degree >= 3
+  // everywhere) is ordered by minimum degree.  cs[v] = the live neighbours of v when
+  // it is eliminated (its L column structure).
   std::vector<int> order;
   order.reserve(m);
-  std::vector<int> deg(m), one(m, -1);
-  std::vector<char> gone(m, 0), queued(m, 0);
-  std::vector<int> queue;
-  queue.reserve(m);
-  for (int v = 0; v < m; ++v) {
-    deg[v] = adj_ptr[v + 1] - adj_ptr[v];
-    if (deg[v] <= 1) {
-      queue.push_back(v);
-      queued[v] = 1;
+  std::vector<std::vector<int>> nb(m), cs(m);
+  for (int v = 0; v < m; ++v) nb[v].assign(adj_idx.begin() + adj_ptr[v], adj_idx.begin() + adj_ptr[v + 1]);
+  std::vector<char> gone(m, 0), blocked(m, 0);
+  static const bool no_compress = getenv("ABD_CHOL_NO_COMPRESS") != nullptr;
+  auto drop = [](std::vector<int>& l, int x) {
+    auto it = std::find(l.begin(), l.end(), x);
+    if (it != l.end()) l.erase(it);
+  };
+  std::vector<int> sel;
+  for (;;) {
+    bool progress = false;
+    sel.clear();
+    for (int v = 0; v < m; ++v)
+      if (!gone[v] && nb[v].size() <= 1) sel.push_back(v);
+    for (int v : sel) {  // rake (a lone pair: the second end follows with no neighbour)
+      if (gone[v]) continue;
+      cs[v] = nb[v];
+      for (int u : nb[v]) drop(nb[u], v);
+      nb[v].clear();
+      gone[v] = 1;
+      order.push_back(v);
+      progress = true;
     }
-  }
-  for (size_t qi = 0; qi < queue.size(); ++qi) {
-    int v = queue[qi];
-    gone[v] = 1;
-    order.push_back(v);
-    for (int e = adj_ptr[v]; e < adj_ptr[v + 1]; ++e) {
-      int u = adj_idx[e];
-      if (gone[u]) continue;
-      one[v] = u;  // the single live neighbour
-      if (--deg[u] <= 1 && !queued[u]) {
-        queued[u] = 1;
-        queue.push_back(u);
+    if (!no_compress) {
+      sel.clear();
+      for (int v = 0; v < m; ++v) blocked[v] = 0;
+      for (int v = 0; v < m; ++v)
+        if (!gone[v] && !blocked[v] && nb[v].size() == 2) {
+          sel.push_back(v);
+          blocked[v] = 1;
+          blocked[nb[v][0]] = 1;
+          blocked[nb[v][1]] = 1;
+        }
+      for (int v : sel) {  // compress: v's neighbours a, b become adjacent (fill)
+        const int a2 = nb[v][0], b2 = nb[v][1];
+        cs[v] = nb[v];
+        drop(nb[a2], v);
+        drop(nb[b2], v);
+        if (std::find(nb[a2].begin(), nb[a2].end(), b2) == nb[a2].end()) {
+          nb[a2].push_back(b2);
+          nb[b2].push_back(a2);
+        }
+        nb[v].clear();
+        gone[v] = 1;
+        order.push_back(v);
+        progress = true;
       }
-      break;
     }
+    if (!progress) break;
   }
-  std::vector<int> csp(m + 1, 0), csi;
-  std::vector<std::vector<int>> core_cs;
-  std::vector<int> core_glob;  // local id of each 2-core node
   if ((int)order.size() < m) {
-    std::vector<int> core_id(m, -1);
+    std::vector<int> core_id(m, -1), core_glob;
     for (int v = 0; v < m; ++v)
       if (!gone[v]) {
         core_id[v] = (int)core_glob.size();
         core_glob.push_back(v);
       }
     const int mc = (int)core_glob.size();
-    std::vector<std::vector<int>> cadj(mc);
+    std::vector<std::vector<int>> cadj(mc), core_cs;
     for (int c = 0; c < mc; ++c) {
-      int v = core_glob[c];
-      for (int e = adj_ptr[v]; e < adj_ptr[v + 1]; ++e)
-        if (core_id[adj_idx[e]] >= 0) cadj[c].push_back(core_id[adj_idx[e]]);
+      for (int u : nb[core_glob[c]]) cadj[c].push_back(core_id[u]);
+      std::sort(cadj[c].begin(), cadj[c].end());
     }
     std::vector<int> corder;
     min_degree(mc, cadj, corder, core_cs);
     for (int c : corder) order.push_back(core_glob[c]);
+    for (int c = 0; c < mc; ++c) {
+      std::vector<int>& l = cs[core_glob[c]];
+      l.clear();
+      for (int x : core_cs[c]) l.push_back(core_glob[x]);
+    }
   }
   std::vector<int> pos(m);
   for (int i = 0; i < m; ++i) pos[order[i]] = i;
-  {
-    std::vector<int> core_of(m, -1);
-    for (size_t c = 0; c < core_glob.size(); ++c) core_of[core_glob[c]] = (int)c;
-    for (int v = 0; v < m; ++v)
-      csp[v + 1] = csp[v] + (core_of[v] >= 0 ? (int)core_cs[core_of[v]].size() : (one[v] >= 0 ? 1 : 0));
-    csi.resize(csp[m]);
-    for (int v = 0; v < m; ++v) {
-      if (core_of[v] >= 0) {
-        std::vector<int>& c = core_cs[core_of[v]];
-        for (int& x : c) x = core_glob[x];
-        std::sort(c.begin(), c.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
-        std::copy(c.begin(), c.end(), csi.begin() + csp[v]);
-      } else if (one[v] >= 0) {
-        csi[csp[v]] = one[v];
-      }
-    }
+  std::vector<int> csp(m + 1, 0), csi;
+  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (int)cs[v].size();
+  csi.resize(csp[m]);
+  for (int v = 0; v < m; ++v) {
+    std::vector<int>& c = cs[v];
+    std::sort(c.begin(), c.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
+    std::copy(c.begin(), c.end(), csi.begin() + csp[v]);
   }
   an.ms_order = ms_since(t0);
   t0 = clk::now();
@@ -919,8 +939,7 @@ static void launch_resid(Scene& s, const double* rhs, const double* x) {
   k_resid<<<RED_BLOCKS, RED_THREADS, 0, st>>>(s.H.n, s.H.row_ptr.p, s.H.col.p, s.H.val.p, x, rhs, w.r.p, w.part.p);
   note_launch("k_resid");
   reduce_fixed_multi(st, w.part.p, RED_BLOCKS, 2, w.scal.p + 4);
-  CK(cudaMemcpyAsync(s.h_pinned + 24, w.scal.p + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(reinterpret_cast<int*>(s.h_pinned + 28), w.bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  pack_to_host(st, s.h_pinned + 24, {{w.scal.p + 4, 16, 0}, {w.bad.p, 4, 32}});
 }
 
 void chol_begin(Scene& s, const double* rhs, double* x) {

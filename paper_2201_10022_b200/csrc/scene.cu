@@ -136,6 +136,32 @@ void dev_set_i64(cudaStream_t st, int64_t* p, int64_t v) {
   note_launch("k_set");
 }
 
+struct PackArgs {
+  const int* src[8];
+  int words[8];
+  int off[8];
+  int n;
+  int* dst;
+};
+__global__ void k_pack(PackArgs a) {
+  for (int i = 0; i < a.n; ++i)
+    for (int w = threadIdx.x; w < a.words[i]; w += blockDim.x) a.dst[a.off[i] + w] = a.src[i][w];
+}
+
+void pack_to_host(cudaStream_t st, void* host_dst, std::initializer_list<PackItem> items) {
+  PackArgs a{};
+  a.dst = reinterpret_cast<int*>(host_dst);
+  for (const PackItem& it : items) {
+    if (a.n == 8) throw Error(ABD_ERR_ARG, "pack_to_host: more than 8 items");
+    a.src[a.n] = reinterpret_cast<const int*>(it.src);
+    a.words[a.n] = it.bytes / 4;
+    a.off[a.n] = it.dst_off / 4;
+    ++a.n;
+  }
+  k_pack<<<1, 32, 0, st>>>(a);
+  note_launch("k_pack");
+}
+
 static const bool g_prof_on = getenv("ABD_HOST_PROF") != nullptr;
 struct ProfSite {
   int64_t n = 0;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <initializer_list>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +34,16 @@ void host_sync(cudaStream_t st, const char* site);
 void dev_set_u64(cudaStream_t st, unsigned long long* p, unsigned long long v);
 void dev_set_i32(cudaStream_t st, int* p, int v);
 void dev_set_i64(cudaStream_t st, int64_t* p, int64_t v);
+// gather small device scalars into pinned host memory with ONE kernel (the
+// kernel stores straight into the UVA-mapped pinned buffer): replaces a
+// series of tiny cudaMemcpyAsync D2H copies before a host sync.
+// bytes and dst_off are multiples of 4.
+struct PackItem {
+  const void* src;
+  int bytes;
+  int dst_off;
+};
+void pack_to_host(cudaStream_t st, void* host_dst, std::initializer_list<PackItem> items);
 void host_prof_dump();
 void host_prof_reset();
 #define ABD_STR2(x) #x

@@ -1,7 +1,7 @@
 """GPU timeline of pile Newton steps through CUPTI (torch.profiler): kernel/memcpy
 spans on the device, idle gaps between them and what precedes each gap.
 
-    python tools/gpu_timeline.py [STEPS] > gpurun_out/timeline.txt
+    python tools/gpu_timeline.py [STEPS] [pile|boxstack|cubes|chainmail] > gpurun_out/timeline.txt
 """
 import collections
 import ctypes as C
@@ -18,12 +18,18 @@ from paper_2201_10022_b200 import _native, scenes  # noqa: E402
 from paper_2201_10022_b200.solver import step_params_c  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+WL = sys.argv[2] if len(sys.argv) > 2 else "pile"
 torch.cuda.init()
 torch.zeros(1, device="cuda")
-spec = scenes.icosphere_pile(seed=0)
+spec = {"pile": scenes.icosphere_pile, "boxstack": scenes.box_stack, "cubes": scenes.cube_drop,
+        "chainmail": scenes.chainmail}[WL](seed=0)
 model, state, params = spec.build()
-ck = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_data", "pile_step150.npz"))
-q, qd = ck["q"].copy(), ck["q_dot"].copy()
+if WL == "pile":
+    ck = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_data",
+                              "pile_step150.npz"))
+    q, qd = ck["q"].copy(), ck["q_dot"].copy()
+else:
+    q, qd = state.q.copy(), state.q_dot.copy()
 L = _native.lib()
 sc = model.gpu_scene()
 forces = np.ascontiguousarray(model.forces(0, 0.0, q))
