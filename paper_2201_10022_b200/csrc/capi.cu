@@ -383,6 +383,90 @@ int abd_bsr_cholesky(int n, int bdim, const double* diag, int64_t n_off, const i
 }
 
 // ---------------------------------------------------------------------------
+// static primitive groups of the broad-phase cull (see Scene::grp_*): per body and
+// kind, primitives sorted by the Morton code of their rest centroid, 32 per group,
+// with the rest AABB of each group's vertices
+static void build_prim_groups(Scene& s, int B, const std::vector<int>& vo, const std::vector<int>& eo,
+                              const std::vector<int>& to, const double* rest, const std::vector<int>& ge,
+                              const std::vector<int>& gt) {
+  s.has_groups = s.max_v <= 256;
+  if (!s.has_groups) return;
+  const std::vector<int>* offs[3] = {&vo, &eo, &to};
+  for (int kind = 0; kind < 3; ++kind) {
+    const std::vector<int>& off = *offs[kind];
+    const int n_all = off[B];
+    std::vector<int> gid(n_all);
+    std::vector<unsigned> gpk(n_all);
+    std::vector<int> goff(B + 1, 0);
+    std::vector<double> gbox;
+    std::vector<std::pair<uint32_t, int>> key;
+    for (int b = 0; b < B; ++b) {
+      const int v0 = vo[b], np = off[b + 1] - off[b];
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (int v = vo[b]; v < vo[b + 1]; ++v)
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = std::min(lo[k], rest[3 * (int64_t)v + k]);
+          hi[k] = std::max(hi[k], rest[3 * (int64_t)v + k]);
+        }
+      auto verts = [&](int i, int* out) {
+        const int g = off[b] + i;
+        if (kind == 0) { out[0] = v0 + i; return 1; }
+        if (kind == 1) { out[0] = ge[2 * g]; out[1] = ge[2 * g + 1]; return 2; }
+        out[0] = gt[3 * g]; out[1] = gt[3 * g + 1]; out[2] = gt[3 * g + 2];
+        return 3;
+      };
+      key.clear();
+      for (int i = 0; i < np; ++i) {
+        int vs[3];
+        const int nv = verts(i, vs);
+        uint32_t code = 0;
+        int cell[3];
+        for (int k = 0; k < 3; ++k) {
+          double c = 0.0;
+          for (int m = 0; m < nv; ++m) c += rest[3 * (int64_t)vs[m] + k];
+          c /= nv;
+          const double ext = hi[k] - lo[k];
+          int q = ext > 0 ? (int)((c - lo[k]) / ext * 1023.0) : 0;
+          cell[k] = std::min(1023, std::max(0, q));
+        }
+        for (int bit = 9; bit >= 0; --bit)
+          for (int k = 0; k < 3; ++k) code = (code << 1) | ((cell[k] >> bit) & 1);
+        key.push_back({code, i});
+      }
+      std::sort(key.begin(), key.end());
+      for (int i = 0; i < np; ++i) {
+        const int loc = key[i].second;
+        int vs[3];
+        const int nv = verts(loc, vs);
+        unsigned pk = 0;
+        for (int m = 0; m < nv; ++m) pk |= (unsigned)(vs[m] - v0) << (8 * m);
+        gid[off[b] + i] = loc;
+        gpk[off[b] + i] = pk;
+      }
+      const int ng = (np + 31) / 32;
+      goff[b + 1] = goff[b] + ng;
+      for (int g = 0; g < ng; ++g) {
+        double glo[3] = {1e300, 1e300, 1e300}, ghi[3] = {-1e300, -1e300, -1e300};
+        for (int i = 32 * g; i < std::min(np, 32 * g + 32); ++i) {
+          int vs[3];
+          const int nv = verts(key[i].second, vs);
+          for (int m = 0; m < nv; ++m)
+            for (int k = 0; k < 3; ++k) {
+              glo[k] = std::min(glo[k], rest[3 * (int64_t)vs[m] + k]);
+              ghi[k] = std::max(ghi[k], rest[3 * (int64_t)vs[m] + k]);
+            }
+        }
+        for (int k = 0; k < 3; ++k) gbox.push_back(0.5 * (glo[k] + ghi[k]));
+        for (int k = 0; k < 3; ++k) gbox.push_back(0.5 * (ghi[k] - glo[k]) * (1.0 + 1e-12) + 1e-300);
+      }
+    }
+    s.grp_id[kind].upload(gid.data(), n_all, s.stream);
+    s.grp_pk[kind].upload(gpk.data(), n_all, s.stream);
+    s.grp_off[kind].upload(goff.data(), B + 1, s.stream);
+    s.grp_box[kind].upload(gbox.data(), gbox.size(), s.stream);
+  }
+}
+
 abd_scene* abd_scene_create(int n_bodies, const int64_t* v_off, const int64_t* e_off, const int64_t* t_off,
                             const double* rest, const int64_t* edges, const int64_t* tris, const double* edge_len_sq,
                             const uint8_t* dynamic, const double* mass, const double* stiffness) {
@@ -428,6 +512,7 @@ abd_scene* abd_scene_create(int n_bodies, const int64_t* v_off, const int64_t* e
       }
     }
     cudaStream_t st = s.stream;
+    build_prim_groups(s, B, vo, eo, to, rest, ge, gt);
     s.v_off.upload(vo.data(), B + 1, st);
     s.e_off.upload(eo.data(), B + 1, st);
     s.t_off.upload(to.data(), B + 1, st);

@@ -389,10 +389,49 @@ __device__ __forceinline__ void box_from_cache(const PrimGeo& g, int kind, int g
   }
 }
 
+// static primitive groups (Scene::grp_*), per kind
+struct GrpGeo {
+  const int* id[3];
+  const unsigned* pk[3];
+  const double* box[3];
+  const int* off[3];
+};
+
+// conservative swept world box of a group's rest AABB (centre c, half extent e)
+// under q0 and q1, inflated by h and a rounding margin: it contains the swept box of
+// every primitive of the group, so culling against it only prunes
+__device__ __forceinline__ void group_box(const double* __restrict__ gb, const double* __restrict__ q0b,
+                                          const double* __restrict__ q1b, double h, double* o) {
+  double lo[3], hi[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = INFINITY;
+    hi[k] = -INFINITY;
+  }
+  for (int u = 0; u < 2; ++u) {
+    const double* q = u ? q1b : q0b;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double a0 = q[3 + 3 * i], a1 = q[4 + 3 * i], a2 = q[5 + 3 * i];
+      const double w = q[i] + a0 * gb[0] + a1 * gb[1] + a2 * gb[2];
+      const double E = fabs(a0) * gb[3] + fabs(a1) * gb[4] + fabs(a2) * gb[5];
+      const double m = 1e-12 * (1.0 + fabs(w) + E);
+      lo[i] = fmin(lo[i], w - E - m);
+      hi[i] = fmax(hi[i], w + E + m);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    o[k] = lo[k] - h;
+    o[3 + k] = hi[k] + h;
+  }
+}
+
 __global__ void __launch_bounds__(P2_THREADS, 3)
-    k_prim_pairs2(PrimGeo g, int64_t n_ov, const int2* __restrict__ ov, const double* __restrict__ bbox,
-                  unsigned long long* counters, int64_t cap_vf, int64_t cap_ee, int4* out_vf, int4* out_ee,
-                  int cap_list, int2* tab, int* unsorted, int rank, int world) {
+    k_prim_pairs2(PrimGeo g, GrpGeo gr, int use_groups, int64_t n_ov, const int2* __restrict__ ov,
+                  const double* __restrict__ bbox, unsigned long long* counters, int64_t cap_vf, int64_t cap_ee,
+                  int4* out_vf, int4* out_ee, int cap_list, int2* tab, int* unsorted, int rank, int world,
+                  unsigned long long* work) {
   extern __shared__ double p2_sm[];
   double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
   double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
@@ -404,8 +443,16 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   __shared__ int meta[16];  // v0,e0,t0 (i) | v0,e0,t0 (j) | nv,ne,nt (i) | nv,ne,nt (j)
   __shared__ int lcount[6];
   __shared__ double obox[6];
+  __shared__ int gfirst[6], gcount[6], ghits;
+  __shared__ int hitg[256];
+  // pairs are handed out dynamically (their costs vary by orders of magnitude);
   // multi-GPU: this rank takes overlap pairs rank, rank + world, ... (table rows of the others stay 0)
-  for (int64_t pi = rank + (int64_t)blockIdx.x * world; pi < n_ov; pi += (int64_t)gridDim.x * world) {
+  __shared__ long long next_k;
+  for (;;) {
+    if (threadIdx.x == 0) next_k = (long long)atomicAdd(work, 1ull);
+    __syncthreads();
+    const int64_t pi = rank + (int64_t)next_k * world;
+    if (pi >= n_ov) break;
     const int2 pr = ov[pi];
     const int bi = pr.x, bj = pr.y;
     if (threadIdx.x < 6) {
@@ -420,6 +467,13 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int k = threadIdx.x - 32;
       obox[k] = fmax(bbox[6 * bi + k], bbox[6 * bj + k]);
       obox[3 + k] = fmin(bbox[6 * bi + 3 + k], bbox[6 * bj + 3 + k]);
+    } else if (use_groups && threadIdx.x >= 64 && threadIdx.x < 70) {
+      const int l = threadIdx.x - 64, side = l / 3, kind = l % 3;
+      const int body = side ? bj : bi;
+      const int a = gr.off[kind][body];
+      gfirst[l] = a;
+      gcount[l] = gr.off[kind][body + 1] - a;
+      if (l == 0) ghits = 0;
     }
     __syncthreads();
     // vertex boxes of both bodies
@@ -432,7 +486,46 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       }
     }
     __syncthreads();
-    // one cull pass over the six lists (list id = 3 * side + kind); topology is
+    if (use_groups && gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5] <= 256) {
+      // cull in two stages: (a) the static groups of 32 primitives of the six lists
+      // against the overlap box (conservative swept boxes of their rest AABBs);
+      // (b) the primitives of the surviving groups, one warp per group
+      const int gt = gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5];
+      for (int t = threadIdx.x; t < gt; t += P2_THREADS) {
+        int l = 0, r = t;
+        while (r >= gcount[l]) {
+          r -= gcount[l];
+          ++l;
+        }
+        const int side = l / 3, kind = l % 3, body = side ? bj : bi;
+        double gb[6];
+        group_box(gr.box[kind] + 6 * (int64_t)(gfirst[l] + r), g.q0 + 12 * (int64_t)body,
+                  g.q1 + 12 * (int64_t)body, g.h, gb);
+        const bool hit = gb[0] <= obox[3] && obox[0] <= gb[3] && gb[1] <= obox[4] && obox[1] <= gb[4] &&
+                         gb[2] <= obox[5] && obox[2] <= gb[5];
+        if (hit) hitg[atomicAdd(&ghits, 1)] = (l << 16) | r;
+      }
+      __syncthreads();
+      const int lane = threadIdx.x & 31;
+      for (int u = threadIdx.x >> 5; u < ghits; u += P2_THREADS / 32) {
+        const int l = hitg[u] >> 16, r = hitg[u] & 0xffff;
+        const int side = l / 3, kind = l % 3;
+        const int i = 32 * r + lane;
+        if (i < meta[6 + l]) {
+          const int64_t gi = (int64_t)meta[l] + i;  // prim offset of the body (grouped order)
+          const unsigned pk = gr.pk[kind][gi];
+          double bx[6];
+          box_from_packed(kind, pk, vb + 6 * side * P2_VCAP, bx);
+          const bool keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] &&
+                            bx[2] <= obox[5] && obox[2] <= bx[5];
+          if (keep) {
+            const int at = atomicAdd(&lcount[l], 1);
+            lists[l * cap_list + at] = gr.id[kind][gi];
+            lpk[l * cap_list + at] = pk;
+          }
+        }
+      }
+    } else // one cull pass over the six lists (list id = 3 * side + kind); topology is
     // prefetched 4 primitives per thread, survivors keep id + packed local vertex ids
     {
       const int tot = meta[6] + meta[7] + meta[8] + meta[9] + meta[10] + meta[11];
@@ -1077,9 +1170,19 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
       w.tab.resize(3 * (size_t)n_ov);
       if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_ov * sizeof(int2), st));
       CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
-      k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
+      CK(cudaMemsetAsync(w.ull.p + 11, 0, sizeof(unsigned long long), st));
+      static const bool no_groups = getenv("ABD_BP_NO_GROUPS") != nullptr;
+      GrpGeo gg{};
+      for (int k = 0; k < 3; ++k) {
+        gg.id[k] = s.grp_id[k].p;
+        gg.pk[k] = s.grp_pk[k].p;
+        gg.box[k] = s.grp_box[k].p;
+        gg.off[k] = s.grp_off[k].p;
+      }
+      const int ug = s.has_groups && !no_groups ? 1 : 0;
+      k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
                                                        (int64_t)c.ee.cap, c.vf.p, c.ee.p, cap_list, w.tab.p,
-                                                       unsorted, s.comm.rank, s.comm.world);
+                                                       unsorted, s.comm.rank, s.comm.world, w.ull.p + 11);
     } else {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
       k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,

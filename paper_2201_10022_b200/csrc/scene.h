@@ -174,6 +174,15 @@ struct Scene {
   DVec<double> rest;              // V * 3
   DVec<int> edges;                // E * 2 (global vertex ids)
   DVec<int> tris;                 // T * 3 (global vertex ids)
+  // static primitive groups for the broad phase cull (bodies with <= 256 vertices):
+  // per kind (0 vertex, 1 edge, 2 triangle) the body's primitives in rest-space
+  // Morton order, in groups of 32: local ids, packed local vertex ids (8 bits each),
+  // per-group rest AABB (centre, half extent) and per-body group offsets
+  bool has_groups = false;
+  DVec<int> grp_id[3];
+  DVec<unsigned> grp_pk[3];
+  DVec<double> grp_box[3];
+  DVec<int> grp_off[3];  // B + 1
   DVec<double> elen2;             // E
   DVec<int> vert_body, edge_body, tri_body;
   DVec<unsigned char> dyn;        // B
