@@ -484,6 +484,7 @@ static void mark_structure(Scene& s) {
   if (!w.ch_pre_ev) CK(cudaEventCreateWithFlags(&w.ch_pre_ev, cudaEventDisableTiming));
   CK(cudaEventRecord(w.ch_pre_ev, s.stream));
   w.ch_pre = true;
+  chol_analysis_post(s);
 }
 
 void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v) {

@@ -13,6 +13,11 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
 // k_chol.cu: sparse block Cholesky + refinement; returns the number of triangular solves
 int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine = 3);
 void chol_begin(Scene& s, const double* rhs, double* x);
+// the host analysis of the coupling structure copied out by mark_structure runs on a
+// worker thread while the pair-block / reduction kernels are launched (post), or is
+// discarded when the pattern changes (drop)
+void chol_analysis_post(Scene& s);
+void chol_analysis_drop(Scene& s);
 int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed);
 void spmv(Scene& s, const double* x, double* y);
 void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off);

@@ -26,7 +26,11 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <condition_variable>
 #include <cstdlib>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <iterator>
 #include <numeric>
 #include <queue>
@@ -594,8 +598,15 @@ static Analysis chol_analyze(Scene& s) {
     cur.swap(un);
   }
 
-  // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order
-  std::vector<int> loc(n, -1), glob;
+  // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order;
+  // host scratch persists across analyses (no allocations in the steady state)
+  std::vector<int>&loc = w.hs_i[0], &glob = w.hs_i[1], &adj_ptr = w.hs_i[2], &adj_idx = w.hs_i[3],
+                  &deg = w.hs_i[4], &live = w.hs_i[5], &live2 = w.hs_i[6], &sel = w.hs_i[7], &cs0 = w.hs_i[8],
+                  &cs1 = w.hs_i[9], &order = w.hs_i[10], &pos = w.hs_i[11], &csp = w.hs_i[12], &csi = w.hs_i[13];
+  std::vector<char>&gone = w.hs_c[0], &blocked = w.hs_c[1];
+  const double ms_cur = ms_since(t0);
+  loc.assign(n, -1);
+  glob.clear();
   for (uint64_t e : cur) {
     loc[(int)(e >> 32)] = 0;
     loc[(int)(e & 0xffffffffu)] = 0;
@@ -608,111 +619,164 @@ static Analysis chol_analyze(Scene& s) {
     }
   const int m = (int)glob.size();
   an.n_coupled = m;
-  // adjacency (CSR) in key order is already sorted per node (keys sorted by (i, j))
-  std::vector<int> adj_ptr(m + 1, 0), adj_idx(2 * an.n_edges);
+  adj_ptr.assign(m + 1, 0);
+  adj_idx.resize(2 * an.n_edges);
   for (uint64_t e : cur) {
     adj_ptr[loc[(int)(e >> 32)] + 1]++;
     adj_ptr[loc[(int)(e & 0xffffffffu)] + 1]++;
   }
   for (int v = 0; v < m; ++v) adj_ptr[v + 1] += adj_ptr[v];
-  {
-    std::vector<int> fp(adj_ptr.begin(), adj_ptr.end() - 1);
-    for (uint64_t e : cur) {
-      int a2 = loc[(int)(e >> 32)], b2 = loc[(int)(e & 0xffffffffu)];
-      adj_idx[fp[a2]++] = b2;
-      adj_idx[fp[b2]++] = a2;
-    }
+  deg.assign(m, 0);
+  for (uint64_t e : cur) {
+    const int a2 = loc[(int)(e >> 32)], b2 = loc[(int)(e & 0xffffffffu)];
+    adj_idx[adj_ptr[a2] + deg[a2]++] = b2;
+    adj_idx[adj_ptr[b2] + deg[b2]++] = a2;
   }
+  const double ms_adj = ms_since(t0);
   // Elimination order by tree contraction (contact graphs of piles are forests of
   // stacked chains): rounds of rake (every node of degree <= 1 at the start of the
   // round; no fill) and compress (an independent set of degree-2 nodes; the fill
   // edge joins the two neighbours), so a chain of L bodies is eliminated in
   // O(log L) elimination-tree levels instead of L / 2.  What remains (degree >= 3
-  // everywhere) is ordered by minimum degree.  cs[v] = the live neighbours of v when
-  // it is eliminated (its L column structure).
-  std::vector<int> order;
-  order.reserve(m);
-  std::vector<std::vector<int>> nb(m), cs(m);
-  for (int v = 0; v < m; ++v) nb[v].assign(adj_idx.begin() + adj_ptr[v], adj_idx.begin() + adj_ptr[v + 1]);
-  std::vector<char> gone(m, 0), blocked(m, 0);
+  // everywhere) is ordered by minimum degree.  cs0/cs1 = the live neighbours of a
+  // raked / compressed node when it is eliminated (its L column structure).
+  // The live neighbour list of v is adj_idx[adj_ptr[v], adj_ptr[v] + deg[v]),
+  // edited in place: rake and compress never raise a degree.
+  order.clear();
+  cs0.assign(m, -1);
+  cs1.assign(m, -1);
+  gone.assign(m, 0);
+  blocked.assign(m, 0);
+  live.resize(m);
+  std::iota(live.begin(), live.end(), 0);
   static const bool no_compress = getenv("ABD_CHOL_NO_COMPRESS") != nullptr;
-  auto drop = [](std::vector<int>& l, int x) {
-    auto it = std::find(l.begin(), l.end(), x);
-    if (it != l.end()) l.erase(it);
+  auto drop = [&](int u, int x) {
+    int* l = adj_idx.data() + adj_ptr[u];
+    const int d = deg[u];
+    for (int i = 0; i < d; ++i)
+      if (l[i] == x) {
+        l[i] = l[d - 1];
+        deg[u] = d - 1;
+        return;
+      }
   };
-  std::vector<int> sel;
+  auto relink = [&](int u, int x, int y) {  // in u's list: x -> y, or drop x when y is already there
+    int* l = adj_idx.data() + adj_ptr[u];
+    const int d = deg[u];
+    int ix = -1;
+    bool has_y = false;
+    for (int i = 0; i < d; ++i) {
+      if (l[i] == x) ix = i;
+      if (l[i] == y) has_y = true;
+    }
+    if (has_y) {
+      l[ix] = l[d - 1];
+      deg[u] = d - 1;
+    } else {
+      l[ix] = y;
+    }
+  };
   for (;;) {
     bool progress = false;
     sel.clear();
-    for (int v = 0; v < m; ++v)
-      if (!gone[v] && nb[v].size() <= 1) sel.push_back(v);
+    for (int v : live)
+      if (deg[v] <= 1) sel.push_back(v);
     for (int v : sel) {  // rake (a lone pair: the second end follows with no neighbour)
       if (gone[v]) continue;
-      cs[v] = nb[v];
-      for (int u : nb[v]) drop(nb[u], v);
-      nb[v].clear();
+      if (deg[v] == 1) {
+        const int u = adj_idx[adj_ptr[v]];
+        cs0[v] = u;
+        drop(u, v);
+      }
+      deg[v] = 0;
       gone[v] = 1;
       order.push_back(v);
       progress = true;
     }
     if (!no_compress) {
       sel.clear();
-      for (int v = 0; v < m; ++v) blocked[v] = 0;
-      for (int v = 0; v < m; ++v)
-        if (!gone[v] && !blocked[v] && nb[v].size() == 2) {
+      for (int v : live) blocked[v] = 0;
+      for (int v : live)
+        if (!gone[v] && !blocked[v] && deg[v] == 2) {
+          const int* l = adj_idx.data() + adj_ptr[v];
           sel.push_back(v);
           blocked[v] = 1;
-          blocked[nb[v][0]] = 1;
-          blocked[nb[v][1]] = 1;
+          blocked[l[0]] = 1;
+          blocked[l[1]] = 1;
         }
       for (int v : sel) {  // compress: v's neighbours a, b become adjacent (fill)
-        const int a2 = nb[v][0], b2 = nb[v][1];
-        cs[v] = nb[v];
-        drop(nb[a2], v);
-        drop(nb[b2], v);
-        if (std::find(nb[a2].begin(), nb[a2].end(), b2) == nb[a2].end()) {
-          nb[a2].push_back(b2);
-          nb[b2].push_back(a2);
-        }
-        nb[v].clear();
+        const int* l = adj_idx.data() + adj_ptr[v];
+        const int a2 = l[0], b2 = l[1];
+        cs0[v] = a2;
+        cs1[v] = b2;
+        relink(a2, v, b2);
+        relink(b2, v, a2);
+        deg[v] = 0;
         gone[v] = 1;
         order.push_back(v);
         progress = true;
       }
     }
-    if (!progress) break;
+    live2.clear();
+    for (int v : live)
+      if (!gone[v]) live2.push_back(v);
+    live.swap(live2);
+    if (!progress || live.empty()) break;
   }
+  const double ms_contract = ms_since(t0);
+  const int n_core = m - (int)order.size();
+  std::vector<std::vector<int>> core_cs;
+  std::vector<int> core_glob;
   if ((int)order.size() < m) {
-    std::vector<int> core_id(m, -1), core_glob;
-    for (int v = 0; v < m; ++v)
-      if (!gone[v]) {
-        core_id[v] = (int)core_glob.size();
-        core_glob.push_back(v);
-      }
+    std::vector<int> core_id(m, -1);
+    core_glob = live;
     const int mc = (int)core_glob.size();
-    std::vector<std::vector<int>> cadj(mc), core_cs;
+    for (int c = 0; c < mc; ++c) core_id[core_glob[c]] = c;
+    std::vector<std::vector<int>> cadj(mc);
     for (int c = 0; c < mc; ++c) {
-      for (int u : nb[core_glob[c]]) cadj[c].push_back(core_id[u]);
+      const int v = core_glob[c];
+      for (int i = 0; i < deg[v]; ++i) cadj[c].push_back(core_id[adj_idx[adj_ptr[v] + i]]);
       std::sort(cadj[c].begin(), cadj[c].end());
     }
     std::vector<int> corder;
     min_degree(mc, cadj, corder, core_cs);
     for (int c : corder) order.push_back(core_glob[c]);
-    for (int c = 0; c < mc; ++c) {
-      std::vector<int>& l = cs[core_glob[c]];
-      l.clear();
-      for (int x : core_cs[c]) l.push_back(core_glob[x]);
-    }
+    for (auto& l : core_cs)
+      for (int& x : l) x = core_glob[x];
   }
-  std::vector<int> pos(m);
+  const double ms_core = ms_since(t0);
+  static const bool trace_ord = getenv("ABD_TRACE_CHOL") != nullptr;
+  if (trace_ord)
+    fprintf(stderr, "[abd chol order] m=%d core=%d cur_ms=%.3f adj_ms=%.3f contract_ms=%.3f core_ms=%.3f\n", m, n_core,
+            ms_cur, ms_adj, ms_contract, ms_core);
+  pos.resize(m);
   for (int i = 0; i < m; ++i) pos[order[i]] = i;
-  std::vector<int> csp(m + 1, 0), csi;
-  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (int)cs[v].size();
+  csp.assign(m + 1, 0);
+  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (cs0[v] >= 0) + (cs1[v] >= 0);
+  for (size_t c = 0; c < core_glob.size(); ++c) csp[core_glob[c] + 1] = (int)core_cs[c].size();
+  if (!core_glob.empty()) {  // recount: core nodes carry their min-degree column structures
+    std::vector<int> cnt(m, 0);
+    for (int v = 0; v < m; ++v) cnt[v] = (cs0[v] >= 0) + (cs1[v] >= 0);
+    for (size_t c = 0; c < core_glob.size(); ++c) cnt[core_glob[c]] = (int)core_cs[c].size();
+    csp[0] = 0;
+    for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + cnt[v];
+  }
   csi.resize(csp[m]);
   for (int v = 0; v < m; ++v) {
-    std::vector<int>& c = cs[v];
-    std::sort(c.begin(), c.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
-    std::copy(c.begin(), c.end(), csi.begin() + csp[v]);
+    int* o = csi.data() + csp[v];
+    const int k = csp[v + 1] - csp[v];
+    if (k == 1) {
+      o[0] = cs0[v];
+    } else if (k == 2 && cs1[v] >= 0) {
+      const bool sw = pos[cs1[v]] < pos[cs0[v]];
+      o[0] = sw ? cs1[v] : cs0[v];
+      o[1] = sw ? cs0[v] : cs1[v];
+    }
+  }
+  for (size_t c = 0; c < core_glob.size(); ++c) {
+    std::vector<int>& l = core_cs[c];
+    std::sort(l.begin(), l.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
+    std::copy(l.begin(), l.end(), csi.begin() + csp[core_glob[c]]);
   }
   an.ms_order = ms_since(t0);
   t0 = clk::now();
@@ -723,10 +787,16 @@ static Analysis chol_analyze(Scene& s) {
   an.n_blk = n + (int64_t)nbo;
   an.ms_sub[0] = ms_since(t0);
   // row lists (local i): (k, off block) for k eliminated before i, in elimination order of k
-  std::vector<int> rcnt(m + 1, 0);
+  std::vector<int>&rcnt = w.hs_i[14], &rfill = w.hs_i[15], &r_k = w.hs_i[16], &r_b = w.hs_i[17],
+                   &upd_ptr = w.hs_i[18], &upd = w.hs_i[19], &level = w.hs_i[20], &root = w.hs_i[21],
+                   &csize = w.hs_i[22], &cdepth = w.hs_i[23], &comps = w.hs_i[24], &cta_of = w.hs_i[25],
+                   &cta_nlvl = w.hs_i[26], &lcnt = w.hs_i[27], &fillp = w.hs_i[28];
+  rcnt.assign(m + 1, 0);
   for (int e = 0; e < nbo; ++e) rcnt[csi[e] + 1]++;
   for (int v = 0; v < m; ++v) rcnt[v + 1] += rcnt[v];
-  std::vector<int> rfill(rcnt.begin(), rcnt.end() - 1), r_k(nbo), r_b(nbo);
+  rfill.assign(rcnt.begin(), rcnt.end() - 1);
+  r_k.resize(nbo);
+  r_b.resize(nbo);
   for (int k : order)
     for (int e = csp[k]; e < csp[k + 1]; ++e) {
       int i = csi[e];
@@ -736,7 +806,8 @@ static Analysis chol_analyze(Scene& s) {
     }
   an.ms_sub[1] = ms_since(t0);
   // update pairs for off block (i, j): k in rows(j) with i in cs[k]
-  std::vector<int> upd_ptr(nbo + 1, 0), upd;
+  upd_ptr.assign(nbo + 1, 0);
+  upd.clear();
   for (int j = 0; j < m; ++j)
     for (int b = csp[j]; b < csp[j + 1]; ++b) {
       const int i = csi[b];
@@ -754,14 +825,17 @@ static Analysis chol_analyze(Scene& s) {
   an.n_upd = (int64_t)upd.size() / 2;
   an.ms_sub[2] = ms_since(t0);
   // elimination-tree levels and component roots (local)
-  std::vector<int> level(m, 0), root(m);
+  level.assign(m, 0);
+  root.resize(m);
   for (int v : order)
     if (csp[v + 1] > csp[v]) level[csi[csp[v]]] = std::max(level[csi[csp[v]]], level[v] + 1);
   for (int q = m - 1; q >= 0; --q) {
     int v = order[q];
     root[v] = csp[v + 1] == csp[v] ? v : root[csi[csp[v]]];
   }
-  std::vector<int> csize(m, 0), cdepth(m, 0), comps;
+  csize.assign(m, 0);
+  cdepth.assign(m, 0);
+  comps.clear();
   for (int v = 0; v < m; ++v) {
     csize[root[v]]++;
     cdepth[root[v]] = std::max(cdepth[root[v]], level[v] + 1);
@@ -789,7 +863,8 @@ static Analysis chol_analyze(Scene& s) {
   const int n_icta = (n_iso + iso_per_cta - 1) / iso_per_cta;
   const int n_cta = std::max(1, n_ccta + n_icta);
   an.n_cta = n_cta;
-  std::vector<int> cta_of(m, -1), cta_nlvl(n_cta, 0);
+  cta_of.assign(m, -1);
+  cta_nlvl.assign(n_cta, 0);
   {
     typedef std::pair<int64_t, int> LI;
     std::priority_queue<LI, std::vector<LI>, std::greater<LI>> load;
@@ -829,7 +904,8 @@ static Analysis chol_analyze(Scene& s) {
       cta_nl[c] = cta_nlvl[c];
       e += cta_nlvl[c] + 1;
     }
-    std::vector<int> cnt(n_lvl_entries + 1, 0);
+    std::vector<int>& cnt = lcnt;
+    cnt.assign(n_lvl_entries + 1, 0);
     for (int v = 0; v < m; ++v) cnt[cta_lvl[cta_of[root[v]]] + level[v]]++;
     int run = 0;
     for (int c = 0; c < n_ccta; ++c)
@@ -838,7 +914,7 @@ static Analysis chol_analyze(Scene& s) {
         lvl_ptr[ix] = run;
         if (l < cta_nlvl[c]) run += cnt[ix];
       }
-    std::vector<int> fillp(lvl_ptr, lvl_ptr + n_lvl_entries);
+    fillp.assign(lvl_ptr, lvl_ptr + n_lvl_entries);
     for (int v = 0; v < m; ++v) nodes[fillp[cta_lvl[cta_of[root[v]]] + level[v]]++] = glob[v];
     // isolated nodes, iso_per_cta per CTA in node order
     int iso = m;
@@ -942,6 +1018,98 @@ static void launch_resid(Scene& s, const double* rhs, const double* x) {
   pack_to_host(st, s.h_pinned + 24, {{w.scal.p + 4, 16, 0}, {w.bad.p, 4, 32}});
 }
 
+// ---------------------------------------------------------------------------
+// analysis worker: one host thread per scene, one job at a time
+namespace {
+struct CholWorker {
+  Scene* s = nullptr;
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  bool job = false, quit = false, has_result = false;
+  Analysis result;
+  std::exception_ptr err;
+  explicit CholWorker(Scene* sc) : s(sc) {
+    th = std::thread([this] { loop(); });
+  }
+  ~CholWorker() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      quit = true;
+    }
+    cv.notify_all();
+    th.join();
+  }
+  void loop() {
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu);
+      cv.wait(lk, [this] { return job || quit; });
+      if (quit) return;
+      lk.unlock();
+      Analysis a;
+      std::exception_ptr e;
+      try {
+        a = chol_analyze(*s);
+      } catch (...) {
+        e = std::current_exception();
+      }
+      lk.lock();
+      result = a;
+      err = e;
+      has_result = true;
+      job = false;
+      lk.unlock();
+      cv.notify_all();
+    }
+  }
+  void post() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return !job; });
+    has_result = false;
+    err = nullptr;
+    job = true;
+    lk.unlock();
+    cv.notify_all();
+  }
+  // waits for the job in flight; true (and the analysis) when one was posted
+  bool take(Analysis& out) {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [this] { return !job; });
+    if (!has_result) return false;
+    has_result = false;
+    if (err) {
+      std::exception_ptr e = err;
+      err = nullptr;
+      std::rethrow_exception(e);
+    }
+    out = result;
+    return true;
+  }
+};
+
+CholWorker* worker(Scene& s, bool create) {
+  if (!s.chol_worker && create) s.chol_worker = std::make_shared<CholWorker>(&s);
+  return static_cast<CholWorker*>(s.chol_worker.get());
+}
+}  // namespace
+
+void chol_analysis_post(Scene& s) {
+  static const bool off = getenv("ABD_CHOL_SYNC_ANALYSIS") != nullptr;
+  if (off || s.H.n == 0) return;
+  worker(s, true)->post();
+}
+
+void chol_analysis_drop(Scene& s) {
+  CholWorker* wk = worker(s, false);
+  Analysis a;
+  if (wk) {
+    try {
+      wk->take(a);
+    } catch (...) {
+    }
+  }
+}
+
 void chol_begin(Scene& s, const double* rhs, double* x) {
   Bsr& H = s.H;
   Scene::Work& w = s.w;
@@ -954,7 +1122,9 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   HMARK();
   auto th0 = std::chrono::steady_clock::now();
   w.bad.resize(1);
-  Analysis an = chol_analyze(s);
+  Analysis an;
+  CholWorker* wk = worker(s, false);
+  if (!wk || !wk->take(an)) an = chol_analyze(s);
   HMARK();
   run.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
   run.active = true;

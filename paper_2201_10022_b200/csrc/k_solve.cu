@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "driver.h"
 #include "kernels.h"
 #include "abd_pblk.cuh"
 
@@ -248,6 +249,7 @@ void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64
   if (from_cands && wk.pat_valid && s.cands.ov_matches_pattern && wk.pat_n_f == n_f &&
       wk.pat_fric_gen == s.fric.gen && H.n == s.n_dyn)
     return;
+  chol_analysis_drop(s);  // an analysis in flight belongs to the old pattern
   s.w.ch_pre = false;  // any structure copied out for the Cholesky belongs to the old pattern
   wk.pat_valid = false;
   cudaStream_t st = s.stream;
@@ -353,17 +355,13 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
     k_contribs<<<grid_for(np, 256), 256, 0, st>>>(np, s.pblk.bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
                                                   H.upper_keys.p, H.upper_pos.p, ka.p, va.p);
     note_launch("k_contribs");
-    cub::DoubleBuffer<uint32_t> dk(ka.p, kb.p);
-    cub::DoubleBuffer<int> dv(va.p, vb.p);
-    size_t bytes = 0;
     int kb_bits = bits_for(H.nnzb) + 1;  // the 0xffffffff "absent" key still sorts last
     if (kb_bits > 32) kb_bits = 32;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, dk, dv, (int)m, 0, kb_bits, st));
-    s.tmp_bytes.resize(bytes);
-    CK(cub::DeviceRadixSort::SortPairs(s.tmp_bytes.p, bytes, dk, dv, (int)m, 0, kb_bits, st));
-    k_seg_bounds<<<grid_for(m, 256), 256, 0, st>>>(m, dk.Current(), H.nnzb, seg_s.p, seg_e.p);
+    bool alt = false;
+    sort_pairs_u32(s, ka.p, kb.p, va.p, vb.p, m, kb_bits, alt);
+    k_seg_bounds<<<grid_for(m, 256), 256, 0, st>>>(m, alt ? kb.p : ka.p, H.nnzb, seg_s.p, seg_e.p);
     note_launch("k_seg_bounds");
-    cv = dv.Current();
+    cv = alt ? vb.p : va.p;
   }
   s.grad.resize(12 * (int64_t)n);
   k_reduce_blocks<<<grid_for(H.nnzb * 32, 32 * RB_WARPS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, seg_s.p, seg_e.p, cv,

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 
 #include "kernels.h"
 #include "scene.h"
@@ -54,6 +55,7 @@ Scene::Scene() {
 }
 
 Scene::~Scene() {
+  chol_worker.reset();  // joins the analysis thread before any buffer it uses goes away
   if (stream) cudaStreamDestroy(stream);
   if (side) cudaStreamDestroy(side);
   if (fork_ev) cudaEventDestroy(fork_ev);
@@ -76,10 +78,60 @@ void scan_exclusive_i32(Scene& s, const int* in, int* out, int64_t n) {
   CK(cub::DeviceScan::ExclusiveSum(s.tmp_bytes.p, bytes, in, out, (int)n, s.stream));
 }
 
+// Small sorts (n <= 16384 keys of <= 32 bits): one CTA, cub::BlockRadixSort, one
+// launch instead of the device sort's memset + histogram + scan + onesweep passes.
+// Stable (padding sorts after every real key), so the result equals the device sort's.
+constexpr int BS_THREADS = 1024, BS_ITEMS = 16, BS_CAP = BS_THREADS * BS_ITEMS;
+typedef cub::BlockRadixSort<uint32_t, BS_THREADS, BS_ITEMS, int> BlockSortU32;
+
+template <class K>
+__global__ void __launch_bounds__(BS_THREADS) k_block_sort(const K* __restrict__ kin, const int* __restrict__ vin,
+                                                           K* kout, int* vout, int n, int end_bit) {
+  extern __shared__ __align__(16) unsigned char bs_smem[];
+  auto& temp = *reinterpret_cast<typename BlockSortU32::TempStorage*>(bs_smem);
+  uint32_t k[BS_ITEMS];
+  int v[BS_ITEMS];
+#pragma unroll
+  for (int i = 0; i < BS_ITEMS; ++i) {
+    const int idx = threadIdx.x * BS_ITEMS + i;  // blocked: input order preserved
+    k[i] = idx < n ? (uint32_t)kin[idx] : 0xffffffffu;
+    v[i] = idx < n ? vin[idx] : -1;
+  }
+  BlockSortU32(temp).SortBlockedToStriped(k, v, 0, end_bit);
+#pragma unroll
+  for (int i = 0; i < BS_ITEMS; ++i) {
+    const int idx = i * BS_THREADS + threadIdx.x;
+    if (idx < n) {
+      kout[idx] = (K)k[i];
+      vout[idx] = v[i];
+    }
+  }
+}
+
+template <class K>
+static bool block_sort(Scene& s, K* keys, K* keys_alt, int* vals, int* vals_alt, int64_t n, int end_bit) {
+  static const bool off = getenv("ABD_NO_BLOCK_SORT") != nullptr;
+  if (off || n > BS_CAP || end_bit > 32) return false;
+  static bool attr = false;
+  const int smem = (int)sizeof(typename BlockSortU32::TempStorage);
+  if (!attr) {
+    CK(cudaFuncSetAttribute((void*)k_block_sort<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute((void*)k_block_sort<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  k_block_sort<K><<<1, BS_THREADS, smem, s.stream>>>(keys, vals, keys_alt, vals_alt, (int)n, end_bit);
+  note_launch("k_block_sort");
+  return true;
+}
+
 void sort_pairs_u64(Scene& s, uint64_t* keys, uint64_t* keys_alt, int* vals, int* vals_alt, int64_t n,
                     int end_bit, bool& result_in_alt) {
   result_in_alt = false;
   if (n <= 1) return;
+  if (block_sort(s, keys, keys_alt, vals, vals_alt, n, end_bit)) {
+    result_in_alt = true;
+    return;
+  }
   cub::DoubleBuffer<uint64_t> k(keys, keys_alt);
   cub::DoubleBuffer<int> v(vals, vals_alt);
   size_t bytes = 0;
@@ -93,6 +145,10 @@ void sort_pairs_u32(Scene& s, uint32_t* keys, uint32_t* keys_alt, int* vals, int
                     bool& result_in_alt) {
   result_in_alt = false;
   if (n <= 1) return;
+  if (block_sort(s, keys, keys_alt, vals, vals_alt, n, end_bit)) {
+    result_in_alt = true;
+    return;
+  }
   cub::DoubleBuffer<uint32_t> k(keys, keys_alt);
   cub::DoubleBuffer<int> v(vals, vals_alt);
   size_t bytes = 0;
@@ -168,6 +224,7 @@ struct ProfSite {
   double host_ms = 0.0, blocked_ms = 0.0;
 };
 static std::map<std::string, ProfSite> g_sites;
+static std::mutex g_prof_mu;
 static std::chrono::steady_clock::time_point g_last;
 static bool g_last_set = false;
 
@@ -180,6 +237,7 @@ void host_sync(cudaStream_t st, const char* site) {
   auto t0 = clk::now();
   CK(cudaStreamSynchronize(st));
   auto t1 = clk::now();
+  std::lock_guard<std::mutex> g(g_prof_mu);
   const char* base = strrchr(site, '/');
   ProfSite& p = g_sites[base ? base + 1 : site];
   p.n += 1;
@@ -192,6 +250,7 @@ void host_sync(cudaStream_t st, const char* site) {
 void host_mark(const char* site) {
   if (!g_prof_on) return;
   auto t = std::chrono::steady_clock::now();
+  std::lock_guard<std::mutex> g(g_prof_mu);
   const char* base = strrchr(site, '/');
   ProfSite& p = g_sites[std::string("mark ") + (base ? base + 1 : site)];
   p.n += 1;

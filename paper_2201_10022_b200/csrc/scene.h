@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <initializer_list>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -217,6 +218,9 @@ struct Scene {
 
   // persistent workspaces (grown, never shrunk: no cudaMalloc in steady state)
   struct Work {
+    // host scratch of the Cholesky analysis (reused: no allocations in the steady state)
+    std::vector<int> hs_i[32];
+    std::vector<char> hs_c[2];
     DVec<int64_t> comm_cnt, comm_buf, fric_keys, fric_keys_all;  // multi-GPU scratch
     DVec<int> act;      // compacted active candidate indices (VF then EE)
     DVec<int> moll;     // active EE slots with an active mollifier (deferred 9-column path)
@@ -286,6 +290,8 @@ struct Scene {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, tev0 = nullptr, tev1 = nullptr;
   bool instrument = true;
 
+  // host worker thread of the Cholesky analysis (k_chol.cu); stopped first on destruction
+  std::shared_ptr<void> chol_worker;
   Scene();
   ~Scene();
 };
