@@ -341,7 +341,7 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   std::swap(s.stream, s.side);
   CK(cudaEventRecord(s.join_ev, s.side));
   EventTimer tm(s, 2);
-  launch_ccd_both(s, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p);
+  launch_ccd_both(s, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p, /*track=*/true);
   tm.stop();
   CK(cudaStreamWaitEvent(st, s.join_ev, 0));
   k_alpha_trial<<<grid_for(NB, 256), 256, 0, st>>>(NB, s.q.p, s.dq.p, tmin, P.ccd_step_scale, s.q_trial.p);
@@ -354,8 +354,19 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   comm_allreduce(s, w.lsscal.p, 8, 0, 0);
   comm_allreduce(s, w.lserr.p, 2, 1, 2);
   double* hp = s.h_pinned + 32;
-  pack_to_host(st, hp, {{tmin, 8, 0}, {w.lsscal.p, 64, 8}, {w.lserr.p, 8, 72}});
+  pack_to_host(st, hp, {{tmin, 8, 0}, {w.lsscal.p, 64, 8}, {w.lserr.p, 8, 72}, {w.ull.p + 12, 4, 80}});
   SSYNC(st);
+  {
+    // this line search's slow queries are the next iteration's hot list
+    const int n_slow = std::min<int>(*reinterpret_cast<const int*>(hp + 10), CCD_HOT_CAP);
+    w.hot_rows.resize(CCD_HOT_CAP);
+    w.hot_kind.resize(CCD_HOT_CAP);
+    if (n_slow > 0) {
+      CK(cudaMemcpyAsync(w.hot_rows.p, w.slow_rows.p, n_slow * sizeof(int4), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(w.hot_kind.p, w.slow_kind.p, n_slow * sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
+    w.hot_n = n_slow;
+  }
   const int* he = reinterpret_cast<const int*>(hp + 9);
   if (he[0]) throw Error(ABD_ERR_CCD_DOMAIN, "CCD query issued at non-positive initial distance");
   if (he[1]) throw Error(ABD_ERR_BARRIER_DOMAIN, "barrier evaluated at non-positive squared distance "
@@ -613,6 +624,9 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       s.dq.zero(stream);
       k_expand_dq<<<grid_for(ND, 256), 256, 0, stream>>>(s.n_dyn, s.dyn_body.p, dsrc, sign, s.dq.p);
       note_launch("k_expand_dq");
+      // the previous line search's slowest ACCD queries start now on side2 (exact,
+      // without the shared cut) and overlap the broad phase
+      launch_ccd_hot(s, s.q.p, s.dq.p, P.ccd_slack);
       // candidates over the proposed interval [q, q + dq]
       t0 = clk::now();
       launch_axpy_q(s, s.q.p, 1.0, s.dq.p, s.q_trial.p, NB);  // q + dq (exact add)

@@ -5,6 +5,7 @@
 #include "abd_misc.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -379,24 +380,73 @@ __global__ void k_ccd(SceneView sv, int kind, int64_t n, const int4* __restrict_
 }
 
 // K5 over both candidate lists in one launch (VF rows first, then EE): the
-// heavy-tailed ACCD queries of the two kinds share one tail instead of two
+// heavy-tailed ACCD queries of the two kinds share one tail instead of two.
+// Hot queries (rows of the hot list, already evaluated exactly by k_ccd_hot while
+// the broad phase ran) take their precomputed t; queries that need >= slow_it
+// iterations (hot ones included) form the next hot list.
+__device__ __forceinline__ double ccd_row(const SceneView& sv, int kind, int4 row, const double* __restrict__ q,
+                                          const double* __restrict__ dq, double slack,
+                                          volatile const unsigned long long* cut, bool& bad, int& it) {
+  PairIds ids = pair_ids(sv, kind, row);
+  V3 x[4], xb[4], dx[4];
+  pair_points(sv, ids, q, x, xb);
+  for (int k = 0; k < 4; ++k) {
+    int b = ids.body[k];
+    dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+  }
+  return accd_query(kind, x, dx, slack, 1.0, 512, cut, bad, &it);
+}
+
+__global__ void k_ccd_hot(SceneView sv, int n, const int4* __restrict__ rows, const int* __restrict__ kind,
+                          const double* __restrict__ q, const double* __restrict__ dq, double slack, double* t_out,
+                          int* bad_out, int* it_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool bad = false;
+  int it = 0;
+  t_out[i] = ccd_row(sv, kind[i], rows[i], q, dq, slack, nullptr, bad, it);
+  bad_out[i] = bad ? 1 : 0;
+  it_out[i] = it;
+}
+
 __global__ void k_ccd_both(SceneView sv, int64_t n_vf, const int4* __restrict__ vf, int64_t n_ee,
                            const int4* __restrict__ ee, const double* __restrict__ q, const double* __restrict__ dq,
-                           double slack, unsigned long long* tmin, int* err) {
+                           double slack, unsigned long long* tmin, int* err, HotCcd h) {
+  __shared__ int4 hr[CCD_HOT_CAP];
+  __shared__ int hk[CCD_HOT_CAP];
+  for (int j = threadIdx.x; j < h.n; j += blockDim.x) {
+    hr[j] = h.rows[j];
+    hk[j] = h.kind[j];
+  }
+  __syncthreads();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double t = INFINITY;
   if (i < n_vf + n_ee) {
     const int kind = i < n_vf ? KIND_VF : KIND_EE;
-    PairIds ids = pair_ids(sv, kind, kind == KIND_VF ? vf[i] : ee[i - n_vf]);
-    V3 x[4], xb[4], dx[4];
-    pair_points(sv, ids, q, x, xb);
-    for (int k = 0; k < 4; ++k) {
-      int b = ids.body[k];
-      dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
+    const int4 r = kind == KIND_VF ? vf[i] : ee[i - n_vf];
+    int hit = -1;
+    for (int j = 0; j < h.n; ++j)
+      if (hk[j] == kind && hr[j].x == r.x && hr[j].y == r.y && hr[j].z == r.z && hr[j].w == r.w) {
+        hit = j;
+        break;
+      }
+    int it = 0;
+    if (hit >= 0) {
+      t = h.t[hit];
+      it = h.it[hit];
+      if (h.bad[hit]) atomicExch(err, 1);
+    } else {
+      bool bad = false;
+      t = ccd_row(sv, kind, r, q, dq, slack, tmin, bad, it);
+      if (bad) atomicExch(err, 1);
     }
-    bool bad = false;
-    t = accd_query(kind, x, dx, slack, 1.0, 512, tmin, bad);
-    if (bad) atomicExch(err, 1);
+    if (h.slow_cap > 0 && it >= h.slow_it) {
+      const unsigned at = atomicAdd(h.slow_cnt, 1u);
+      if ((int)at < h.slow_cap) {
+        h.slow_rows[at] = r;
+        h.slow_kind[at] = kind;
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
   if ((threadIdx.x & 31) == 0 && t < INFINITY) atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
@@ -791,13 +841,83 @@ void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double sl
   }
 }
 
+void launch_ccd_hot(Scene& s, const double* q, const double* dq, double slack) {
+  Scene::Work& w = s.w;
+  w.hot_pending = false;
+  static const bool off = getenv("ABD_CCD_NO_HOT") != nullptr;
+  if (off || w.hot_n == 0) return;
+  w.hot_t.resize(CCD_HOT_CAP);
+  w.hot_bad.resize(CCD_HOT_CAP);
+  w.hot_it.resize(CCD_HOT_CAP);
+  CK(cudaEventRecord(s.hot_fork_ev, s.stream));
+  CK(cudaStreamWaitEvent(s.side2, s.hot_fork_ev, 0));
+  k_ccd_hot<<<1, CCD_HOT_CAP, 0, s.side2>>>(view(s), w.hot_n, w.hot_rows.p, w.hot_kind.p, q, dq, slack, w.hot_t.p,
+                                            w.hot_bad.p, w.hot_it.p);
+  note_launch("k_ccd_hot");
+  CK(cudaEventRecord(s.hot_ev, s.side2));
+  w.hot_pending = true;
+}
+
 void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, unsigned long long* tmin,
-                     int* err) {
+                     int* err, bool track) {
   const int64_t n = s.cands.n_vf + s.cands.n_ee;
+  Scene::Work& w = s.w;
+  HotCcd h{};
+  if (track) {
+    w.slow_rows.resize(CCD_HOT_CAP);
+    w.slow_kind.resize(CCD_HOT_CAP);
+    h.slow_rows = w.slow_rows.p;
+    h.slow_kind = w.slow_kind.p;
+    h.slow_cnt = reinterpret_cast<unsigned*>(w.ull.p + 12);
+    h.slow_cap = CCD_HOT_CAP;
+    h.slow_it = CCD_SLOW_IT;
+    CK(cudaMemsetAsync(h.slow_cnt, 0, sizeof(unsigned), s.stream));
+    if (w.hot_pending) {
+      CK(cudaStreamWaitEvent(s.stream, s.hot_ev, 0));
+      h.rows = w.hot_rows.p;
+      h.kind = w.hot_kind.p;
+      h.t = w.hot_t.p;
+      h.bad = w.hot_bad.p;
+      h.it = w.hot_it.p;
+      h.n = w.hot_n;
+    }
+    w.hot_pending = false;
+  }
   if (!n) return;
   k_ccd_both<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), s.cands.n_vf, s.cands.vf.p, s.cands.n_ee, s.cands.ee.p,
-                                                    q, dq, slack, tmin, err);
+                                                    q, dq, slack, tmin, err, h);
   note_launch("k_ccd");
+  static const bool stats = getenv("ABD_CCD_SLOW") != nullptr;
+  if (stats) {
+    // diagnostic: the slowest queries (iterations, t, row) of this call
+    for (int kind = 0; kind < 2; ++kind) {
+      int64_t nk;
+      const int4* rows = rows_of(s, kind, nk);
+      if (!nk) continue;
+      DVec<int> its;
+      DVec<double> ts;
+      its.resize(nk);
+      ts.resize(nk);
+      k_ccd_dbg<<<grid_for(nk, 128), 128, 0, s.stream>>>(view(s), kind, nk, rows, q, dq, slack, its.p, ts.p);
+      std::vector<int> hi(nk);
+      std::vector<double> ht(nk);
+      std::vector<int4> hr(nk);
+      its.download(hi.data(), nk, s.stream);
+      ts.download(ht.data(), nk, s.stream);
+      CK(cudaMemcpyAsync(hr.data(), rows, nk * sizeof(int4), cudaMemcpyDeviceToHost, s.stream));
+      SSYNC(s.stream);
+      std::vector<int64_t> idx(nk);
+      for (int64_t i = 0; i < nk; ++i) idx[i] = i;
+      std::partial_sort(idx.begin(), idx.begin() + std::min<int64_t>(6, nk), idx.end(),
+                        [&](int64_t a, int64_t b) { return hi[a] > hi[b]; });
+      fprintf(stderr, "[ccd slow] kind=%d", kind);
+      for (int64_t k = 0; k < std::min<int64_t>(6, nk); ++k) {
+        const int4 r = hr[idx[k]];
+        fprintf(stderr, " (%d,%d,%d,%d:it=%d,t=%.3e)", r.x, r.y, r.z, r.w, hi[idx[k]], ht[idx[k]]);
+      }
+      fprintf(stderr, "\n");
+    }
+  }
 }
 
 void launch_body_terms(Scene& s, const double* q, const double* qt, double dt, double* grad0, double* diag0,

@@ -63,8 +63,24 @@ void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, do
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best_bits);
 void launch_friction_pre(Scene& s, int kind, const double* q, double kappa, double dh, const int* flags,
                          const int* pos, int64_t base, double* basis_out);
+// ACCD hot list (Scene::Work::hot_*): capacity and the iteration count that makes a query "slow"
+constexpr int CCD_HOT_CAP = 64;
+constexpr int CCD_SLOW_IT = 32;
+struct HotCcd {
+  const int4* rows;
+  const int* kind;
+  const double* t;
+  const int* bad;
+  const int* it;
+  int n;
+  int4* slow_rows;
+  int* slow_kind;
+  unsigned* slow_cnt;
+  int slow_cap, slow_it;
+};
+void launch_ccd_hot(Scene& s, const double* q, const double* dq, double slack);
 void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, unsigned long long* tmin,
-                     int* err);
+                     int* err, bool track = false);
 void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack,
                 unsigned long long* tmin_bits, int* err);
 // per-body inertia + orthogonality terms (K1): grad0/diag0 per dynamic slot, energy partials

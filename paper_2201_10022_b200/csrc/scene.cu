@@ -42,6 +42,9 @@ Scene::Scene() {
   CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&hot_fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&hot_ev, cudaEventDisableTiming));
   CK(cudaMallocHost(&h_pinned, 64 * sizeof(double)));
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
@@ -60,6 +63,9 @@ Scene::~Scene() {
   if (side) cudaStreamDestroy(side);
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (join_ev) cudaEventDestroy(join_ev);
+  if (side2) cudaStreamDestroy(side2);
+  if (hot_fork_ev) cudaEventDestroy(hot_fork_ev);
+  if (hot_ev) cudaEventDestroy(hot_ev);
   if (h_pinned) cudaFreeHost(h_pinned);
   for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
     if (e) cudaEventDestroy(e);

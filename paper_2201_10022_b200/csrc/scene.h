@@ -168,6 +168,8 @@ struct Scene {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;            // forked work that overlaps the main stream (event-joined)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaStream_t side2 = nullptr;  // early ACCD of the hot queries (overlaps the broad phase)
+  cudaEvent_t hot_fork_ev = nullptr, hot_ev = nullptr;
   int num_sms = 148;
 
   // geometry (immutable after create)
@@ -220,6 +222,13 @@ struct Scene {
   struct Work {
     // host scratch of the Cholesky analysis (reused: no allocations in the steady state)
     std::vector<int> hs_i[32];
+    // ACCD hot list: the slowest queries (>= CCD_SLOW_IT iterations) of the previous
+    // line search, re-evaluated right after the solve on side2 while the broad phase runs
+    DVec<int4> hot_rows, slow_rows;
+    DVec<int> hot_kind, slow_kind, hot_bad, hot_it;
+    DVec<double> hot_t;
+    int hot_n = 0;
+    bool hot_pending = false;
     std::vector<char> hs_c[2];
     DVec<int64_t> comm_cnt, comm_buf, fric_keys, fric_keys_all;  // multi-GPU scratch
     DVec<int> act;      // compacted active candidate indices (VF then EE)
