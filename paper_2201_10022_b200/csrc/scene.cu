@@ -88,7 +88,8 @@ void scan_exclusive_i32(Scene& s, const int* in, int* out, int64_t n) {
 // launch instead of the device sort's memset + histogram + scan + onesweep passes.
 // Stable (padding sorts after every real key), so the result equals the device sort's.
 constexpr int BS_THREADS = 1024, BS_ITEMS = 16, BS_CAP = BS_THREADS * BS_ITEMS;
-typedef cub::BlockRadixSort<uint32_t, BS_THREADS, BS_ITEMS, int> BlockSortU32;
+typedef cub::BlockRadixSort<uint32_t, BS_THREADS, BS_ITEMS, int, 6> BlockSortU32;
+static_assert(sizeof(BlockSortU32::TempStorage) <= 200 * 1024, "block sort smem");
 
 template <class K>
 __global__ void __launch_bounds__(BS_THREADS) k_block_sort(const K* __restrict__ kin, const int* __restrict__ vin,
