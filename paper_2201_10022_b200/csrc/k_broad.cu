@@ -1061,6 +1061,70 @@ static void sort_rows(Scene& s, DVec<int4>& rows, int64_t n, int w1, int w3) {
   CK(cudaMemcpyAsync(rows.p, w.rows_tmp.p, n * sizeof(int4), cudaMemcpyDeviceToDevice, s.stream));
 }
 
+// inflated boxes of the body-pair superset: exact box +- frac x cell (cell from k_cell_size)
+__global__ void k_inflate_boxes(int B, const double* __restrict__ bbox, const double* __restrict__ cell_p,
+                                double frac, double* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double m = frac * *cell_p;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    out[6 * b + k] = bbox[6 * b + k] - m;
+    out[6 * b + 3 + k] = bbox[6 * b + 3 + k] + m;
+  }
+}
+
+// one CTA: (1) every exact swept box inside its inflated box? (2) the superset pairs
+// whose exact boxes overlap, compacted in order (the superset is canonical, so is the
+// result).  out_info = {count, violation}.
+constexpr int VL_THREADS = 1024, VL_ITEMS = 8;
+__global__ void __launch_bounds__(VL_THREADS) k_vl_filter(int B, const double* __restrict__ bbox,
+                                                          const double* __restrict__ vl_box, int64_t n_sup,
+                                                          const int2* __restrict__ sup, int2* out, int* out_info) {
+  typedef cub::BlockScan<int, VL_THREADS> Scan;
+  __shared__ typename Scan::TempStorage temp;
+  __shared__ int viol, base;
+  if (threadIdx.x == 0) {
+    viol = 0;
+    base = 0;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += VL_THREADS) {
+    const double* x = bbox + 6 * b;
+    const double* y = vl_box + 6 * b;
+    if (!(x[0] >= y[0] && x[1] >= y[1] && x[2] >= y[2] && x[3] <= y[3] && x[4] <= y[4] && x[5] <= y[5])) viol = 1;
+  }
+  for (int64_t c0 = 0; c0 < n_sup; c0 += (int64_t)VL_THREADS * VL_ITEMS) {
+    const int64_t i0 = c0 + (int64_t)threadIdx.x * VL_ITEMS;
+    bool f[VL_ITEMS];
+    int2 pr[VL_ITEMS];
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < VL_ITEMS; ++k) {
+      const int64_t i = i0 + k;
+      f[k] = false;
+      if (i < n_sup) {
+        pr[k] = sup[i];
+        f[k] = box_overlap(bbox + 6 * pr[k].x, bbox + 6 * pr[k].y);
+      }
+      cnt += f[k];
+    }
+    int off = 0, tot = 0;
+    Scan(temp).ExclusiveSum(cnt, off, tot);
+    const int b0 = base;
+#pragma unroll
+    for (int k = 0; k < VL_ITEMS; ++k)
+      if (f[k]) out[b0 + off++] = pr[k];
+    __syncthreads();
+    if (threadIdx.x == 0) base = b0 + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out_info[0] = base;
+    out_info[1] = viol;
+  }
+}
+
 void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   cudaStream_t st = s.stream;
   double h = 0.5 * d_hat;
@@ -1071,63 +1135,110 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   s.bbox.resize(6 * s.B);
   k_body_boxes<<<grid_for((int64_t)s.B * 32, 256), 256, 0, st>>>(s.B, s.v_off.p, s.rest.p, q0, q1, h, s.bbox.p);
   note_launch("k_body_boxes");
-  // body pairs on a uniform grid (cell = 90th-percentile body extent)
-  bool alt = false;
-  w.k0.resize(s.B);
-  w.k1.resize(s.B);
-  w.va.resize(s.B + 1);
-  w.vb.resize(s.B + 1);
-  w.ka.resize(s.B);
-  w.kb.resize(s.B);
-  k_extent_keys<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.ka.p);
-  note_launch("k_extent_keys");
-  w.scal.resize(4);
-  k_cell_size<<<1, 1024, 0, st>>>(s.B, w.ka.p, w.scal.p);
-  note_launch("k_cell_size");
-  k_cell_keys2<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.scal.p, w.ka.p, w.va.p);
-  note_launch("k_cell_keys");
-  sort_pairs_u32(s, w.ka.p, w.kb.p, w.va.p, w.vb.p, s.B, CELL_KEY_BITS, alt);
-  const uint32_t* skeys = alt ? w.kb.p : w.ka.p;
-  const int* sbody = alt ? w.vb.p : w.va.p;
-  int n_small = s.B;  // large bodies carry CELL_LARGE and sort last; the lookups never match them
-  unsigned long long* ovc = w.ull.p + 6;
-  unsigned long long* hov = reinterpret_cast<unsigned long long*>(s.h_pinned);
-  if (c.ov.cap < 256) c.ov.resize(256);
-  for (int attempt = 0; attempt < 3; ++attempt) {
-    CK(cudaMemsetAsync(ovc, 0, sizeof(unsigned long long), st));
-    k_grid_pairs<<<grid_for((int64_t)s.B * GP_COLS, 128), 128, 0, st>>>(s.B, s.bbox.p, s.dyn.p, skeys, sbody, n_small, w.scal.p, ovc,
-                                                     (int64_t)c.ov.cap, c.ov.p);
-    note_launch("k_grid_pairs");
-    k_large_pairs<<<grid_for(s.B, 128), 128, 0, st>>>(s.B, s.bbox.p, s.dyn.p, skeys, sbody, w.scal.p, ovc,
-                                                      (int64_t)c.ov.cap, c.ov.p);
-    note_launch("k_large_pairs");
-    CK(cudaMemcpyAsync(hov, ovc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  // body pairs: filter the superset with the exact boxes (one CTA, one sync); rebuild
+  // the superset on the uniform grid when a box left its inflated box
+  static const double vl_frac = getenv("ABD_VL_MARGIN") ? atof(getenv("ABD_VL_MARGIN")) : 0.05;
+  const bool use_vl = vl_frac > 0.0;
+  int* vl_info = reinterpret_cast<int*>(w.ull.p + 13);
+  int n_ov = 0;
+  bool have = false;
+  if (use_vl && w.vl_valid) {
+    if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
+    k_vl_filter<<<1, VL_THREADS, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, w.vl_n, w.vl_pairs.p, c.ov.p, vl_info);
+    note_launch("k_vl_filter");
+    int* hi = reinterpret_cast<int*>(s.h_pinned);
+    pack_to_host(st, hi, {{vl_info, 8, 0}});
     SSYNC(st);
-    if (hov[0] <= c.ov.cap) break;
-    c.ov.resize(hov[0]);
+    if (hi[1] == 0) {
+      n_ov = hi[0];
+      have = true;
+    }
   }
-  int n_ov = (int)hov[0];
+  if (!have) {
+    // superset of pairs on a uniform grid (cell = largest extent <= 4x the median)
+    bool alt = false;
+    w.k0.resize(s.B);
+    w.k1.resize(s.B);
+    w.va.resize(s.B + 1);
+    w.vb.resize(s.B + 1);
+    w.ka.resize(s.B);
+    w.kb.resize(s.B);
+    w.scal.resize(4);
+    const double* gbox = s.bbox.p;
+    if (use_vl) {
+      k_extent_keys<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.ka.p);
+      note_launch("k_extent_keys");
+      k_cell_size<<<1, 1024, 0, st>>>(s.B, w.ka.p, w.scal.p);
+      note_launch("k_cell_size");
+      w.vl_box.resize(6 * s.B);
+      k_inflate_boxes<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.scal.p, vl_frac, w.vl_box.p);
+      note_launch("k_inflate_boxes");
+      gbox = w.vl_box.p;
+    }
+    k_extent_keys<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, gbox, w.ka.p);
+    note_launch("k_extent_keys");
+    k_cell_size<<<1, 1024, 0, st>>>(s.B, w.ka.p, w.scal.p);
+    note_launch("k_cell_size");
+    k_cell_keys2<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, gbox, w.scal.p, w.ka.p, w.va.p);
+    note_launch("k_cell_keys");
+    sort_pairs_u32(s, w.ka.p, w.kb.p, w.va.p, w.vb.p, s.B, CELL_KEY_BITS, alt);
+    const uint32_t* skeys = alt ? w.kb.p : w.ka.p;
+    const int* sbody = alt ? w.vb.p : w.va.p;
+    int n_small = s.B;  // large bodies carry CELL_LARGE and sort last; the lookups never match them
+    unsigned long long* ovc = w.ull.p + 6;
+    unsigned long long* hov = reinterpret_cast<unsigned long long*>(s.h_pinned);
+    DVec<int2>& dst = use_vl ? w.vl_pairs : c.ov;
+    if (dst.cap < 256) dst.resize(256);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+      CK(cudaMemsetAsync(ovc, 0, sizeof(unsigned long long), st));
+      k_grid_pairs<<<grid_for((int64_t)s.B * GP_COLS, 128), 128, 0, st>>>(s.B, gbox, s.dyn.p, skeys, sbody, n_small,
+                                                                          w.scal.p, ovc, (int64_t)dst.cap, dst.p);
+      note_launch("k_grid_pairs");
+      k_large_pairs<<<grid_for(s.B, 128), 128, 0, st>>>(s.B, gbox, s.dyn.p, skeys, sbody, w.scal.p, ovc,
+                                                        (int64_t)dst.cap, dst.p);
+      note_launch("k_large_pairs");
+      CK(cudaMemcpyAsync(hov, ovc, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+      SSYNC(st);
+      if (hov[0] <= dst.cap) break;
+      dst.resize(hov[0]);
+    }
+    const int n_g = (int)hov[0];
+    dst.n = n_g;
+    // canonical (i, j) order
+    if (n_g > 0) {
+      int bB = bits_for(s.B - 1);
+      w.k0.resize(n_g);
+      w.k1.resize(n_g);
+      w.va.resize(n_g);
+      w.vb.resize(n_g);
+      k_pair_keys<<<grid_for(n_g, 256), 256, 0, st>>>(n_g, dst.p, bB, w.k0.p, w.va.p);
+      note_launch("k_pair_keys");
+      sort_pairs_u64(s, w.k0.p, w.k1.p, w.va.p, w.vb.p, n_g, 2 * bB, alt);
+      w.pairs_tmp.resize(n_g);
+      k_gather<int2><<<grid_for(n_g, 256), 256, 0, st>>>(n_g, alt ? w.vb.p : w.va.p, dst.p, w.pairs_tmp.p);
+      note_launch("k_gather");
+      CK(cudaMemcpyAsync(dst.p, w.pairs_tmp.p, n_g * sizeof(int2), cudaMemcpyDeviceToDevice, st));
+    }
+    if (use_vl) {
+      w.vl_n = n_g;
+      w.vl_valid = true;
+      if ((int64_t)c.ov.cap < std::max(n_g, 1)) c.ov.resize(std::max(n_g, 1));
+      k_vl_filter<<<1, VL_THREADS, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, w.vl_n, w.vl_pairs.p, c.ov.p, vl_info);
+      note_launch("k_vl_filter");
+      int* hi = reinterpret_cast<int*>(s.h_pinned);
+      pack_to_host(st, hi, {{vl_info, 8, 0}});
+      SSYNC(st);
+      n_ov = hi[0];
+    } else {
+      n_ov = n_g;
+    }
+  }
   c.n_ov = n_ov;
   c.ov.n = n_ov;
   c.ov_matches_pattern = false;
   if (n_ov == 0) {
     c.ov_matches_pattern = w.pat_n_ov == 0;
     return;
-  }
-  // canonical (i, j) order of overlap pairs
-  {
-    int bB = bits_for(s.B - 1);
-    w.k0.resize(n_ov);
-    w.k1.resize(n_ov);
-    w.va.resize(n_ov);
-    w.vb.resize(n_ov);
-    k_pair_keys<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, c.ov.p, bB, w.k0.p, w.va.p);
-    note_launch("k_pair_keys");
-    sort_pairs_u64(s, w.k0.p, w.k1.p, w.va.p, w.vb.p, n_ov, 2 * bB, alt);
-    w.pairs_tmp.resize(n_ov);
-    k_gather<int2><<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, alt ? w.vb.p : w.va.p, c.ov.p, w.pairs_tmp.p);
-    note_launch("k_gather");
-    CK(cudaMemcpyAsync(c.ov.p, w.pairs_tmp.p, n_ov * sizeof(int2), cudaMemcpyDeviceToDevice, st));
   }
   // is every dynamic overlap pair already a block of the resident BSR pattern?
   // (read back with the primitive-pair counts below; build_pattern then keeps the

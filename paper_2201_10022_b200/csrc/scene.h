@@ -245,6 +245,13 @@ struct Scene {
     int64_t pat_n_ov = -1, pat_n_f = -1, pat_fric_gen = -1;
     bool pat_valid = false;
     DVec<int2> pairs_tmp;
+    // body-pair superset ("Verlet list"): canonical (i, j) pairs whose boxes inflated
+    // by a margin overlap; each broad phase filters it with the exact swept boxes and
+    // rebuilds it only when a body's box leaves its inflated box
+    DVec<double> vl_box;
+    DVec<int2> vl_pairs;
+    int64_t vl_n = 0;
+    bool vl_valid = false;
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
     DVec<double> lsred, lsscal;  // merged CCD + e0 + first-trial line-search reductions
