@@ -2,6 +2,7 @@
 // out; exceptions mapped to abd_status + thread-local message.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -523,6 +524,13 @@ abd_scene* abd_scene_create(int n_bodies, const int64_t* v_off, const int64_t* e
     s.vert_body.upload(vb.data(), s.V, st);
     s.edge_body.upload(eb.data(), s.E, st);
     s.tri_body.upload(tb.data(), s.T, st);
+    {
+      std::vector<double> rm(3 * (size_t)B, 0.0);
+      for (int b = 0; b < B; ++b)
+        for (int v = vo[b]; v < vo[b + 1]; ++v)
+          for (int k = 0; k < 3; ++k) rm[3 * b + k] = std::max(rm[3 * b + k], std::fabs(rest[3 * (int64_t)v + k]));
+      s.body_rmax.upload(rm.data(), 3 * (size_t)B, st);
+    }
     s.h_dyn.assign(dynamic, dynamic + B);
     s.dyn.upload(s.h_dyn.data(), B, st);
     s.h_slot.assign(B, -1);

@@ -1125,6 +1125,278 @@ __global__ void __launch_bounds__(VL_THREADS) k_vl_filter(int B, const double* _
   }
 }
 
+// ---------------------------------------------------------------------------
+// primitive Verlet list (Work::pvl_*)
+// exact swept boxes of the candidate rows' primitives overlap? (contact.py:222-229 boxes)
+__global__ void k_pvl_flags(PrimGeo g, int64_t n_vf, const int4* __restrict__ vf, int64_t n_ee,
+                            const int4* __restrict__ ee, int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_vf + n_ee) return;
+  const bool is_vf = i < n_vf;
+  const int4 r = is_vf ? vf[i] : ee[i - n_vf];
+  int va[3], vb2[3];
+  int na, nb;
+  if (is_vf) {
+    va[0] = g.v_off[r.x] + r.y;
+    na = 1;
+    const int* t = g.tris + 3 * (int64_t)(g.t_off[r.z] + r.w);
+    vb2[0] = t[0];
+    vb2[1] = t[1];
+    vb2[2] = t[2];
+    nb = 3;
+  } else {
+    const int* ea = g.edges + 2 * (int64_t)(g.e_off[r.x] + r.y);
+    const int* eb = g.edges + 2 * (int64_t)(g.e_off[r.z] + r.w);
+    va[0] = ea[0];
+    va[1] = ea[1];
+    vb2[0] = eb[0];
+    vb2[1] = eb[1];
+    na = nb = 2;
+  }
+  double A[6], Bx[6], t6[6];
+  for (int side = 0; side < 2; ++side) {
+    const int body = side ? r.z : r.x;
+    const int* vv = side ? vb2 : va;
+    const int nv = side ? nb : na;
+    double* o = side ? Bx : A;
+    vertex_box(g.rest, vv[0], g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h, o);
+    for (int m = 1; m < nv; ++m) {
+      vertex_box(g.rest, vv[m], g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h, t6);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        o[k] = fmin(o[k], t6[k]);
+        o[3 + k] = fmax(o[3 + k], t6[3 + k]);
+      }
+    }
+  }
+  flags[i] = A[0] <= Bx[3] && Bx[0] <= A[3] && A[1] <= Bx[4] && Bx[1] <= A[4] && A[2] <= Bx[5] && Bx[2] <= A[5];
+}
+
+// every body's current sweep [q0, q1] within half the margin of the build sweep
+// [Q0, Q1]: for each end, its deviation e from the closest point of the segment
+// bounds every vertex's displacement by sum_j |e_A,ij| R_j + |e_p,i| (R = max |rest|)
+__global__ void k_pvl_check(int B, const double* __restrict__ q0, const double* __restrict__ q1,
+                            const double* __restrict__ Q0, const double* __restrict__ Q1,
+                            const double* __restrict__ rmax, double lim, int* viol) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double* P = Q0 + 12 * (int64_t)b;
+  const double* Pe = Q1 + 12 * (int64_t)b;
+  double d[12], dd = 0.0;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    d[k] = Pe[k] - P[k];
+    dd += d[k] * d[k];
+  }
+  bool bad = false;
+  for (int u = 0; u < 2; ++u) {
+    const double* x = (u ? q1 : q0) + 12 * (int64_t)b;
+    double proj = 0.0;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) proj += (x[k] - P[k]) * d[k];
+    const double al = dd > 0.0 ? fmin(1.0, fmax(0.0, proj / dd)) : 0.0;
+    double e[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) e[k] = x[k] - (P[k] + al * d[k]);
+    for (int i = 0; i < 3; ++i) {
+      const double bound = fabs(e[i]) + fabs(e[3 + 3 * i]) * rmax[3 * b] + fabs(e[4 + 3 * i]) * rmax[3 * b + 1] +
+                           fabs(e[5 + 3 * i]) * rmax[3 * b + 2];
+      if (!(bound <= lim)) bad = true;
+    }
+  }
+  if (bad) atomicExch(viol, 1);
+}
+
+// primitive candidates of the body pairs ov (vertex boxes inflated by h, primitives
+// culled against the body boxes bbox): rows into vf / ee in deterministic order
+// (overlap pair, product, prim_a, prim_b), or canonical order when a chunk overflowed
+static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double h, const int2* ov, int n_ov,
+                           const double* bbox, DVec<int4>& vf, DVec<int4>& ee, int64_t& n_vf, int64_t& n_ee,
+                           int* ov_same, bool& ov_same_h) {
+  cudaStream_t st = s.stream;
+  Scene::Work& w = s.w;
+  PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
+  unsigned long long* counters = w.ull.p + 4;
+  int* unsorted = reinterpret_cast<int*>(w.ull.p + 8);
+  bool chunked = false;
+  if (vf.cap < 1024) vf.resize(1024);
+  if (ee.cap < 1024) ee.resize(1024);
+  unsigned long long* hc = reinterpret_cast<unsigned long long*>(s.h_pinned);
+  for (int attempt = 0; attempt < 3; ++attempt) {
+    CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
+    static bool attr = false;
+    const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
+    const size_t p2_smem = sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) +
+                           2 * sizeof(int) * 6 * (size_t)cap_list + sizeof(unsigned) * P2_HCAP;
+    const bool use2 = (s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1")) || s.comm.world > 1;
+    if (s.comm.world > 1 && !(s.max_v <= P2_VCAP && p2_smem <= 100 * 1024))
+      throw Error(ABD_ERR_ARG, "partitioned broad phase needs <= 256 vertices per body");
+    if (!attr) {
+      CK(cudaFuncSetAttribute((void*)k_prim_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM));
+      CK(cudaFuncSetAttribute((void*)k_prim_pairs2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      attr = true;
+    }
+    if (s.instrument) CK(cudaEventRecord(s.ev0, st));
+    if (use2) {
+      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 3);
+      w.tab.resize(3 * (size_t)n_ov);
+      if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_ov * sizeof(int2), st));
+      CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
+      CK(cudaMemsetAsync(w.ull.p + 11, 0, sizeof(unsigned long long), st));
+      static const bool no_groups = getenv("ABD_BP_NO_GROUPS") != nullptr;
+      GrpGeo gg{};
+      for (int k = 0; k < 3; ++k) {
+        gg.id[k] = s.grp_id[k].p;
+        gg.pk[k] = s.grp_pk[k].p;
+        gg.box[k] = s.grp_box[k].p;
+        gg.off[k] = s.grp_off[k].p;
+      }
+      const int ug = s.has_groups && !no_groups ? 1 : 0;
+      k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, ov, bbox, counters, (int64_t)vf.cap,
+                                                       (int64_t)ee.cap, vf.p, ee.p, cap_list, w.tab.p,
+                                                       unsorted, s.comm.rank, s.comm.world, w.ull.p + 11);
+    } else {
+      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
+      k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, ov, bbox, counters, (int64_t)vf.cap,
+                                                      (int64_t)ee.cap, vf.p, ee.p);
+    }
+    note_launch("k_prim_pairs");
+    if (s.instrument) CK(cudaEventRecord(s.ev1, st));
+    pack_to_host(st, hc, {{counters, 16, 0}, {unsorted, 4, 16}, {ov_same, 4, 24}});
+    SSYNC(st);
+    ov_same_h = *reinterpret_cast<int*>(hc + 3) != 0;
+    chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;
+    if (s.instrument) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+      Scene::KStat& k = s.kstat[3];
+      k.launches += 1;
+      k.units += n_ov;
+      k.ms += ms;
+      // SURVEY §8(d) K2: rest xyz, int32 edges/tris, q0+q1 per body, int4 candidate rows
+      k.bytes += 24.0 * (double)s.V + 8.0 * (double)s.E + 12.0 * (double)s.T + 192.0 * (double)s.B +
+                 16.0 * (double)(hc[0] + hc[1]);
+    }
+    if (hc[0] <= vf.cap && hc[1] <= ee.cap) break;
+    if (hc[0] > vf.cap) vf.resize(hc[0]);
+    if (hc[1] > ee.cap) ee.resize(hc[1]);
+  }
+  n_vf = (int64_t)hc[0];
+  n_ee = (int64_t)hc[1];
+  vf.n = n_vf;
+  ee.n = n_ee;
+  if (!chunked) {
+    // canonical (c0, c2, c1, c3) order by radix sort
+    sort_rows(s, vf, n_vf, bits_for(s.max_v - 1), bits_for(s.max_t - 1));
+    sort_rows(s, ee, n_ee, bits_for(s.max_e - 1), bits_for(s.max_e - 1));
+    return;
+  }
+  // Deterministic order without a global sort: (overlap pair, product, prim_a, prim_b).
+  // Each (pair, product) chunk was sorted in shared memory; chunks move to their
+  // prefix-sum offsets in pair order.  (abd_get_candidates returns the canonical order.)
+  w.cnt.resize(2 * n_ov + 1);
+  w.off.resize(2 * n_ov + 1);
+  w.va.resize(n_ov + 1);
+  w.vb.resize(n_ov + 1);
+  k_chunk_counts<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, w.tab.p, w.cnt.p, w.va.p);
+  note_launch("k_chunk_counts");
+  scan_exclusive_i32(s, w.cnt.p, w.off.p, 2 * n_ov);
+  scan_exclusive_i32(s, w.va.p, w.vb.p, n_ov);
+  w.rows_tmp.resize(std::max<int64_t>(n_vf, 1));
+  if (n_vf) {
+    k_chunk_move<<<grid_for(2 * n_ov * 32, 256), 256, 0, st>>>(n_ov, w.tab.p, 0, 2, w.off.p, vf.p, w.rows_tmp.p);
+    note_launch("k_chunk_move");
+    std::swap(vf.p, w.rows_tmp.p);
+    std::swap(vf.cap, w.rows_tmp.cap);
+    std::swap(vf.n, w.rows_tmp.n);
+    vf.n = n_vf;
+  }
+  w.rows_tmp.resize(std::max<int64_t>(n_ee, 1));
+  if (n_ee) {
+    k_chunk_move<<<grid_for(n_ov * 32, 256), 256, 0, st>>>(n_ov, w.tab.p, 2, 1, w.vb.p, ee.p, w.rows_tmp.p);
+    note_launch("k_chunk_move");
+    std::swap(ee.p, w.rows_tmp.p);
+    std::swap(ee.cap, w.rows_tmp.cap);
+    std::swap(ee.n, w.rows_tmp.n);
+    ee.n = n_ee;
+  }
+}
+
+static void prim_stage(Scene& s, const double* q0, const double* q1, double h, int n_ov, int* ov_same) {
+  cudaStream_t st = s.stream;
+  Cands& c = s.cands;
+  Scene::Work& w = s.w;
+  // off by default: in the late pile the Newton sweeps move by centimetres per iteration,
+  // so a margin that holds them makes the superset (and its rebuilds) costlier than
+  // the exact broad phase (measured: 11.2 -> 8.6 steps/s at 1% of the cell)
+  static const double pvl_frac = getenv("ABD_PVL_MARGIN") ? atof(getenv("ABD_PVL_MARGIN")) : 0.0;
+  const bool use_pvl = pvl_frac > 0.0 && w.vl_valid && w.vl_cell > 0.0 && s.has_groups;
+  bool same = false;
+  if (use_pvl) {
+    PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
+    int* info = reinterpret_cast<int*>(w.ull.p + 14);  // {n_vf, n_ee, viol, -}
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const bool valid = w.pvl_valid && w.pvl_gen == w.vl_gen && w.pvl_h == h;
+      if (!valid) {
+        // rebuild: candidates of the whole body superset for margin-inflated boxes
+        const double m = pvl_frac * w.vl_cell;
+        bool dummy = false;
+        int* no_same = reinterpret_cast<int*>(w.ull.p + 15);
+        CK(cudaMemsetAsync(no_same, 0, sizeof(int), st));
+        prim_pairs_run(s, q0, q1, h + m, w.vl_pairs.p, (int)w.vl_n, w.vl_box.p, w.pvl_vf, w.pvl_ee, w.pvl_nvf,
+                       w.pvl_nee, no_same, dummy);
+        w.pvl_q0.resize(12 * (size_t)s.B);
+        w.pvl_q1.resize(12 * (size_t)s.B);
+        CK(cudaMemcpyAsync(w.pvl_q0.p, q0, 12 * (size_t)s.B * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(w.pvl_q1.p, q1, 12 * (size_t)s.B * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        w.pvl_m = m;
+        w.pvl_h = h;
+        w.pvl_gen = w.vl_gen;
+        w.pvl_valid = true;
+      }
+      CK(cudaMemsetAsync(info, 0, 4 * sizeof(int), st));
+      k_pvl_check<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, q0, q1, w.pvl_q0.p, w.pvl_q1.p, s.body_rmax.p,
+                                                      0.5 * w.pvl_m, info + 2);
+      note_launch("k_pvl_check");
+      const int64_t ns = w.pvl_nvf + w.pvl_nee;
+      w.pvl_flags.resize(std::max<int64_t>(ns, 1));
+      if (ns)
+        k_pvl_flags<<<grid_for(ns, 128), 128, 0, st>>>(g, w.pvl_nvf, w.pvl_vf.p, w.pvl_nee, w.pvl_ee.p,
+                                                       w.pvl_flags.p);
+      note_launch("k_pvl_flags");
+      if ((int64_t)c.vf.cap < std::max<int64_t>(w.pvl_nvf, 1024)) c.vf.resize(std::max<int64_t>(w.pvl_nvf, 1024));
+      if ((int64_t)c.ee.cap < std::max<int64_t>(w.pvl_nee, 1024)) c.ee.resize(std::max<int64_t>(w.pvl_nee, 1024));
+      size_t b1 = 0, b2 = 0;
+      CK(cub::DeviceSelect::Flagged(nullptr, b1, w.pvl_vf.p, w.pvl_flags.p, c.vf.p, info, (int)w.pvl_nvf, st));
+      CK(cub::DeviceSelect::Flagged(nullptr, b2, w.pvl_ee.p, w.pvl_flags.p + w.pvl_nvf, c.ee.p, info + 1,
+                                    (int)w.pvl_nee, st));
+      s.tmp_bytes.resize(std::max<size_t>(std::max(b1, b2), 16));
+      if (w.pvl_nvf)
+        CK(cub::DeviceSelect::Flagged(s.tmp_bytes.p, b1, w.pvl_vf.p, w.pvl_flags.p, c.vf.p, info, (int)w.pvl_nvf,
+                                      st));
+      if (w.pvl_nee)
+        CK(cub::DeviceSelect::Flagged(s.tmp_bytes.p, b2, w.pvl_ee.p, w.pvl_flags.p + w.pvl_nvf, c.ee.p, info + 1,
+                                      (int)w.pvl_nee, st));
+      int* hi = reinterpret_cast<int*>(s.h_pinned);
+      pack_to_host(st, hi, {{info, 16, 0}, {ov_same, 4, 16}});
+      SSYNC(st);
+      if (hi[2] && valid) {
+        w.pvl_valid = false;  // a body left its margin: rebuild and filter again
+        continue;
+      }
+      same = hi[4] != 0;
+      c.n_vf = hi[0];
+      c.n_ee = hi[1];
+      c.vf.n = c.n_vf;
+      c.ee.n = c.n_ee;
+      c.ov_matches_pattern = same;
+      return;
+    }
+  }
+  prim_pairs_run(s, q0, q1, h, c.ov.p, n_ov, s.bbox.p, c.vf, c.ee, c.n_vf, c.n_ee, ov_same, same);
+  c.ov_matches_pattern = same;
+}
+
 void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   cudaStream_t st = s.stream;
   double h = 0.5 * d_hat;
@@ -1222,13 +1494,15 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     if (use_vl) {
       w.vl_n = n_g;
       w.vl_valid = true;
+      w.vl_gen += 1;
       if ((int64_t)c.ov.cap < std::max(n_g, 1)) c.ov.resize(std::max(n_g, 1));
       k_vl_filter<<<1, VL_THREADS, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, w.vl_n, w.vl_pairs.p, c.ov.p, vl_info);
       note_launch("k_vl_filter");
       int* hi = reinterpret_cast<int*>(s.h_pinned);
-      pack_to_host(st, hi, {{vl_info, 8, 0}});
+      pack_to_host(st, hi, {{vl_info, 8, 0}, {w.scal.p, 8, 8}});
       SSYNC(st);
       n_ov = hi[0];
+      w.vl_cell = reinterpret_cast<const double*>(hi)[1];
     } else {
       n_ov = n_g;
     }
@@ -1253,112 +1527,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   } else {
     CK(cudaMemsetAsync(ov_same, 0, sizeof(int), st));
   }
-  // primitive pairs
-  PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
-  unsigned long long* counters = w.ull.p + 4;
-  int* unsorted = reinterpret_cast<int*>(w.ull.p + 8);
-  bool chunked = false;
-  if (c.vf.cap < 1024) c.vf.resize(1024);
-  if (c.ee.cap < 1024) c.ee.resize(1024);
-  unsigned long long* hc = reinterpret_cast<unsigned long long*>(s.h_pinned);
-  for (int attempt = 0; attempt < 3; ++attempt) {
-    CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
-    static bool attr = false;
-    const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
-    const size_t p2_smem = sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) +
-                           2 * sizeof(int) * 6 * (size_t)cap_list + sizeof(unsigned) * P2_HCAP;
-    const bool use2 = (s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1")) || s.comm.world > 1;
-    if (s.comm.world > 1 && !(s.max_v <= P2_VCAP && p2_smem <= 100 * 1024))
-      throw Error(ABD_ERR_ARG, "partitioned broad phase needs <= 256 vertices per body");
-    if (!attr) {
-      CK(cudaFuncSetAttribute((void*)k_prim_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM));
-      CK(cudaFuncSetAttribute((void*)k_prim_pairs2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
-      attr = true;
-    }
-    if (s.instrument) CK(cudaEventRecord(s.ev0, st));
-    if (use2) {
-      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 3);
-      w.tab.resize(3 * (size_t)n_ov);
-      if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_ov * sizeof(int2), st));
-      CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
-      CK(cudaMemsetAsync(w.ull.p + 11, 0, sizeof(unsigned long long), st));
-      static const bool no_groups = getenv("ABD_BP_NO_GROUPS") != nullptr;
-      GrpGeo gg{};
-      for (int k = 0; k < 3; ++k) {
-        gg.id[k] = s.grp_id[k].p;
-        gg.pk[k] = s.grp_pk[k].p;
-        gg.box[k] = s.grp_box[k].p;
-        gg.off[k] = s.grp_off[k].p;
-      }
-      const int ug = s.has_groups && !no_groups ? 1 : 0;
-      k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
-                                                       (int64_t)c.ee.cap, c.vf.p, c.ee.p, cap_list, w.tab.p,
-                                                       unsorted, s.comm.rank, s.comm.world, w.ull.p + 11);
-    } else {
-      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
-      k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, c.ov.p, s.bbox.p, counters, (int64_t)c.vf.cap,
-                                                      (int64_t)c.ee.cap, c.vf.p, c.ee.p);
-    }
-    note_launch("k_prim_pairs");
-    if (s.instrument) CK(cudaEventRecord(s.ev1, st));
-    pack_to_host(st, hc, {{counters, 16, 0}, {unsorted, 4, 16}, {ov_same, 4, 24}});
-    SSYNC(st);
-    c.ov_matches_pattern = *reinterpret_cast<int*>(hc + 3) != 0;
-    chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;
-    if (s.instrument) {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
-      Scene::KStat& k = s.kstat[3];
-      k.launches += 1;
-      k.units += n_ov;
-      k.ms += ms;
-      // SURVEY §8(d) K2: rest xyz, int32 edges/tris, q0+q1 per body, int4 candidate rows
-      k.bytes += 24.0 * (double)s.V + 8.0 * (double)s.E + 12.0 * (double)s.T + 192.0 * (double)s.B +
-                 16.0 * (double)(hc[0] + hc[1]);
-    }
-    if (hc[0] <= c.vf.cap && hc[1] <= c.ee.cap) break;
-    if (hc[0] > c.vf.cap) c.vf.resize(hc[0]);
-    if (hc[1] > c.ee.cap) c.ee.resize(hc[1]);
-  }
-  c.n_vf = (int64_t)hc[0];
-  c.n_ee = (int64_t)hc[1];
-  c.vf.n = c.n_vf;
-  c.ee.n = c.n_ee;
-  if (!chunked) {
-    // canonical (c0, c2, c1, c3) order by radix sort
-    sort_rows(s, c.vf, c.n_vf, bits_for(s.max_v - 1), bits_for(s.max_t - 1));
-    sort_rows(s, c.ee, c.n_ee, bits_for(s.max_e - 1), bits_for(s.max_e - 1));
-    return;
-  }
-  // Deterministic order without a global sort: (overlap pair, product, prim_a, prim_b).
-  // Each (pair, product) chunk was sorted in shared memory; chunks move to their
-  // prefix-sum offsets in pair order.  (abd_get_candidates returns the canonical order.)
-  w.cnt.resize(2 * n_ov + 1);
-  w.off.resize(2 * n_ov + 1);
-  w.va.resize(n_ov + 1);
-  w.vb.resize(n_ov + 1);
-  k_chunk_counts<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, w.tab.p, w.cnt.p, w.va.p);
-  note_launch("k_chunk_counts");
-  scan_exclusive_i32(s, w.cnt.p, w.off.p, 2 * n_ov);
-  scan_exclusive_i32(s, w.va.p, w.vb.p, n_ov);
-  w.rows_tmp.resize(std::max<int64_t>(c.n_vf, 1));
-  if (c.n_vf) {
-    k_chunk_move<<<grid_for(2 * n_ov * 32, 256), 256, 0, st>>>(n_ov, w.tab.p, 0, 2, w.off.p, c.vf.p, w.rows_tmp.p);
-    note_launch("k_chunk_move");
-    std::swap(c.vf.p, w.rows_tmp.p);
-    std::swap(c.vf.cap, w.rows_tmp.cap);
-    std::swap(c.vf.n, w.rows_tmp.n);
-    c.vf.n = c.n_vf;
-  }
-  w.rows_tmp.resize(std::max<int64_t>(c.n_ee, 1));
-  if (c.n_ee) {
-    k_chunk_move<<<grid_for(n_ov * 32, 256), 256, 0, st>>>(n_ov, w.tab.p, 2, 1, w.vb.p, c.ee.p, w.rows_tmp.p);
-    note_launch("k_chunk_move");
-    std::swap(c.ee.p, w.rows_tmp.p);
-    std::swap(c.ee.cap, w.rows_tmp.cap);
-    std::swap(c.ee.n, w.rows_tmp.n);
-    c.ee.n = c.n_ee;
-  }
+  prim_stage(s, q0, q1, h, n_ov, ov_same);
 }
 
 }  // namespace abd

@@ -217,6 +217,7 @@ struct Scene {
   double* h_pinned = nullptr;  // small pinned staging for scalars
   DVec<double> vbox;  // V * 6 vertex boxes (broad phase)
   DVec<double> bbox;  // B * 6 body boxes
+  DVec<double> body_rmax;  // B * 3: max |rest coordinate| per axis (primitive Verlet-list bound)
 
   // persistent workspaces (grown, never shrunk: no cudaMalloc in steady state)
   struct Work {
@@ -252,6 +253,18 @@ struct Scene {
     DVec<int2> vl_pairs;
     int64_t vl_n = 0;
     bool vl_valid = false;
+    int vl_gen = 0;
+    double vl_cell = 0.0;
+    // primitive-pair superset ("primitive Verlet list"): the candidate rows of the body
+    // superset for vertex boxes inflated by pvl_m, built for the sweep [pvl_q0, pvl_q1];
+    // valid while every body stays within pvl_m / 2 of that sweep (k_pvl_check)
+    DVec<int4> pvl_vf, pvl_ee;
+    int64_t pvl_nvf = 0, pvl_nee = 0;
+    DVec<double> pvl_q0, pvl_q1;
+    DVec<int> pvl_flags;
+    double pvl_m = 0.0, pvl_h = -1.0;
+    int pvl_gen = -1;
+    bool pvl_valid = false;
     DVec<unsigned long long> ull;   // small atomics scratch (8 slots)
     DVec<double> grad0, diag0, neg, pinv, r, z, p, p2, Ap, part, scal, basis;
     DVec<double> lsred, lsscal;  // merged CCD + e0 + first-trial line-search reductions
