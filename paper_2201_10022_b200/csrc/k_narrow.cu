@@ -397,11 +397,13 @@ __device__ __forceinline__ double ccd_row(const SceneView& sv, int kind, int4 ro
   return accd_query(kind, x, dx, slack, 1.0, 512, cut, bad, &it);
 }
 
+// one hot query per warp (lane 0): the queries' branch paths and iteration counts
+// differ, so sharing a warp would serialise their divergent chains
 __global__ void k_ccd_hot(SceneView sv, int n, const int4* __restrict__ rows, const int* __restrict__ kind,
                           const double* __restrict__ q, const double* __restrict__ dq, double slack, double* t_out,
                           int* bad_out, int* it_out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n || (threadIdx.x & 31) != 0) return;
   bool bad = false;
   int it = 0;
   t_out[i] = ccd_row(sv, kind[i], rows[i], q, dq, slack, nullptr, bad, it);
@@ -851,8 +853,8 @@ void launch_ccd_hot(Scene& s, const double* q, const double* dq, double slack) {
   w.hot_it.resize(CCD_HOT_CAP);
   CK(cudaEventRecord(s.hot_fork_ev, s.stream));
   CK(cudaStreamWaitEvent(s.side2, s.hot_fork_ev, 0));
-  k_ccd_hot<<<1, CCD_HOT_CAP, 0, s.side2>>>(view(s), w.hot_n, w.hot_rows.p, w.hot_kind.p, q, dq, slack, w.hot_t.p,
-                                            w.hot_bad.p, w.hot_it.p);
+  k_ccd_hot<<<w.hot_n, 32, 0, s.side2>>>(view(s), w.hot_n, w.hot_rows.p, w.hot_kind.p, q, dq, slack, w.hot_t.p,
+                                         w.hot_bad.p, w.hot_it.p);
   note_launch("k_ccd_hot");
   CK(cudaEventRecord(s.hot_ev, s.side2));
   w.hot_pending = true;
