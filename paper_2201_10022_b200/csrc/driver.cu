@@ -503,8 +503,17 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   s.w.grad0.resize(std::max(12 * n, 1));
   s.w.diag0.resize(std::max(144 * n, 1));
   // body terms enter once (rank 0); pair terms are split across ranks
+  // body terms on the side stream: only the reduction consumes them, so the
+  // activity-scan sync below does not wait for them
+  bool body_forked = false;
   if (s.comm.rank == 0) {
+    CK(cudaEventRecord(s.fork_ev, s.stream));
+    CK(cudaStreamWaitEvent(s.side, s.fork_ev, 0));
+    std::swap(s.stream, s.side);
     launch_body_terms(s, q, qt, dt, s.w.grad0.p, s.w.diag0.p, nullptr, 1);
+    std::swap(s.stream, s.side);
+    CK(cudaEventRecord(s.join_ev, s.side));
+    body_forked = true;
   } else {
     s.w.grad0.zero(s.stream);
     s.w.diag0.zero(s.stream);
@@ -518,6 +527,7 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   contact_blocks(s, q, kappa, dh, 1, /*mark=*/true);
   HMARK();
   append_friction_blocks(s, q, dt, eps_v, 1);
+  if (body_forked) CK(cudaStreamWaitEvent(s.stream, s.join_ev, 0));
   reduce_system(s, s.w.diag0.p, s.w.grad0.p);
   HMARK();
   if (s.comm.world > 1) {

@@ -1074,57 +1074,6 @@ __global__ void k_inflate_boxes(int B, const double* __restrict__ bbox, const do
   }
 }
 
-// one CTA: (1) every exact swept box inside its inflated box? (2) the superset pairs
-// whose exact boxes overlap, compacted in order (the superset is canonical, so is the
-// result).  out_info = {count, violation}.
-constexpr int VL_THREADS = 1024, VL_ITEMS = 8;
-__global__ void __launch_bounds__(VL_THREADS) k_vl_filter(int B, const double* __restrict__ bbox,
-                                                          const double* __restrict__ vl_box, int64_t n_sup,
-                                                          const int2* __restrict__ sup, int2* out, int* out_info) {
-  typedef cub::BlockScan<int, VL_THREADS> Scan;
-  __shared__ typename Scan::TempStorage temp;
-  __shared__ int viol, base;
-  if (threadIdx.x == 0) {
-    viol = 0;
-    base = 0;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < B; b += VL_THREADS) {
-    const double* x = bbox + 6 * b;
-    const double* y = vl_box + 6 * b;
-    if (!(x[0] >= y[0] && x[1] >= y[1] && x[2] >= y[2] && x[3] <= y[3] && x[4] <= y[4] && x[5] <= y[5])) viol = 1;
-  }
-  for (int64_t c0 = 0; c0 < n_sup; c0 += (int64_t)VL_THREADS * VL_ITEMS) {
-    const int64_t i0 = c0 + (int64_t)threadIdx.x * VL_ITEMS;
-    bool f[VL_ITEMS];
-    int2 pr[VL_ITEMS];
-    int cnt = 0;
-#pragma unroll
-    for (int k = 0; k < VL_ITEMS; ++k) {
-      const int64_t i = i0 + k;
-      f[k] = false;
-      if (i < n_sup) {
-        pr[k] = sup[i];
-        f[k] = box_overlap(bbox + 6 * pr[k].x, bbox + 6 * pr[k].y);
-      }
-      cnt += f[k];
-    }
-    int off = 0, tot = 0;
-    Scan(temp).ExclusiveSum(cnt, off, tot);
-    const int b0 = base;
-#pragma unroll
-    for (int k = 0; k < VL_ITEMS; ++k)
-      if (f[k]) out[b0 + off++] = pr[k];
-    __syncthreads();
-    if (threadIdx.x == 0) base = b0 + tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    out_info[0] = base;
-    out_info[1] = viol;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // primitive Verlet list (Work::pvl_*)
 // exact swept boxes of the candidate rows' primitives overlap? (contact.py:222-229 boxes)
@@ -1397,6 +1346,41 @@ static void prim_stage(Scene& s, const double* q0, const double* q1, double h, i
   c.ov_matches_pattern = same;
 }
 
+__global__ void k_vl_contain(int B, const double* __restrict__ bbox, const double* __restrict__ vl_box, int* viol) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double* x = bbox + 6 * b;
+  const double* y = vl_box + 6 * b;
+  if (!(x[0] >= y[0] && x[1] >= y[1] && x[2] >= y[2] && x[3] <= y[3] && x[4] <= y[4] && x[5] <= y[5]))
+    atomicExch(viol, 1);
+}
+
+__global__ void k_vl_flags(int64_t n, const int2* __restrict__ sup, const double* __restrict__ bbox, int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 pr = sup[i];
+  flags[i] = box_overlap(bbox + 6 * pr.x, bbox + 6 * pr.y);
+}
+
+// the Verlet-list filter over the whole GPU: containment flag, overlap flags and an
+// ordered (stable) compaction into c.ov; info = {count, violation} on the device
+static void vl_filter(Scene& s, int* info) {
+  cudaStream_t st = s.stream;
+  Scene::Work& w = s.w;
+  Cands& c = s.cands;
+  CK(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
+  k_vl_contain<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, info + 1);
+  note_launch("k_vl_contain");
+  if (w.vl_n == 0) return;
+  w.flags.resize(w.vl_n);
+  k_vl_flags<<<grid_for(w.vl_n, 256), 256, 0, st>>>(w.vl_n, w.vl_pairs.p, s.bbox.p, w.flags.p);
+  note_launch("k_vl_flags");
+  size_t bytes = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, bytes, w.vl_pairs.p, w.flags.p, c.ov.p, info, (int)w.vl_n, st));
+  s.tmp_bytes.resize(std::max<size_t>(bytes, 16));
+  CK(cub::DeviceSelect::Flagged(s.tmp_bytes.p, bytes, w.vl_pairs.p, w.flags.p, c.ov.p, info, (int)w.vl_n, st));
+}
+
 void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   cudaStream_t st = s.stream;
   double h = 0.5 * d_hat;
@@ -1416,8 +1400,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   bool have = false;
   if (use_vl && w.vl_valid) {
     if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
-    k_vl_filter<<<1, VL_THREADS, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, w.vl_n, w.vl_pairs.p, c.ov.p, vl_info);
-    note_launch("k_vl_filter");
+    vl_filter(s, vl_info);
     int* hi = reinterpret_cast<int*>(s.h_pinned);
     pack_to_host(st, hi, {{vl_info, 8, 0}});
     SSYNC(st);
@@ -1496,8 +1479,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
       w.vl_valid = true;
       w.vl_gen += 1;
       if ((int64_t)c.ov.cap < std::max(n_g, 1)) c.ov.resize(std::max(n_g, 1));
-      k_vl_filter<<<1, VL_THREADS, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, w.vl_n, w.vl_pairs.p, c.ov.p, vl_info);
-      note_launch("k_vl_filter");
+      vl_filter(s, vl_info);
       int* hi = reinterpret_cast<int*>(s.h_pinned);
       pack_to_host(st, hi, {{vl_info, 8, 0}, {w.scal.p, 8, 8}});
       SSYNC(st);
