@@ -93,7 +93,7 @@ __global__ void k_csr_positions(int n, int64_t n_off, const uint64_t* __restrict
 // val = pair << 2 | which (0: haa/ga, 1: hbb/gb, 2: hab, 3: hab^T)
 __global__ void k_contribs(int64_t np, const int2* __restrict__ bodies, const int* __restrict__ slot,
                            const int* __restrict__ diag_pos, int64_t n_off, const int2* __restrict__ upper_keys,
-                           const int* __restrict__ upper_pos, uint32_t* keys, int* vals) {
+                           const int* __restrict__ upper_pos, uint32_t* keys, int* vals, int* cnt) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= np) return;
   int2 b = bodies[p];
@@ -127,6 +127,22 @@ __global__ void k_contribs(int64_t np, const int2* __restrict__ bodies, const in
   vals[3 * p + 1] = (int)(p << 2) | 1;
   keys[3 * p + 2] = k2;
   vals[3 * p + 2] = (int)(p << 2) | v2;
+  if (cnt) {
+    if (k0 != 0xffffffffu) atomicAdd(cnt + k0, 1);
+    if (k1 != 0xffffffffu) atomicAdd(cnt + k1, 1);
+    if (k2 != 0xffffffffu) atomicAdd(cnt + k2, 1);
+  }
+}
+
+// contributions into their block segments (unordered within a segment; the
+// reduction orders each segment by value = pair-major, as the stable sort did)
+__global__ void k_contrib_fill(int64_t m, const uint32_t* __restrict__ keys, const int* __restrict__ vals,
+                               const int* __restrict__ seg, int* fill, int* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint32_t k = keys[i];
+  if (k == 0xffffffffu) return;
+  out[seg[k] + atomicAdd(fill + k, 1)] = vals[i];
 }
 
 __global__ void k_seg_bounds(int64_t m, const uint32_t* __restrict__ keys, int64_t nnzb, int* start, int* end) {
@@ -148,11 +164,12 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
                                                                  const int* __restrict__ col,
                                                                  const int* __restrict__ seg_start,
                                                                  const int* __restrict__ seg_end,
-                                                                 const int* __restrict__ cvals,
+                                                                 const int* cvals,
                                                                  const double* __restrict__ pblk,
                                                                  const double* __restrict__ diag0,
                                                                  const double* __restrict__ grad0, double* val,
-                                                                 double* grad, const int* __restrict__ row_of) {
+                                                                 double* grad, const int* __restrict__ row_of,
+                                                                 int* sorted_out) {
   __shared__ double srec[RB_WARPS][RB_PER_LANE * 32];
   int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -171,6 +188,17 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
   }
   if (is_diag && lane < 12) gacc = grad0[12 * (int64_t)r + lane];
   const int s0 = seg_start[w], s1 = seg_end[w];
+  if (sorted_out) {
+    // rank sort of the segment by value (unique): pair-major summation order
+    for (int i = s0 + lane; i < s1; i += 32) {
+      const int vi = cvals[i];
+      int r = 0;
+      for (int j = s0; j < s1; ++j) r += cvals[j] < vi;
+      sorted_out[s0 + r] = vi;
+    }
+    __syncwarp();
+    cvals = sorted_out;
+  }
   double* sr = srec[wid];
   double nxt[RB_PER_LANE];
   int vnext = 0;
@@ -343,17 +371,23 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
   DVec<int>& seg_s = s.w.seg_s;
   DVec<int>& seg_e = s.w.seg_e;
   DVec<int>& row_of = s.w.row_of;
-  seg_s.resize(H.nnzb);
-  seg_e.resize(H.nnzb);
+  static const bool sort_path = getenv("ABD_CONTRIB_SORT") != nullptr;
+  seg_s.resize(H.nnzb + 1);
+  seg_e.resize(H.nnzb + 1);
   row_of.resize(H.nnzb);
-  seg_s.zero(st);
-  seg_e.zero(st);
   k_row_of<<<grid_for(n, 128), 128, 0, st>>>(n, H.row_ptr.p, row_of.p);
   note_launch("k_row_of");
   const int* cv = va.p;
-  if (np > 0) {
+  const int* sb = seg_s.p;
+  const int* se = seg_e.p;
+  int* sorted_out = nullptr;
+  if (sort_path || np == 0) {
+    seg_s.zero(st);
+    seg_e.zero(st);
+  }
+  if (np > 0 && sort_path) {
     k_contribs<<<grid_for(np, 256), 256, 0, st>>>(np, s.pblk.bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
-                                                  H.upper_keys.p, H.upper_pos.p, ka.p, va.p);
+                                                  H.upper_keys.p, H.upper_pos.p, ka.p, va.p, nullptr);
     note_launch("k_contribs");
     int kb_bits = bits_for(H.nnzb) + 1;  // the 0xffffffff "absent" key still sorts last
     if (kb_bits > 32) kb_bits = 32;
@@ -362,11 +396,28 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
     k_seg_bounds<<<grid_for(m, 256), 256, 0, st>>>(m, alt ? kb.p : ka.p, H.nnzb, seg_s.p, seg_e.p);
     note_launch("k_seg_bounds");
     cv = alt ? vb.p : va.p;
+  } else if (np > 0) {
+    // counting placement: per-block counts, exclusive scan (segment starts), fill;
+    // the reduction rank-sorts each (short) segment
+    DVec<int>& cnt = s.w.cnt;
+    cnt.resize(H.nnzb + 1);
+    cnt.zero(st);
+    k_contribs<<<grid_for(np, 256), 256, 0, st>>>(np, s.pblk.bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
+                                                  H.upper_keys.p, H.upper_pos.p, ka.p, va.p, cnt.p);
+    note_launch("k_contribs");
+    scan_exclusive_i32(s, cnt.p, seg_s.p, H.nnzb + 1);
+    cnt.zero(st);
+    k_contrib_fill<<<grid_for(m, 256), 256, 0, st>>>(m, ka.p, va.p, seg_s.p, cnt.p, vb.p);
+    note_launch("k_contrib_fill");
+    cv = vb.p;
+    sorted_out = va.p;  // keys/vals of the contributions are dead after the fill
+    sb = seg_s.p;
+    se = seg_s.p + 1;
   }
   s.grad.resize(12 * (int64_t)n);
-  k_reduce_blocks<<<grid_for(H.nnzb * 32, 32 * RB_WARPS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, seg_s.p, seg_e.p, cv,
+  k_reduce_blocks<<<grid_for(H.nnzb * 32, 32 * RB_WARPS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, sb, se, cv,
                                                               s.pblk.blk.p, diag0, grad0, H.val.p, s.grad.p,
-                                                              row_of.p);
+                                                              row_of.p, sorted_out);
   note_launch("k_reduce_blocks");
 }
 
