@@ -235,15 +235,7 @@ static void energy_terms(Scene& s, const double* q, const double* qt, double dt,
   s.w.err.resize(2);
   s.w.err.zero(s.stream);
   s.w.scal.resize(4);
-  if (s.comm.rank == 0) launch_body_terms(s, q, qt, dt, nullptr, nullptr, s.red.p, 0);
-  else CK(cudaMemsetAsync(s.red.p, 0, RED_BLOCKS * sizeof(double), s.stream));
-  launch_contact_energy(s, KIND_VF, q, kappa, dh, s.red.p + RED_BLOCKS, s.w.err.p);
-  launch_contact_energy(s, KIND_EE, q, kappa, dh, s.red.p + 2 * RED_BLOCKS, s.w.err.p);
-  if (s.fric.n)
-    launch_friction(s.stream, s.fric.n, s.fric.bodies.p, s.fric.rec.p, s.fric.mu, q, s.dyn.p, dt, eps_v, 0,
-                    s.red.p + 3 * RED_BLOCKS, nullptr, nullptr, nullptr);
-  else
-    CK(cudaMemsetAsync(s.red.p + 3 * RED_BLOCKS, 0, RED_BLOCKS * sizeof(double), s.stream));
+  launch_energy_all(s, q, qt, dt, kappa, dh, eps_v, s.red.p, s.w.err.p);
   reduce_fixed_multi(s.stream, s.red.p, RED_BLOCKS, 4, s.w.scal.p);
   comm_allreduce(s, s.w.scal.p, 4, 0, 0);
   comm_allreduce(s, s.w.err.p, 1, 1, 2);
@@ -297,15 +289,7 @@ double ip_value(Scene& s, const double* q, const double* qt, double dt, double k
 // fixed-order sums into scal4[0..3], barrier-domain flag into err
 static void launch_energy(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh,
                           double eps_v, double* red4, double* scal4, int* err) {
-  if (s.comm.rank == 0) launch_body_terms(s, q, qt, dt, nullptr, nullptr, red4, 0);
-  else CK(cudaMemsetAsync(red4, 0, RED_BLOCKS * sizeof(double), s.stream));
-  launch_contact_energy(s, KIND_VF, q, kappa, dh, red4 + RED_BLOCKS, err);
-  launch_contact_energy(s, KIND_EE, q, kappa, dh, red4 + 2 * RED_BLOCKS, err);
-  if (s.fric.n)
-    launch_friction(s.stream, s.fric.n, s.fric.bodies.p, s.fric.rec.p, s.fric.mu, q, s.dyn.p, dt, eps_v, 0,
-                    red4 + 3 * RED_BLOCKS, nullptr, nullptr, nullptr);
-  else
-    CK(cudaMemsetAsync(red4 + 3 * RED_BLOCKS, 0, RED_BLOCKS * sizeof(double), s.stream));
+  launch_energy_all(s, q, qt, dt, kappa, dh, eps_v, red4, err);
   reduce_fixed_multi(s.stream, red4, RED_BLOCKS, 4, scal4);
 }
 

@@ -248,12 +248,14 @@ __global__ void k_scatter_active(int64_t n, const int* __restrict__ flags, const
   if (i < n && flags[i]) act[pos[i]] = (int)i;
 }
 
-__global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
-                                 const double* __restrict__ q, double kappa, double dh, double* partials, int* err) {
+__device__ __forceinline__ void contact_energy_part(const SceneView& sv, int kind, int64_t n,
+                                                    const int4* __restrict__ rows, const double* __restrict__ q,
+                                                    double kappa, double dh, double* partials, int* err, int bx,
+                                                    int nbx) {
   __shared__ double sh[RED_THREADS];
   double acc = 0.0;
   double dh2 = dh * dh;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = bx * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)nbx * blockDim.x) {
     PairIds ids = pair_ids(sv, kind, rows[i]);
     V3 z[4], xb[4];
     pair_points(sv, ids, q, z, xb);
@@ -270,7 +272,12 @@ __global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* 
     if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+  if (threadIdx.x == 0) partials[bx] = sh[0];
+}
+
+__global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
+                                 const double* __restrict__ q, double kappa, double dh, double* partials, int* err) {
+  contact_energy_part(sv, kind, n, rows, q, kappa, dh, partials, err, blockIdx.x, gridDim.x);
 }
 
 __global__ void k_cand_min_d2(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
@@ -613,17 +620,15 @@ __global__ void __launch_bounds__(32 * BT_WARPS) k_body_derivs(int n_dyn, const 
 
 // K1 energy only (line-search trials), one warp per dynamic slot: coalesced reads
 // of the 12x12 mass block, fixed-order warp and block sums
-__global__ void __launch_bounds__(RED_THREADS) k_body_energy_w(int n_dyn, const int* __restrict__ dyn_body,
-                                                               const double* __restrict__ mass,
-                                                               const double* __restrict__ stiff,
-                                                               const double* __restrict__ q,
-                                                               const double* __restrict__ qt, double dt,
-                                                               double* partials) {
+__device__ __forceinline__ void body_energy_part(int n_dyn, const int* __restrict__ dyn_body,
+                                                 const double* __restrict__ mass, const double* __restrict__ stiff,
+                                                 const double* __restrict__ q, const double* __restrict__ qt,
+                                                 double dt, double* partials, int bx, int nbx) {
   __shared__ double sh[RED_THREADS / 32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = gridDim.x * (RED_THREADS / 32);
+  const int nw = nbx * (RED_THREADS / 32);
   double acc = 0.0;  // lane 0: this warp's bodies in slot order
-  for (int sidx = blockIdx.x * (RED_THREADS / 32) + w; sidx < n_dyn; sidx += nw) {
+  for (int sidx = bx * (RED_THREADS / 32) + w; sidx < n_dyn; sidx += nw) {
     const int b = dyn_body[sidx];
     const double* M = mass + 144 * (int64_t)b;
     const double* qb = q + 12 * (int64_t)b;
@@ -647,8 +652,93 @@ __global__ void __launch_bounds__(RED_THREADS) k_body_energy_w(int n_dyn, const 
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int k2 = 0; k2 < RED_THREADS / 32; ++k2) t += sh[k2];
-    partials[blockIdx.x] = t;
+    partials[bx] = t;
   }
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_body_energy_w(int n_dyn, const int* __restrict__ dyn_body,
+                                                               const double* __restrict__ mass,
+                                                               const double* __restrict__ stiff,
+                                                               const double* __restrict__ q,
+                                                               const double* __restrict__ qt, double dt,
+                                                               double* partials) {
+  body_energy_part(n_dyn, dyn_body, mass, stiff, q, qt, dt, partials, blockIdx.x, gridDim.x);
+}
+
+// K6 in one launch: blocks [0, R) body terms, [R, 2R) contact VF, [2R, 3R) contact
+// EE, [3R, 4R) friction (R = RED_BLOCKS).  Every part keeps its own fixed grid of R
+// blocks, so the partials -- and their fixed-order sums -- are bitwise those of the
+// separate kernels, while the parts run side by side.
+struct EnergyArgs {
+  SceneView sv;
+  const double *q, *qt, *mass, *stiff;
+  const int* dyn_body;
+  int n_dyn, with_body;
+  double dt, kappa, dh, mu, eh;
+  int64_t n_vf, n_ee, n_f;
+  const int4 *vf, *ee;
+  const int2* fb;
+  const double* frec;
+  double* red4;
+  int* err;
+};
+
+__global__ void __launch_bounds__(RED_THREADS) k_energy_all(EnergyArgs a) {
+  const int part = blockIdx.x / RED_BLOCKS, bx = blockIdx.x % RED_BLOCKS;
+  double* out = a.red4 + part * RED_BLOCKS;
+  if (part == 0) {
+    if (a.with_body) body_energy_part(a.n_dyn, a.dyn_body, a.mass, a.stiff, a.q, a.qt, a.dt, out, bx, RED_BLOCKS);
+    else if (threadIdx.x == 0) out[bx] = 0.0;
+  } else if (part < 3) {
+    const int kind = part == 1 ? KIND_VF : KIND_EE;
+    contact_energy_part(a.sv, kind, kind == KIND_VF ? a.n_vf : a.n_ee, kind == KIND_VF ? a.vf : a.ee, a.q, a.kappa,
+                        a.dh, out, a.err, bx, RED_BLOCKS);
+  } else {
+    __shared__ double sh[RED_THREADS];
+    double acc = 0.0;
+    for (int64_t i = bx * (int64_t)blockDim.x + threadIdx.x; i < a.n_f; i += (int64_t)RED_BLOCKS * blockDim.x) {
+      const int2 b = a.fb[i];
+      const double* r = a.frec + i * FRIC_STRIDE;
+      FricEval e = friction_eval(r, a.q + 12 * b.x, a.q + 12 * b.y, a.eh);
+      acc += a.mu * r[50] * e.f0;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[bx] = sh[0];
+  }
+}
+
+void launch_energy_all(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh,
+                       double eps_v, double* red4, int* err) {
+  EnergyArgs a;
+  a.sv = view(s);
+  a.q = q;
+  a.qt = qt;
+  a.mass = s.mass.p;
+  a.stiff = s.stiff.p;
+  a.dyn_body = s.dyn_body.p;
+  a.n_dyn = s.n_dyn;
+  a.with_body = s.comm.rank == 0 ? 1 : 0;
+  a.dt = dt;
+  a.kappa = kappa;
+  a.dh = dh;
+  a.mu = s.fric.mu;
+  a.eh = eps_v * dt;
+  a.n_vf = s.cands.n_vf;
+  a.n_ee = s.cands.n_ee;
+  a.n_f = s.fric.n;
+  a.vf = s.cands.vf.p;
+  a.ee = s.cands.ee.p;
+  a.fb = s.fric.bodies.p;
+  a.frec = s.fric.rec.p;
+  a.red4 = red4;
+  a.err = err;
+  k_energy_all<<<4 * RED_BLOCKS, RED_THREADS, 0, s.stream>>>(a);
+  note_launch("k_energy_all");
 }
 
 // K1 energy only (line-search trials): 0.5 dq^T M dq + dt^2 V_perp per dynamic slot

@@ -79,6 +79,9 @@ struct HotCcd {
   int slow_cap, slow_it;
 };
 void launch_ccd_hot(Scene& s, const double* q, const double* dq, double slack);
+// K6 (body | contact VF | contact EE | friction partials, 4 x RED_BLOCKS) in one launch
+void launch_energy_all(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh,
+                       double eps_v, double* red4, int* err);
 void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, unsigned long long* tmin,
                      int* err, bool track = false);
 void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack,
