@@ -124,9 +124,7 @@ static int active_scan(Scene& s, const double* q, double dh) {
   w.err.resize(2);
   w.err.zero(s.stream);
   double dh2 = dh * dh;
-  launch_pair_flags(s, KIND_VF, q, dh2, w.flags.p, w.err.p);
-  launch_pair_flags(s, KIND_EE, q, dh2, w.flags.p + n_vf, w.err.p);
-  CK(cudaMemsetAsync(w.flags.p + n, 0, sizeof(int), s.stream));
+  launch_pair_flags_both(s, q, dh2, w.flags.p, w.err.p);
   scan_exclusive_i32(s, w.flags.p, w.pos.p, n + 1);
   // compacted active list: act[pos[i]] = i (VF slots first, then EE)
   w.act.resize(n + 1);
@@ -151,8 +149,20 @@ int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int p
   s.pblk.n = total;
   EventTimer tm(s, 1);
   (void)n_vf;
+  // VF pairs on side2 beside the EE pairs (+ mollified EE) on the main stream
+  const bool fork_vf = s.w.n_act_vf > 0 && total - s.w.n_act_vf > 0;
+  if (fork_vf) {
+    CK(cudaEventRecord(s.pb_fork_ev, s.stream));
+    CK(cudaStreamWaitEvent(s.side2, s.pb_fork_ev, 0));
+    std::swap(s.stream, s.side2);
+  }
   launch_pair_blocks_act(s, KIND_VF, q, kappa, dh, project, s.w.act.p, 0, s.w.n_act_vf);
+  if (fork_vf) {
+    std::swap(s.stream, s.side2);
+    CK(cudaEventRecord(s.pb_ev, s.side2));
+  }
   launch_pair_blocks_act(s, KIND_EE, q, kappa, dh, project, s.w.act.p, s.w.n_act_vf, total - s.w.n_act_vf);
+  if (fork_vf) CK(cudaStreamWaitEvent(s.stream, s.pb_ev, 0));
   tm.stop();
   // algorithmic bytes (scene form): candidate record 16 B + 4 rest points 96 B
   // (+ eps 8 B for EE) per candidate, one compact PB_STRIDE record written per active pair

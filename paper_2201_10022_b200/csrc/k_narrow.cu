@@ -80,6 +80,34 @@ __global__ void k_pair_flags(SceneView sv, int kind, int64_t n, const int4* __re
   if (on && !(d2 > 0.0)) atomicExch(err, 1);
 }
 
+// activity flags over VF then EE candidates in one launch; flags[n] = 0 (the scan's tail)
+__global__ void k_pair_flags_both(SceneView sv, int64_t n_vf, const int4* __restrict__ vf, int64_t n_ee,
+                                  const int4* __restrict__ ee, const double* __restrict__ q, double dh2, int* flags,
+                                  int* err) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n = n_vf + n_ee;
+  if (i > n) return;
+  if (i == n) {
+    flags[n] = 0;
+    return;
+  }
+  const int kind = i < n_vf ? KIND_VF : KIND_EE;
+  PairIds ids = pair_ids(sv, kind, kind == KIND_VF ? vf[i] : ee[i - n_vf]);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  double d2 = pair_d2(kind, z);
+  int on = d2 < dh2;
+  flags[i] = on;
+  if (on && !(d2 > 0.0)) atomicExch(err, 1);
+}
+
+void launch_pair_flags_both(Scene& s, const double* q, double dh2, int* flags, int* err) {
+  const int64_t n = s.cands.n_vf + s.cands.n_ee;
+  k_pair_flags_both<<<grid_for(n + 1, 128), 128, 0, s.stream>>>(view(s), s.cands.n_vf, s.cands.vf.p, s.cands.n_ee,
+                                                                s.cands.ee.p, q, dh2, flags, err);
+  note_launch("k_pair_flags");
+}
+
 // K3 first pass: one thread per candidate, active ones write g24 | haa | hbb | hab
 // same over the compacted active list: full warps instead of ~1/4 active lanes;
 // specialised per kind so the VF kernel carries none of the mollified-EE state.

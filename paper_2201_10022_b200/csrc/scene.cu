@@ -45,6 +45,8 @@ Scene::Scene() {
   CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&hot_fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&hot_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&pb_fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&pb_ev, cudaEventDisableTiming));
   CK(cudaMallocHost(&h_pinned, 64 * sizeof(double)));
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
@@ -66,6 +68,8 @@ Scene::~Scene() {
   if (side2) cudaStreamDestroy(side2);
   if (hot_fork_ev) cudaEventDestroy(hot_fork_ev);
   if (hot_ev) cudaEventDestroy(hot_ev);
+  if (pb_fork_ev) cudaEventDestroy(pb_fork_ev);
+  if (pb_ev) cudaEventDestroy(pb_ev);
   if (h_pinned) cudaFreeHost(h_pinned);
   for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
     if (e) cudaEventDestroy(e);

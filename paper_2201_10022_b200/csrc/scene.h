@@ -170,6 +170,7 @@ struct Scene {
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaStream_t side2 = nullptr;  // early ACCD of the hot queries (overlaps the broad phase)
   cudaEvent_t hot_fork_ev = nullptr, hot_ev = nullptr;
+  cudaEvent_t pb_fork_ev = nullptr, pb_ev = nullptr;  // VF pair blocks on side2
   int num_sms = 148;
 
   // geometry (immutable after create)
