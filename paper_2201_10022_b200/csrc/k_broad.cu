@@ -431,7 +431,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
     k_prim_pairs2(PrimGeo g, GrpGeo gr, int use_groups, int64_t n_ov, const int2* __restrict__ ov,
                   const double* __restrict__ bbox, unsigned long long* counters, int64_t cap_vf, int64_t cap_ee,
                   int4* out_vf, int4* out_ee, int cap_list, int2* tab, int* unsorted, int rank, int world,
-                  unsigned long long* work) {
+                  unsigned long long* work, const int* n_ov_dev) {
+  if (n_ov_dev) n_ov = *n_ov_dev;  // deferred count (Verlet-list filter result, no host sync)
   extern __shared__ double p2_sm[];
   double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
   double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
@@ -715,8 +716,9 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
 }
 
 __global__ void k_ov_in_pattern(int64_t n, const int2* __restrict__ ov, const int* __restrict__ slot, int64_t n_off,
-                                const int2* __restrict__ keys, int* inside) {
+                                const int2* __restrict__ keys, int* inside, const int* n_dev) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (n_dev) n = *n_dev;
   if (i >= n) return;
   const int sa = slot[ov[i].x], sb = slot[ov[i].y];
   if (sa < 0 || sb < 0 || sa == sb) return;  // no block for pairs with a kinematic body
@@ -1159,9 +1161,12 @@ __global__ void k_pvl_check(int B, const double* __restrict__ q0, const double* 
 // primitive candidates of the body pairs ov (vertex boxes inflated by h, primitives
 // culled against the body boxes bbox): rows into vf / ee in deterministic order
 // (overlap pair, product, prim_a, prim_b), or canonical order when a chunk overflowed
-static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double h, const int2* ov, int n_ov,
+static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double h, const int2* ov, int& n_ov,
                            const double* bbox, DVec<int4>& vf, DVec<int4>& ee, int64_t& n_vf, int64_t& n_ee,
-                           int* ov_same, bool& ov_same_h) {
+                           int* ov_same, bool& ov_same_h, const int* n_ov_dev = nullptr, int* viol_h = nullptr) {
+  // n_ov_dev: the pair count is on the device (n_ov is then only a capacity); it is
+  // read back with the candidate counts, together with the Verlet-list violation flag
+  const int n_cap = n_ov;
   cudaStream_t st = s.stream;
   Scene::Work& w = s.w;
   PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
@@ -1187,9 +1192,9 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
     }
     if (s.instrument) CK(cudaEventRecord(s.ev0, st));
     if (use2) {
-      int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms * 3);
-      w.tab.resize(3 * (size_t)n_ov);
-      if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_ov * sizeof(int2), st));
+      int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n_cap, (int64_t)s.num_sms * 3));
+      w.tab.resize(3 * (size_t)std::max(n_cap, 1));
+      if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_cap * sizeof(int2), st));
       CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
       CK(cudaMemsetAsync(w.ull.p + 11, 0, sizeof(unsigned long long), st));
       static const bool no_groups = getenv("ABD_BP_NO_GROUPS") != nullptr;
@@ -1203,7 +1208,7 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
       const int ug = s.has_groups && !no_groups ? 1 : 0;
       k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, ov, bbox, counters, (int64_t)vf.cap,
                                                        (int64_t)ee.cap, vf.p, ee.p, cap_list, w.tab.p,
-                                                       unsorted, s.comm.rank, s.comm.world, w.ull.p + 11);
+                                                       unsorted, s.comm.rank, s.comm.world, w.ull.p + 11, n_ov_dev);
     } else {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
       k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, ov, bbox, counters, (int64_t)vf.cap,
@@ -1211,9 +1216,17 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
     }
     note_launch("k_prim_pairs");
     if (s.instrument) CK(cudaEventRecord(s.ev1, st));
-    pack_to_host(st, hc, {{counters, 16, 0}, {unsorted, 4, 16}, {ov_same, 4, 24}});
+    if (n_ov_dev)
+      pack_to_host(st, hc, {{counters, 16, 0}, {unsorted, 4, 16}, {ov_same, 4, 24}, {n_ov_dev, 8, 32}});
+    else
+      pack_to_host(st, hc, {{counters, 16, 0}, {unsorted, 4, 16}, {ov_same, 4, 24}});
     SSYNC(st);
     ov_same_h = *reinterpret_cast<int*>(hc + 3) != 0;
+    if (n_ov_dev) {
+      n_ov = reinterpret_cast<const int*>(hc + 4)[0];
+      if (viol_h) *viol_h = reinterpret_cast<const int*>(hc + 4)[1];
+      if (viol_h && *viol_h) return;  // the caller rebuilds the Verlet list and starts over
+    }
     chunked = use2 && *reinterpret_cast<int*>(hc + 2) == 0;
     if (s.instrument) {
       float ms = 0.f;
@@ -1234,6 +1247,7 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
   n_ee = (int64_t)hc[1];
   vf.n = n_vf;
   ee.n = n_ee;
+  if (n_ov == 0) return;
   if (!chunked) {
     // canonical (c0, c2, c1, c3) order by radix sort
     sort_rows(s, vf, n_vf, bits_for(s.max_v - 1), bits_for(s.max_t - 1));
@@ -1271,7 +1285,8 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
   }
 }
 
-static void prim_stage(Scene& s, const double* q0, const double* q1, double h, int n_ov, int* ov_same) {
+static void prim_stage(Scene& s, const double* q0, const double* q1, double h, int& n_ov, int* ov_same,
+                       const int* n_ov_dev = nullptr, int* viol_h = nullptr) {
   cudaStream_t st = s.stream;
   Cands& c = s.cands;
   Scene::Work& w = s.w;
@@ -1279,7 +1294,7 @@ static void prim_stage(Scene& s, const double* q0, const double* q1, double h, i
   // so a margin that holds them makes the superset (and its rebuilds) costlier than
   // the exact broad phase (measured: 11.2 -> 8.6 steps/s at 1% of the cell)
   static const double pvl_frac = getenv("ABD_PVL_MARGIN") ? atof(getenv("ABD_PVL_MARGIN")) : 0.0;
-  const bool use_pvl = pvl_frac > 0.0 && w.vl_valid && w.vl_cell > 0.0 && s.has_groups;
+  const bool use_pvl = pvl_frac > 0.0 && w.vl_valid && w.vl_cell > 0.0 && s.has_groups && !n_ov_dev;
   bool same = false;
   if (use_pvl) {
     PrimGeo g{s.rest.p, q0, q1, h, s.v_off.p, s.e_off.p, s.t_off.p, s.edges.p, s.tris.p};
@@ -1292,7 +1307,8 @@ static void prim_stage(Scene& s, const double* q0, const double* q1, double h, i
         bool dummy = false;
         int* no_same = reinterpret_cast<int*>(w.ull.p + 15);
         CK(cudaMemsetAsync(no_same, 0, sizeof(int), st));
-        prim_pairs_run(s, q0, q1, h + m, w.vl_pairs.p, (int)w.vl_n, w.vl_box.p, w.pvl_vf, w.pvl_ee, w.pvl_nvf,
+        int n_sup = (int)w.vl_n;
+        prim_pairs_run(s, q0, q1, h + m, w.vl_pairs.p, n_sup, w.vl_box.p, w.pvl_vf, w.pvl_ee, w.pvl_nvf,
                        w.pvl_nee, no_same, dummy);
         w.pvl_q0.resize(12 * (size_t)s.B);
         w.pvl_q1.resize(12 * (size_t)s.B);
@@ -1342,7 +1358,8 @@ static void prim_stage(Scene& s, const double* q0, const double* q1, double h, i
       return;
     }
   }
-  prim_pairs_run(s, q0, q1, h, c.ov.p, n_ov, s.bbox.p, c.vf, c.ee, c.n_vf, c.n_ee, ov_same, same);
+  prim_pairs_run(s, q0, q1, h, c.ov.p, n_ov, s.bbox.p, c.vf, c.ee, c.n_vf, c.n_ee, ov_same, same, n_ov_dev,
+                 viol_h);
   c.ov_matches_pattern = same;
 }
 
@@ -1398,6 +1415,34 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   int* vl_info = reinterpret_cast<int*>(w.ull.p + 13);
   int n_ov = 0;
   bool have = false;
+  // the filtered count stays on the device and is read back with the primitive-pair
+  // counts (one sync less); a containment violation then restarts the broad phase
+  static const bool no_defer = getenv("ABD_VL_SYNC") != nullptr;
+  const bool defer = use_vl && w.vl_valid && !no_defer && s.max_v <= P2_VCAP && !getenv("ABD_BP_V1");
+  if (defer) {
+    if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
+    vl_filter(s, vl_info);
+    int* ov_same = reinterpret_cast<int*>(w.ull.p + 9);
+    if (w.pat_valid && s.H.n == s.n_dyn) {
+      dev_set_i32(st, ov_same, 1);
+      k_ov_in_pattern<<<grid_for(std::max<int64_t>(w.vl_n, 1), 256), 256, 0, st>>>(
+          w.vl_n, c.ov.p, s.slot.p, s.H.n_off, s.H.upper_keys.p, ov_same, vl_info);
+      note_launch("k_ov_in_pattern");
+    } else {
+      CK(cudaMemsetAsync(ov_same, 0, sizeof(int), st));
+    }
+    int n_cap = (int)w.vl_n;
+    int viol = 0;
+    prim_stage(s, q0, q1, h, n_cap, ov_same, vl_info, &viol);
+    if (viol) {
+      w.vl_valid = false;
+      broad_phase(s, q0, q1, d_hat);
+      return;
+    }
+    c.n_ov = n_cap;
+    c.ov.n = n_cap;
+    return;
+  }
   if (use_vl && w.vl_valid) {
     if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
     vl_filter(s, vl_info);
@@ -1504,7 +1549,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
     const int one = 1;
     dev_set_i32(st, ov_same, one);
     k_ov_in_pattern<<<grid_for(n_ov, 256), 256, 0, st>>>(n_ov, c.ov.p, s.slot.p, s.H.n_off, s.H.upper_keys.p,
-                                                         ov_same);
+                                                         ov_same, nullptr);
     note_launch("k_ov_in_pattern");
   } else {
     CK(cudaMemsetAsync(ov_same, 0, sizeof(int), st));
