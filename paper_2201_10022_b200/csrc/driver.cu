@@ -112,6 +112,7 @@ struct EventTimer {
 };
 
 static void mark_structure(Scene& s);
+static void mark_structure_early(Scene& s, const double* q, double dh);
 
 // flags + exclusive scan of candidate activity (d^2 < d_hat^2) into s.w.flags/pos;
 // returns the active count (one host sync, also checks the barrier domain)
@@ -342,6 +343,7 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   note_launch("k_alpha_trial");
   launch_energy(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v,
                 w.lsred.p + 4 * RED_BLOCKS, w.lsscal.p + 4, w.lserr.p + 1);
+  w.ch_early = false;
   // partitioned: global CCD bound (t >= 0: min of the bit patterns == min of the values),
   // energies and error flags over all ranks
   comm_allreduce(s, tmin, 1, 0, 1);
@@ -378,6 +380,15 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   r.alpha = r.amax >= 1.0 ? 1.0 : std::fmin(1.0, P.ccd_step_scale * r.amax);
   r.e0 = ip_combine(hp + 1);
   r.e = ip_combine(hp + 5);
+  // accepted first trial: the next iteration's coupling structure is that of q_trial;
+  // when the next assemble keeps the BSR pattern (its overlap pairs are already in
+  // it -- decided by this iteration's broad phase), mark it now and start the
+  // analysis while the next iteration's activity scan, pair blocks and reduction run
+  static const bool no_early = getenv("ABD_CHOL_NO_EARLY") != nullptr;
+  const bool keeps_pattern = w.pat_valid && s.cands.ov_matches_pattern && s.H.n == s.n_dyn &&
+                             w.pat_fric_gen == s.fric.gen && w.pat_n_f == s.fric.n;
+  if (!no_early && P.linear_solver != 1 && s.n_dyn > 0 && s.comm.world == 1 && keeps_pattern && r.e < r.e0)
+    mark_structure_early(s, s.q_trial.p, P.d_hat);
   return r;
 }
 
@@ -462,8 +473,41 @@ __global__ void k_mark_active_rows(int64_t n, const int4* __restrict__ rows, con
 
 // structure flags (active contact candidates + friction pairs) copied to the host
 // right after the activity scan, so the host analysis overlaps the pair blocks
+// structure at the accepted first trial q_trial (== the next iterate): marked on the
+// side stream, flags only (the pattern -- and the upper keys already on the host --
+// is kept, see line_search_first), then the analysis job is posted
+static void mark_structure_early(Scene& s, const double* q, double dh) {
+  Scene::Work& w = s.w;
+  const int64_t n_off = s.H.n_off;
+  CK(cudaEventRecord(s.fork_ev, s.stream));
+  CK(cudaStreamWaitEvent(s.side, s.fork_ev, 0));
+  std::swap(s.stream, s.side);
+  w.ch_flags.resize(std::max<int64_t>(n_off, 1));
+  if (n_off) {
+    w.ch_flags.zero(s.stream);
+    launch_mark_active_q(s, q, dh * dh, w.ch_flags.p);
+    if (s.fric.n) {
+      k_mark_active<<<grid_for(s.fric.n, 256), 256, 0, s.stream>>>(s.fric.n, s.fric.bodies.p, s.slot.p, n_off,
+                                                                   s.H.upper_keys.p, w.ch_flags.p);
+      note_launch("k_mark_active");
+    }
+    int* hm = w.h_meta.reserve(3 * (size_t)n_off);
+    CK(cudaMemcpyAsync(hm, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  }
+  if (!w.ch_pre_ev) CK(cudaEventCreateWithFlags(&w.ch_pre_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(w.ch_pre_ev, s.stream));
+  std::swap(s.stream, s.side);
+  w.ch_pre = true;
+  w.ch_early = true;
+  chol_analysis_post(s);
+}
+
 static void mark_structure(Scene& s) {
   Scene::Work& w = s.w;
+  if (w.ch_early) {  // marked at the accepted trial and already being analysed
+    w.ch_early = false;
+    return;
+  }
   const int64_t n_off = s.H.n_off;
   w.ch_flags.resize(std::max<int64_t>(n_off, 1));
   if (n_off) {

@@ -518,7 +518,7 @@ static Analysis chol_analyze(Scene& s) {
   using clk = std::chrono::steady_clock;
   Bsr& H = s.H;
   Scene::Work& w = s.w;
-  cudaStream_t st = s.stream;
+  cudaStream_t st = s.main_stream;  // s.stream may be swapped to a side stream by the main thread
   const int n = H.n;
   const int64_t n_off = H.n_off;
   Analysis an;

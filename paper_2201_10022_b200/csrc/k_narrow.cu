@@ -108,6 +108,45 @@ void launch_pair_flags_both(Scene& s, const double* q, double dh2, int* flags, i
   note_launch("k_pair_flags");
 }
 
+// coupling structure at q (the line search's first trial, i.e. the next Newton
+// iterate when it is accepted): pattern blocks of active candidates, marked by
+// binary search in the sorted upper keys (as driver.cu k_mark_active_rows)
+__global__ void k_mark_active_q(SceneView sv, int64_t n_vf, const int4* __restrict__ vf, int64_t n_ee,
+                                const int4* __restrict__ ee, const double* __restrict__ q, double dh2,
+                                const int* __restrict__ slot, int64_t n_off, const int2* __restrict__ keys,
+                                int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_vf + n_ee) return;
+  const int kind = i < n_vf ? KIND_VF : KIND_EE;
+  const int4 r = kind == KIND_VF ? vf[i] : ee[i - n_vf];
+  const int sa = slot[r.x], sb = slot[r.z];
+  if (sa < 0 || sb < 0 || sa == sb) return;
+  PairIds ids = pair_ids(sv, kind, r);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  if (!(pair_d2(kind, z) < dh2)) return;
+  const int a = min(sa, sb), c = max(sa, sb);
+  int64_t lo = 0, hi = n_off - 1;
+  while (lo <= hi) {
+    const int64_t m = (lo + hi) >> 1;
+    const int2 k = keys[m];
+    if (k.x < a || (k.x == a && k.y < c)) lo = m + 1;
+    else if (k.x == a && k.y == c) {
+      flags[m] = 1;
+      return;
+    } else hi = m - 1;
+  }
+}
+
+void launch_mark_active_q(Scene& s, const double* q, double dh2, int* flags) {
+  const int64_t n = s.cands.n_vf + s.cands.n_ee;
+  if (!n || !s.H.n_off) return;
+  k_mark_active_q<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), s.cands.n_vf, s.cands.vf.p, s.cands.n_ee,
+                                                          s.cands.ee.p, q, dh2, s.slot.p, s.H.n_off,
+                                                          s.H.upper_keys.p, flags);
+  note_launch("k_mark_active_q");
+}
+
 // K3 first pass: one thread per candidate, active ones write g24 | haa | hbb | hab
 // same over the compacted active list: full warps instead of ~1/4 active lanes;
 // specialised per kind so the VF kernel carries none of the mollified-EE state.

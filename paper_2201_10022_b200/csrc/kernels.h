@@ -55,6 +55,7 @@ void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const doubl
 // ---- scene narrow phase (k_narrow.cu) ----
 // activity flags d^2 < d_hat^2 for the resident candidates of `kind`
 void launch_pair_flags_both(Scene& s, const double* q, double dh2, int* flags, int* err);
+void launch_mark_active_q(Scene& s, const double* q, double dh2, int* flags);
 void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err);
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act);
 void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, double dh, int project,

@@ -39,6 +39,7 @@ Scene::Scene() {
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  main_stream = stream;
   CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));

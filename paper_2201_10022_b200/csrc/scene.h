@@ -167,6 +167,7 @@ struct Scene {
   int max_v = 0, max_e = 0, max_t = 0;  // per-body primitive maxima (sort key widths)
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;            // forked work that overlaps the main stream (event-joined)
+  cudaStream_t main_stream = nullptr;     // == stream, never swapped (used by the analysis worker thread)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaStream_t side2 = nullptr;  // early ACCD of the hot queries (overlaps the broad phase)
   cudaEvent_t hot_fork_ev = nullptr, hot_ev = nullptr;
@@ -293,6 +294,9 @@ struct Scene {
     std::vector<uint64_t> ch_edges_cur;
     // structure flags + keys copied out by assemble() (event-ordered); consumed once
     bool ch_pre = false;
+    // the next iteration's structure was marked at the accepted line-search trial
+    // and its analysis posted early (mark_structure then has nothing to do)
+    bool ch_early = false;
     cudaEvent_t ch_pre_ev = nullptr;
     // an in-flight chol_begin awaiting chol_finish
     struct CholRun {
