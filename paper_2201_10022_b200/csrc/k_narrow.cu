@@ -67,19 +67,6 @@ __device__ __forceinline__ void pair_points(const SceneView& sv, const PairIds& 
   }
 }
 
-__global__ void k_pair_flags(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
-                             const double* __restrict__ q, double dh2, int* flags, int* err) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  PairIds ids = pair_ids(sv, kind, rows[i]);
-  V3 z[4], xb[4];
-  pair_points(sv, ids, q, z, xb);
-  double d2 = pair_d2(kind, z);
-  int on = d2 < dh2;
-  flags[i] = on;
-  if (on && !(d2 > 0.0)) atomicExch(err, 1);
-}
-
 // activity flags over VF then EE candidates in one launch; flags[n] = 0 (the scan's tail)
 __global__ void k_pair_flags_both(SceneView sv, int64_t n_vf, const int4* __restrict__ vf, int64_t n_ee,
                                   const int4* __restrict__ ee, const double* __restrict__ q, double dh2, int* flags,
@@ -147,8 +134,8 @@ void launch_mark_active_q(Scene& s, const double* q, double dh2, int* flags) {
   note_launch("k_mark_active_q");
 }
 
-// K3 first pass: one thread per candidate, active ones write g24 | haa | hbb | hab
-// same over the compacted active list: full warps instead of ~1/4 active lanes;
+// K3 first pass over the compacted active list (full warps instead of ~1/4 active
+// lanes), one compact record per active pair (abd_pblk.cuh);
 // specialised per kind so the VF kernel carries none of the mollified-EE state.
 // EE pairs whose mollifier is active (near-parallel edges) are deferred to
 // k_pair_blocks_moll, so the common EE pairs also run the lean 5-column kernel.
@@ -342,11 +329,6 @@ __device__ __forceinline__ void contact_energy_part(const SceneView& sv, int kin
   if (threadIdx.x == 0) partials[bx] = sh[0];
 }
 
-__global__ void k_contact_energy(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
-                                 const double* __restrict__ q, double kappa, double dh, double* partials, int* err) {
-  contact_energy_part(sv, kind, n, rows, q, kappa, dh, partials, err, blockIdx.x, gridDim.x);
-}
-
 __global__ void k_cand_min_d2(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows,
                               const double* __restrict__ q, unsigned long long* best) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -431,29 +413,7 @@ __global__ void k_friction_pre(SceneView sv, int kind, int64_t n, const int4* __
   }
 }
 
-// K5: ACCD over candidates with a global min (ccd.py:130-153)
-__global__ void k_ccd(SceneView sv, int kind, int64_t n, const int4* __restrict__ rows, const double* __restrict__ q,
-                      const double* __restrict__ dq, double slack, unsigned long long* tmin, int* err) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  double t = INFINITY;
-  if (i < n) {
-    PairIds ids = pair_ids(sv, kind, rows[i]);
-    V3 x[4], xb[4], dx[4];
-    pair_points(sv, ids, q, x, xb);
-    for (int k = 0; k < 4; ++k) {
-      int b = ids.body[k];
-      dx[k] = sv.dyn[b] ? world_pos(dq + 12 * (int64_t)b, xb[k]) : V3{0.0, 0.0, 0.0};
-    }
-    bool bad = false;
-    t = accd_query(kind, x, dx, slack, 1.0, 512, tmin, bad);
-    if (bad) atomicExch(err, 1);
-  }
-  // one ordered-bits atomic per warp (t >= 0, so the bit patterns order like the values)
-  for (int o = 16; o > 0; o >>= 1) t = fmin(t, __shfl_xor_sync(0xffffffffu, t, o));
-  if ((threadIdx.x & 31) == 0 && t < INFINITY) atomicMin(tmin, (unsigned long long)__double_as_longlong(t));
-}
-
-// K5 over both candidate lists in one launch (VF rows first, then EE): the
+// K5: ACCD over candidates with a global min (ccd.py:130-153), over both candidate lists in one launch (VF rows first, then EE): the
 // heavy-tailed ACCD queries of the two kinds share one tail instead of two.
 // Hot queries (rows of the hot list, already evaluated exactly by k_ccd_hot while
 // the broad phase ran) take their precomputed t; queries that need >= slow_it
@@ -894,15 +854,6 @@ static const int4* rows_of(const Scene& s, int kind, int64_t& n) {
   return kind == KIND_VF ? s.cands.vf.p : s.cands.ee.p;
 }
 
-void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err) {
-  int64_t n;
-  const int4* rows = rows_of(s, kind, n);
-  if (!n) return;
-  k_pair_flags<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dh2, flags, err);
-  note_launch("k_pair_flags");
-}
-
-
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act) {
   if (!n) return;
   k_scatter_active<<<grid_for(n, 256), 256, 0, s.stream>>>(n, flags, pos, act);
@@ -935,13 +886,6 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
   note_launch("k_pair_blocks");
 }
 
-void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, double dh, double* partials, int* err) {
-  int64_t n;
-  const int4* rows = rows_of(s, kind, n);
-  k_contact_energy<<<RED_BLOCKS, RED_THREADS, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, partials, err);
-  note_launch("k_contact_energy");
-}
-
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best) {
   int64_t n;
   const int4* rows = rows_of(s, kind, n);
@@ -958,46 +902,6 @@ void launch_friction_pre(Scene& s, int kind, const double* q, double kappa, doub
   k_friction_pre<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, kappa, dh, flags, pos, base,
                                                          s.fric.bodies.p, s.fric.rec.p, basis_out);
   note_launch("k_friction_pre");
-}
-
-void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack, unsigned long long* tmin,
-                int* err) {
-  int64_t n;
-  const int4* rows = rows_of(s, kind, n);
-  if (!n) return;
-  k_ccd<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dq, slack, tmin, err);
-  note_launch("k_ccd");
-  static const bool stats = getenv("ABD_CCD_STATS") != nullptr;
-  if (stats) {
-    DVec<int> its;
-    DVec<double> ts;
-    its.resize(n);
-    ts.resize(n);
-    k_ccd_dbg<<<grid_for(n, 128), 128, 0, s.stream>>>(view(s), kind, n, rows, q, dq, slack, its.p, ts.p);
-    std::vector<int> hi(n);
-    std::vector<double> ht(n);
-    its.download(hi.data(), n, s.stream);
-    ts.download(ht.data(), n, s.stream);
-    SSYNC(s.stream);
-    double tmn = 1.0;
-    for (int64_t i = 0; i < n; ++i) tmn = std::fmin(tmn, ht[i]);
-    int64_t h[6] = {0, 0, 0, 0, 0, 0}, below2 = 0, sum_it = 0;
-    int mx = 0, mx_it_t_lo = 0;
-    for (int64_t i = 0; i < n; ++i) {
-      int it = hi[i];
-      sum_it += it;
-      mx = std::max(mx, it);
-      h[it <= 1 ? 0 : it <= 4 ? 1 : it <= 16 ? 2 : it <= 64 ? 3 : it <= 256 ? 4 : 5]++;
-      if (ht[i] < 2.0 * tmn) {
-        ++below2;
-        mx_it_t_lo = std::max(mx_it_t_lo, it);
-      }
-    }
-    fprintf(stderr, "[ccd] kind=%d n=%lld tmin=%.4e mean_it=%.2f max_it=%d hist(<=1,4,16,64,256,>)=%lld %lld %lld %lld %lld %lld "
-            "t<2tmin: %lld (max it %d)\n", kind, (long long)n, tmn, (double)sum_it / n, mx, (long long)h[0],
-            (long long)h[1], (long long)h[2], (long long)h[3], (long long)h[4], (long long)h[5], (long long)below2,
-            mx_it_t_lo);
-  }
 }
 
 void launch_ccd_hot(Scene& s, const double* q, const double* dq, double slack) {

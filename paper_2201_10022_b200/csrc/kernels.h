@@ -56,12 +56,9 @@ void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const doubl
 // activity flags d^2 < d_hat^2 for the resident candidates of `kind`
 void launch_pair_flags_both(Scene& s, const double* q, double dh2, int* flags, int* err);
 void launch_mark_active_q(Scene& s, const double* q, double dh2, int* flags);
-void launch_pair_flags(Scene& s, int kind, const double* q, double dh2, int* flags, int* err);
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act);
 void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, double dh, int project,
                             const int* act, int64_t slot_off, int64_t count);
-void launch_contact_energy(Scene& s, int kind, const double* q, double kappa, double dh, double* partials,
-                           int* err);
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best_bits);
 void launch_friction_pre(Scene& s, int kind, const double* q, double kappa, double dh, const int* flags,
                          const int* pos, int64_t base, double* basis_out);
@@ -86,8 +83,6 @@ void launch_energy_all(Scene& s, const double* q, const double* qt, double dt, d
                        double eps_v, double* red4, int* err);
 void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, unsigned long long* tmin,
                      int* err, bool track = false);
-void launch_ccd(Scene& s, int kind, const double* q, const double* dq, double slack,
-                unsigned long long* tmin_bits, int* err);
 // per-body inertia + orthogonality terms (K1): grad0/diag0 per dynamic slot, energy partials
 void launch_body_terms(Scene& s, const double* q, const double* q_tilde, double dt, double* grad0,
                        double* diag0, double* energy_partials, int want_derivs);
