@@ -167,6 +167,9 @@ typedef struct abd_step_params {
   /* Newton linear solve: 0 = sparse block Cholesky + refinement (BlockCholesky.solve_refined,
    * sparse.py:90-161; the reference's solver), 1 = pipelined block-Jacobi PCG to pcg_rel_tol */
   int linear_solver;
+  /* 1: StepStats.min_iterate_distance = min over the Newton iterates of
+   * global_min_distance(q) (StepParams.audit_iterates, solver.py:577-580) */
+  int audit_iterates;
 } abd_step_params;
 
 typedef struct abd_step_stats {
@@ -174,6 +177,7 @@ typedef struct abd_step_stats {
   int pcg_iters_total;     /* PCG iterations, or triangular solves of the Cholesky path */
   int64_t candidates;      /* max candidate count over the step (StepStats.candidates) */
   double min_distance, ip_value, max_ortho_error, last_dq_over_dt;
+  double min_iterate_distance; /* +inf unless audit_iterates */
   double t_broad, t_assemble, t_solve, t_ccd, t_line_search, t_total; /* ms, CUDA events */
 } abd_step_stats;
 

@@ -993,10 +993,12 @@ class OracleStepStats:
     max_ortho_error: float
     energy_trace: list
     alphas: list
+    min_iterate_distance: float = np.inf
 
 
-def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True):
-    """solver.py:493-628 (friction_outer_iters = 1, no joint reduction)."""
+def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True, audit_iterates=False):
+    """solver.py:493-628 (friction_outer_iters = 1, no joint reduction); audit_iterates
+    as StepParams.audit_iterates (solver.py:577-580)."""
     q0 = np.array(q, dtype=float, copy=True)
     qt = q_tilde(model, q0, q_dot, forces, prm.dt)
     cands = broad_phase(model.bodies, q0, q0, prm.d_hat)
@@ -1005,6 +1007,7 @@ def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True
     qc = q0.copy()
     iters, conv = 0, False
     trace, alphas = [], []
+    min_iter = np.inf
     maxc = len(cands)
     dd = np.zeros(0)
     for _ in range(prm.max_newton_iters):
@@ -1028,6 +1031,8 @@ def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True
         trace.append(e_new)
         alphas.append(alpha)
         iters += 1
+        if audit_iterates:
+            min_iter = min(min_iter, global_min_distance(model.bodies, qc))
     if not conv:
         warnings.warn("Newton did not converge", RuntimeWarning)
     qd = np.zeros_like(qc)
@@ -1041,5 +1046,5 @@ def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True
             md = global_min_distance(model.bodies, qc)
     stats = OracleStepStats(
         iters, conv, md, maxc, ip_value(model, qc, ip, prm),
-        max((ortho_error(qc[b]) for b in model.dyn), default=0.0), trace, alphas)
+        max((ortho_error(qc[b]) for b in model.dyn), default=0.0), trace, alphas, min_iter)
     return qc, qd, stats

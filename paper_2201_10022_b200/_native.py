@@ -37,14 +37,14 @@ class StepParamsC(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("dt", "d_hat", "kappa_barrier", "mu", "epsilon_v", "newton_tol",
                                           "ccd_slack", "ccd_step_scale", "pcg_rel_tol")] + \
                [(n, C.c_int) for n in ("max_newton_iters", "friction_outer_iters", "pcg_max_iters",
-                                      "compute_min_distance", "linear_solver")]
+                                      "compute_min_distance", "linear_solver", "audit_iterates")]
 
 
 class StepStatsC(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("iterations", "converged", "nondescent_fallbacks", "pcg_iters_total")] + \
                [("candidates", C.c_int64)] + \
                [(n, C.c_double) for n in ("min_distance", "ip_value", "max_ortho_error", "last_dq_over_dt",
-                                          "t_broad", "t_assemble", "t_solve", "t_ccd", "t_line_search", "t_total")]
+                                          "min_iterate_distance", "t_broad", "t_assemble", "t_solve", "t_ccd", "t_line_search", "t_total")]
 
 
 _SIGS = {

@@ -585,6 +585,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   auto t_start = clk::now();
   static const bool trace_newton = getenv("ABD_TRACE_NEWTON") != nullptr;
   st = abd_step_stats{};
+  st.min_iterate_distance = INFINITY;
   cudaStream_t stream = s.stream;
   int64_t NB = 12 * (int64_t)s.B;
   int64_t ND = 12 * (int64_t)s.n_dyn;
@@ -703,6 +704,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       if (trace) trace[n_trace] = e;
       ++n_trace;
       st.iterations += 1;
+      if (P.audit_iterates) st.min_iterate_distance = std::fmin(st.min_iterate_distance, global_min_distance(s, s.q.p));
     }
     st.converged = converged ? 1 : 0;
   }

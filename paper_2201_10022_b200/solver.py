@@ -233,7 +233,7 @@ def step_params_c(params: StepParams, min_distance=True, pcg_rel_tol=1e-8,
         ccd_step_scale=params.ccd_step_scale, pcg_rel_tol=pcg_rel_tol,
         max_newton_iters=params.max_newton_iters, friction_outer_iters=params.friction_outer_iters,
         pcg_max_iters=pcg_max_iters, compute_min_distance=1 if min_distance else 0,
-        linear_solver=1 if params.linear_solver == "pcg" else 0)
+        linear_solver=1 if params.linear_solver == "pcg" else 0, audit_iterates=1 if params.audit_iterates else 0)
 
 
 def advance_step(model: SystemModel, state: SimState, params: StepParams):
@@ -276,5 +276,6 @@ def advance_step(model: SystemModel, state: SimState, params: StepParams):
         step=state.step_index, iterations=st.iterations, converged=bool(st.converged),
         min_distance=st.min_distance, candidates=int(st.candidates), ip_value=st.ip_value,
         max_ortho_error=st.max_ortho_error, energy_trace=list(trace[:st.iterations]),
+        min_iterate_distance=st.min_iterate_distance,
         timings=timings, pcg_iterations=st.pcg_iters_total)
     return new_state, stats

@@ -423,3 +423,25 @@ def test_kernel_launch_counter_moves():
     n0 = _native.kernel_launches()
     P.point_triangle_closest(np.zeros(3), [0, 0, 1.0], [1.0, 0, 1], [0, 1.0, 1])
     assert _native.kernel_launches() > n0
+
+
+def test_audit_iterates_min_distance():
+    """StepParams.audit_iterates (solver.py:577-580): min over the Newton iterates of
+    global_min_distance, against the oracle on a box-stack step."""
+    from paper_2201_10022_b200 import scenes
+    spec = scenes.box_stack(seed=0, steps=1)
+    model, state, params = spec.build()
+    params.audit_iterates = True
+    masses = [g.matrix if g is not None else None for g in model.gmass]
+    stiff = [m.stiffness_scale if m is not None else None for m in model.materials]
+    om = O.OracleModel(model.bodies, masses, stiff)
+    prm = O.OracleParams(dt=params.dt, d_hat=params.d_hat, kappa_barrier=params.kappa_barrier, mu=params.mu,
+                         newton_tol=params.newton_tol)
+    q, qd = state.q.copy(), state.q_dot.copy()
+    for _ in range(3):
+        f = model.forces(state.step_index, state.time + params.dt, state.q)
+        state, st = P.advance_step(model, state, params)
+        q, qd, ost = O.advance_step(om, q, qd, f, prm, audit_iterates=True)
+        assert st.iterations == ost.iterations
+        assert np.isfinite(st.min_iterate_distance) and st.min_iterate_distance > 0
+        assert st.min_iterate_distance == pytest.approx(ost.min_iterate_distance, rel=1e-9)
