@@ -122,6 +122,13 @@ int abd_set_candidates(abd_scene* s, int64_t n_vf, const int64_t* vf, int64_t n_
 int abd_contact_energy(abd_scene* s, const double* q, double kappa, double d_hat, double* energy);
 /* candidate_min_distance_sq  contact.py:541-557 (returns +inf when empty) */
 int abd_candidate_min_d2(abd_scene* s, const double* q, double* d2);
+/* intersection audit: exact closed-triangle intersection (triangles_intersect_batch,
+ * intersect.py:18-42); tri_a, tri_b (n,3,3); out[i] = 1 when they intersect */
+int abd_tri_intersect_batch(int64_t n, const double* tri_a, const double* tri_b, uint8_t* out);
+/* body pairs i < j whose surfaces intersect or one contains the other at q
+ * (_intersecting_body_pairs, scene.py:652-698): pairs (cap,2) in canonical order,
+ * n_pairs = total found (pairs beyond cap are not written) */
+int abd_intersecting_pairs(abd_scene* s, const double* q, int64_t cap, int64_t* pairs, int64_t* n_pairs);
 /* global_min_distance  solver.py:396-473 (exact; pairs of two kinematic bodies skipped) */
 int abd_global_min_distance(abd_scene* s, const double* q, double* dist);
 /* contact_gradient_hessian  contact.py:646-675 -> resident PairBlocks; n_active out */

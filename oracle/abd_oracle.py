@@ -1048,3 +1048,76 @@ def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True
         iters, conv, md, maxc, ip_value(model, qc, ip, prm),
         max((ortho_error(qc[b]) for b in model.dyn), default=0.0), trace, alphas, min_iter)
     return qc, qd, stats
+
+
+# ---------------------------------------------------------------------------
+# intersection audit (intersect.py:18-42, scene.py:627-698)
+
+def tri_intersect_batch(ta, tb):
+    """Closed-triangle separating-axis test on (N,3,3) pairs (intersect.py:18-42):
+    axes = face normals, 9 edge-edge crosses, 6 in-plane edge normals; an axis
+    with |axis|^2 <= 1e-30 is skipped; touching counts as intersecting."""
+    ta = np.asarray(ta, dtype=float).reshape(-1, 3, 3)
+    tb = np.asarray(tb, dtype=float).reshape(-1, 3, 3)
+    ea = np.stack([ta[:, 1] - ta[:, 0], ta[:, 2] - ta[:, 1], ta[:, 0] - ta[:, 2]], axis=1)
+    eb = np.stack([tb[:, 1] - tb[:, 0], tb[:, 2] - tb[:, 1], tb[:, 0] - tb[:, 2]], axis=1)
+    na = np.cross(ea[:, 0], ea[:, 1])
+    nb = np.cross(eb[:, 0], eb[:, 1])
+    ax = [na[:, None], nb[:, None]]
+    ax += [np.cross(ea[:, i], eb[:, j])[:, None] for i in range(3) for j in range(3)]
+    ax += [np.cross(ea[:, i], na)[:, None] for i in range(3)]
+    ax += [np.cross(eb[:, i], nb)[:, None] for i in range(3)]
+    ax = np.concatenate(ax, axis=1)
+    pa = np.einsum("nak,npk->nap", ax, ta)
+    pb = np.einsum("nak,npk->nap", ax, tb)
+    sep = (pa.min(axis=2) > pb.max(axis=2)) | (pb.min(axis=2) > pa.max(axis=2))
+    live = np.einsum("nak,nak->na", ax, ax) > 1e-30
+    return ~(sep & live).any(axis=1)
+
+
+def _ray_parity_inside(p, X, tris):
+    """scene.py:627-649: ray along a fixed skewed direction, odd hit count = inside."""
+    d = np.array([0.5424426421, 0.7866258632, 0.2954766431])
+    v0, v1, v2 = X[tris[:, 0]], X[tris[:, 1]], X[tris[:, 2]]
+    e1, e2 = v1 - v0, v2 - v0
+    h = np.cross(np.broadcast_to(d, e2.shape), e2)
+    a = np.einsum("ij,ij->i", e1, h)
+    ok = np.abs(a) > 1e-14
+    f = np.where(ok, 1.0 / np.where(ok, a, 1.0), 0.0)
+    s = p - v0
+    u = f * np.einsum("ij,ij->i", s, h)
+    qv = np.cross(s, e1)
+    v = f * np.einsum("ij,j->i", qv, d)
+    t = f * np.einsum("ij,ij->i", e2, qv)
+    return int((ok & (u >= 0) & (u <= 1) & (v >= 0) & (u + v <= 1) & (t > 1e-12)).sum()) % 2 == 1
+
+
+def intersecting_body_pairs(bodies, q_all):
+    """scene.py:652-698 on generalized coordinates: box-overlapping body pairs,
+    triangle SAT on triangle pairs whose boxes meet the overlap box and each other,
+    else containment by ray parity both ways."""
+    q_all = np.asarray(q_all, dtype=float).reshape(len(bodies), 12)
+    Xs = [world_points(np.asarray(b.rest, dtype=float), q_all[i]) for i, b in enumerate(bodies)]
+    tris = [np.asarray(b.triangles, dtype=np.int64) for b in bodies]
+    lo = [x.min(axis=0) for x in Xs]
+    hi = [x.max(axis=0) for x in Xs]
+    out = []
+    for i in range(len(bodies)):
+        for j in range(i + 1, len(bodies)):
+            olo, ohi = np.maximum(lo[i], lo[j]), np.minimum(hi[i], hi[j])
+            if (olo > ohi).any():
+                continue
+            Ta, Tb = Xs[i][tris[i]], Xs[j][tris[j]]
+            alo, ahi, blo, bhi = Ta.min(axis=1), Ta.max(axis=1), Tb.min(axis=1), Tb.max(axis=1)
+            ka = np.nonzero(((alo <= ohi) & (ahi >= olo)).all(axis=1))[0]
+            kb = np.nonzero(((blo <= ohi) & (bhi >= olo)).all(axis=1))[0]
+            hit = False
+            if len(ka) and len(kb):
+                m = ((alo[ka][:, None] <= bhi[kb][None]) & (blo[kb][None] <= ahi[ka][:, None])).all(axis=2)
+                ii, jj = np.nonzero(m)
+                hit = bool(len(ii)) and bool(tri_intersect_batch(Ta[ka[ii]], Tb[kb[jj]]).any())
+            if not hit:
+                hit = _ray_parity_inside(Xs[i][0], Xs[j], tris[j]) or _ray_parity_inside(Xs[j][0], Xs[i], tris[i])
+            if hit:
+                out.append((i, j))
+    return out

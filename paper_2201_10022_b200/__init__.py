@@ -7,6 +7,7 @@ kernels through the C-ABI in include/abd_b200.h.  There is no CPU
 fallback: compute calls raise if libabd_b200.so or the GPU is missing.
 Setup-time types (meshes, masses, shapes) are host code.
 """
+from .aabb import Aabb, aabb_of, aabb_overlap
 from .body import (
     BodyCoords,
     BodyMaterial,
@@ -56,6 +57,7 @@ from .distance import (
     point_triangle_closest,
     point_triangle_distance_sq,
 )
+from .intersect import intersecting_body_pairs, triangles_intersect, triangles_intersect_batch
 from .mesh import SurfaceMesh, build_edges
 from .shapes import box_mesh, icosphere_mesh, torus_mesh
 from .solver import (

@@ -66,6 +66,8 @@ _SIGS = {
     "abd_bsr_pcg": (i32, [i32, i32, dp, i64, lp, dp, dp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
     "abd_bsr_cholesky": (i32, [i32, i32, dp, i64, lp, dp, dp, dbl, i32, dp, C.POINTER(i32), C.POINTER(dbl)]),
     "abd_scene_create": (vp, [i32, lp, lp, lp, dp, lp, lp, dp, up8, dp, dp]),
+    "abd_tri_intersect_batch": (i32, [i64, dp, dp, up8]),
+    "abd_intersecting_pairs": (i32, [vp, dp, i64, lp, C.POINTER(i64)]),
     "abd_scene_destroy": (None, [vp]),
     "abd_broad_phase": (i32, [vp, dp, dp, dbl, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "abd_get_candidates": (i32, [vp, lp, lp, lp]),

@@ -652,6 +652,32 @@ int abd_candidate_min_d2(abd_scene* h, const double* q, double* d2) {
   });
 }
 
+int abd_tri_intersect_batch(int64_t n, const double* tri_a, const double* tri_b, uint8_t* out) {
+  return guard([&] {
+    ensure_device();
+    if (n < 0) throw Error(ABD_ERR_ARG, "n < 0");
+    if (n == 0) return;
+    cudaStream_t st = g_stream();
+    Dev<double> da(st), db(st);
+    Dev<unsigned char> dout(st);
+    launch_tri_intersect(st, n, da.up(tri_a, 9 * n), db.up(tri_b, 9 * n), dout.alloc(n));
+    dout.down(out, n);
+    sync(st);
+  });
+}
+
+int abd_intersecting_pairs(abd_scene* h, const double* q, int64_t cap, int64_t* pairs, int64_t* n_pairs) {
+  return guard([&] {
+    SC(h);
+    std::vector<int2> r = intersecting_body_pairs(s, up_q(s, s.q_trial, q));
+    *n_pairs = (int64_t)r.size();
+    for (int64_t k = 0; k < std::min<int64_t>(cap, (int64_t)r.size()); ++k) {
+      pairs[2 * k] = r[k].x;
+      pairs[2 * k + 1] = r[k].y;
+    }
+  });
+}
+
 int abd_global_min_distance(abd_scene* h, const double* q, double* dist) {
   return guard([&] {
     SC(h);

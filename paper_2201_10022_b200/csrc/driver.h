@@ -30,6 +30,8 @@ void comm_allreduce(Scene& s, void* dptr, int64_t count, int dtype, int op);
 int64_t comm_allgather_i64(Scene& s, const int64_t* local, int64_t n_local, DVec<int64_t>& out);
 // k_stats.cu
 double global_min_distance(Scene& s, const double* q);
+// body pairs (i < j) whose closed surfaces intersect or contain one another (k_audit.cu)
+std::vector<int2> intersecting_body_pairs(Scene& s, const double* q);
 // driver.cu
 int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark = false);
 void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, int project);

@@ -1076,6 +1076,12 @@ __global__ void k_inflate_boxes(int B, const double* __restrict__ bbox, const do
   }
 }
 
+void launch_body_boxes(Scene& s, const double* q0, const double* q1, double h, double* out) {
+  if (s.B == 0) return;
+  k_body_boxes<<<grid_for((int64_t)s.B * 32, 256), 256, 0, s.stream>>>(s.B, s.v_off.p, s.rest.p, q0, q1, h, out);
+  note_launch("k_body_boxes");
+}
+
 // ---------------------------------------------------------------------------
 // primitive Verlet list (Work::pvl_*)
 // exact swept boxes of the candidate rows' primitives overlap? (contact.py:222-229 boxes)

@@ -3,6 +3,8 @@
 #include "abd_math.cuh"
 #include "scene.h"
 
+#include <vector>
+
 namespace abd {
 
 void note_launch(const char* name);
@@ -54,6 +56,10 @@ void launch_friction(cudaStream_t st, int64_t n, const int2* bodies, const doubl
 
 // ---- scene narrow phase (k_narrow.cu) ----
 // activity flags d^2 < d_hat^2 for the resident candidates of `kind`
+// swept body boxes (union of vertex boxes inflated by h) into out (B x 6)
+void launch_body_boxes(Scene& s, const double* q0, const double* q1, double h, double* out);
+// intersection audit (k_audit.cu)
+void launch_tri_intersect(cudaStream_t st, int64_t n, const double* ta, const double* tb, unsigned char* out);
 void launch_pair_flags_both(Scene& s, const double* q, double dh2, int* flags, int* err);
 void launch_mark_active_q(Scene& s, const double* q, double dh2, int* flags);
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act);

@@ -242,3 +242,13 @@ def test_small_config_trajectories(golden, name, steps):
         ref = g["q"][s + 1]
         assert np.abs(q - ref).max() / np.abs(ref).max() <= 1e-6, (name, s)
         assert st.iterations == g["iterations"][s]
+
+
+def test_oracle_intersection_audit_golden(golden):
+    """Oracle restatement of the intersection audit against the reference's own verdicts."""
+    g = golden("intersect.npz")
+    assert np.array_equal(O.tri_intersect_batch(g["tri_a"], g["tri_b"]), g["tri_hit"])
+    for c in range(2):
+        bodies = oracle_bodies(f"s{c}_", g)
+        pairs = O.intersecting_body_pairs(bodies, g[f"s{c}_q"])
+        assert [list(p) for p in pairs] == g[f"s{c}_pairs"].tolist()
