@@ -337,6 +337,31 @@ def gen_ico_pile(steps=40):
     save("ico_pile.npz", out)
 
 
+def gen_friction_outer(pre=22, steps=8):
+    """The 2x2x2 icosphere pile with friction_outer_iters=2 (solver.py:523-531): the
+    lagged friction is refreshed (broad phase + friction_precompute at q) after the
+    first Newton solve of each step.  `pre` ordinary steps first, so contacts exist."""
+    spec = scenes.icosphere_pile(seed=3, nx=2, ny=2, nz=2, mu=0.5, subdiv=1)
+    model = ref_model(spec.meshes, spec.dynamic, spec.density, spec.kappa_ortho)
+    params = rs.StepParams(**spec.params)
+    state = rs.SimState(q=spec.q0.copy(), q_dot=spec.q_dot0.copy())
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for _ in range(pre):
+            state, _ = rs.advance_step(model, state, params)
+        out = dict(q_start=state.q.copy(), qdot_start=state.q_dot.copy(), step_start=np.array(state.step_index),
+                   time_start=np.array(state.time))
+        params2 = rs.StepParams(**dict(spec.params, friction_outer_iters=2))
+        qs, its = [], []
+        for _ in range(steps):
+            state, st = rs.advance_step(model, state, params2)
+            qs.append(state.q.copy())
+            its.append(st.iterations)
+    out.update(q=np.array(qs), iterations=np.array(its))
+    print(f"friction outer: {steps} steps, iterations {its}")
+    save("friction_outer.npz", out)
+
+
 def gen_trajectory(name, spec, steps):
     """Reference trajectory of a small version of a BASELINE scene (q per step, iterations, min distance)."""
     model = ref_model(spec.meshes, spec.dynamic, spec.density, spec.kappa_ortho)
@@ -378,6 +403,8 @@ if __name__ == "__main__":
         gen_box_stack()
     if "ico_pile" in which:
         gen_ico_pile()
+    if "friction_outer" in which:
+        gen_friction_outer()
     if "cube_drop" in which:
         gen_cube_drop()
     if "chainmail" in which:

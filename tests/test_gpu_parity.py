@@ -458,3 +458,23 @@ def test_intersection_audit(golden):
     for c in range(2):
         bodies = [P.CollisionBody(v, t, e, bool(d)) for v, t, e, d in unpack_meshes(f"s{c}_", g)]
         assert [list(p) for p in P.intersecting_body_pairs(bodies, g[f"s{c}_q"])] == g[f"s{c}_pairs"].tolist()
+
+
+def test_friction_outer_iterations(golden):
+    """friction_outer_iters=2 (solver.py:523-531): the lagged friction is refreshed at
+    the Newton solution and the solve repeated; trajectory and iteration counts
+    against the reference's own run from the same state."""
+    g = golden("friction_outer.npz")
+    from paper_2201_10022_b200 import scenes
+    spec = scenes.icosphere_pile(seed=3, nx=2, ny=2, nz=2, mu=0.5, subdiv=1)
+    model, state, params = spec.build()
+    params.friction_outer_iters = 2
+    state.q, state.q_dot = g["q_start"].copy(), g["qdot_start"].copy()
+    state.step_index, state.time = int(g["step_start"]), float(g["time_start"])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for s in range(len(g["iterations"])):
+            state, st = P.advance_step(model, state, params)
+            ref = g["q"][s]
+            assert np.abs(state.q - ref).max() / np.abs(ref).max() <= 1e-6, s
+            assert st.iterations == int(g["iterations"][s]), s
