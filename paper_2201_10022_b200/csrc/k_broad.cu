@@ -591,6 +591,9 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int lt = a_thr ? la : lb, ll = a_thr ? lb : la;
       const int kt = a_thr ? ka : kb, kl = a_thr ? kb : ka;
       const int st_ = a_thr ? sa : sb, sl = a_thr ? sb : sa;
+      // hcount of the previous product is dead here: every thread read it into cnt
+      // before that product's hbase barrier, which thread 0 has passed
+      if (threadIdx.x == 0) hcount = 0;
       // materialise the loop side's boxes
       for (int t = threadIdx.x; t < nl; t += P2_THREADS)
         box_from_packed(kl, lpk[ll * cap_list + t], vb + 6 * sl * P2_VCAP, obx + 6 * t);
@@ -599,8 +602,6 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int body_a = prod == 1 ? bj : bi, body_b = prod == 1 ? bi : bj;
       const int G = nt >= P2_THREADS ? 1 : P2_THREADS / nt;
       const int Lc = (nl + G - 1) / G;
-      if (threadIdx.x == 0) hcount = 0;
-      __syncthreads();
       // pass 0: hits into shared memory; pass 1 (only when they overflow P2_HCAP):
       // straight into the reserved chunk, which is then flagged for a global sort
       for (int pass = 0; pass < 2; ++pass) {
@@ -707,10 +708,10 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
               }
             }
           }
-          __syncthreads();
+          // no barrier: the output only reads hk / hbase, which the next product
+          // rewrites after its materialise barrier and hbase barrier respectively
         }
       }
-      __syncthreads();
     }
   }
 }
