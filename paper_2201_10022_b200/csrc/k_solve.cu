@@ -159,7 +159,14 @@ __global__ void k_seg_bounds(int64_t m, const uint32_t* __restrict__ keys, int64
 // by one coalesced warp load (the next record prefetched into registers while the
 // current one is evaluated), so the ~60 per-entry reads hit shared memory
 constexpr int RB_WARPS = 8;
+constexpr int RB_SPLIT = 4;  // warps per BSR block: the contributions are dealt round-robin
+constexpr int RB_POS = RB_WARPS / RB_SPLIT;  // BSR blocks per CTA
 constexpr int RB_PER_LANE = (PB_STRIDE + 31) / 32;
+// RB_SPLIT warps per CSR position that is a diagonal or an upper block; warp s sums
+// the contributions s, s + RB_SPLIT, ... of the block's segment (each record staged
+// in shared memory by one coalesced warp load, the next one prefetched), then the
+// partial blocks are added in warp order: a fixed, deterministic summation order
+// with a quarter of the serial chain of one warp per block
 __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const int* __restrict__ row_ptr,
                                                                  const int* __restrict__ col,
                                                                  const int* __restrict__ seg_start,
@@ -171,53 +178,58 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
                                                                  double* grad, const int* __restrict__ row_of,
                                                                  int* sorted_out) {
   __shared__ double srec[RB_WARPS][RB_PER_LANE * 32];
-  int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  __shared__ double part[RB_WARPS][160];
+  __shared__ double gpart[RB_WARPS][12];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int64_t nnzb = row_ptr[n];
-  if (w >= nnzb) return;
-  int r = row_of[w];
-  int c = col[w];
-  if (c < r) return;  // lower blocks are written by their upper twin
-  bool is_diag = c == r;
+  const int split = wid % RB_SPLIT;
+  const int64_t w = (int64_t)blockIdx.x * RB_POS + wid / RB_SPLIT;
+  const int64_t nnzb = row_ptr[n];
+  int r = 0, c = -1;
+  if (w < nnzb) {
+    r = row_of[w];
+    c = col[w];
+  }
+  const bool active = w < nnzb && c >= r;  // lower blocks are written by their upper twin
+  const bool is_diag = c == r;
+  const int s0 = active ? seg_start[w] : 0, s1 = active ? seg_end[w] : 0;
+  if (sorted_out && active && split == 0) {
+    // rank sort of the segment by value (unique): pair-major order
+    for (int i = s0 + lane; i < s1; i += 32) {
+      const int vi = cvals[i];
+      int rk = 0;
+      for (int j = s0; j < s1; ++j) rk += cvals[j] < vi;
+      sorted_out[s0 + rk] = vi;
+    }
+  }
+  __syncthreads();
+  const int* cv = sorted_out ? sorted_out : cvals;
   double acc[5];
   double gacc = 0.0;
 #pragma unroll
   for (int e = 0; e < 5; ++e) {
     int idx = lane + 32 * e;
-    acc[e] = (is_diag && idx < 144) ? diag0[144 * (int64_t)r + idx] : 0.0;
+    acc[e] = (active && split == 0 && is_diag && idx < 144) ? diag0[144 * (int64_t)r + idx] : 0.0;
   }
-  if (is_diag && lane < 12) gacc = grad0[12 * (int64_t)r + lane];
-  const int s0 = seg_start[w], s1 = seg_end[w];
-  if (sorted_out) {
-    // rank sort of the segment by value (unique): pair-major summation order
-    for (int i = s0 + lane; i < s1; i += 32) {
-      const int vi = cvals[i];
-      int r = 0;
-      for (int j = s0; j < s1; ++j) r += cvals[j] < vi;
-      sorted_out[s0 + r] = vi;
-    }
-    __syncwarp();
-    cvals = sorted_out;
-  }
+  if (active && split == 0 && is_diag && lane < 12) gacc = grad0[12 * (int64_t)r + lane];
   double* sr = srec[wid];
   double nxt[RB_PER_LANE];
   int vnext = 0;
-  if (s0 < s1) {
-    vnext = cvals[s0];
+  if (s0 + split < s1) {
+    vnext = cv[s0 + split];
     const double* blk = pblk + (int64_t)(vnext >> 2) * PB_STRIDE;
 #pragma unroll
     for (int j = 0; j < RB_PER_LANE; ++j)
       if (lane + 32 * j < PB_STRIDE) nxt[j] = blk[lane + 32 * j];
   }
-  for (int t = s0; t < s1; ++t) {
+  for (int t = s0 + split; t < s1; t += RB_SPLIT) {
     const int which = vnext & 3;
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < RB_PER_LANE; ++j)
       if (lane + 32 * j < PB_STRIDE) sr[lane + 32 * j] = nxt[j];
     __syncwarp();
-    if (t + 1 < s1) {
-      vnext = cvals[t + 1];
+    if (t + RB_SPLIT < s1) {
+      vnext = cv[t + RB_SPLIT];
       const double* blk = pblk + (int64_t)(vnext >> 2) * PB_STRIDE;
 #pragma unroll
       for (int j = 0; j < RB_PER_LANE; ++j)
@@ -237,6 +249,16 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
     }
     if (which < 2 && lane < 12) gacc += sr[12 * which + lane];
   }
+#pragma unroll
+  for (int e = 0; e < 5; ++e) part[wid][lane + 32 * e] = acc[e];
+  if (lane < 12) gpart[wid][lane] = gacc;
+  __syncthreads();
+  if (!active || split != 0) return;
+#pragma unroll
+  for (int e = 0; e < 5; ++e)
+    for (int sp = 1; sp < RB_SPLIT; ++sp) acc[e] += part[wid + sp][lane + 32 * e];
+  if (lane < 12)
+    for (int sp = 1; sp < RB_SPLIT; ++sp) gacc += gpart[wid + sp][lane];
   double* out = val + 144 * w;
 #pragma unroll
   for (int e = 0; e < 5; ++e) {
@@ -416,7 +438,7 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
     se = seg_s.p + 1;
   }
   s.grad.resize(12 * (int64_t)n);
-  k_reduce_blocks<<<grid_for(H.nnzb * 32, 32 * RB_WARPS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, sb, se, cv,
+  k_reduce_blocks<<<grid_for(H.nnzb, RB_POS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, sb, se, cv,
                                                               s.pblk.blk.p, diag0, grad0, H.val.p, s.grad.p,
                                                               row_of.p, sorted_out);
   note_launch("k_reduce_blocks");
