@@ -512,18 +512,27 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
         const int l = hitg[u] >> 16, r = hitg[u] & 0xffff;
         const int side = l / 3, kind = l % 3;
         const int i = 32 * r + lane;
+        bool keep = false;
+        unsigned pk = 0;
+        int id = 0;
         if (i < meta[6 + l]) {
           const int64_t gi = (int64_t)meta[l] + i;  // prim offset of the body (grouped order)
-          const unsigned pk = gr.pk[kind][gi];
+          pk = gr.pk[kind][gi];
+          id = gr.id[kind][gi];
           double bx[6];
           box_from_packed(kind, pk, vb + 6 * side * P2_VCAP, bx);
-          const bool keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] &&
-                            bx[2] <= obox[5] && obox[2] <= bx[5];
-          if (keep) {
-            const int at = atomicAdd(&lcount[l], 1);
-            lists[l * cap_list + at] = gr.id[kind][gi];
-            lpk[l * cap_list + at] = pk;
-          }
+          keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] && bx[2] <= obox[5] &&
+                 obox[2] <= bx[5];
+        }
+        // the whole warp works on one group (one list): one shared-memory atomic per warp
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(&lcount[l], __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+          const int at = base + __popc(m & ((1u << lane) - 1));
+          lists[l * cap_list + at] = id;
+          lpk[l * cap_list + at] = pk;
         }
       }
     } else // one cull pass over the six lists (list id = 3 * side + kind); topology is
