@@ -713,13 +713,13 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   k_qdot<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.dyn.p, s.q.p, s.q0.p, P.dt, s.q_dot.p);
   note_launch("k_qdot");
   // stats (solver.py:604-627)
+  st.ip_value = ip_value(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
   st.min_distance = NAN;
   if (P.compute_min_distance) {
     double cm = candidate_min_d2(s, s.q.p);
     if (cm < P.d_hat * P.d_hat) st.min_distance = std::sqrt(cm);
-    else st.min_distance = global_min_distance(s, s.q.p);
+    else st.min_distance = global_min_distance_stats(s, s.q.p);
   }
-  st.ip_value = ip_value(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
   {
     unsigned long long* m = s.w.ull.p + 3;
     CK(cudaMemsetAsync(m, 0, sizeof(unsigned long long), stream));

@@ -1427,7 +1427,9 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   // body pairs: filter the superset with the exact boxes (one CTA, one sync); rebuild
   // the superset on the uniform grid when a box left its inflated box
   static const double vl_frac = getenv("ABD_VL_MARGIN") ? atof(getenv("ABD_VL_MARGIN")) : 0.05;
-  const bool use_vl = vl_frac > 0.0;
+  // the superset serves the stepping broad phase (h = d_hat / 2); a call with another
+  // inflation (the stats' distance search) runs the exact grid path and leaves it alone
+  const bool use_vl = vl_frac > 0.0 && (w.vl_h < 0.0 || w.vl_h == h);
   int* vl_info = reinterpret_cast<int*>(w.ull.p + 13);
   int n_ov = 0;
   bool have = false;
@@ -1539,6 +1541,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
       w.vl_n = n_g;
       w.vl_valid = true;
       w.vl_gen += 1;
+      w.vl_h = h;
       if ((int64_t)c.ov.cap < std::max(n_g, 1)) c.ov.resize(std::max(n_g, 1));
       vl_filter(s, vl_info);
       int* hi = reinterpret_cast<int*>(s.h_pinned);

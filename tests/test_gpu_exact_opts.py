@@ -10,6 +10,7 @@ and off, and the final states are compared bit for bit:
 * ABD_CHOL_SYNC_ANALYSIS -- analysis on the worker thread
 * ABD_CONTRIB_SORT    -- counting placement of the system contributions
 * ABD_BP_NO_GROUPS    -- static primitive groups in the primitive cull
+* ABD_GMD_EXHAUSTIVE  -- end-of-step global minimum distance by the widened broad phase
 """
 import os
 import subprocess
@@ -33,17 +34,19 @@ spec = {{"cube_drop": lambda: scenes.cube_drop(seed=0, n=2),
          "pile": lambda: scenes.icosphere_pile(seed=3, nx=2, ny=2, nz=3, mu=0.5, subdiv=1),
          "chainmail": lambda: scenes.chainmail(seed=0, n_chains=2, links=3, chains_x=2)}}[name]()
 model, state, params = spec.build()
-its = []
+its, mind, ipv = [], [], []
 with warnings.catch_warnings():
     warnings.simplefilter("ignore")
     for _ in range(steps):
         state, st = P.advance_step(model, state, params)
         its.append(st.iterations)
-np.savez(out, q=state.q, q_dot=state.q_dot, its=np.array(its))
+        mind.append(st.min_distance)
+        ipv.append(st.ip_value)
+np.savez(out, q=state.q, q_dot=state.q_dot, its=np.array(its), mind=np.array(mind), ipv=np.array(ipv))
 """
 
 OFF = {"ABD_CCD_NO_HOT": "1", "ABD_VL_MARGIN": "0", "ABD_CHOL_NO_EARLY": "1", "ABD_CHOL_SYNC_ANALYSIS": "1",
-       "ABD_CONTRIB_SORT": "1", "ABD_BP_NO_GROUPS": "1"}
+       "ABD_CONTRIB_SORT": "1", "ABD_BP_NO_GROUPS": "1", "ABD_GMD_EXHAUSTIVE": "1"}
 
 
 def _run(tmp_path, name, steps, extra_env, tag):
@@ -65,3 +68,5 @@ def test_optimisations_are_bitwise_exact(tmp_path, name, steps):
     assert np.array_equal(on["its"], off["its"])
     assert np.array_equal(on["q"], off["q"])
     assert np.array_equal(on["q_dot"], off["q_dot"])
+    assert np.array_equal(on["mind"], off["mind"])  # StepStats.min_distance (exhaustive vs fast stats search)
+    assert np.array_equal(on["ipv"], off["ipv"])
