@@ -427,18 +427,31 @@ __device__ __forceinline__ void group_box(const double* __restrict__ gb, const d
   }
 }
 
+template <bool RUNS>
 __global__ void __launch_bounds__(P2_THREADS, 3)
     k_prim_pairs2(PrimGeo g, GrpGeo gr, int use_groups, int64_t n_ov, const int2* __restrict__ ov,
                   const double* __restrict__ bbox, unsigned long long* counters, int64_t cap_vf, int64_t cap_ee,
-                  int4* out_vf, int4* out_ee, int cap_list, int2* tab, int* unsorted, int rank, int world,
+                  int4* out_vf, int4* out_ee, int cap_list, int3 cap_k, int2* tab, int* unsorted,
+                  int rank, int world,
                   unsigned long long* work, const int* n_ov_dev) {
   if (n_ov_dev) n_ov = *n_ov_dev;  // deferred count (Verlet-list filter result, no host sync)
   extern __shared__ double p2_sm[];
   double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
   double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
-  int* lists = reinterpret_cast<int*>(obx + 6 * (size_t)cap_list);  // [6][cap_list] local ids
-  unsigned* lpk = reinterpret_cast<unsigned*>(lists + 6 * (size_t)cap_list);  // packed local vertex ids
-  unsigned* hk = lpk + 6 * (size_t)cap_list;  // [P2_HCAP] hits of the current product
+  // survivor lists (list l = 3 side + kind) with per-kind capacities cap_k = (V, E, T)
+  const int ltot = 2 * (cap_k.x + cap_k.y + cap_k.z);
+  int* lists = reinterpret_cast<int*>(obx + 6 * (size_t)cap_list);  // [ltot] local ids
+  unsigned* lpk = reinterpret_cast<unsigned*>(lists + ltot);  // packed local vertex ids
+  unsigned* hk = lpk + ltot;  // [P2_HCAP] hits of the current product
+#define LOFF(l) ((l) / 3 * (cap_k.x + cap_k.y + cap_k.z) + ((l) % 3 > 0 ? cap_k.x : 0) + ((l) % 3 > 1 ? cap_k.y : 0))
+  // runs: the survivors of one static group are contiguous in their list; run k of
+  // list l covers [run_s, run_s + run_n) and carries a conservative float box of its
+  // survivors, so a product only pairs runs whose boxes overlap
+  __shared__ int nrun[6];
+  __shared__ unsigned short run_s[6][32], run_n[6][32];
+  __shared__ float run_b[6][32][6];
+  __shared__ unsigned tmask[32];
+  __shared__ int runs_ok;
   __shared__ int hcount;
   __shared__ unsigned long long hbase;
   __shared__ int meta[16];  // v0,e0,t0 (i) | v0,e0,t0 (j) | nv,ne,nt (i) | nv,ne,nt (j)
@@ -464,6 +477,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       meta[3 * side + kind] = a;
       meta[6 + 3 * side + kind] = b - a;
       lcount[threadIdx.x] = 0;
+      if (threadIdx.x == 0 && !use_groups) runs_ok = 0;  // (thread 64 writes it otherwise)
     } else if (threadIdx.x >= 32 && threadIdx.x < 35) {
       const int k = threadIdx.x - 32;
       obox[k] = fmax(bbox[6 * bi + k], bbox[6 * bj + k]);
@@ -474,7 +488,11 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int a = gr.off[kind][body];
       gfirst[l] = a;
       gcount[l] = gr.off[kind][body + 1] - a;
-      if (l == 0) ghits = 0;
+      nrun[l] = 0;
+      if (l == 0) {
+        ghits = 0;
+        runs_ok = RUNS ? 1 : 0;
+      }
     }
     __syncthreads();
     // vertex boxes of both bodies
@@ -515,14 +533,14 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
         bool keep = false;
         unsigned pk = 0;
         int id = 0;
+        double bxs[6];
         if (i < meta[6 + l]) {
           const int64_t gi = (int64_t)meta[l] + i;  // prim offset of the body (grouped order)
           pk = gr.pk[kind][gi];
           id = gr.id[kind][gi];
-          double bx[6];
-          box_from_packed(kind, pk, vb + 6 * side * P2_VCAP, bx);
-          keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] && bx[2] <= obox[5] &&
-                 obox[2] <= bx[5];
+          box_from_packed(kind, pk, vb + 6 * side * P2_VCAP, bxs);
+          keep = bxs[0] <= obox[3] && obox[0] <= bxs[3] && bxs[1] <= obox[4] && obox[1] <= bxs[4] &&
+                 bxs[2] <= obox[5] && obox[2] <= bxs[5];
         }
         // the whole warp works on one group (one list): one shared-memory atomic per warp
         const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -531,13 +549,43 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) {
           const int at = base + __popc(m & ((1u << lane) - 1));
-          lists[l * cap_list + at] = id;
-          lpk[l * cap_list + at] = pk;
+          lists[LOFF(l) + at] = id;
+          lpk[LOFF(l) + at] = pk;
+        }
+        if (RUNS && m) {
+          // the run's box: union of its survivors' boxes, rounded outward to float
+          double lo0 = keep ? bxs[0] : INFINITY, lo1 = keep ? bxs[1] : INFINITY, lo2 = keep ? bxs[2] : INFINITY;
+          double hi0 = keep ? bxs[3] : -INFINITY, hi1 = keep ? bxs[4] : -INFINITY, hi2 = keep ? bxs[5] : -INFINITY;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            lo0 = fmin(lo0, __shfl_xor_sync(0xffffffffu, lo0, o));
+            lo1 = fmin(lo1, __shfl_xor_sync(0xffffffffu, lo1, o));
+            lo2 = fmin(lo2, __shfl_xor_sync(0xffffffffu, lo2, o));
+            hi0 = fmax(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+            hi1 = fmax(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+            hi2 = fmax(hi2, __shfl_xor_sync(0xffffffffu, hi2, o));
+          }
+          if (lane == 0) {
+            const int k = atomicAdd(&nrun[l], 1);
+            if (k < 32) {
+              run_s[l][k] = (unsigned short)base;
+              run_n[l][k] = (unsigned short)__popc(m);
+              run_b[l][k][0] = __double2float_rd(lo0);
+              run_b[l][k][1] = __double2float_rd(lo1);
+              run_b[l][k][2] = __double2float_rd(lo2);
+              run_b[l][k][3] = __double2float_ru(hi0);
+              run_b[l][k][4] = __double2float_ru(hi1);
+              run_b[l][k][5] = __double2float_ru(hi2);
+            } else {
+              runs_ok = 0;
+            }
+          }
         }
       }
-    } else // one cull pass over the six lists (list id = 3 * side + kind); topology is
+    } else  // one cull pass over the six lists (list id = 3 * side + kind); topology is
     // prefetched 4 primitives per thread, survivors keep id + packed local vertex ids
     {
+      if (threadIdx.x == 0) runs_ok = 0;  // no runs on this path
       const int tot = meta[6] + meta[7] + meta[8] + meta[9] + meta[10] + meta[11];
       for (int t0 = threadIdx.x; t0 < tot; t0 += 4 * P2_THREADS) {
         unsigned pk[4];
@@ -578,8 +626,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
                             bx[2] <= obox[5] && obox[2] <= bx[5];
           if (keep) {
             const int at = atomicAdd(&lcount[l], 1);
-            lists[l * cap_list + at] = loc[u];
-            lpk[l * cap_list + at] = pk[u];
+            lists[LOFF(l) + at] = loc[u];
+            lpk[LOFF(l) + at] = pk[u];
           }
         }
       }
@@ -605,7 +653,22 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       if (threadIdx.x == 0) hcount = 0;
       // materialise the loop side's boxes
       for (int t = threadIdx.x; t < nl; t += P2_THREADS)
-        box_from_packed(kl, lpk[ll * cap_list + t], vb + 6 * sl * P2_VCAP, obx + 6 * t);
+        box_from_packed(kl, lpk[LOFF(ll) + t], vb + 6 * sl * P2_VCAP, obx + 6 * t);
+      // run-pair mask: bit j of tmask[k] = run k of the thread side meets run j of the loop side
+      // (only for large products: for small ones the plain warp-synchronous sweep wins)
+      const bool use_runs = RUNS && runs_ok != 0 && nt * nl >= 4096;  // uniform
+      const int nrt = use_runs ? min(nrun[lt], 32) : 0, nrl = use_runs ? min(nrun[ll], 32) : 1;
+      if (RUNS && use_runs) {
+        for (int t = threadIdx.x; t < 32; t += P2_THREADS) tmask[t] = 0u;
+        __syncthreads();
+        for (int t = threadIdx.x; t < nrt * nrl; t += P2_THREADS) {
+          const int k = t / nrl, j = t % nrl;
+          const float* A = run_b[lt][k];
+          const float* B = run_b[ll][j];
+          if (A[0] <= B[3] && B[0] <= A[3] && A[1] <= B[4] && B[1] <= A[4] && A[2] <= B[5] && B[2] <= A[5])
+            atomicOr(&tmask[k], 1u << j);
+        }
+      }
       __syncthreads();
       const bool is_vf = prod < 2;
       const int body_a = prod == 1 ? bj : bi, body_b = prod == 1 ? bi : bj;
@@ -620,13 +683,48 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
           if (threadIdx.x == 0) hcount = 0;
           __syncthreads();
         }
+        if (RUNS && use_runs && pass == 0) {
+          // filtered: each (own, chunk) thread walks only the loop-side runs its own
+          // run's box meets; runs of disjoint boxes hold no overlapping primitive pair
+          for (int base = 0; base < nt * G; base += P2_THREADS) {
+            const int idx = base + threadIdx.x;
+            if (idx >= nt * G) break;
+            const int own = idx % nt, chunk = idx / nt;
+            int kr = 0;  // the run holding own (runs are appended in any order)
+            for (int k = 0; k < nrt; ++k)
+              if (own >= run_s[lt][k] && own < run_s[lt][k] + run_n[lt][k]) kr = k;
+            double ob[6];
+            const int own_local = lists[LOFF(lt) + own];
+            box_from_packed(kt, lpk[LOFF(lt) + own], vb + 6 * st_ * P2_VCAP, ob);
+            unsigned mk = tmask[kr];
+            int cyc = 0;  // position in this thread's filtered sequence mod G (chunks take every G-th)
+            while (mk) {
+              const int j = __ffs(mk) - 1;
+              mk &= mk - 1;
+              const int y0 = run_s[ll][j], y1 = y0 + run_n[ll][j];
+              for (int y = y0; y < y1; ++y) {
+                const bool mine = cyc == chunk;
+                if (++cyc == G) cyc = 0;
+                if (!mine) continue;
+                const double* b2 = obx + 6 * y;
+                if (ob[0] <= b2[3] && b2[0] <= ob[3] && ob[1] <= b2[4] && b2[1] <= ob[4] && ob[2] <= b2[5] &&
+                    b2[2] <= ob[5]) {
+                  const int at = atomicAdd(&hcount, 1);
+                  const int yl = lists[LOFF(ll) + y];
+                  const int pa = a_thr ? own_local : yl, pb = a_thr ? yl : own_local;
+                  if (at < P2_HCAP) hk[at] = ((unsigned)pa << 16) | (unsigned)pb;
+                }
+              }
+            }
+          }
+        } else
         for (int base = 0; base < nt * G; base += P2_THREADS) {
           const int idx = base + threadIdx.x;
           const bool live = idx < nt * G;
           const int own = live ? idx % nt : 0, chunk = idx / nt;
           double ob[6];
-          const int own_local = live ? lists[lt * cap_list + own] : 0;
-          if (live) box_from_packed(kt, lpk[lt * cap_list + own], vb + 6 * st_ * P2_VCAP, ob);
+          const int own_local = live ? lists[LOFF(lt) + own] : 0;
+          if (live) box_from_packed(kt, lpk[LOFF(lt) + own], vb + 6 * st_ * P2_VCAP, ob);
           const int y0 = chunk * Lc;
           for (int yy = 0; yy < Lc; ++yy) {
             const int y = y0 + yy;
@@ -644,7 +742,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
               b0 = __shfl_sync(0xffffffffu, b0, __ffs(m) - 1);
               if (hit) {
                 const int at = b0 + __popc(m & ((1u << lane) - 1));
-                const int yl = lists[ll * cap_list + y];
+                const int yl = lists[LOFF(ll) + y];
                 const int pa = a_thr ? own_local : yl, pb = a_thr ? yl : own_local;
                 if (pass == 0) {
                   if (at < P2_HCAP) hk[at] = ((unsigned)pa << 16) | (unsigned)pb;
@@ -1196,14 +1294,16 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
     CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
     static bool attr = false;
     const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
+    const int3 cap_k = make_int3(s.max_v, s.max_e, s.max_t);
     const size_t p2_smem = sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) +
-                           2 * sizeof(int) * 6 * (size_t)cap_list + sizeof(unsigned) * P2_HCAP;
+                           2 * sizeof(int) * 2 * (size_t)(cap_k.x + cap_k.y + cap_k.z) + sizeof(unsigned) * P2_HCAP;
     const bool use2 = (s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1")) || s.comm.world > 1;
     if (s.comm.world > 1 && !(s.max_v <= P2_VCAP && p2_smem <= 100 * 1024))
       throw Error(ABD_ERR_ARG, "partitioned broad phase needs <= 256 vertices per body");
     if (!attr) {
       CK(cudaFuncSetAttribute((void*)k_prim_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BP_SMEM));
-      CK(cudaFuncSetAttribute((void*)k_prim_pairs2, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      CK(cudaFuncSetAttribute((void*)k_prim_pairs2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+      CK(cudaFuncSetAttribute((void*)k_prim_pairs2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
       attr = true;
     }
     if (s.instrument) CK(cudaEventRecord(s.ev0, st));
@@ -1222,9 +1322,15 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
         gg.off[k] = s.grp_off[k].p;
       }
       const int ug = s.has_groups && !no_groups ? 1 : 0;
-      k_prim_pairs2<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, ov, bbox, counters, (int64_t)vf.cap,
-                                                       (int64_t)ee.cap, vf.p, ee.p, cap_list, w.tab.p,
-                                                       unsorted, s.comm.rank, s.comm.world, w.ull.p + 11, n_ov_dev);
+      // run-pair filtering of the products pays for large meshes (tori: 960 edges +
+      // triangles per body, products of thousands of pairs); for the pile's
+      // icospheres (800) the plain sweep is faster
+      static const int runs_env = getenv("ABD_BP_RUNS") ? atoi(getenv("ABD_BP_RUNS")) : -1;
+      const int runs = runs_env >= 0 ? runs_env : (s.max_e + s.max_t > 800 ? 1 : 0);
+      auto kfn = runs ? k_prim_pairs2<true> : k_prim_pairs2<false>;
+      kfn<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, ov, bbox, counters, (int64_t)vf.cap, (int64_t)ee.cap,
+                                             vf.p, ee.p, cap_list, cap_k, w.tab.p, unsorted, s.comm.rank,
+                                             s.comm.world, w.ull.p + 11, n_ov_dev);
     } else {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
       k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, ov, bbox, counters, (int64_t)vf.cap,

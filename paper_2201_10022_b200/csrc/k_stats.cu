@@ -108,16 +108,21 @@ __global__ void k_pair_min_d2(SceneView sv, const int* __restrict__ vb_off_unuse
 // at the next step, so they may be overwritten): the broad phase at q with vertex
 // boxes inflated by hp gives every primitive pair whose box gap is <= 2 hp; the
 // minimum distance m over them is the global minimum whenever m <= 2 hp, because a
-// closer pair would have a box gap < m and be a candidate.  hp grows 4x per attempt;
-// after three the exhaustive search below decides.
+// closer pair would have a box gap < m and be a candidate.  hp grows 2x per attempt;
+// after four the exhaustive search below decides.
 double global_min_distance_stats(Scene& s, const double* q) {
   static const bool off = getenv("ABD_GMD_EXHAUSTIVE") != nullptr;
   if (!off && s.B >= 2 && s.has_groups) {
-    double hp = 0.1 * (s.w.vl_cell > 0.0 ? s.w.vl_cell : 1.0);
-    for (int attempt = 0; attempt < 3; ++attempt, hp *= 4.0) {
+    // first inflation just covers the previous step's minimum (it changes slowly):
+    // a tight candidate set, widened 2x per miss
+    double hp = s.w.gmd_prev > 0.0 ? 0.55 * s.w.gmd_prev : 0.02 * (s.w.vl_cell > 0.0 ? s.w.vl_cell : 1.0);
+    for (int attempt = 0; attempt < 4; ++attempt, hp *= 2.0) {
       broad_phase(s, q, q, 2.0 * hp);
       const double cm = candidate_min_d2(s, q);
-      if (cm <= (2.0 * hp) * (2.0 * hp)) return std::sqrt(cm);
+      if (cm <= (2.0 * hp) * (2.0 * hp)) {
+        s.w.gmd_prev = std::sqrt(cm);
+        return s.w.gmd_prev;
+      }
     }
   }
   return global_min_distance(s, q);

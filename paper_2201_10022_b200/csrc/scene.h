@@ -258,6 +258,7 @@ struct Scene {
     int vl_gen = 0;
     double vl_cell = 0.0;
     double vl_h = -1.0;  // vertex-box inflation the superset was built for
+    double gmd_prev = 0.0;  // last end-of-step global minimum distance (first inflation guess)
     // primitive-pair superset ("primitive Verlet list"): the candidate rows of the body
     // superset for vertex boxes inflated by pvl_m, built for the sweep [pvl_q0, pvl_q1];
     // valid while every body stays within pvl_m / 2 of that sweep (k_pvl_check)
