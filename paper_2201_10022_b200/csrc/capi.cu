@@ -853,18 +853,14 @@ int abd_get_system(abd_scene* h, double* grad, double* diag, int64_t* off_keys, 
 int abd_solve_resident(abd_scene* h, double rel_tol, int max_iters, double* dx, int* iters, double* rel_res) {
   return guard([&] {
     SC(h);
-    int64_t N = 12 * (int64_t)s.H.n;
-    DVec<double> neg, x;
-    neg.resize(std::max<int64_t>(N, 1));
-    x.resize(std::max<int64_t>(N, 1));
-    std::vector<double> g(N);
-    s.grad.download(g.data(), N, s.stream);
-    sync(s.stream);
-    for (auto& v : g) v = -v;
-    neg.upload(g.data(), N, s.stream);
+    const int64_t N = 12 * (int64_t)s.H.n;
+    // -g and x stay on the device (the scene's persistent Newton workspaces)
+    s.w.neg.resize(std::max<int64_t>(N, 1));
+    s.dx.resize(std::max<int64_t>(N, 1));
+    launch_neg(s.stream, N, s.grad.p, s.w.neg.p);
     double rel = 0.0;
-    int it = pcg_solve(s, neg.p, x.p, rel_tol, max_iters, rel);
-    x.download(dx, N, s.stream);
+    int it = pcg_solve(s, s.w.neg.p, s.dx.p, rel_tol, max_iters, rel);
+    s.dx.download(dx, N, s.stream);
     sync(s.stream);
     if (iters) *iters = it;
     if (rel_res) *rel_res = rel;
@@ -874,18 +870,13 @@ int abd_solve_resident(abd_scene* h, double rel_tol, int max_iters, double* dx, 
 int abd_solve_resident_cholesky(abd_scene* h, double rel_tol, double* dx, int* solves, double* rel_res) {
   return guard([&] {
     SC(h);
-    int64_t N = 12 * (int64_t)s.H.n;
-    DVec<double> neg, x;
-    neg.resize(std::max<int64_t>(N, 1));
-    x.resize(std::max<int64_t>(N, 1));
-    std::vector<double> g(N);
-    s.grad.download(g.data(), N, s.stream);
-    sync(s.stream);
-    for (auto& v : g) v = -v;
-    neg.upload(g.data(), N, s.stream);
+    const int64_t N = 12 * (int64_t)s.H.n;
+    s.w.neg.resize(std::max<int64_t>(N, 1));
+    s.dx.resize(std::max<int64_t>(N, 1));
+    launch_neg(s.stream, N, s.grad.p, s.w.neg.p);
     double rel = 0.0;
-    int ns = chol_solve(s, neg.p, x.p, rel_tol, rel);
-    x.download(dx, N, s.stream);
+    int ns = chol_solve(s, s.w.neg.p, s.dx.p, rel_tol, rel);
+    s.dx.download(dx, N, s.stream);
     sync(s.stream);
     if (solves) *solves = ns;
     if (rel_res) *rel_res = rel;

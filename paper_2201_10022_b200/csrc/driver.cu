@@ -65,6 +65,12 @@ __global__ void k_neg(int64_t n, const double* __restrict__ a, double* b) {
   if (i < n) b[i] = -a[i];
 }
 
+void launch_neg(cudaStream_t st, int64_t n, const double* a, double* b) {
+  if (n <= 0) return;
+  k_neg<<<grid_for(n, 256), 256, 0, st>>>(n, a, b);
+  note_launch("k_neg");
+}
+
 // per dynamic body ||A A^T - I||_F (ortho_error, body.py:216-220), max via bits
 __global__ void k_ortho_err(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ q,
                             unsigned long long* out) {

@@ -13,6 +13,7 @@ int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_it
 // k_chol.cu: sparse block Cholesky + refinement; returns the number of triangular solves
 int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine = 3);
 void chol_begin(Scene& s, const double* rhs, double* x);
+void launch_neg(cudaStream_t st, int64_t n, const double* a, double* b);  // b = -a
 // the host analysis of the coupling structure copied out by mark_structure runs on a
 // worker thread while the pair-block / reduction kernels are launched (post), or is
 // discarded when the pattern changes (drop)
