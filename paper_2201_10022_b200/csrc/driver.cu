@@ -716,6 +716,13 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   }
   st.last_dq_over_dt = last_dq;
   st.candidates = max_c;
+  // an early analysis posted for an iteration that did not come belongs to no
+  // structure a later call may assemble: discard it
+  if (s.w.ch_early) {
+    chol_analysis_drop(s);
+    s.w.ch_early = false;
+    s.w.ch_pre = false;
+  }
   k_qdot<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.dyn.p, s.q.p, s.q0.p, P.dt, s.q_dot.p);
   note_launch("k_qdot");
   // stats (solver.py:604-627)
