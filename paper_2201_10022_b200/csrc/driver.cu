@@ -360,7 +360,7 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   SSYNC(st);
   {
     // this line search's slow queries are the next iteration's hot list
-    const int n_slow = std::min<int>(*reinterpret_cast<const int*>(hp + 10), CCD_HOT_CAP);
+    const int n_slow = std::max(0, std::min<int>(*reinterpret_cast<const int*>(hp + 10), CCD_HOT_CAP));
     w.hot_rows.resize(CCD_HOT_CAP);
     w.hot_kind.resize(CCD_HOT_CAP);
     if (n_slow > 0) {

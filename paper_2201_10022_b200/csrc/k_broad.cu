@@ -1277,7 +1277,8 @@ __global__ void k_pvl_check(int B, const double* __restrict__ q0, const double* 
 // (overlap pair, product, prim_a, prim_b), or canonical order when a chunk overflowed
 static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double h, const int2* ov, int& n_ov,
                            const double* bbox, DVec<int4>& vf, DVec<int4>& ee, int64_t& n_vf, int64_t& n_ee,
-                           int* ov_same, bool& ov_same_h, const int* n_ov_dev = nullptr, int* viol_h = nullptr) {
+                           int* ov_same, bool& ov_same_h, const int* n_ov_dev = nullptr, int* viol_h = nullptr,
+                           bool no_prezero = false) {
   // n_ov_dev: the pair count is on the device (n_ov is then only a capacity); it is
   // read back with the candidate counts, together with the Verlet-list violation flag
   const int n_cap = n_ov;
@@ -1291,7 +1292,8 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
   if (ee.cap < 1024) ee.resize(1024);
   unsigned long long* hc = reinterpret_cast<unsigned long long*>(s.h_pinned);
   for (int attempt = 0; attempt < 3; ++attempt) {
-    CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
+    // the counters, overflow flag and work queue start zeroed (broad_phase); retries re-zero
+    if (attempt > 0 || no_prezero) CK(cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st));
     static bool attr = false;
     const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
     const int3 cap_k = make_int3(s.max_v, s.max_e, s.max_t);
@@ -1311,8 +1313,10 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
       int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n_cap, (int64_t)s.num_sms * 3));
       w.tab.resize(3 * (size_t)std::max(n_cap, 1));
       if (s.comm.world > 1) CK(cudaMemsetAsync(w.tab.p, 0, 3 * (size_t)n_cap * sizeof(int2), st));
-      CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
-      CK(cudaMemsetAsync(w.ull.p + 11, 0, sizeof(unsigned long long), st));
+      if (attempt > 0 || no_prezero) {
+        CK(cudaMemsetAsync(unsorted, 0, sizeof(int), st));
+        CK(cudaMemsetAsync(w.ull.p + 11, 0, sizeof(unsigned long long), st));
+      }
       static const bool no_groups = getenv("ABD_BP_NO_GROUPS") != nullptr;
       GrpGeo gg{};
       for (int k = 0; k < 3; ++k) {
@@ -1431,7 +1435,7 @@ static void prim_stage(Scene& s, const double* q0, const double* q1, double h, i
         CK(cudaMemsetAsync(no_same, 0, sizeof(int), st));
         int n_sup = (int)w.vl_n;
         prim_pairs_run(s, q0, q1, h + m, w.vl_pairs.p, n_sup, w.vl_box.p, w.pvl_vf, w.pvl_ee, w.pvl_nvf,
-                       w.pvl_nee, no_same, dummy);
+                       w.pvl_nee, no_same, dummy, nullptr, nullptr, /*no_prezero=*/true);
         w.pvl_q0.resize(12 * (size_t)s.B);
         w.pvl_q1.resize(12 * (size_t)s.B);
         CK(cudaMemcpyAsync(w.pvl_q0.p, q0, 12 * (size_t)s.B * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1503,11 +1507,11 @@ __global__ void k_vl_flags(int64_t n, const int2* __restrict__ sup, const double
 
 // the Verlet-list filter over the whole GPU: containment flag, overlap flags and an
 // ordered (stable) compaction into c.ov; info = {count, violation} on the device
-static void vl_filter(Scene& s, int* info) {
+static void vl_filter(Scene& s, int* info, bool zero_info) {
   cudaStream_t st = s.stream;
   Scene::Work& w = s.w;
   Cands& c = s.cands;
-  CK(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
+  if (zero_info) CK(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
   k_vl_contain<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, info + 1);
   note_launch("k_vl_contain");
   if (w.vl_n == 0) return;
@@ -1526,6 +1530,10 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   Cands& c = s.cands;
   Scene::Work& w = s.w;
   c.n_vf = c.n_ee = c.n_ov = 0;
+  // one memset for this broad phase's device scalars (w.ull[4..13]: pair / candidate
+  // counters, overflow flag, work queue, pattern flag, Verlet-list info) and the
+  // following line search's slow-query counter
+  CK(cudaMemsetAsync(w.ull.p + 4, 0, 10 * sizeof(unsigned long long), st));
   if (s.B < 2) return;
   s.bbox.resize(6 * s.B);
   k_body_boxes<<<grid_for((int64_t)s.B * 32, 256), 256, 0, st>>>(s.B, s.v_off.p, s.rest.p, q0, q1, h, s.bbox.p);
@@ -1545,15 +1553,13 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   const bool defer = use_vl && w.vl_valid && !no_defer && s.max_v <= P2_VCAP && !getenv("ABD_BP_V1");
   if (defer) {
     if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
-    vl_filter(s, vl_info);
-    int* ov_same = reinterpret_cast<int*>(w.ull.p + 9);
+    vl_filter(s, vl_info, false);
+    int* ov_same = reinterpret_cast<int*>(w.ull.p + 9);  // zeroed with the broad phase's scalars
     if (w.pat_valid && s.H.n == s.n_dyn) {
       dev_set_i32(st, ov_same, 1);
       k_ov_in_pattern<<<grid_for(std::max<int64_t>(w.vl_n, 1), 256), 256, 0, st>>>(
           w.vl_n, c.ov.p, s.slot.p, s.H.n_off, s.H.upper_keys.p, ov_same, vl_info);
       note_launch("k_ov_in_pattern");
-    } else {
-      CK(cudaMemsetAsync(ov_same, 0, sizeof(int), st));
     }
     int n_cap = (int)w.vl_n;
     int viol = 0;
@@ -1569,7 +1575,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   }
   if (use_vl && w.vl_valid) {
     if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
-    vl_filter(s, vl_info);
+    vl_filter(s, vl_info, true);
     int* hi = reinterpret_cast<int*>(s.h_pinned);
     pack_to_host(st, hi, {{vl_info, 8, 0}});
     SSYNC(st);
@@ -1649,7 +1655,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
       w.vl_gen += 1;
       w.vl_h = h;
       if ((int64_t)c.ov.cap < std::max(n_g, 1)) c.ov.resize(std::max(n_g, 1));
-      vl_filter(s, vl_info);
+      vl_filter(s, vl_info, true);
       int* hi = reinterpret_cast<int*>(s.h_pinned);
       pack_to_host(st, hi, {{vl_info, 8, 0}, {w.scal.p, 8, 8}});
       SSYNC(st);

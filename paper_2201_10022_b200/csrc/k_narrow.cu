@@ -933,8 +933,7 @@ void launch_ccd_both(Scene& s, const double* q, const double* dq, double slack, 
     h.slow_kind = w.slow_kind.p;
     h.slow_cnt = reinterpret_cast<unsigned*>(w.ull.p + 12);
     h.slow_cap = CCD_HOT_CAP;
-    h.slow_it = CCD_SLOW_IT;
-    CK(cudaMemsetAsync(h.slow_cnt, 0, sizeof(unsigned), s.stream));
+    h.slow_it = CCD_SLOW_IT;  // slow_cnt was zeroed with the broad phase's scalars
     if (w.hot_pending) {
       CK(cudaStreamWaitEvent(s.stream, s.hot_ev, 0));
       h.rows = w.hot_rows.p;
