@@ -165,13 +165,28 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
   pair_points(sv, ids, q, z, xb);
   out_bodies[slot] = make_int2(r.x, r.z);
   if (KIND == KIND_EE && ee_mollified(z, ids.eps)) {
-    moll_list[atomicAdd(moll_count, 1)] = (int)slot;
+    if (moll_list) moll_list[atomicAdd(moll_count, 1)] = (int)slot;
     return;
   }
   double* blk = out_blk + slot * PB_STRIDE;
   PairEval ev = contact_pair_eval<true, 1>(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0,
                                            project != 0, blk);
   out_d2[slot] = ev.d2;
+}
+
+// the mollified active EE slots, listed ahead of the pair-block kernels so their
+// (slower) 9-column records build on a side stream beside the plain EE pairs
+__global__ void k_moll_classify(SceneView sv, int64_t count, const int* __restrict__ act, int64_t cand_off,
+                                const int4* __restrict__ rows, const double* __restrict__ q, int64_t slot_off,
+                                int* moll_list, int* moll_count) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int64_t slot = slot_off + t;
+  int4 r = rows[act[slot] - cand_off];
+  PairIds ids = pair_ids(sv, KIND_EE, r);
+  V3 z[4], xb[4];
+  pair_points(sv, ids, q, z, xb);
+  if (ee_mollified(z, ids.eps)) moll_list[atomicAdd(moll_count, 1)] = (int)slot;
 }
 
 // Warp-parallel PSD clamp of a symmetric 9x9 (padded to 10) in shared memory:
@@ -874,13 +889,31 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
   } else {
     s.w.moll.resize(std::max<int64_t>(count, 1));
     CK(cudaMemsetAsync(moll_count, 0, sizeof(int), s.stream));
-    k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q,
-                                                                        kappa, dh, project, slot_off, s.pblk.bodies.p,
-                                                                        s.pblk.blk.p, s.pblk.d2.p, s.w.moll.p,
-                                                                        moll_count);
+    static const bool serial = getenv("ABD_MOLL_SERIAL") != nullptr;
     const int grid = (int)std::min<int64_t>(grid_for(count, MOLL_WARPS), 16 * (int64_t)s.num_sms);
-    k_pair_blocks_moll<<<grid, 32 * MOLL_WARPS, 0, s.stream>>>(view(s), s.w.moll.p, moll_count, act, cand_off, rows,
-                                                               q, kappa, dh, project, s.pblk.blk.p, s.pblk.d2.p);
+    if (serial) {
+      k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(
+          view(s), kind, count, act, cand_off, rows, q, kappa, dh, project, slot_off, s.pblk.bodies.p, s.pblk.blk.p,
+          s.pblk.d2.p, s.w.moll.p, moll_count);
+      k_pair_blocks_moll<<<grid, 32 * MOLL_WARPS, 0, s.stream>>>(view(s), s.w.moll.p, moll_count, act, cand_off,
+                                                                 rows, q, kappa, dh, project, s.pblk.blk.p,
+                                                                 s.pblk.d2.p);
+    } else {
+      // list the mollified slots, build them on side3 while the plain EE pairs run here
+      k_moll_classify<<<grid_for(count, 256), 256, 0, s.stream>>>(view(s), count, act, cand_off, rows, q, slot_off,
+                                                                  s.w.moll.p, moll_count);
+      note_launch("k_moll_classify");
+      CK(cudaEventRecord(s.moll_fork_ev, s.stream));
+      CK(cudaStreamWaitEvent(s.side3, s.moll_fork_ev, 0));
+      k_pair_blocks_moll<<<grid, 32 * MOLL_WARPS, 0, s.side3>>>(view(s), s.w.moll.p, moll_count, act, cand_off,
+                                                                rows, q, kappa, dh, project, s.pblk.blk.p,
+                                                                s.pblk.d2.p);
+      CK(cudaEventRecord(s.moll_ev, s.side3));
+      k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(
+          view(s), kind, count, act, cand_off, rows, q, kappa, dh, project, slot_off, s.pblk.bodies.p, s.pblk.blk.p,
+          s.pblk.d2.p, nullptr, nullptr);
+      CK(cudaStreamWaitEvent(s.stream, s.moll_ev, 0));
+    }
     note_launch("k_pair_blocks_moll");
   }
   note_launch("k_pair_blocks");

@@ -44,6 +44,9 @@ Scene::Scene() {
   CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&side3, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&moll_fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&moll_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&hot_fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&hot_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&pb_fork_ev, cudaEventDisableTiming));
@@ -67,6 +70,9 @@ Scene::~Scene() {
   if (fork_ev) cudaEventDestroy(fork_ev);
   if (join_ev) cudaEventDestroy(join_ev);
   if (side2) cudaStreamDestroy(side2);
+  if (side3) cudaStreamDestroy(side3);
+  if (moll_fork_ev) cudaEventDestroy(moll_fork_ev);
+  if (moll_ev) cudaEventDestroy(moll_ev);
   if (hot_fork_ev) cudaEventDestroy(hot_fork_ev);
   if (hot_ev) cudaEventDestroy(hot_ev);
   if (pb_fork_ev) cudaEventDestroy(pb_fork_ev);

@@ -172,6 +172,8 @@ struct Scene {
   cudaStream_t side2 = nullptr;  // early ACCD of the hot queries (overlaps the broad phase)
   cudaEvent_t hot_fork_ev = nullptr, hot_ev = nullptr;
   cudaEvent_t pb_fork_ev = nullptr, pb_ev = nullptr;  // VF pair blocks on side2
+  cudaStream_t side3 = nullptr;  // mollified EE pair blocks beside the plain EE pairs
+  cudaEvent_t moll_fork_ev = nullptr, moll_ev = nullptr;
   int num_sms = 148;
 
   // geometry (immutable after create)

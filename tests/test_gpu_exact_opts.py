@@ -11,6 +11,7 @@ and off, and the final states are compared bit for bit:
 * ABD_CONTRIB_SORT    -- counting placement of the system contributions
 * ABD_BP_NO_GROUPS    -- static primitive groups in the primitive cull
 * ABD_GMD_EXHAUSTIVE  -- end-of-step global minimum distance by the widened broad phase
+* ABD_MOLL_SERIAL     -- mollified EE pair blocks on a side stream beside the plain EE pairs
 """
 import os
 import subprocess
@@ -46,7 +47,8 @@ np.savez(out, q=state.q, q_dot=state.q_dot, its=np.array(its), mind=np.array(min
 """
 
 OFF = {"ABD_CCD_NO_HOT": "1", "ABD_VL_MARGIN": "0", "ABD_CHOL_NO_EARLY": "1", "ABD_CHOL_SYNC_ANALYSIS": "1",
-       "ABD_CONTRIB_SORT": "1", "ABD_BP_NO_GROUPS": "1", "ABD_GMD_EXHAUSTIVE": "1"}
+       "ABD_CONTRIB_SORT": "1", "ABD_BP_NO_GROUPS": "1", "ABD_GMD_EXHAUSTIVE": "1",
+       "ABD_MOLL_SERIAL": "1"}
 
 
 def _run(tmp_path, name, steps, extra_env, tag):
