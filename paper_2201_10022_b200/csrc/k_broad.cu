@@ -59,12 +59,30 @@ __global__ void k_body_boxes(int B, const int* __restrict__ v_off, const double*
   int lane = threadIdx.x & 31;
   if (w >= B) return;
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int v = v_off[w] + lane; v < v_off[w + 1]; v += 32) {
-    double b[6];
-    vertex_box(rest, v, q0 + 12 * (int64_t)w, q1 + 12 * (int64_t)w, h, b);
-    for (int k = 0; k < 3; ++k) {
-      lo[k] = fmin(lo[k], b[k]);
-      hi[k] = fmax(hi[k], b[3 + k]);
+  // BB_UNROLL vertices per lane in flight: their rest loads issue together instead
+  // of one DRAM round trip per vertex (min / max do not depend on the order)
+  constexpr int BB_UNROLL = 4;
+  const int v0 = v_off[w], v1 = v_off[w + 1];
+  const double* q0b = q0 + 12 * (int64_t)w;
+  const double* q1b = q1 + 12 * (int64_t)w;
+  for (int base = v0 + lane; base < v1; base += 32 * BB_UNROLL) {
+    V3 xb[BB_UNROLL];
+#pragma unroll
+    for (int u = 0; u < BB_UNROLL; ++u) {
+      const int v = base + 32 * u;
+      if (v < v1) xb[u] = ld3(rest + 3 * (int64_t)v);
+    }
+#pragma unroll
+    for (int u = 0; u < BB_UNROLL; ++u) {
+      if (base + 32 * u >= v1) break;
+      const V3 a = world_pos(q0b, xb[u]);
+      const V3 c = world_pos(q1b, xb[u]);
+      lo[0] = fmin(lo[0], xsub(fmin(a.x, c.x), h));
+      lo[1] = fmin(lo[1], xsub(fmin(a.y, c.y), h));
+      lo[2] = fmin(lo[2], xsub(fmin(a.z, c.z), h));
+      hi[0] = fmax(hi[0], xadd(fmax(a.x, c.x), h));
+      hi[1] = fmax(hi[1], xadd(fmax(a.y, c.y), h));
+      hi[2] = fmax(hi[2], xadd(fmax(a.z, c.z), h));
     }
   }
   for (int o = 16; o > 0; o >>= 1)
