@@ -44,12 +44,13 @@ __global__ void k_alpha_trial(int64_t n, const double* __restrict__ q, const dou
   out[i] = xadd(q[i], xmul(alpha, dq[i]));
 }
 
-__global__ void k_expand_dq(int n_dyn, const int* __restrict__ dyn_body, const double* __restrict__ dx, double sign,
+// dq over all bodies: sign * dx for dynamic bodies, 0 for static ones (no memset)
+__global__ void k_expand_dq(int B, const int* __restrict__ slot, const double* __restrict__ dx, double sign,
                             double* dq) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= 12 * (int64_t)n_dyn) return;
-  int s = (int)(t / 12), c = (int)(t % 12);
-  dq[12 * (int64_t)dyn_body[s] + c] = sign * dx[t];
+  if (t >= 12 * (int64_t)B) return;
+  const int k = slot[t / 12];
+  dq[t] = k >= 0 ? sign * dx[12 * (int64_t)k + t % 12] : 0.0;
 }
 
 __global__ void k_qdot(int B, const unsigned char* __restrict__ dyn, const double* __restrict__ q,
@@ -676,8 +677,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         dsrc = s.grad.p;
         sign = -1.0;
       }
-      s.dq.zero(stream);
-      k_expand_dq<<<grid_for(ND, 256), 256, 0, stream>>>(s.n_dyn, s.dyn_body.p, dsrc, sign, s.dq.p);
+      k_expand_dq<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.slot.p, dsrc, sign, s.dq.p);
       note_launch("k_expand_dq");
       // the previous line search's slowest ACCD queries start now on side2 (exact,
       // without the shared cut) and overlap the broad phase
