@@ -1,27 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark: fp64 ABD Newton steps on the 10k-body icosphere pile (BASELINE config 4).
+"""Benchmark: fp64 ABD Newton steps on the 10k-body pile (BASELINE config 4).
 
-    python bench.py [--gpus N --steps K --warmup W --start S]
-    python bench.py --impl reference ...        (CPU oracle arm)
+    python bench.py [--gpus N --steps K --warmup W]
+    python bench.py --impl reference ...        (the reference path on the host CPU)
+    python bench.py --workload {micro,chainmail,cubes,boxstack} ...
 
 A "step" is one implicit time step (`advance_step`: broad phase, friction
 precompute, Newton loop with assembly / Cholesky / CCD / line search, stats).
-By default the timed steps are [153, 163) from the committed step-150
-checkpoint of the 200-step pile run (the late, contact-dense phase);
-`--ckpt none --start S` times [S + W, S + W + K) from the seeded initial state.
-`value` is measured on the device-resident C-ABI path; `e2e` repeats the same
-window through the Python API (`advance_step`) with host numpy state (H2D q,
-q_dot, forces and D2H q, q_dot every step).  Under torchrun (N > 1) the ranks
-partition ONE pile (per-pair work split by overlap body pair, NCCL all-reduce
-of the system, replicated solve): strong scaling, max-over-ranks device time.
+
+Pile (headline).  The late, contact-dense window [150, 200) of the 200-step run
+is stepped in full from the committed checkpoint `bench_data/pile_step150.npz`
+(the GPU state after 150 steps; SimState is the complete inter-step state), each
+step timed with CUDA events on the scene stream.  `value` = K / (sum of the K
+step times), the K steps spread evenly over the 50-step window; `config` also
+reports the whole window and the full 200-step run from step 0 (also timed step
+by step).  `e2e` repeats the window through the public Python API with host
+numpy state (H2D q, q_dot, forces and D2H q, q_dot inside every timed step).
+`--gpus N` (N > 1) starts N ranks under torch.distributed.run when WORLD_SIZE is
+unset; the ranks partition ONE pile (strong scaling, max-over-ranks device time).
 Prints one JSON line (rank 0).
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import glob
+import hashlib
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -33,6 +40,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK = 6650.0
+WINDOW = (150, 200)  # late window of the 200-step config-4 run
+CKPT = os.path.join(ROOT, "bench_data", "pile_step150.npz")
+METRICS = {"pile": "sim steps/s (10k-body icosphere pile, fp64 ABD)",
+           "chainmail": "sim steps/s (10k-link chainmail, fp64 ABD)",
+           "cubes": "sim steps/s (1000-cube drop, fp64 ABD)",
+           "boxstack": "sim steps/s (4-cube box stack, fp64 ABD)"}
 
 
 def peaks():
@@ -41,6 +54,30 @@ def peaks():
             return json.load(f), "measured"
     except Exception:
         return {"hbm_gbs": HBM_FALLBACK}, "fallback"
+
+
+def src_hash():
+    """Digest of the CUDA sources the library is built from (keys measured ncu traffic)."""
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2201_10022_b200", "csrc", "*")))
+    for p in files + [os.path.join(ROOT, "include", "abd_b200.h")]:
+        with open(p, "rb") as f:
+            h.update(os.path.basename(p).encode() + f.read())
+    return h.hexdigest()[:16]
+
+
+def measured_traffic(workload, kernel):
+    """ncu DRAM bytes per launch of `kernel` on `workload`, if captured on THIS source tree
+    (tools/measure_traffic.py writes profiles/traffic_<workload>.json with the src hash)."""
+    path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        d = json.load(open(path))
+    except Exception:
+        return None, "no capture"
+    if d.get("src_hash") != src_hash():
+        return None, f"capture {os.path.relpath(path, ROOT)} is for another source tree"
+    k = d.get("kernels", {}).get(kernel)
+    return (k.get("dram_bytes_per_launch") if k else None), os.path.relpath(path, ROOT)
 
 
 class ClockSampler:
@@ -88,83 +125,157 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def spread(n, k):
+    """k indices spread evenly over range(n) (all of them when k >= n)."""
+    if k >= n:
+        return list(range(n))
+    return sorted({int((i + 0.5) * n / k) for i in range(k)})
+
+
 # ---------------------------------------------------------------------------
-def oracle_sample_rate(spec_kw, start_steps, budget_s, threads_note, threads=None):
-    """Oracle advance_step steps/s on a 8x8x2 sub-pile (same generator), scaled to 10k bodies."""
+# CPU legs: the oracle restatement of the reference path on the actual 10k pile
+def _oracle_pile():
+    from types import SimpleNamespace
+
     from oracle import abd_oracle as O
     from paper_2201_10022_b200 import scenes
     from paper_2201_10022_b200.body import mass_matrix
 
-    spec = scenes.icosphere_pile(seed=0, nx=8, ny=8, nz=2, **spec_kw)
-    from types import SimpleNamespace
+    spec = scenes.icosphere_pile(seed=0)
     bodies, masses, stiff = [], [], []
-    cache = {}
     for m, dyn in zip(spec.meshes, spec.dynamic):
         d = m.vertices[m.edges[:, 1]] - m.vertices[m.edges[:, 0]]
         bodies.append(SimpleNamespace(rest=m.vertices, triangles=m.triangles, edges=m.edges,
                                       edge_rest_len_sq=np.einsum("ij,ij->i", d, d), dynamic=bool(dyn)))
         if dyn:
-            if id(m) not in cache:
-                cache[id(m)] = mass_matrix(m, spec.density)
-            gm, vol = cache[id(m)]
+            gm, vol = mass_matrix(m, spec.density)
             masses.append(gm.matrix)
             stiff.append(spec.kappa_ortho * vol)
         else:
             masses.append(None)
             stiff.append(None)
     model = O.OracleModel(bodies, masses, stiff)
-    prm = O.OracleParams(**spec.params)
     f = np.zeros((len(bodies), 12))
-    g = np.array(spec.gravity)
+    g = np.asarray(spec.gravity, dtype=float)
     for b in model.dyn:
         f[b, :3] = masses[b][0, 0] * g
         f[b, 3:] = np.kron(g, masses[b][0, 3:6])
-    q, qd = spec.q0.copy(), spec.q_dot0.copy()
-    warnings.simplefilter("ignore")
-    from threadpoolctl import threadpool_limits
-    limiter = threadpool_limits(limits=threads) if threads else None
-    for _ in range(start_steps):
-        q, qd, _ = O.advance_step(model, q, qd, f, prm, min_distance=False)
-    n = 0
-    t0 = time.perf_counter()
-    iters = 0
-    while True:
-        q, qd, st = O.advance_step(model, q, qd, f, prm, min_distance=True)
-        n += 1
-        iters += st.iterations
-        el = time.perf_counter() - t0
-        if el >= budget_s or n >= 200:
-            break
-    if limiter is not None:
-        limiter.restore_original_limits()
-    nb = int(model.dynamic.sum())
-    scale = nb / 10000.0
-    return {"rate_sample": n / el, "steps": n, "seconds": el, "iters": iters, "bodies": nb,
-            "value": n / el * scale, "scale": scale, "note": threads_note}
+    return O, model, O.OracleParams(**spec.params), f
+
+
+class OraclePileNewton:
+    """The reference's Newton step (solver.py:493-628) restated by oracle/abd_oracle.py,
+    run on the 10k pile from the step-150 checkpoint one Newton iteration at a time:
+    setup = q_tilde + broad_phase(q, q) + friction_precompute; iteration = assemble +
+    sparse direct solve (BlockCholesky's contract, solve_refined) + broad_phase(q, q + dq)
+    + CCD-capped line search."""
+
+    def __init__(self, workers):
+        from threadpoolctl import threadpool_limits
+
+        self.limiter = threadpool_limits(limits=workers)
+        self.workers = workers
+        self.O, self.model, self.prm, self.f = _oracle_pile()
+        ck = np.load(CKPT)
+        self.q0, self.qd = ck["q"].copy(), ck["q_dot"].copy()
+        self.q = self.q0.copy()
+        self.ip = None
+
+    def setup(self):
+        O, m, p = self.O, self.model, self.prm
+        t0 = time.perf_counter()
+        qt = O.q_tilde(m, self.q0, self.qd, self.f, p.dt)
+        c = O.broad_phase(m.bodies, self.q0, self.q0, p.d_hat, workers=self.workers)
+        fr = O.friction_precompute(m.bodies, self.q0, c.vf, c.ee, p.kappa_barrier, p.d_hat, p.mu)
+        self.ip = O.OracleIP(qt, fr, c)
+        self.q = self.q0.copy()
+        return time.perf_counter() - t0
+
+    def iteration(self):
+        O, m, p = self.O, self.model, self.prm
+        t0 = time.perf_counter()
+        g, D, off = O.assemble(m, self.q, self.ip, p)
+        dd = O.solve_sparse(D, off, g)
+        if float(g @ dd) >= 0.0:
+            dd = -g
+        dq = np.zeros_like(self.q)
+        dq[m.dyn] = dd.reshape(-1, 12)
+        self.ip.cands = O.broad_phase(m.bodies, self.q, self.q + dq, p.d_hat, workers=self.workers)
+        alpha, _, _ = O.line_search(m, self.q, dq, self.ip, p)
+        self.q = self.q + alpha * dq
+        return time.perf_counter() - t0
+
+    def close(self):
+        self.limiter.restore_original_limits()
+
+
+def late_iters_per_step():
+    """Newton iterations per late-window step: the reference's own count on its step from the
+    checkpoint (tests/golden/pile_step150.npz, stage B) when present, else the cap (64)."""
+    try:
+        g = np.load(os.path.join(ROOT, "tests", "golden", "pile_step150.npz"))
+        if "B_iterations" in g.files:
+            return int(g["B_iterations"]), "reference advance_step from the step-150 checkpoint"
+    except Exception:
+        pass
+    return 64, "max_newton_iters (every GPU step of the window hits it)"
+
+
+def cpu_baseline_pile(n_iter=1):
+    """Rank 0, N = 1: the oracle on ONE thread, setup + n_iter Newton iterations of the
+    10k pile from the step-150 checkpoint (~20-30 s)."""
+    r = OraclePileNewton(workers=1)
+    try:
+        t_setup = r.setup()
+        t_it = [r.iteration() for _ in range(n_iter)]
+    finally:
+        r.close()
+    its, src = late_iters_per_step()
+    it_s = float(np.mean(t_it))
+    step_s = t_setup + its * it_s
+    return {"value": 1.0 / step_s, "unit": "steps/s", "cores": 1, "kind": "port",
+            "newton_it_per_s": 1.0 / it_s,
+            "sample": (f"oracle/abd_oracle.py on the 10k pile (config 4) at the step-150 checkpoint, 1 thread: "
+                       f"step setup (q_tilde, broad phase, friction) {t_setup:.2f}s + {n_iter} Newton iteration(s) "
+                       f"(assemble, sparse direct solve, broad phase, CCD line search) {it_s:.2f}s each; "
+                       f"steps/s = 1 / (setup + {its} x iteration), {its} = {src}")}
 
 
 def run_reference(args):
-    """--impl reference: the oracle restatement of the reference path on the host CPU."""
+    """--impl reference: the reference path (oracle restatement; /root/reference is absent
+    on the GPU box) on the host CPU with every host thread, on the headline pile."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
-    r = oracle_sample_rate({}, args.warmup, args.steps * 4.0, f"numpy, {cores} host threads available")
+    warnings.simplefilter("ignore")
+    r = OraclePileNewton(workers=cores)
+    try:
+        t_setup = r.setup()
+        for _ in range(max(0, args.warmup - 1)):
+            r.iteration()
+        t_it = [r.iteration() for _ in range(args.steps)]
+    finally:
+        r.close()
+    its, src = late_iters_per_step()
+    it_s = float(np.mean(t_it))
+    value = 1.0 / (t_setup + its * it_s)
+    sample = (f"oracle/abd_oracle.py on the 10k pile at the step-150 checkpoint with {cores} host threads "
+              f"(broad phase over {cores} forked workers, BLAS threads {cores}): step setup {t_setup:.2f}s, "
+              f"then {args.warmup - 1} warm-up + {args.steps} timed Newton iterations ({it_s:.2f}s mean; "
+              f"assemble, sparse direct solve, broad phase, CCD line search); steps/s = 1 / (setup + {its} x "
+              f"iteration), {its} = {src}")
     line = {
-        "impl": "reference", "metric": "sim steps/s (10k-body icosphere pile, fp64 ABD)", "value": r["value"],
-        "unit": "steps/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
-        "ms_per_step": 1e3 / r["value"] if r["value"] else None, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
-        "config": {"workload": "icosphere_pile 20x20x25 (10,001 bodies, seed 0): CPU sample = 8x8x2 sub-pile "
-                               "of the same generator, scaled linearly by body count",
-                   "parallelism": f"cpu ({cores} host threads)"},
-        "cpu_baseline": {"value": r["value"], "unit": "steps/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} "
-                                   f"icospheres + ground, same generator) from step {args.warmup}, "
-                                   f"{r['steps']} steps in {r['seconds']:.1f}s, x{r['scale']:.4f} linear "
-                                   "body scaling to 10k (optimistic for the CPU)"},
-        "e2e": {"value": r["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRICS["pile"], "value": value, "unit": "steps/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded procedural scene)",
+        "config": {"workload": "icosphere_pile 20x20x25 (10001 bodies, seed 0), late window from checkpoint "
+                               "bench_data/pile_step150.npz", "newton_it_per_s": 1.0 / it_s,
+                   "iteration_s": t_it, "setup_s": t_setup, "parallelism": f"cpu ({cores} host threads)"},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t0,
     }
     print(json.dumps(line), flush=True)
@@ -181,14 +292,15 @@ def run_micro(args):
 
     t0 = time.perf_counter()
     data = scenes.microbench_pairs(seed=0, n_bodies=args.micro_bodies, n_vf=args.micro_pairs,
-                                   n_ee=args.micro_pairs)
+                                   n_ee=args.micro_pairs, d_lo_frac=args.micro_dlo)
     sysm = microbench.PairSystem(data)
     setup_s = time.perf_counter() - t0
     L = _native.lib()
     sc = sysm.scene
     for _ in range(args.warmup):
         sysm.assemble()
-        sysm.solve()
+        if not args.micro_no_solve:
+            sysm.solve()
     _native.check(L.abd_kernel_stats_reset(sc.ptr))
     n_launch0 = _native.kernel_launches()
     asm_ms, sol_ms, iters, rels = [], [], [], []
@@ -199,6 +311,8 @@ def run_micro(args):
             sysm.assemble()
             _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
             asm_ms.append(ms.value)
+            if args.micro_no_solve:
+                continue
             _native.check(L.abd_timer_start(sc.ptr))
             _, it, rel = sysm.solve()
             _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
@@ -225,22 +339,24 @@ def run_micro(args):
     k3_ms = float(np.mean(asm_ms))
     cpu = None
     if not args.no_cpu:
-        cpu = micro_cpu_rate(args.cpu_budget)
+        cpu = micro_cpu_rate(args.cpu_budget, args.micro_dlo)
+    traffic, tsrc = measured_traffic("micro", "k_cg" if sol_ms else "k_pair_blocks")
     line = {
         "metric": "microbench assemble + PCG time (100k bodies, 10M VF + 10M EE pairs, fp64)",
         "value": tot_ms / args.steps, "unit": "ms", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, scenes.microbench_pairs)",
         "config": {"workload": f"BASELINE config 2: {B} bodies, {sysm.n_vf} VF + {sysm.n_ee} EE pairs, "
-                               f"Morton +-1..4 body graph ({sysm.n_off} off-diagonal blocks), all pairs active",
-                   "assemble_ms": float(np.mean(asm_ms)), "pcg_ms": float(np.mean(sol_ms)),
-                   "pcg_iters": iters, "pcg_rel_res": rels, "pcg_ms_per_iter": it_ms,
+                               f"d ~ U({args.micro_dlo} d_hat, d_hat), Morton +-1..4 body graph "
+                               f"({sysm.n_off} off-diagonal blocks), all pairs active",
+                   "assemble_ms": float(np.mean(asm_ms)), "pcg_ms": float(np.mean(sol_ms)) if sol_ms else None,
+                   "pcg_iters": iters, "pcg_rel_res": rels, "pcg_ms_per_iter": it_ms if sol_ms else None,
                    "pairs_per_s_assemble": P_all / (k3_ms * 1e-3), "setup_s": setup_s,
                    "l2": "inputs (~2 GB rest + 22 GB pair records) exceed L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": "K4 PCG iteration (k_cg) / K3 assemble",
-                     "achieved": it_bytes / (it_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                     "frac": it_bytes / (it_ms * 1e-3) / 1e9 / hbm, "traffic": None,
-                     "algorithmic_bytes_per_launch": it_bytes,
+                     "achieved": it_bytes / (it_ms * 1e-3) / 1e9 if sol_ms else None, "peak": hbm, "unit": "GB/s",
+                     "frac": it_bytes / (it_ms * 1e-3) / 1e9 / hbm if sol_ms else None, "traffic": traffic,
+                     "traffic_source": tsrc, "algorithmic_bytes_per_launch": it_bytes,
                      "bytes_model": "K4: 1152 (N_blk + B_d) + 13 x 96 B_d per PCG iteration",
                      "assemble": {"achieved": k3_bytes / (k3_ms * 1e-3) / 1e9, "bytes": k3_bytes,
                                   "frac": k3_bytes / (k3_ms * 1e-3) / 1e9 / hbm,
@@ -251,7 +367,7 @@ def run_micro(args):
     print(json.dumps(line), flush=True)
 
 
-def micro_cpu_rate(budget_s):
+def micro_cpu_rate(budget_s, d_lo):
     """Oracle per-pair pipeline (contact_blocks: distance, barrier, J^T H J, 24x24 PSD), pairs/s, 1 thread,
     on a sample drawn by the same generator (2,000 bodies, equal VF / EE counts)."""
     from types import SimpleNamespace
@@ -263,7 +379,7 @@ def micro_cpu_rate(budget_s):
     lim = threadpool_limits(limits=1)
     n, el, seed = 0, 0.0, 1
     while el < budget_s:
-        d = scenes.microbench_pairs(seed=seed, n_bodies=2000, n_vf=2000, n_ee=2000)
+        d = scenes.microbench_pairs(seed=seed, n_bodies=2000, n_vf=2000, n_ee=2000, d_lo_frac=d_lo)
         a = microbench.soup_arrays(d)
         bodies = []
         for b in range(len(d["q"])):
@@ -285,35 +401,141 @@ def micro_cpu_rate(budget_s):
 
 
 # ---------------------------------------------------------------------------
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--start", type=int, default=0, help="untimed steps before warm-up (no checkpoint)")
-    ap.add_argument("--ckpt", default=os.path.join(ROOT, "bench_data", "pile_step150.npz"),
-                    help="start state (q, q_dot, step) of the 20x20x25 pile; 'none' = step 0")
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--nx", type=int, default=20)
-    ap.add_argument("--nz", type=int, default=25)
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--workload", default="pile", choices=["pile", "micro", "chainmail", "cubes", "boxstack"],
-                    help="pile = BASELINE config 4 (headline); micro = config 2 kernel microbenchmark; "
-                         "chainmail = config 5; cubes = config 3 (1000-cube drop); boxstack = config 1")
-    ap.add_argument("--micro-bodies", type=int, default=100_000)
-    ap.add_argument("--micro-pairs", type=int, default=10_000_000, help="VF pairs = EE pairs")
-    args = ap.parse_args()
-    if args.workload == "micro":
-        if args.impl == "reference" or int(os.environ.get("RANK", "0")) != 0:
-            return
-        run_micro(args)
+def maybe_spawn(args):
+    """`--gpus N` with N > 1 and no launcher: re-exec under torch.distributed.run (one rank per
+    GPU).  Under a launcher, WORLD_SIZE must equal --gpus."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            with socket.socket() as s:
+                s.bind(("127.0.0.1", 0))
+                port = s.getsockname()[1]
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+            os.execv(sys.executable, cmd)
         return
-    if args.impl == "reference":
-        run_reference(args)
-        return
+    if int(ws) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with matching values")
 
+
+class Run:
+    """One scene on this rank's GPU, stepped through the device-resident C-ABI path
+    (`abd_advance_step`) or the Python API, every step timed on the scene stream."""
+
+    def __init__(self, args, dist):
+        import paper_2201_10022_b200 as P
+        from paper_2201_10022_b200 import _native, scenes
+        from paper_2201_10022_b200.solver import step_params_c
+
+        self.P, self.N, self.dist = P, _native, dist
+        wl = args.workload
+        self.spec = {"pile": lambda: scenes.icosphere_pile(seed=0, nx=args.nx, ny=args.nx, nz=args.nz),
+                     "chainmail": lambda: scenes.chainmail(seed=0), "cubes": lambda: scenes.cube_drop(seed=0),
+                     "boxstack": lambda: scenes.box_stack(seed=0)}[wl]()
+        self.model, self.state0, self.params = self.spec.build()
+        self.B = len(self.model.bodies)
+        self.L = _native.lib()
+        self.sc = self.model.gpu_scene()
+        if dist is not None:
+            # one pile over all ranks (csrc/comm.cu)
+            from paper_2201_10022_b200.dist import attach_nccl
+            attach_nccl(self.model)
+        self.cp = step_params_c(self.params)
+        self.st = _native.StepStatsC()
+        self.forces = np.ascontiguousarray(self.model.forces(0, self.params.dt, self.state0.q), dtype=np.float64)
+        self.first = True
+        # small scenes (configs 1 and 3) fit in L2: flush it (write 512 MB) before every timed step
+        self.flush = wl in ("cubes", "boxstack")
+        self.fbuf = None
+        if self.flush:
+            import torch
+            self.fbuf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
+
+    def set_state(self, q, qd):
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        qd = np.ascontiguousarray(qd, dtype=np.float64)
+        self.N.check(self.L.abd_set_state(self.sc.ptr, q.ctypes.data, qd.ctypes.data))
+
+    def get_state(self):
+        q, qd = np.empty((self.B, 12)), np.empty((self.B, 12))
+        self.N.check(self.L.abd_get_state(self.sc.ptr, q.ctypes.data, qd.ctypes.data))
+        return q, qd
+
+    def _flush(self):
+        if self.flush:
+            import torch
+            self.fbuf.fill_(1.0)
+            torch.cuda.synchronize()
+
+    def device_steps(self, n):
+        """n steps on the resident state; per-step (ms, Newton iterations)."""
+        ms = C.c_double(0.0)
+        out = []
+        for _ in range(n):
+            self._flush()
+            self.N.check(self.L.abd_timer_start(self.sc.ptr))
+            self.N.check(self.L.abd_advance_step(self.sc.ptr, self.forces.ctypes.data if self.first else None,
+                                                 C.byref(self.cp), C.byref(self.st), None))
+            self.N.check(self.L.abd_timer_stop(self.sc.ptr, C.byref(ms)))
+            self.first = False
+            out.append((ms.value, self.st.iterations))
+        return out
+
+    def api_steps(self, state, n):
+        """n steps through the public Python API (host numpy state, copies in every step)."""
+        ms = C.c_double(0.0)
+        out = []
+        for _ in range(n):
+            self._flush()
+            self.N.check(self.L.abd_timer_start(self.sc.ptr))
+            state, st = self.P.advance_step(self.model, state, self.params)
+            self.N.check(self.L.abd_timer_stop(self.sc.ptr, C.byref(ms)))
+            out.append((ms.value, st.iterations))
+        self.first = True  # advance_step uploaded its own forces
+        return state, out
+
+    def max_over_ranks(self, xs):
+        if self.dist is None:
+            return np.asarray(xs, dtype=float)
+        import torch
+        t = torch.tensor(np.asarray(xs, dtype=float), dtype=torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def kernel_stats(self):
+        names = {0: ("k_chol", "k_chol_factor + k_chol_solve (K4 sparse block Cholesky, one factor + solve "
+                               "per Newton iteration)",
+                     "A blocks read + L written (1152 B each), 2x1152 B per update pair, L read twice by the "
+                     "solve, 4 vectors of 96 B per body"),
+                 1: ("k_pair_blocks", "k_pair_blocks (K3 contact pair gradient/Hessian, VF + EE launches)",
+                     "SURVEY 8(d) K3: 112 P_vf + 120 P_ee + 96 B + 1152 N_blk + 96 B_d"),
+                 2: ("k_ccd", "k_ccd (K5 additive CCD, VF + EE launches)", "SURVEY 8(d) K5: 112 (P_vf + P_ee) + 192 B"),
+                 3: ("k_prim_pairs", "k_prim_pairs (K2 broad phase primitive pairs)",
+                     "SURVEY 8(d) K2: 24 V + 8 E + 12 T + 192 B + 16 (P_vf + P_ee)")}
+        kst = {}
+        for which, (name, desc, model) in names.items():
+            n_, t_, b_, u_ = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
+            self.N.check(self.L.abd_kernel_stats(self.sc.ptr, which, C.byref(n_), C.byref(t_), C.byref(b_),
+                                                 C.byref(u_)))
+            kst[name] = {"launches": n_.value, "ms": t_.value, "bytes": b_.value, "units": u_.value,
+                         "desc": desc, "bytes_model": model}
+        return kst
+
+
+def rate(ms_list, iters=None):
+    tot = float(np.sum(ms_list))
+    d = {"steps": len(ms_list), "ms": tot, "steps_per_s": len(ms_list) / (tot * 1e-3) if tot else None}
+    if iters is not None:
+        d["newton_iters"] = int(np.sum(iters))
+        d["newton_it_per_s"] = float(np.sum(iters)) / (tot * 1e-3) if tot else None
+    return d
+
+
+def run_scene(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -324,199 +546,167 @@ def main():
         torch.cuda.set_device(local)
         dist_mod.init_process_group("nccl")
         dist = dist_mod
-
-    import paper_2201_10022_b200 as P
-    from paper_2201_10022_b200 import _native, scenes
-    from paper_2201_10022_b200.solver import step_params_c
-
-    if args.workload == "pile":
-        spec = scenes.icosphere_pile(seed=0, nx=args.nx, ny=args.nx, nz=args.nz)
-    elif args.workload == "chainmail":
-        spec = scenes.chainmail(seed=0)
-    elif args.workload == "cubes":
-        spec = scenes.cube_drop(seed=0)
-    else:
-        spec = scenes.box_stack(seed=0)
-    model, state, params = spec.build()
-    B = len(model.bodies)
-    L = _native.lib()
-    sc = model.gpu_scene()
-    if world > 1:
-        # one pile over all ranks: per-pair work split by overlap body pair, the system /
-        # energies / CCD bound all-reduced over NCCL, the solve replicated (csrc/comm.cu)
-        from paper_2201_10022_b200.dist import attach_nccl
-        attach_nccl(model)
-    step0, time0 = 0, 0.0
-    use_ckpt = args.workload == "pile" and args.ckpt.lower() != "none" and (args.nx, args.nz) == (20, 25)
-    if use_ckpt:
-        ck = np.load(args.ckpt)
-        assert int(ck["seed"]) == 0 and ck["q"].shape == state.q.shape
-        state.q, state.q_dot = ck["q"].copy(), ck["q_dot"].copy()
-        step0, time0 = int(ck["step"]), float(ck["time"])
-        args.start = 0
-    forces = np.ascontiguousarray(model.forces(step0, time0 + params.dt, state.q), dtype=np.float64)
-    q = np.ascontiguousarray(state.q, dtype=np.float64)
-    qd = np.ascontiguousarray(state.q_dot, dtype=np.float64)
-    _native.check(L.abd_set_state(sc.ptr, q.ctypes.data, qd.ctypes.data))
-    cp = step_params_c(params)
-    st = _native.StepStatsC()
     warnings.simplefilter("ignore")
+    r = Run(args, dist)
+    pile = args.workload == "pile" and (args.nx, args.nz) == (20, 25) and args.ckpt.lower() != "none"
 
-    def step(first=False):
-        _native.check(L.abd_advance_step(sc.ptr, forces.ctypes.data if first else None, C.byref(cp), C.byref(st),
-                                         None))
-        return st.iterations
+    if pile:
+        ck = np.load(args.ckpt)
+        assert int(ck["seed"]) == 0 and ck["q"].shape == (r.B, 12)
+        q_ck, qd_ck, step0 = ck["q"].copy(), ck["q_dot"].copy(), int(ck["step"])
+        n_win = WINDOW[1] - step0
+        r.forces = np.ascontiguousarray(r.model.forces(step0, (step0 + 1) * r.params.dt, q_ck), dtype=np.float64)
+        # warm-up from the checkpoint, then back to it
+        r.set_state(q_ck, qd_ck)
+        r.device_steps(args.warmup)
+        r.set_state(q_ck, qd_ck)
+        q_start, qd_start = q_ck, qd_ck
+    else:
+        r.set_state(r.state0.q, r.state0.q_dot)
+        r.device_steps(args.start + args.warmup)
+        q_start, qd_start = r.get_state()
+        step0 = args.start + args.warmup
+        n_win = args.steps
+    timed = spread(n_win, args.steps)
 
-    step(first=True)
-    for _ in range(args.start + args.warmup - 1):
-        step()
-    # snapshot the window's initial state for the e2e pass
-    q_start = np.empty((B, 12))
-    qd_start = np.empty((B, 12))
-    _native.check(L.abd_get_state(sc.ptr, q_start.ctypes.data, qd_start.ctypes.data))
-
-    def barrier():
-        if dist:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if not dist:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    _native.check(L.abd_kernel_stats_reset(sc.ptr))
-    n_launch0 = _native.kernel_launches()
-    barrier()
-    iters = 0
-    pcg_total = 0
-    # small scenes (configs 1 and 3) fit in L2: flush it (write 512 MB) before every
-    # timed step and time the steps one by one so the flush stays outside the sum
-    flush = args.workload in ("cubes", "boxstack")
-    fbuf = None
-    if flush:
-        import torch
-        fbuf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")
-    ms = C.c_double(0.0)
+    # device-resident pass over the window; the K timed steps are spread over it
+    r.N.check(r.L.abd_kernel_stats_reset(r.sc.ptr))
+    n_launch0 = r.N.kernel_launches()
+    r.barrier()
     with ClockSampler(local) as clk:
-        if flush:
-            tot = 0.0
-            for _ in range(args.steps):
-                fbuf.fill_(1.0)
-                torch.cuda.synchronize()
-                _native.check(L.abd_timer_start(sc.ptr))
-                iters += step()
-                pcg_total += st.pcg_iters_total
-                _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
-                tot += ms.value
-            ms.value = tot
-        else:
-            _native.check(L.abd_timer_start(sc.ptr))
-            for _ in range(args.steps):
-                iters += step()
-                pcg_total += st.pcg_iters_total
-            _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms)))
-    barrier()
-    launches = _native.kernel_launches() - n_launch0
-    elapsed_ms = max_over_ranks(ms.value)
-    iters_all = max_over_ranks(float(iters))
-    value = args.steps / (elapsed_ms * 1e-3)  # one partitioned pile: whole-job steps/s
-    # per-kernel live stats (CUDA events on the scene stream, this rank); the roofline
-    # is reported for the instrumented kernel with the largest share of the timed region
-    names = {0: ("k_chol", "k_chol_factor + k_chol_solve (K4 sparse block Cholesky, one factor + solve "
-                           "per Newton iteration; PCG iterations when linear_solver='pcg')",
-                 "A blocks read + L written (1152 B each), 2x1152 B per update pair, L read twice by the "
-                 "solve, 4 vectors of 96 B per body"),
-             1: ("k_pair_blocks", "k_pair_blocks (K3 contact pair gradient/Hessian, VF + EE launches)",
-                 "SURVEY 8(d) K3: 112 P_vf + 120 P_ee + 96 B + 1152 N_blk + 96 B_d"),
-             2: ("k_ccd", "k_ccd (K5 additive CCD, VF + EE launches)", "SURVEY 8(d) K5: 112 (P_vf + P_ee) + 192 B"),
-             3: ("k_prim_pairs", "k_prim_pairs (K2 broad phase primitive pairs)",
-                 "SURVEY 8(d) K2: 24 V + 8 E + 12 T + 192 B + 16 (P_vf + P_ee)")}
-    kst = {}
-    for which, (name, _, _) in names.items():
-        n_, t_, b_, u_ = C.c_int64(), C.c_double(), C.c_double(), C.c_int64()
-        _native.check(L.abd_kernel_stats(sc.ptr, which, C.byref(n_), C.byref(t_), C.byref(b_), C.byref(u_)))
-        kst[name] = {"launches": n_.value, "ms": t_.value, "bytes": b_.value, "units": u_.value,
-                     "share_of_step": t_.value / elapsed_ms if elapsed_ms else None,
-                     "achieved_gbs": (b_.value / (t_.value * 1e-3) / 1e9) if t_.value else None}
-    top = max(names, key=lambda k: kst[names[k][0]]["ms"])
-    tname, tdesc, tmodel = names[top]
+        per = r.device_steps(n_win)
+    r.barrier()
+    launches_window = r.N.kernel_launches() - n_launch0
+    ms_all = r.max_over_ranks([p[0] for p in per])
+    it_all = [p[1] for p in per]
+    kst = r.kernel_stats()
+    q_dev_end, _ = r.get_state()
+    ms_t = ms_all[timed]
+    it_t = [it_all[i] for i in timed]
+    elapsed_ms = float(np.sum(ms_t))
+    value = len(timed) / (elapsed_ms * 1e-3)
+    launches = int(round(launches_window * len(timed) / max(1, n_win)))
+    win_ms = float(np.sum(ms_all))
+
+    # roofline: the instrumented kernel with the largest share of the window
+    for k in kst.values():
+        k["share_of_step"] = k["ms"] / win_ms if win_ms else None
+        k["achieved_gbs"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] else None
+    top = max(kst, key=lambda k: kst[k]["ms"])
+    pc = kst[top]
     pk, pk_kind = peaks()
     hbm = float(pk.get("hbm_gbs", HBM_FALLBACK))
-    pc = kst[tname]
     achieved = (pc["bytes"] / pc["launches"]) / (pc["ms"] / pc["launches"] * 1e-3) / 1e9 if pc["launches"] else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(tname)
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "kernel": tdesc, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm if hbm else None, "traffic": traffic,
+    traffic, tsrc = measured_traffic(args.workload, top)
+    roofline = {"bound": "hbm", "kernel": pc["desc"], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm if hbm else None, "traffic": traffic, "traffic_source": tsrc,
                 "algorithmic_bytes_per_launch": pc["bytes"] / pc["launches"] if pc["launches"] else None,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})", "bytes_model": tmodel,
-                "share_of_step": pc["share_of_step"], "kernels": kst}
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})", "bytes_model": pc["bytes_model"],
+                "share_of_step": pc["share_of_step"],
+                "kernels": {k: {kk: vv for kk, vv in v.items() if kk not in ("desc", "bytes_model")}
+                            for k, v in kst.items()},
+                "measured_over": f"all {n_win} steps of the window"}
 
-    # e2e through the public Python API with host numpy state
+    # e2e: the same window through the public Python API with host numpy state
     e2e = None
     if not args.no_e2e:
-        w0 = step0 + args.start + args.warmup
-        state2 = P.SimState(q=q_start.copy(), q_dot=qd_start.copy(), time=w0 * params.dt, step_index=w0)
-        barrier()
-        _native.check(L.abd_timer_start(sc.ptr))
-        for _ in range(args.steps):
-            state2, _st = P.advance_step(model, state2, params)
-        ms2 = C.c_double(0.0)
-        _native.check(L.abd_timer_stop(sc.ptr, C.byref(ms2)))
-        barrier()
-        e_ms = max_over_ranks(ms2.value)
-        e2e = {"value": args.steps / (e_ms * 1e-3), "unit": "steps/s",
-               "h2d_bytes_per_step": 3 * 96 * B, "d2h_bytes_per_step": 2 * 96 * B,
-               "path": "paper_2201_10022_b200.advance_step (Python API, host numpy q/q_dot/forces)"}
+        state = r.P.SimState(q=q_start.copy(), q_dot=qd_start.copy(), time=step0 * r.params.dt, step_index=step0)
+        r.barrier()
+        state, per2 = r.api_steps(state, n_win)
+        r.barrier()
+        ms2 = r.max_over_ranks([p[0] for p in per2])
+        e_ms = float(np.sum(ms2[timed]))
+        e2e = {"value": len(timed) / (e_ms * 1e-3), "unit": "steps/s",
+               "h2d_bytes_per_step": 3 * 96 * r.B, "d2h_bytes_per_step": 2 * 96 * r.B,
+               "path": "paper_2201_10022_b200.advance_step (Python API, host numpy q/q_dot/forces)",
+               "window": rate(ms2, [p[1] for p in per2]),
+               "same_final_state_as_device_pass": bool(np.array_equal(state.q, q_dev_end))}
+
+    # the full 200-step run from step 0 (pile), every step timed
+    full = None
+    if pile and not args.no_full_run:
+        r.set_state(r.state0.q, r.state0.q_dot)
+        r.forces = np.ascontiguousarray(r.model.forces(0, r.params.dt, r.state0.q), dtype=np.float64)
+        r.first = True
+        r.barrier()
+        q150 = None
+        perf = []
+        for s in range(WINDOW[1]):
+            perf += r.device_steps(1)
+            if s + 1 == step0:
+                q150, _ = r.get_state()
+        r.barrier()
+        msf = r.max_over_ranks([p[0] for p in perf])
+        itf = [p[1] for p in perf]
+        full = rate(msf, itf)
+        full["early_0_50"] = rate(msf[:50], itf[:50])
+        full["middle_50_150"] = rate(msf[50:150], itf[50:150])
+        full["late_150_200"] = rate(msf[150:], itf[150:])
+        full["checkpoint_rel_diff_at_step150"] = float(np.abs(q150 - q_ck).max() / np.abs(q_ck).max())
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and args.workload == "pile":
-        r = oracle_sample_rate({}, args.warmup, args.cpu_budget, "1 thread", threads=1)
-        cpu = {"value": r["value"], "unit": "steps/s", "cores": 1, "kind": "port",
-               "sample": f"oracle/abd_oracle.py advance_step on a 8x8x2 sub-pile ({r['bodies']} icospheres + "
-                         f"ground, same generator) from step {args.warmup}: {r['steps']} steps in "
-                         f"{r['seconds']:.1f}s ({r['rate_sample']:.3f} steps/s), x{r['scale']:.4f} linear body "
-                         "scaling to the 10k pile (optimistic for the CPU)"}
+    if rank == 0 and world == 1 and not args.no_cpu and pile:
+        cpu = cpu_baseline_pile()
 
     if rank == 0:
-        metric = {"pile": "sim steps/s (10k-body icosphere pile, fp64 ABD)",
-                  "chainmail": "sim steps/s (10k-link chainmail, fp64 ABD)",
-                  "cubes": "sim steps/s (1000-cube drop, fp64 ABD)",
-                  "boxstack": "sim steps/s (4-cube box stack, fp64 ABD)"}[args.workload]
-        wl = (f"icosphere_pile {args.nx}x{args.nx}x{args.nz} ({B} bodies, seed 0)" if args.workload == "pile"
-              else f"{spec.name} ({B} bodies, seed 0; BASELINE config "
+        wl = (f"icosphere_pile {args.nx}x{args.nx}x{args.nz} ({r.B} bodies, seed 0)" if args.workload == "pile"
+              else f"{r.spec.name} ({r.B} bodies, seed 0; BASELINE config "
                    f"{ {'chainmail': 5, 'cubes': 3, 'boxstack': 1}[args.workload]})")
+        win = f"[{step0}, {step0 + n_win})"
         line = {
-            "metric": metric, "value": value, "unit": "steps/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "metric": METRICS[args.workload], "value": value, "unit": "steps/s",
+            "n_gpus": world, "steps": len(timed), "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / len(timed), "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded procedural scene)",
-            "config": {"workload": f"{wl}, "
-                                   f"steps [{step0 + args.start + args.warmup}, {step0 + args.start + args.warmup + args.steps})"
-                                   + (f" from checkpoint {os.path.relpath(args.ckpt, ROOT)} (step {step0} of the "
-                                      "200-step run; late, contact-dense phase)" if use_ckpt else ""),
-                       "newton_iters": int(iters_all), "newton_it_per_s": iters_all / (elapsed_ms * 1e-3),
-                       "pcg_iters": pcg_total,
-                       "l2": ("L2 flushed (512 MB write) before every timed step; steps timed one by one"
-                              if flush else "per-step working set exceeds L2 (rest+topology+vertex boxes "
-                              "> 126 MB); no flush"),
+            "config": {"workload": wl + (f", late window {win} of the 200-step run from checkpoint "
+                                         f"{os.path.relpath(args.ckpt, ROOT)}" if pile else f", steps {win}"),
+                       "timed_steps": [step0 + i for i in timed],
+                       "newton_iters": int(np.sum(it_t)), "newton_it_per_s": float(np.sum(it_t)) / (elapsed_ms * 1e-3),
+                       "window": rate(ms_all, it_all), "full_run": full,
+                       "l2": ("L2 flushed (512 MB write) before every timed step" if r.flush else
+                              "per-step working set exceeds L2 (rest+topology+vertex boxes > 126 MB); no flush"),
                        "parallelism": (f"pair-partitioned over {world} GPUs (NCCL all-reduce of the system, "
                                        "replicated solve)") if world > 1 else "single"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "gpu_launches_window": int(launches_window), "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--start", type=int, default=0, help="untimed steps before warm-up (non-pile workloads)")
+    ap.add_argument("--ckpt", default=CKPT, help="pile start state (q, q_dot, step); 'none' = from step 0")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--nx", type=int, default=20)
+    ap.add_argument("--nz", type=int, default=25)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-full-run", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--workload", default="pile", choices=["pile", "micro", "chainmail", "cubes", "boxstack"],
+                    help="pile = BASELINE config 4 (headline); micro = config 2 kernel microbenchmark; "
+                         "chainmail = config 5; cubes = config 3 (1000-cube drop); boxstack = config 1")
+    ap.add_argument("--micro-bodies", type=int, default=100_000)
+    ap.add_argument("--micro-pairs", type=int, default=10_000_000, help="VF pairs = EE pairs")
+    ap.add_argument("--micro-dlo", type=float, default=0.1, help="d ~ U(dlo * d_hat, d_hat)")
+    ap.add_argument("--micro-no-solve", action="store_true")
+    args = ap.parse_args()
+    maybe_spawn(args)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    if args.workload == "micro":
+        if int(os.environ.get("RANK", "0")) == 0:
+            run_micro(args)
+        return
+    run_scene(args)
 
 
 if __name__ == "__main__":

@@ -129,8 +129,13 @@ int abd_tri_intersect_batch(int64_t n, const double* tri_a, const double* tri_b,
  * (_intersecting_body_pairs, scene.py:652-698): pairs (cap,2) in canonical order,
  * n_pairs = total found (pairs beyond cap are not written) */
 int abd_intersecting_pairs(abd_scene* s, const double* q, int64_t cap, int64_t* pairs, int64_t* n_pairs);
-/* global_min_distance  solver.py:396-473 (exact; pairs of two kinematic bodies skipped) */
-int abd_global_min_distance(abd_scene* s, const double* q, double* dist);
+/* generation counters of the resident candidate and friction sets: bumped by every call
+ * that rewrites them (abd_set_*, abd_broad_phase, abd_friction_precompute, abd_advance_step
+ * and its stats broad phase).  Host-side caches of "what is resident" key on these. */
+int abd_resident_generation(abd_scene* s, int64_t* cand_gen, int64_t* fric_gen);
+/* global_min_distance  solver.py:396-473 (exact; pairs of two kinematic bodies are skipped
+ * when skip_static_pairs != 0, the reference default) */
+int abd_global_min_distance(abd_scene* s, const double* q, int skip_static_pairs, double* dist);
 /* contact_gradient_hessian  contact.py:646-675 -> resident PairBlocks; n_active out */
 int abd_contact_gradient_hessian(abd_scene* s, const double* q, double kappa, double d_hat, int project,
                                  int64_t* n_active);

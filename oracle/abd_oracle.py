@@ -671,7 +671,41 @@ class OracleCandidates:
         return len(self.vf) + len(self.ee)
 
 
-def broad_phase(bodies, q_start, q_end, d_hat):
+_BP = {}  # per-call inputs shared with forked workers
+
+
+def _bp_pairs(lo_hi):
+    """Primitive candidates of the overlapping body pairs pairs[lo:hi] (contact.py:276-335)."""
+    boxes, blo, bhi, pairs = _BP["boxes"], _BP["blo"], _BP["bhi"], _BP["pairs"]
+    vf, ee = [], []
+    for i, j in pairs[lo_hi[0]:lo_hi[1]]:
+        i, j = int(i), int(j)
+        olo, ohi = np.maximum(blo[i], blo[j]), np.minimum(bhi[i], bhi[j])
+        sel = []
+        for bx in (boxes[i], boxes[j]):
+            sel.append([(_clip(lo, hi, olo, ohi), lo, hi) for lo, hi in bx])
+        (vi, vlo_i, vhi_i), (ei, elo_i, ehi_i), (ti, tlo_i, thi_i) = sel[0]
+        (vj, vlo_j, vhi_j), (ej, elo_j, ehi_j), (tj, tlo_j, thi_j) = sel[1]
+        for (a_idx, alo, ahi, b_idx, blo_, bhi_, ba, bb, kind) in (
+            (vi, vlo_i, vhi_i, tj, tlo_j, thi_j, i, j, "vf"),
+            (vj, vlo_j, vhi_j, ti, tlo_i, thi_i, j, i, "vf"),
+            (ei, elo_i, ehi_i, ej, elo_j, ehi_j, i, j, "ee"),
+        ):
+            hit = _box_hits(alo[a_idx], ahi[a_idx], blo_[b_idx], bhi_[b_idx])
+            if len(hit) == 0:
+                continue
+            rows = np.empty((len(hit), 4), dtype=np.int64)
+            rows[:, 0], rows[:, 1] = ba, a_idx[hit[:, 0]]
+            rows[:, 2], rows[:, 3] = bb, b_idx[hit[:, 1]]
+            (vf if kind == "vf" else ee).append(rows)
+    z = np.zeros((0, 4), dtype=np.int64)
+    return (np.concatenate(vf) if vf else z), (np.concatenate(ee) if ee else z)
+
+
+def broad_phase(bodies, q_start, q_end, d_hat, workers=1):
+    """contact.py:338-412: exact candidate set, sorted by (c0, c2, c1, c3).  The body
+    pairs are independent, so `workers` > 1 splits them over forked processes (the
+    result is the same set; rows are sorted afterwards)."""
     n = len(bodies)
     h = 0.5 * d_hat
     X0 = all_world_points(bodies, q_start)
@@ -680,36 +714,35 @@ def broad_phase(bodies, q_start, q_end, d_hat):
     blo = np.array([bx[0][0].min(axis=0) for bx in boxes]).reshape(n, 3)
     bhi = np.array([bx[0][1].max(axis=0) for bx in boxes]).reshape(n, 3)
     dyn = np.array([b.dynamic for b in bodies], dtype=bool)
-    vf, ee, ov = [], [], []
-    for i in range(n):
-        for j in range(i + 1, n):
-            if not (dyn[i] or dyn[j]):
-                continue
-            if np.any(blo[i] > bhi[j]) or np.any(blo[j] > bhi[i]):
-                continue
-            ov.append((i, j))
-            olo, ohi = np.maximum(blo[i], blo[j]), np.minimum(bhi[i], bhi[j])
-            sel = []
-            for bx in (boxes[i], boxes[j]):
-                sel.append([(_clip(lo, hi, olo, ohi), lo, hi) for lo, hi in bx])
-            (vi, vlo_i, vhi_i), (ei, elo_i, ehi_i), (ti, tlo_i, thi_i) = sel[0]
-            (vj, vlo_j, vhi_j), (ej, elo_j, ehi_j), (tj, tlo_j, thi_j) = sel[1]
-            for (a_idx, alo, ahi, b_idx, blo_, bhi_, ba, bb, kind) in (
-                (vi, vlo_i, vhi_i, tj, tlo_j, thi_j, i, j, "vf"),
-                (vj, vlo_j, vhi_j, ti, tlo_i, thi_i, j, i, "vf"),
-                (ei, elo_i, ehi_i, ej, elo_j, ehi_j, i, j, "ee"),
-            ):
-                hit = _box_hits(alo[a_idx], ahi[a_idx], blo_[b_idx], bhi_[b_idx])
-                if len(hit) == 0:
-                    continue
-                rows = np.empty((len(hit), 4), dtype=np.int64)
-                rows[:, 0], rows[:, 1] = ba, a_idx[hit[:, 0]]
-                rows[:, 2], rows[:, 3] = bb, b_idx[hit[:, 1]]
-                (vf if kind == "vf" else ee).append(rows)
+    # body pairs i < j with a dynamic side and closed box overlap (contact.py:366-369),
+    # tested in row chunks; listed in (i, j) lexicographic order
+    pairs = []
+    for i0 in range(0, n, 256):
+        i1 = min(n, i0 + 256)
+        hit = np.all((blo[i0:i1, None, :] <= bhi[None, :, :]) & (blo[None, :, :] <= bhi[i0:i1, None, :]), axis=2)
+        hit &= np.arange(n)[None, :] > np.arange(i0, i1)[:, None]
+        hit &= dyn[i0:i1, None] | dyn[None, :]
+        ii, jj = np.nonzero(hit)
+        pairs.append(np.stack([ii + i0, jj], axis=1))
+    pairs = np.concatenate(pairs).astype(np.int64) if pairs else np.zeros((0, 2), dtype=np.int64)
+    _BP.update(boxes=boxes, blo=blo, bhi=bhi, pairs=pairs)
+    try:
+        if workers > 1 and len(pairs) > 64:
+            import multiprocessing as mp
+
+            cuts = np.linspace(0, len(pairs), 4 * workers + 1).astype(int)
+            with mp.get_context("fork").Pool(workers) as pool:
+                parts = pool.map(_bp_pairs, list(zip(cuts[:-1], cuts[1:])))
+        else:
+            parts = [_bp_pairs((0, len(pairs)))]
+    finally:
+        _BP.clear()
+    vf = [p[0] for p in parts if len(p[0])]
+    ee = [p[1] for p in parts if len(p[1])]
     return OracleCandidates(
         _lexsort_rows(np.concatenate(vf)) if vf else np.zeros((0, 4), dtype=np.int64),
         _lexsort_rows(np.concatenate(ee)) if ee else np.zeros((0, 4), dtype=np.int64),
-        np.asarray(ov, dtype=np.int64).reshape(-1, 2),
+        pairs.reshape(-1, 2),
     )
 
 
@@ -898,6 +931,42 @@ def solve_dense(diag, off, g):
     return -np.linalg.solve(L.T, np.linalg.solve(L, g))
 
 
+def bsr_csr(diag, off):
+    """The full symmetric BSR (both triangles) as a scipy CSR matrix."""
+    import scipy.sparse as sp
+
+    n = len(diag)
+    keys = list(off.keys())
+    rows = [np.arange(n)] + ([np.array([k[0] for k in keys]), np.array([k[1] for k in keys])] if keys else [])
+    cols = [np.arange(n)] + ([np.array([k[1] for k in keys]), np.array([k[0] for k in keys])] if keys else [])
+    blks = [diag] + ([np.array([off[k] for k in keys]), np.array([off[k].T for k in keys])] if keys else [])
+    r, c, b = np.concatenate(rows), np.concatenate(cols), np.concatenate(blks)
+    ii = (12 * r[:, None, None] + np.arange(12)[None, :, None]).repeat(12, axis=2)
+    jj = (12 * c[:, None, None] + np.arange(12)[None, None, :]).repeat(12, axis=1)
+    return sp.csr_matrix((b.reshape(-1), (ii.reshape(-1), jj.reshape(-1))), shape=(12 * n, 12 * n))
+
+
+def solve_sparse(diag, off, g, rel_tol=1e-8, max_refine=3):
+    """Newton solve H dq = -g by a sparse direct factorisation (SuperLU) with the
+    refinement contract of BlockCholesky.solve_refined (sparse.py:90-161): the
+    reference's algorithm class at scenes where a dense matrix cannot be formed."""
+    from scipy.sparse.linalg import splu
+
+    if len(diag) == 0:
+        return np.zeros(0)
+    A = bsr_csr(diag, off).tocsc()
+    lu = splu(A)
+    b = -np.asarray(g, dtype=float)
+    x = lu.solve(b)
+    bn = np.linalg.norm(b)
+    for _ in range(max_refine):
+        r = b - A @ x
+        if np.linalg.norm(r) <= rel_tol * bn:
+            break
+        x = x + lu.solve(r)
+    return x
+
+
 def pcg_block_jacobi(diag, off, b, rel_tol=1e-8, max_iters=100000):
     """numpy block-Jacobi PCG (CPU baseline for the sm_100a PCG)."""
     n = len(diag)
@@ -1014,6 +1083,8 @@ def advance_step(model, q, q_dot, forces, prm, solver="dense", min_distance=True
         g, D, O = assemble(model, qc, ip, prm)
         if solver == "dense":
             dd = solve_dense(D, O, g)
+        elif solver == "sparse":
+            dd = solve_sparse(D, O, g)
         else:
             dd = pcg_block_jacobi(D, O, -g)[0]
         if len(dd) == 0 or np.abs(dd).max() / prm.dt < prm.newton_tol:

@@ -7,6 +7,7 @@ codes map back to the reference's exception types.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import os
 import weakref
 
@@ -74,7 +75,8 @@ _SIGS = {
     "abd_set_candidates": (i32, [vp, i64, lp, i64, lp, i64, lp]),
     "abd_contact_energy": (i32, [vp, dp, dbl, dbl, C.POINTER(dbl)]),
     "abd_candidate_min_d2": (i32, [vp, dp, C.POINTER(dbl)]),
-    "abd_global_min_distance": (i32, [vp, dp, C.POINTER(dbl)]),
+"abd_resident_generation": (i32, [vp, C.POINTER(i64), C.POINTER(i64)]),
+    "abd_global_min_distance": (i32, [vp, dp, i32, C.POINTER(dbl)]),
     "abd_contact_gradient_hessian": (i32, [vp, dp, dbl, dbl, i32, C.POINTER(i64)]),
     "abd_get_pair_blocks": (i32, [vp, lp, lp, dp, dp, dp]),
     "abd_friction_precompute": (i32, [vp, dp, dbl, dbl, dbl, C.POINTER(i64)]),
@@ -343,26 +345,36 @@ class Scene:
         return f64(q).reshape(self.n_bodies, 12)
 
     # candidate / friction residency
+    def generations(self):
+        a, b = i64(0), i64(0)
+        check(lib().abd_resident_generation(self.ptr, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    # The resident sets are keyed on the caller's arrays (identity AND content digest)
+    # plus the C side's generation counter at upload time: any C call that rewrote the
+    # resident set since (advance_step, broad_phase, friction_precompute, the stats
+    # broad phase) bumps the counter and forces a re-upload.
     def set_candidates(self, cands):
-        key = (id(cands), id(cands.vf), id(cands.ee), id(cands.overlap_pairs))
-        if getattr(cands, "_resident", None) is self and self._cand_key == key:
-            return
         vf, ee, ov = i64a(cands.vf).reshape(-1, 4), i64a(cands.ee).reshape(-1, 4), i64a(cands.overlap_pairs).reshape(-1, 2)
+        key = (id(cands), _digest(vf, ee, ov))
+        if self._cand_key is not None and self._cand_key == (key, self.generations()[0]):
+            return
         check(lib().abd_set_candidates(self.ptr, len(vf), vf, len(ee), ee, len(ov), ov))
-        self._cand_key = key
-        try:
-            cands._resident = self
-        except AttributeError:
-            pass
+        self._cand_key = (key, self.generations()[0])
+
+    def adopt_candidates(self, cands):
+        """`cands` was just read back from the resident set: record it as resident."""
+        vf, ee, ov = i64a(cands.vf).reshape(-1, 4), i64a(cands.ee).reshape(-1, 4), i64a(cands.overlap_pairs).reshape(-1, 2)
+        self._cand_key = ((id(cands), _digest(vf, ee, ov)), self.generations()[0])
 
     def set_friction(self, fr):
-        key = (id(fr), id(fr.lam), fr.lam.tobytes() if len(fr.lam) < 4096 else id(fr.lam))
-        if self._fric_key == key:
+        ba, bb, lam = i64a(fr.body_a), i64a(fr.body_b), f64(fr.lam)
+        tm, off = f64(fr.tangent_map).reshape(-1), f64(fr.offset).reshape(-1)
+        key = (id(fr), float(fr.mu), _digest(ba, bb, lam, tm, off))
+        if self._fric_key is not None and self._fric_key == (key, self.generations()[1]):
             return
-        n = len(fr.lam)
-        check(lib().abd_set_friction(self.ptr, n, i64a(fr.body_a), i64a(fr.body_b), f64(fr.lam), float(fr.mu),
-                                     f64(fr.tangent_map).reshape(-1), f64(fr.offset).reshape(-1)))
-        self._fric_key = key
+        check(lib().abd_set_friction(self.ptr, len(lam), ba, bb, lam, float(fr.mu), tm, off))
+        self._fric_key = (key, self.generations()[1])
 
     def broad_phase(self, q0, q1, d_hat):
         a, b, c = i64(0), i64(0), i64(0)
@@ -373,6 +385,14 @@ class Scene:
         ov = np.empty((c.value, 2), dtype=np.int64)
         check(lib().abd_get_candidates(self.ptr, vf, ee, ov))
         return vf, ee, ov
+
+
+def _digest(*arrays):
+    h = hashlib.blake2b(digest_size=16)
+    for a in arrays:
+        h.update(np.int64(a.size).tobytes())
+        h.update(memoryview(np.ascontiguousarray(a)).cast("B"))
+    return h.digest()
 
 
 _SCENES: dict = {}

@@ -141,8 +141,7 @@ def broad_phase(bodies, q_start, q_end, d_hat) -> CandidateSet:
     sc = _native.scene_for(bodies)
     vf, ee, ov = sc.broad_phase(q_start, q_end, d_hat)
     cs = CandidateSet(vf, ee, ov, 0)
-    cs._resident = sc
-    sc._cand_key = (id(cs), id(cs.vf), id(cs.ee), id(cs.overlap_pairs))
+    sc.adopt_candidates(cs)
     return cs
 
 

@@ -629,6 +629,7 @@ int abd_set_candidates(abd_scene* h, int64_t n_vf, const int64_t* vf, int64_t n_
     s.cands.n_vf = n_vf;
     s.cands.n_ee = n_ee;
     s.cands.n_ov = n_ov;
+    s.cands.gen += 1;
     sync(s.stream);
   });
 }
@@ -678,10 +679,18 @@ int abd_intersecting_pairs(abd_scene* h, const double* q, int64_t cap, int64_t* 
   });
 }
 
-int abd_global_min_distance(abd_scene* h, const double* q, double* dist) {
+int abd_resident_generation(abd_scene* h, int64_t* cand_gen, int64_t* fric_gen) {
   return guard([&] {
     SC(h);
-    *dist = global_min_distance(s, up_q(s, s.q_trial, q));
+    *cand_gen = s.cands.gen;
+    *fric_gen = s.fric.gen;
+  });
+}
+
+int abd_global_min_distance(abd_scene* h, const double* q, int skip_static_pairs, double* dist) {
+  return guard([&] {
+    SC(h);
+    *dist = global_min_distance(s, up_q(s, s.q_trial, q), skip_static_pairs ? 1 : 0);
   });
 }
 

@@ -30,7 +30,7 @@ void comm_destroy(Scene& s);
 void comm_allreduce(Scene& s, void* dptr, int64_t count, int dtype, int op);
 int64_t comm_allgather_i64(Scene& s, const int64_t* local, int64_t n_local, DVec<int64_t>& out);
 // k_stats.cu
-double global_min_distance(Scene& s, const double* q);
+double global_min_distance(Scene& s, const double* q, int skip_static = 1);
 // the same value for the end-of-step stats; overwrites the resident candidate set
 double global_min_distance_stats(Scene& s, const double* q);
 // body pairs (i < j) whose closed surfaces intersect or contain one another (k_audit.cu)

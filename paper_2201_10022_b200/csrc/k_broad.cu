@@ -1548,6 +1548,7 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   Cands& c = s.cands;
   Scene::Work& w = s.w;
   c.n_vf = c.n_ee = c.n_ov = 0;
+  c.gen += 1;
   // one memset for this broad phase's device scalars (w.ull[4..13]: pair / candidate
   // counters, overflow flag, work queue, pattern flag, Verlet-list info) and the
   // following line search's slow-query counter

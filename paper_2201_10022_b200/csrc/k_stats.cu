@@ -44,7 +44,7 @@ __device__ __forceinline__ double box_gap(const double* a, const double* b) {
 // pass 0: argmin gap (packed gap bits | pair index is not needed: we keep min gap
 // and, separately, one pair achieving it); pass 1: list pairs with gap < bound
 __global__ void k_pair_gaps(int B, const unsigned char* __restrict__ dyn, const double* __restrict__ bbox, double bound,
-                            unsigned long long* min_gap, int2* list, int* count, int cap) {
+                            unsigned long long* min_gap, int2* list, int* count, int cap, int skip_static) {
   int64_t total = (int64_t)B * (B - 1) / 2;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     // invert t -> (i, j), i < j, row-major over the upper triangle
@@ -53,7 +53,7 @@ __global__ void k_pair_gaps(int B, const unsigned char* __restrict__ dyn, const 
     while (i > 0 && i * (2 * (int64_t)B - i - 1) / 2 > t) --i;
     while ((i + 1) * (2 * (int64_t)B - i - 2) / 2 <= t) ++i;
     int64_t j = t - i * (2 * (int64_t)B - i - 1) / 2 + i + 1;
-    if (!(dyn[i] || dyn[j])) continue;
+    if (skip_static && !(dyn[i] || dyn[j])) continue;
     double g = box_gap(bbox + 6 * i, bbox + 6 * j);
     if (min_gap) atomicMin(min_gap, (unsigned long long)__double_as_longlong(g));
     if (list && g < bound) {
@@ -128,7 +128,7 @@ double global_min_distance_stats(Scene& s, const double* q) {
   return global_min_distance(s, q);
 }
 
-double global_min_distance(Scene& s, const double* q) {
+double global_min_distance(Scene& s, const double* q, int skip_static) {
   cudaStream_t st = s.stream;
   if (s.B < 2) return INFINITY;
   s.bbox.resize(6 * s.B);
@@ -139,7 +139,7 @@ double global_min_distance(Scene& s, const double* q) {
   unsigned long long inf = (unsigned long long)__builtin_bit_cast(long long, (double)INFINITY);
   dev_set_u64(st, mg.p, inf);
   int grid = s.num_sms * 8;
-  k_pair_gaps<<<grid, 256, 0, st>>>(s.B, s.dyn.p, s.bbox.p, 0.0, mg.p, nullptr, nullptr, 0);
+  k_pair_gaps<<<grid, 256, 0, st>>>(s.B, s.dyn.p, s.bbox.p, 0.0, mg.p, nullptr, nullptr, 0, skip_static);
   note_launch("k_pair_gaps");
   unsigned long long hg = 0;
   CK(cudaMemcpyAsync(&hg, mg.p, sizeof(hg), cudaMemcpyDeviceToHost, st));
@@ -157,7 +157,7 @@ double global_min_distance(Scene& s, const double* q) {
     for (;;) {
       list.resize(cap);
       cnt.zero(st);
-      k_pair_gaps<<<grid, 256, 0, st>>>(s.B, s.dyn.p, s.bbox.p, bound, nullptr, list.p, cnt.p, cap);
+      k_pair_gaps<<<grid, 256, 0, st>>>(s.B, s.dyn.p, s.bbox.p, bound, nullptr, list.p, cnt.p, cap, skip_static);
       note_launch("k_pair_gaps");
       int hc = 0;
       CK(cudaMemcpyAsync(&hc, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -114,6 +114,7 @@ struct Cands {
   DVec<int2> ov;      // overlapping body pairs (i < j)
   int64_t n_vf = 0, n_ee = 0, n_ov = 0;
   bool ov_matches_pattern = false;  // ov equals the overlap list of the resident BSR pattern
+  int64_t gen = 0;                  // bumped whenever the resident candidate set is rewritten
 };
 
 // lagged friction records (compact form of contact.py:687-708)

@@ -188,7 +188,8 @@ def assemble(q_all, ip: IncrementalPotentialState, params: StepParams, timings: 
 
 
 def solve_newton_system(hessian: BlockSparseMatrix, gradient: np.ndarray) -> np.ndarray:
-    """H dq = -g by block-Jacobi PCG to 1e-8 relative residual (solver.py:345-348)."""
+    """H dq = -g by the device sparse block Cholesky with iterative refinement to 1e-8 relative
+    residual (solver.py:345-348; sparse.py:90-161)."""
     return hessian.factor().solve_refined(-np.asarray(gradient, dtype=float), rel_tol=1e-8)
 
 
@@ -217,11 +218,10 @@ def line_search(q_all, delta_q, ip: IncrementalPotentialState, params: StepParam
 
 def global_min_distance(bodies, q_all, skip_static_pairs=True) -> float:
     """Exact minimum inter-body distance (solver.py:396-473), on the GPU."""
-    if not skip_static_pairs:
-        raise NotImplementedError("only skip_static_pairs=True is supported")
     sc = _native.scene_for(bodies)
     out = C.c_double(0.0)
-    _native.check(_native.lib().abd_global_min_distance(sc.ptr, sc.q(q_all), C.byref(out)))
+    _native.check(_native.lib().abd_global_min_distance(sc.ptr, sc.q(q_all), int(bool(skip_static_pairs)),
+                                                        C.byref(out)))
     return float(out.value)
 
 
