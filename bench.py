@@ -554,7 +554,7 @@ def run_scene(args):
         ck = np.load(args.ckpt)
         assert int(ck["seed"]) == 0 and ck["q"].shape == (r.B, 12)
         q_ck, qd_ck, step0 = ck["q"].copy(), ck["q_dot"].copy(), int(ck["step"])
-        n_win = WINDOW[1] - step0
+        n_win = min(WINDOW[1] - step0, args.window_steps)
         r.forces = np.ascontiguousarray(r.model.forces(step0, (step0 + 1) * r.params.dt, q_ck), dtype=np.float64)
         # warm-up from the checkpoint, then back to it
         r.set_state(q_ck, qd_ck)
@@ -689,6 +689,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-full-run", action="store_true")
+    ap.add_argument("--window-steps", type=int, default=WINDOW[1] - WINDOW[0],
+                    help="pile: steps of the late window stepped (default all 50); for experiments only")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--workload", default="pile", choices=["pile", "micro", "chainmail", "cubes", "boxstack"],
                     help="pile = BASELINE config 4 (headline); micro = config 2 kernel microbenchmark; "

@@ -679,6 +679,8 @@ int abd_intersecting_pairs(abd_scene* h, const double* q, int64_t cap, int64_t* 
   });
 }
 
+static std::vector<int64_t> canonical_record_order(Scene& s, int64_t total);
+
 int abd_resident_generation(abd_scene* h, int64_t* cand_gen, int64_t* fric_gen) {
   return guard([&] {
     SC(h);
@@ -699,7 +701,37 @@ int abd_contact_gradient_hessian(abd_scene* h, const double* q, double kappa, do
   return guard([&] {
     SC(h);
     *n_active = contact_blocks(s, up_q(s, s.q_trial, q), kappa, d_hat, project);
+    s.pblk_order = canonical_record_order(s, *n_active);
   });
+}
+
+// The device keeps active pair records in its own candidate order (per overlap pair);
+// the reference lists them as the active VF rows in canonical (c0, c2, c1, c3) order,
+// then the active EE rows (contact.py:646-675, :722-790).  Right after an active scan,
+// w.act[p] is the candidate slot of record p (VF slots first): the permutation that
+// reads the records out in the reference's order.
+static std::vector<int64_t> canonical_record_order(Scene& s, int64_t total) {
+  std::vector<int64_t> perm(total);
+  if (total <= 0) return perm;
+  std::vector<int> act(total);
+  std::vector<int4> vf(s.cands.n_vf), ee(s.cands.n_ee);
+  CK(cudaMemcpyAsync(act.data(), s.w.act.p, total * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+  s.cands.vf.download(vf.data(), vf.size(), s.stream);
+  s.cands.ee.download(ee.data(), ee.size(), s.stream);
+  sync(s.stream);
+  const int64_t n_vf = s.cands.n_vf;
+  auto row = [&](int64_t p) -> const int4& { return act[p] < n_vf ? vf[act[p]] : ee[act[p] - n_vf]; };
+  for (int64_t p = 0; p < total; ++p) perm[p] = p;
+  std::sort(perm.begin(), perm.end(), [&](int64_t a, int64_t b) {
+    const bool ka = act[a] >= n_vf, kb = act[b] >= n_vf;
+    if (ka != kb) return kb;
+    const int4 &p = row(a), &q = row(b);
+    if (p.x != q.x) return p.x < q.x;
+    if (p.z != q.z) return p.z < q.z;
+    if (p.y != q.y) return p.y < q.y;
+    return p.w < q.w;
+  });
+  return perm;
 }
 
 int abd_get_pair_blocks(abd_scene* h, int64_t* body_a, int64_t* body_b, double* grad, double* hess, double* d_sq) {
@@ -716,11 +748,14 @@ int abd_get_pair_blocks(abd_scene* h, int64_t* body_a, int64_t* body_b, double* 
     dense.download(blk.data(), (size_t)n * PB_DENSE, s.stream);
     s.pblk.d2.download(d2.data(), n, s.stream);
     sync(s.stream);
-    for (int64_t i = 0; i < n; ++i) {
-      if (body_a) body_a[i] = b[i].x;
-      if (body_b) body_b[i] = b[i].y;
-      if (d_sq) d_sq[i] = d2[i];
-      const double* o = &blk[(size_t)i * PB_DENSE];
+    const bool ordered = (int64_t)s.pblk_order.size() == n;
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t i = k;
+      const int64_t src = ordered ? s.pblk_order[k] : k;
+      if (body_a) body_a[i] = b[src].x;
+      if (body_b) body_b[i] = b[src].y;
+      if (d_sq) d_sq[i] = d2[src];
+      const double* o = &blk[(size_t)src * PB_DENSE];
       if (grad) std::memcpy(grad + 24 * i, o, 24 * sizeof(double));
       if (hess) {
         double* H = hess + 576 * i;
@@ -742,6 +777,8 @@ int abd_friction_precompute(abd_scene* h, const double* q_prev, double kappa, do
     static thread_local DVec<double>* basis = nullptr;
     if (!basis) basis = new DVec<double>();
     *n = friction_precompute(s, up_q(s, s.q_trial, q_prev), kappa, d_hat, mu, basis);
+    s.fric_order = canonical_record_order(s, *n);
+    s.fric_order_gen = s.fric.gen;
     s.red.resize(std::max<int64_t>(*n, 1) * 6);
     CK(cudaMemcpyAsync(s.red.p, basis->p, std::max<int64_t>(*n, 1) * 6 * sizeof(double), cudaMemcpyDeviceToDevice,
                        s.stream));
@@ -760,15 +797,18 @@ int abd_get_friction(abd_scene* h, int64_t* body_a, int64_t* body_b, double* lam
     s.fric.rec.download(rec.data(), (size_t)n * FRIC_STRIDE, s.stream);
     if (basis && n) CK(cudaMemcpyAsync(bs.data(), s.red.p, n * 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
     sync(s.stream);
+    // reference order when this set came from abd_friction_precompute (else device order)
+    const bool ordered = s.fric_order_gen == s.fric.gen && (int64_t)s.fric_order.size() == n;
     for (int64_t i = 0; i < n; ++i) {
-      body_a[i] = b[i].x;
-      body_b[i] = b[i].y;
-      const double* r = &rec[(size_t)i * FRIC_STRIDE];
+      const int64_t k = ordered ? s.fric_order[i] : i;
+      body_a[i] = b[k].x;
+      body_b[i] = b[k].y;
+      const double* r = &rec[(size_t)k * FRIC_STRIDE];
       std::memcpy(tangent_map + 48 * i, r, 48 * sizeof(double));
       offset[2 * i] = r[48];
       offset[2 * i + 1] = r[49];
       lam[i] = r[50];
-      if (basis) std::memcpy(basis + 6 * i, &bs[6 * i], 6 * sizeof(double));
+      if (basis) std::memcpy(basis + 6 * i, &bs[6 * k], 6 * sizeof(double));
     }
   });
 }

@@ -164,6 +164,9 @@ struct Comm {
 
 struct Scene {
   int B = 0, n_dyn = 0;
+  // host-side readout permutations into the reference's record order (capi.cu)
+  std::vector<int64_t> pblk_order, fric_order;
+  int64_t fric_order_gen = -1;
   int64_t V = 0, E = 0, T = 0;
   int max_v = 0, max_e = 0, max_t = 0;  // per-body primitive maxima (sort key widths)
   cudaStream_t stream = nullptr;

@@ -156,6 +156,52 @@ def stage_a(model, state, params, out):
           f"e {e:.10g} ({time.perf_counter() - t0:.1f}s)", flush=True)
 
 
+def stage_scales(model, state, params, out):
+    """Per-block magnitude of the summed terms (the comparator's denominator for sums
+    with cancellation): for each dynamic slot, |M(q - q~)| + dt^2 |grad V_perp| + sum over
+    contact / friction pairs of |their 12-block gradient|; the same with Frobenius
+    norms for the diagonal and off-diagonal Hessian blocks (solver.py:283-342)."""
+    import stiffbody.body as rb
+
+    q0 = state.q
+    ck = dict(out)
+    c0 = rc.CandidateSet(ck["A_c0_vf"].astype(np.int64), ck["A_c0_ee"].astype(np.int64),
+                         ck["A_c0_ov"].astype(np.int64))
+    slot = model.slot_of
+    nd = model.n_dyn
+    gs, ds = np.zeros(nd), np.zeros(nd)
+    qt = ck["A_qtilde"]
+    for b in model.dyn_indices:
+        s = slot[int(b)]
+        M = model.gmass[b].matrix
+        gs[s] += np.linalg.norm(M @ (q0[b] - qt[b])) + params.dt ** 2 * np.linalg.norm(
+            rb.ortho_gradient(q0[b], model.materials[b]))
+        ds[s] += np.linalg.norm(M) + params.dt ** 2 * np.linalg.norm(
+            rb.ortho_hessian(q0[b], model.materials[b], project_psd=True))
+    keys = [tuple(k) for k in ck["A_off_keys"]]
+    kidx = {k: i for i, k in enumerate(keys)}
+    os_ = np.zeros(len(keys))
+    fr = rc.FrictionData(ck["A_fr_a"], ck["A_fr_b"], ck["A_fr_lam"], params.mu, ck["A_fr_tmap"], ck["A_fr_off"],
+                         np.zeros((len(ck["A_fr_lam"]), 3, 2)))
+    parts = [rc.contact_gradient_hessian(model.bodies, q0, c0, params.kappa_barrier, params.d_hat),
+             rc.friction_gradient_hessian(q0, fr, params.dt, params.epsilon_v, model.dynamic)]
+    for blk in parts:
+        for k in range(len(blk.body_a)):
+            a, b = int(blk.body_a[k]), int(blk.body_b[k])
+            sa, sb = slot.get(a), slot.get(b)
+            if sa is not None:
+                gs[sa] += np.linalg.norm(blk.grad[k, :12])
+                ds[sa] += np.linalg.norm(blk.hess[k, :12, :12])
+            if sb is not None:
+                gs[sb] += np.linalg.norm(blk.grad[k, 12:])
+                ds[sb] += np.linalg.norm(blk.hess[k, 12:, 12:])
+            if sa is not None and sb is not None:
+                os_[kidx[(min(sa, sb), max(sa, sb))]] += np.linalg.norm(blk.hess[k, :12, 12:])
+    out["A_grad_scale"], out["A_diag_scale"], out["A_off_scale"] = gs, ds, os_
+    print(f"  scales: grad median {np.median(gs):.4g}, off median {np.median(os_) if len(os_) else 0:.4g}",
+          flush=True)
+
+
 def fast_solve(H, g):
     """solve_newton_system's contract (solver.py:345-348, sparse.py:148-161) by SuperLU."""
     import scipy.sparse as sp
@@ -241,6 +287,13 @@ def main(steps):
         print(f"checkpoint step {n}", flush=True)
         if "A_seconds" not in out:
             stage_a(model, state, params, out)
+            save(path, out)
+        if "A_grad_scale" not in out:
+            stage_scales(model, state, params, out)
+            if "--scales-side" in flags:  # another process still owns `path` (stage B running)
+                save(path.replace(".npz", "_scales.npz"),
+                     {k: out[k] for k in ("A_grad_scale", "A_diag_scale", "A_off_scale")})
+                continue
             save(path, out)
         if "B_seconds" not in out and "--no-b" not in flags:
             stage_b(model, state, params, out)

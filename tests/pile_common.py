@@ -19,6 +19,31 @@ def golden_path(step):
     return os.path.join(GOLDEN, f"pile_step{step}.npz")
 
 
+def load_golden(step):
+    """The fixture, with the per-block term scales merged in when they were written to a
+    side file (pile_step{N}_scales.npz) while stage B still owned the main file."""
+    g = dict(np.load(golden_path(step)))
+    side = golden_path(step).replace(".npz", "_scales.npz")
+    if os.path.exists(side):
+        for k, v in np.load(side).items():
+            g.setdefault(k, v)
+    return g
+
+
+def scaled_rel(a, b, scale):
+    """max over blocks of ||a - b|| / scale: `scale` is the magnitude of the terms summed
+    into each block (A_*_scale in the fixture), so cancellation in a sum of large
+    opposing contact terms does not inflate the comparison (SURVEY §8(c) comparator 2,
+    norm-relative per block)."""
+    a = np.asarray(a, dtype=float).reshape(len(b), -1)
+    b = np.asarray(b, dtype=float).reshape(len(b), -1)
+    e = np.linalg.norm(a - b, axis=1)
+    scale = np.asarray(scale, dtype=float)
+    if np.any(e[scale == 0] != 0):
+        return np.inf
+    return float((e[scale > 0] / scale[scale > 0]).max()) if np.any(scale > 0) else 0.0
+
+
 def checkpoint(step):
     ck = np.load(os.path.join(ROOT, "bench_data", f"pile_step{step}.npz"))
     return {k: ck[k] for k in ck.files}
