@@ -3,21 +3,22 @@
 // rel_tol=1e-8) (sparse.py:90-161, solver.py:345-348) restated for B200.
 //
 // Per Newton iteration:
-//   * analysis (host, C++): the exactly-zero pattern blocks (overlapping body
-//     boxes without an active contact) are dropped, the remaining block graph
-//     is ordered by minimum degree, the symbolic factor (fill), elimination
-//     tree and its levels are built, and connected components are packed onto
-//     CTAs.  Contact graphs of piles are forests of short chains, so the fill
-//     is ~0 and the tree height is tens of levels.
-//   * factor + solve (k_chol_factor_solve): one CTA walks the levels of its components with
-//     __syncthreads between levels; a warp (lane t = row t) owns one node:
-//     D = A_jj - sum_k L_jk L_jk^T, 12x12 Cholesky, then L_ij = (A_ij -
-//     sum_k L_ik L_jk^T) L_jj^-T for every block of the column.  Left-looking
-//     with fixed update order: deterministic, no atomics.
-//     The forward substitution of node j runs right after its factor; the
-//     backward sweep follows in the same kernel (levels descending).  The
-//     12x12 pivots are in-register Cholesky factors (shuffles, rsqrt per pivot).
-//   * refinement solves (k_chol_solve) reuse the factor and 1 / L_cc.
+//   * analysis (host, C++, on a worker thread overlapping the pair-block
+//     kernels): the exactly-zero pattern blocks (overlapping body boxes without
+//     an active contact) are dropped; the remaining block graph is ordered by
+//     tree contraction (rake / compress) + minimum degree on the 2-core; the
+//     symbolic factor (fill), the elimination tree and the task graph are packed
+//     into one plan buffer.  A plan whose graph contains the new structure is
+//     reused (extra blocks hold exact zeros).
+//   * factor + solve (k_chol_sched): a persistent grid of warps runs node tasks
+//     from one GPU-wide FIFO.  A node's column (D = A_jj - sum L_jk L_jk^T, 12x12
+//     Cholesky, L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T) and its forward
+//     substitution start when its elimination-tree children are done; its
+//     backward substitution when its parent's is done.  Left-looking with a fixed
+//     update order: deterministic, whatever the schedule.  The 12x12 pivots are
+//     in-register Cholesky factors (shuffles, rsqrt per pivot).  Isolated nodes
+//     (no coupling) are single factor + solve tasks.
+//   * refinement solves reuse the factor and 1 / L_cc (same kernel, no factor).
 //   * refinement exactly as solve_refined: r = b - A x over the resident BSR,
 //     stop when |r| <= rel_tol |b|, at most 3 corrections.
 // A failed pivot raises ABD_ERR_FACTORIZATION with the smallest failing
@@ -40,19 +41,31 @@
 
 namespace abd {
 
-constexpr int CH_THREADS = 384;
+constexpr int CH_THREADS = 128;
 constexpr int CH_HW = CH_THREADS / 32;  // warps per CTA (one node per warp, lane t = row t)
+constexpr int CH_MAX_GRID = 128;        // task-graph CTAs: the graph's width, not the GPU's
 
 // Plan layout (one packed int buffer uploaded per analysis).  L holds the n
 // diagonal blocks first (L_jj at index j), then the off-diagonal blocks.
+// Scheduling: every node is a task; a node's factor column (and its forward
+// substitution) may start once all its elimination-tree children are done (its
+// column only reads L blocks of descendants), its backward substitution once its
+// parent's is done.  Ready tasks go through one GPU-wide FIFO; every warp of a
+// persistent grid pops, runs and pushes, so a component's levels spread over all
+// SMs instead of one CTA (a settled pile couples ~2,300 bodies into one component
+// whose elimination tree is ~60 levels deep).  Isolated nodes (no coupling) are
+// independent factor + solve tasks handed out by a second counter.
 struct CholView {
-  int n;
-  const int* nodes;     // node ids, CTA-major then level-major (isolated nodes last)
-  const int* lvl_ptr;   // per CTA: nlvl + 1 offsets into nodes (absolute)
-  const int* cta_lvl;   // per CTA: start index into lvl_ptr
-  const int* cta_nlvl;  // per CTA: number of levels
+  int n, n_coupled, n_leaves, n_iso, n_tasks;  // n_tasks = 2 n_coupled + off-diagonal blocks
+  const int* leaves;    // coupled nodes with no elimination-tree child, deepest first
+  const int* iso;       // isolated nodes
+  const int* parent;    // elimination-tree parent (node id) or -1
+  const int* nchild;    // elimination-tree child counts (initial dependency counters)
+  const int* child_ptr; // n + 1: children of each node
+  const int* child_idx;
   const int* col_ptr;   // n + 1: off-diagonal blocks of column j (index k -> L block n + k)
   const int* blk_row;   // per off block: row node i
+  const int* blk_col;   // per off block: column node j
   const int* bsr_row;   // BSR row_ptr / col: A(i, j) found by binary search in row i (absent: fill)
   const int* bsr_col;
   int* apos;            // per off block: BSR position of A(i, j) or -1, filled by k_chol_apos
@@ -66,12 +79,20 @@ struct CholView {
   double* L;            // L blocks, 144 doubles each (row-major)
   double* dinv;         // n x 12: 1 / L_jj[c][c]
   int* bad;
-  long long* dbg;       // optional per-node phase clocks of CTA 0 (ABD_CHOL_CLOCK)
+  int* dep;             // n: remaining children (reset per launch)
+  int* bleft;           // n: remaining off-diagonal block tasks of each column
+  int* queue;           // n_tasks slots: j (diagonal), n + j (backward), 2n + b (block); -1 = not yet pushed
+  unsigned* ctr;        // [0] pop head, [1] push tail, [2] isolated-node head
+  unsigned long long* trace;  // optional (ABD_CHOL_TRACE_TASKS): per popped slot (item, t_pop, t_start, t_end)
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-// full-warp shuffles: every lane of a warp runs the same node, so no partial-mask
-// convergence checks are generated
+
 // position of block (r, c) in the sorted-column CSR, or -1
 __device__ __forceinline__ int bsr_find(const int* __restrict__ row_ptr, const int* __restrict__ col, int r, int c) {
   int lo = row_ptr[r], hi = row_ptr[r + 1] - 1;
@@ -85,6 +106,8 @@ __device__ __forceinline__ int bsr_find(const int* __restrict__ row_ptr, const i
   return -1;
 }
 
+// full-warp shuffles: every lane of a warp runs the same node, so no partial-mask
+// convergence checks are generated
 __device__ __forceinline__ double hshfl(unsigned mask, double v, int src) { return __shfl_sync(mask, v, src); }
 
 // 1/sqrt(x): MUFU.RSQ64H seed (rsqrt.approx.f64) + 2 Newton steps (>= 53 bits);
@@ -160,250 +183,465 @@ __device__ __forceinline__ double upper_solve12(unsigned mask, int t, double acc
   return x;
 }
 
-// Factor + forward substitution (levels ascending), then backward substitution
-// (levels descending), one CTA per group of components.  x receives y, then x.
 // BSR positions of the factor's off-diagonal source blocks, all nodes in parallel
-// (takes the binary searches off the level-serial critical path)
+// (takes the binary searches off the dependency-serial critical path)
 __global__ void k_chol_apos(CholView v) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= v.n) return;
   for (int b = v.col_ptr[j]; b < v.col_ptr[j + 1]; ++b) v.apos[b] = bsr_find(v.bsr_row, v.bsr_col, v.blk_row[b], j);
 }
 
-__global__ void __launch_bounds__(CH_THREADS) k_chol_factor_solve(CholView v, const double* __restrict__ b,
-                                                                   double* x) {
-  __shared__ double Ss[CH_HW][12][13];  // per warp: staged L_jk / symmetrisation / L_jj
-  __shared__ double Ts[CH_HW][12][13];  // per warp: staged L_jk of update pairs
-  const int hw = threadIdx.x >> 5, t = threadIdx.x & 31;
-  const int tt = t < 12 ? t : 0;
-  const unsigned mask = 0xffffffffu;
-  double (*S)[13] = Ss[hw];
-  double (*T)[13] = Ts[hw];
-  const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
-  for (int l = 0; l < nl; ++l) {
-    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
-    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
-      const int j = v.nodes[idx];
-      long long ck0 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
-      double d[12];
-      {
-        const double* A = v.val + 144 * (int64_t)v.diag_pos[j] + 12 * tt;
+// Data produced by other warps during the launch (L blocks, 1/L_cc, x) is read
+// with ld.global.cg: L1 is not coherent across SMs, and a neighbouring node's
+// entries may share a line that this SM cached before they were written.
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int atom_dec_acq_rel(int* p) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], -1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
+// ---- per-warp operand pipeline: 12x12 blocks staged in shared memory by cp.async
+// (L2-coherent .cg copies; NST stages in flight so the L2 round trips of
+// consecutive block products overlap), products on the FP64 tensor core
+// (mma.m8n8k4.f64: a 12x12x12 product = 2x2 output tiles x 3 k-steps, padded to
+// 16x16; measured 327 vs 1509 cycles per product for the 12-lane FMA form,
+// tools/ubench/chol_upd.cu).
+constexpr int NST = 6;
+struct WarpSmem {
+  double stage[NST][2][144];  // two operand blocks per stage
+  double vec[NST][12];        // y_k per stage (diagonal task)
+  double pa[144];             // prefetched A block (A_jj / A_ij)
+  double pl[144];             // prefetched L_jj (block task)
+  double pv[12];              // prefetched b_j (diagonal task) / 1 / L_jj[c][c] (block task)
+  double S[12][13];           // result rows (+ the forward-substitution column) / L_jj rows
+};
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_pipe() { asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// stage one 12x12 block (1152 B = 72 x 16 B) with the whole warp
+__device__ __forceinline__ void stage_block(double* dst, const double* src, int lane) {
+  for (int c = lane; c < 72; c += 32) cp16(dst + 2 * c, src + 2 * c);
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Warp-wide 12x12 products on m8n8k4 fragments.  Lane l holds A / B fragment
+// entries (row 8 mi + (l >> 2), col 4 kk + (l & 3)) -- the same pattern for both
+// operands, since B = M^T in col layout reads M row-major -- and accumulator
+// entries (row 8 mi + (l >> 2), col 8 ni + 2 (l & 3) + e).  One accumulator set
+// per k-step keeps the three MMAs of a tile independent.
+struct Acc {
+  double c[3][2][2][2];
+};
+__device__ __forceinline__ void acc_zero(Acc& a) {
 #pragma unroll
-        for (int c = 0; c < 12; ++c) d[c] = A[c];
-      }
-      double acc = b[12 * (int64_t)j + tt];
-      // D = A_jj - sum_k L_jk L_jk^T and b_j - sum_k L_jk y_k over the row list of j
-      for (int e = v.row_ptr[j]; e < v.row_ptr[j + 1]; ++e) {
-        const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
-        const double* yk = x + 12 * (int64_t)v.row_col[e];
-        double lr[12];
+  for (int i = 0; i < 24; ++i) (&a.c[0][0][0][0])[i] = 0.0;
+}
+// a -= X Y^T (X, Y 12x12 row-major in shared memory); ycol: optional 12-vector in
+// column 12 of Y^T (the forward substitution's y_k rides along in the padding)
+__device__ __forceinline__ void acc_sub_xyt(Acc& a, const double* X, const double* Y, const double* ycol, int lane) {
+  const int r = lane >> 2, k4 = lane & 3;
 #pragma unroll
-        for (int m = 0; m < 12; ++m) lr[m] = Lk[m];
-        __syncwarp(mask);
-        if (t < 12) {
+  for (int kk = 0; kk < 3; ++kk) {
+    double fa[2], fb[2];
 #pragma unroll
-          for (int m = 0; m < 12; ++m) S[t][m] = lr[m];
-        }
-        __syncwarp(mask);
-        double s2 = 0.0;
-#pragma unroll
-        for (int m = 0; m < 12; ++m) s2 = fma(lr[m], yk[m], s2);
-        acc -= s2;
-#pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int m = 0; m < 12; ++m) s = fma(lr[m], S[c][m], s);
-          d[c] -= s;
-        }
-      }
-      // symmetrise (sparse.py:117: cholesky(0.5 (D + D^T)))
-      __syncwarp(mask);
-      if (t < 12) {
-#pragma unroll
-        for (int c = 0; c < 12; ++c) S[t][c] = d[c];
-      }
-      __syncwarp(mask);
-#pragma unroll
-      for (int c = 0; c < 12; ++c) d[c] = 0.5 * (d[c] + S[c][tt]);
-      double rinv[12];
-      long long ck1 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
-      const bool ok = chol12(mask, t, d, rinv);
-      long long ck2 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
-      if (!ok && t == 0) atomicMin(v.bad, j);
-      __syncwarp(mask);
-      if (t < 12) {
-        double* Ld = v.L + 144 * (int64_t)j + 12 * t;
-#pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          Ld[c] = d[c];
-          S[t][c] = d[c];  // L_jj rows for the off-diagonal solves below
-        }
-        double mine = rinv[0];
-#pragma unroll
-        for (int c = 1; c < 12; ++c)
-          if (c == t) mine = rinv[c];
-        v.dinv[12 * (int64_t)j + t] = mine;
-      }
-      // forward substitution for node j
-      const double y = lower_solve12(mask, t, acc, d, rinv);
-      if (t < 12) x[12 * (int64_t)j + t] = y;
-      __syncwarp(mask);
-      long long ck3 = (v.dbg && blockIdx.x == 0) ? clock64() : 0;
-      // off-diagonal blocks of column j: L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
-      for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
-        double bt[12];
-        const int ap = v.apos[bb];
-        if (ap >= 0) {
-          const double* A = v.val + 144 * (int64_t)ap + 12 * tt;
-#pragma unroll
-          for (int c = 0; c < 12; ++c) bt[c] = A[c];
-        } else {
-#pragma unroll
-          for (int c = 0; c < 12; ++c) bt[c] = 0.0;
-        }
-        for (int u = v.upd_ptr[bb]; u < v.upd_ptr[bb + 1]; ++u) {
-          const int2 pq = v.upd[u];
-          const double* Li = v.L + 144 * (int64_t)pq.x + 12 * tt;  // row t of L_ik
-          const double* Lj = v.L + 144 * (int64_t)pq.y + 12 * tt;  // row t of L_jk (staged)
-          double lr[12];
-#pragma unroll
-          for (int m = 0; m < 12; ++m) lr[m] = Li[m];
-          __syncwarp(mask);
-          if (t < 12) {
-#pragma unroll
-            for (int m = 0; m < 12; ++m) T[t][m] = Lj[m];
-          }
-          __syncwarp(mask);
-#pragma unroll
-          for (int c = 0; c < 12; ++c) {
-            double s = 0.0;
-#pragma unroll
-            for (int m = 0; m < 12; ++m) s = fma(lr[m], T[c][m], s);
-            bt[c] -= s;
-          }
-        }
-        // row t of X with X L_jj^T = B (forward substitution against L_jj rows)
-        double xr[12];
-#pragma unroll
-        for (int c = 0; c < 12; ++c) {
-          double s = bt[c];
-#pragma unroll
-          for (int m = 0; m < 12; ++m)
-            if (m < c) s = fma(-S[c][m], xr[m], s);
-          xr[c] = s * rinv[c];
-        }
-        if (t < 12) {
-          double* Lo = v.L + 144 * (int64_t)(v.n + bb) + 12 * t;
-#pragma unroll
-          for (int c = 0; c < 12; ++c) Lo[c] = xr[c];
-        }
-      }
-      __syncwarp(mask);
-      if (v.dbg && blockIdx.x == 0 && t == 0 && idx - v.lvl_ptr[c0] < 256) {
-        long long* o = v.dbg + 8 * (idx - v.lvl_ptr[c0]);
-        o[0] = j;
-        o[1] = l;
-        o[2] = ck0;
-        o[3] = ck1;
-        o[4] = ck2;
-        o[5] = ck3;
-        o[6] = clock64();
-        o[7] = v.col_ptr[j + 1] - v.col_ptr[j];
-      }
+    for (int mi = 0; mi < 2; ++mi) {
+      const bool in = 8 * mi + r < 12;
+      fa[mi] = in ? -X[(8 * mi + r) * 12 + 4 * kk + k4] : 0.0;
+      fb[mi] = in ? Y[(8 * mi + r) * 12 + 4 * kk + k4] : ((ycol && mi == 1 && r == 4) ? ycol[4 * kk + k4] : 0.0);
     }
-    __syncthreads();
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) dmma(a.c[kk][mi][ni][0], a.c[kk][mi][ni][1], fa[mi], fb[ni]);
   }
-  // backward: L^T x = y, levels descending
-  for (int l = nl - 1; l >= 0; --l) {
-    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
-    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
-      const int j = v.nodes[idx];
-      double acc = x[12 * (int64_t)j + tt];
-      for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
-        const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;  // column tt of L_ij
-        const double* xi = x + 12 * (int64_t)v.blk_row[bb];
-        double s = 0.0;
+}
+// out[r][c] = base[r][c] + acc (r, c < 12; column 12 = vbase[r] + acc when vbase)
+__device__ __forceinline__ void acc_store(const Acc& a, const double* base, const double* vbase,
+                                          double (*out)[13], int lane) {
+  const int r = lane >> 2, c2 = 2 * (lane & 3);
 #pragma unroll
-        for (int r = 0; r < 12; ++r) s = fma(Lb[12 * r], xi[r], s);
-        acc -= s;
-      }
-      double lcol[12], rinv[12];
-      const double* Ld = v.L + 144 * (int64_t)j + tt;
-      const double* di = v.dinv + 12 * (int64_t)j;
+  for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int m = 0; m < 12; ++m) {
-        lcol[m] = Ld[12 * m];
-        rinv[m] = di[m];
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 8 * mi + r, col = 8 * ni + c2 + e;
+        const double s = a.c[0][mi][ni][e] + a.c[1][mi][ni][e] + a.c[2][mi][ni][e];
+        if (row < 12 && col < 12) out[row][col] = (base ? base[row * 12 + col] : 0.0) + s;
+        else if (row < 12 && col == 12 && vbase) out[row][12] = vbase[row] + s;
       }
-      const double xv = upper_solve12(mask, t, acc, lcol, rinv);
-      __syncwarp(mask);
-      if (t < 12) x[12 * (int64_t)j + t] = xv;
+}
+
+// Diagonal task of node j.  factor: D = A_jj - sum_k L_jk L_jk^T over the row list
+// (fixed order), L_jj = chol(0.5 (D + D^T)), y_j = L_jj^-1 (b_j - sum_k L_jk y_k).
+// !factor: y_j only, with the resident factor.
+__device__ __forceinline__ void chol_diag(const CholView& v, int j, const double* __restrict__ b, double* x,
+                                          bool factor, WarpSmem& sm) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  const unsigned mask = 0xffffffffu;
+  double d[12], rinv[12];
+  const int e0 = v.row_ptr[j], U = v.row_ptr[j + 1] - e0;
+  if (!factor) {  // refinement solve: y_j = L_jj^-1 (b_j - sum_k L_jk y_k), scalar
+    double acc = b[12 * (int64_t)j + tt];
+    for (int e = e0; e < e0 + U; ++e) {
+      const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
+      const double* yk = x + 12 * (int64_t)v.row_col[e];
+      double s2 = 0.0;
+#pragma unroll
+      for (int m = 0; m < 12; ++m) s2 = fma(Lk[m], __ldcg(yk + m), s2);
+      acc -= s2;
     }
-    __syncthreads();
+    const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
+    const double* di = v.dinv + 12 * (int64_t)j;
+#pragma unroll
+    for (int m = 0; m < 12; ++m) {
+      d[m] = Ld[m];
+      rinv[m] = di[m];
+    }
+    const double y = lower_solve12(mask, t, acc, d, rinv);
+    if (t < 12) x[12 * (int64_t)j + t] = y;
+    return;
+  }
+  // prefetch A_jj and b_j, then the row list's L_jk / y_k stages
+  stage_block(sm.pa, v.val + 144 * (int64_t)v.diag_pos[j], t);
+  if (t < 6) cp16(sm.pv + 2 * t, b + 12 * (int64_t)j + 2 * t);
+  cp_commit();
+  auto issue = [&](int u) {
+    const int e = e0 + u;
+    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)v.row_blk[e], t);
+    if (t < 6) cp16(sm.vec[u % NST] + 2 * t, x + 12 * (int64_t)v.row_col[e] + 2 * t);
+  };
+  for (int p = 0; p < NST - 1; ++p) {
+    if (p < U) issue(p);
+    cp_commit();
+  }
+  Acc ac;
+  acc_zero(ac);
+  for (int u = 0; u < U; ++u) {
+    cp_wait_pipe();
+    __syncwarp(mask);
+    const double* Lk = sm.stage[u % NST][0];
+    acc_sub_xyt(ac, Lk, Lk, sm.vec[u % NST], t);
+    __syncwarp(mask);
+    if (u + NST - 1 < U) issue(u + NST - 1);
+    cp_commit();
+  }
+  cp_wait_all();
+  __syncwarp(mask);
+  double (*S)[13] = sm.S;
+  acc_store(ac, sm.pa, sm.pv, S, t);
+  __syncwarp(mask);
+  // symmetrise (sparse.py:117: cholesky(0.5 (D + D^T)))
+#pragma unroll
+  for (int c = 0; c < 12; ++c) d[c] = 0.5 * (S[tt][c] + S[c][tt]);
+  const double acc = S[tt][12];
+  __syncwarp(mask);
+  const bool ok = chol12(mask, t, d, rinv);
+  if (!ok && t == 0) atomicMin(v.bad, j);
+  if (t < 12) {
+    double* Ld = v.L + 144 * (int64_t)j + 12 * t;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) Ld[c] = d[c];
+    double mine = rinv[0];
+#pragma unroll
+    for (int c = 1; c < 12; ++c)
+      if (c == t) mine = rinv[c];
+    v.dinv[12 * (int64_t)j + t] = mine;
+  }
+  const double y = lower_solve12(mask, t, acc, d, rinv);
+  if (t < 12) x[12 * (int64_t)j + t] = y;
+}
+
+// Block task: L_ij = (A_ij - sum_u L_ik L_jk^T) L_jj^-T for one off-diagonal block of
+// column j (its update pairs in fixed order), after j's diagonal task.
+__device__ __forceinline__ void chol_block(const CholView& v, int bb, WarpSmem& sm) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  const unsigned mask = 0xffffffffu;
+  const int j = v.blk_col[bb];
+  const int ap = v.apos[bb];
+  // prefetch A_ij (absent: fill), L_jj and 1 / L_jj[c][c], then the update stages
+  if (ap >= 0) stage_block(sm.pa, v.val + 144 * (int64_t)ap, t);
+  stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
+  if (t < 6) cp16(sm.pv + 2 * t, v.dinv + 12 * (int64_t)j + 2 * t);
+  cp_commit();
+  const int u0 = v.upd_ptr[bb], U = v.upd_ptr[bb + 1] - u0;
+  auto issue = [&](int u) {
+    const int2 pq = v.upd[u0 + u];
+    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)pq.x, t);  // L_ik
+    stage_block(sm.stage[u % NST][1], v.L + 144 * (int64_t)pq.y, t);  // L_jk
+  };
+  for (int p = 0; p < NST - 1; ++p) {
+    if (p < U) issue(p);
+    cp_commit();
+  }
+  Acc ac;
+  acc_zero(ac);
+  for (int u = 0; u < U; ++u) {
+    cp_wait_pipe();
+    __syncwarp(mask);
+    acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][1], nullptr, t);
+    __syncwarp(mask);
+    if (u + NST - 1 < U) issue(u + NST - 1);
+    cp_commit();
+  }
+  cp_wait_all();
+  __syncwarp(mask);
+  double (*S)[13] = sm.S;
+  acc_store(ac, ap >= 0 ? sm.pa : nullptr, nullptr, S, t);
+  __syncwarp(mask);
+  double bt[12], rinv[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    bt[c] = S[tt][c];
+    rinv[c] = sm.pv[c];
+  }
+  // row t of X with X L_jj^T = B (forward substitution against the rows of L_jj)
+  const double* Lj = sm.pl;
+  double xr[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    double s = bt[c];
+#pragma unroll
+    for (int m = 0; m < 12; ++m)
+      if (m < c) s = fma(-Lj[12 * c + m], xr[m], s);
+    xr[c] = s * rinv[c];
+  }
+  __syncwarp(mask);
+  if (t < 12) {
+    double* Lo = v.L + 144 * (int64_t)(v.n + bb) + 12 * t;
+#pragma unroll
+    for (int c = 0; c < 12; ++c) Lo[c] = xr[c];
   }
 }
 
-// x = A^-1 b with the resident factor (refinement corrections)
-__global__ void __launch_bounds__(CH_THREADS) k_chol_solve(CholView v, const double* __restrict__ b, double* x) {
-  const int hw = threadIdx.x >> 5, t = threadIdx.x & 31;
+// Backward task of node j: x_j = L_jj^-T (y_j - sum_i L_ij^T x_i) over its column.
+__device__ __forceinline__ void chol_backward(const CholView& v, int j, double* x) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
   const unsigned mask = 0xffffffffu;
-  const int c0 = v.cta_lvl[blockIdx.x], nl = v.cta_nlvl[blockIdx.x];
-  const int tt = t < 12 ? t : 0;
-  for (int l = 0; l < nl; ++l) {
-    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
-    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
-      const int j = v.nodes[idx];
-      double acc = b[12 * (int64_t)j + tt];
-      for (int e = v.row_ptr[j]; e < v.row_ptr[j + 1]; ++e) {
-        const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
-        const double* yk = x + 12 * (int64_t)v.row_col[e];
-        double s = 0.0;
+  double acc = ldcg(x + 12 * (int64_t)j + tt);
+  for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
+    const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;  // column tt of L_ij
+    const double* xi = x + 12 * (int64_t)v.blk_row[bb];
+    double s = 0.0;
 #pragma unroll
-        for (int m = 0; m < 12; ++m) s = fma(Lk[m], yk[m], s);
-        acc -= s;
-      }
-      double lrow[12], rinv[12];
-      const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
-      const double* di = v.dinv + 12 * (int64_t)j;
-#pragma unroll
-      for (int m = 0; m < 12; ++m) {
-        lrow[m] = Ld[m];
-        rinv[m] = di[m];
-      }
-      const double y = lower_solve12(mask, t, acc, lrow, rinv);
-      if (t < 12) x[12 * (int64_t)j + t] = y;
-    }
-    __syncthreads();
+    for (int r = 0; r < 12; ++r) s = fma(ldcg(Lb + 12 * r), ldcg(xi + r), s);
+    acc -= s;
   }
-  for (int l = nl - 1; l >= 0; --l) {
-    const int lo = v.lvl_ptr[c0 + l], hi = v.lvl_ptr[c0 + l + 1];
-    for (int idx = lo + hw; idx < hi; idx += CH_HW) {
-      const int j = v.nodes[idx];
-      double acc = x[12 * (int64_t)j + tt];
-      for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
-        const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;
-        const double* xi = x + 12 * (int64_t)v.blk_row[bb];
-        double s = 0.0;
+  double lcol[12], rinv[12];
+  const double* Ld = v.L + 144 * (int64_t)j + tt;
+  const double* di = v.dinv + 12 * (int64_t)j;
 #pragma unroll
-        for (int r = 0; r < 12; ++r) s = fma(Lb[12 * r], xi[r], s);
-        acc -= s;
-      }
-      double lcol[12], rinv[12];
-      const double* Ld = v.L + 144 * (int64_t)j + tt;
-      const double* di = v.dinv + 12 * (int64_t)j;
+  for (int m = 0; m < 12; ++m) {
+    lcol[m] = ldcg(Ld + 12 * m);
+    rinv[m] = ldcg(di + m);
+  }
+  const double xv = upper_solve12(mask, t, acc, lcol, rinv);
+  __syncwarp(mask);
+  if (t < 12) x[12 * (int64_t)j + t] = xv;
+}
+
+// Isolated node: factor (or reuse) L_jj and solve both triangles in one task.
+__device__ __forceinline__ void chol_isolated(const CholView& v, int j, const double* __restrict__ b, double* x,
+                                              bool factor, double (*S)[13]) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  const unsigned mask = 0xffffffffu;
+  double d[12], rinv[12];
+  const double acc = b[12 * (int64_t)j + tt];
+  if (factor) {
+    const double* A = v.val + 144 * (int64_t)v.diag_pos[j] + 12 * tt;
 #pragma unroll
-      for (int m = 0; m < 12; ++m) {
-        lcol[m] = Ld[12 * m];
-        rinv[m] = di[m];
-      }
-      const double xv = upper_solve12(mask, t, acc, lcol, rinv);
-      __syncwarp(mask);
-      if (t < 12) x[12 * (int64_t)j + t] = xv;
+    for (int c = 0; c < 12; ++c) d[c] = A[c];
+    __syncwarp(mask);
+    if (t < 12) {
+#pragma unroll
+      for (int c = 0; c < 12; ++c) S[t][c] = d[c];
     }
-    __syncthreads();
+    __syncwarp(mask);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) d[c] = 0.5 * (d[c] + S[c][tt]);
+    const bool ok = chol12(mask, t, d, rinv);
+    if (!ok && t == 0) atomicMin(v.bad, j);
+    if (t < 12) {
+      double* Ld = v.L + 144 * (int64_t)j + 12 * t;
+#pragma unroll
+      for (int c = 0; c < 12; ++c) Ld[c] = d[c];
+      double mine = rinv[0];
+#pragma unroll
+      for (int c = 1; c < 12; ++c)
+        if (c == t) mine = rinv[c];
+      v.dinv[12 * (int64_t)j + t] = mine;
+    }
+  } else {
+    const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
+    const double* di = v.dinv + 12 * (int64_t)j;
+#pragma unroll
+    for (int m = 0; m < 12; ++m) {
+      d[m] = Ld[m];
+      rinv[m] = di[m];
+    }
+  }
+  const double y = lower_solve12(mask, t, acc, d, rinv);
+  // column t of L from the rows (transpose through shared memory)
+  __syncwarp(mask);
+  if (t < 12) {
+#pragma unroll
+    for (int c = 0; c < 12; ++c) S[t][c] = d[c];
+  }
+  __syncwarp(mask);
+  double lcol[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) lcol[c] = S[c][tt];
+  const double xv = upper_solve12(mask, t, y, lcol, rinv);
+  __syncwarp(mask);
+  if (t < 12) x[12 * (int64_t)j + t] = xv;
+}
+
+__global__ void k_chol_sched_init(CholView v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n) {
+    v.dep[i] = v.nchild[i];
+    v.bleft[i] = v.col_ptr[i + 1] - v.col_ptr[i];
+  }
+  if (i < v.n_tasks) v.queue[i] = i < v.n_leaves ? v.leaves[i] : -1;
+  if (i < 3) v.ctr[i] = i == 1 ? (unsigned)v.n_leaves : 0u;
+}
+
+// Isolated nodes (no coupling): one independent factor + solve per warp.
+__global__ void __launch_bounds__(CH_THREADS) k_chol_iso(CholView v, const double* __restrict__ b, double* x,
+                                                         int factor) {
+  __shared__ double Ss[CH_HW][12][13];
+  const int hw = threadIdx.x >> 5;
+  for (int i = blockIdx.x * CH_HW + hw; i < v.n_iso; i += gridDim.x * CH_HW)
+    chol_isolated(v, v.iso[i], b, x, factor != 0, Ss[hw]);
+}
+
+__device__ __forceinline__ void push_task(const CholView& v, int item) {
+  const unsigned slot = atomicAdd(v.ctr + 1, 1u);
+  st_release(v.queue + slot, item);
+}
+
+// node j is complete (its column of L and y_j): release its parent, or start the
+// backward sweep at a root.  Lane 0 only, after the warp's writes are fenced.
+__device__ __forceinline__ void node_done(const CholView& v, int j) {
+  const int p = v.parent[j];
+  if (p < 0) push_task(v, v.n + j);
+  else if (atom_dec_acq_rel(v.dep + p) == 1) push_task(v, p);
+}
+
+// Persistent factor (+ forward / backward substitution) over the task FIFO of the
+// coupled nodes.  Tasks: j < n -> diagonal task of node j; n + j -> backward task
+// of node j; 2n + b -> off-diagonal block task b (factor only).  A warp that pops
+// a slot not yet pushed polls it with backoff: every unpushed slot is produced by
+// a warp that is running a task, so the grid cannot deadlock, whatever the
+// residency.  The grid is sized to the task graph's width, not the GPU: idle
+// pollers would only load L2.
+__global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const double* __restrict__ b, double* x,
+                                                           int factor) {
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  const int hw = threadIdx.x >> 5, t = threadIdx.x & 31;
+  WarpSmem& sm = reinterpret_cast<WarpSmem*>(ch_smem)[hw];
+  const unsigned mask = 0xffffffffu;
+  const bool fac = factor != 0;
+  const int total = fac ? v.n_tasks : 2 * v.n_coupled;
+  for (;;) {
+    int idx = 0;
+    if (t == 0) idx = (int)atomicAdd(v.ctr, 1u);
+    idx = __shfl_sync(mask, idx, 0);
+    if (idx >= total) break;
+    const unsigned long long t_pop = v.trace ? gtimer() : 0;
+    int item = -1;
+    if (t == 0) {
+      unsigned ns = 32;
+      while ((item = ld_acquire(v.queue + idx)) < 0) {
+        __nanosleep(ns);
+        ns = min(2u * ns, 1024u);
+      }
+    }
+    item = __shfl_sync(mask, item, 0);
+    __syncwarp(mask);
+    __threadfence();
+    const unsigned long long t_start = v.trace ? gtimer() : 0;
+    if (item < v.n) {  // diagonal task
+      const int j = item;
+      chol_diag(v, j, b, x, fac, sm);
+      __threadfence();
+      __syncwarp(mask);
+      if (v.trace && t == 0) {
+        unsigned long long* o = v.trace + 4 * (int64_t)idx;
+        o[0] = (unsigned long long)item | ((unsigned long long)(unsigned)(v.row_ptr[j + 1] - v.row_ptr[j]) << 32);
+        o[1] = t_pop;
+        o[2] = t_start;
+        o[3] = gtimer();
+      }
+      const int c0 = v.col_ptr[j], c1 = v.col_ptr[j + 1];
+      if (t == 0) {
+        if (fac && c1 > c0) {
+          const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0));
+          for (int c = c0; c < c1; ++c) st_release(v.queue + slot + (c - c0), 2 * v.n + c);
+        } else {
+          node_done(v, j);
+        }
+      }
+    } else if (item < 2 * v.n) {  // backward task
+      const int j = item - v.n;
+      chol_backward(v, j, x);
+      __threadfence();
+      __syncwarp(mask);
+      if (v.trace && t == 0) {
+        unsigned long long* o = v.trace + 4 * (int64_t)idx;
+        o[0] = (unsigned long long)item;
+        o[1] = t_pop;
+        o[2] = t_start;
+        o[3] = gtimer();
+      }
+      const int c0 = v.child_ptr[j], c1 = v.child_ptr[j + 1];
+      if (t == 0 && c1 > c0) {
+        const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0));
+        for (int c = c0; c < c1; ++c) st_release(v.queue + slot + (c - c0), v.n + v.child_idx[c]);
+      }
+    } else {  // off-diagonal block task
+      const int bb = item - 2 * v.n;
+      chol_block(v, bb, sm);
+      __threadfence();
+      __syncwarp(mask);
+      if (v.trace && t == 0) {
+        unsigned long long* o = v.trace + 4 * (int64_t)idx;
+        o[0] = (unsigned long long)item | ((unsigned long long)(unsigned)(v.upd_ptr[bb + 1] - v.upd_ptr[bb]) << 32);
+        o[1] = t_pop;
+        o[2] = t_start;
+        o[3] = gtimer();
+      }
+      if (t == 0) {
+        const int j = v.blk_col[bb];
+        if (atom_dec_acq_rel(v.bleft + j) == 1) node_done(v, j);
+      }
+    }
   }
 }
+
 
 // nonzero flags of the upper off-diagonal pattern blocks
 __global__ void k_block_nz(int64_t n_off, const int* __restrict__ upper_pos, const double* __restrict__ val,
@@ -458,6 +696,51 @@ __global__ void k_resid(int n, const int* __restrict__ row_ptr, const int* __res
 __global__ void k_add_inplace(int64_t n, double* x, const double* d) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) x[i] += d[i];
+}
+
+// Sections of the packed plan buffer
+enum { CH_LEAVES, CH_ISO, CH_PARENT, CH_NCHILD, CH_CHILDP, CH_CHILDI, CH_COLP, CH_BROW, CH_BCOL, CH_ROWP, CH_ROWB,
+       CH_ROWC, CH_UPDP, CH_UPD, CH_NSEC };
+
+static CholView plan_view(Scene& s) {
+  Scene::Work& w = s.w;
+  const size_t* o = w.ch_cache.offs;
+  const int* dp = w.ch_plan.p;
+  const int n = s.H.n;
+  const int m = (int)w.ch_cache.stats[1];
+  const int nbo = (int)(w.ch_cache.stats[2] - n);
+  return CholView{n,
+                  m,
+                  (int)w.ch_cache.stats[7],
+                  n - m,
+                  2 * m + nbo,
+                  dp + o[CH_LEAVES],
+                  dp + o[CH_ISO],
+                  dp + o[CH_PARENT],
+                  dp + o[CH_NCHILD],
+                  dp + o[CH_CHILDP],
+                  dp + o[CH_CHILDI],
+                  dp + o[CH_COLP],
+                  dp + o[CH_BROW],
+                  dp + o[CH_BCOL],
+                  s.H.row_ptr.p,
+                  s.H.col.p,
+                  w.ch_apos.p,
+                  dp + o[CH_ROWP],
+                  dp + o[CH_ROWB],
+                  dp + o[CH_ROWC],
+                  dp + o[CH_UPDP],
+                  reinterpret_cast<const int2*>(dp + o[CH_UPD]),
+                  s.H.diag_pos.p,
+                  s.H.val.p,
+                  w.ch_L.p,
+                  w.ch_dinv.p,
+                  w.bad.p,
+                  w.ch_dep.p,
+                  w.ch_bleft.p,
+                  w.ch_queue.p,
+                  w.ch_ctr.p,
+                  nullptr};
 }
 
 // ---------------------------------------------------------------------------
@@ -543,29 +826,6 @@ static Analysis chol_analyze(Scene& s) {
   an.ms_sync = ms_since(t0);
   t0 = clk::now();
   Scene::Work::CholCache& cc = w.ch_cache;
-  auto make_view = [&](const size_t* o) {
-    const int* dp = w.ch_plan.p;
-    return CholView{n,
-                    dp + o[0],
-                    dp + o[1],
-                    dp + o[2],
-                    dp + o[3],
-                    dp + o[4],
-                    dp + o[5],
-                    H.row_ptr.p,
-                    H.col.p,
-                    w.ch_apos.p,
-                    dp + o[7],
-                    dp + o[8],
-                    dp + o[9],
-                    dp + o[10],
-                    reinterpret_cast<const int2*>(dp + o[11]),
-                    H.diag_pos.p,
-                    H.val.p,
-                    w.ch_L.p,
-                    w.ch_dinv.p,
-                    w.bad.p};
-  };
   // nonzero couplings (keys are sorted (i < j)); the cached plan is reused when
   // they are a subset of the cached graph (extra blocks then hold exact zeros)
   std::vector<uint64_t>& cur = w.ch_edges_cur;
@@ -581,7 +841,7 @@ static Analysis chol_analyze(Scene& s) {
     an.n_edges = cc.stats[4];
     an.max_level = (int)cc.stats[5];
     an.largest = (int)cc.stats[6];
-    an.view = make_view(cc.offs);
+    an.view = plan_view(s);
     an.cached = true;
     ++cc.hits;
     return an;
@@ -598,6 +858,16 @@ static Analysis chol_analyze(Scene& s) {
     cur.swap(un);
   }
 
+  static const char* dump_graph = getenv("ABD_CHOL_DUMP_GRAPH");  // tools: coupling graph of the last analysis
+  if (dump_graph) {
+    if (FILE* f = fopen(dump_graph, "wb")) {
+      const int64_t ne = (int64_t)cur.size();
+      fwrite(&n, sizeof(int), 1, f);
+      fwrite(&ne, sizeof(int64_t), 1, f);
+      fwrite(cur.data(), sizeof(uint64_t), cur.size(), f);
+      fclose(f);
+    }
+  }
   // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order;
   // host scratch persists across analyses (no allocations in the steady state)
   std::vector<int>&loc = w.hs_i[0], &glob = w.hs_i[1], &adj_ptr = w.hs_i[2], &adj_idx = w.hs_i[3],
@@ -789,8 +1059,7 @@ static Analysis chol_analyze(Scene& s) {
   // row lists (local i): (k, off block) for k eliminated before i, in elimination order of k
   std::vector<int>&rcnt = w.hs_i[14], &rfill = w.hs_i[15], &r_k = w.hs_i[16], &r_b = w.hs_i[17],
                    &upd_ptr = w.hs_i[18], &upd = w.hs_i[19], &level = w.hs_i[20], &root = w.hs_i[21],
-                   &csize = w.hs_i[22], &cdepth = w.hs_i[23], &comps = w.hs_i[24], &cta_of = w.hs_i[25],
-                   &cta_nlvl = w.hs_i[26], &lcnt = w.hs_i[27], &fillp = w.hs_i[28];
+                   &csize = w.hs_i[22], &cdepth = w.hs_i[23], &comps = w.hs_i[24];
   rcnt.assign(m + 1, 0);
   for (int e = 0; e < nbo; ++e) rcnt[csi[e] + 1]++;
   for (int v = 0; v < m; ++v) rcnt[v + 1] += rcnt[v];
@@ -856,79 +1125,85 @@ static Analysis chol_analyze(Scene& s) {
     fprintf(stderr, "\n");
   }
   an.ms_sub[3] = ms_since(t0);
-  // CTAs: components (largest first onto the least loaded), then isolated nodes
-  const int n_iso = n - m;
-  const int iso_per_cta = 4 * CH_HW;
-  const int n_ccta = std::min((int)comps.size(), 2 * s.num_sms);
-  const int n_icta = (n_iso + iso_per_cta - 1) / iso_per_cta;
-  const int n_cta = std::max(1, n_ccta + n_icta);
-  an.n_cta = n_cta;
-  cta_of.assign(m, -1);
-  cta_nlvl.assign(n_cta, 0);
-  {
-    typedef std::pair<int64_t, int> LI;
-    std::priority_queue<LI, std::vector<LI>, std::greater<LI>> load;
-    for (int c = 0; c < n_ccta; ++c) load.push({0, c});
-    for (int r : comps) {
-      LI top = load.top();
-      load.pop();
-      cta_of[r] = top.second;
-      cta_nlvl[top.second] = std::max(cta_nlvl[top.second], cdepth[r]);
-      top.first += (int64_t)csize[r] + 8 * (int64_t)cdepth[r];
-      load.push(top);
-    }
-  }
-  for (int c = n_ccta; c < n_cta; ++c) cta_nlvl[c] = (n_iso > 0) ? 1 : 0;
-
   an.ms_sub[4] = ms_since(t0);
-  // packed plan: nodes | lvl_ptr | cta_lvl | cta_nlvl | col_ptr | blk_row | blk_apos | row_ptr |
-  //              row_blk | row_col | upd_ptr | (pad) | upd pairs
-  int n_lvl_entries = 0;
-  for (int c = 0; c < n_cta; ++c) n_lvl_entries += cta_nlvl[c] + 1;
-  size_t off_nodes = 0, off_lvl = off_nodes + n, off_ctal = off_lvl + n_lvl_entries, off_ctan = off_ctal + n_cta,
-         off_colp = off_ctan + n_cta, off_brow = off_colp + n + 1, off_bapos = off_brow + nbo,
-         off_rowp = off_bapos + nbo, off_rowb = off_rowp + n + 1, off_rowc = off_rowb + nbo,
-         off_updp = off_rowc + nbo, off_upd = off_updp + nbo + 1;
-  off_upd += off_upd & 1;  // int2 alignment
-  const size_t total = off_upd + upd.size() + 2;
-  int* hp = w.h_plan.reserve(total);
-  int* nodes = hp + off_nodes;
-  int* lvl_ptr = hp + off_lvl;
-  int* cta_lvl = hp + off_ctal;
-  int* cta_nl = hp + off_ctan;
-  {
-    // count nodes per (cta, level), then prefix offsets
-    int e = 0;
-    for (int c = 0; c < n_cta; ++c) {
-      cta_lvl[c] = e;
-      cta_nl[c] = cta_nlvl[c];
-      e += cta_nlvl[c] + 1;
-    }
-    std::vector<int>& cnt = lcnt;
-    cnt.assign(n_lvl_entries + 1, 0);
-    for (int v = 0; v < m; ++v) cnt[cta_lvl[cta_of[root[v]]] + level[v]]++;
-    int run = 0;
-    for (int c = 0; c < n_ccta; ++c)
-      for (int l = 0; l <= cta_nlvl[c]; ++l) {
-        int ix = cta_lvl[c] + l;
-        lvl_ptr[ix] = run;
-        if (l < cta_nlvl[c]) run += cnt[ix];
-      }
-    fillp.assign(lvl_ptr, lvl_ptr + n_lvl_entries);
-    for (int v = 0; v < m; ++v) nodes[fillp[cta_lvl[cta_of[root[v]]] + level[v]]++] = glob[v];
-    // isolated nodes, iso_per_cta per CTA in node order
-    int iso = m;
-    for (int c = n_ccta; c < n_cta; ++c) {
-      lvl_ptr[cta_lvl[c]] = iso;
-      iso = std::min(n, iso + iso_per_cta);
-      lvl_ptr[cta_lvl[c] + 1] = iso;
-    }
-    int q = m;
-    for (int v = 0; v < n; ++v)
-      if (loc[v] < 0) nodes[q++] = v;
+  // task graph: elimination-tree parents, child lists, leaves (deepest first), isolated nodes
+  std::vector<int>&par = w.hs_i[26], &dep = w.hs_i[27], &leaves = w.hs_i[28];
+  par.assign(m, -1);
+  for (int v = 0; v < m; ++v)
+    if (csp[v + 1] > csp[v]) par[v] = csi[csp[v]];
+  dep.assign(m, 0);
+  for (int q = m - 1; q >= 0; --q) {
+    const int v = order[q];
+    dep[v] = par[v] < 0 ? 0 : dep[par[v]] + 1;
   }
-  int* col_ptr = hp + off_colp;
-  int* row_ptr = hp + off_rowp;
+  std::vector<int> nch(m, 0);
+  for (int v = 0; v < m; ++v)
+    if (par[v] >= 0) nch[par[v]]++;
+  leaves.clear();
+  for (int v = 0; v < m; ++v)
+    if (nch[v] == 0) leaves.push_back(v);
+  std::sort(leaves.begin(), leaves.end(),
+            [&](int a2, int b2) { return dep[a2] != dep[b2] ? dep[a2] > dep[b2] : glob[a2] < glob[b2]; });
+  const int n_leaves = (int)leaves.size();
+  const int n_iso = n - m;
+  an.n_cta = 0;  // set at launch
+  static const bool trace_cp = getenv("ABD_TRACE_CHOL") != nullptr;
+  if (trace_cp) {  // task costs in 12x12 block products: rows + sum over column blocks (1 + updates)
+    std::vector<int64_t> cost(m, 0), cp(m, 0);
+    int64_t tot = 0, maxc = 0, maxcp = 0;
+    int maxcol = 0, maxrow = 0;
+    for (int v : order) {
+      int64_t c = rcnt[v + 1] - rcnt[v];
+      for (int b2 = csp[v]; b2 < csp[v + 1]; ++b2) c += 1 + (upd_ptr[b2 + 1] - upd_ptr[b2]);
+      cost[v] = c;
+      cp[v] += c;
+      if (par[v] >= 0) cp[par[v]] = std::max(cp[par[v]], cp[v]);
+      tot += c;
+      maxc = std::max(maxc, c);
+      maxcp = std::max(maxcp, cp[v]);
+      maxcol = std::max(maxcol, csp[v + 1] - csp[v]);
+      maxrow = std::max(maxrow, rcnt[v + 1] - rcnt[v]);
+    }
+    fprintf(stderr, "[abd chol cp] m=%d core=%d leaves=%d total=%lld maxcost=%lld critpath=%lld maxcol=%d maxrow=%d\n",
+            m, n_core, n_leaves, (long long)tot, (long long)maxc, (long long)maxcp, maxcol, maxrow);
+  }
+  // packed plan: leaves | iso | parent | nchild | child_ptr | child_idx | col_ptr | blk_row |
+  //              row_ptr | row_blk | row_col | upd_ptr | (pad) | upd pairs
+  size_t o[CH_NSEC + 1];
+  o[0] = 0;
+  const size_t len[CH_NSEC] = {(size_t)n_leaves, (size_t)n_iso, (size_t)n, (size_t)n, (size_t)n + 1, (size_t)m,
+                               (size_t)n + 1, (size_t)nbo, (size_t)nbo, (size_t)n + 1, (size_t)nbo, (size_t)nbo,
+                               (size_t)nbo + 1, upd.size()};
+  for (int k = 0; k < CH_NSEC; ++k) {
+    o[k + 1] = o[k] + len[k];
+    if (k + 1 == CH_UPD) o[k + 1] += o[k + 1] & 1;  // int2 alignment of the update pairs
+  }
+  const size_t total = o[CH_NSEC] + 2;
+  int* hp = w.h_plan.reserve(total);
+  for (int i = 0; i < n_leaves; ++i) hp[o[CH_LEAVES] + i] = glob[leaves[i]];
+  {
+    int q = 0;
+    for (int v = 0; v < n; ++v)
+      if (loc[v] < 0) hp[o[CH_ISO] + q++] = v;
+  }
+  int* parent = hp + o[CH_PARENT];
+  int* nchild = hp + o[CH_NCHILD];
+  int* child_ptr = hp + o[CH_CHILDP];
+  int* child_idx = hp + o[CH_CHILDI];
+  for (int v = 0; v < n; ++v) {
+    const int l = loc[v];
+    parent[v] = (l >= 0 && par[l] >= 0) ? glob[par[l]] : -1;
+    nchild[v] = l >= 0 ? nch[l] : 0;
+  }
+  child_ptr[0] = 0;
+  for (int v = 0; v < n; ++v) child_ptr[v + 1] = child_ptr[v] + nchild[v];
+  {
+    std::vector<int> fill(child_ptr, child_ptr + n);
+    for (int v = 0; v < n; ++v)  // children in ascending node order (deterministic)
+      if (parent[v] >= 0) child_idx[fill[parent[v]]++] = v;
+  }
+  int* col_ptr = hp + o[CH_COLP];
+  int* row_ptr = hp + o[CH_ROWP];
   {
     // per global node column/row ranges (empty for isolated nodes)
     int c = 0, r = 0;
@@ -938,12 +1213,13 @@ static Analysis chol_analyze(Scene& s) {
       int l = loc[v];
       if (l >= 0) {
         for (int b = csp[l]; b < csp[l + 1]; ++b) {  // b == c + q: locals follow global order
-          hp[off_brow + b] = glob[csi[b]];
+          hp[o[CH_BROW] + b] = glob[csi[b]];
+          hp[o[CH_BCOL] + b] = v;
         }
         c += csp[l + 1] - csp[l];
         for (int e2 = rcnt[l]; e2 < rcnt[l + 1]; ++e2) {
-          hp[off_rowb + r] = r_b[e2] + n;
-          hp[off_rowc + r] = glob[r_k[e2]];
+          hp[o[CH_ROWB] + r] = r_b[e2] + n;
+          hp[o[CH_ROWC] + r] = glob[r_k[e2]];
           ++r;
         }
       }
@@ -952,23 +1228,26 @@ static Analysis chol_analyze(Scene& s) {
     row_ptr[n] = r;
   }
   an.ms_sub[5] = ms_since(t0);
-  std::copy(upd_ptr.begin(), upd_ptr.end(), hp + off_updp);
-  std::copy(upd.begin(), upd.end(), hp + off_upd);
+  std::copy(upd_ptr.begin(), upd_ptr.end(), hp + o[CH_UPDP]);
+  std::copy(upd.begin(), upd.end(), hp + o[CH_UPD]);
   w.ch_plan.resize(total);
   CK(cudaMemcpyAsync(w.ch_plan.p, hp, total * sizeof(int), cudaMemcpyHostToDevice, st));
   w.ch_L.resize(144 * std::max<int64_t>(an.n_blk, 1));
   w.ch_dinv.resize(12 * std::max<int64_t>(n, 1));
   w.ch_apos.resize(std::max<int64_t>(an.n_blk - n, 1));
-  const size_t offs[13] = {off_nodes, off_lvl,  off_ctal, off_ctan, off_colp, off_brow, off_bapos,
-                           off_rowp,  off_rowb, off_rowc, off_updp, off_upd,  total};
-  an.view = make_view(offs);
+  w.ch_dep.resize(std::max(n, 1));
+  w.ch_bleft.resize(std::max(n, 1));
+  w.ch_queue.resize(std::max(2 * m + nbo, 1));
+  w.ch_ctr.resize(4);
   cc.valid = true;
   cc.n = n;
   cc.n_off = n_off;
   cc.edges.swap(cur);
-  const int64_t st8[8] = {an.n_cta, an.n_coupled, an.n_blk, an.n_upd, an.n_edges, an.max_level, an.largest, 0};
+  const int64_t st8[8] = {an.n_cta, an.n_coupled, an.n_blk, an.n_upd, an.n_edges, an.max_level, an.largest,
+                          n_leaves};
   std::copy(st8, st8 + 8, cc.stats);
-  std::copy(offs, offs + 13, cc.offs);
+  std::copy(o, o + CH_NSEC + 1, cc.offs);
+  an.view = plan_view(s);
   an.ms_plan = ms_since(t0);
   static const bool trace_sub = getenv("ABD_TRACE_CHOL") != nullptr;
   if (trace_sub)
@@ -982,31 +1261,58 @@ static Analysis chol_analyze(Scene& s) {
 // split so the driver can fold the residual check into its own host sync:
 //   chol_begin  : analysis + factor/solve + residual + async copies (no sync)
 //   chol_finish : after a stream sync, pivot check, residual test, corrections
-static CholView plan_view(Scene& s) {
-  Scene::Work& w = s.w;
-  const size_t* o = w.ch_cache.offs;
-  const int* dp = w.ch_plan.p;
-  return CholView{s.H.n,
-                  dp + o[0],
-                  dp + o[1],
-                  dp + o[2],
-                  dp + o[3],
-                  dp + o[4],
-                  dp + o[5],
-                  s.H.row_ptr.p,
-                  s.H.col.p,
-                  w.ch_apos.p,
-                  dp + o[7],
-                  dp + o[8],
-                  dp + o[9],
-                  dp + o[10],
-                  reinterpret_cast<const int2*>(dp + o[11]),
-                  s.H.diag_pos.p,
-                  s.H.val.p,
-                  w.ch_L.p,
-                  w.ch_dinv.p,
-                  w.bad.p,
-                  nullptr};
+// one factor (+ both substitutions) or one pair of substitutions over the task FIFO;
+// returns the grid size
+static int launch_sched(Scene& s, const CholView& v, const double* b, double* x, bool factor) {
+  cudaStream_t st = s.stream;
+  static int bps = 0;
+  const size_t smem = CH_HW * sizeof(WarpSmem);
+  if (!bps) {
+    CK(cudaFuncSetAttribute(k_chol_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_chol_sched, CH_THREADS, smem));
+    bps = std::max(bps, 1);
+  }
+  const int init_n = std::max(v.n, v.n_tasks);
+  k_chol_sched_init<<<grid_for(std::max(init_n, 3), 256), 256, 0, st>>>(v);
+  note_launch("k_chol_sched_init");
+  // isolated nodes on a side stream beside the task graph (joined before returning)
+  if (v.n_iso > 0) {
+    CK(cudaEventRecord(s.ch_fork_ev, st));
+    CK(cudaStreamWaitEvent(s.side4, s.ch_fork_ev, 0));
+    const int ig = (int)std::min<int64_t>((int64_t)s.num_sms * 4, (v.n_iso + CH_HW - 1) / CH_HW);
+    k_chol_iso<<<ig, CH_THREADS, 0, s.side4>>>(v, b, x, factor ? 1 : 0);
+    note_launch("k_chol_iso");
+    CK(cudaEventRecord(s.ch_join_ev, s.side4));
+  }
+  // coupled task graph: about one warp per leaf (the widest front), at most what fits
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(std::min<int64_t>((int64_t)s.num_sms * bps, CH_MAX_GRID),
+                           ((int64_t)std::max(v.n_leaves, 1) + CH_HW - 1) / CH_HW));
+  static const char* trace_path = getenv("ABD_CHOL_TRACE_TASKS");  // tools: per-task timeline of factorizations
+  static DVec<unsigned long long> tbuf;
+  CholView vv = v;
+  if (trace_path && factor) {
+    tbuf.resize(4 * (int64_t)std::max(v.n_tasks, 1));
+    tbuf.zero(st);
+    vv.trace = tbuf.p;
+  }
+  if (v.n_coupled > 0) {
+    k_chol_sched<<<grid, CH_THREADS, smem, st>>>(vv, b, x, factor ? 1 : 0);
+    note_launch(factor ? "k_chol_sched(factor)" : "k_chol_sched(solve)");
+  }
+  if (trace_path && factor) {
+    std::vector<unsigned long long> h(4 * (int64_t)std::max(v.n_tasks, 1));
+    tbuf.download(h.data(), h.size(), st);
+    SSYNC(st);
+    if (FILE* f = fopen(trace_path, "ab")) {
+      const int hdr[4] = {v.n, v.n_coupled, v.n_tasks, grid};
+      fwrite(hdr, sizeof(int), 4, f);
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      fclose(f);
+    }
+  }
+  if (v.n_iso > 0) CK(cudaStreamWaitEvent(st, s.ch_join_ev, 0));
+  return grid;
 }
 
 static void launch_resid(Scene& s, const double* rhs, const double* x) {
@@ -1149,31 +1455,10 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
     kstat_flush(s, 0);
     CK(cudaEventRecord(ks.e0, st));
   }
-  static const bool clk_dbg = getenv("ABD_CHOL_CLOCK") != nullptr;
-  static DVec<long long> dbgbuf;
-  if (clk_dbg) {
-    dbgbuf.resize(8 * 256);
-    dbgbuf.zero(st);
-    v.dbg = dbgbuf.p;
-  }
   k_chol_apos<<<grid_for(n, 128), 128, 0, st>>>(v);
   note_launch("k_chol_apos");
-  k_chol_factor_solve<<<an.n_cta, CH_THREADS, 0, st>>>(v, rhs, x);
-  note_launch("k_chol_factor_solve");
+  run.n_cta = launch_sched(s, v, rhs, x, true);
   if (s.instrument) CK(cudaEventRecord(ks.e1, st));
-  if (clk_dbg) {
-    std::vector<long long> hb(8 * 256);
-    dbgbuf.download(hb.data(), hb.size(), st);
-    SSYNC(st);
-    long long t0c = hb[2];
-    fprintf(stderr, "[abd chol clock] node level start D_done chol_done fwd_done end n_off (cycles from first)\n");
-    for (int q = 0; q < 256; ++q) {
-      long long* o = &hb[8 * q];
-      if (o[2] == 0) continue;
-      fprintf(stderr, "  %6lld %3lld %8lld %6lld %6lld %6lld %6lld %lld\n", o[0], o[1], o[2] - t0c, o[3] - o[2],
-              o[4] - o[3], o[5] - o[4], o[6] - o[5], o[7]);
-    }
-  }
   w.r.resize(N);
   w.z.resize(N);
   w.part.resize(2 * RED_BLOCKS);
@@ -1202,8 +1487,7 @@ int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool&
     rel_res = bn > 0.0 ? rn / bn : 0.0;
     if (bn == 0.0 || rn <= rel_tol * bn || refine >= max_refine) break;
     CholView v = plan_view(s);
-    k_chol_solve<<<run.n_cta, CH_THREADS, 0, st>>>(v, w.r.p, w.z.p);
-    note_launch("k_chol_solve");
+    launch_sched(s, v, w.r.p, w.z.p, false);
     k_add_inplace<<<grid_for(N, 256), 256, 0, st>>>(N, run.x, w.z.p);
     note_launch("k_add_inplace");
     changed = true;

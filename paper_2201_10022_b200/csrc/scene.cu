@@ -51,6 +51,9 @@ Scene::Scene() {
   CK(cudaEventCreateWithFlags(&hot_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&pb_fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&pb_ev, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&side4, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ch_fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ch_join_ev, cudaEventDisableTiming));
   CK(cudaMallocHost(&h_pinned, 64 * sizeof(double)));
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
@@ -77,6 +80,9 @@ Scene::~Scene() {
   if (hot_ev) cudaEventDestroy(hot_ev);
   if (pb_fork_ev) cudaEventDestroy(pb_fork_ev);
   if (pb_ev) cudaEventDestroy(pb_ev);
+  if (side4) cudaStreamDestroy(side4);
+  if (ch_fork_ev) cudaEventDestroy(ch_fork_ev);
+  if (ch_join_ev) cudaEventDestroy(ch_join_ev);
   if (h_pinned) cudaFreeHost(h_pinned);
   for (cudaEvent_t e : {ev0, ev1, tev0, tev1})
     if (e) cudaEventDestroy(e);

@@ -177,6 +177,8 @@ struct Scene {
   cudaEvent_t hot_fork_ev = nullptr, hot_ev = nullptr;
   cudaEvent_t pb_fork_ev = nullptr, pb_ev = nullptr;  // VF pair blocks on side2
   cudaStream_t side3 = nullptr;  // mollified EE pair blocks beside the plain EE pairs
+  cudaStream_t side4 = nullptr;  // Cholesky: isolated nodes beside the coupled task graph
+  cudaEvent_t ch_fork_ev = nullptr, ch_join_ev = nullptr;
   cudaEvent_t moll_fork_ev = nullptr, moll_ev = nullptr;
   int num_sms = 148;
 
@@ -285,7 +287,8 @@ struct Scene {
     DVec<long long> cl_slot_off, cl_minv;
     DVec<double> minv;
     // sparse block Cholesky plan (one packed int buffer) and factor (k_chol.cu)
-    DVec<int> ch_flags, ch_plan, ch_apos;
+    DVec<int> ch_flags, ch_plan, ch_apos, ch_dep, ch_bleft, ch_queue;
+    DVec<unsigned> ch_ctr;
     DVec<double> ch_L, ch_dinv;
     HostPinned<int> h_plan, h_meta;
     // last analysed pattern (nonzero flags + keys) and its plan: Newton iterations
@@ -296,7 +299,7 @@ struct Scene {
       int64_t n_off = 0;
       std::vector<uint64_t> edges;  // (i << 32 | j) nonzero couplings the plan was built for
       int64_t stats[8] = {};
-      size_t offs[13] = {};
+      size_t offs[16] = {};
       int64_t hits = 0, misses = 0;
     } ch_cache;
     std::vector<uint64_t> ch_edges_cur;
