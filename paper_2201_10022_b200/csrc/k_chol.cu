@@ -82,7 +82,7 @@ struct CholView {
   int* dep;             // n: remaining children (reset per launch)
   int* bleft;           // n: remaining off-diagonal block tasks of each column
   int* queue;           // n_tasks slots: j (diagonal), n + j (backward), 2n + b (block); -1 = not yet pushed
-  unsigned* ctr;        // [0] pop head, [1] push tail, [2] isolated-node head
+  unsigned* ctr;        // [0] pop head, [1] push tail, [2] unused, [3] tasks done
   unsigned long long* trace;  // optional (ABD_CHOL_TRACE_TASKS): per popped slot (item, t_pop, t_start, t_end)
 };
 
@@ -526,7 +526,7 @@ __global__ void k_chol_sched_init(CholView v) {
     v.bleft[i] = v.col_ptr[i + 1] - v.col_ptr[i];
   }
   if (i < v.n_tasks) v.queue[i] = i < v.n_leaves ? v.leaves[i] : -1;
-  if (i < 3) v.ctr[i] = i == 1 ? (unsigned)v.n_leaves : 0u;
+  if (i < 4) v.ctr[i] = i == 1 ? (unsigned)v.n_leaves : 0u;
 }
 
 // Isolated nodes (no coupling): one independent factor + solve per warp.
@@ -543,21 +543,32 @@ __device__ __forceinline__ void push_task(const CholView& v, int item) {
   st_release(v.queue + slot, item);
 }
 
-// node j is complete (its column of L and y_j): release its parent, or start the
-// backward sweep at a root.  Lane 0 only, after the warp's writes are fenced.
-__device__ __forceinline__ void node_done(const CholView& v, int j) {
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// node j is complete (its column of L and y_j): the task that becomes ready -- the
+// backward task at a root, or the parent's diagonal task once its last child is
+// done -- or -1.  Lane 0 only, after the warp's writes are fenced.
+__device__ __forceinline__ int node_ready(const CholView& v, int j) {
   const int p = v.parent[j];
-  if (p < 0) push_task(v, v.n + j);
-  else if (atom_dec_acq_rel(v.dep + p) == 1) push_task(v, p);
+  if (p < 0) return v.n + j;
+  return atom_dec_acq_rel(v.dep + p) == 1 ? p : -1;
 }
 
 // Persistent factor (+ forward / backward substitution) over the task FIFO of the
 // coupled nodes.  Tasks: j < n -> diagonal task of node j; n + j -> backward task
-// of node j; 2n + b -> off-diagonal block task b (factor only).  A warp that pops
-// a slot not yet pushed polls it with backoff: every unpushed slot is produced by
-// a warp that is running a task, so the grid cannot deadlock, whatever the
-// residency.  The grid is sized to the task graph's width, not the GPU: idle
-// pollers would only load L2.
+// of node j; 2n + b -> off-diagonal block task b (factor only).  A warp that makes
+// a task ready runs one of them itself next (continuation: chains of the
+// elimination tree never go through the FIFO) and pushes the others.  A warp that
+// pops a slot not yet pushed polls it with backoff until it is filled or every
+// task is done; every unpushed slot is produced by a warp that is running a task,
+// so the grid cannot deadlock, whatever the residency.  The grid is sized to the
+// task graph's width, not the GPU: idle pollers would only load L2.
 __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const double* __restrict__ b, double* x,
                                                            int factor) {
   extern __shared__ __align__(16) unsigned char ch_smem[];
@@ -566,82 +577,94 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
   const unsigned mask = 0xffffffffu;
   const bool fac = factor != 0;
   const int total = fac ? v.n_tasks : 2 * v.n_coupled;
+  constexpr int EXIT = -2;
+  int next = -1;  // continuation task (warp-uniform)
   for (;;) {
-    int idx = 0;
-    if (t == 0) idx = (int)atomicAdd(v.ctr, 1u);
-    idx = __shfl_sync(mask, idx, 0);
-    if (idx >= total) break;
-    const unsigned long long t_pop = v.trace ? gtimer() : 0;
-    int item = -1;
-    if (t == 0) {
-      unsigned ns = 32;
-      while ((item = ld_acquire(v.queue + idx)) < 0) {
-        __nanosleep(ns);
-        ns = min(2u * ns, 1024u);
+    int item;
+    unsigned long long t_pop = 0;
+    if (next >= 0) {
+      item = next;
+      next = -1;
+      fence_acq_rel();  // lane 0 acquired the dependency; order every lane's reads after it
+    } else {
+      int idx = 0;
+      if (t == 0) idx = (int)atomicAdd(v.ctr, 1u);
+      idx = __shfl_sync(mask, idx, 0);
+      if (idx >= total) break;
+      if (v.trace) t_pop = gtimer();
+      item = -1;
+      if (t == 0) {
+        unsigned ns = 32;
+        while ((item = ld_relaxed(v.queue + idx)) < 0) {
+          if (ld_relaxed(reinterpret_cast<const int*>(v.ctr + 3)) >= total) {
+            item = EXIT;
+            break;
+          }
+          __nanosleep(ns);
+          ns = min(2u * ns, 256u);
+        }
       }
+      item = __shfl_sync(mask, item, 0);
+      if (item == EXIT) break;
+      item = ld_acquire(v.queue + idx);  // every lane acquires the producer's writes
     }
-    item = __shfl_sync(mask, item, 0);
-    __syncwarp(mask);
-    __threadfence();
     const unsigned long long t_start = v.trace ? gtimer() : 0;
+    int info = 0;
     if (item < v.n) {  // diagonal task
       const int j = item;
       chol_diag(v, j, b, x, fac, sm);
-      __threadfence();
+      fence_acq_rel();
       __syncwarp(mask);
-      if (v.trace && t == 0) {
-        unsigned long long* o = v.trace + 4 * (int64_t)idx;
-        o[0] = (unsigned long long)item | ((unsigned long long)(unsigned)(v.row_ptr[j + 1] - v.row_ptr[j]) << 32);
-        o[1] = t_pop;
-        o[2] = t_start;
-        o[3] = gtimer();
-      }
-      const int c0 = v.col_ptr[j], c1 = v.col_ptr[j + 1];
       if (t == 0) {
-        if (fac && c1 > c0) {
-          const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0));
-          for (int c = c0; c < c1; ++c) st_release(v.queue + slot + (c - c0), 2 * v.n + c);
+        info = v.row_ptr[j + 1] - v.row_ptr[j];
+        const int c0 = v.col_ptr[j], c1 = v.col_ptr[j + 1];
+        if (fac && c1 > c0) {  // run the first block here, the others in parallel
+          if (c1 - c0 > 1) {
+            const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0 - 1));
+            for (int c = c0 + 1; c < c1; ++c) st_release(v.queue + slot + (c - c0 - 1), 2 * v.n + c);
+          }
+          next = 2 * v.n + c0;
         } else {
-          node_done(v, j);
+          next = node_ready(v, j);
         }
       }
     } else if (item < 2 * v.n) {  // backward task
       const int j = item - v.n;
       chol_backward(v, j, x);
-      __threadfence();
+      fence_acq_rel();
       __syncwarp(mask);
-      if (v.trace && t == 0) {
-        unsigned long long* o = v.trace + 4 * (int64_t)idx;
-        o[0] = (unsigned long long)item;
-        o[1] = t_pop;
-        o[2] = t_start;
-        o[3] = gtimer();
-      }
-      const int c0 = v.child_ptr[j], c1 = v.child_ptr[j + 1];
-      if (t == 0 && c1 > c0) {
-        const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0));
-        for (int c = c0; c < c1; ++c) st_release(v.queue + slot + (c - c0), v.n + v.child_idx[c]);
+      if (t == 0) {
+        const int c0 = v.child_ptr[j], c1 = v.child_ptr[j + 1];
+        if (c1 - c0 > 1) {
+          const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0 - 1));
+          for (int c = c0 + 1; c < c1; ++c) st_release(v.queue + slot + (c - c0 - 1), v.n + v.child_idx[c]);
+        }
+        if (c1 > c0) next = v.n + v.child_idx[c0];
       }
     } else {  // off-diagonal block task
       const int bb = item - 2 * v.n;
       chol_block(v, bb, sm);
-      __threadfence();
+      fence_acq_rel();
       __syncwarp(mask);
-      if (v.trace && t == 0) {
-        unsigned long long* o = v.trace + 4 * (int64_t)idx;
-        o[0] = (unsigned long long)item | ((unsigned long long)(unsigned)(v.upd_ptr[bb + 1] - v.upd_ptr[bb]) << 32);
-        o[1] = t_pop;
+      if (t == 0) {
+        info = v.upd_ptr[bb + 1] - v.upd_ptr[bb];
+        const int j = v.blk_col[bb];
+        if (atom_dec_acq_rel(v.bleft + j) == 1) next = node_ready(v, j);
+      }
+    }
+    if (t == 0) {
+      const unsigned done = atomicAdd(v.ctr + 3, 1u);
+      if (v.trace) {
+        unsigned long long* o = v.trace + 4 * (int64_t)done;
+        o[0] = (unsigned long long)(unsigned)item | ((unsigned long long)(unsigned)info << 32);
+        o[1] = t_pop ? t_pop : t_start;
         o[2] = t_start;
         o[3] = gtimer();
       }
-      if (t == 0) {
-        const int j = v.blk_col[bb];
-        if (atom_dec_acq_rel(v.bleft + j) == 1) node_done(v, j);
-      }
     }
+    next = __shfl_sync(mask, next, 0);
   }
 }
-
 
 // nonzero flags of the upper off-diagonal pattern blocks
 __global__ void k_block_nz(int64_t n_off, const int* __restrict__ upper_pos, const double* __restrict__ val,
@@ -1074,23 +1097,38 @@ static Analysis chol_analyze(Scene& s) {
       rfill[i]++;
     }
   an.ms_sub[1] = ms_since(t0);
-  // update pairs for off block (i, j): k in rows(j) with i in cs[k]
+  // update pairs for off block (i, j): k in rows(j) with i in cs[k], in elimination
+  // order of k.  Every pair (j, i) of cs[k] (j before i) is one such update, so the
+  // lists are built by walking each column's pairs once: O(#updates x |cs[j]|).
   upd_ptr.assign(nbo + 1, 0);
-  upd.clear();
-  for (int j = 0; j < m; ++j)
-    for (int b = csp[j]; b < csp[j + 1]; ++b) {
-      const int i = csi[b];
-      for (int e = rcnt[j]; e < rcnt[j + 1]; ++e) {
-        const int k = r_k[e];
-        for (int f = csp[k]; f < csp[k + 1]; ++f)
-          if (csi[f] == i) {
-            upd.push_back(n + f);
-            upd.push_back(n + r_b[e]);
-            break;
-          }
+  std::vector<int>& ub = w.hs_i[29];
+  ub.clear();
+  auto find_blk = [&](int j, int i) {
+    for (int f = csp[j]; f < csp[j + 1]; ++f)
+      if (csi[f] == i) return f;
+    return -1;
+  };
+  for (int k : order)
+    for (int a2 = csp[k]; a2 < csp[k + 1]; ++a2)
+      for (int b2 = a2 + 1; b2 < csp[k + 1]; ++b2) {
+        const int blk = find_blk(csi[a2], csi[b2]);
+        ub.push_back(blk);
+        upd_ptr[blk + 1]++;
       }
-      upd_ptr[b + 1] = (int)(upd.size() / 2);
-    }
+  for (int b = 0; b < nbo; ++b) upd_ptr[b + 1] += upd_ptr[b];
+  upd.resize(2 * (size_t)upd_ptr[nbo]);
+  {
+    std::vector<int>& fill = w.hs_i[30];
+    fill.assign(upd_ptr.begin(), upd_ptr.end() - 1);
+    size_t q = 0;
+    for (int k : order)
+      for (int a2 = csp[k]; a2 < csp[k + 1]; ++a2)
+        for (int b2 = a2 + 1; b2 < csp[k + 1]; ++b2) {
+          const int at = fill[ub[q++]]++;
+          upd[2 * (size_t)at] = n + b2;      // L_ik
+          upd[2 * (size_t)at + 1] = n + a2;  // L_jk
+        }
+  }
   an.n_upd = (int64_t)upd.size() / 2;
   an.ms_sub[2] = ms_since(t0);
   // elimination-tree levels and component roots (local)
@@ -1273,7 +1311,7 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     bps = std::max(bps, 1);
   }
   const int init_n = std::max(v.n, v.n_tasks);
-  k_chol_sched_init<<<grid_for(std::max(init_n, 3), 256), 256, 0, st>>>(v);
+  k_chol_sched_init<<<grid_for(std::max(init_n, 4), 256), 256, 0, st>>>(v);
   note_launch("k_chol_sched_init");
   // isolated nodes on a side stream beside the task graph (joined before returning)
   if (v.n_iso > 0) {

@@ -1,7 +1,7 @@
 """GPU timeline of pile Newton steps through CUPTI (torch.profiler): kernel/memcpy
 spans on the device, idle gaps between them and what precedes each gap.
 
-    python tools/gpu_timeline.py [STEPS] [pile|boxstack|cubes|chainmail] > gpurun_out/timeline.txt
+    python tools/gpu_timeline.py [STEPS] [pile|boxstack|cubes|chainmail] [CKPT] > gpurun_out/timeline.txt
 """
 import collections
 import ctypes as C
@@ -25,8 +25,8 @@ spec = {"pile": scenes.icosphere_pile, "boxstack": scenes.box_stack, "cubes": sc
         "chainmail": scenes.chainmail}[WL](seed=0)
 model, state, params = spec.build()
 if WL == "pile":
-    ck = np.load(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_data",
-                              "pile_step150.npz"))
+    ck = np.load(sys.argv[3] if len(sys.argv) > 3 else os.path.join(
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_data", "pile_step150.npz"))
     q, qd = ck["q"].copy(), ck["q_dot"].copy()
 else:
     q, qd = state.q.copy(), state.q_dot.copy()
