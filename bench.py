@@ -66,9 +66,9 @@ def src_hash():
     return h.hexdigest()[:16]
 
 
-def measured_traffic(workload, kernel):
-    """ncu DRAM bytes per launch of `kernel` on `workload`, if captured on THIS source tree
-    (tools/measure_traffic.py writes profiles/traffic_<workload>.json with the src hash)."""
+def measured_capture(workload):
+    """ncu capture of this workload's kernels on THIS source tree (tools/measure_traffic.py
+    writes profiles/traffic_<workload>.json with the src hash), or (None, why)."""
     path = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     try:
         d = json.load(open(path))
@@ -76,8 +76,41 @@ def measured_traffic(workload, kernel):
         return None, "no capture"
     if d.get("src_hash") != src_hash():
         return None, f"capture {os.path.relpath(path, ROOT)} is for another source tree"
+    return d, os.path.relpath(path, ROOT)
+
+
+def measured_traffic(workload, kernel):
+    """ncu DRAM bytes per launch of `kernel` on `workload`, if captured on this source tree."""
+    d, src = measured_capture(workload)
+    if d is None:
+        return None, src
     k = d.get("kernels", {}).get(kernel)
-    return (k.get("dram_bytes_per_launch") if k else None), os.path.relpath(path, ROOT)
+    return (k.get("dram_bytes_per_launch") if k else None), src
+
+
+def fp64_table(workload, kst):
+    """Executed FP64 flops per launch (ncu: 2 DFMA + DADD + DMUL + 512 per DMMA m8n8k4) over the
+    live per-launch time (bench CUDA events) for the instrumented kernels, over the ncu
+    duration otherwise, against the DFMA peak measured by tools/ubench/dfma.cu."""
+    d, src = measured_capture(workload)
+    if d is None:
+        return {"source": src}
+    try:
+        peak = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    except Exception:
+        peak = None
+    out = {"source": src, "peak_tflops": (peak or {}).get("dfma_tflops"),
+           "peak_source": "profiles/fp64_peak.json (tools/ubench/dfma.cu DFMA probe)" if peak else None}
+    for g, k in d.get("kernels", {}).items():
+        f = k.get("fp64") or {}
+        flops = f.get("flops_per_launch")
+        live = kst.get(g)
+        ms = live["ms"] / live["launches"] if live and live.get("launches") else f.get("ms_per_launch")
+        tf = flops / (ms * 1e-3) / 1e12 if (flops is not None and ms) else None
+        out[g] = {"flops_per_launch": flops, "ms_per_launch": ms, "achieved_tflops": tf,
+                  "frac": tf / out["peak_tflops"] if (tf is not None and out["peak_tflops"]) else None,
+                  "time": "live" if live else "ncu (cold)"}
+    return out
 
 
 class ClockSampler:
@@ -605,7 +638,8 @@ def run_scene(args):
                 "share_of_step": pc["share_of_step"],
                 "kernels": {k: {kk: vv for kk, vv in v.items() if kk not in ("desc", "bytes_model")}
                             for k, v in kst.items()},
-                "measured_over": f"all {n_win} steps of the window"}
+                "measured_over": f"all {n_win} steps of the window",
+                "fp64": fp64_table(args.workload, kst)}
 
     # e2e: the same window through the public Python API with host numpy state
     e2e = None

@@ -216,6 +216,16 @@ int abd_scene_set_comm_nccl(abd_scene* s, const uint8_t* id128, int rank, int wo
 int abd_scene_set_comm_callback(abd_scene* s, int rank, int world, abd_allreduce_fn fn, void* user);
 
 int abd_set_state(abd_scene* s, const double* q, const double* q_dot);
+/* World positions of every vertex (bodies concatenated, V x 3) at host q (n_bodies x 12), or at the
+ * resident state when q is NULL: x = rest @ A^T + p with the reference's rounding
+ * (contact.py:149-153 world_positions_all; scene.py:341-349 world_vertices for frames). */
+int abd_world_vertices(abd_scene* s, const double* q, double* out);
+/* Joint reduction q_dyn = T u + q_const (constraints.py:206-402, SystemModel.reduction,
+ * solver.py:114): T row-major (12 n_dyn x n_unknowns), copied to the device; n_unknowns = 0
+ * removes it.  With a reduction, abd_advance_step solves the Newton system through
+ * T^T H T (solver.py:479-490, dense on the device) and falls back to T T^T (-g) on a
+ * non-descent direction (solver.py:557-561).  Single-rank scenes only. */
+int abd_set_reduction(abd_scene* s, int64_t n_unknowns, const double* T);
 int abd_get_state(abd_scene* s, double* q, double* q_dot);
 /* forces (n_bodies,12) host; NULL = reuse the last uploaded forces. energy_trace may be NULL
  * (else >= max_newton_iters*friction_outer_iters doubles). */

@@ -26,6 +26,17 @@ from .body import (
     world_positions,
 )
 from .ccd import CcdQuery, accd_toi, accd_toi_batch, step_filter
+from .constraints import (
+    Reduction,
+    ReparamMap,
+    VirtualTet,
+    build_constrained_system,
+    constrain_linear,
+    make_axis_tet,
+    make_free_tet,
+    phi,
+    reparam_map,
+)
 from .contact import (
     BarrierDomainError,
     CandidateSet,
@@ -59,7 +70,8 @@ from .distance import (
 )
 from .intersect import intersecting_body_pairs, triangles_intersect, triangles_intersect_batch
 from .mesh import SurfaceMesh, build_edges
-from .shapes import box_mesh, icosphere_mesh, torus_mesh
+from .scene import FrameStats, SceneConfig, SceneState, audit_intersections, load_scene, read_obj, run, write_obj_frame
+from .shapes import box_mesh, icosphere_mesh, prism_mesh, torus_mesh, wedge_mesh
 from .solver import (
     IncrementalPotentialState,
     SimState,

@@ -98,6 +98,8 @@ _SIGS = {
     "abd_timer_stop": (i32, [vp, C.POINTER(dbl)]),
     "abd_set_state": (i32, [vp, vp, vp]),
     "abd_get_state": (i32, [vp, vp, vp]),
+    "abd_set_reduction": (i32, [vp, i64, vp]),
+    "abd_world_vertices": (i32, [vp, dp, dp]),
     "abd_advance_step": (i32, [vp, vp, C.POINTER(StepParamsC), C.POINTER(StepStatsC), vp]),
 }
 

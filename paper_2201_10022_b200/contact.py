@@ -68,8 +68,13 @@ class CollisionBody:
 
 
 def world_positions_all(bodies, q_all) -> list:
-    q_all = np.asarray(q_all, dtype=float).reshape(len(bodies), 12)
-    return [b.rest @ q[3:].reshape(3, 3).T + q[:3] for b, q in zip(bodies, q_all)]
+    """Per-body world vertices rest @ A^T + p (contact.py:149-153) on the GPU
+    (abd_world_vertices, the reference's rounding)."""
+    sc = _native.scene_for(bodies)
+    X = np.empty((sum(len(b.rest) for b in bodies), 3))
+    _native.check(_native.lib().abd_world_vertices(sc.ptr, sc.q(q_all), X))
+    off = np.cumsum([0] + [len(b.rest) for b in bodies])
+    return [X[off[k]:off[k + 1]] for k in range(len(bodies))]
 
 
 @dataclass(frozen=True)

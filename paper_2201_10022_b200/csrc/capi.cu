@@ -679,6 +679,18 @@ int abd_intersecting_pairs(abd_scene* h, const double* q, int64_t cap, int64_t* 
   });
 }
 
+int abd_world_vertices(abd_scene* h, const double* q, double* out) {
+  return guard([&] {
+    SC(h);
+    const double* qd = q ? up_q(s, s.q_trial, q) : s.q.p;
+    DVec<double>& X = s.w.basis;  // scratch
+    X.resize(3 * std::max<int64_t>(s.V, 1));
+    world_vertices(s, qd, X.p);
+    if (s.V) X.download(out, 3 * (size_t)s.V, s.stream);
+    sync(s.stream);
+  });
+}
+
 static std::vector<int64_t> canonical_record_order(Scene& s, int64_t total);
 
 int abd_resident_generation(abd_scene* h, int64_t* cand_gen, int64_t* fric_gen) {
@@ -1013,6 +1025,14 @@ int abd_get_state(abd_scene* h, double* q, double* q_dot) {
     if (q) s.q.download(q, 12 * (size_t)s.B, s.stream);
     if (q_dot) s.q_dot.download(q_dot, 12 * (size_t)s.B, s.stream);
     sync(s.stream);
+  });
+}
+
+int abd_set_reduction(abd_scene* h, int64_t n_unknowns, const double* T) {
+  return guard([&] {
+    SC(h);
+    if (n_unknowns > 0 && !T) throw Error(ABD_ERR_ARG, "null reduction matrix");
+    set_reduction(s, n_unknowns, T);
   });
 }
 

@@ -394,7 +394,8 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   static const bool no_early = getenv("ABD_CHOL_NO_EARLY") != nullptr;
   const bool keeps_pattern = w.pat_valid && s.cands.ov_matches_pattern && s.H.n == s.n_dyn &&
                              w.pat_fric_gen == s.fric.gen && w.pat_n_f == s.fric.n;
-  if (!no_early && P.linear_solver != 1 && s.n_dyn > 0 && s.comm.world == 1 && keeps_pattern && r.e < r.e0)
+  if (!no_early && P.linear_solver != 1 && s.red_nu == 0 && s.n_dyn > 0 && s.comm.world == 1 && keeps_pattern &&
+      r.e < r.e0)
     mark_structure_early(s, s.q_trial.p, P.d_hat);
   return r;
 }
@@ -569,7 +570,7 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   const int2* fp = fric_pattern(s, nfp);
   build_pattern(s, s.cands.ov.p, s.cands.n_ov, fp, nfp, /*from_cands=*/true);
   HMARK();
-  contact_blocks(s, q, kappa, dh, 1, /*mark=*/true);
+  contact_blocks(s, q, kappa, dh, 1, /*mark=*/s.red_nu == 0);
   HMARK();
   append_friction_blocks(s, q, dt, eps_v, 1);
   if (body_forked) CK(cudaStreamWaitEvent(s.stream, s.join_ev, 0));
@@ -639,8 +640,10 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       if (ND) {
         k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
         note_launch("k_neg");
-        const bool chol = P.linear_solver != 1;
-        if (chol) chol_begin(s, s.w.neg.p, s.dx.p);
+        const bool reduced = s.red_nu > 0;  // joints: dense T^T H T (k_reduced.cu)
+        const bool chol = !reduced && P.linear_solver != 1;
+        if (reduced) reduced_solve(s, s.w.neg.p, s.dx.p);
+        else if (chol) chol_begin(s, s.w.neg.p, s.dx.p);
         else pcg_it = pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
         HMARK();
         // |dx|_inf and g.dx in one pass; the Cholesky residual check shares the host sync
@@ -674,8 +677,12 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       const double* dsrc = s.dx.p;
       if (gd >= 0.0) {
         st.nondescent_fallbacks += 1;
-        dsrc = s.grad.p;
-        sign = -1.0;
+        if (s.red_nu > 0) {  // T (T^T (-g)) (solver.py:560-561)
+          reduced_project(s, s.w.neg.p, s.dx.p);
+        } else {
+          dsrc = s.grad.p;
+          sign = -1.0;
+        }
       }
       k_expand_dq<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.slot.p, dsrc, sign, s.dq.p);
       note_launch("k_expand_dq");

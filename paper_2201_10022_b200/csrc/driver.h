@@ -22,6 +22,10 @@ void chol_analysis_drop(Scene& s);
 int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed);
 void spmv(Scene& s, const double* x, double* y);
 void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off);
+// k_reduced.cu: joint-reduced Newton direction (solver.py:479-490)
+void set_reduction(Scene& s, int64_t nu, const double* T_host);
+void reduced_solve(Scene& s, const double* neg_g, double* dx);
+void reduced_project(Scene& s, const double* v, double* out);
 // comm.cu
 void comm_get_nccl_id(void* out128);
 void comm_init_nccl(Scene& s, const void* id128, int rank, int world);
@@ -35,6 +39,7 @@ double global_min_distance(Scene& s, const double* q, int skip_static = 1);
 double global_min_distance_stats(Scene& s, const double* q);
 // body pairs (i < j) whose closed surfaces intersect or contain one another (k_audit.cu)
 std::vector<int2> intersecting_body_pairs(Scene& s, const double* q);
+void world_vertices(Scene& s, const double* q, double* out);
 // driver.cu
 int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark = false);
 void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, int project);

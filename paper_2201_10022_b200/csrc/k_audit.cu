@@ -91,6 +91,13 @@ __global__ void k_world_vertices(int64_t V, const int* __restrict__ vert_body, c
   out[3 * v + 2] = x.z;
 }
 
+// world vertices of every body at q (device) into out (device, V x 3)
+void world_vertices(Scene& s, const double* q, double* out) {
+  if (!s.V) return;
+  k_world_vertices<<<grid_for(s.V, 256), 256, 0, s.stream>>>(s.V, s.vert_body.p, s.rest.p, q, out);
+  note_launch("k_world_vertices");
+}
+
 // all body pairs i < j whose vertex boxes overlap (closed), scene.py:660-668; the
 // audit is not on the stepping path, so the O(B^2) box loop of the reference is
 // kept (one thread per row i, pairs appended in any order, sorted on the host)

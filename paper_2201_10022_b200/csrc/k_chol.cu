@@ -775,14 +775,73 @@ struct Analysis {
   int64_t n_blk = 0, n_upd = 0, n_edges = 0;
   int max_level = 0, largest = 0;
   double ms_sync = 0, ms_order = 0, ms_plan = 0, ms_sub[6] = {};
-  bool cached = false;
+  bool cached = false, order_reused = false;
   CholView view{};
 };
 
 // minimum-degree elimination on a (local) graph; colstruct[v] = neighbours
 // still alive when v is eliminated (its L column structure), order = elimination order.
+void min_degree_lists(int m, std::vector<std::vector<int>>& adj, std::vector<int>& order,
+                      std::vector<std::vector<int>>& colstruct);
+
+// Same elimination (repeatedly the live node of smallest (degree, id); its live
+// neighbours become a clique) on adjacency bitsets: a neighbour update is W word
+// ORs instead of a sorted-list merge.  Identical order and column structures to
+// min_degree_lists; used while the core fits in a few hundred words per row.
 void min_degree(int m, std::vector<std::vector<int>>& adj, std::vector<int>& order,
                 std::vector<std::vector<int>>& colstruct) {
+  const int W = (m + 63) / 64;
+  if (m > 8192) {
+    min_degree_lists(m, adj, order, colstruct);
+    return;
+  }
+  order.clear();
+  order.reserve(m);
+  colstruct.assign(m, {});
+  std::vector<uint64_t> bits((size_t)m * W, 0ull), nb(W);
+  std::vector<int> deg(m);
+  for (int v = 0; v < m; ++v) {
+    uint64_t* r = bits.data() + (size_t)v * W;
+    for (int a : adj[v]) r[a >> 6] |= 1ull << (a & 63);
+    deg[v] = (int)adj[v].size();
+  }
+  std::vector<char> done(m, 0);
+  typedef std::pair<int, int> DI;
+  std::vector<DI> hv;
+  hv.reserve(2 * m);
+  for (int v = 0; v < m; ++v) hv.push_back({deg[v], v});
+  std::priority_queue<DI, std::vector<DI>, std::greater<DI>> heap(std::greater<DI>(), std::move(hv));
+  std::vector<int> list;
+  while (!heap.empty()) {
+    DI top = heap.top();
+    heap.pop();
+    const int v = top.second;
+    if (done[v] || top.first != deg[v]) continue;
+    done[v] = 1;
+    order.push_back(v);
+    const uint64_t* rv = bits.data() + (size_t)v * W;
+    std::copy(rv, rv + W, nb.begin());
+    list.clear();
+    for (int w = 0; w < W; ++w)
+      for (uint64_t x = nb[w]; x; x &= x - 1) list.push_back(64 * w + __builtin_ctzll(x));
+    colstruct[v] = list;  // ascending ids, as the sorted lists
+    for (int a : list) {
+      uint64_t* ra = bits.data() + (size_t)a * W;
+      int d = 0;
+      for (int w = 0; w < W; ++w) {
+        ra[w] |= nb[w];
+        if (w == (a >> 6)) ra[w] &= ~(1ull << (a & 63));
+        if (w == (v >> 6)) ra[w] &= ~(1ull << (v & 63));
+        d += __builtin_popcountll(ra[w]);
+      }
+      deg[a] = d;
+      heap.push({d, a});
+    }
+  }
+}
+
+void min_degree_lists(int m, std::vector<std::vector<int>>& adj, std::vector<int>& order,
+                      std::vector<std::vector<int>>& colstruct) {
   order.clear();
   order.reserve(m);
   colstruct.assign(m, {});
@@ -812,6 +871,74 @@ void min_degree(int m, std::vector<std::vector<int>>& adj, std::vector<int>& ord
       heap.push({(int)out.size(), a});
     }
   }
+}
+
+constexpr double ORDER_REUSE_FILL = 1.05;  // factor blocks and update pairs, over the fresh order's
+
+// Symbolic factorization of the local graph (adjacency adj_ptr / adj_idx, full
+// degrees deg) under the cached global elimination order `gorder`, preceded by the
+// nodes not in it (ascending local id).  Column structure of v = its later
+// neighbours plus its elimination-tree children's structures minus v, sorted by
+// position.  Fills order / pos / csp / csi as the fresh ordering does; false when the
+// factor would exceed max_nnz off-diagonal blocks or max_upd update pairs.
+bool symbolic_fixed_order(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj_idx,
+                          const std::vector<int>& deg, const std::vector<int>& loc, const std::vector<int>& gorder,
+                          int64_t max_nnz, int64_t max_upd, std::vector<int>* scratch, std::vector<int>& order,
+                          std::vector<int>& pos, std::vector<int>& csp, std::vector<int>& csi) {
+  int64_t upd = 0;
+  std::vector<int>&seen = scratch[0], &mark = scratch[1], &head = scratch[2], &nxt = scratch[3], &st0 = scratch[4],
+                  &len = scratch[5], &flat = scratch[6], &L = scratch[7];
+  seen.assign(m, 0);
+  order.clear();
+  for (int g : gorder)
+    if (loc[g] >= 0) seen[loc[g]] = 1;
+  for (int v = 0; v < m; ++v)
+    if (!seen[v]) order.push_back(v);
+  for (int g : gorder)
+    if (loc[g] >= 0) order.push_back(loc[g]);
+  if ((int)order.size() != m) return false;
+  pos.resize(m);
+  for (int i = 0; i < m; ++i) pos[order[i]] = i;
+  mark.assign(m, -1);
+  head.assign(m, -1);
+  nxt.assign(m, -1);
+  st0.assign(m, 0);
+  len.assign(m, 0);
+  flat.clear();
+  for (int i = 0; i < m; ++i) {
+    const int v = order[i];
+    L.clear();
+    for (int e = adj_ptr[v]; e < adj_ptr[v] + deg[v]; ++e) {
+      const int u = adj_idx[e];
+      if (pos[u] > i && mark[u] != v) {
+        mark[u] = v;
+        L.push_back(u);
+      }
+    }
+    for (int c = head[v]; c >= 0; c = nxt[c])
+      for (int k = st0[c]; k < st0[c] + len[c]; ++k) {
+        const int u = flat[k];
+        if (u != v && mark[u] != v) {
+          mark[u] = v;
+          L.push_back(u);
+        }
+      }
+    std::sort(L.begin(), L.end(), [&](int a, int b) { return pos[a] < pos[b]; });
+    st0[v] = (int)flat.size();
+    len[v] = (int)L.size();
+    flat.insert(flat.end(), L.begin(), L.end());
+    upd += (int64_t)L.size() * ((int64_t)L.size() - 1) / 2;  // update pairs of this column
+    if ((int64_t)flat.size() > max_nnz || upd > max_upd) return false;
+    if (!L.empty()) {
+      nxt[v] = head[L[0]];
+      head[L[0]] = v;
+    }
+  }
+  csp.assign(m + 1, 0);
+  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + len[v];
+  csi.resize(csp[m]);
+  for (int v = 0; v < m; ++v) std::copy(flat.begin() + st0[v], flat.begin() + st0[v] + len[v], csi.begin() + csp[v]);
+  return true;
 }
 
 double ms_since(std::chrono::steady_clock::time_point t) {
@@ -926,151 +1053,173 @@ static Analysis chol_analyze(Scene& s) {
     adj_idx[adj_ptr[b2] + deg[b2]++] = a2;
   }
   const double ms_adj = ms_since(t0);
-  // Elimination order by tree contraction (contact graphs of piles are forests of
-  // stacked chains): rounds of rake (every node of degree <= 1 at the start of the
-  // round; no fill) and compress (an independent set of degree-2 nodes; the fill
-  // edge joins the two neighbours), so a chain of L bodies is eliminated in
-  // O(log L) elimination-tree levels instead of L / 2.  What remains (degree >= 3
-  // everywhere) is ordered by minimum degree.  cs0/cs1 = the live neighbours of a
-  // raked / compressed node when it is eliminated (its L column structure).
-  // The live neighbour list of v is adj_idx[adj_ptr[v], adj_ptr[v] + deg[v]),
-  // edited in place: rake and compress never raise a degree.
-  order.clear();
-  cs0.assign(m, -1);
-  cs1.assign(m, -1);
-  gone.assign(m, 0);
-  blocked.assign(m, 0);
-  live.resize(m);
-  std::iota(live.begin(), live.end(), 0);
-  static const bool no_compress = getenv("ABD_CHOL_NO_COMPRESS") != nullptr;
-  auto drop = [&](int u, int x) {
-    int* l = adj_idx.data() + adj_ptr[u];
-    const int d = deg[u];
-    for (int i = 0; i < d; ++i)
-      if (l[i] == x) {
-        l[i] = l[d - 1];
-        deg[u] = d - 1;
-        return;
-      }
-  };
-  auto relink = [&](int u, int x, int y) {  // in u's list: x -> y, or drop x when y is already there
-    int* l = adj_idx.data() + adj_ptr[u];
-    const int d = deg[u];
-    int ix = -1;
-    bool has_y = false;
-    for (int i = 0; i < d; ++i) {
-      if (l[i] == x) ix = i;
-      if (l[i] == y) has_y = true;
-    }
-    if (has_y) {
-      l[ix] = l[d - 1];
-      deg[u] = d - 1;
-    } else {
-      l[ix] = y;
-    }
-  };
-  for (;;) {
-    bool progress = false;
-    sel.clear();
-    for (int v : live)
-      if (deg[v] <= 1) sel.push_back(v);
-    for (int v : sel) {  // rake (a lone pair: the second end follows with no neighbour)
-      if (gone[v]) continue;
-      if (deg[v] == 1) {
-        const int u = adj_idx[adj_ptr[v]];
-        cs0[v] = u;
-        drop(u, v);
-      }
-      deg[v] = 0;
-      gone[v] = 1;
-      order.push_back(v);
-      progress = true;
-    }
-    if (!no_compress) {
-      sel.clear();
-      for (int v : live) blocked[v] = 0;
-      for (int v : live)
-        if (!gone[v] && !blocked[v] && deg[v] == 2) {
-          const int* l = adj_idx.data() + adj_ptr[v];
-          sel.push_back(v);
-          blocked[v] = 1;
-          blocked[l[0]] = 1;
-          blocked[l[1]] = 1;
+  // Order reuse: a miss inside a step (the union graph grew by a few contacts)
+  // keeps the step's fresh elimination order -- nodes new to the graph first -- and
+  // redoes only the symbolic factorization, unless the fill grows by more than
+  // ORDER_REUSE_FILL over the fresh order's, in factor blocks or update pairs (then
+  // the graph is ordered afresh).
+  static const bool no_reuse = getenv("ABD_CHOL_NO_ORDER_REUSE") != nullptr;
+  int n_core = 0;
+  bool reused = false;
+  if (!no_reuse && cc.valid && cc.n == n && !cc.gorder.empty())
+    reused = symbolic_fixed_order(m, adj_ptr, adj_idx, deg, loc, cc.gorder, (int64_t)(ORDER_REUSE_FILL * cc.fresh_nnz),
+                                  (int64_t)(ORDER_REUSE_FILL * cc.fresh_upd), w.hs_i + 31, order, pos, csp, csi);
+  if (!reused) {
+    // Elimination order by tree contraction (contact graphs of piles are forests of
+    // stacked chains): rounds of rake (every node of degree <= 1 at the start of the
+    // round; no fill) and compress (an independent set of degree-2 nodes; the fill
+    // edge joins the two neighbours), so a chain of L bodies is eliminated in
+    // O(log L) elimination-tree levels instead of L / 2.  What remains (degree >= 3
+    // everywhere) is ordered by minimum degree.  cs0/cs1 = the live neighbours of a
+    // raked / compressed node when it is eliminated (its L column structure).
+    // The live neighbour list of v is adj_idx[adj_ptr[v], adj_ptr[v] + deg[v]),
+    // edited in place: rake and compress never raise a degree.
+    order.clear();
+    cs0.assign(m, -1);
+    cs1.assign(m, -1);
+    gone.assign(m, 0);
+    blocked.assign(m, 0);
+    live.resize(m);
+    std::iota(live.begin(), live.end(), 0);
+    static const bool no_compress = getenv("ABD_CHOL_NO_COMPRESS") != nullptr;
+    auto drop = [&](int u, int x) {
+      int* l = adj_idx.data() + adj_ptr[u];
+      const int d = deg[u];
+      for (int i = 0; i < d; ++i)
+        if (l[i] == x) {
+          l[i] = l[d - 1];
+          deg[u] = d - 1;
+          return;
         }
-      for (int v : sel) {  // compress: v's neighbours a, b become adjacent (fill)
-        const int* l = adj_idx.data() + adj_ptr[v];
-        const int a2 = l[0], b2 = l[1];
-        cs0[v] = a2;
-        cs1[v] = b2;
-        relink(a2, v, b2);
-        relink(b2, v, a2);
+    };
+    auto relink = [&](int u, int x, int y) {  // in u's list: x -> y, or drop x when y is already there
+      int* l = adj_idx.data() + adj_ptr[u];
+      const int d = deg[u];
+      int ix = -1;
+      bool has_y = false;
+      for (int i = 0; i < d; ++i) {
+        if (l[i] == x) ix = i;
+        if (l[i] == y) has_y = true;
+      }
+      if (has_y) {
+        l[ix] = l[d - 1];
+        deg[u] = d - 1;
+      } else {
+        l[ix] = y;
+      }
+    };
+    for (;;) {
+      bool progress = false;
+      sel.clear();
+      for (int v : live)
+        if (deg[v] <= 1) sel.push_back(v);
+      for (int v : sel) {  // rake (a lone pair: the second end follows with no neighbour)
+        if (gone[v]) continue;
+        if (deg[v] == 1) {
+          const int u = adj_idx[adj_ptr[v]];
+          cs0[v] = u;
+          drop(u, v);
+        }
         deg[v] = 0;
         gone[v] = 1;
         order.push_back(v);
         progress = true;
       }
+      if (!no_compress) {
+        sel.clear();
+        for (int v : live) blocked[v] = 0;
+        for (int v : live)
+          if (!gone[v] && !blocked[v] && deg[v] == 2) {
+            const int* l = adj_idx.data() + adj_ptr[v];
+            sel.push_back(v);
+            blocked[v] = 1;
+            blocked[l[0]] = 1;
+            blocked[l[1]] = 1;
+          }
+        for (int v : sel) {  // compress: v's neighbours a, b become adjacent (fill)
+          const int* l = adj_idx.data() + adj_ptr[v];
+          const int a2 = l[0], b2 = l[1];
+          cs0[v] = a2;
+          cs1[v] = b2;
+          relink(a2, v, b2);
+          relink(b2, v, a2);
+          deg[v] = 0;
+          gone[v] = 1;
+          order.push_back(v);
+          progress = true;
+        }
+      }
+      live2.clear();
+      for (int v : live)
+        if (!gone[v]) live2.push_back(v);
+      live.swap(live2);
+      if (!progress || live.empty()) break;
     }
-    live2.clear();
-    for (int v : live)
-      if (!gone[v]) live2.push_back(v);
-    live.swap(live2);
-    if (!progress || live.empty()) break;
-  }
-  const double ms_contract = ms_since(t0);
-  const int n_core = m - (int)order.size();
-  std::vector<std::vector<int>> core_cs;
-  std::vector<int> core_glob;
-  if ((int)order.size() < m) {
-    std::vector<int> core_id(m, -1);
-    core_glob = live;
-    const int mc = (int)core_glob.size();
-    for (int c = 0; c < mc; ++c) core_id[core_glob[c]] = c;
-    std::vector<std::vector<int>> cadj(mc);
-    for (int c = 0; c < mc; ++c) {
-      const int v = core_glob[c];
-      for (int i = 0; i < deg[v]; ++i) cadj[c].push_back(core_id[adj_idx[adj_ptr[v] + i]]);
-      std::sort(cadj[c].begin(), cadj[c].end());
+    const double ms_contract = ms_since(t0);
+    n_core = m - (int)order.size();
+    std::vector<std::vector<int>> core_cs;
+    std::vector<int> core_glob;
+    if ((int)order.size() < m) {
+      std::vector<int> core_id(m, -1);
+      core_glob = live;
+      const int mc = (int)core_glob.size();
+      for (int c = 0; c < mc; ++c) core_id[core_glob[c]] = c;
+      std::vector<std::vector<int>> cadj(mc);
+      for (int c = 0; c < mc; ++c) {
+        const int v = core_glob[c];
+        for (int i = 0; i < deg[v]; ++i) cadj[c].push_back(core_id[adj_idx[adj_ptr[v] + i]]);
+        std::sort(cadj[c].begin(), cadj[c].end());
+      }
+      std::vector<int> corder;
+      min_degree(mc, cadj, corder, core_cs);
+      for (int c : corder) order.push_back(core_glob[c]);
+      for (auto& l : core_cs)
+        for (int& x : l) x = core_glob[x];
     }
-    std::vector<int> corder;
-    min_degree(mc, cadj, corder, core_cs);
-    for (int c : corder) order.push_back(core_glob[c]);
-    for (auto& l : core_cs)
-      for (int& x : l) x = core_glob[x];
-  }
-  const double ms_core = ms_since(t0);
-  static const bool trace_ord = getenv("ABD_TRACE_CHOL") != nullptr;
-  if (trace_ord)
-    fprintf(stderr, "[abd chol order] m=%d core=%d cur_ms=%.3f adj_ms=%.3f contract_ms=%.3f core_ms=%.3f\n", m, n_core,
-            ms_cur, ms_adj, ms_contract, ms_core);
-  pos.resize(m);
-  for (int i = 0; i < m; ++i) pos[order[i]] = i;
-  csp.assign(m + 1, 0);
-  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (cs0[v] >= 0) + (cs1[v] >= 0);
-  for (size_t c = 0; c < core_glob.size(); ++c) csp[core_glob[c] + 1] = (int)core_cs[c].size();
-  if (!core_glob.empty()) {  // recount: core nodes carry their min-degree column structures
-    std::vector<int> cnt(m, 0);
-    for (int v = 0; v < m; ++v) cnt[v] = (cs0[v] >= 0) + (cs1[v] >= 0);
-    for (size_t c = 0; c < core_glob.size(); ++c) cnt[core_glob[c]] = (int)core_cs[c].size();
-    csp[0] = 0;
-    for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + cnt[v];
-  }
-  csi.resize(csp[m]);
-  for (int v = 0; v < m; ++v) {
-    int* o = csi.data() + csp[v];
-    const int k = csp[v + 1] - csp[v];
-    if (k == 1) {
-      o[0] = cs0[v];
-    } else if (k == 2 && cs1[v] >= 0) {
-      const bool sw = pos[cs1[v]] < pos[cs0[v]];
-      o[0] = sw ? cs1[v] : cs0[v];
-      o[1] = sw ? cs0[v] : cs1[v];
+    const double ms_core = ms_since(t0);
+    static const bool trace_ord = getenv("ABD_TRACE_CHOL") != nullptr;
+    if (trace_ord)
+      fprintf(stderr, "[abd chol order] m=%d core=%d cur_ms=%.3f adj_ms=%.3f contract_ms=%.3f core_ms=%.3f\n", m, n_core,
+              ms_cur, ms_adj, ms_contract, ms_core);
+    pos.resize(m);
+    for (int i = 0; i < m; ++i) pos[order[i]] = i;
+    csp.assign(m + 1, 0);
+    for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (cs0[v] >= 0) + (cs1[v] >= 0);
+    for (size_t c = 0; c < core_glob.size(); ++c) csp[core_glob[c] + 1] = (int)core_cs[c].size();
+    if (!core_glob.empty()) {  // recount: core nodes carry their min-degree column structures
+      std::vector<int> cnt(m, 0);
+      for (int v = 0; v < m; ++v) cnt[v] = (cs0[v] >= 0) + (cs1[v] >= 0);
+      for (size_t c = 0; c < core_glob.size(); ++c) cnt[core_glob[c]] = (int)core_cs[c].size();
+      csp[0] = 0;
+      for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + cnt[v];
+    }
+    csi.resize(csp[m]);
+    for (int v = 0; v < m; ++v) {
+      int* o = csi.data() + csp[v];
+      const int k = csp[v + 1] - csp[v];
+      if (k == 1) {
+        o[0] = cs0[v];
+      } else if (k == 2 && cs1[v] >= 0) {
+        const bool sw = pos[cs1[v]] < pos[cs0[v]];
+        o[0] = sw ? cs1[v] : cs0[v];
+        o[1] = sw ? cs0[v] : cs1[v];
+      }
+    }
+    for (size_t c = 0; c < core_glob.size(); ++c) {
+      std::vector<int>& l = core_cs[c];
+      std::sort(l.begin(), l.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
+      std::copy(l.begin(), l.end(), csi.begin() + csp[core_glob[c]]);
+    }
+    cc.gorder.resize(m);
+    for (int i = 0; i < m; ++i) cc.gorder[i] = glob[order[i]];
+    cc.fresh_nnz = csp[m];
+    cc.fresh_upd = 0;
+    for (int v = 0; v < m; ++v) {
+      const int64_t k = csp[v + 1] - csp[v];
+      cc.fresh_upd += k * (k - 1) / 2;
     }
   }
-  for (size_t c = 0; c < core_glob.size(); ++c) {
-    std::vector<int>& l = core_cs[c];
-    std::sort(l.begin(), l.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
-    std::copy(l.begin(), l.end(), csi.begin() + csp[core_glob[c]]);
-  }
+  an.order_reused = reused;
   an.ms_order = ms_since(t0);
   t0 = clk::now();
 
@@ -1481,7 +1630,7 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   run.stats[3] = an.max_level;
   run.stats[4] = an.largest;
   run.stats[5] = an.n_coupled;
-  run.stats[6] = an.cached ? 1 : 0;
+  run.stats[6] = an.cached ? 1 : (an.order_reused ? 2 : 0);  // 2: order reused
   run.ms3[0] = an.ms_sync;
   run.ms3[1] = an.ms_order;
   run.ms3[2] = an.ms_plan;

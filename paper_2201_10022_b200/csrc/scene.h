@@ -232,7 +232,7 @@ struct Scene {
   // persistent workspaces (grown, never shrunk: no cudaMalloc in steady state)
   struct Work {
     // host scratch of the Cholesky analysis (reused: no allocations in the steady state)
-    std::vector<int> hs_i[32];
+    std::vector<int> hs_i[40];
     // ACCD hot list: the slowest queries (>= CCD_SLOW_IT iterations) of the previous
     // line search, re-evaluated right after the solve on side2 while the broad phase runs
     DVec<int4> hot_rows, slow_rows;
@@ -301,6 +301,9 @@ struct Scene {
       int64_t stats[8] = {};
       size_t offs[16] = {};
       int64_t hits = 0, misses = 0;
+      std::vector<int> gorder;  // elimination order (global ids) of the step's last fresh ordering
+      int64_t fresh_nnz = 0;    // its off-diagonal factor blocks
+      int64_t fresh_upd = 0;    // and update pairs
     } ch_cache;
     std::vector<uint64_t> ch_edges_cur;
     // structure flags + keys copied out by assemble() (event-ordered); consumed once
@@ -321,6 +324,11 @@ struct Scene {
   } w;
 
   Comm comm;
+
+  // joint reduction q_dyn = T u + q_const (constraints.py): dense T (12 n_dyn x red_nu),
+  // red_nu = 0 without joints; workspaces of the reduced solve (k_reduced.cu)
+  int64_t red_nu = 0;
+  DVec<double> red_T, red_W, red_X, red_A, red_v;
 
   // per-kernel instrumentation (CUDA events on `stream`)
   struct KStat {

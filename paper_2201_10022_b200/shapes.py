@@ -10,7 +10,7 @@ import numpy as np
 
 from .mesh import SurfaceMesh
 
-__all__ = ["box_mesh", "icosphere_mesh", "torus_mesh", "hexahedron_mesh"]
+__all__ = ["box_mesh", "icosphere_mesh", "torus_mesh", "hexahedron_mesh", "prism_mesh", "wedge_mesh"]
 
 # corners of [-1, 1]^3 and the 12 CCW-outward triangles (two per face)
 _CORNERS = np.array([[x, y, z] for z in (-1, 1) for (x, y) in ((-1, -1), (1, -1), (1, 1), (-1, 1))],
@@ -88,3 +88,43 @@ def torus_mesh(major=0.1, minor=0.02, n_major=24, n_minor=8, center=(0.0, 0.0, 0
     if np.einsum("ij,ij->i", a - pts.mean(0) * 0, np.cross(b, c)).sum() < 0:
         m = SurfaceMesh(m.vertices, m.triangles[:, ::-1])
     return m
+
+
+def _outward(m: SurfaceMesh) -> SurfaceMesh:
+    """Flip every triangle when the signed volume is negative."""
+    a, b, c = (m.vertices[m.triangles[:, k]] for k in range(3))
+    if np.einsum("ij,ij->i", a, np.cross(b, c)).sum() < 0:
+        return SurfaceMesh(m.vertices, m.triangles[:, ::-1])
+    return m
+
+
+def prism_mesh(n_sides=6, radius=1.0, height=1.0, axis=2) -> SurfaceMesh:
+    """Closed regular prism about a coordinate axis (reference shapes.py:125-152 layout:
+    bottom ring, top ring, bottom centre, top centre)."""
+    n = int(n_sides)
+    t = 2.0 * np.pi * np.arange(n) / n
+    plane = [k for k in range(3) if k != axis]
+    v = np.zeros((2 * n + 2, 3))
+    for ring, h in ((0, -0.5 * height), (1, 0.5 * height)):
+        v[ring * n:(ring + 1) * n, plane[0]] = radius * np.cos(t)
+        v[ring * n:(ring + 1) * n, plane[1]] = radius * np.sin(t)
+        v[ring * n:(ring + 1) * n, axis] = h
+    v[2 * n, axis], v[2 * n + 1, axis] = -0.5 * height, 0.5 * height
+    tris = []
+    for i in range(n):
+        j = (i + 1) % n
+        tris += [(i, j, n + j), (i, n + j, n + i), (2 * n, j, i), (2 * n + 1, n + i, n + j)]
+    return _outward(SurfaceMesh(v, np.asarray(tris, dtype=np.int64)))
+
+
+def wedge_mesh(theta0, theta1, r_inner, r_outer, depth) -> SurfaceMesh:
+    """Annular-sector prism in the xz plane extruded along y, centred on its corner mean
+    (reference shapes.py:96-122; corners in the box corner order)."""
+    def at(th, r, y):
+        return [r * np.cos(th), y, r * np.sin(th)]
+
+    c = []
+    for y in (-0.5 * depth, 0.5 * depth):
+        c += [at(theta0, r_inner, y), at(theta1, r_inner, y), at(theta1, r_outer, y), at(theta0, r_outer, y)]
+    c = np.asarray(c, dtype=float)
+    return _outward(hexahedron_mesh(c - c.mean(axis=0)))

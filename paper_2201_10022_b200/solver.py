@@ -236,11 +236,29 @@ def step_params_c(params: StepParams, min_distance=True, pcg_rel_tol=1e-8,
         linear_solver=1 if params.linear_solver == "pcg" else 0, audit_iterates=1 if params.audit_iterates else 0)
 
 
+def _sync_reduction(model: SystemModel, sc) -> None:
+    """Device copy of the joint reduction's T (abd_set_reduction), refreshed when the model's
+    reduction object or its T changes; removed when the model has none."""
+    red = model.reduction
+    key = None if red is None else (id(red), id(red.T), red.T.shape)
+    if getattr(sc, "_red_key", None) == key:
+        return
+    if red is None:
+        _native.check(_native.lib().abd_set_reduction(sc.ptr, 0, None))
+    else:
+        T = np.ascontiguousarray(red.T, dtype=np.float64)
+        if T.shape[0] != 12 * model.n_dyn:
+            raise ValueError(f"reduction T has {T.shape[0]} rows, expected 12 x {model.n_dyn} dynamic bodies")
+        _native.check(_native.lib().abd_set_reduction(sc.ptr, T.shape[1], T.ctypes.data))
+        sc._red_T = T  # keep the host copy alive with the key
+    sc._red_key = key
+
+
 def advance_step(model: SystemModel, state: SimState, params: StepParams):
-    """One implicit-Euler step (solver.py:493-628) fully on the device."""
-    if model.reduction is not None:
-        raise NotImplementedError("joint reduction (constraints.py) is outside the GPU hot path")
+    """One implicit-Euler step (solver.py:493-628) fully on the device; with a joint reduction
+    the Newton direction comes from T^T H T on the device (solver.py:479-490)."""
     sc = model.gpu_scene()
+    _sync_reduction(model, sc)
     B = len(model.bodies)
     q0 = np.ascontiguousarray(state.q, dtype=np.float64).reshape(B, 12)
     qd = np.ascontiguousarray(state.q_dot, dtype=np.float64).reshape(B, 12)
@@ -267,6 +285,9 @@ def advance_step(model: SystemModel, state: SimState, params: StepParams):
     new_state = state.copy()
     new_state.q = q
     new_state.q_dot = qdn
+    if model.reduction is not None:  # solver.py:595-600 (host bookkeeping of the reduced state)
+        new_state.u = model.reduction.extract_u(q[model.dyn_indices].reshape(-1))
+        new_state.u_dot = model.reduction.extract_u_rate(qdn[model.dyn_indices].reshape(-1))
     new_state.time = t_next
     new_state.step_index = state.step_index + 1
     timings = {"broad_phase": st.t_broad * 1e-3, "narrow_phase": 0.0, "assembly": st.t_assemble * 1e-3,

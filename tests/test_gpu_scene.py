@@ -1,0 +1,183 @@
+"""Scene loader, stepping driver, frames and audit vs the REFERENCE.
+
+Same scene files as the reference fixtures (tests/scene_files.py,
+tests/golden/scenes.npz from tests/golden/make_golden_scene.py).  Tolerances:
+normalisation (scale, origin, diameter) and the initial q / q_dot to 1e-12;
+per-frame world vertices to 1e-6 relative to the scene extent; the stats.csv
+header byte-identical; its deterministic columns: step, iterations, converged and
+candidates identical, min_distance / ip_value within 1e-6 relative, the ortho error
+(a cancellation-formed ~1e-8 quantity) within 1e-9 absolute;
+audit verdicts identical.  Plus the reference's own scene tests
+(pkg/tests/test_scene.py) that need the GPU (loading, intersection/containment
+rejection, frame denormalisation round trip, audit of hand-made frames,
+determinism across repeats and worker counts).
+"""
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(__file__), "golden", "scenes.npz")
+
+
+@pytest.fixture(scope="module")
+def scene_paths(tmp_path_factory):
+    from paper_2201_10022_b200 import shapes
+    from scene_files import write_scenes
+
+    return write_scenes(tmp_path_factory.mktemp("scenes"), shapes)
+
+
+@pytest.mark.parametrize("name", ["two_cubes", "drop", "hinge", "wheel"])
+def test_scene_run_vs_reference(scene_paths, tmp_path, name):
+    from paper_2201_10022_b200.scene import STATS_HEADER, load_scene, read_obj_objects, run
+    from scene_files import STEPS
+
+    g = np.load(G)
+    sc = load_scene(scene_paths[name])
+    assert abs(sc.scale - float(g[f"{name}_scale"])) <= 1e-12 * float(g[f"{name}_scale"])
+    assert np.allclose(sc.origin, g[f"{name}_origin"], rtol=0, atol=1e-12)
+    assert abs(sc.scene_diameter - float(g[f"{name}_diameter"])) <= 1e-12
+    assert np.allclose(sc.state.q, g[f"{name}_q0"], rtol=0, atol=1e-12)
+    assert np.allclose(sc.state.q_dot, g[f"{name}_qd0"], rtol=0, atol=1e-12)
+    nu = -1 if sc.model.reduction is None else sc.model.reduction.n_unknowns
+    assert nu == int(g[f"{name}_nu"])
+    out = tmp_path / "out"
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        stats, violations, _ = run(sc, STEPS[name], out_dir=out, audit=True)
+    assert len(violations) == int(g[f"{name}_violations"]) == 0
+    rows = (out / "stats.csv").read_text().strip().splitlines()
+    assert rows[0] == STATS_HEADER == str(g[f"{name}_csv_header"])
+    ref_rows = [r.split(",") for r in g[f"{name}_csv_det"]]
+    assert len(rows) - 1 == len(ref_rows)
+    for mine, ref in zip(rows[1:], ref_rows):
+        c = mine.split(",")
+        assert len(c) == 15
+        assert c[0] == ref[0] and c[1] == ref[1] and c[2] == ref[2] and c[4] == ref[4], (mine, ref)
+        for k in (3, 5, 7):
+            a, b = float(c[k]), float(ref[k])
+            assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12) or (not np.isfinite(b) and a == b), (k, mine, ref)
+        # max ortho error ||A A^T - I|| (~1e-8, formed by cancellation): absolute, consistent with
+        # DOFs agreeing to 1e-6 of O(1) affine entries through many stiff Newton solves
+        assert abs(float(c[6]) - float(ref[6])) <= 1e-9, (mine, ref)
+    frames = sorted(out.glob("frame_*.obj"))
+    assert [f.name for f in frames] == list(g[f"{name}_frame_names"])
+    ext = 1.0 / float(g[f"{name}_scale"])
+    for f in frames:
+        objs = read_obj_objects(f)
+        assert [n for n, _, _ in objs] == list(g[f"{name}_objnames"])
+        V = np.concatenate([v for _, v, _ in objs])
+        assert np.abs(V - g[f"{name}_{f.stem}"]).max() <= 1e-6 * ext, f.name
+
+
+def _two_cubes(tmp_path, gap=0.5):
+    import json
+
+    from paper_2201_10022_b200.shapes import box_mesh
+    from scene_files import write_mesh_obj
+
+    write_mesh_obj(tmp_path / "cube.obj", box_mesh(1.0))
+    raw = {"name": "two-cubes", "gravity": [0.0, 0.0, 0.0], "params": {"dt": 0.01},
+           "output": {"frame_interval": 1, "seed": 0, "workers": 1},
+           "bodies": [{"name": "a", "mesh": "cube.obj", "density": 1000.0},
+                      {"name": "b", "mesh": "cube.obj", "translation": [1.0 + gap, 0, 0]}]}
+    p = tmp_path / "scene.json"
+    p.write_text(json.dumps(raw), encoding="utf-8")
+    return p
+
+
+def test_load_normalisation_and_frame_round_trip(tmp_path):
+    """test_scene.py:48-82."""
+    from paper_2201_10022_b200.scene import load_scene, read_obj_objects, run
+    from paper_2201_10022_b200.shapes import box_mesh
+
+    sc = load_scene(_two_cubes(tmp_path))
+    assert len(sc.model.bodies) == 2 and sum(len(m.triangles) for m in sc.meshes) == 24
+    w = sc.world_vertices(denormalize=False)
+    lo = np.min([x.min(axis=0) for x in w], axis=0)
+    hi = np.max([x.max(axis=0) for x in w], axis=0)
+    assert np.isclose((hi - lo).max(), 1.0)
+    run(sc, 0, out_dir=tmp_path / "out")
+    objs = read_obj_objects(tmp_path / "out" / "frame_000000.obj")
+    assert [n for n, _, _ in objs] == ["a", "b"]
+    cube = box_mesh(1.0)
+    assert np.allclose(objs[0][1], cube.vertices, atol=1e-9)
+    assert np.allclose(objs[1][1], cube.vertices + [1.5, 0, 0], atol=1e-9)
+
+
+def test_initial_intersection_and_containment_rejected(tmp_path):
+    """test_scene.py:84-103."""
+    import json
+
+    from paper_2201_10022_b200.scene import load_scene
+    from paper_2201_10022_b200.shapes import box_mesh
+    from scene_files import write_mesh_obj
+
+    with pytest.raises(ValueError, match="intersects"):
+        load_scene(_two_cubes(tmp_path, gap=-0.5))
+    write_mesh_obj(tmp_path / "big.obj", box_mesh(2.0))
+    write_mesh_obj(tmp_path / "small.obj", box_mesh(0.3))
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps({"bodies": [{"name": "big", "mesh": "big.obj"}, {"name": "small", "mesh": "small.obj"}]}))
+    with pytest.raises(ValueError, match="intersects"):
+        load_scene(p)
+
+
+def test_audit_hand_made_frames(tmp_path):
+    """test_scene.py:192-215."""
+    from paper_2201_10022_b200.scene import audit_intersections, write_obj_frame
+    from paper_2201_10022_b200.shapes import box_mesh
+
+    cube = box_mesh(1.0)
+    (tmp_path / "bad").mkdir()
+    (tmp_path / "ok").mkdir()
+    write_obj_frame(tmp_path / "bad" / "frame_000000.obj", ["a", "b"],
+                    [cube.vertices, cube.vertices + [0.3, 0.2, 0.1]], [cube.triangles, cube.triangles])
+    v = audit_intersections(tmp_path / "bad")
+    assert len(v) == 1 and v[0][1:] == ("a", "b")
+    write_obj_frame(tmp_path / "ok" / "frame_000000.obj", ["a", "b"],
+                    [cube.vertices, cube.vertices + [2.0, 0, 0]], [cube.triangles, cube.triangles])
+    assert audit_intersections(tmp_path / "ok") == []
+
+
+def test_run_deterministic_across_repeats_and_workers(scene_paths, tmp_path):
+    """test_scene.py:170-189: frames and deterministic CSV columns repeat bitwise."""
+    from paper_2201_10022_b200.scene import load_scene, run
+
+    def go(tag, workers):
+        sc = load_scene(scene_paths["drop"])
+        sc.params.workers = workers
+        out = tmp_path / tag
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            run(sc, 8, out_dir=out)
+        frames = [p.read_text() for p in sorted(out.glob("frame_*.obj"))]
+        rows = (out / "stats.csv").read_text().strip().splitlines()[1:]
+        return frames, [",".join(r.split(",")[:8]) for r in rows]
+
+    f1, s1 = go("r1", 1)
+    f2, s2 = go("r2", 1)
+    f4, s4 = go("r4", 4)
+    assert f1 == f2 == f4 and s1 == s2 == s4
+
+
+def test_cli_simulate_and_audit(scene_paths, tmp_path):
+    """test_scene.py:237-261: exit codes of the command-line front end."""
+    from paper_2201_10022_b200.cli import main
+    from paper_2201_10022_b200.scene import write_obj_frame
+    from paper_2201_10022_b200.shapes import box_mesh
+
+    out = tmp_path / "cli_out"
+    assert main(["simulate", str(scene_paths["drop"]), "--steps", "5", "--out", str(out), "--audit", "--strict",
+                 "--quiet"]) == 0
+    assert (out / "stats.csv").exists()
+    assert main(["audit", str(out)]) == 0
+    cube = box_mesh(1.0)
+    (tmp_path / "bad").mkdir()
+    write_obj_frame(tmp_path / "bad" / "frame_000000.obj", ["a", "b"], [cube.vertices, cube.vertices + [0.2, 0.1, 0.0]],
+                    [cube.triangles, cube.triangles])
+    assert main(["audit", str(tmp_path / "bad")]) == 1
