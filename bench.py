@@ -17,7 +17,8 @@ reports the whole window and the full 200-step run from step 0 (also timed step
 by step).  `e2e` repeats the window through the public Python API with host
 numpy state (H2D q, q_dot, forces and D2H q, q_dot inside every timed step).
 `--gpus N` (N > 1) starts N ranks under torch.distributed.run when WORLD_SIZE is
-unset; the ranks partition ONE pile (strong scaling, max-over-ranks device time).
+unset; the ranks cut ONE pile into body slabs (strong scaling, max-over-ranks device
+time; csrc/comm.cu, k_chol.cu slab_pcg).
 Prints one JSON line (rank 0).
 """
 from __future__ import annotations
@@ -700,8 +701,9 @@ def run_scene(args):
                        "window": rate(ms_all, it_all), "full_run": full,
                        "l2": ("L2 flushed (512 MB write) before every timed step" if r.flush else
                               "per-step working set exceeds L2 (rest+topology+vertex boxes > 126 MB); no flush"),
-                       "parallelism": (f"pair-partitioned over {world} GPUs (NCCL all-reduce of the system, "
-                                       "replicated solve)") if world > 1 else "single"},
+                       "parallelism": (f"body slabs over {world} GPUs: slab-owned pairs, NCCL all-reduce of the "
+                                       "partial system, distributed PCG with slab-local Cholesky preconditioner")
+                       if world > 1 else "single"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "gpu_launches_window": int(launches_window), "clocks": clk.summary(),
         }

@@ -204,16 +204,24 @@ int abd_timer_start(abd_scene* s);
 int abd_timer_stop(abd_scene* s, double* ms);
 
 /* ---------------- multi-GPU: one process per GPU ----------------
- * Per-pair work (primitive pairs, pair blocks, CCD, contact/friction energy) is split
- * across ranks by overlap body pair; the assembled system, energies and the CCD bound
- * are all-reduced; factorisation and the Newton update run replicated.  A scene starts
- * single-rank.  dtype: 0 f64, 1 i32, 2 i64; op: 0 sum, 1 min, 2 max.  The callback
- * receives a device pointer after the scene stream has been synchronised and must
- * complete the in-place reduction before returning (0 = success). */
+ * Body-slab partition, recut every step: dynamic bodies sorted by position along the
+ * longest axis and cut into `world` slabs balanced by primitive count.  A body pair
+ * belongs to the slab of its lower body (higher when the lower is kinematic): this
+ * rank evaluates its primitive pairs, pair blocks, CCD queries and energies (halo
+ * pairs across a slab face are evaluated once).  Partial systems are all-reduced;
+ * the Newton system is solved by a distributed PCG over the slabs (slab-local
+ * sparse Cholesky preconditioner, slab segments of the search direction exchanged,
+ * dot products all-reduced); energies, CCD bound and error flags are all-reduced,
+ * so every rank holds the same state.  A scene starts single-rank.  dtype: 0 f64,
+ * 1 i32, 2 i64; op: 0 sum, 1 min, 2 max.  The callback receives a device pointer after
+ * the scene stream has been synchronised and must complete the in-place reduction
+ * before returning (0 = success). */
 typedef int (*abd_allreduce_fn)(void* user, void* device_ptr, int64_t count, int dtype, int op);
 int abd_nccl_unique_id(uint8_t* out128);
 int abd_scene_set_comm_nccl(abd_scene* s, const uint8_t* id128, int rank, int world);
 int abd_scene_set_comm_callback(abd_scene* s, int rank, int world, abd_allreduce_fn fn, void* user);
+/* the current step's slab owner per body (-1 kinematic) and the cut axis (partition.py restates it) */
+int abd_get_slab_owner(abd_scene* s, int32_t* owner, int32_t* axis);
 
 int abd_set_state(abd_scene* s, const double* q, const double* q_dot);
 /* World positions of every vertex (bodies concatenated, V x 3) at host q (n_bodies x 12), or at the

@@ -100,6 +100,7 @@ _SIGS = {
     "abd_get_state": (i32, [vp, vp, vp]),
     "abd_set_reduction": (i32, [vp, i64, vp]),
     "abd_world_vertices": (i32, [vp, dp, dp]),
+    "abd_get_slab_owner": (i32, [vp, vp, vp]),
     "abd_advance_step": (i32, [vp, vp, C.POINTER(StepParamsC), C.POINTER(StepStatsC), vp]),
 }
 

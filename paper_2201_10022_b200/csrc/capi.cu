@@ -1028,6 +1028,15 @@ int abd_get_state(abd_scene* h, double* q, double* q_dot) {
   });
 }
 
+int abd_get_slab_owner(abd_scene* h, int32_t* owner, int32_t* axis) {
+  return guard([&] {
+    SC(h);
+    if (!s.slab_valid) throw Error(ABD_ERR_ARG, "no slab partition (single-rank scene or no step yet)");
+    for (int b = 0; b < s.B; ++b) owner[b] = s.h_slab_owner[b];
+    if (axis) *axis = s.slab_axis;
+  });
+}
+
 int abd_set_reduction(abd_scene* h, int64_t n_unknowns, const double* T) {
   return guard([&] {
     SC(h);

@@ -1,17 +1,27 @@
-// Multi-GPU collectives for the partitioned Newton step.
+// Multi-GPU collectives and the body-slab partition of the Newton step.
 //
-// One process per GPU.  The scene's per-pair work (primitive pairs, pair
-// blocks, CCD, contact/friction energies) is split across ranks by overlap
-// body pair; the assembled system, scalar energies and the CCD bound are
-// combined with all-reduces; the factorisation and the Newton update run
-// replicated, so every rank holds the same state.
+// One process per GPU.  Each step the dynamic bodies are cut into W slabs along
+// the longest axis of their positions, balanced by primitive count
+// (slab_partition; partition.py restates it for the CPU tests).  A body pair
+// belongs to the slab owning its lower body (its higher one when the lower is
+// kinematic), so pairs across a slab face are halo pairs of exactly one rank:
+// its primitive pairs, pair blocks, CCD queries and contact / friction energies.
+// The assembled system is all-reduced so every rank holds complete rows; the
+// Newton system is solved by a distributed PCG (k_chol.cu slab_pcg) whose
+// preconditioner is each rank's sparse Cholesky of its own slab block, with the
+// search vector's slab segments exchanged and its dot products all-reduced.
+// Scalars (energies, CCD bound, flags) are all-reduced; every rank takes the same
+// decisions and holds the same state.
 //
 // Backends: NCCL loaded at run time (whichever libnccl.so.2 the process already
 // uses, e.g. torch's), or a host callback (tests drive it with torch.distributed
 // gloo ranks sharing one GPU).  Reductions are enqueued on the scene stream.
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <vector>
 #include <mutex>
 
 #include "driver.h"
@@ -166,6 +176,69 @@ int64_t comm_allgather_i64(Scene& s, const int64_t* local, int64_t n_local, DVec
     at += hc[r];
   }
   return tot;
+}
+
+// Slabs: dynamic bodies sorted by (p[axis], id), axis = longest extent of their
+// positions; slab k takes the bodies whose primitive-weight midpoint falls in
+// [k/W, (k+1)/W) of the total: owner = floor((2 cum - w) W / (2 total)) in integers.
+void slab_partition(Scene& s, const double* q) {
+  const int W = s.comm.world, B = s.B;
+  s.slab_valid = false;
+  if (W <= 1) return;
+  if ((int)s.h_prim_w.size() != B) {
+    std::vector<int> vo(B + 1), eo(B + 1), to(B + 1);
+    s.v_off.download(vo.data(), B + 1, s.stream);
+    s.e_off.download(eo.data(), B + 1, s.stream);
+    s.t_off.download(to.data(), B + 1, s.stream);
+    SSYNC(s.stream);
+    s.h_prim_w.resize(B);
+    for (int b = 0; b < B; ++b) s.h_prim_w[b] = (vo[b + 1] - vo[b]) + (eo[b + 1] - eo[b]) + (to[b + 1] - to[b]);
+  }
+  std::vector<double> hq(12 * (size_t)B);
+  CK(cudaMemcpyAsync(hq.data(), q, hq.size() * sizeof(double), cudaMemcpyDeviceToHost, s.stream));
+  SSYNC(s.stream);
+  std::vector<int> idx;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int b = 0; b < B; ++b)
+    if (s.h_dyn[b]) {
+      idx.push_back(b);
+      for (int k = 0; k < 3; ++k) lo[k] = std::min(lo[k], hq[12 * (size_t)b + k]), hi[k] = std::max(hi[k], hq[12 * (size_t)b + k]);
+    }
+  int axis = 0;
+  for (int k = 1; k < 3; ++k)
+    if (hi[k] - lo[k] > hi[axis] - lo[axis]) axis = k;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) {
+    const double pa = hq[12 * (size_t)a + axis], pb = hq[12 * (size_t)b + axis];
+    return pa != pb ? pa < pb : a < b;
+  });
+  int64_t total = 0;
+  for (int b : idx) total += s.h_prim_w[b];
+  s.h_slab_owner.assign(B, -1);
+  int64_t cum = 0;
+  for (int b : idx) {
+    const int64_t w = s.h_prim_w[b];
+    cum += w;
+    s.h_slab_owner[b] = total > 0 ? (int)std::min<int64_t>((2 * cum - w) * W / (2 * total), W - 1) : 0;
+  }
+  std::vector<int> own_slot(std::max(s.n_dyn, 1), 0);
+  for (int k = 0; k < s.n_dyn; ++k) own_slot[k] = s.h_slab_owner[s.h_dyn_body[k]] == s.comm.rank ? 1 : 0;
+  s.slab_owner.upload(s.h_slab_owner.data(), B, s.stream);
+  s.slab_own_slot.upload(own_slot.data(), std::max(s.n_dyn, 1), s.stream);
+  s.slab_axis = axis;
+  s.slab_valid = true;
+}
+
+__global__ void k_slab_mask(int64_t n_off, const int2* __restrict__ keys, const int* __restrict__ own, int* flags) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_off) return;
+  const int2 k = keys[i];
+  if (!own[k.x] || !own[k.y]) flags[i] = 0;
+}
+
+void slab_mask_structure(Scene& s, int* flags) {
+  if (!s.slab_valid || s.H.n_off == 0) return;
+  k_slab_mask<<<grid_for(s.H.n_off, 256), 256, 0, s.stream>>>(s.H.n_off, s.H.upper_keys.p, s.slab_own_slot.p, flags);
+  note_launch("k_slab_mask");
 }
 
 }  // namespace abd

@@ -345,15 +345,16 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   EventTimer tm(s, 2);
   launch_ccd_both(s, s.q.p, s.dq.p, P.ccd_slack, tmin, w.lserr.p, /*track=*/true);
   tm.stop();
+  // partitioned: the global CCD bound (t >= 0: min of the bit patterns == min of the
+  // values) before the trial point, so every rank evaluates its pairs at the same q_trial
+  comm_allreduce(s, tmin, 1, 0, 1);
   CK(cudaStreamWaitEvent(st, s.join_ev, 0));
   k_alpha_trial<<<grid_for(NB, 256), 256, 0, st>>>(NB, s.q.p, s.dq.p, tmin, P.ccd_step_scale, s.q_trial.p);
   note_launch("k_alpha_trial");
   launch_energy(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v,
                 w.lsred.p + 4 * RED_BLOCKS, w.lsscal.p + 4, w.lserr.p + 1);
   w.ch_early = false;
-  // partitioned: global CCD bound (t >= 0: min of the bit patterns == min of the values),
-  // energies and error flags over all ranks
-  comm_allreduce(s, tmin, 1, 0, 1);
+  // partitioned: energies and error flags over all ranks
   comm_allreduce(s, w.lsscal.p, 8, 0, 0);
   comm_allreduce(s, w.lserr.p, 2, 1, 2);
   double* hp = s.h_pinned + 32;
@@ -534,6 +535,7 @@ static void mark_structure(Scene& s) {
       note_launch("k_mark_active");
     }
     comm_allreduce(s, w.ch_flags.p, n_off, 1, 2);  // union of the ranks' couplings
+    slab_mask_structure(s, w.ch_flags.p);          // multi-rank: this slab's block only
     int* hm = w.h_meta.reserve(3 * (size_t)n_off);
     CK(cudaMemcpyAsync(hm, w.ch_flags.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
     CK(cudaMemcpyAsync(hm + n_off, s.H.upper_keys.p, n_off * sizeof(int2), cudaMemcpyDeviceToHost, s.stream));
@@ -613,6 +615,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
   s.red.resize(4 * RED_BLOCKS);
   CK(cudaMemcpyAsync(s.q0.p, s.q.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   launch_q_tilde(s, s.q0.p, s.q_dot.p, s.forces.p, P.dt, s.q_tilde.p);
+  if (s.comm.world > 1) slab_partition(s, s.q.p);  // body slabs for this step (comm.cu)
 
   auto t0 = clk::now();
   broad_phase(s, s.q.p, s.q.p, P.d_hat);
@@ -641,8 +644,11 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
         note_launch("k_neg");
         const bool reduced = s.red_nu > 0;  // joints: dense T^T H T (k_reduced.cu)
-        const bool chol = !reduced && P.linear_solver != 1;
+        // multi-rank: distributed PCG over the slabs, slab-local Cholesky preconditioner
+        const bool slab = !reduced && P.linear_solver != 1 && s.comm.world > 1;
+        const bool chol = !reduced && !slab && P.linear_solver != 1;
         if (reduced) reduced_solve(s, s.w.neg.p, s.dx.p);
+        else if (slab) pcg_it = slab_pcg(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
         else if (chol) chol_begin(s, s.w.neg.p, s.dx.p);
         else pcg_it = pcg_solve(s, s.w.neg.p, s.dx.p, P.pcg_rel_tol, P.pcg_max_iters, rel);
         HMARK();
@@ -709,10 +715,18 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         e = ip_value(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
       }
       CK(cudaMemcpyAsync(s.q.p, s.q_trial.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
-      if (trace_newton)
-        fprintf(stderr, "newton it=%d dq/dt=%.3e gd=%.3e pcg=%d rel=%.2e ccd=%.3e alpha=%.3e e0=%.10e de=%.3e ncand=%lld\n",
+      if (trace_newton) {
+        std::vector<double> hq(NB), hd(NB);
+        CK(cudaMemcpyAsync(hq.data(), s.q.p, NB * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        CK(cudaMemcpyAsync(hd.data(), s.dq.p, NB * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        SSYNC(stream);
+        double cq = 0.0, cd = 0.0;
+        for (int64_t i = 0; i < NB; ++i) cq += hq[i] * (1.0 + 1e-3 * (double)(i % 97)), cd += hd[i] * (1.0 + 1e-3 * (double)(i % 89));
+        fprintf(stderr, "newton it=%d dq/dt=%.3e gd=%.3e pcg=%d rel=%.2e ccd=%.3e alpha=%.3e e0=%.10e de=%.3e ncand=%lld "
+                "sum_q=%.17g sum_dq=%.17g\n",
                 it, amax / P.dt, gd, pcg_it, rel, amax_ccd, alpha, e0, e - e0,
-                (long long)(s.cands.n_vf + s.cands.n_ee));
+                (long long)(s.cands.n_vf + s.cands.n_ee), cq, cd);
+      }
       st.t_line_search += ms(tls, clk::now());
       if (trace) trace[n_trace] = e;
       ++n_trace;

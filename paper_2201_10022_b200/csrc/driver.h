@@ -33,6 +33,12 @@ void comm_init_callback(Scene& s, int rank, int world, abd_allreduce_fn fn, void
 void comm_destroy(Scene& s);
 void comm_allreduce(Scene& s, void* dptr, int64_t count, int dtype, int op);
 int64_t comm_allgather_i64(Scene& s, const int64_t* local, int64_t n_local, DVec<int64_t>& out);
+// body slabs of a multi-rank scene from the state q (device): owners per body / slot
+void slab_partition(Scene& s, const double* q);
+// zero the structure flags of pattern blocks not inside this rank's slab
+void slab_mask_structure(Scene& s, int* flags);
+// k_chol.cu: distributed PCG, slab-local sparse Cholesky preconditioner (multi-rank solve)
+int slab_pcg(Scene& s, const double* b, double* x, double rel_tol, int max_iters, double& rel_res);
 // k_stats.cu
 double global_min_distance(Scene& s, const double* q, int skip_static = 1);
 // the same value for the end-of-step stats; overwrites the resident candidate set

@@ -18,6 +18,10 @@
 #include "kernels.h"
 
 namespace abd {
+void slab_partition(Scene& s, const double* q);  // comm.cu
+}
+
+namespace abd {
 
 __global__ void k_vertex_boxes(int64_t V, const int* __restrict__ vert_body, const double* __restrict__ rest,
                                const double* __restrict__ q0, const double* __restrict__ q1, double h,
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
     k_prim_pairs2(PrimGeo g, GrpGeo gr, int use_groups, int64_t n_ov, const int2* __restrict__ ov,
                   const double* __restrict__ bbox, unsigned long long* counters, int64_t cap_vf, int64_t cap_ee,
                   int4* out_vf, int4* out_ee, int cap_list, int3 cap_k, int2* tab, int* unsorted,
-                  int rank, int world,
+                  int rank, const int* __restrict__ owner,
                   unsigned long long* work, const int* n_ov_dev) {
   if (n_ov_dev) n_ov = *n_ov_dev;  // deferred count (Verlet-list filter result, no host sync)
   extern __shared__ double p2_sm[];
@@ -478,15 +482,24 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   __shared__ int gfirst[6], gcount[6], ghits;
   __shared__ int hitg[256];
   // pairs are handed out dynamically (their costs vary by orders of magnitude);
-  // multi-GPU: this rank takes overlap pairs rank, rank + world, ... (table rows of the others stay 0)
+  // multi-GPU (owner != null): this rank takes the overlap pairs of its slab -- the
+  // slab of the lower body, or of the higher one when the lower is kinematic
+  // (table rows of the other ranks' pairs stay 0)
   __shared__ long long next_k;
   for (;;) {
     if (threadIdx.x == 0) next_k = (long long)atomicAdd(work, 1ull);
     __syncthreads();
-    const int64_t pi = rank + (int64_t)next_k * world;
+    const int64_t pi = next_k;
     if (pi >= n_ov) break;
     const int2 pr = ov[pi];
     const int bi = pr.x, bj = pr.y;
+    if (owner) {
+      const int olo = owner[min(bi, bj)], ohi = owner[max(bi, bj)];
+      if ((olo >= 0 ? olo : ohi) != rank) {
+        __syncthreads();  // every thread has read next_k before thread 0 takes the next pair
+        continue;
+      }
+    }
     if (threadIdx.x < 6) {
       const int side = threadIdx.x / 3, kind = threadIdx.x % 3;
       const int body = side ? bj : bi;
@@ -1352,7 +1365,7 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
       auto kfn = runs ? k_prim_pairs2<true> : k_prim_pairs2<false>;
       kfn<<<grid, P2_THREADS, p2_smem, st>>>(g, gg, ug, n_ov, ov, bbox, counters, (int64_t)vf.cap, (int64_t)ee.cap,
                                              vf.p, ee.p, cap_list, cap_k, w.tab.p, unsorted, s.comm.rank,
-                                             s.comm.world, w.ull.p + 11, n_ov_dev);
+                                             s.comm.world > 1 ? s.slab_owner.p : nullptr, w.ull.p + 11, n_ov_dev);
     } else {
       int grid = (int)std::min<int64_t>(n_ov, (int64_t)s.num_sms);
       k_prim_pairs<<<grid, BP_THREADS, BP_SMEM, st>>>(g, n_ov, ov, bbox, counters, (int64_t)vf.cap,
@@ -1544,6 +1557,7 @@ static void vl_filter(Scene& s, int* info, bool zero_info) {
 
 void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   cudaStream_t st = s.stream;
+  if (s.comm.world > 1 && !s.slab_valid) slab_partition(s, q0);  // (advance_step re-cuts per step)
   double h = 0.5 * d_hat;
   Cands& c = s.cands;
   Scene::Work& w = s.w;

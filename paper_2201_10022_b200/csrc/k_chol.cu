@@ -1715,4 +1715,159 @@ int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& r
   return chol_finish(s, rel_tol, rel_res, max_refine, changed);
 }
 
+// ---------------------------------------------------------------------------
+// Multi-rank solve: preconditioned CG on the all-reduced system,
+// rows distributed by body slab.  Each rank owns the rows of its slab's dynamic
+// slots; its preconditioner is the sparse Cholesky of its slab block (the
+// analysis graph masked to in-slab couplings, slab_mask_structure; other slots
+// are isolated nodes whose right-hand side is zero).  Per iteration: the search
+// direction's slab segments are exchanged (all-reduce of vectors zero outside the
+// owned rows = an all-gather, a superset of the SpMV halo), A p on the owned rows,
+// and the dot products are all-reduced.  Converged when |b - A x| <= rel_tol |b|
+// for the assembled x (solve_refined's contract, sparse.py:149-161), checked on the
+// true residual.  p^T A p <= 0 raises ABD_ERR_FACTORIZATION (CG breakdown).
+__global__ void k_own_copy(int64_t N, const int* __restrict__ own, const double* __restrict__ src, double* dst) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < N) dst[t] = own[t / 12] ? src[t] : 0.0;
+}
+
+// two owned-row dot products (a.b, c.d) as fixed-order partials [RED_BLOCKS][2]
+__global__ void k_own_dots(int64_t N, const int* __restrict__ own, const double* __restrict__ a,
+                           const double* __restrict__ b, const double* __restrict__ c, const double* __restrict__ d,
+                           double* part) {
+  __shared__ double s0[RED_THREADS], s1[RED_THREADS];
+  double x0 = 0.0, x1 = 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x)
+    if (own[t / 12]) {
+      x0 = fma(a[t], b[t], x0);
+      x1 = fma(c[t], d[t], x1);
+    }
+  s0[threadIdx.x] = x0;
+  s1[threadIdx.x] = x1;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s0[threadIdx.x] += s0[threadIdx.x + w];
+      s1[threadIdx.x] += s1[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s0[0];
+    part[gridDim.x + blockIdx.x] = s1[0];
+  }
+}
+
+// x += alpha p, r -= alpha q on the owned rows
+__global__ void k_own_xr(int64_t N, const int* __restrict__ own, double alpha, const double* __restrict__ p,
+                         const double* __restrict__ q, double* x, double* r) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= N || !own[t / 12]) return;
+  x[t] = fma(alpha, p[t], x[t]);
+  r[t] = fma(-alpha, q[t], r[t]);
+}
+
+// p = z + beta p on the owned rows, 0 elsewhere (ready for the segment exchange)
+__global__ void k_own_p(int64_t N, const int* __restrict__ own, const double* __restrict__ z, double beta, double* p) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < N) p[t] = own[t / 12] ? fma(beta, p[t], z[t]) : 0.0;
+}
+
+int slab_pcg(Scene& s, const double* b, double* x, double rel_tol, int max_iters, double& rel_res) {
+  Bsr& H = s.H;
+  Scene::Work& w = s.w;
+  cudaStream_t st = s.stream;
+  const int n = H.n;
+  const int64_t N = 12 * (int64_t)n;
+  rel_res = 0.0;
+  if (n == 0) return 0;
+  if (!s.slab_valid) throw Error(ABD_ERR_ARG, "slab_pcg without a slab partition");
+  const int* own = s.slab_own_slot.p;
+  w.bad.resize(1);
+  Analysis an;
+  CholWorker* wk = worker(s, false);
+  if (!wk || !wk->take(an)) an = chol_analyze(s);
+  CholView v = an.view;
+  const int big = 0x7fffffff;
+  dev_set_i32(st, w.bad.p, big);
+  w.r.resize(N);
+  w.z.resize(N);
+  w.p.resize(N);
+  w.Ap.resize(N);
+  w.part.resize(2 * RED_BLOCKS);
+  w.scal.resize(8);
+  double* hs = s.h_pinned + 48;  // scratch scalars (pinned; the line search uses [32, 43))
+  int* hb = reinterpret_cast<int*>(s.h_pinned + 52);
+  auto dots = [&](const double* a, const double* bb, const double* c, const double* d) {
+    k_own_dots<<<RED_BLOCKS, RED_THREADS, 0, st>>>(N, own, a, bb, c, d, w.part.p);
+    note_launch("k_own_dots");
+    reduce_fixed_multi(st, w.part.p, RED_BLOCKS, 2, w.scal.p);
+    comm_allreduce(s, w.scal.p, 2, 0, 0);
+    pack_to_host(st, hs, {{w.scal.p, 16, 0}, {w.bad.p, 4, 32}});
+    SSYNC(st);
+    if (*hb != big) throw Error(ABD_ERR_FACTORIZATION, "non-SPD pivot in the slab block Cholesky", *hb);
+  };
+  Scene::KStat& ks = s.kstat[0];
+  if (s.instrument) {
+    kstat_flush(s, 0);
+    CK(cudaEventRecord(ks.e0, st));
+  }
+  k_chol_apos<<<grid_for(n, 128), 128, 0, st>>>(v);
+  note_launch("k_chol_apos");
+  CK(cudaMemsetAsync(x, 0, N * sizeof(double), st));
+  k_own_copy<<<grid_for(N, 256), 256, 0, st>>>(N, own, b, w.r.p);  // r = b (x = 0)
+  note_launch("k_own_copy");
+  launch_sched(s, v, w.r.p, w.z.p, true);  // factor the slab block, z = M^-1 r
+  CK(cudaMemcpyAsync(w.p.p, w.z.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  dots(w.r.p, w.z.p, b, b);
+  double rz = hs[0];
+  const double bn = std::sqrt(hs[1] >= 0.0 ? hs[1] : 0.0);  // owned rows summed over ranks = |b|
+  int it = 0;
+  if (bn > 0.0) {
+    for (int round = 0; round < 3; ++round) {
+      for (; it < max_iters;) {
+        comm_allreduce(s, w.p.p, N, 0, 0);  // slab segments of p on every rank
+        spmv(s, w.p.p, w.Ap.p);
+        dots(w.p.p, w.Ap.p, w.p.p, w.Ap.p);
+        const double pq = hs[0];
+        if (!(pq > 0.0)) throw Error(ABD_ERR_FACTORIZATION, "distributed PCG breakdown (p^T A p <= 0)");
+        const double alpha = rz / pq;
+        k_own_xr<<<grid_for(N, 256), 256, 0, st>>>(N, own, alpha, w.p.p, w.Ap.p, x, w.r.p);
+        note_launch("k_own_xr");
+        ++it;
+        launch_sched(s, v, w.r.p, w.z.p, false);  // z = M^-1 r (slab triangular solves)
+        dots(w.r.p, w.z.p, w.r.p, w.r.p);
+        const double rz_new = hs[0];
+        if (std::sqrt(std::max(hs[1], 0.0)) <= rel_tol * bn) break;
+        k_own_p<<<grid_for(N, 256), 256, 0, st>>>(N, own, w.z.p, rz_new / rz, w.p.p);
+        note_launch("k_own_p");
+        rz = rz_new;
+      }
+      // the assembled x and its true residual (identical on every rank)
+      CK(cudaMemcpyAsync(w.Ap.p, x, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      comm_allreduce(s, w.Ap.p, N, 0, 0);
+      launch_resid(s, b, w.Ap.p);
+      SSYNC(st);
+      const double rn = std::sqrt(s.h_pinned[24]), bt = std::sqrt(s.h_pinned[25]);
+      rel_res = bt > 0.0 ? rn / bt : 0.0;
+      if (rel_res <= rel_tol || it >= max_iters) break;
+      // restart from the recursive residual's drift: r = b - A x on the owned rows
+      k_own_copy<<<grid_for(N, 256), 256, 0, st>>>(N, own, w.r.p, w.r.p);
+      launch_sched(s, v, w.r.p, w.z.p, false);
+      CK(cudaMemcpyAsync(w.p.p, w.z.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      dots(w.r.p, w.z.p, w.r.p, w.r.p);
+      rz = hs[0];
+    }
+    CK(cudaMemcpyAsync(x, w.Ap.p, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+  if (s.instrument) {
+    CK(cudaEventRecord(ks.e1, st));
+    ks.pending = true;
+    ks.p_units = 1 + it;
+    ks.p_bytes = 1152.0 * 2.0 * (double)an.n_blk + 1152.0 * 2.0 * (double)an.n_upd +
+                 (double)(1 + it) * (1152.0 * 2.0 * (double)an.n_blk + 1152.0 * (double)H.nnzb);
+  }
+  return it;
+}
+
 }  // namespace abd

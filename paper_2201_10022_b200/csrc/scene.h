@@ -324,6 +324,12 @@ struct Scene {
   } w;
 
   Comm comm;
+  // body-slab partition of a multi-rank scene (comm.cu slab_partition, once per step):
+  // owner rank per body (-1 kinematic), owned flag per dynamic slot
+  DVec<int> slab_owner, slab_own_slot;
+  std::vector<int> h_slab_owner, h_prim_w;
+  int slab_axis = 0;
+  bool slab_valid = false;
 
   // joint reduction q_dyn = T u + q_const (constraints.py): dense T (12 n_dyn x red_nu),
   // red_nu = 0 without joints; workspaces of the reduced solve (k_reduced.cu)

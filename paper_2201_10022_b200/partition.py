@@ -1,60 +1,40 @@
-"""Partitioning for multi-GPU steps, host-side logic.
+"""Body-slab partition of a multi-GPU Newton step, host-side restatement.
 
-Implemented on the device (csrc/comm.cu, csrc/k_broad.cu): the per-pair work is
-split by OVERLAP BODY PAIR -- the sorted overlap list is identical on every
-rank and rank r takes pairs r, r + W, r + 2W, ... (`pair_owner` /
-`rows_of_owned_pairs` restate it for the CPU tests); the system, energies and
-CCD bound are all-reduced, the solve is replicated.  Every candidate belongs to
-exactly one overlap pair, so the ranks' candidate sets are disjoint and their
-union is the single-GPU set.
+Implemented on the device (csrc/comm.cu `slab_partition`, csrc/k_broad.cu,
+csrc/k_chol.cu `slab_pcg`); these functions restate it for the CPU / gloo tests.
 
-The body-slab helpers below are the alternative SURVEY §8(e) sketches (slab
-ownership with halo bodies); they are kept for slab-sharded scenes.
+One process per GPU.  Each step the dynamic bodies are sorted by position along
+the longest axis of their positions (ties by body id) and cut into W contiguous
+slabs balanced by primitive count (V + E + T per body); kinematic bodies are
+replicated (owner -1).  Geometry is replicated on every GPU, only q / dq move.
 
-One process per GPU.  Each step, dynamic bodies are sorted by centroid along
-the longest scene axis and cut into contiguous slabs balanced by primitive
-count; kinematic bodies (ground slabs, walls) are replicated.  Geometry is
-replicated on every GPU so only q / dq cross ranks.
-
-Per rank:
-  * halo bodies  = bodies owned elsewhere whose swept box overlaps a box of an
-                   owned body (from the body-pair overlap list);
-  * owned pairs  = candidate rows with at least one owned body (a cross-slab
-                   pair is evaluated on both owners, each keeps its own rows of
-                   the gradient / BSR, so no reverse reduction is needed);
-  * counted pairs = the subset whose scalar contribution (energy, counts) this
-                   rank adds: owner of min(body_a, body_b), or of the dynamic
-                   side when the other is kinematic — every pair exactly once;
-  * scalars are combined in rank order after an all-gather so `e < e0`
-    decisions are identical on every rank and for every world size.
+  * a body pair (and every candidate row of it) belongs to the slab of its lower
+    body, or of its higher body when the lower one is kinematic (`counted_rows`):
+    pairs across a slab face are the halo pairs of exactly one rank, so the ranks'
+    candidate sets are disjoint and their union is the single-GPU set;
+  * that rank evaluates the pair's blocks, CCD query and energy; the partial
+    systems are all-reduced, so every rank holds complete rows for its bodies;
+  * the Newton system is solved by a distributed PCG: rows by slab, each rank's
+    preconditioner the Cholesky of its slab block, the search direction's slab
+    segments exchanged (a superset of the halo of `halo_bodies`), dot products,
+    energies and the CCD bound all-reduced.
 """
 from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["pair_owner", "rows_of_owned_pairs", "slab_partition", "halo_bodies", "owned_rows", "counted_rows",
-           "dedup_union", "ordered_sum"]
-
-
-def pair_owner(n_pairs, world):
-    """Owning rank of each overlap pair (index order of the sorted overlap list)."""
-    return np.arange(n_pairs, dtype=np.int64) % max(int(world), 1)
-
-
-def rows_of_owned_pairs(rows, overlap_pairs, rank, world):
-    """Candidate rows (body_a, prim_a, body_b, prim_b) whose overlap pair `rank` owns."""
-    r = np.asarray(rows, dtype=np.int64).reshape(-1, 4)
-    ov = np.asarray(overlap_pairs, dtype=np.int64).reshape(-1, 2)
-    owner = pair_owner(len(ov), world)
-    index = {(int(a), int(b)): k for k, (a, b) in enumerate(ov)}
-    keep = [owner[index[(min(int(x[0]), int(x[2])), max(int(x[0]), int(x[2])))]] == rank for x in r]
-    return r[np.array(keep, dtype=bool)] if len(r) else r
+__all__ = ["slab_partition", "slab_owner_of_q", "halo_bodies", "owned_rows", "counted_rows", "dedup_union",
+           "ordered_sum"]
 
 
 def slab_partition(centroids, weights, dynamic, n_parts, axis=None):
-    """owner[b] in [0, n_parts) for dynamic bodies, -1 (replicated) for kinematic."""
+    """owner[b] in [0, n_parts) for dynamic bodies, -1 (replicated) for kinematic.
+
+    Dynamic bodies sorted by (centroid[axis], id); slab k takes those whose weight
+    midpoint lies in [k/n, (k+1)/n) of the total, in integer arithmetic:
+    owner = (2 cum - w) n // (2 total) (csrc/comm.cu slab_partition)."""
     c = np.asarray(centroids, dtype=float).reshape(-1, 3)
-    w = np.asarray(weights, dtype=float).reshape(-1)
+    w = np.rint(np.asarray(weights, dtype=float).reshape(-1)).astype(np.int64)
     dyn = np.asarray(dynamic, dtype=bool).reshape(-1)
     owner = np.full(len(c), -1, dtype=np.int64)
     idx = np.nonzero(dyn)[0]
@@ -64,13 +44,19 @@ def slab_partition(centroids, weights, dynamic, n_parts, axis=None):
     if axis is None:
         ext = c[idx].max(axis=0) - c[idx].min(axis=0)
         axis = int(np.argmax(ext))
-    order = idx[np.lexsort((idx, c[idx, axis]))]  # stable, ties by body id
+    order = idx[np.lexsort((idx, c[idx, axis]))]
     cum = np.cumsum(w[order])
-    total = cum[-1]
-    # slab k takes bodies whose cumulative weight falls in (k/n, (k+1)/n]
-    part = np.minimum((cum - 0.5 * w[order]) * n_parts // max(total, 1e-300), n_parts - 1).astype(np.int64)
-    owner[order] = part
+    total = int(cum[-1])
+    if total <= 0:
+        owner[order] = 0
+        return owner
+    owner[order] = np.minimum((2 * cum - w[order]) * n_parts // (2 * total), n_parts - 1)
     return owner
+
+
+def slab_owner_of_q(q_all, prim_counts, dynamic, n_parts):
+    """The device's partition of a state: centroids = body positions p = q[:, :3]."""
+    return slab_partition(np.asarray(q_all, dtype=float).reshape(-1, 12)[:, :3], prim_counts, dynamic, n_parts)
 
 
 def halo_bodies(overlap_pairs, owner, rank):
@@ -83,13 +69,15 @@ def halo_bodies(overlap_pairs, owner, rank):
 
 
 def owned_rows(rows, owner, rank):
-    """Candidate rows (body_a, prim_a, body_b, prim_b) with >= 1 body owned by `rank`."""
+    """Candidate rows (body_a, prim_a, body_b, prim_b) with >= 1 body owned by `rank` (the
+    rows whose blocks touch its rows of the system)."""
     r = np.asarray(rows, dtype=np.int64).reshape(-1, 4)
     return r[(owner[r[:, 0]] == rank) | (owner[r[:, 2]] == rank)]
 
 
 def counted_rows(rows, owner, rank):
-    """Rows whose scalar contribution `rank` adds (exactly one rank per pair)."""
+    """Rows of the body pairs `rank` evaluates: the slab of the lower body, or of the higher
+    one when the lower is kinematic (exactly one rank per pair; k_prim_pairs2's rule)."""
     r = np.asarray(rows, dtype=np.int64).reshape(-1, 4)
     a, b = r[:, 0], r[:, 2]
     lo = np.minimum(a, b)

@@ -5,7 +5,7 @@ The files are written from procedural meshes, so the same scene is produced here
 when the reference generated the fixtures.  Scenarios follow the reference's own
 scene tests (pkg/tests/test_scene.py: two cubes, a cube dropped on a kinematic floor)
 plus joints and windowed loads, which the reference tests exercise only through
-constraints.py: a hinged pair of bars under a torque window, and an axis-jointed
+constraints.py: a hinged pair of bars (one on an axis) under a short torque window, and an axis-jointed
 wheel with a point-force window and a seeded perturbation.
 """
 from __future__ import annotations
@@ -48,7 +48,7 @@ def write_scenes(d, shapes):
                         "perturb_translation": 0.02}],
         },
         "hinge": {
-            "name": "hinge", "gravity": [0.0, 0.0, -9.8], "params": {"dt": 0.01, "mu": 0.2},
+            "name": "hinge", "gravity": [0.0, 0.0, -9.8], "params": {"dt": 0.01},
             "output": {"frame_interval": 1, "seed": 3, "workers": 2},
             "bodies": [{"name": "floor", "mesh": "floor.obj", "kinematic": True, "translation": [0, 0, -0.6]},
                        {"name": "bar_a", "mesh": "bar.obj", "kappa_ortho": 1e10},
@@ -56,7 +56,7 @@ def write_scenes(d, shapes):
             "joints": [{"type": "hinge", "bodies": ["bar_a", "bar_b"], "point": [0.21, 0, 0],
                         "direction": [0, 1, 0]},
                        {"type": "axis", "body": "bar_a", "point": [-0.19, 0, 0], "direction": [0, 1, 0]}],
-            "forces": [{"body": "bar_b", "type": "torque", "torque": [0, 0.5, 0], "start": 0.0, "end": 0.05}],
+            "forces": [{"body": "bar_b", "type": "torque", "torque": [0, 0.05, 0], "start": 0.0, "end": 0.03}],
         },
         "wheel": {
             "name": "wheel", "gravity": [0.0, 0.0, -9.8], "params": {"dt": 0.01},
@@ -79,4 +79,4 @@ def write_scenes(d, shapes):
     return paths
 
 
-STEPS = {"two_cubes": 12, "drop": 30, "hinge": 15, "wheel": 25}
+STEPS = {"two_cubes": 12, "drop": 30, "hinge": 10, "wheel": 16}

@@ -358,7 +358,7 @@ def test_box_stack_trajectory(golden):
             assert st.min_distance == pytest.approx(g["min_distance"][s], rel=1e-6)
             assert st.ip_value == pytest.approx(g["ip_value"][s], rel=1e-6, abs=1e-12)
             iters.append(st.iterations)
-    assert sum(iters) == pytest.approx(int(g["iterations"].sum()), rel=0.05)
+    assert iters == [int(x) for x in g["iterations"]]  # the reference's Newton count, step by step
 
 
 def test_ico_pile_trajectory(golden):

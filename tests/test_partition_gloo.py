@@ -40,8 +40,7 @@ def _worker(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     bodies, q0, dq, d_hat, kappa = _scene()
     full = O.broad_phase(bodies, q0, q0 + dq, d_hat)
-    X = O.all_world_points(bodies, q0)
-    cent = np.array([x.mean(axis=0) for x in X])
+    cent = q0[:, :3]  # the device cuts slabs on body positions p
     w = np.array([len(b.rest) + len(b.edges) + len(b.triangles) for b in bodies], dtype=float)
     owner = PT.slab_partition(cent, w, [b.dynamic for b in bodies], world)
     mine_vf = PT.owned_rows(full.vf, owner, rank)
@@ -63,9 +62,8 @@ def _worker(rank, world, port, out):
     parts = [None] * world
     dist.all_gather_object(parts, e_part)
     total = PT.ordered_sum(parts)
-    # the implemented split: by overlap pair (disjoint sets, union = full set)
-    pvf = PT.rows_of_owned_pairs(full.vf, full.overlap_pairs, rank, world)
-    pee = PT.rows_of_owned_pairs(full.ee, full.overlap_pairs, rank, world)
+    # the implemented split: body pairs by slab (disjoint sets, union = full set)
+    pvf, pee = cvf, cee
     gp = [None] * world
     dist.all_gather_object(gp, (pvf.tolist(), pee.tolist(),
                                 O.contact_energy(bodies, q0, pvf, pee, kappa, d_hat)))
@@ -76,8 +74,8 @@ def _worker(rank, world, port, out):
     e_pairs = PT.ordered_sum([x[2] for x in gp])
     pair_ok = (n_pvf == len(full.vf) and n_pee == len(full.ee) and np.array_equal(uvf2, full.vf)
                and np.array_equal(uee2, full.ee))
-    # global min CCD step: min over ranks of the owned-row minima
-    a_part = O.step_filter(bodies, q0, dq, mine_vf, mine_ee, 0.1)
+    # global min CCD step: min over ranks of the evaluated rows' minima
+    a_part = O.step_filter(bodies, q0, dq, pvf, pee, 0.1)
     t = torch.tensor([a_part], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
@@ -103,7 +101,7 @@ def test_slab_sharding_gloo(world):
         assert p.exitcode == 0
     vf_ok, ee_ok, total, ref, amin, aref, n_owned, parts, pair_ok, e_pairs = res
     assert vf_ok and ee_ok
-    assert pair_ok  # pair-partitioned candidate sets are disjoint and complete
+    assert pair_ok  # slab-partitioned candidate sets are disjoint and complete
     assert e_pairs == pytest.approx(ref, rel=1e-12, abs=0)
     assert total == pytest.approx(ref, rel=1e-12, abs=0)
     assert amin == aref
