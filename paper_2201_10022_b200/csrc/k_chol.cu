@@ -56,7 +56,7 @@ constexpr int CH_MAX_GRID = 128;        // task-graph CTAs: the graph's width, n
 // whose elimination tree is ~60 levels deep).  Isolated nodes (no coupling) are
 // independent factor + solve tasks handed out by a second counter.
 struct CholView {
-  int n, n_coupled, n_leaves, n_iso, n_tasks;  // n_tasks = 2 n_coupled + off-diagonal blocks
+  int n, n_coupled, n_leaves, n_iso, n_tasks;  // factor-mode tasks: partials + off-diagonal blocks + n_coupled
   const int* leaves;    // coupled nodes with no elimination-tree child, deepest first
   const int* iso;       // isolated nodes
   const int* parent;    // elimination-tree parent (node id) or -1
@@ -81,10 +81,23 @@ struct CholView {
   int* bad;
   int* dep;             // n: remaining children (reset per launch)
   int* bleft;           // n: remaining off-diagonal block tasks of each column
-  int* queue;           // n_tasks slots: j (diagonal), n + j (backward), 2n + b (block); -1 = not yet pushed
+  int* queue;           // task slots (item ids, see k_chol_sched); -1 = not yet pushed
   unsigned* ctr;        // [0] pop head, [1] push tail, [2] unused, [3] tasks done
   unsigned long long* trace;  // optional (ABD_CHOL_TRACE_TASKS): per popped slot (item, t_pop, t_start, t_end)
+  // factor mode: the products of a heavy diagonal / block task are split into
+  // partial tasks (fixed chunks, summed in chunk order by the finalizing warp)
+  int n_part, n_init;   // partial tasks; initially ready partials (the leaves')
+  const int* part_ptr;  // n + 1: partials of node j (its diagonal's, then its column blocks')
+  const int4* part;     // per partial: (0 diagonal / 1 block, node / block, lo, hi) product range
+  const int* dnp;       // n: diagonal partials of node j (1 = unsplit chol_diag)
+  const int* bpart;     // per off block: its first partial
+  const int* bnp;       // per off block: its partial count (>= 1)
+  const int* init;      // n_init: partials of the leaves, deepest leaves first
+  double* scratch;      // n_part x PART_STRIDE partial sums
+  int* dleft;           // n: remaining diagonal partials
+  int* bgate;           // per off block: remaining partials + 1 (the column's diagonal)
 };
+constexpr int PART_STRIDE = 156;  // 12 x 13 (the forward-substitution column rides along)
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -295,6 +308,24 @@ __device__ __forceinline__ void acc_store(const Acc& a, const double* base, cons
       }
 }
 
+// g[r][c] (12 x 13, row-major) = the accumulator (column 12: the ycol products)
+__device__ __forceinline__ void acc_store_raw(const Acc& a, double* g, int lane) {
+  const int r = lane >> 2, c2 = 2 * (lane & 3);
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 8 * mi + r, col = 8 * ni + c2 + e;
+        if (row < 12 && col < 13) g[row * 13 + col] = a.c[0][mi][ni][e] + a.c[1][mi][ni][e] + a.c[2][mi][ni][e];
+      }
+}
+
+struct WarpSmem;
+__device__ __forceinline__ void diag_finish(const CholView& v, int j, double* x, WarpSmem& sm);
+__device__ __forceinline__ void block_finish(const CholView& v, int bb, WarpSmem& sm);
+
 // Diagonal task of node j.  factor: D = A_jj - sum_k L_jk L_jk^T over the row list
 // (fixed order), L_jj = chol(0.5 (D + D^T)), y_j = L_jj^-1 (b_j - sum_k L_jk y_k).
 // !factor: y_j only, with the resident factor.
@@ -351,9 +382,17 @@ __device__ __forceinline__ void chol_diag(const CholView& v, int j, const double
   }
   cp_wait_all();
   __syncwarp(mask);
-  double (*S)[13] = sm.S;
-  acc_store(ac, sm.pa, sm.pv, S, t);
+  acc_store(ac, sm.pa, sm.pv, sm.S, t);
   __syncwarp(mask);
+  diag_finish(v, j, x, sm);
+}
+
+// D (+ the right-hand side in column 12) in sm.S -> L_jj, 1 / L_jj[c][c], y_j
+__device__ __forceinline__ void diag_finish(const CholView& v, int j, double* x, WarpSmem& sm) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  const unsigned mask = 0xffffffffu;
+  double d[12], rinv[12];
+  double (*S)[13] = sm.S;
   // symmetrise (sparse.py:117: cholesky(0.5 (D + D^T)))
 #pragma unroll
   for (int c = 0; c < 12; ++c) d[c] = 0.5 * (S[tt][c] + S[c][tt]);
@@ -409,9 +448,16 @@ __device__ __forceinline__ void chol_block(const CholView& v, int bb, WarpSmem& 
   }
   cp_wait_all();
   __syncwarp(mask);
-  double (*S)[13] = sm.S;
-  acc_store(ac, ap >= 0 ? sm.pa : nullptr, nullptr, S, t);
+  acc_store(ac, ap >= 0 ? sm.pa : nullptr, nullptr, sm.S, t);
   __syncwarp(mask);
+  block_finish(v, bb, sm);
+}
+
+// S = A_ij - sum (in sm.S), L_jj in sm.pl, 1 / L_jj[c][c] in sm.pv: L_ij = S L_jj^-T
+__device__ __forceinline__ void block_finish(const CholView& v, int bb, WarpSmem& sm) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  const unsigned mask = 0xffffffffu;
+  double (*S)[13] = sm.S;
   double bt[12], rinv[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) {
@@ -435,6 +481,99 @@ __device__ __forceinline__ void chol_block(const CholView& v, int bb, WarpSmem& 
 #pragma unroll
     for (int c = 0; c < 12; ++c) Lo[c] = xr[c];
   }
+}
+
+// Partial of a split diagonal task: -sum over row entries [lo, hi) of L_jk L_jk^T
+// (and -sum L_jk y_k in column 12) into out (12 x 13).
+__device__ __forceinline__ void chol_diag_part(const CholView& v, int lo, int hi, const double* x, double* out,
+                                               WarpSmem& sm) {
+  const int t = threadIdx.x & 31;
+  const unsigned mask = 0xffffffffu;
+  const int U = hi - lo;
+  auto issue = [&](int u) {
+    const int e = lo + u;
+    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)v.row_blk[e], t);
+    if (t < 6) cp16(sm.vec[u % NST] + 2 * t, x + 12 * (int64_t)v.row_col[e] + 2 * t);
+  };
+  for (int p = 0; p < NST - 1; ++p) {
+    if (p < U) issue(p);
+    cp_commit();
+  }
+  Acc ac;
+  acc_zero(ac);
+  for (int u = 0; u < U; ++u) {
+    cp_wait_pipe();
+    __syncwarp(mask);
+    const double* Lk = sm.stage[u % NST][0];
+    acc_sub_xyt(ac, Lk, Lk, sm.vec[u % NST], t);
+    __syncwarp(mask);
+    if (u + NST - 1 < U) issue(u + NST - 1);
+    cp_commit();
+  }
+  cp_wait_all();
+  __syncwarp(mask);
+  acc_store_raw(ac, out, t);
+}
+
+// Partial of a split block task: -sum over update pairs [lo, hi) of L_ik L_jk^T into out.
+__device__ __forceinline__ void chol_block_part(const CholView& v, int lo, int hi, double* out, WarpSmem& sm) {
+  const int t = threadIdx.x & 31;
+  const unsigned mask = 0xffffffffu;
+  const int U = hi - lo;
+  auto issue = [&](int u) {
+    const int2 pq = v.upd[lo + u];
+    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)pq.x, t);  // L_ik
+    stage_block(sm.stage[u % NST][1], v.L + 144 * (int64_t)pq.y, t);  // L_jk
+  };
+  for (int p = 0; p < NST - 1; ++p) {
+    if (p < U) issue(p);
+    cp_commit();
+  }
+  Acc ac;
+  acc_zero(ac);
+  for (int u = 0; u < U; ++u) {
+    cp_wait_pipe();
+    __syncwarp(mask);
+    acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][1], nullptr, t);
+    __syncwarp(mask);
+    if (u + NST - 1 < U) issue(u + NST - 1);
+    cp_commit();
+  }
+  cp_wait_all();
+  __syncwarp(mask);
+  acc_store_raw(ac, out, t);
+}
+
+// sm.S (12 x 13) = base + the partials p0 .. p0 + np - 1 in order (written by other warps)
+__device__ __forceinline__ void sum_partials(const CholView& v, const double* base, const double* vbase, int p0, int np,
+                                             WarpSmem& sm) {
+  const int t = threadIdx.x & 31;
+  for (int e = t; e < PART_STRIDE; e += 32) {
+    const int r = e / 13, c = e % 13;
+    double a = c < 12 ? (base ? base[12 * r + c] : 0.0) : (vbase ? vbase[r] : 0.0);
+    for (int q = 0; q < np; ++q) a += __ldcg(v.scratch + (int64_t)(p0 + q) * PART_STRIDE + e);
+    sm.S[r][c] = a;
+  }
+  __syncwarp();
+}
+
+// The last partial of a split diagonal: D = A_jj + partials, b_j + partials -> diag_finish.
+__device__ __forceinline__ void chol_diag_final(const CholView& v, int j, int p0, int np, const double* b, double* x,
+                                                WarpSmem& sm) {
+  sum_partials(v, v.val + 144 * (int64_t)v.diag_pos[j], b + 12 * (int64_t)j, p0, np, sm);
+  diag_finish(v, j, x, sm);
+}
+
+// The last of a block's partials and its column's diagonal: S = A_ij + partials,
+// L_ij = S L_jj^-T.
+__device__ __forceinline__ void chol_block_final(const CholView& v, int bb, WarpSmem& sm) {
+  const int t = threadIdx.x & 31;
+  const int j = v.blk_col[bb];
+  for (int e = t; e < 144; e += 32) sm.pl[e] = __ldcg(v.L + 144 * (int64_t)j + e);
+  if (t < 12) sm.pv[t] = __ldcg(v.dinv + 12 * (int64_t)j + t);
+  const int ap = v.apos[bb];
+  sum_partials(v, ap >= 0 ? v.val + 144 * (int64_t)ap : nullptr, nullptr, v.bpart[bb], v.bnp[bb], sm);
+  block_finish(v, bb, sm);
 }
 
 // Backward task of node j: x_j = L_jj^-T (y_j - sum_i L_ij^T x_i) over its column.
@@ -519,14 +658,21 @@ __device__ __forceinline__ void chol_isolated(const CholView& v, int j, const do
   if (t < 12) x[12 * (int64_t)j + t] = xv;
 }
 
-__global__ void k_chol_sched_init(CholView v) {
+__global__ void k_chol_sched_init(CholView v, int factor) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nbo = v.col_ptr[v.n];
   if (i < v.n) {
     v.dep[i] = v.nchild[i];
     v.bleft[i] = v.col_ptr[i + 1] - v.col_ptr[i];
+    if (factor) v.dleft[i] = v.dnp[i];
   }
-  if (i < v.n_tasks) v.queue[i] = i < v.n_leaves ? v.leaves[i] : -1;
-  if (i < 4) v.ctr[i] = i == 1 ? (unsigned)v.n_leaves : 0u;
+  if (factor && i < nbo) v.bgate[i] = v.bnp[i] + 1;
+  if (factor) {
+    if (i < v.n_tasks) v.queue[i] = i < v.n_init ? v.init[i] : -1;
+  } else if (i < 2 * v.n_coupled) {
+    v.queue[i] = i < v.n_leaves ? v.leaves[i] : -1;
+  }
+  if (i < 4) v.ctr[i] = i == 1 ? (unsigned)(factor ? v.n_init : v.n_leaves) : 0u;
 }
 
 // Isolated nodes (no coupling): one independent factor + solve per warp.
@@ -560,9 +706,67 @@ __device__ __forceinline__ int node_ready(const CholView& v, int j) {
   return atom_dec_acq_rel(v.dep + p) == 1 ? p : -1;
 }
 
+// push items [a, b) except the first, which is returned (the caller's continuation)
+__device__ __forceinline__ int push_rest(const CholView& v, int a, int b) {
+  if (b - a > 1) {
+    const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(b - a - 1));
+    for (int c = a + 1; c < b; ++c) st_release(v.queue + slot + (c - a - 1), c);
+  }
+  return b > a ? a : -1;
+}
+
+// factor mode: node j is complete; the parent's partials when it becomes ready (the
+// first one returned, the others pushed), the backward task at a root, or -1
+__device__ __forceinline__ int node_ready_f(const CholView& v, int j, int bwd0) {
+  const int p = v.parent[j];
+  if (p < 0) return bwd0 + j;
+  if (atom_dec_acq_rel(v.dep + p) != 1) return -1;
+  return push_rest(v, v.part_ptr[p], v.part_ptr[p + 1]);
+}
+
+// factor mode, whole warp: node j's diagonal is final; its unsplit column blocks and
+// the split ones whose partials are all done become ready -- one lane per block, the
+// first returned (warp-uniform), the others pushed with one slot reservation; no
+// blocks: node done
+__device__ __forceinline__ int diag_done_warp(const CholView& v, int j, int bwd0) {
+  const int t = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const int c0 = v.col_ptr[j], c1 = v.col_ptr[j + 1];
+  if (c1 == c0) {
+    int r = -1;
+    if (t == 0) r = node_ready_f(v, j, bwd0);
+    return __shfl_sync(full, r, 0);
+  }
+  int first = -1;
+  for (int base = c0; base < c1; base += 32) {
+    const int c = base + t;
+    bool ready = false;
+    if (c < c1) ready = v.bnp[c] == 0 || atom_dec_acq_rel(v.bgate + c) == 1;
+    unsigned m = __ballot_sync(full, ready);
+    if (!m) continue;
+    if (first < 0) {
+      const int lead = __ffs(m) - 1;
+      first = v.n_part + base + lead;
+      m &= ~(1u << lead);
+    }
+    const int k = __popc(m);
+    unsigned slot = 0;
+    if (t == 0 && k) slot = atomicAdd(v.ctr + 1, (unsigned)k);
+    slot = __shfl_sync(full, slot, 0);
+    if ((m >> t) & 1u) st_release(v.queue + slot + __popc(m & ((1u << t) - 1u)), v.n_part + c);
+  }
+  return first;
+}
+
 // Persistent factor (+ forward / backward substitution) over the task FIFO of the
-// coupled nodes.  Tasks: j < n -> diagonal task of node j; n + j -> backward task
-// of node j; 2n + b -> off-diagonal block task b (factor only).  A warp that makes
+// coupled nodes.  Factor mode: items [0, P) are partial tasks (a diagonal's or a
+// block's products in fixed chunks; an unsplit diagonal runs chol_diag whole), then
+// [P, P + nbo) block finals, then backward tasks.  A node's partials are all
+// released together when its last child completes, so a block's update sum runs
+// beside its column's diagonal; the last of a split task's partials (by atomic
+// count) sums them in chunk order and finishes it: deterministic, whatever the
+// schedule.  Solve mode (refinement, preconditioner): j < n -> forward task of node
+// j, n + j -> backward task.  A warp that makes
 // a task ready runs one of them itself next (continuation: chains of the
 // elimination tree never go through the FIFO) and pushes the others.  A warp that
 // pops a slot not yet pushed polls it with backoff until it is filled or every
@@ -577,6 +781,8 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
   const unsigned mask = 0xffffffffu;
   const bool fac = factor != 0;
   const int total = fac ? v.n_tasks : 2 * v.n_coupled;
+  const int nbo = v.col_ptr[v.n];
+  const int bwd0 = fac ? v.n_part + nbo : v.n;  // first backward item
   constexpr int EXIT = -2;
   int next = -1;  // continuation task (warp-uniform)
   for (;;) {
@@ -610,26 +816,61 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
     }
     const unsigned long long t_start = v.trace ? gtimer() : 0;
     int info = 0;
-    if (item < v.n) {  // diagonal task
+    if (fac && item < v.n_part) {  // partial of a diagonal or block task
+      const int4 pt = v.part[item];
+      if (pt.x == 0) {
+        const int j = pt.y;
+        const int np = v.dnp[j];
+        bool fin = true;
+        if (np == 1) {
+          chol_diag(v, j, b, x, true, sm);
+        } else {
+          chol_diag_part(v, pt.z, pt.w, x, v.scratch + (int64_t)item * PART_STRIDE, sm);
+          fence_acq_rel();
+          __syncwarp(mask);
+          int last = 0;
+          if (t == 0) last = atom_dec_acq_rel(v.dleft + j) == 1;
+          fin = __shfl_sync(mask, last, 0) != 0;
+          if (fin) {
+            fence_acq_rel();
+            chol_diag_final(v, j, v.part_ptr[j], np, b, x, sm);
+          }
+        }
+        if (fin) {
+          fence_acq_rel();
+          __syncwarp(mask);
+          next = diag_done_warp(v, j, bwd0);
+        }
+        info = pt.w - pt.z;
+      } else {
+        const int bb = pt.y;
+        chol_block_part(v, pt.z, pt.w, v.scratch + (int64_t)item * PART_STRIDE, sm);
+        fence_acq_rel();
+        __syncwarp(mask);
+        if (t == 0 && atom_dec_acq_rel(v.bgate + bb) == 1) next = v.n_part + bb;
+        info = pt.w - pt.z;
+      }
+    } else if (fac && item < bwd0) {  // a block after its column's diagonal (and its partials, if split)
+      const int bb = item - v.n_part;
+      if (v.bnp[bb] == 0) chol_block(v, bb, sm);  // unsplit: its update sum and L_jj^-T here
+      else chol_block_final(v, bb, sm);
+      fence_acq_rel();
+      __syncwarp(mask);
+      if (t == 0) {
+        const int j = v.blk_col[bb];
+        if (atom_dec_acq_rel(v.bleft + j) == 1) next = node_ready_f(v, j, bwd0);
+      }
+    } else if (!fac && item < v.n) {  // diagonal task (solve mode: forward substitution only)
       const int j = item;
       chol_diag(v, j, b, x, fac, sm);
       fence_acq_rel();
       __syncwarp(mask);
       if (t == 0) {
         info = v.row_ptr[j + 1] - v.row_ptr[j];
-        const int c0 = v.col_ptr[j], c1 = v.col_ptr[j + 1];
-        if (fac && c1 > c0) {  // run the first block here, the others in parallel
-          if (c1 - c0 > 1) {
-            const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0 - 1));
-            for (int c = c0 + 1; c < c1; ++c) st_release(v.queue + slot + (c - c0 - 1), 2 * v.n + c);
-          }
-          next = 2 * v.n + c0;
-        } else {
-          next = node_ready(v, j);
-        }
+        next = node_ready(v, j);
       }
-    } else if (item < 2 * v.n) {  // backward task
-      const int j = item - v.n;
+    } else {  // backward task
+      const int j = item - bwd0;
       chol_backward(v, j, x);
       fence_acq_rel();
       __syncwarp(mask);
@@ -637,19 +878,9 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
         const int c0 = v.child_ptr[j], c1 = v.child_ptr[j + 1];
         if (c1 - c0 > 1) {
           const unsigned slot = atomicAdd(v.ctr + 1, (unsigned)(c1 - c0 - 1));
-          for (int c = c0 + 1; c < c1; ++c) st_release(v.queue + slot + (c - c0 - 1), v.n + v.child_idx[c]);
+          for (int c = c0 + 1; c < c1; ++c) st_release(v.queue + slot + (c - c0 - 1), bwd0 + v.child_idx[c]);
         }
-        if (c1 > c0) next = v.n + v.child_idx[c0];
-      }
-    } else {  // off-diagonal block task
-      const int bb = item - 2 * v.n;
-      chol_block(v, bb, sm);
-      fence_acq_rel();
-      __syncwarp(mask);
-      if (t == 0) {
-        info = v.upd_ptr[bb + 1] - v.upd_ptr[bb];
-        const int j = v.blk_col[bb];
-        if (atom_dec_acq_rel(v.bleft + j) == 1) next = node_ready(v, j);
+        if (c1 > c0) next = bwd0 + v.child_idx[c0];
       }
     }
     if (t == 0) {
@@ -723,7 +954,10 @@ __global__ void k_add_inplace(int64_t n, double* x, const double* d) {
 
 // Sections of the packed plan buffer
 enum { CH_LEAVES, CH_ISO, CH_PARENT, CH_NCHILD, CH_CHILDP, CH_CHILDI, CH_COLP, CH_BROW, CH_BCOL, CH_ROWP, CH_ROWB,
-       CH_ROWC, CH_UPDP, CH_UPD, CH_NSEC };
+       CH_ROWC, CH_UPDP, CH_UPD, CH_PARTP, CH_PART, CH_DNP, CH_BPART, CH_BNP, CH_INIT, CH_NSEC };
+// task splitting: a diagonal (row products) or block (update pairs) task with more
+// than PART_MIN products is split into chunks of PART_CHUNK
+constexpr int PART_MIN = 12, PART_CHUNK = 8;
 
 static CholView plan_view(Scene& s) {
   Scene::Work& w = s.w;
@@ -732,38 +966,51 @@ static CholView plan_view(Scene& s) {
   const int n = s.H.n;
   const int m = (int)w.ch_cache.stats[1];
   const int nbo = (int)(w.ch_cache.stats[2] - n);
-  return CholView{n,
-                  m,
-                  (int)w.ch_cache.stats[7],
-                  n - m,
-                  2 * m + nbo,
-                  dp + o[CH_LEAVES],
-                  dp + o[CH_ISO],
-                  dp + o[CH_PARENT],
-                  dp + o[CH_NCHILD],
-                  dp + o[CH_CHILDP],
-                  dp + o[CH_CHILDI],
-                  dp + o[CH_COLP],
-                  dp + o[CH_BROW],
-                  dp + o[CH_BCOL],
-                  s.H.row_ptr.p,
-                  s.H.col.p,
-                  w.ch_apos.p,
-                  dp + o[CH_ROWP],
-                  dp + o[CH_ROWB],
-                  dp + o[CH_ROWC],
-                  dp + o[CH_UPDP],
-                  reinterpret_cast<const int2*>(dp + o[CH_UPD]),
-                  s.H.diag_pos.p,
-                  s.H.val.p,
-                  w.ch_L.p,
-                  w.ch_dinv.p,
-                  w.bad.p,
-                  w.ch_dep.p,
-                  w.ch_bleft.p,
-                  w.ch_queue.p,
-                  w.ch_ctr.p,
-                  nullptr};
+  const int n_part = (int)w.ch_cache.stats[8], n_init = (int)w.ch_cache.stats[9];
+  CholView v{n,
+             m,
+             (int)w.ch_cache.stats[7],
+             n - m,
+             n_part + nbo + m,
+             dp + o[CH_LEAVES],
+             dp + o[CH_ISO],
+             dp + o[CH_PARENT],
+             dp + o[CH_NCHILD],
+             dp + o[CH_CHILDP],
+             dp + o[CH_CHILDI],
+             dp + o[CH_COLP],
+             dp + o[CH_BROW],
+             dp + o[CH_BCOL],
+             s.H.row_ptr.p,
+             s.H.col.p,
+             w.ch_apos.p,
+             dp + o[CH_ROWP],
+             dp + o[CH_ROWB],
+             dp + o[CH_ROWC],
+             dp + o[CH_UPDP],
+             reinterpret_cast<const int2*>(dp + o[CH_UPD]),
+             s.H.diag_pos.p,
+             s.H.val.p,
+             w.ch_L.p,
+             w.ch_dinv.p,
+             w.bad.p,
+             w.ch_dep.p,
+             w.ch_bleft.p,
+             w.ch_queue.p,
+             w.ch_ctr.p,
+             nullptr};
+  v.n_part = n_part;
+  v.n_init = n_init;
+  v.part_ptr = dp + o[CH_PARTP];
+  v.part = reinterpret_cast<const int4*>(dp + o[CH_PART]);
+  v.dnp = dp + o[CH_DNP];
+  v.bpart = dp + o[CH_BPART];
+  v.bnp = dp + o[CH_BNP];
+  v.init = dp + o[CH_INIT];
+  v.scratch = w.ch_scratch.p;
+  v.dleft = w.ch_dleft.p;
+  v.bgate = w.ch_bgate.p;
+  return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -1354,16 +1601,36 @@ static Analysis chol_analyze(Scene& s) {
     fprintf(stderr, "[abd chol cp] m=%d core=%d leaves=%d total=%lld maxcost=%lld critpath=%lld maxcol=%d maxrow=%d\n",
             m, n_core, n_leaves, (long long)tot, (long long)maxc, (long long)maxcp, maxcol, maxrow);
   }
+  // split factor tasks: a diagonal with R row products / a block with U update pairs
+  // above PART_MIN becomes ceil(. / PART_CHUNK) partial tasks released with the node
+  // (ABD_CHOL_NO_SPLIT: none).  An unsplit diagonal is one whole task; an unsplit
+  // block (bnp = 0) runs whole after its diagonal, as without splitting.
+  static const bool no_split = getenv("ABD_CHOL_NO_SPLIT") != nullptr;
+  auto nparts = [&](int k) { return (!no_split && k > PART_MIN) ? (k + PART_CHUNK - 1) / PART_CHUNK : 1; };
+  auto bparts = [&](int k) { const int q = nparts(k); return q > 1 ? q : 0; };
+  int64_t n_part = 0, n_init = 0;
+  {
+    std::vector<int> per(m, 0);
+    for (int v = 0; v < m; ++v) {
+      per[v] = nparts(rcnt[v + 1] - rcnt[v]);
+      for (int b2 = csp[v]; b2 < csp[v + 1]; ++b2) per[v] += bparts(upd_ptr[b2 + 1] - upd_ptr[b2]);
+      n_part += per[v];
+    }
+    for (int v : leaves) n_init += per[v];
+  }
   // packed plan: leaves | iso | parent | nchild | child_ptr | child_idx | col_ptr | blk_row |
-  //              row_ptr | row_blk | row_col | upd_ptr | (pad) | upd pairs
+  //              row_ptr | row_blk | row_col | upd_ptr | (pad) | upd pairs | part_ptr | (pad) |
+  //              part (int4) | dnp | bpart | bnp | init
   size_t o[CH_NSEC + 1];
   o[0] = 0;
   const size_t len[CH_NSEC] = {(size_t)n_leaves, (size_t)n_iso, (size_t)n, (size_t)n, (size_t)n + 1, (size_t)m,
                                (size_t)n + 1, (size_t)nbo, (size_t)nbo, (size_t)n + 1, (size_t)nbo, (size_t)nbo,
-                               (size_t)nbo + 1, upd.size()};
+                               (size_t)nbo + 1, upd.size(), (size_t)n + 1, 4 * (size_t)n_part, (size_t)n,
+                               (size_t)nbo, (size_t)nbo, (size_t)n_init};
   for (int k = 0; k < CH_NSEC; ++k) {
     o[k + 1] = o[k] + len[k];
-    if (k + 1 == CH_UPD) o[k + 1] += o[k + 1] & 1;  // int2 alignment of the update pairs
+    if (k + 1 == CH_UPD) o[k + 1] += o[k + 1] & 1;          // int2 alignment of the update pairs
+    if (k + 1 == CH_PART) o[k + 1] = (o[k + 1] + 3) & ~(size_t)3;  // int4 alignment of the partials
   }
   const size_t total = o[CH_NSEC] + 2;
   int* hp = w.h_plan.reserve(total);
@@ -1414,6 +1681,49 @@ static Analysis chol_analyze(Scene& s) {
     col_ptr[n] = c;
     row_ptr[n] = r;
   }
+  {
+    // partial tasks per global node: its diagonal's chunks of the row list, then each
+    // column block's chunks of its update pairs (equal splits)
+    int* partp = hp + o[CH_PARTP];
+    int* part = hp + o[CH_PART];
+    int* dnp = hp + o[CH_DNP];
+    int* bpart = hp + o[CH_BPART];
+    int* bnp = hp + o[CH_BNP];
+    int pc = 0;
+    for (int v = 0; v < n; ++v) {
+      partp[v] = pc;
+      dnp[v] = 0;
+      if (loc[v] < 0) continue;
+      const int r0 = row_ptr[v], R = row_ptr[v + 1] - r0;
+      const int d = nparts(R);
+      dnp[v] = d;
+      for (int q = 0; q < d; ++q, ++pc) {
+        part[4 * pc] = 0;
+        part[4 * pc + 1] = v;
+        part[4 * pc + 2] = r0 + (int)((int64_t)R * q / d);
+        part[4 * pc + 3] = r0 + (int)((int64_t)R * (q + 1) / d);
+      }
+      for (int b = col_ptr[v]; b < col_ptr[v + 1]; ++b) {
+        const int u0 = upd_ptr[b], U = upd_ptr[b + 1] - u0;
+        const int nb = bparts(U);
+        bpart[b] = pc;
+        bnp[b] = nb;
+        for (int q = 0; q < nb; ++q, ++pc) {
+          part[4 * pc] = 1;
+          part[4 * pc + 1] = b;
+          part[4 * pc + 2] = u0 + (int)((int64_t)U * q / nb);
+          part[4 * pc + 3] = u0 + (int)((int64_t)U * (q + 1) / nb);
+        }
+      }
+    }
+    partp[n] = pc;
+    int* init = hp + o[CH_INIT];
+    int k = 0;
+    for (int i = 0; i < n_leaves; ++i) {
+      const int g = glob[leaves[i]];
+      for (int p2 = partp[g]; p2 < partp[g + 1]; ++p2) init[k++] = p2;
+    }
+  }
   an.ms_sub[5] = ms_since(t0);
   std::copy(upd_ptr.begin(), upd_ptr.end(), hp + o[CH_UPDP]);
   std::copy(upd.begin(), upd.end(), hp + o[CH_UPD]);
@@ -1424,15 +1734,18 @@ static Analysis chol_analyze(Scene& s) {
   w.ch_apos.resize(std::max<int64_t>(an.n_blk - n, 1));
   w.ch_dep.resize(std::max(n, 1));
   w.ch_bleft.resize(std::max(n, 1));
-  w.ch_queue.resize(std::max(2 * m + nbo, 1));
+  w.ch_queue.resize(std::max<int64_t>(std::max<int64_t>(2 * m, n_part + nbo + m), 1));
   w.ch_ctr.resize(4);
+  w.ch_dleft.resize(std::max(n, 1));
+  w.ch_bgate.resize(std::max(nbo, 1));
+  w.ch_scratch.resize(std::max<int64_t>(n_part, 1) * PART_STRIDE);
   cc.valid = true;
   cc.n = n;
   cc.n_off = n_off;
   cc.edges.swap(cur);
-  const int64_t st8[8] = {an.n_cta, an.n_coupled, an.n_blk, an.n_upd, an.n_edges, an.max_level, an.largest,
-                          n_leaves};
-  std::copy(st8, st8 + 8, cc.stats);
+  const int64_t st10[10] = {an.n_cta, an.n_coupled, an.n_blk, an.n_upd, an.n_edges, an.max_level, an.largest,
+                            n_leaves, n_part, n_init};
+  std::copy(st10, st10 + 10, cc.stats);
   std::copy(o, o + CH_NSEC + 1, cc.offs);
   an.view = plan_view(s);
   an.ms_plan = ms_since(t0);
@@ -1459,8 +1772,8 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_chol_sched, CH_THREADS, smem));
     bps = std::max(bps, 1);
   }
-  const int init_n = std::max(v.n, v.n_tasks);
-  k_chol_sched_init<<<grid_for(std::max(init_n, 4), 256), 256, 0, st>>>(v);
+  const int init_n = std::max(std::max(v.n, v.n_tasks), std::max(2 * v.n_coupled, v.n_tasks - v.n_part));
+  k_chol_sched_init<<<grid_for(std::max(init_n, 4), 256), 256, 0, st>>>(v, factor ? 1 : 0);
   note_launch("k_chol_sched_init");
   // isolated nodes on a side stream beside the task graph (joined before returning)
   if (v.n_iso > 0) {

@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
                                                          const int4* __restrict__ rows, const double* __restrict__ q,
                                                          double kappa, double dh, int project, int64_t slot_off,
                                                          int2* out_bodies, double* out_blk, double* out_d2,
-                                                         int* moll_list, int* moll_count) {
+                                                         int* moll_list, int* moll_count,
+                                                         const unsigned char* __restrict__ moll_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= count) return;
   (void)kind_unused;
@@ -164,7 +165,9 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
   V3 z[4], xb[4];
   pair_points(sv, ids, q, z, xb);
   out_bodies[slot] = make_int2(r.x, r.z);
-  if (KIND == KIND_EE && ee_mollified(z, ids.eps)) {
+  // mollified EE pairs belong to k_pair_blocks_moll: the predicate comes from
+  // k_moll_classify's flag when it ran (evaluated once), else it is evaluated here
+  if (KIND == KIND_EE && (moll_flag ? moll_flag[t] != 0 : ee_mollified(z, ids.eps))) {
     if (moll_list) moll_list[atomicAdd(moll_count, 1)] = (int)slot;
     return;
   }
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
 // (slower) 9-column records build on a side stream beside the plain EE pairs
 __global__ void k_moll_classify(SceneView sv, int64_t count, const int* __restrict__ act, int64_t cand_off,
                                 const int4* __restrict__ rows, const double* __restrict__ q, int64_t slot_off,
-                                int* moll_list, int* moll_count) {
+                                int* moll_list, int* moll_count, unsigned char* moll_flag) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= count) return;
   const int64_t slot = slot_off + t;
@@ -186,7 +189,9 @@ __global__ void k_moll_classify(SceneView sv, int64_t count, const int* __restri
   PairIds ids = pair_ids(sv, KIND_EE, r);
   V3 z[4], xb[4];
   pair_points(sv, ids, q, z, xb);
-  if (ee_mollified(z, ids.eps)) moll_list[atomicAdd(moll_count, 1)] = (int)slot;
+  const bool m = ee_mollified(z, ids.eps);
+  moll_flag[t] = m ? 1 : 0;
+  if (m) moll_list[atomicAdd(moll_count, 1)] = (int)slot;
 }
 
 // Warp-parallel PSD clamp of a symmetric 9x9 (padded to 10) in shared memory:
@@ -885,7 +890,8 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
   if (kind == KIND_VF) {
     k_pair_blocks_act<KIND_VF><<<grid_for(count, 64), 64, 0, s.stream>>>(view(s), kind, count, act, cand_off, rows, q,
                                                                         kappa, dh, project, slot_off, s.pblk.bodies.p,
-                                                                        s.pblk.blk.p, s.pblk.d2.p, nullptr, nullptr);
+                                                                        s.pblk.blk.p, s.pblk.d2.p, nullptr, nullptr,
+                                                                        nullptr);
   } else {
     s.w.moll.resize(std::max<int64_t>(count, 1));
     CK(cudaMemsetAsync(moll_count, 0, sizeof(int), s.stream));
@@ -894,14 +900,15 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
     if (serial) {
       k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(
           view(s), kind, count, act, cand_off, rows, q, kappa, dh, project, slot_off, s.pblk.bodies.p, s.pblk.blk.p,
-          s.pblk.d2.p, s.w.moll.p, moll_count);
+          s.pblk.d2.p, s.w.moll.p, moll_count, nullptr);
       k_pair_blocks_moll<<<grid, 32 * MOLL_WARPS, 0, s.stream>>>(view(s), s.w.moll.p, moll_count, act, cand_off,
                                                                  rows, q, kappa, dh, project, s.pblk.blk.p,
                                                                  s.pblk.d2.p);
     } else {
       // list the mollified slots, build them on side3 while the plain EE pairs run here
+      s.w.moll_flag.resize(std::max<int64_t>(count, 1));
       k_moll_classify<<<grid_for(count, 256), 256, 0, s.stream>>>(view(s), count, act, cand_off, rows, q, slot_off,
-                                                                  s.w.moll.p, moll_count);
+                                                                  s.w.moll.p, moll_count, s.w.moll_flag.p);
       note_launch("k_moll_classify");
       CK(cudaEventRecord(s.moll_fork_ev, s.stream));
       CK(cudaStreamWaitEvent(s.side3, s.moll_fork_ev, 0));
@@ -911,7 +918,7 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
       CK(cudaEventRecord(s.moll_ev, s.side3));
       k_pair_blocks_act<KIND_EE><<<grid_for(count, 64), 64, 0, s.stream>>>(
           view(s), kind, count, act, cand_off, rows, q, kappa, dh, project, slot_off, s.pblk.bodies.p, s.pblk.blk.p,
-          s.pblk.d2.p, nullptr, nullptr);
+          s.pblk.d2.p, nullptr, nullptr, s.w.moll_flag.p);
       CK(cudaStreamWaitEvent(s.stream, s.moll_ev, 0));
     }
     note_launch("k_pair_blocks_moll");

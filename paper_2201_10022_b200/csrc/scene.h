@@ -244,6 +244,7 @@ struct Scene {
     DVec<int64_t> comm_cnt, comm_buf, fric_keys, fric_keys_all;  // multi-GPU scratch
     DVec<int> act;      // compacted active candidate indices (VF then EE)
     DVec<int> moll;     // active EE slots with an active mollifier (deferred 9-column path)
+    DVec<unsigned char> moll_flag;  // per active EE slot: mollified (k_moll_classify, read by k_pair_blocks_act)
     int64_t n_act_vf = 0;
     DVec<int> flags, pos, err, order, cnt, off, seg_s, seg_e, row_of, nsel, bad, iters;
     DVec<uint64_t> k0, k1, e0, e1;
@@ -287,7 +288,8 @@ struct Scene {
     DVec<long long> cl_slot_off, cl_minv;
     DVec<double> minv;
     // sparse block Cholesky plan (one packed int buffer) and factor (k_chol.cu)
-    DVec<int> ch_flags, ch_plan, ch_apos, ch_dep, ch_bleft, ch_queue;
+    DVec<int> ch_flags, ch_plan, ch_apos, ch_dep, ch_bleft, ch_queue, ch_dleft, ch_bgate;
+    DVec<double> ch_scratch;  // partial sums of split factor tasks
     DVec<unsigned> ch_ctr;
     DVec<double> ch_L, ch_dinv;
     HostPinned<int> h_plan, h_meta;
@@ -298,8 +300,8 @@ struct Scene {
       int n = 0;
       int64_t n_off = 0;
       std::vector<uint64_t> edges;  // (i << 32 | j) nonzero couplings the plan was built for
-      int64_t stats[8] = {};
-      size_t offs[16] = {};
+      int64_t stats[12] = {};
+      size_t offs[32] = {};
       int64_t hits = 0, misses = 0;
       std::vector<int> gorder;  // elimination order (global ids) of the step's last fresh ordering
       int64_t fresh_nnz = 0;    // its off-diagonal factor blocks
