@@ -1805,8 +1805,8 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     tbuf.download(h.data(), h.size(), st);
     SSYNC(st);
     if (FILE* f = fopen(trace_path, "ab")) {
-      const int hdr[4] = {v.n, v.n_coupled, v.n_tasks, grid};
-      fwrite(hdr, sizeof(int), 4, f);
+      const int hdr[6] = {v.n, v.n_coupled, v.n_tasks, grid, v.n_part, v.n_tasks - v.n_part - v.n_coupled};
+      fwrite(hdr, sizeof(int), 6, f);
       fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
       fclose(f);
     }

@@ -1,0 +1,68 @@
+"""Per-task timeline of Cholesky factorizations (ABD_CHOL_TRACE_TASKS=file): task-type
+durations, concurrency profile and the waiting between a task becoming poppable and
+starting.  Usage: python tools/chol_task_trace.py TRACE.bin [which factorization, default last]"""
+import struct
+import sys
+
+import numpy as np
+
+
+def load(path):
+    data = open(path, "rb").read()
+    out, off = [], 0
+    while off < len(data):
+        n, m, nt, grid, npart, nbo = struct.unpack_from("6i", data, off)
+        off += 24
+        rec = np.frombuffer(data, dtype=np.uint64, count=4 * nt, offset=off).reshape(nt, 4)
+        off += 32 * nt
+        out.append((n, m, nt, grid, npart, nbo, rec))
+    return out
+
+
+def main():
+    facs = load(sys.argv[1])
+    k = int(sys.argv[2]) if len(sys.argv) > 2 else -1
+    n, m, nt, grid, npart, nbo, rec = facs[k]
+    rec = rec[rec[:, 3] > 0]
+    item = (rec[:, 0] & 0xffffffff).astype(np.int64)
+    info = (rec[:, 0] >> 32).astype(np.int64)
+    tpop, ts, te = rec[:, 1].astype(np.int64), rec[:, 2].astype(np.int64), rec[:, 3].astype(np.int64)
+    t0 = ts.min()
+    kind = np.where(item < npart, 0, np.where(item < npart + nbo, 1, 2))
+    names = ["partial/diag", "block", "backward"]
+    print(f"{len(facs)} factorizations; this one: n={n} coupled={m} tasks={nt} (partials {npart}, blocks {nbo}) "
+          f"grid={grid} CTAs, span {(te.max() - t0) / 1e3:.1f} us, busy {(te - ts).sum() / 1e3:.1f} warp-us")
+    for kk in range(3):
+        sel = kind == kk
+        d = (te - ts)[sel]
+        if sel.any():
+            print(f"  {names[kk]:14s} n={sel.sum():6d} mean {d.mean() / 1e3:6.2f} us  p90 {np.percentile(d, 90) / 1e3:6.2f}"
+                  f"  max {d.max() / 1e3:6.2f}  total {d.sum() / 1e3:8.1f} us  info mean {info[sel].mean():.1f} max {info[sel].max()}")
+    # factor phase end = last non-backward end
+    fend = te[kind < 2].max()
+    print(f"  factor phase {(fend - t0) / 1e3:.1f} us, backward phase {(te.max() - fend) / 1e3:.1f} us")
+    # concurrency profile in 10 us bins
+    bins = np.arange(t0, te.max() + 10000, 10000)
+    conc = np.zeros(len(bins) - 1)
+    for a, b in zip(ts, te):
+        i0, i1 = np.searchsorted(bins, a, "right") - 1, np.searchsorted(bins, b, "right") - 1
+        for i in range(max(i0, 0), min(i1, len(conc) - 1) + 1):
+            lo, hi = max(a, bins[i]), min(b, bins[i + 1])
+            if hi > lo:
+                conc[i] += (hi - lo) / 10000
+    print("  mean running tasks per 10 us bin:", " ".join(f"{c:.1f}" for c in conc))
+    # popped-but-waiting (polled a slot before it was filled) vs continuation
+    wait = ts - tpop
+    print(f"  pop->start wait: mean {wait.mean() / 1e3:.2f} us, p90 {np.percentile(wait, 90) / 1e3:.2f} us "
+          f"(0 for continuations: {np.mean(wait == 0) * 100:.0f}% of tasks)")
+    # tasks in the low-concurrency tail (last 30% of the factor phase)
+    tail = (ts > t0 + 0.7 * (fend - t0)) & (kind < 2)
+    for kk in range(2):
+        sel = tail & (kind == kk)
+        if sel.any():
+            d = (te - ts)[sel]
+            print(f"  tail {names[kk]:14s} n={sel.sum():5d} mean {d.mean() / 1e3:6.2f} us, info mean {info[sel].mean():.1f}")
+
+
+if __name__ == "__main__":
+    main()
