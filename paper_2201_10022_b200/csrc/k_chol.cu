@@ -577,25 +577,45 @@ __device__ __forceinline__ void chol_block_final(const CholView& v, int bb, Warp
 }
 
 // Backward task of node j: x_j = L_jj^-T (y_j - sum_i L_ij^T x_i) over its column.
-__device__ __forceinline__ void chol_backward(const CholView& v, int j, double* x) {
+__device__ __forceinline__ void chol_backward(const CholView& v, int j, double* x, WarpSmem& sm) {
   const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
   const unsigned mask = 0xffffffffu;
-  double acc = ldcg(x + 12 * (int64_t)j + tt);
-  for (int bb = v.col_ptr[j]; bb < v.col_ptr[j + 1]; ++bb) {
-    const double* Lb = v.L + 144 * (int64_t)(v.n + bb) + tt;  // column tt of L_ij
-    const double* xi = x + 12 * (int64_t)v.blk_row[bb];
-    double s = 0.0;
-#pragma unroll
-    for (int r = 0; r < 12; ++r) s = fma(ldcg(Lb + 12 * r), ldcg(xi + r), s);
-    acc -= s;
+  // L_jj, 1 / L_jj[c][c] and the column's blocks L_ij with x_i staged by cp.async
+  // (all loads in flight together instead of one dependent L2 round trip per block)
+  stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
+  if (t < 6) cp16(sm.pv + 2 * t, v.dinv + 12 * (int64_t)j + 2 * t);
+  cp_commit();
+  const int c0 = v.col_ptr[j], U = v.col_ptr[j + 1] - c0;
+  auto issue = [&](int u) {
+    const int bb = c0 + u;
+    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)(v.n + bb), t);
+    if (t < 6) cp16(sm.vec[u % NST] + 2 * t, x + 12 * (int64_t)v.blk_row[bb] + 2 * t);
+  };
+  for (int p = 0; p < NST - 1; ++p) {
+    if (p < U) issue(p);
+    cp_commit();
   }
+  double acc = ldcg(x + 12 * (int64_t)j + tt);
+  for (int u = 0; u < U; ++u) {
+    cp_wait_pipe();
+    __syncwarp(mask);
+    const double* Lb = sm.stage[u % NST][0] + tt;  // column tt of L_ij
+    const double* xi = sm.vec[u % NST];
+    double s2 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 12; ++r) s2 = fma(Lb[12 * r], xi[r], s2);
+    acc -= s2;
+    __syncwarp(mask);
+    if (u + NST - 1 < U) issue(u + NST - 1);
+    cp_commit();
+  }
+  cp_wait_all();
+  __syncwarp(mask);
   double lcol[12], rinv[12];
-  const double* Ld = v.L + 144 * (int64_t)j + tt;
-  const double* di = v.dinv + 12 * (int64_t)j;
 #pragma unroll
   for (int m = 0; m < 12; ++m) {
-    lcol[m] = ldcg(Ld + 12 * m);
-    rinv[m] = ldcg(di + m);
+    lcol[m] = sm.pl[12 * m + tt];
+    rinv[m] = sm.pv[m];
   }
   const double xv = upper_solve12(mask, t, acc, lcol, rinv);
   __syncwarp(mask);
@@ -871,7 +891,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
       }
     } else {  // backward task
       const int j = item - bwd0;
-      chol_backward(v, j, x);
+      chol_backward(v, j, x, sm);
       fence_acq_rel();
       __syncwarp(mask);
       if (t == 0) {
