@@ -147,7 +147,14 @@ static int active_scan(Scene& s, const double* q, double dh) {
   return hp[0];
 }
 
-int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark) {
+// active sets at least this large take the fused run assembly (k_pair_runs) when the
+// caller reduces into the system (assemble); ABD_RUNS=0/1 forces it off / on
+static bool use_runs(int64_t total) {
+  const char* e = getenv("ABD_RUNS");  // read per call: tests switch it inside one process
+  return e ? atoi(e) != 0 : total >= (int64_t)1 << 20;
+}
+
+int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark, bool allow_runs) {
   int64_t n_vf = s.cands.n_vf;
   int total = active_scan(s, q, dh);
   if (mark) mark_structure(s);
@@ -155,8 +162,17 @@ int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int p
   s.pblk.blk.resize((int64_t)std::max(total, 1) * PB_STRIDE);
   s.pblk.d2.resize(std::max(total, 1));
   s.pblk.n = total;
+  s.pblk.n_runs = 0;
   EventTimer tm(s, 1);
   (void)n_vf;
+  if (allow_runs && total > 0 && use_runs(total)) {
+    launch_pair_runs(s, q, kappa, dh, project, s.w.act.p, s.w.n_act_vf, total);
+    tm.stop();
+    // records stay on chip: candidate record + rest points read, one run partial written per run
+    tm.done(total, 112.0 * (double)(s.cands.n_vf + s.cands.n_ee) + 8.0 * (double)s.cands.n_ee +
+                       8.0 * RUN_STRIDE * (double)s.pblk.n_runs);
+    return total;
+  }
   // VF pairs on side2 beside the EE pairs (+ mollified EE) on the main stream
   const bool fork_vf = s.w.n_act_vf > 0 && total - s.w.n_act_vf > 0;
   if (fork_vf) {
@@ -572,7 +588,7 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   const int2* fp = fric_pattern(s, nfp);
   build_pattern(s, s.cands.ov.p, s.cands.n_ov, fp, nfp, /*from_cands=*/true);
   HMARK();
-  contact_blocks(s, q, kappa, dh, 1, /*mark=*/s.red_nu == 0);
+  contact_blocks(s, q, kappa, dh, 1, /*mark=*/s.red_nu == 0, /*allow_runs=*/true);
   HMARK();
   append_friction_blocks(s, q, dt, eps_v, 1);
   if (body_forked) CK(cudaStreamWaitEvent(s.stream, s.join_ev, 0));

@@ -47,7 +47,8 @@ double global_min_distance_stats(Scene& s, const double* q);
 std::vector<int2> intersecting_body_pairs(Scene& s, const double* q);
 void world_vertices(Scene& s, const double* q, double* out);
 // driver.cu
-int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark = false);
+int64_t contact_blocks(Scene& s, const double* q, double kappa, double dh, int project, bool mark = false,
+                       bool allow_runs = false);
 void append_friction_blocks(Scene& s, const double* q, double dt, double eps_v, int project);
 int64_t friction_precompute(Scene& s, const double* q, double kappa, double dh, double mu, DVec<double>* basis);
 double contact_energy(Scene& s, const double* q, double kappa, double dh);

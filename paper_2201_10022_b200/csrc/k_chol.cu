@@ -1515,22 +1515,24 @@ static Analysis chol_analyze(Scene& s) {
   an.ms_sub[1] = ms_since(t0);
   // update pairs for off block (i, j): k in rows(j) with i in cs[k], in elimination
   // order of k.  Every pair (j, i) of cs[k] (j before i) is one such update, so the
-  // lists are built by walking each column's pairs once: O(#updates x |cs[j]|).
+  // lists are built by walking each column's pairs once: O(#updates + sum |cs[j]|).
   upd_ptr.assign(nbo + 1, 0);
   std::vector<int>& ub = w.hs_i[29];
   ub.clear();
-  auto find_blk = [&](int j, int i) {
-    for (int f = csp[j]; f < csp[j + 1]; ++f)
-      if (csi[f] == i) return f;
-    return -1;
-  };
+  // the later entries of cs[k] after j = csi[a2] are a subset of cs[j], both sorted by
+  // elimination position: one merge walk finds their blocks in column j
+  ub.reserve(4096);
   for (int k : order)
-    for (int a2 = csp[k]; a2 < csp[k + 1]; ++a2)
+    for (int a2 = csp[k]; a2 < csp[k + 1]; ++a2) {
+      const int j = csi[a2];
+      int f = csp[j];
       for (int b2 = a2 + 1; b2 < csp[k + 1]; ++b2) {
-        const int blk = find_blk(csi[a2], csi[b2]);
-        ub.push_back(blk);
-        upd_ptr[blk + 1]++;
+        const int i = csi[b2];
+        while (csi[f] != i) ++f;  // present by the fill property (f < csp[j + 1])
+        ub.push_back(f);
+        upd_ptr[f + 1]++;
       }
+    }
   for (int b = 0; b < nbo; ++b) upd_ptr[b + 1] += upd_ptr[b];
   upd.resize(2 * (size_t)upd_ptr[nbo]);
   {

@@ -3,6 +3,7 @@
 // inertia + orthogonality terms (K1).
 #include "abd_contact.cuh"
 #include "abd_misc.cuh"
+#include "abd_pblk.cuh"
 #include "kernels.h"
 
 #include <algorithm>
@@ -175,6 +176,109 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
   PairEval ev = contact_pair_eval<true, 1>(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0,
                                            project != 0, blk);
   out_d2[slot] = ev.d2;
+}
+
+// ---------------------------------------------------------------------------
+// Fused assembly of large active sets (config 2: millions of active pairs):
+// records never round-trip HBM.  A warp takes a window of 32 consecutive active
+// slots of one kind; each lane evaluates its pair into a compact record in shared
+// memory (contact_pair_eval, as k_pair_blocks_act); the window's runs -- maximal
+// lane ranges of one body pair -- are then summed, lane by lane in slot order, into
+// dense run partials (aa | bb | ab blocks and both gradients in the reference's DOF
+// order), which reduce_system adds to the BSR blocks as contributions of their own.
+// Mollified EE pairs keep their 9-column record path (k_pair_blocks_moll).  Sums in
+// fixed orders: deterministic.
+constexpr int RUN_WARPS = 2;
+
+template <int KIND>
+__device__ __forceinline__ int2 run_pair(const int4* __restrict__ rows, const int* __restrict__ act, int64_t cand_off,
+                                         int64_t slot_off, int64_t count, const unsigned char* __restrict__ moll_flag,
+                                         int64_t t, bool& fused, int4& r) {
+  fused = false;
+  if (t >= count) return make_int2(-1, -1);
+  r = rows[act[slot_off + t] - cand_off];
+  fused = KIND == KIND_VF || !moll_flag || !moll_flag[t];
+  return make_int2(r.x, r.z);
+}
+
+// lanes that start a run (fused, and a different body pair or a non-fused lane before)
+__device__ __forceinline__ unsigned run_starts(bool fused, int2 bp, int lane) {
+  const int px = __shfl_up_sync(0xffffffffu, bp.x, 1), py = __shfl_up_sync(0xffffffffu, bp.y, 1);
+  const bool pf = __shfl_up_sync(0xffffffffu, fused ? 1 : 0, 1) != 0;
+  const bool start = fused && (lane == 0 || !pf || px != bp.x || py != bp.y);
+  return __ballot_sync(0xffffffffu, start);
+}
+
+template <int KIND>
+__global__ void k_run_count(int64_t count, const int* __restrict__ act, int64_t cand_off,
+                            const int4* __restrict__ rows, int64_t slot_off, const unsigned char* __restrict__ moll_flag,
+                            int64_t n_win, int* wcount) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n_win) return;
+  bool f;
+  int4 r;
+  const int2 bp = run_pair<KIND>(rows, act, cand_off, slot_off, count, moll_flag, 32 * w + lane, f, r);
+  const unsigned m = run_starts(f, bp, lane);
+  if (lane == 0) wcount[w] = __popc(m);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(32 * RUN_WARPS) k_pair_runs(SceneView sv, int64_t count, const int* __restrict__ act,
+                                                               int64_t cand_off, const int4* __restrict__ rows,
+                                                               const double* __restrict__ q, double kappa, double dh,
+                                                               int project, int64_t slot_off,
+                                                               const unsigned char* __restrict__ moll_flag,
+                                                               int64_t n_win, const int* __restrict__ wbase,
+                                                               int2* out_bodies, double* out_d2, double* run_part,
+                                                               int2* run_bodies) {
+  extern __shared__ double run_sm[];  // [RUN_WARPS][32][PB_STRIDE]
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * RUN_WARPS + wl;
+  if (w >= n_win) return;
+  double* recs = run_sm + (size_t)wl * 32 * PB_STRIDE;
+  const int64_t t = 32 * w + lane;
+  bool f;
+  int4 r;
+  const int2 bp = run_pair<KIND>(rows, act, cand_off, slot_off, count, moll_flag, t, f, r);
+  if (t < count) {
+    const int64_t slot = slot_off + t;
+    out_bodies[slot] = f ? make_int2(-1, -1) : bp;  // folded pairs contribute through their run
+    if (f) {
+      PairIds ids = pair_ids(sv, KIND, r);
+      V3 z[4], xb[4];
+      pair_points(sv, ids, q, z, xb);
+      PairEval ev = contact_pair_eval<true, 1>(KIND, z, xb, ids.eps, kappa, dh, sv.dyn[r.x] != 0, sv.dyn[r.z] != 0,
+                                               project != 0, recs + (size_t)lane * PB_STRIDE);
+      out_d2[slot] = ev.d2;
+    }
+  }
+  const unsigned starts = run_starts(f, bp, lane);
+  const unsigned fused = __ballot_sync(0xffffffffu, f);
+  __syncwarp();
+  const int base = wbase[w];
+  unsigned rem = starts;
+  for (int k = 0; rem; ++k) {
+    const int l0 = __ffs(rem) - 1;
+    rem &= rem - 1;
+    // the run ends at the next start or the next non-fused lane
+    const unsigned stop = (starts | ~fused) & ~((2u << l0) - 1u);
+    const int l1 = stop ? __ffs(stop) - 1 : 32;
+    double* out = run_part + (int64_t)(base + k) * RUN_STRIDE;
+    for (int e = lane; e < RUN_STRIDE; e += 32) {
+      double a = 0.0;
+      if (e < 432) {
+        const int blk = e / 144, idx = e % 144, i = idx / 12, c = idx % 12;
+        const int R = blk == 1 ? 12 + i : i, C = blk == 0 ? c : 12 + c;
+        for (int l = l0; l < l1; ++l) a += pb_entry(recs + (size_t)l * PB_STRIDE, R, C);
+      } else {
+        for (int l = l0; l < l1; ++l) a += recs[(size_t)l * PB_STRIDE + (e - 432)];
+      }
+      out[e] = a;
+    }
+    const int bx = __shfl_sync(0xffffffffu, bp.x, l0), by = __shfl_sync(0xffffffffu, bp.y, l0);
+    if (lane == 0) run_bodies[base + k] = make_int2(bx, by);
+  }
 }
 
 // the mollified active EE slots, listed ahead of the pair-block kernels so their
@@ -924,6 +1028,78 @@ void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, d
     note_launch("k_pair_blocks_moll");
   }
   note_launch("k_pair_blocks");
+}
+
+// Fused run assembly over all active contact pairs (VF slots [0, n_vf_act), EE after):
+// counts the runs per window, scans them (one host read of the total), evaluates.
+void launch_pair_runs(Scene& s, const double* q, double kappa, double dh, int project, const int* act,
+                      int64_t n_vf_act, int64_t total) {
+  cudaStream_t st = s.stream;
+  const int64_t n_ee_act = total - n_vf_act;
+  const int64_t win_vf = (n_vf_act + 31) / 32, win_ee = (n_ee_act + 31) / 32, nwin = win_vf + win_ee;
+  PairBlockSet& pb = s.pblk;
+  pb.run_wcount.resize(nwin + 1);
+  pb.run_wbase.resize(nwin + 1);
+  int* moll_count = reinterpret_cast<int*>(s.w.ull.p + 10);
+  const int4* vf = s.cands.vf.p;
+  const int4* ee = s.cands.ee.p;
+  const int64_t cand_ee = s.cands.n_vf;
+  const unsigned char* mflag = nullptr;
+  if (n_ee_act > 0) {
+    s.w.moll.resize(std::max<int64_t>(n_ee_act, 1));
+    s.w.moll_flag.resize(std::max<int64_t>(n_ee_act, 1));
+    CK(cudaMemsetAsync(moll_count, 0, sizeof(int), st));
+    k_moll_classify<<<grid_for(n_ee_act, 256), 256, 0, st>>>(view(s), n_ee_act, act, cand_ee, ee, q, n_vf_act,
+                                                              s.w.moll.p, moll_count, s.w.moll_flag.p);
+    note_launch("k_moll_classify");
+    mflag = s.w.moll_flag.p;
+  }
+  CK(cudaMemsetAsync(pb.run_wcount.p + nwin, 0, sizeof(int), st));
+  if (win_vf) {
+    k_run_count<KIND_VF><<<grid_for(32 * win_vf, 256), 256, 0, st>>>(n_vf_act, act, 0, vf, 0, nullptr, win_vf,
+                                                                     pb.run_wcount.p);
+    note_launch("k_run_count");
+  }
+  if (win_ee) {
+    k_run_count<KIND_EE><<<grid_for(32 * win_ee, 256), 256, 0, st>>>(n_ee_act, act, cand_ee, ee, n_vf_act, mflag,
+                                                                     win_ee, pb.run_wcount.p + win_vf);
+    note_launch("k_run_count");
+  }
+  scan_exclusive_i32(s, pb.run_wcount.p, pb.run_wbase.p, nwin + 1);
+  int hn = 0;
+  CK(cudaMemcpyAsync(&hn, pb.run_wbase.p + nwin, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SSYNC(st);
+  pb.n_runs = hn;
+  pb.run_part.resize(std::max<int64_t>(hn, 1) * RUN_STRIDE);
+  pb.run_bodies.resize(std::max(hn, 1));
+  const size_t smem = (size_t)RUN_WARPS * 32 * PB_STRIDE * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_pair_runs<KIND_VF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_pair_runs<KIND_EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  if (win_vf) {
+    k_pair_runs<KIND_VF><<<grid_for(win_vf, RUN_WARPS), 32 * RUN_WARPS, smem, st>>>(
+        view(s), n_vf_act, act, 0, vf, q, kappa, dh, project, 0, nullptr, win_vf, pb.run_wbase.p, pb.bodies.p,
+        pb.d2.p, pb.run_part.p, pb.run_bodies.p);
+    note_launch("k_pair_runs");
+  }
+  if (win_ee) {
+    // the mollified EE pairs build their 9-column records beside the runs
+    const int grid = (int)std::min<int64_t>(grid_for(n_ee_act, MOLL_WARPS), 16 * (int64_t)s.num_sms);
+    CK(cudaEventRecord(s.moll_fork_ev, st));
+    CK(cudaStreamWaitEvent(s.side3, s.moll_fork_ev, 0));
+    k_pair_blocks_moll<<<grid, 32 * MOLL_WARPS, 0, s.side3>>>(view(s), s.w.moll.p, moll_count, act, cand_ee, ee, q,
+                                                              kappa, dh, project, pb.blk.p, pb.d2.p);
+    note_launch("k_pair_blocks_moll");
+    CK(cudaEventRecord(s.moll_ev, s.side3));
+    k_pair_runs<KIND_EE><<<grid_for(win_ee, RUN_WARPS), 32 * RUN_WARPS, smem, st>>>(
+        view(s), n_ee_act, act, cand_ee, ee, q, kappa, dh, project, n_vf_act, mflag, win_ee,
+        pb.run_wbase.p + win_vf, pb.bodies.p, pb.d2.p, pb.run_part.p, pb.run_bodies.p);
+    note_launch("k_pair_runs");
+    CK(cudaStreamWaitEvent(st, s.moll_ev, 0));
+  }
 }
 
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best) {

@@ -93,11 +93,13 @@ __global__ void k_csr_positions(int n, int64_t n_off, const uint64_t* __restrict
 // val = pair << 2 | which (0: haa/ga, 1: hbb/gb, 2: hab, 3: hab^T)
 __global__ void k_contribs(int64_t np, const int2* __restrict__ bodies, const int* __restrict__ slot,
                            const int* __restrict__ diag_pos, int64_t n_off, const int2* __restrict__ upper_keys,
-                           const int* __restrict__ upper_pos, uint32_t* keys, int* vals, int* cnt) {
+                           const int* __restrict__ upper_pos, uint32_t* keys, int* vals, int* cnt,
+                           int64_t val_off = 0) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= np) return;
   int2 b = bodies[p];
-  int sa = slot[b.x], sb = slot[b.y];
+  // (-1, -1): a pair folded into a run partial (k_pair_runs), no contribution of its own
+  int sa = b.x >= 0 ? slot[b.x] : -1, sb = b.y >= 0 ? slot[b.y] : -1;
   uint32_t k0 = 0xffffffffu, k1 = 0xffffffffu, k2 = 0xffffffffu;
   int v2 = 0;
   if (sa >= 0) k0 = (uint32_t)diag_pos[sa];
@@ -121,12 +123,13 @@ __global__ void k_contribs(int64_t np, const int2* __restrict__ bodies, const in
       v2 = sa < sb ? 2 : 3;
     }
   }
+  const int64_t pv = p + val_off;  // run partials follow the records in value order
   keys[3 * p] = k0;
-  vals[3 * p] = (int)(p << 2) | 0;
+  vals[3 * p] = (int)(pv << 2) | 0;
   keys[3 * p + 1] = k1;
-  vals[3 * p + 1] = (int)(p << 2) | 1;
+  vals[3 * p + 1] = (int)(pv << 2) | 1;
   keys[3 * p + 2] = k2;
-  vals[3 * p + 2] = (int)(p << 2) | v2;
+  vals[3 * p + 2] = (int)(pv << 2) | v2;
   if (cnt) {
     if (k0 != 0xffffffffu) atomicAdd(cnt + k0, 1);
     if (k1 != 0xffffffffu) atomicAdd(cnt + k1, 1);
@@ -176,7 +179,8 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
                                                                  const double* __restrict__ diag0,
                                                                  const double* __restrict__ grad0, double* val,
                                                                  double* grad, const int* __restrict__ row_of,
-                                                                 int* sorted_out) {
+                                                                 int* sorted_out, int64_t n_rec,
+                                                                 const double* __restrict__ run_part) {
   __shared__ double srec[RB_WARPS][RB_PER_LANE * 32];
   __shared__ double part[RB_WARPS][160];
   __shared__ double gpart[RB_WARPS][12];
@@ -214,15 +218,39 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
   double* sr = srec[wid];
   double nxt[RB_PER_LANE];
   int vnext = 0;
-  if (s0 + split < s1) {
-    vnext = cv[s0 + split];
-    const double* blk = pblk + (int64_t)(vnext >> 2) * PB_STRIDE;
+  // contributions v >> 2 < n_rec are compact records (staged, next one prefetched);
+  // the others are dense run partials (aa | bb | ab | ga | gb, RUN_STRIDE doubles)
+  auto prefetch = [&](int v) {
+    if ((int64_t)(v >> 2) >= n_rec) return;
+    const double* blk = pblk + (int64_t)(v >> 2) * PB_STRIDE;
 #pragma unroll
     for (int j = 0; j < RB_PER_LANE; ++j)
       if (lane + 32 * j < PB_STRIDE) nxt[j] = blk[lane + 32 * j];
+  };
+  if (s0 + split < s1) {
+    vnext = cv[s0 + split];
+    prefetch(vnext);
   }
   for (int t = s0 + split; t < s1; t += RB_SPLIT) {
     const int which = vnext & 3;
+    const int64_t src = vnext >> 2;
+    if (src >= n_rec) {  // dense run partial
+      const double* P = run_part + (src - n_rec) * RUN_STRIDE;
+      if (t + RB_SPLIT < s1) {
+        vnext = cv[t + RB_SPLIT];
+        prefetch(vnext);
+      }
+#pragma unroll
+      for (int e = 0; e < 5; ++e) {
+        int idx = lane + 32 * e;
+        if (idx < 144) {
+          const int i = idx / 12, k = idx % 12;
+          acc[e] += which == 3 ? P[288 + 12 * k + i] : P[144 * which + idx];
+        }
+      }
+      if (which < 2 && lane < 12) gacc += P[432 + 12 * which + lane];
+      continue;
+    }
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < RB_PER_LANE; ++j)
@@ -230,10 +258,7 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
     __syncwarp();
     if (t + RB_SPLIT < s1) {
       vnext = cv[t + RB_SPLIT];
-      const double* blk = pblk + (int64_t)(vnext >> 2) * PB_STRIDE;
-#pragma unroll
-      for (int j = 0; j < RB_PER_LANE; ++j)
-        if (lane + 32 * j < PB_STRIDE) nxt[j] = blk[lane + 32 * j];
+      prefetch(vnext);
     }
     // target entry (i, k) = H24(12 s_r + i, 12 s_c + k) for the aa / bb / ab blocks;
     // which 3 is the transposed ab block: H24(k, 12 + i)
@@ -382,7 +407,8 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
   int n = H.n;
   if (n == 0) return;
   int64_t np = s.pblk.n;
-  int64_t m = 3 * np;
+  const int64_t nr = s.pblk.n_runs;  // dense run partials (k_pair_runs), after the records
+  int64_t m = 3 * (np + nr);
   DVec<uint32_t>& ka = s.w.ka;
   DVec<uint32_t>& kb = s.w.kb;
   DVec<int>& va = s.w.va;
@@ -404,10 +430,11 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
   const int* sb = seg_s.p;
   const int* se = seg_e.p;
   int* sorted_out = nullptr;
-  if (sort_path || np == 0) {
+  if (sort_path || np + nr == 0) {
     seg_s.zero(st);
     seg_e.zero(st);
   }
+  if (nr > 0 && sort_path) throw Error(ABD_ERR_ARG, "ABD_CONTRIB_SORT does not take run partials");
   if (np > 0 && sort_path) {
     k_contribs<<<grid_for(np, 256), 256, 0, st>>>(np, s.pblk.bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
                                                   H.upper_keys.p, H.upper_pos.p, ka.p, va.p, nullptr);
@@ -419,15 +446,23 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
     k_seg_bounds<<<grid_for(m, 256), 256, 0, st>>>(m, alt ? kb.p : ka.p, H.nnzb, seg_s.p, seg_e.p);
     note_launch("k_seg_bounds");
     cv = alt ? vb.p : va.p;
-  } else if (np > 0) {
+  } else if (np + nr > 0) {
     // counting placement: per-block counts, exclusive scan (segment starts), fill;
     // the reduction rank-sorts each (short) segment
     DVec<int>& cnt = s.w.cnt;
     cnt.resize(H.nnzb + 1);
     cnt.zero(st);
-    k_contribs<<<grid_for(np, 256), 256, 0, st>>>(np, s.pblk.bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
-                                                  H.upper_keys.p, H.upper_pos.p, ka.p, va.p, cnt.p);
-    note_launch("k_contribs");
+    if (np > 0) {
+      k_contribs<<<grid_for(np, 256), 256, 0, st>>>(np, s.pblk.bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
+                                                    H.upper_keys.p, H.upper_pos.p, ka.p, va.p, cnt.p);
+      note_launch("k_contribs");
+    }
+    if (nr > 0) {
+      k_contribs<<<grid_for(nr, 256), 256, 0, st>>>(nr, s.pblk.run_bodies.p, s.slot.p, H.diag_pos.p, H.n_off,
+                                                    H.upper_keys.p, H.upper_pos.p, ka.p + 3 * np, va.p + 3 * np,
+                                                    cnt.p, np);
+      note_launch("k_contribs");
+    }
     scan_exclusive_i32(s, cnt.p, seg_s.p, H.nnzb + 1);
     cnt.zero(st);
     k_contrib_fill<<<grid_for(m, 256), 256, 0, st>>>(m, ka.p, va.p, seg_s.p, cnt.p, vb.p);
@@ -440,7 +475,7 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
   s.grad.resize(12 * (int64_t)n);
   k_reduce_blocks<<<grid_for(H.nnzb, RB_POS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, sb, se, cv,
                                                               s.pblk.blk.p, diag0, grad0, H.val.p, s.grad.p,
-                                                              row_of.p, sorted_out);
+                                                              row_of.p, sorted_out, np, s.pblk.run_part.p);
   note_launch("k_reduce_blocks");
 }
 

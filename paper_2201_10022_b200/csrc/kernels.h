@@ -63,6 +63,8 @@ void launch_tri_intersect(cudaStream_t st, int64_t n, const double* ta, const do
 void launch_pair_flags_both(Scene& s, const double* q, double dh2, int* flags, int* err);
 void launch_mark_active_q(Scene& s, const double* q, double dh2, int* flags);
 void launch_scatter_active(Scene& s, int64_t n, const int* flags, const int* pos, int* act);
+void launch_pair_runs(Scene& s, const double* q, double kappa, double dh, int project, const int* act,
+                      int64_t n_vf_act, int64_t total);
 void launch_pair_blocks_act(Scene& s, int kind, const double* q, double kappa, double dh, int project,
                             const int* act, int64_t slot_off, int64_t count);
 void launch_cand_min_d2(Scene& s, int kind, const double* q, unsigned long long* best_bits);

@@ -131,11 +131,19 @@ struct FrictionSet {
 // factors (abd_pblk.cuh); PB_DENSE = g24 | haa | hbb | hab for dense readout
 constexpr int PB_STRIDE = 136;
 constexpr int PB_DENSE = 24 + 3 * 144;
+constexpr int RUN_STRIDE = 456;  // run partial: aa 144 | bb 144 | ab 144 | ga 12 | gb 12 (reference DOFs)
+
 struct PairBlockSet {
-  DVec<int2> bodies;
+  DVec<int2> bodies;  // (-1, -1) for pairs folded into a run partial
   DVec<double> blk;  // PB_STRIDE per pair
   DVec<double> d2;
   int64_t n = 0;
+  // fused assembly of large active sets (k_pair_runs): per run of consecutive active
+  // pairs of one body pair (within a 32-pair window) its summed blocks and gradients
+  DVec<int2> run_bodies;
+  DVec<double> run_part;  // RUN_STRIDE per run
+  DVec<int> run_wcount, run_wbase;
+  int64_t n_runs = 0;
 };
 
 // symmetric BSR over dynamic slots, stored in full (both triangles) CSR

@@ -57,7 +57,8 @@ def morton_pattern(order):
 def soup_arrays(data):
     """Scene + candidate arrays for `scenes.microbench_pairs` output.
 
-    Returns dict(v_off, e_off, t_off, rest, edges, tris, el2, vf, ee, ov): local
+    Returns dict(v_off, e_off, t_off, rest, edges, tris, el2, vf, ee, ov, vf_perm, ee_perm)
+    (rows grouped by body pair; row k is generated pair perm[k]): local
     vertex indices in edges/tris, candidate rows (body, prim, body, prim) in the
     reference's CandidateSet convention (contact.py:175-204; EE with body_a < body_b).
     """
@@ -106,9 +107,14 @@ def soup_arrays(data):
     el2 = dv[:, 0] * dv[:, 0] + dv[:, 1] * dv[:, 1] + dv[:, 2] * dv[:, 2]
     vf_rows = np.stack([va, v_local, vb, t_idx], axis=1)
     ee_rows = np.stack([ea, e_idx[:ne], eb, e_idx[ne:]], axis=1)
+    # candidates grouped by body pair, as the broad phase emits them (overlap-pair
+    # order): consecutive pairs of one body pair form the runs the fused assembly sums
+    vf_perm = np.lexsort((np.arange(len(vf_rows)), vf_rows[:, 2], vf_rows[:, 0]))
+    ee_perm = np.lexsort((np.arange(len(ee_rows)), ee_rows[:, 2], ee_rows[:, 0]))
+    vf_rows, ee_rows = vf_rows[vf_perm], ee_rows[ee_perm]
     ov = morton_pattern(data["order"])
     return dict(v_off=v_off, e_off=e_off, t_off=t_off, rest=rest, edges=edges, tris=tris, el2=el2,
-                vf=vf_rows, ee=ee_rows, ov=ov)
+                vf=vf_rows, ee=ee_rows, ov=ov, vf_perm=vf_perm, ee_perm=ee_perm)
 
 
 class PairSystem:

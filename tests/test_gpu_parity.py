@@ -478,3 +478,18 @@ def test_friction_outer_iterations(golden):
             ref = g["q"][s]
             assert np.abs(state.q - ref).max() / np.abs(ref).max() <= 1e-6, s
             assert st.iterations == int(g["iterations"][s]), s
+
+
+def test_box_stack_trajectory_fused_runs(golden, monkeypatch):
+    """The fused run assembly (ABD_RUNS=1: k_pair_runs, dense run partials) on the box stack:
+    the reference's trajectory to 1e-6 per step with its Newton counts."""
+    monkeypatch.setenv("ABD_RUNS", "1")
+    g = golden("box_stack.npz")
+    model, state, params = _box_stack_model(g)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for s in range(len(g["iterations"])):
+            state, st = P.advance_step(model, state, params)
+            ref = g["q"][s + 1]
+            assert np.abs(state.q - ref).max() / np.abs(ref).max() <= 1e-6, s
+            assert st.iterations == int(g["iterations"][s]), s

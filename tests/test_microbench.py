@@ -41,14 +41,19 @@ def test_soup_reproduces_pairs():
     vf, ee = a["vf"], a["ee"]
     x0 = rest[vo[vf[:, 0]] + vf[:, 1]]
     tri = a["tris"][to[vf[:, 2]] + vf[:, 3]] + vo[vf[:, 2]][:, None]
-    assert np.array_equal(np.concatenate([x0[:, None], rest[tri]], axis=1), d["vf"]["rest"])
+    assert np.array_equal(np.concatenate([x0[:, None], rest[tri]], axis=1), d["vf"]["rest"][a["vf_perm"]])
     ea = a["edges"][eo[ee[:, 0]] + ee[:, 1]] + vo[ee[:, 0]][:, None]
     eb = a["edges"][eo[ee[:, 2]] + ee[:, 3]] + vo[ee[:, 2]][:, None]
     er = d["ee"]["rest"].copy()
     sw = d["ee"]["body_a"] > d["ee"]["body_b"]
     er[sw] = er[sw][:, [2, 3, 0, 1]]
+    er = er[a["ee_perm"]]
     assert np.array_equal(np.concatenate([rest[ea], rest[eb]], axis=1), er)
     assert (ee[:, 0] < ee[:, 2]).all()
+    # grouped by body pair (the runs of the fused assembly)
+    for rows in (vf, ee):
+        k = rows[:, 0] * (1 << 32) + rows[:, 2]
+        assert (np.diff(k) >= 0).all()
     # every pair's body pair is a block of the Morton +-1..4 pattern
     ov = {tuple(r) for r in a["ov"]}
     for rows in (vf, ee):
@@ -70,7 +75,11 @@ def test_pairs_distances_in_range():
 
 
 @pytest.mark.gpu
-def test_microbench_assemble_and_pcg_vs_oracle():
+@pytest.mark.parametrize("runs", ["0", "1"])
+def test_microbench_assemble_and_pcg_vs_oracle(runs, monkeypatch):
+    """runs=1: the fused run assembly (k_pair_runs: records stay in shared memory, one
+    dense partial per run of one body pair), which config 2's 20M active pairs take."""
+    monkeypatch.setenv("ABD_RUNS", runs)
     d, a = _small()
     B = len(d["q"])
     sysm = mb.PairSystem(d)

@@ -9,6 +9,7 @@
 #include <chrono>
 using clk = std::chrono::steady_clock;
 double ms_since(clk::time_point t){ return std::chrono::duration<double,std::milli>(clk::now()-t).count(); }
+constexpr int PART_MIN = 12, PART_CHUNK = 8;
 void min_degree_lists(int m, std::vector<std::vector<int>>& adj, std::vector<int>& order,
                       std::vector<std::vector<int>>& colstruct);
 
@@ -101,11 +102,81 @@ void min_degree_lists(int m, std::vector<std::vector<int>>& adj, std::vector<int
   }
 }
 
+constexpr double ORDER_REUSE_FILL = 1.05;  // factor blocks and update pairs, over the fresh order's
 
-struct An { int n_cta=0; int64_t n_edges=0; int n_coupled=0; int64_t n_blk=0, n_upd=0; int max_level=0, largest=0; double ms_order=0, ms_sub[6]={}; };
-struct Wk { std::vector<int> hs_i[40]; std::vector<char> hs_c[4]; };
+// Symbolic factorization of the local graph (adjacency adj_ptr / adj_idx, full
+// degrees deg) under the cached global elimination order `gorder`, preceded by the
+// nodes not in it (ascending local id).  Column structure of v = its later
+// neighbours plus its elimination-tree children's structures minus v, sorted by
+// position.  Fills order / pos / csp / csi as the fresh ordering does; false when the
+// factor would exceed max_nnz off-diagonal blocks or max_upd update pairs.
+bool symbolic_fixed_order(int m, const std::vector<int>& adj_ptr, const std::vector<int>& adj_idx,
+                          const std::vector<int>& deg, const std::vector<int>& loc, const std::vector<int>& gorder,
+                          int64_t max_nnz, int64_t max_upd, std::vector<int>* scratch, std::vector<int>& order,
+                          std::vector<int>& pos, std::vector<int>& csp, std::vector<int>& csi) {
+  int64_t upd = 0;
+  std::vector<int>&seen = scratch[0], &mark = scratch[1], &head = scratch[2], &nxt = scratch[3], &st0 = scratch[4],
+                  &len = scratch[5], &flat = scratch[6], &L = scratch[7];
+  seen.assign(m, 0);
+  order.clear();
+  for (int g : gorder)
+    if (loc[g] >= 0) seen[loc[g]] = 1;
+  for (int v = 0; v < m; ++v)
+    if (!seen[v]) order.push_back(v);
+  for (int g : gorder)
+    if (loc[g] >= 0) order.push_back(loc[g]);
+  if ((int)order.size() != m) return false;
+  pos.resize(m);
+  for (int i = 0; i < m; ++i) pos[order[i]] = i;
+  mark.assign(m, -1);
+  head.assign(m, -1);
+  nxt.assign(m, -1);
+  st0.assign(m, 0);
+  len.assign(m, 0);
+  flat.clear();
+  for (int i = 0; i < m; ++i) {
+    const int v = order[i];
+    L.clear();
+    for (int e = adj_ptr[v]; e < adj_ptr[v] + deg[v]; ++e) {
+      const int u = adj_idx[e];
+      if (pos[u] > i && mark[u] != v) {
+        mark[u] = v;
+        L.push_back(u);
+      }
+    }
+    for (int c = head[v]; c >= 0; c = nxt[c])
+      for (int k = st0[c]; k < st0[c] + len[c]; ++k) {
+        const int u = flat[k];
+        if (u != v && mark[u] != v) {
+          mark[u] = v;
+          L.push_back(u);
+        }
+      }
+    std::sort(L.begin(), L.end(), [&](int a, int b) { return pos[a] < pos[b]; });
+    st0[v] = (int)flat.size();
+    len[v] = (int)L.size();
+    flat.insert(flat.end(), L.begin(), L.end());
+    upd += (int64_t)L.size() * ((int64_t)L.size() - 1) / 2;  // update pairs of this column
+    if ((int64_t)flat.size() > max_nnz || upd > max_upd) return false;
+    if (!L.empty()) {
+      nxt[v] = head[L[0]];
+      head[L[0]] = v;
+    }
+  }
+  csp.assign(m + 1, 0);
+  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + len[v];
+  csi.resize(csp[m]);
+  for (int v = 0; v < m; ++v) std::copy(flat.begin() + st0[v], flat.begin() + st0[v] + len[v], csi.begin() + csp[v]);
+  return true;
+}
+
+
+struct An { int n_cta=0; int64_t n_edges=0; int n_coupled=0; int64_t n_blk=0, n_upd=0; int max_level=0, largest=0; double ms_order=0, ms_sub[6]={}; bool order_reused=false;};
+struct CC { bool valid=false; int n=0; std::vector<int> gorder; int64_t fresh_nnz=0, fresh_upd=0; };
+struct Wk { std::vector<int> hs_i[40]; std::vector<char> hs_c[4]; CC ch_cache; };
 void run(int n, std::vector<uint64_t>& cur, Wk& w, An& an){
   auto t0 = clk::now();
+  CC& cc = w.ch_cache;
   // coupled nodes (>= 1 nonzero coupling) get local ids in ascending node order;
   // host scratch persists across analyses (no allocations in the steady state)
   std::vector<int>&loc = w.hs_i[0], &glob = w.hs_i[1], &adj_ptr = w.hs_i[2], &adj_idx = w.hs_i[3],
@@ -141,151 +212,173 @@ void run(int n, std::vector<uint64_t>& cur, Wk& w, An& an){
     adj_idx[adj_ptr[b2] + deg[b2]++] = a2;
   }
   const double ms_adj = ms_since(t0);
-  // Elimination order by tree contraction (contact graphs of piles are forests of
-  // stacked chains): rounds of rake (every node of degree <= 1 at the start of the
-  // round; no fill) and compress (an independent set of degree-2 nodes; the fill
-  // edge joins the two neighbours), so a chain of L bodies is eliminated in
-  // O(log L) elimination-tree levels instead of L / 2.  What remains (degree >= 3
-  // everywhere) is ordered by minimum degree.  cs0/cs1 = the live neighbours of a
-  // raked / compressed node when it is eliminated (its L column structure).
-  // The live neighbour list of v is adj_idx[adj_ptr[v], adj_ptr[v] + deg[v]),
-  // edited in place: rake and compress never raise a degree.
-  order.clear();
-  cs0.assign(m, -1);
-  cs1.assign(m, -1);
-  gone.assign(m, 0);
-  blocked.assign(m, 0);
-  live.resize(m);
-  std::iota(live.begin(), live.end(), 0);
-  static const bool no_compress = getenv("ABD_CHOL_NO_COMPRESS") != nullptr;
-  auto drop = [&](int u, int x) {
-    int* l = adj_idx.data() + adj_ptr[u];
-    const int d = deg[u];
-    for (int i = 0; i < d; ++i)
-      if (l[i] == x) {
-        l[i] = l[d - 1];
-        deg[u] = d - 1;
-        return;
-      }
-  };
-  auto relink = [&](int u, int x, int y) {  // in u's list: x -> y, or drop x when y is already there
-    int* l = adj_idx.data() + adj_ptr[u];
-    const int d = deg[u];
-    int ix = -1;
-    bool has_y = false;
-    for (int i = 0; i < d; ++i) {
-      if (l[i] == x) ix = i;
-      if (l[i] == y) has_y = true;
-    }
-    if (has_y) {
-      l[ix] = l[d - 1];
-      deg[u] = d - 1;
-    } else {
-      l[ix] = y;
-    }
-  };
-  for (;;) {
-    bool progress = false;
-    sel.clear();
-    for (int v : live)
-      if (deg[v] <= 1) sel.push_back(v);
-    for (int v : sel) {  // rake (a lone pair: the second end follows with no neighbour)
-      if (gone[v]) continue;
-      if (deg[v] == 1) {
-        const int u = adj_idx[adj_ptr[v]];
-        cs0[v] = u;
-        drop(u, v);
-      }
-      deg[v] = 0;
-      gone[v] = 1;
-      order.push_back(v);
-      progress = true;
-    }
-    if (!no_compress) {
-      sel.clear();
-      for (int v : live) blocked[v] = 0;
-      for (int v : live)
-        if (!gone[v] && !blocked[v] && deg[v] == 2) {
-          const int* l = adj_idx.data() + adj_ptr[v];
-          sel.push_back(v);
-          blocked[v] = 1;
-          blocked[l[0]] = 1;
-          blocked[l[1]] = 1;
+  // Order reuse: a miss inside a step (the union graph grew by a few contacts)
+  // keeps the step's fresh elimination order -- nodes new to the graph first -- and
+  // redoes only the symbolic factorization, unless the fill grows by more than
+  // ORDER_REUSE_FILL over the fresh order's, in factor blocks or update pairs (then
+  // the graph is ordered afresh).
+  static const bool no_reuse = getenv("ABD_CHOL_NO_ORDER_REUSE") != nullptr;
+  int n_core = 0;
+  bool reused = false;
+  if (!no_reuse && cc.valid && cc.n == n && !cc.gorder.empty())
+    reused = symbolic_fixed_order(m, adj_ptr, adj_idx, deg, loc, cc.gorder, (int64_t)(ORDER_REUSE_FILL * cc.fresh_nnz),
+                                  (int64_t)(ORDER_REUSE_FILL * cc.fresh_upd), w.hs_i + 31, order, pos, csp, csi);
+  if (!reused) {
+    // Elimination order by tree contraction (contact graphs of piles are forests of
+    // stacked chains): rounds of rake (every node of degree <= 1 at the start of the
+    // round; no fill) and compress (an independent set of degree-2 nodes; the fill
+    // edge joins the two neighbours), so a chain of L bodies is eliminated in
+    // O(log L) elimination-tree levels instead of L / 2.  What remains (degree >= 3
+    // everywhere) is ordered by minimum degree.  cs0/cs1 = the live neighbours of a
+    // raked / compressed node when it is eliminated (its L column structure).
+    // The live neighbour list of v is adj_idx[adj_ptr[v], adj_ptr[v] + deg[v]),
+    // edited in place: rake and compress never raise a degree.
+    order.clear();
+    cs0.assign(m, -1);
+    cs1.assign(m, -1);
+    gone.assign(m, 0);
+    blocked.assign(m, 0);
+    live.resize(m);
+    std::iota(live.begin(), live.end(), 0);
+    static const bool no_compress = getenv("ABD_CHOL_NO_COMPRESS") != nullptr;
+    auto drop = [&](int u, int x) {
+      int* l = adj_idx.data() + adj_ptr[u];
+      const int d = deg[u];
+      for (int i = 0; i < d; ++i)
+        if (l[i] == x) {
+          l[i] = l[d - 1];
+          deg[u] = d - 1;
+          return;
         }
-      for (int v : sel) {  // compress: v's neighbours a, b become adjacent (fill)
-        const int* l = adj_idx.data() + adj_ptr[v];
-        const int a2 = l[0], b2 = l[1];
-        cs0[v] = a2;
-        cs1[v] = b2;
-        relink(a2, v, b2);
-        relink(b2, v, a2);
+    };
+    auto relink = [&](int u, int x, int y) {  // in u's list: x -> y, or drop x when y is already there
+      int* l = adj_idx.data() + adj_ptr[u];
+      const int d = deg[u];
+      int ix = -1;
+      bool has_y = false;
+      for (int i = 0; i < d; ++i) {
+        if (l[i] == x) ix = i;
+        if (l[i] == y) has_y = true;
+      }
+      if (has_y) {
+        l[ix] = l[d - 1];
+        deg[u] = d - 1;
+      } else {
+        l[ix] = y;
+      }
+    };
+    for (;;) {
+      bool progress = false;
+      sel.clear();
+      for (int v : live)
+        if (deg[v] <= 1) sel.push_back(v);
+      for (int v : sel) {  // rake (a lone pair: the second end follows with no neighbour)
+        if (gone[v]) continue;
+        if (deg[v] == 1) {
+          const int u = adj_idx[adj_ptr[v]];
+          cs0[v] = u;
+          drop(u, v);
+        }
         deg[v] = 0;
         gone[v] = 1;
         order.push_back(v);
         progress = true;
       }
+      if (!no_compress) {
+        sel.clear();
+        for (int v : live) blocked[v] = 0;
+        for (int v : live)
+          if (!gone[v] && !blocked[v] && deg[v] == 2) {
+            const int* l = adj_idx.data() + adj_ptr[v];
+            sel.push_back(v);
+            blocked[v] = 1;
+            blocked[l[0]] = 1;
+            blocked[l[1]] = 1;
+          }
+        for (int v : sel) {  // compress: v's neighbours a, b become adjacent (fill)
+          const int* l = adj_idx.data() + adj_ptr[v];
+          const int a2 = l[0], b2 = l[1];
+          cs0[v] = a2;
+          cs1[v] = b2;
+          relink(a2, v, b2);
+          relink(b2, v, a2);
+          deg[v] = 0;
+          gone[v] = 1;
+          order.push_back(v);
+          progress = true;
+        }
+      }
+      live2.clear();
+      for (int v : live)
+        if (!gone[v]) live2.push_back(v);
+      live.swap(live2);
+      if (!progress || live.empty()) break;
     }
-    live2.clear();
-    for (int v : live)
-      if (!gone[v]) live2.push_back(v);
-    live.swap(live2);
-    if (!progress || live.empty()) break;
-  }
-  const double ms_contract = ms_since(t0);
-  const int n_core = m - (int)order.size();
-  std::vector<std::vector<int>> core_cs;
-  std::vector<int> core_glob;
-  if ((int)order.size() < m) {
-    std::vector<int> core_id(m, -1);
-    core_glob = live;
-    const int mc = (int)core_glob.size();
-    for (int c = 0; c < mc; ++c) core_id[core_glob[c]] = c;
-    std::vector<std::vector<int>> cadj(mc);
-    for (int c = 0; c < mc; ++c) {
-      const int v = core_glob[c];
-      for (int i = 0; i < deg[v]; ++i) cadj[c].push_back(core_id[adj_idx[adj_ptr[v] + i]]);
-      std::sort(cadj[c].begin(), cadj[c].end());
+    const double ms_contract = ms_since(t0);
+    n_core = m - (int)order.size();
+    std::vector<std::vector<int>> core_cs;
+    std::vector<int> core_glob;
+    if ((int)order.size() < m) {
+      std::vector<int> core_id(m, -1);
+      core_glob = live;
+      const int mc = (int)core_glob.size();
+      for (int c = 0; c < mc; ++c) core_id[core_glob[c]] = c;
+      std::vector<std::vector<int>> cadj(mc);
+      for (int c = 0; c < mc; ++c) {
+        const int v = core_glob[c];
+        for (int i = 0; i < deg[v]; ++i) cadj[c].push_back(core_id[adj_idx[adj_ptr[v] + i]]);
+        std::sort(cadj[c].begin(), cadj[c].end());
+      }
+      std::vector<int> corder;
+      min_degree(mc, cadj, corder, core_cs);
+      for (int c : corder) order.push_back(core_glob[c]);
+      for (auto& l : core_cs)
+        for (int& x : l) x = core_glob[x];
     }
-    std::vector<int> corder;
-    auto cadj2=cadj; auto tmd=clk::now(); min_degree(mc, cadj, corder, core_cs); if(getenv("MDT")){ std::vector<int> o2; std::vector<std::vector<int>> c2; auto t3=clk::now(); for(int r=0;r<20;++r){auto cc=cadj2; min_degree_lists(mc, cc, o2, c2);} fprintf(stderr,"lists x20 %.3f ms\n", ms_since(t3)); t3=clk::now(); for(int r=0;r<20;++r){auto cc=cadj2; min_degree(mc, cc, o2, c2);} fprintf(stderr,"bits x20 %.3f ms\n", ms_since(t3));} if(getenv("MDT")) {size_t nz=0; for(auto&c:core_cs) nz+=c.size(); size_t e=0; for(auto&c:cadj) e+=c.size(); fprintf(stderr,"md %.3f ms mc=%d nnzL=%zu\n", ms_since(tmd), mc, nz);}
-    for (int c : corder) order.push_back(core_glob[c]);
-    for (auto& l : core_cs)
-      for (int& x : l) x = core_glob[x];
-  }
-  const double ms_core = ms_since(t0);
-  static const bool trace_ord = getenv("ABD_TRACE_CHOL") != nullptr;
-  if (trace_ord)
-    fprintf(stderr, "[abd chol order] m=%d core=%d cur_ms=%.3f adj_ms=%.3f contract_ms=%.3f core_ms=%.3f\n", m, n_core,
-            ms_cur, ms_adj, ms_contract, ms_core);
-  pos.resize(m);
-  for (int i = 0; i < m; ++i) pos[order[i]] = i;
-  csp.assign(m + 1, 0);
-  for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (cs0[v] >= 0) + (cs1[v] >= 0);
-  for (size_t c = 0; c < core_glob.size(); ++c) csp[core_glob[c] + 1] = (int)core_cs[c].size();
-  if (!core_glob.empty()) {  // recount: core nodes carry their min-degree column structures
-    std::vector<int> cnt(m, 0);
-    for (int v = 0; v < m; ++v) cnt[v] = (cs0[v] >= 0) + (cs1[v] >= 0);
-    for (size_t c = 0; c < core_glob.size(); ++c) cnt[core_glob[c]] = (int)core_cs[c].size();
-    csp[0] = 0;
-    for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + cnt[v];
-  }
-  csi.resize(csp[m]);
-  for (int v = 0; v < m; ++v) {
-    int* o = csi.data() + csp[v];
-    const int k = csp[v + 1] - csp[v];
-    if (k == 1) {
-      o[0] = cs0[v];
-    } else if (k == 2 && cs1[v] >= 0) {
-      const bool sw = pos[cs1[v]] < pos[cs0[v]];
-      o[0] = sw ? cs1[v] : cs0[v];
-      o[1] = sw ? cs0[v] : cs1[v];
+    const double ms_core = ms_since(t0);
+    static const bool trace_ord = getenv("ABD_TRACE_CHOL") != nullptr;
+    if (trace_ord)
+      fprintf(stderr, "[abd chol order] m=%d core=%d cur_ms=%.3f adj_ms=%.3f contract_ms=%.3f core_ms=%.3f\n", m, n_core,
+              ms_cur, ms_adj, ms_contract, ms_core);
+    pos.resize(m);
+    for (int i = 0; i < m; ++i) pos[order[i]] = i;
+    csp.assign(m + 1, 0);
+    for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + (cs0[v] >= 0) + (cs1[v] >= 0);
+    for (size_t c = 0; c < core_glob.size(); ++c) csp[core_glob[c] + 1] = (int)core_cs[c].size();
+    if (!core_glob.empty()) {  // recount: core nodes carry their min-degree column structures
+      std::vector<int> cnt(m, 0);
+      for (int v = 0; v < m; ++v) cnt[v] = (cs0[v] >= 0) + (cs1[v] >= 0);
+      for (size_t c = 0; c < core_glob.size(); ++c) cnt[core_glob[c]] = (int)core_cs[c].size();
+      csp[0] = 0;
+      for (int v = 0; v < m; ++v) csp[v + 1] = csp[v] + cnt[v];
+    }
+    csi.resize(csp[m]);
+    for (int v = 0; v < m; ++v) {
+      int* o = csi.data() + csp[v];
+      const int k = csp[v + 1] - csp[v];
+      if (k == 1) {
+        o[0] = cs0[v];
+      } else if (k == 2 && cs1[v] >= 0) {
+        const bool sw = pos[cs1[v]] < pos[cs0[v]];
+        o[0] = sw ? cs1[v] : cs0[v];
+        o[1] = sw ? cs0[v] : cs1[v];
+      }
+    }
+    for (size_t c = 0; c < core_glob.size(); ++c) {
+      std::vector<int>& l = core_cs[c];
+      std::sort(l.begin(), l.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
+      std::copy(l.begin(), l.end(), csi.begin() + csp[core_glob[c]]);
+    }
+    cc.gorder.resize(m);
+    for (int i = 0; i < m; ++i) cc.gorder[i] = glob[order[i]];
+    cc.fresh_nnz = csp[m];
+    cc.fresh_upd = 0;
+    for (int v = 0; v < m; ++v) {
+      const int64_t k = csp[v + 1] - csp[v];
+      cc.fresh_upd += k * (k - 1) / 2;
     }
   }
-  for (size_t c = 0; c < core_glob.size(); ++c) {
-    std::vector<int>& l = core_cs[c];
-    std::sort(l.begin(), l.end(), [&](int a2, int b2) { return pos[a2] < pos[b2]; });
-    std::copy(l.begin(), l.end(), csi.begin() + csp[core_glob[c]]);
-  }
+  an.order_reused = reused;
   an.ms_order = ms_since(t0);
   t0 = clk::now();
 
@@ -314,22 +407,24 @@ void run(int n, std::vector<uint64_t>& cur, Wk& w, An& an){
   an.ms_sub[1] = ms_since(t0);
   // update pairs for off block (i, j): k in rows(j) with i in cs[k], in elimination
   // order of k.  Every pair (j, i) of cs[k] (j before i) is one such update, so the
-  // lists are built by walking each column's pairs once: O(#updates x |cs[j]|).
+  // lists are built by walking each column's pairs once: O(#updates + sum |cs[j]|).
   upd_ptr.assign(nbo + 1, 0);
   std::vector<int>& ub = w.hs_i[29];
   ub.clear();
-  auto find_blk = [&](int j, int i) {
-    for (int f = csp[j]; f < csp[j + 1]; ++f)
-      if (csi[f] == i) return f;
-    return -1;
-  };
+  // the later entries of cs[k] after j = csi[a2] are a subset of cs[j], both sorted by
+  // elimination position: one merge walk finds their blocks in column j
+  ub.reserve(4096);
   for (int k : order)
-    for (int a2 = csp[k]; a2 < csp[k + 1]; ++a2)
+    for (int a2 = csp[k]; a2 < csp[k + 1]; ++a2) {
+      const int j = csi[a2];
+      int f = csp[j];
       for (int b2 = a2 + 1; b2 < csp[k + 1]; ++b2) {
-        const int blk = find_blk(csi[a2], csi[b2]);
-        ub.push_back(blk);
-        upd_ptr[blk + 1]++;
+        const int i = csi[b2];
+        while (csi[f] != i) ++f;  // present by the fill property (f < csp[j + 1])
+        ub.push_back(f);
+        upd_ptr[f + 1]++;
       }
+    }
   for (int b = 0; b < nbo; ++b) upd_ptr[b + 1] += upd_ptr[b];
   upd.resize(2 * (size_t)upd_ptr[nbo]);
   {
@@ -420,11 +515,29 @@ void run(int n, std::vector<uint64_t>& cur, Wk& w, An& an){
     fprintf(stderr, "[abd chol cp] m=%d core=%d leaves=%d total=%lld maxcost=%lld critpath=%lld maxcol=%d maxrow=%d\n",
             m, n_core, n_leaves, (long long)tot, (long long)maxc, (long long)maxcp, maxcol, maxrow);
   }
+  // split factor tasks: a diagonal with R row products / a block with U update pairs
+  // above PART_MIN becomes ceil(. / PART_CHUNK) partial tasks released with the node
+  // (ABD_CHOL_NO_SPLIT: none).  An unsplit diagonal is one whole task; an unsplit
+  // block (bnp = 0) runs whole after its diagonal, as without splitting.
+  static const bool no_split = getenv("ABD_CHOL_NO_SPLIT") != nullptr;
+  auto nparts = [&](int k) { return (!no_split && k > PART_MIN) ? (k + PART_CHUNK - 1) / PART_CHUNK : 1; };
+  auto bparts = [&](int k) { const int q = nparts(k); return q > 1 ? q : 0; };
+  int64_t n_part = 0, n_init = 0;
+  {
+    std::vector<int> per(m, 0);
+    for (int v = 0; v < m; ++v) {
+      per[v] = nparts(rcnt[v + 1] - rcnt[v]);
+      for (int b2 = csp[v]; b2 < csp[v + 1]; ++b2) per[v] += bparts(upd_ptr[b2 + 1] - upd_ptr[b2]);
+      n_part += per[v];
+    }
+    for (int v : leaves) n_init += per[v];
+  }
 
 }
 int main(int argc, char** argv){
-  FILE* f=fopen(argv[1],"rb"); int n; int64_t ne; fread(&n,4,1,f); fread(&ne,8,1,f); std::vector<uint64_t> cur(ne); fread(cur.data(),8,ne,f); fclose(f);
+  FILE* f=fopen(argv[1],"rb"); int n; int64_t ne; if(fread(&n,4,1,f)!=1) return 1; if(fread(&ne,8,1,f)!=1) return 1; std::vector<uint64_t> cur(ne); if(fread(cur.data(),8,ne,f)!=(size_t)ne) return 1; fclose(f);
   Wk w;
-  for(int rep=0;rep<10;++rep){ An an; auto t0=clk::now(); run(n,cur,w,an); double tot=ms_since(t0);
-    printf("total %.3f ms: order %.3f sub %.3f %.3f %.3f %.3f %.3f %.3f  m=%d edges=%lld upd=%lld levels=%d\n", tot, an.ms_order, an.ms_sub[0],an.ms_sub[1],an.ms_sub[2],an.ms_sub[3],an.ms_sub[4],an.ms_sub[5], an.n_coupled,(long long)an.n_edges,(long long)an.n_upd, an.max_level);}
+  for(int rep=0;rep<6;++rep){ An an; auto cur2=cur; auto t0=clk::now(); run(n,cur2,w,an); double tot=ms_since(t0);
+    printf("total %.3f ms: order %.3f sub %.3f %.3f %.3f %.3f  m=%d upd=%lld levels=%d reused=%d\n", tot, an.ms_order, an.ms_sub[0],an.ms_sub[1],an.ms_sub[2],an.ms_sub[3], an.n_coupled,(long long)an.n_upd, an.max_level, (int)an.order_reused);
+    w.ch_cache.valid = true; w.ch_cache.n = n; }
 }
