@@ -119,7 +119,7 @@ struct EventTimer {
 };
 
 static void mark_structure(Scene& s);
-static void mark_structure_early(Scene& s, const double* q, double dh);
+static void mark_structure_early(Scene& s, const double* q, double dh, bool on_main = false);
 
 // flags + exclusive scan of candidate activity (d^2 < d_hat^2) into s.w.flags/pos;
 // returns the active count (one host sync, also checks the barrier domain)
@@ -369,7 +369,6 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   note_launch("k_alpha_trial");
   launch_energy(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v,
                 w.lsred.p + 4 * RED_BLOCKS, w.lsscal.p + 4, w.lserr.p + 1);
-  w.ch_early = false;
   // partitioned: energies and error flags over all ranks
   comm_allreduce(s, w.lsscal.p, 8, 0, 0);
   comm_allreduce(s, w.lserr.p, 2, 1, 2);
@@ -411,8 +410,12 @@ static LsFirst line_search_first(Scene& s, const abd_step_params& P, int64_t NB)
   static const bool no_early = getenv("ABD_CHOL_NO_EARLY") != nullptr;
   const bool keeps_pattern = w.pat_valid && s.cands.ov_matches_pattern && s.H.n == s.n_dyn &&
                              w.pat_fric_gen == s.fric.gen && w.pat_n_f == s.fric.n;
+  // also when the trial is rejected (speculation): the backtracked iterate's structure
+  // is usually inside the union with the cached graph; chol_begin verifies it.  Unlike
+  // the accepted-trial case this can change the plan (and rounding): ABD_CHOL_NO_SPECULATE
+  static const bool no_spec = getenv("ABD_CHOL_NO_SPECULATE") != nullptr;
   if (!no_early && P.linear_solver != 1 && s.red_nu == 0 && s.n_dyn > 0 && s.comm.world == 1 && keeps_pattern &&
-      r.e < r.e0)
+      (r.e < r.e0 || !no_spec) && !w.ch_early)
     mark_structure_early(s, s.q_trial.p, P.d_hat);
   return r;
 }
@@ -501,12 +504,14 @@ __global__ void k_mark_active_rows(int64_t n, const int4* __restrict__ rows, con
 // structure at the accepted first trial q_trial (== the next iterate): marked on the
 // side stream, flags only (the pattern -- and the upper keys already on the host --
 // is kept, see line_search_first), then the analysis job is posted
-static void mark_structure_early(Scene& s, const double* q, double dh) {
+static void mark_structure_early(Scene& s, const double* q, double dh, bool on_main) {
   Scene::Work& w = s.w;
   const int64_t n_off = s.H.n_off;
-  CK(cudaEventRecord(s.fork_ev, s.stream));
-  CK(cudaStreamWaitEvent(s.side, s.fork_ev, 0));
-  std::swap(s.stream, s.side);
+  if (!on_main) {
+    CK(cudaEventRecord(s.fork_ev, s.stream));
+    CK(cudaStreamWaitEvent(s.side, s.fork_ev, 0));
+    std::swap(s.stream, s.side);
+  }
   w.ch_flags.resize(std::max<int64_t>(n_off, 1));
   if (n_off) {
     w.ch_flags.zero(s.stream);
@@ -521,35 +526,54 @@ static void mark_structure_early(Scene& s, const double* q, double dh) {
   }
   if (!w.ch_pre_ev) CK(cudaEventCreateWithFlags(&w.ch_pre_ev, cudaEventDisableTiming));
   CK(cudaEventRecord(w.ch_pre_ev, s.stream));
-  std::swap(s.stream, s.side);
+  if (!on_main) std::swap(s.stream, s.side);
   w.ch_pre = true;
   w.ch_early = true;
   chol_analysis_post(s);
 }
 
+// structure flags of the active candidates (activity flags w.flags) and friction pairs
+static void mark_active_flags(Scene& s, int* flags) {
+  const int64_t n_off = s.H.n_off;
+  CK(cudaMemsetAsync(flags, 0, n_off * sizeof(int), s.stream));
+  const int64_t n_vf = s.cands.n_vf, n_ee = s.cands.n_ee;
+  if (n_vf)
+    k_mark_active_rows<<<grid_for(n_vf, 256), 256, 0, s.stream>>>(n_vf, s.cands.vf.p, s.w.flags.p, s.slot.p, n_off,
+                                                                  s.H.upper_keys.p, flags);
+  if (n_ee)
+    k_mark_active_rows<<<grid_for(n_ee, 256), 256, 0, s.stream>>>(n_ee, s.cands.ee.p, s.w.flags.p + n_vf, s.slot.p,
+                                                                  n_off, s.H.upper_keys.p, flags);
+  note_launch("k_mark_active_rows");
+  if (s.fric.n) {
+    k_mark_active<<<grid_for(s.fric.n, 256), 256, 0, s.stream>>>(s.fric.n, s.fric.bodies.p, s.slot.p, n_off,
+                                                                 s.H.upper_keys.p, flags);
+    note_launch("k_mark_active");
+  }
+}
+
 static void mark_structure(Scene& s) {
   Scene::Work& w = s.w;
-  if (w.ch_early) {  // marked at the accepted trial and already being analysed
+  if (w.ch_early) {
+    // the analysis posted at the first line-search trial is in flight; the actual
+    // structure goes to the host beside it, and chol_begin checks that the plan covers
+    // it (a rejected trial's structure may not) before factoring
     w.ch_early = false;
+    const int64_t n_off = s.H.n_off;
+    if (n_off) {
+      w.ch_flags2.resize(n_off);
+      mark_active_flags(s, w.ch_flags2.p);
+      int* hm2 = w.h_meta2.reserve((size_t)n_off);
+      CK(cudaMemcpyAsync(hm2, w.ch_flags2.p, n_off * sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+    }
+    if (!w.ch_act_ev) CK(cudaEventCreateWithFlags(&w.ch_act_ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(w.ch_act_ev, s.stream));
+    w.ch_verify = true;
     return;
   }
   const int64_t n_off = s.H.n_off;
   w.ch_flags.resize(std::max<int64_t>(n_off, 1));
   if (n_off) {
-    w.ch_flags.zero(s.stream);
-    const int64_t n_vf = s.cands.n_vf, n_ee = s.cands.n_ee;
-    if (n_vf)
-      k_mark_active_rows<<<grid_for(n_vf, 256), 256, 0, s.stream>>>(n_vf, s.cands.vf.p, w.flags.p, s.slot.p, n_off,
-                                                                    s.H.upper_keys.p, w.ch_flags.p);
-    if (n_ee)
-      k_mark_active_rows<<<grid_for(n_ee, 256), 256, 0, s.stream>>>(n_ee, s.cands.ee.p, w.flags.p + n_vf, s.slot.p,
-                                                                    n_off, s.H.upper_keys.p, w.ch_flags.p);
-    note_launch("k_mark_active_rows");
-    if (s.fric.n) {
-      k_mark_active<<<grid_for(s.fric.n, 256), 256, 0, s.stream>>>(s.fric.n, s.fric.bodies.p, s.slot.p, n_off,
-                                                                   s.H.upper_keys.p, w.ch_flags.p);
-      note_launch("k_mark_active");
-    }
+    mark_active_flags(s, w.ch_flags.p);
     comm_allreduce(s, w.ch_flags.p, n_off, 1, 2);  // union of the ranks' couplings
     slab_mask_structure(s, w.ch_flags.p);          // multi-rank: this slab's block only
     int* hm = w.h_meta.reserve(3 * (size_t)n_off);
@@ -708,6 +732,19 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
       }
       k_expand_dq<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.slot.p, dsrc, sign, s.dq.p);
       note_launch("k_expand_dq");
+      // speculative analysis of the next iterate's structure, q + alpha_prev dq over the
+      // current candidates, so the host analysis overlaps this iteration's broad phase,
+      // CCD and line search (chol_begin verifies that the plan covers the structure
+      // actually reached, and re-analyses otherwise); ABD_CHOL_NO_SPEC_SOLVE disables
+      static const bool no_spec_solve = getenv("ABD_CHOL_NO_SPEC_SOLVE") != nullptr ||
+                                         getenv("ABD_CHOL_NO_SPECULATE") != nullptr ||
+                                         getenv("ABD_CHOL_NO_EARLY") != nullptr;
+      if (!no_spec_solve && P.linear_solver != 1 && s.red_nu == 0 && s.comm.world == 1 && s.w.pat_valid &&
+          s.H.n == s.n_dyn && s.H.n_off > 0 && !s.w.ch_early) {
+        s.w.q_pred.resize(NB);
+        launch_axpy_q(s, s.q.p, s.w.alpha_prev, s.dq.p, s.w.q_pred.p, NB);
+        mark_structure_early(s, s.w.q_pred.p, P.d_hat, /*on_main=*/true);
+      }
       // the previous line search's slowest ACCD queries start now on side2 (exact,
       // without the shared cut) and overlap the broad phase
       launch_ccd_hot(s, s.q.p, s.dq.p, P.ccd_slack);
@@ -731,6 +768,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
         e = ip_value(s, s.q_trial.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
       }
       CK(cudaMemcpyAsync(s.q.p, s.q_trial.p, NB * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+      s.w.alpha_prev = alpha;
       if (trace_newton) {
         std::vector<double> hq(NB), hd(NB);
         CK(cudaMemcpyAsync(hq.data(), s.q.p, NB * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -760,6 +798,7 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
     s.w.ch_early = false;
     s.w.ch_pre = false;
   }
+  s.w.ch_verify = false;
   k_qdot<<<grid_for(NB, 256), 256, 0, stream>>>(s.B, s.dyn.p, s.q.p, s.q0.p, P.dt, s.q_dot.p);
   note_launch("k_qdot");
   // stats (solver.py:604-627)

@@ -1938,6 +1938,30 @@ void chol_analysis_drop(Scene& s) {
   }
 }
 
+// An analysis posted at the first line-search trial (mark_structure_early) must cover
+// the structure of the iterate actually accepted (copied out by mark_structure); a
+// backtracked iterate whose couplings fall outside it is analysed again here.
+static void chol_verify_early(Scene& s, Analysis& an) {
+  Scene::Work& w = s.w;
+  if (!w.ch_verify) return;
+  w.ch_verify = false;
+  CK(cudaEventSynchronize(w.ch_act_ev));
+  const int64_t n_off = s.H.n_off;
+  const int* f2 = w.h_meta2.p;
+  const int* keys = w.h_meta.p + n_off;
+  const std::vector<uint64_t>& g = w.ch_cache.edges;
+  bool covered = true;
+  for (int64_t k = 0; k < n_off && covered; ++k)
+    if (f2[k]) {
+      const uint64_t e = ((uint64_t)(uint32_t)keys[2 * k] << 32) | (uint32_t)keys[2 * k + 1];
+      covered = std::binary_search(g.begin(), g.end(), e);
+    }
+  if (covered) return;
+  std::copy(f2, f2 + n_off, w.h_meta.p);
+  w.ch_pre = true;
+  an = chol_analyze(s);
+}
+
 void chol_begin(Scene& s, const double* rhs, double* x) {
   Bsr& H = s.H;
   Scene::Work& w = s.w;
@@ -1953,6 +1977,7 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   Analysis an;
   CholWorker* wk = worker(s, false);
   if (!wk || !wk->take(an)) an = chol_analyze(s);
+  chol_verify_early(s, an);
   HMARK();
   run.host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
   run.active = true;

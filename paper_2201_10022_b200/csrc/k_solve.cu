@@ -327,6 +327,7 @@ void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64
   chol_analysis_drop(s);  // an analysis in flight belongs to the old pattern
   s.w.ch_pre = false;  // any structure copied out for the Cholesky belongs to the old pattern
   s.w.ch_early = false;
+  s.w.ch_verify = false;
   wk.pat_valid = false;
   cudaStream_t st = s.stream;
   int n = s.n_dyn;

@@ -322,6 +322,14 @@ struct Scene {
     // and its analysis posted early (mark_structure then has nothing to do)
     bool ch_early = false;
     cudaEvent_t ch_pre_ev = nullptr;
+    // actual structure of an iteration whose analysis was posted early (at the first
+    // line-search trial): checked against the plan in chol_begin
+    DVec<int> ch_flags2;
+    HostPinned<int> h_meta2;
+    cudaEvent_t ch_act_ev = nullptr;
+    bool ch_verify = false;
+    DVec<double> q_pred;       // speculated next iterate (q + alpha_prev dq)
+    double alpha_prev = 1.0;   // the last accepted line-search step
     // an in-flight chol_begin awaiting chol_finish
     struct CholRun {
       bool active = false;

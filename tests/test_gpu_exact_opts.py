@@ -12,6 +12,11 @@ and off, and the final states are compared bit for bit:
 * ABD_BP_NO_GROUPS    -- static primitive groups in the primitive cull
 * ABD_GMD_EXHAUSTIVE  -- end-of-step global minimum distance by the widened broad phase
 * ABD_MOLL_SERIAL     -- mollified EE pair blocks on a side stream beside the plain EE pairs
+
+Speculative Cholesky analyses (of a rejected line-search trial's structure, or of a
+predicted next iterate right after the solve; ABD_CHOL_NO_SPECULATE) can change the
+elimination plan and so the rounding, like the step-local order reuse: they are held
+off in both runs, and the parity tests cover them.
 """
 import os
 import subprocess
@@ -56,6 +61,9 @@ def _run(tmp_path, name, steps, extra_env, tag):
     env = dict(os.environ)
     for k in OFF:
         env.pop(k, None)
+    # speculative early analyses (rejected trials) may change the Cholesky plan and so
+    # the rounding: held off in both runs, which then differ only by the exact options
+    env["ABD_CHOL_NO_SPECULATE"] = "1"
     env.update(extra_env)
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT), name, str(steps), out], env=env,
                        capture_output=True, text=True, timeout=900)
@@ -162,6 +170,7 @@ def test_optimisations_are_bitwise_exact_on_the_full_pile(tmp_path):
         env = dict(os.environ)
         for k in OFF:
             env.pop(k, None)
+        env["ABD_CHOL_NO_SPECULATE"] = "1"  # plan-changing speculation held off in both runs
         env.update(extra)
         r = subprocess.run([sys.executable, "-c", PILE_CHILD.format(root=ROOT, ckpt=ckpt), out, "16"], env=env,
                            capture_output=True, text=True, timeout=900)
