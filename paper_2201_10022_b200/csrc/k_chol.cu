@@ -96,6 +96,11 @@ struct CholView {
   double* scratch;      // n_part x PART_STRIDE partial sums
   int* dleft;           // n: remaining diagonal partials
   int* bgate;           // per off block: remaining partials + 1 (the column's diagonal)
+  // dataflow schedule (k_chol_flow): items in topological order, readiness by flags
+  const int* fseq;      // n_coupled + nbo: per node in elimination order its diagonal (j), then its blocks (n + b)
+  const int* eord;      // n_coupled: coupled nodes in elimination order
+  int* flag;            // n + nbo: = epoch once L block (factor) / y_j (solve, index j) is final
+  int* xflag;           // n: = epoch once x_j (backward substitution) is final
 };
 constexpr int PART_STRIDE = 156;  // 12 x 13 (the forward-substitution column rides along)
 
@@ -917,6 +922,287 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
   }
 }
 
+// ---- dataflow schedule: owner-computes with readiness flags --------------------
+// Every L block (and every forward / backward substitution of a node) is one item;
+// items are handed out in a topological order (elimination order: a node's
+// diagonal, then its column blocks; then the backward substitutions in reverse
+// order) by one atomic counter.  The warp that takes an item accumulates its update
+// list in the plan's fixed order (so the result is bitwise that of the unsplit task
+// graph, whatever the schedule), waiting on each operand's epoch flag as it comes:
+// products whose operands are final are done while later ones are still being
+// computed, so only the last update, the 12x12 pivot and the triangular solve of
+// each level stay on the elimination tree's critical path (the FIFO task graph
+// released a node's whole update sum only once its last child was done).  An item
+// only waits on items earlier in the order, all of which are held by running warps:
+// the least waiting item's operands are being produced, so the grid cannot
+// deadlock, whatever its size or residency.  A wait longer than FLOW_TIMEOUT_NS
+// (an inconsistent plan) raises a factorization error instead of hanging.
+constexpr unsigned long long FLOW_TIMEOUT_NS = 2000000000ull;
+
+__device__ __forceinline__ void cp_wait_dyn(int k) {
+  switch (k) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+  }
+}
+
+// lane 0 polls flags f0 (and f1 when >= 0) until both equal ep; every lane then
+// acquires them (orders its following loads and cp.async copies after the producer's
+// writes).  false on timeout (the flag array is left as is).
+__device__ __forceinline__ bool flow_wait(const CholView& v, const int* fl, int f0, int f1, int ep) {
+  const int t = threadIdx.x & 31;
+  int ok = 1;
+  if (t == 0) {
+    unsigned ns = 32;
+    unsigned long long t0 = 0;
+    while (ld_relaxed(fl + f0) != ep || (f1 >= 0 && ld_relaxed(fl + f1) != ep)) {
+      const unsigned long long now = gtimer();
+      if (!t0) t0 = now;
+      else if (now - t0 > FLOW_TIMEOUT_NS) {
+        ok = 0;
+        atomicMin(v.bad, -1);
+        break;
+      }
+      __nanosleep(ns);
+      ns = min(2u * ns, 256u);
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (ok) {
+    (void)ld_acquire(fl + f0);
+    if (f1 >= 0) (void)ld_acquire(fl + f1);
+  }
+  return ok != 0;
+}
+
+// A list of U update items whose operands are L blocks a[u] (and b[u] when paired)
+// read through a window of 32 items held one per lane: their operand indices and
+// readiness are loaded together (one L2 round trip for 32 flags), so items whose
+// operands are long final cost no per-item flag latency.
+struct FlowWin {
+  int base = 0, nready = 0;  // items [base, base + nready) known final
+  int a = -1, b = -1, c = -1;  // this lane's item operands (c: y_k node for rows)
+};
+
+// refresh the window at item `from` of a row list (diagonal: L_jk, y_k) or an update
+// list (block: L_ik, L_jk)
+__device__ __forceinline__ void flow_window(const CholView& v, FlowWin& w, bool rows, int lo, int U, int from, int ep) {
+  const int t = threadIdx.x & 31;
+  const int u = from + t;
+  bool rdy = true;
+  w.a = w.b = w.c = -1;
+  if (u < U) {
+    if (rows) {
+      w.a = v.row_blk[lo + u];
+      w.c = v.row_col[lo + u];
+      rdy = ld_relaxed(v.flag + w.a) == ep;
+    } else {
+      const int2 pq = v.upd[lo + u];
+      w.a = pq.x;
+      w.b = pq.y;
+      rdy = ld_relaxed(v.flag + pq.x) == ep && ld_relaxed(v.flag + pq.y) == ep;
+    }
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, rdy);
+  w.base = from;
+  w.nready = m == 0xffffffffu ? 32 : __ffs(~m) - 1;
+  if (w.nready > 0) {
+    // the relaxed reads above saw the producers' releases: the fence makes them
+    // acquires, and the warp barrier orders every lane's copies after them
+    fence_acq_rel();
+    __syncwarp();
+  }
+}
+
+// Accumulate the list in order into ac (subtracting products), staging operands by
+// cp.async as they become final.  rows: X = Y = L_jk with y_k riding along.
+__device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool rows, int lo, int U, const double* x,
+                                                int ep, WarpSmem& sm) {
+  const int t = threadIdx.x & 31;
+  const unsigned mask = 0xffffffffu;
+  FlowWin w;
+  int issued = 0;
+  bool ok = true;
+  auto issue = [&](int u) {
+    const int src = u - w.base;
+    const int a = __shfl_sync(mask, w.a, src);
+    const int bb = __shfl_sync(mask, rows ? w.c : w.b, src);
+    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)a, t);
+    if (rows) {
+      if (t < 6) cp16(sm.vec[u % NST] + 2 * t, x + 12 * (int64_t)bb + 2 * t);
+    } else {
+      stage_block(sm.stage[u % NST][1], v.L + 144 * (int64_t)bb, t);
+    }
+    cp_commit();
+  };
+  for (int u = 0; u < U; ++u) {
+    while (issued <= u) {
+      if (issued >= w.base + w.nready || issued >= w.base + 32) {
+        flow_window(v, w, rows, lo, U, issued, ep);
+        if (w.nready == 0) {
+          // block on this item's operands, then reload the window behind it
+          const int f0 = __shfl_sync(mask, w.a, 0), f1 = rows ? -1 : __shfl_sync(mask, w.b, 0);
+          ok = flow_wait(v, v.flag, f0, f1, ep) && ok;
+          flow_window(v, w, rows, lo, U, issued, ep);
+          if (w.nready == 0) w.nready = 1;  // timed out: proceed (the error is raised)
+        }
+      }
+      issue(issued++);
+    }
+    while (issued < U && issued < u + NST && issued < w.base + w.nready && issued < w.base + 32) issue(issued++);
+    cp_wait_dyn(issued - u - 1);
+    __syncwarp(mask);
+    if (rows) acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][0], sm.vec[u % NST], t);
+    else acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][1], nullptr, t);
+    __syncwarp(mask);
+  }
+  return ok;
+}
+
+__device__ __forceinline__ void flow_release(int* p, int ep) {
+  fence_acq_rel();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) st_release(p, ep);
+}
+
+// Persistent dataflow factor (+ forward and backward substitution); !factor: the two
+// substitutions with the resident factor.  Items: factor: [0, m + nbo) fseq, then m
+// backward substitutions in reverse elimination order; solve: [0, m) forward
+// substitutions in elimination order, then the m backward ones.
+__global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const double* __restrict__ b, double* x,
+                                                          int factor, int ep) {
+  extern __shared__ __align__(16) unsigned char ch_smem[];
+  const int hw = threadIdx.x >> 5, t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  WarpSmem& sm = reinterpret_cast<WarpSmem*>(ch_smem)[hw];
+  const unsigned mask = 0xffffffffu;
+  const bool fac = factor != 0;
+  const int m = v.n_coupled;
+  const int nbo = v.col_ptr[v.n];
+  const int nf = fac ? m + nbo : m;
+  const int total = nf + m;
+  for (;;) {
+    int idx = 0;
+    if (t == 0) idx = (int)atomicAdd(v.ctr, 1u);
+    idx = __shfl_sync(mask, idx, 0);
+    if (idx >= total) break;
+    const unsigned long long t_start = v.trace ? gtimer() : 0;
+    if (idx < nf) {
+      const int code = fac ? v.fseq[idx] : v.eord[idx];
+      if (code < v.n && fac) {  // diagonal of node j: D = A_jj - sum L_jk L_jk^T, L_jj, y_j
+        const int j = code;
+        const int e0 = v.row_ptr[j], U = v.row_ptr[j + 1] - e0;
+        stage_block(sm.pa, v.val + 144 * (int64_t)v.diag_pos[j], t);
+        if (t < 6) cp16(sm.pv + 2 * t, b + 12 * (int64_t)j + 2 * t);
+        cp_commit();
+        Acc ac;
+        acc_zero(ac);
+        flow_accumulate(v, ac, true, e0, U, x, ep, sm);
+        cp_wait_all();
+        __syncwarp(mask);
+        acc_store(ac, sm.pa, sm.pv, sm.S, t);
+        __syncwarp(mask);
+        diag_finish(v, j, x, sm);
+        flow_release(v.flag + j, ep);
+      } else if (code < v.n) {  // solve mode: y_j = L_jj^-1 (b_j - sum_k L_jk y_k)
+        const int j = code;
+        const int e0 = v.row_ptr[j], U = v.row_ptr[j + 1] - e0;
+        double acc = b[12 * (int64_t)j + tt];
+        for (int e = e0; e < e0 + U; ++e) {
+          const int k = v.row_col[e];
+          flow_wait(v, v.flag, k, -1, ep);
+          const double* Lk = v.L + 144 * (int64_t)v.row_blk[e] + 12 * tt;
+          const double* yk = x + 12 * (int64_t)k;
+          double s2 = 0.0;
+#pragma unroll
+          for (int q = 0; q < 12; ++q) s2 = fma(Lk[q], __ldcg(yk + q), s2);
+          acc -= s2;
+        }
+        double d[12], rinv[12];
+        const double* Ld = v.L + 144 * (int64_t)j + 12 * tt;
+        const double* di = v.dinv + 12 * (int64_t)j;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) {
+          d[q] = Ld[q];
+          rinv[q] = di[q];
+        }
+        const double y = lower_solve12(mask, t, acc, d, rinv);
+        if (t < 12) x[12 * (int64_t)j + t] = y;
+        flow_release(v.flag + j, ep);
+      } else {  // block L_ij = (A_ij - sum L_ik L_jk^T) L_jj^-T
+        const int bb = code - v.n;
+        const int j = v.blk_col[bb];
+        const int ap = v.apos[bb];
+        if (ap >= 0) stage_block(sm.pa, v.val + 144 * (int64_t)ap, t);
+        cp_commit();
+        const int u0 = v.upd_ptr[bb], U = v.upd_ptr[bb + 1] - u0;
+        Acc ac;
+        acc_zero(ac);
+        flow_accumulate(v, ac, false, u0, U, nullptr, ep, sm);
+        flow_wait(v, v.flag, j, -1, ep);  // L_jj and 1 / L_jj[c][c]
+        stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
+        if (t < 6) cp16(sm.pv + 2 * t, v.dinv + 12 * (int64_t)j + 2 * t);
+        cp_commit();
+        cp_wait_all();
+        __syncwarp(mask);
+        acc_store(ac, ap >= 0 ? sm.pa : nullptr, nullptr, sm.S, t);
+        __syncwarp(mask);
+        block_finish(v, bb, sm);
+        flow_release(v.flag + v.n + bb, ep);
+      }
+    } else {  // backward substitution of node j: x_j = L_jj^-T (y_j - sum_i L_ij^T x_i)
+      const int j = v.eord[m - 1 - (idx - nf)];
+      const int c0 = v.col_ptr[j], U = v.col_ptr[j + 1] - c0;
+      flow_wait(v, v.flag, j, -1, ep);  // y_j (and, factoring, L_jj)
+      stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
+      if (t < 6) cp16(sm.pv + 2 * t, v.dinv + 12 * (int64_t)j + 2 * t);
+      cp_commit();
+      double acc = ldcg(x + 12 * (int64_t)j + tt);
+      // ancestors' x_i in the column's order, each staged with its block once final
+      for (int u = 0; u < U; ++u) {
+        const int bb = c0 + u;
+        const int i = v.blk_row[bb];
+        flow_wait(v, v.xflag, i, -1, ep);
+        stage_block(sm.stage[0][0], v.L + 144 * (int64_t)(v.n + bb), t);
+        if (t < 6) cp16(sm.vec[0] + 2 * t, x + 12 * (int64_t)i + 2 * t);
+        cp_commit();
+        cp_wait_all();
+        __syncwarp(mask);
+        const double* Lb = sm.stage[0][0] + tt;
+        const double* xi = sm.vec[0];
+        double s2 = 0.0;
+#pragma unroll
+        for (int r = 0; r < 12; ++r) s2 = fma(Lb[12 * r], xi[r], s2);
+        acc -= s2;
+        __syncwarp(mask);
+      }
+      cp_wait_all();
+      __syncwarp(mask);
+      double lcol[12], rinv[12];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) {
+        lcol[q] = sm.pl[12 * q + tt];
+        rinv[q] = sm.pv[q];
+      }
+      const double xv = upper_solve12(mask, t, acc, lcol, rinv);
+      __syncwarp(mask);
+      if (t < 12) x[12 * (int64_t)j + t] = xv;
+      flow_release(v.xflag + j, ep);
+    }
+    if (v.trace && t == 0) {
+      const unsigned done = atomicAdd(v.ctr + 3, 1u);
+      unsigned long long* o = v.trace + 4 * (int64_t)done;
+      o[0] = (unsigned long long)(unsigned)idx;
+      o[1] = t_start;
+      o[2] = t_start;
+      o[3] = gtimer();
+    }
+  }
+}
+
 // nonzero flags of the upper off-diagonal pattern blocks
 __global__ void k_block_nz(int64_t n_off, const int* __restrict__ upper_pos, const double* __restrict__ val,
                            int* flags) {
@@ -974,7 +1260,7 @@ __global__ void k_add_inplace(int64_t n, double* x, const double* d) {
 
 // Sections of the packed plan buffer
 enum { CH_LEAVES, CH_ISO, CH_PARENT, CH_NCHILD, CH_CHILDP, CH_CHILDI, CH_COLP, CH_BROW, CH_BCOL, CH_ROWP, CH_ROWB,
-       CH_ROWC, CH_UPDP, CH_UPD, CH_PARTP, CH_PART, CH_DNP, CH_BPART, CH_BNP, CH_INIT, CH_NSEC };
+       CH_ROWC, CH_UPDP, CH_UPD, CH_PARTP, CH_PART, CH_DNP, CH_BPART, CH_BNP, CH_INIT, CH_FSEQ, CH_EORD, CH_NSEC };
 // task splitting: a diagonal (row products) or block (update pairs) task with more
 // than PART_MIN products is split into chunks of PART_CHUNK
 constexpr int PART_MIN = 12, PART_CHUNK = 8;
@@ -1030,6 +1316,10 @@ static CholView plan_view(Scene& s) {
   v.scratch = w.ch_scratch.p;
   v.dleft = w.ch_dleft.p;
   v.bgate = w.ch_bgate.p;
+  v.fseq = dp + o[CH_FSEQ];
+  v.eord = dp + o[CH_EORD];
+  v.flag = w.ch_fl.p;
+  v.xflag = w.ch_fl.p + n + nbo;
   return v;
 }
 
@@ -1648,7 +1938,7 @@ static Analysis chol_analyze(Scene& s) {
   const size_t len[CH_NSEC] = {(size_t)n_leaves, (size_t)n_iso, (size_t)n, (size_t)n, (size_t)n + 1, (size_t)m,
                                (size_t)n + 1, (size_t)nbo, (size_t)nbo, (size_t)n + 1, (size_t)nbo, (size_t)nbo,
                                (size_t)nbo + 1, upd.size(), (size_t)n + 1, 4 * (size_t)n_part, (size_t)n,
-                               (size_t)nbo, (size_t)nbo, (size_t)n_init};
+                               (size_t)nbo, (size_t)nbo, (size_t)n_init, (size_t)m + nbo, (size_t)m};
   for (int k = 0; k < CH_NSEC; ++k) {
     o[k + 1] = o[k] + len[k];
     if (k + 1 == CH_UPD) o[k + 1] += o[k + 1] & 1;          // int2 alignment of the update pairs
@@ -1746,6 +2036,18 @@ static Analysis chol_analyze(Scene& s) {
       for (int p2 = partp[g]; p2 < partp[g + 1]; ++p2) init[k++] = p2;
     }
   }
+  {
+    // dataflow order: per node in elimination order its diagonal, then its column blocks
+    int* fseq = hp + o[CH_FSEQ];
+    int* eord = hp + o[CH_EORD];
+    int q = 0;
+    for (int i = 0; i < m; ++i) {
+      const int g = glob[order[i]];
+      eord[i] = g;
+      fseq[q++] = g;
+      for (int b = col_ptr[g]; b < col_ptr[g + 1]; ++b) fseq[q++] = n + b;
+    }
+  }
   an.ms_sub[5] = ms_since(t0);
   std::copy(upd_ptr.begin(), upd_ptr.end(), hp + o[CH_UPDP]);
   std::copy(upd.begin(), upd.end(), hp + o[CH_UPD]);
@@ -1761,6 +2063,12 @@ static Analysis chol_analyze(Scene& s) {
   w.ch_dleft.resize(std::max(n, 1));
   w.ch_bgate.resize(std::max(nbo, 1));
   w.ch_scratch.resize(std::max<int64_t>(n_part, 1) * PART_STRIDE);
+  {
+    // epoch flags of k_chol_flow: zeroed when (re)allocated, never reset otherwise
+    const size_t cap0 = w.ch_fl.cap;
+    w.ch_fl.resize(2 * (size_t)n + nbo + 1);
+    if (w.ch_fl.cap != cap0) CK(cudaMemsetAsync(w.ch_fl.p, 0, w.ch_fl.cap * sizeof(int), st));
+  }
   cc.valid = true;
   cc.n = n;
   cc.n_off = n_off;
@@ -1794,9 +2102,20 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_chol_sched, CH_THREADS, smem));
     bps = std::max(bps, 1);
   }
-  const int init_n = std::max(std::max(v.n, v.n_tasks), std::max(2 * v.n_coupled, v.n_tasks - v.n_part));
-  k_chol_sched_init<<<grid_for(std::max(init_n, 4), 256), 256, 0, st>>>(v, factor ? 1 : 0);
-  note_launch("k_chol_sched_init");
+  // dataflow schedule (k_chol_flow) by default; ABD_CHOL_FIFO: the task-graph FIFO
+  static const bool fifo = getenv("ABD_CHOL_FIFO") != nullptr;
+  static int bpf = 0;
+  if (!fifo && !bpf) {
+    CK(cudaFuncSetAttribute(k_chol_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpf, k_chol_flow, CH_THREADS, smem));
+    bpf = std::max(bpf, 1);
+  }
+  if (!fifo) CK(cudaMemsetAsync(v.ctr, 0, 4 * sizeof(unsigned), st));
+  else {
+    const int init_n = std::max(std::max(v.n, v.n_tasks), std::max(2 * v.n_coupled, v.n_tasks - v.n_part));
+    k_chol_sched_init<<<grid_for(std::max(init_n, 4), 256), 256, 0, st>>>(v, factor ? 1 : 0);
+    note_launch("k_chol_sched_init");
+  }
   // isolated nodes on a side stream beside the task graph (joined before returning)
   if (v.n_iso > 0) {
     CK(cudaEventRecord(s.ch_fork_ev, st));
@@ -1818,7 +2137,20 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     tbuf.zero(st);
     vv.trace = tbuf.p;
   }
-  if (v.n_coupled > 0) {
+  if (v.n_coupled > 0 && !fifo) {
+    // one warp per item up to what is resident (waiting warps hold their slots)
+    const int nbo = v.n_tasks - v.n_part - v.n_coupled;
+    const int64_t items = (factor ? (int64_t)nbo : 0) + 2 * (int64_t)v.n_coupled;
+    const int fgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)s.num_sms * bpf, (items + CH_HW - 1) / CH_HW));
+    Scene::Work& w = s.w;
+    if (++w.ch_epoch <= 0) {  // wrapped: forget every flag
+      CK(cudaMemsetAsync(w.ch_fl.p, 0, w.ch_fl.cap * sizeof(int), st));
+      w.ch_epoch = 1;
+    }
+    k_chol_flow<<<fgrid, CH_THREADS, smem, st>>>(vv, b, x, factor ? 1 : 0, w.ch_epoch);
+    note_launch(factor ? "k_chol_flow(factor)" : "k_chol_flow(solve)");
+  } else if (v.n_coupled > 0) {
     k_chol_sched<<<grid, CH_THREADS, smem, st>>>(vv, b, x, factor ? 1 : 0);
     note_launch(factor ? "k_chol_sched(factor)" : "k_chol_sched(solve)");
   }
@@ -1827,7 +2159,7 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     tbuf.download(h.data(), h.size(), st);
     SSYNC(st);
     if (FILE* f = fopen(trace_path, "ab")) {
-      const int hdr[6] = {v.n, v.n_coupled, v.n_tasks, grid, v.n_part, v.n_tasks - v.n_part - v.n_coupled};
+      const int hdr[6] = {v.n, v.n_coupled, v.n_tasks, grid, fifo ? v.n_part : -1, v.n_tasks - v.n_part - v.n_coupled};
       fwrite(hdr, sizeof(int), 6, f);
       fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
       fclose(f);

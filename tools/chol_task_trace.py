@@ -28,8 +28,13 @@ def main():
     info = (rec[:, 0] >> 32).astype(np.int64)
     tpop, ts, te = rec[:, 1].astype(np.int64), rec[:, 2].astype(np.int64), rec[:, 3].astype(np.int64)
     t0 = ts.min()
-    kind = np.where(item < npart, 0, np.where(item < npart + nbo, 1, 2))
-    names = ["partial/diag", "block", "backward"]
+    if npart < 0:  # k_chol_flow: items [0, m + nbo) forward (diagonals and blocks), then backward
+        npart = 0
+        kind = np.where(item < m + nbo, 0, 2)
+        names = ["forward item", "-", "backward"]
+    else:
+        kind = np.where(item < npart, 0, np.where(item < npart + nbo, 1, 2))
+        names = ["partial/diag", "block", "backward"]
     print(f"{len(facs)} factorizations; this one: n={n} coupled={m} tasks={nt} (partials {npart}, blocks {nbo}) "
           f"grid={grid} CTAs, span {(te.max() - t0) / 1e3:.1f} us, busy {(te - ts).sum() / 1e3:.1f} warp-us")
     for kk in range(3):
