@@ -950,16 +950,16 @@ __device__ __forceinline__ void cp_wait_dyn(int k) {
   }
 }
 
-// lane 0 polls flags f0 (and f1 when >= 0) until both equal ep; every lane then
-// acquires them (orders its following loads and cp.async copies after the producer's
-// writes).  false on timeout (the flag array is left as is).
+// lane 0 polls flags f0 (and f1 when >= 0) with acquire loads until both equal ep;
+// the warp barrier then orders every lane's following loads and cp.async copies
+// after the producer's writes.  false on timeout (raised as a factorization error).
 __device__ __forceinline__ bool flow_wait(const CholView& v, const int* fl, int f0, int f1, int ep) {
   const int t = threadIdx.x & 31;
   int ok = 1;
   if (t == 0) {
     unsigned ns = 32;
     unsigned long long t0 = 0;
-    while (ld_relaxed(fl + f0) != ep || (f1 >= 0 && ld_relaxed(fl + f1) != ep)) {
+    while (ld_acquire(fl + f0) != ep || (f1 >= 0 && ld_acquire(fl + f1) != ep)) {
       const unsigned long long now = gtimer();
       if (!t0) t0 = now;
       else if (now - t0 > FLOW_TIMEOUT_NS) {
@@ -971,12 +971,31 @@ __device__ __forceinline__ bool flow_wait(const CholView& v, const int* fl, int 
       ns = min(2u * ns, 256u);
     }
   }
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (ok) {
-    (void)ld_acquire(fl + f0);
-    if (f1 >= 0) (void)ld_acquire(fl + f1);
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
+// every lane with `active` polls its flag fl[idx] (one L2 round trip per round for the
+// whole warp) until all equal ep; then a warp barrier (as flow_wait)
+__device__ __forceinline__ bool flow_wait_lanes(const CholView& v, const int* fl, bool active, int idx, int ep) {
+  const unsigned mask = 0xffffffffu;
+  bool done = !active;
+  unsigned ns = 32;
+  unsigned long long t0 = 0;
+  for (;;) {
+    if (!done) done = ld_acquire(fl + idx) == ep;
+    if (__all_sync(mask, done)) break;
+    const unsigned long long now = gtimer();
+    if (!t0) t0 = now;
+    else if (now - t0 > FLOW_TIMEOUT_NS) {
+      if ((threadIdx.x & 31) == 0) atomicMin(v.bad, -1);
+      __syncwarp(mask);
+      return false;
+    }
+    __nanosleep(ns);
+    ns = min(2u * ns, 256u);
   }
-  return ok != 0;
+  __syncwarp(mask);
+  return true;
 }
 
 // A list of U update items whose operands are L blocks a[u] (and b[u] when paired)
@@ -1041,19 +1060,28 @@ __device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool
   };
   for (int u = 0; u < U; ++u) {
     while (issued <= u) {
-      if (issued >= w.base + w.nready || issued >= w.base + 32) {
+      if (issued >= w.base + w.nready) {
         flow_window(v, w, rows, lo, U, issued, ep);
         if (w.nready == 0) {
-          // block on this item's operands, then reload the window behind it
+          // block on this item's operands (the window now starts at it); the rest of
+          // the window is polled again when reached
           const int f0 = __shfl_sync(mask, w.a, 0), f1 = rows ? -1 : __shfl_sync(mask, w.b, 0);
           ok = flow_wait(v, v.flag, f0, f1, ep) && ok;
-          flow_window(v, w, rows, lo, U, issued, ep);
-          if (w.nready == 0) w.nready = 1;  // timed out: proceed (the error is raised)
+          w.nready = 1;
         }
       }
       issue(issued++);
     }
-    while (issued < U && issued < u + NST && issued < w.base + w.nready && issued < w.base + 32) issue(issued++);
+    // issue ahead: within the window's ready run, and past a fully ready window into the
+    // next one (loaded while the staged copies are in flight)
+    while (issued < U && issued < u + NST) {
+      if (issued >= w.base + w.nready) {
+        if (w.nready < 32) break;
+        flow_window(v, w, rows, lo, U, issued, ep);
+        if (w.nready == 0) break;
+      }
+      issue(issued++);
+    }
     cp_wait_dyn(issued - u - 1);
     __syncwarp(mask);
     if (rows) acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][0], sm.vec[u % NST], t);
@@ -1063,8 +1091,9 @@ __device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool
   return ok;
 }
 
+// every lane's writes, then the warp barrier, then lane 0's release store (cumulative:
+// it publishes what the barrier ordered before it)
 __device__ __forceinline__ void flow_release(int* p, int ep) {
-  fence_acq_rel();
   __syncwarp();
   if ((threadIdx.x & 31) == 0) st_release(p, ep);
 }
@@ -1090,6 +1119,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
     idx = __shfl_sync(mask, idx, 0);
     if (idx >= total) break;
     const unsigned long long t_start = v.trace ? gtimer() : 0;
+    unsigned long long t_rdy = 0;
     if (idx < nf) {
       const int code = fac ? v.fseq[idx] : v.eord[idx];
       if (code < v.n && fac) {  // diagonal of node j: D = A_jj - sum L_jk L_jk^T, L_jj, y_j
@@ -1101,6 +1131,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
         Acc ac;
         acc_zero(ac);
         flow_accumulate(v, ac, true, e0, U, x, ep, sm);
+        if (v.trace) t_rdy = gtimer();
         cp_wait_all();
         __syncwarp(mask);
         acc_store(ac, sm.pa, sm.pv, sm.S, t);
@@ -1143,6 +1174,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
         acc_zero(ac);
         flow_accumulate(v, ac, false, u0, U, nullptr, ep, sm);
         flow_wait(v, v.flag, j, -1, ep);  // L_jj and 1 / L_jj[c][c]
+        if (v.trace) t_rdy = gtimer();
         stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
         if (t < 6) cp16(sm.pv + 2 * t, v.dinv + 12 * (int64_t)j + 2 * t);
         cp_commit();
@@ -1157,26 +1189,37 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
       const int j = v.eord[m - 1 - (idx - nf)];
       const int c0 = v.col_ptr[j], U = v.col_ptr[j + 1] - c0;
       flow_wait(v, v.flag, j, -1, ep);  // y_j (and, factoring, L_jj)
+      if (v.trace) t_rdy = gtimer();
       stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
       if (t < 6) cp16(sm.pv + 2 * t, v.dinv + 12 * (int64_t)j + 2 * t);
       cp_commit();
       double acc = ldcg(x + 12 * (int64_t)j + tt);
-      // ancestors' x_i in the column's order, each staged with its block once final
-      for (int u = 0; u < U; ++u) {
-        const int bb = c0 + u;
-        const int i = v.blk_row[bb];
-        flow_wait(v, v.xflag, i, -1, ep);
-        stage_block(sm.stage[0][0], v.L + 144 * (int64_t)(v.n + bb), t);
-        if (t < 6) cp16(sm.vec[0] + 2 * t, x + 12 * (int64_t)i + 2 * t);
+      // the column in chunks of 2 NST blocks: blocks staged once final (factoring: long
+      // before the ancestors' x), then the x_i polled together, summed in column order
+      constexpr int BW = 2 * NST;
+      for (int base = 0; base < U; base += BW) {
+        const int cnt = min(BW, U - base);
+        const bool mine = t < cnt;
+        if (fac) flow_wait_lanes(v, v.flag, mine, v.n + c0 + base + (mine ? t : 0), ep);
+        for (int l = 0; l < cnt; ++l) stage_block(sm.stage[l >> 1][l & 1], v.L + 144 * (int64_t)(v.n + c0 + base + l), t);
         cp_commit();
+        const int i_l = mine ? v.blk_row[c0 + base + t] : 0;
+        flow_wait_lanes(v, v.xflag, mine, i_l, ep);
+        for (int e = t; e < 12 * cnt; e += 32) {
+          const int l = e / 12, r = e - 12 * l;
+          const int i = v.blk_row[c0 + base + l];
+          sm.pa[e] = __ldcg(x + 12 * (int64_t)i + r);
+        }
         cp_wait_all();
         __syncwarp(mask);
-        const double* Lb = sm.stage[0][0] + tt;
-        const double* xi = sm.vec[0];
-        double s2 = 0.0;
+        for (int l = 0; l < cnt; ++l) {
+          const double* Lb = sm.stage[l >> 1][l & 1] + tt;
+          const double* xi = sm.pa + 12 * l;
+          double s2 = 0.0;
 #pragma unroll
-        for (int r = 0; r < 12; ++r) s2 = fma(Lb[12 * r], xi[r], s2);
-        acc -= s2;
+          for (int r = 0; r < 12; ++r) s2 = fma(Lb[12 * r], xi[r], s2);
+          acc -= s2;
+        }
         __syncwarp(mask);
       }
       cp_wait_all();
@@ -1197,7 +1240,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
       unsigned long long* o = v.trace + 4 * (int64_t)done;
       o[0] = (unsigned long long)(unsigned)idx;
       o[1] = t_start;
-      o[2] = t_start;
+      o[2] = t_rdy ? t_rdy : t_start;
       o[3] = gtimer();
     }
   }
@@ -2162,6 +2205,12 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
       const int hdr[6] = {v.n, v.n_coupled, v.n_tasks, grid, fifo ? v.n_part : -1, v.n_tasks - v.n_part - v.n_coupled};
       fwrite(hdr, sizeof(int), 6, f);
       fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      if (!fifo) {  // the flow items' codes (fseq): diagonal j < n, block n + b
+        const int nf = hdr[5] + v.n_coupled;
+        std::vector<int> fs(std::max(nf, 1));
+        CK(cudaMemcpy(fs.data(), v.fseq, nf * sizeof(int), cudaMemcpyDeviceToHost));
+        fwrite(fs.data(), sizeof(int), nf, f);
+      }
       fclose(f);
     }
   }

@@ -15,14 +15,18 @@ def load(path):
         off += 24
         rec = np.frombuffer(data, dtype=np.uint64, count=4 * nt, offset=off).reshape(nt, 4)
         off += 32 * nt
-        out.append((n, m, nt, grid, npart, nbo, rec))
+        fseq = None
+        if npart < 0:  # k_chol_flow traces carry the forward items' codes
+            fseq = np.frombuffer(data, dtype=np.int32, count=m + nbo, offset=off)
+            off += 4 * (m + nbo)
+        out.append((n, m, nt, grid, npart, nbo, rec, fseq))
     return out
 
 
 def main():
     facs = load(sys.argv[1])
     k = int(sys.argv[2]) if len(sys.argv) > 2 else -1
-    n, m, nt, grid, npart, nbo, rec = facs[k]
+    n, m, nt, grid, npart, nbo, rec, fseq = facs[k]
     rec = rec[rec[:, 3] > 0]
     item = (rec[:, 0] & 0xffffffff).astype(np.int64)
     info = (rec[:, 0] >> 32).astype(np.int64)
@@ -30,8 +34,18 @@ def main():
     t0 = ts.min()
     if npart < 0:  # k_chol_flow: items [0, m + nbo) forward (diagonals and blocks), then backward
         npart = 0
-        kind = np.where(item < m + nbo, 0, 2)
-        names = ["forward item", "-", "backward"]
+        code = np.where(item < m + nbo, fseq[np.minimum(item, m + nbo - 1)], -1)
+        kind = np.where(item < m + nbo, np.where(code < n, 0, 1), 2)
+        names = ["diagonal", "block", "backward"]
+        # the last diagonals in elimination order: completion times and what they waited for
+        dsel = np.nonzero(kind == 0)[0]
+        dsel = dsel[np.argsort(item[dsel])][-40:]
+        print("  last 40 diagonals: end (us from start), ready->end (us), grab->ready (us)")
+        print("   ", " ".join(f"{(te[i] - tpop.min()) / 1e3:.0f}/{(te[i] - ts[i]) / 1e3:.1f}/{(ts[i] - tpop[i]) / 1e3:.0f}"
+                            for i in dsel))
+        bsel = np.nonzero(kind == 1)[0]
+        print(f"  blocks ready->end mean {(te[bsel] - ts[bsel]).mean() / 1e3:.2f} us; diagonals ready->end mean "
+              f"{(te[kind == 0] - ts[kind == 0]).mean() / 1e3:.2f} us")
     else:
         kind = np.where(item < npart, 0, np.where(item < npart + nbo, 1, 2))
         names = ["partial/diag", "block", "backward"]
