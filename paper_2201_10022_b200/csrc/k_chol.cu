@@ -938,6 +938,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_sched(CholView v, const dou
 // deadlock, whatever its size or residency.  A wait longer than FLOW_TIMEOUT_NS
 // (an inconsistent plan) raises a factorization error instead of hanging.
 constexpr unsigned long long FLOW_TIMEOUT_NS = 2000000000ull;
+constexpr unsigned FLOW_SLEEP_MAX = 64;  // poll back-off cap (ns): the flag hop is on the critical path
 
 __device__ __forceinline__ void cp_wait_dyn(int k) {
   switch (k) {
@@ -968,7 +969,7 @@ __device__ __forceinline__ bool flow_wait(const CholView& v, const int* fl, int 
         break;
       }
       __nanosleep(ns);
-      ns = min(2u * ns, 256u);
+      ns = min(2u * ns, FLOW_SLEEP_MAX);
     }
   }
   return __shfl_sync(0xffffffffu, ok, 0) != 0;
@@ -992,7 +993,7 @@ __device__ __forceinline__ bool flow_wait_lanes(const CholView& v, const int* fl
       return false;
     }
     __nanosleep(ns);
-    ns = min(2u * ns, 256u);
+    ns = min(2u * ns, FLOW_SLEEP_MAX);
   }
   __syncwarp(mask);
   return true;
@@ -1307,6 +1308,12 @@ enum { CH_LEAVES, CH_ISO, CH_PARENT, CH_NCHILD, CH_CHILDP, CH_CHILDI, CH_COLP, C
 // task splitting: a diagonal (row products) or block (update pairs) task with more
 // than PART_MIN products is split into chunks of PART_CHUNK
 constexpr int PART_MIN = 12, PART_CHUNK = 8;
+// ABD_CHOL_FIFO: factor on the task-graph FIFO (k_chol_sched) instead of the dataflow
+// schedule (k_chol_flow); only the FIFO needs the task-graph sections of the plan
+static bool chol_fifo() {
+  static const bool f = getenv("ABD_CHOL_FIFO") != nullptr;
+  return f;
+}
 
 static CholView plan_view(Scene& s) {
   Scene::Work& w = s.w;
@@ -1917,6 +1924,10 @@ static Analysis chol_analyze(Scene& s) {
   an.ms_sub[4] = ms_since(t0);
   // task graph: elimination-tree parents, child lists, leaves (deepest first), isolated nodes
   std::vector<int>&par = w.hs_i[26], &dep = w.hs_i[27], &leaves = w.hs_i[28];
+  const bool fifo = chol_fifo();
+  static const bool trace_cp = getenv("ABD_TRACE_CHOL") != nullptr;
+  leaves.clear();
+  if (fifo || trace_cp) {
   par.assign(m, -1);
   for (int v = 0; v < m; ++v)
     if (csp[v + 1] > csp[v]) par[v] = csi[csp[v]];
@@ -1925,18 +1936,20 @@ static Analysis chol_analyze(Scene& s) {
     const int v = order[q];
     dep[v] = par[v] < 0 ? 0 : dep[par[v]] + 1;
   }
-  std::vector<int> nch(m, 0);
-  for (int v = 0; v < m; ++v)
-    if (par[v] >= 0) nch[par[v]]++;
-  leaves.clear();
-  for (int v = 0; v < m; ++v)
-    if (nch[v] == 0) leaves.push_back(v);
-  std::sort(leaves.begin(), leaves.end(),
-            [&](int a2, int b2) { return dep[a2] != dep[b2] ? dep[a2] > dep[b2] : glob[a2] < glob[b2]; });
+  }
+  std::vector<int>& nch = w.hs_i[25];
+  if (fifo) {
+    nch.assign(m, 0);
+    for (int v = 0; v < m; ++v)
+      if (par[v] >= 0) nch[par[v]]++;
+    for (int v = 0; v < m; ++v)
+      if (nch[v] == 0) leaves.push_back(v);
+    std::sort(leaves.begin(), leaves.end(),
+              [&](int a2, int b2) { return dep[a2] != dep[b2] ? dep[a2] > dep[b2] : glob[a2] < glob[b2]; });
+  }
   const int n_leaves = (int)leaves.size();
   const int n_iso = n - m;
   an.n_cta = 0;  // set at launch
-  static const bool trace_cp = getenv("ABD_TRACE_CHOL") != nullptr;
   if (trace_cp) {  // task costs in 12x12 block products: rows + sum over column blocks (1 + updates)
     std::vector<int64_t> cost(m, 0), cp(m, 0);
     int64_t tot = 0, maxc = 0, maxcp = 0;
@@ -1964,7 +1977,7 @@ static Analysis chol_analyze(Scene& s) {
   auto nparts = [&](int k) { return (!no_split && k > PART_MIN) ? (k + PART_CHUNK - 1) / PART_CHUNK : 1; };
   auto bparts = [&](int k) { const int q = nparts(k); return q > 1 ? q : 0; };
   int64_t n_part = 0, n_init = 0;
-  {
+  if (fifo) {
     std::vector<int> per(m, 0);
     for (int v = 0; v < m; ++v) {
       per[v] = nparts(rcnt[v + 1] - rcnt[v]);
@@ -1978,10 +1991,11 @@ static Analysis chol_analyze(Scene& s) {
   //              part (int4) | dnp | bpart | bnp | init
   size_t o[CH_NSEC + 1];
   o[0] = 0;
-  const size_t len[CH_NSEC] = {(size_t)n_leaves, (size_t)n_iso, (size_t)n, (size_t)n, (size_t)n + 1, (size_t)m,
+  const size_t nf = fifo ? (size_t)n : 0, mf = fifo ? (size_t)m : 0, bf = fifo ? (size_t)nbo : 0;
+  const size_t len[CH_NSEC] = {(size_t)n_leaves, (size_t)n_iso, nf, nf, fifo ? nf + 1 : 0, mf,
                                (size_t)n + 1, (size_t)nbo, (size_t)nbo, (size_t)n + 1, (size_t)nbo, (size_t)nbo,
-                               (size_t)nbo + 1, upd.size(), (size_t)n + 1, 4 * (size_t)n_part, (size_t)n,
-                               (size_t)nbo, (size_t)nbo, (size_t)n_init, (size_t)m + nbo, (size_t)m};
+                               (size_t)nbo + 1, upd.size(), fifo ? nf + 1 : 0, 4 * (size_t)n_part, nf,
+                               bf, bf, (size_t)n_init, (size_t)m + nbo, (size_t)m};
   for (int k = 0; k < CH_NSEC; ++k) {
     o[k + 1] = o[k] + len[k];
     if (k + 1 == CH_UPD) o[k + 1] += o[k + 1] & 1;          // int2 alignment of the update pairs
@@ -1999,14 +2013,14 @@ static Analysis chol_analyze(Scene& s) {
   int* nchild = hp + o[CH_NCHILD];
   int* child_ptr = hp + o[CH_CHILDP];
   int* child_idx = hp + o[CH_CHILDI];
-  for (int v = 0; v < n; ++v) {
-    const int l = loc[v];
-    parent[v] = (l >= 0 && par[l] >= 0) ? glob[par[l]] : -1;
-    nchild[v] = l >= 0 ? nch[l] : 0;
-  }
-  child_ptr[0] = 0;
-  for (int v = 0; v < n; ++v) child_ptr[v + 1] = child_ptr[v] + nchild[v];
-  {
+  if (fifo) {
+    for (int v = 0; v < n; ++v) {
+      const int l = loc[v];
+      parent[v] = (l >= 0 && par[l] >= 0) ? glob[par[l]] : -1;
+      nchild[v] = l >= 0 ? nch[l] : 0;
+    }
+    child_ptr[0] = 0;
+    for (int v = 0; v < n; ++v) child_ptr[v + 1] = child_ptr[v] + nchild[v];
     std::vector<int> fill(child_ptr, child_ptr + n);
     for (int v = 0; v < n; ++v)  // children in ascending node order (deterministic)
       if (parent[v] >= 0) child_idx[fill[parent[v]]++] = v;
@@ -2036,7 +2050,7 @@ static Analysis chol_analyze(Scene& s) {
     col_ptr[n] = c;
     row_ptr[n] = r;
   }
-  {
+  if (fifo) {
     // partial tasks per global node: its diagonal's chunks of the row list, then each
     // column block's chunks of its update pairs (equal splits)
     int* partp = hp + o[CH_PARTP];
@@ -2146,7 +2160,7 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     bps = std::max(bps, 1);
   }
   // dataflow schedule (k_chol_flow) by default; ABD_CHOL_FIFO: the task-graph FIFO
-  static const bool fifo = getenv("ABD_CHOL_FIFO") != nullptr;
+  const bool fifo = chol_fifo();
   static int bpf = 0;
   if (!fifo && !bpf) {
     CK(cudaFuncSetAttribute(k_chol_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
