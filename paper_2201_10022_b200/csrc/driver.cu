@@ -568,6 +568,7 @@ static void mark_structure(Scene& s) {
     if (!w.ch_act_ev) CK(cudaEventCreateWithFlags(&w.ch_act_ev, cudaEventDisableTiming));
     CK(cudaEventRecord(w.ch_act_ev, s.stream));
     w.ch_verify = true;
+    chol_verify_post(s);  // the worker checks (and re-analyses) beside the pair blocks
     return;
   }
   const int64_t n_off = s.H.n_off;

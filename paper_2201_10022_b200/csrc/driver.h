@@ -19,6 +19,7 @@ void launch_neg(cudaStream_t st, int64_t n, const double* a, double* b);  // b =
 // discarded when the pattern changes (drop)
 void chol_analysis_post(Scene& s);
 void chol_analysis_drop(Scene& s);
+void chol_verify_post(Scene& s);
 int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed);
 void spmv(Scene& s, const double* x, double* y);
 void load_bsr(Scene& s, int n, int bdim, const double* diag, int64_t n_off, const int64_t* keys, const double* off);

@@ -2241,15 +2241,18 @@ static void launch_resid(Scene& s, const double* rhs, const double* x) {
   pack_to_host(st, s.h_pinned + 24, {{w.scal.p + 4, 16, 0}, {w.bad.p, 4, 32}});
 }
 
+static void chol_verify_core(Scene& s, Analysis& an);
+
 // ---------------------------------------------------------------------------
-// analysis worker: one host thread per scene, one job at a time
+// analysis worker: one host thread per scene, one job at a time; a verify request
+// (mark_structure after a speculative analysis) runs after the job, on the worker
 namespace {
 struct CholWorker {
   Scene* s = nullptr;
   std::thread th;
   std::mutex mu;
   std::condition_variable cv;
-  bool job = false, quit = false, has_result = false;
+  bool job = false, vreq = false, quit = false, has_result = false;
   Analysis result;
   std::exception_ptr err;
   explicit CholWorker(Scene* sc) : s(sc) {
@@ -2266,28 +2269,56 @@ struct CholWorker {
   void loop() {
     for (;;) {
       std::unique_lock<std::mutex> lk(mu);
-      cv.wait(lk, [this] { return job || quit; });
+      cv.wait(lk, [this] { return job || vreq || quit; });
       if (quit) return;
-      lk.unlock();
-      Analysis a;
-      std::exception_ptr e;
-      try {
-        a = chol_analyze(*s);
-      } catch (...) {
-        e = std::current_exception();
+      if (job) {
+        lk.unlock();
+        Analysis a;
+        std::exception_ptr e;
+        try {
+          a = chol_analyze(*s);
+        } catch (...) {
+          e = std::current_exception();
+        }
+        lk.lock();
+        result = a;
+        err = e;
+        has_result = true;
+        job = false;
+      } else {
+        // the actual structure against the speculative plan (re-analysed on a miss)
+        Analysis a = result;
+        const bool run = has_result && !err;
+        lk.unlock();
+        std::exception_ptr e;
+        if (run) {
+          try {
+            chol_verify_core(*s, a);
+          } catch (...) {
+            e = std::current_exception();
+          }
+        }
+        lk.lock();
+        if (run) {
+          result = a;
+          err = e;
+        }
+        vreq = false;
       }
-      lk.lock();
-      result = a;
-      err = e;
-      has_result = true;
-      job = false;
       lk.unlock();
       cv.notify_all();
     }
   }
+  void request_verify() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      vreq = true;
+    }
+    cv.notify_all();
+  }
   void post() {
     std::unique_lock<std::mutex> lk(mu);
-    cv.wait(lk, [this] { return !job; });
+    cv.wait(lk, [this] { return !job && !vreq; });
     has_result = false;
     err = nullptr;
     job = true;
@@ -2297,7 +2328,7 @@ struct CholWorker {
   // waits for the job in flight; true (and the analysis) when one was posted
   bool take(Analysis& out) {
     std::unique_lock<std::mutex> lk(mu);
-    cv.wait(lk, [this] { return !job; });
+    cv.wait(lk, [this] { return !job && !vreq; });
     if (!has_result) return false;
     has_result = false;
     if (err) {
@@ -2340,6 +2371,20 @@ static void chol_verify_early(Scene& s, Analysis& an) {
   Scene::Work& w = s.w;
   if (!w.ch_verify) return;
   w.ch_verify = false;
+  chol_verify_core(s, an);
+}
+
+// hand the check to the worker (it runs after the speculative analysis, overlapping
+// the pair blocks and the reduction); without a worker chol_begin does it
+void chol_verify_post(Scene& s) {
+  CholWorker* wk = worker(s, false);
+  if (!wk) return;
+  s.w.ch_verify = false;
+  wk->request_verify();
+}
+
+static void chol_verify_core(Scene& s, Analysis& an) {
+  Scene::Work& w = s.w;
   CK(cudaEventSynchronize(w.ch_act_ev));
   const int64_t n_off = s.H.n_off;
   const int* f2 = w.h_meta2.p;

@@ -58,17 +58,21 @@ bycat = collections.Counter()
 for e in gpu:
     bycat[e["cat"]] += e["dur"]
 print("busy by category:", dict(bycat))
+# true idle time: no op on any stream; each gap keyed by the op that ended last before
+# it and the op that starts it
 gaps = collections.defaultdict(lambda: [0, 0.0])
 gap_tot = 0.0
-for a, b in zip(gpu, gpu[1:]):
-    g = b["ts"] - (a["ts"] + a["dur"])
-    if g <= 0:
-        continue
-    gap_tot += g
-    key = a["name"].split("(")[0][:48] + " -> " + b["name"].split("(")[0][:48]
-    gaps[key][0] += 1
-    gaps[key][1] += g
-print(f"idle gaps total {gap_tot:.0f}us")
+end, last = gpu[0]["ts"] + gpu[0]["dur"], gpu[0]
+for b in gpu[1:]:
+    g = b["ts"] - end
+    if g > 0:
+        gap_tot += g
+        key = last["name"].split("(")[0][:48] + " -> " + b["name"].split("(")[0][:48]
+        gaps[key][0] += 1
+        gaps[key][1] += g
+    if b["ts"] + b["dur"] > end:
+        end, last = b["ts"] + b["dur"], b
+print(f"idle (no op on any stream) total {gap_tot:.0f}us")
 for k, (n, g) in sorted(gaps.items(), key=lambda kv: -kv[1][1])[:45]:
     print(f"  {g:9.0f}us n={n:5d} avg={g / n:7.1f}us  {k}")
 kt = collections.defaultdict(lambda: [0, 0.0])
@@ -79,3 +83,13 @@ for e in gpu:
 print("device time by op:")
 for k, (n, d) in sorted(kt.items(), key=lambda kv: -kv[1][1])[:40]:
     print(f"  {d:9.0f}us n={n:5d} avg={d / n:7.1f}us  {k}")
+
+# one Newton iteration in the middle of the last step: ops with stream, start, duration
+if os.environ.get("ABD_TIMELINE_ITER"):
+    ks = [i for i, e in enumerate(gpu) if e["name"].startswith("abd::k_chol_flow") or e["name"].startswith("abd::k_chol_sched")]
+    if len(ks) > 3:
+        a, b = ks[len(ks) // 2], ks[len(ks) // 2 + 1]
+        t_a = gpu[a]["ts"]
+        print("one iteration (us from the Cholesky launch; stream; duration):")
+        for e in gpu[a:b + 1]:
+            print(f"  {e['ts'] - t_a:8.1f} s{e.get('args', {}).get('stream', '?'):<3} {e['dur']:7.1f}  {e['name'].split('(')[0][:70]}")
