@@ -101,6 +101,8 @@ struct CholView {
   const int* eord;      // n_coupled: coupled nodes in elimination order
   int* flag;            // n + nbo: = epoch once L block (factor) / y_j (solve, index j) is final
   int* xflag;           // n: = epoch once x_j (backward substitution) is final
+  int* sflag;           // n: = epoch once sbuf[k] (the parent block's update sum of column k) is final
+  double* sbuf;         // n x 144: S_pk = A_pk - sum L_pi L_ki^T of each column's parent block p
 };
 constexpr int PART_STRIDE = 156;  // 12 x 13 (the forward-substitution column rides along)
 
@@ -244,6 +246,7 @@ struct WarpSmem {
   double pl[144];             // prefetched L_jj (block task)
   double pv[12];              // prefetched b_j (diagonal task) / 1 / L_jj[c][c] (block task)
   double S[12][13];           // result rows (+ the forward-substitution column) / L_jj rows
+  double dv[NST][12];         // 1 / L_kk[c][c] per stage (k_chol_flow: a child's parent block)
 };
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
@@ -458,20 +461,15 @@ __device__ __forceinline__ void chol_block(const CholView& v, int bb, WarpSmem& 
   block_finish(v, bb, sm);
 }
 
-// S = A_ij - sum (in sm.S), L_jj in sm.pl, 1 / L_jj[c][c] in sm.pv: L_ij = S L_jj^-T
-__device__ __forceinline__ void block_finish(const CholView& v, int bb, WarpSmem& sm) {
-  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
-  const unsigned mask = 0xffffffffu;
-  double (*S)[13] = sm.S;
+// lane t: row t of X with X L_jj^T = B (forward substitution against the rows of
+// L_jj); brow = row t of B (stride 1), Lj = L_jj rows, rinv = 1 / L_jj[c][c]
+__device__ __forceinline__ void trsm_row(const double* brow, const double* Lj, const double* rv, double xr[12]) {
   double bt[12], rinv[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) {
-    bt[c] = S[tt][c];
-    rinv[c] = sm.pv[c];
+    bt[c] = brow[c];
+    rinv[c] = rv[c];
   }
-  // row t of X with X L_jj^T = B (forward substitution against the rows of L_jj)
-  const double* Lj = sm.pl;
-  double xr[12];
 #pragma unroll
   for (int c = 0; c < 12; ++c) {
     double s = bt[c];
@@ -480,6 +478,14 @@ __device__ __forceinline__ void block_finish(const CholView& v, int bb, WarpSmem
       if (m < c) s = fma(-Lj[12 * c + m], xr[m], s);
     xr[c] = s * rinv[c];
   }
+}
+
+// S = A_ij - sum (in sm.S), L_jj in sm.pl, 1 / L_jj[c][c] in sm.pv: L_ij = S L_jj^-T
+__device__ __forceinline__ void block_finish(const CholView& v, int bb, WarpSmem& sm) {
+  const int t = threadIdx.x & 31, tt = t < 12 ? t : 0;
+  const unsigned mask = 0xffffffffu;
+  double xr[12];
+  trsm_row(sm.S[tt], sm.pl, sm.pv, xr);
   __syncwarp(mask);
   if (t < 12) {
     double* Lo = v.L + 144 * (int64_t)(v.n + bb) + 12 * t;
@@ -999,6 +1005,13 @@ __device__ __forceinline__ bool flow_wait_lanes(const CholView& v, const int* fl
   return true;
 }
 
+// every lane's writes, then the warp barrier, then lane 0's release store (cumulative:
+// it publishes what the barrier ordered before it)
+__device__ __forceinline__ void flow_release(int* p, int ep) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) st_release(p, ep);
+}
+
 // A list of U update items whose operands are L blocks a[u] (and b[u] when paired)
 // read through a window of 32 items held one per lane: their operand indices and
 // readiness are loaded together (one L2 round trip for 32 flags), so items whose
@@ -1019,7 +1032,11 @@ __device__ __forceinline__ void flow_window(const CholView& v, FlowWin& w, bool 
     if (rows) {
       w.a = v.row_blk[lo + u];
       w.c = v.row_col[lo + u];
-      rdy = ld_relaxed(v.flag + w.a) == ep;
+      // L_jk of a child k (j = k's parent: the first block of column k) is this
+      // diagonal's to finish: ready once k's diagonal and its update sum S_jk are
+      w.b = w.a - v.n == v.col_ptr[w.c];
+      rdy = w.b ? (ld_relaxed(v.sflag + w.c) == ep && ld_relaxed(v.flag + w.c) == ep)
+                : ld_relaxed(v.flag + w.a) == ep;
     } else {
       const int2 pq = v.upd[lo + u];
       w.a = pq.x;
@@ -1047,16 +1064,24 @@ __device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool
   FlowWin w;
   int issued = 0;
   bool ok = true;
+  unsigned fin = 0;  // stages holding a child's parent block to finish (bit = stage)
   auto issue = [&](int u) {
     const int src = u - w.base;
     const int a = __shfl_sync(mask, w.a, src);
     const int bb = __shfl_sync(mask, rows ? w.c : w.b, src);
-    stage_block(sm.stage[u % NST][0], v.L + 144 * (int64_t)a, t);
-    if (rows) {
-      if (t < 6) cp16(sm.vec[u % NST] + 2 * t, x + 12 * (int64_t)bb + 2 * t);
+    const int par = rows ? __shfl_sync(mask, w.b, src) : 0;
+    const int sl = u % NST;
+    if (par) {  // S_jk, L_kk, 1 / L_kk[c][c], y_k
+      stage_block(sm.stage[sl][0], v.sbuf + 144 * (int64_t)bb, t);
+      stage_block(sm.stage[sl][1], v.L + 144 * (int64_t)bb, t);
+      if (t < 6) cp16(sm.dv[sl] + 2 * t, v.dinv + 12 * (int64_t)bb + 2 * t);
+      fin |= 1u << sl;
     } else {
-      stage_block(sm.stage[u % NST][1], v.L + 144 * (int64_t)bb, t);
+      fin &= ~(1u << sl);
+      stage_block(sm.stage[sl][0], v.L + 144 * (int64_t)a, t);
+      if (!rows) stage_block(sm.stage[sl][1], v.L + 144 * (int64_t)bb, t);
     }
+    if (rows && t < 6) cp16(sm.vec[sl] + 2 * t, x + 12 * (int64_t)bb + 2 * t);
     cp_commit();
   };
   for (int u = 0; u < U; ++u) {
@@ -1066,7 +1091,9 @@ __device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool
         if (w.nready == 0) {
           // block on this item's operands (the window now starts at it); the rest of
           // the window is polled again when reached
-          const int f0 = __shfl_sync(mask, w.a, 0), f1 = rows ? -1 : __shfl_sync(mask, w.b, 0);
+          const int a0 = __shfl_sync(mask, w.a, 0), b0 = __shfl_sync(mask, w.b, 0), c0 = __shfl_sync(mask, w.c, 0);
+          const int f0 = rows ? (b0 ? (int)(v.sflag - v.flag) + c0 : a0) : a0;
+          const int f1 = rows ? (b0 ? c0 : -1) : b0;
           ok = flow_wait(v, v.flag, f0, f1, ep) && ok;
           w.nready = 1;
         }
@@ -1085,6 +1112,26 @@ __device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool
     }
     cp_wait_dyn(issued - u - 1);
     __syncwarp(mask);
+    if (rows && ((fin >> (u % NST)) & 1u)) {
+      // a child's parent block: L_jk = S_jk L_kk^-T here (one flag hop and one block
+      // staging fewer on the critical path than a block task), published for the
+      // other updates and the backward substitution, then its product
+      const int sl = u % NST;
+      const int fb = v.row_blk[lo + u];
+      double xr[12];
+      trsm_row(sm.stage[sl][0] + 12 * (t < 12 ? t : 0), sm.stage[sl][1], sm.dv[sl], xr);
+      __syncwarp(mask);
+      if (t < 12) {
+        double* Lo = v.L + 144 * (int64_t)fb + 12 * t;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) {
+          sm.stage[sl][0][12 * t + c] = xr[c];
+          Lo[c] = xr[c];
+        }
+      }
+      flow_release(v.flag + fb, ep);
+      __syncwarp(mask);
+    }
     if (rows) acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][0], sm.vec[u % NST], t);
     else acc_sub_xyt(ac, sm.stage[u % NST][0], sm.stage[u % NST][1], nullptr, t);
     __syncwarp(mask);
@@ -1092,12 +1139,6 @@ __device__ __forceinline__ bool flow_accumulate(const CholView& v, Acc& ac, bool
   return ok;
 }
 
-// every lane's writes, then the warp barrier, then lane 0's release store (cumulative:
-// it publishes what the barrier ordered before it)
-__device__ __forceinline__ void flow_release(int* p, int ep) {
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) st_release(p, ep);
-}
 
 // Persistent dataflow factor (+ forward and backward substitution); !factor: the two
 // substitutions with the resident factor.  Items: factor: [0, m + nbo) fseq, then m
@@ -1174,6 +1215,21 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
         Acc ac;
         acc_zero(ac);
         flow_accumulate(v, ac, false, u0, U, nullptr, ep, sm);
+        if (bb == v.col_ptr[j]) {
+          // j's parent block: publish S = A_pj - sum for the parent's diagonal, which
+          // finishes L_pj itself
+          cp_wait_all();
+          __syncwarp(mask);
+          acc_store(ac, ap >= 0 ? sm.pa : nullptr, nullptr, sm.S, t);
+          __syncwarp(mask);
+          if (t < 12) {
+            double* So = v.sbuf + 144 * (int64_t)j + 12 * t;
+#pragma unroll
+            for (int c = 0; c < 12; ++c) So[c] = sm.S[t][c];
+          }
+          flow_release(v.sflag + j, ep);
+          goto item_done;
+        }
         flow_wait(v, v.flag, j, -1, ep);  // L_jj and 1 / L_jj[c][c]
         if (v.trace) t_rdy = gtimer();
         stage_block(sm.pl, v.L + 144 * (int64_t)j, t);
@@ -1236,6 +1292,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol_flow(CholView v, const doub
       if (t < 12) x[12 * (int64_t)j + t] = xv;
       flow_release(v.xflag + j, ep);
     }
+  item_done:
     if (v.trace && t == 0) {
       const unsigned done = atomicAdd(v.ctr + 3, 1u);
       unsigned long long* o = v.trace + 4 * (int64_t)done;
@@ -1370,6 +1427,8 @@ static CholView plan_view(Scene& s) {
   v.eord = dp + o[CH_EORD];
   v.flag = w.ch_fl.p;
   v.xflag = w.ch_fl.p + n + nbo;
+  v.sflag = w.ch_fl.p + 2 * n + nbo;
+  v.sbuf = w.ch_sbuf.p;
   return v;
 }
 
@@ -2123,7 +2182,8 @@ static Analysis chol_analyze(Scene& s) {
   {
     // epoch flags of k_chol_flow: zeroed when (re)allocated, never reset otherwise
     const size_t cap0 = w.ch_fl.cap;
-    w.ch_fl.resize(2 * (size_t)n + nbo + 1);
+    w.ch_fl.resize(3 * (size_t)n + nbo + 1);
+    w.ch_sbuf.resize(144 * (size_t)std::max(n, 1));
     if (w.ch_fl.cap != cap0) CK(cudaMemsetAsync(w.ch_fl.p, 0, w.ch_fl.cap * sizeof(int), st));
   }
   cc.valid = true;
@@ -2189,8 +2249,10 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
   static const char* trace_path = getenv("ABD_CHOL_TRACE_TASKS");  // tools: per-task timeline of factorizations
   static DVec<unsigned long long> tbuf;
   CholView vv = v;
+  // trace slots: the FIFO's tasks, or the flow's items (diagonals, blocks, backward)
+  const int n_trace = fifo ? v.n_tasks : v.n_tasks + v.n_coupled;
   if (trace_path && factor) {
-    tbuf.resize(4 * (int64_t)std::max(v.n_tasks, 1));
+    tbuf.resize(4 * (int64_t)std::max(n_trace, 1));
     tbuf.zero(st);
     vv.trace = tbuf.p;
   }
@@ -2212,11 +2274,11 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
     note_launch(factor ? "k_chol_sched(factor)" : "k_chol_sched(solve)");
   }
   if (trace_path && factor) {
-    std::vector<unsigned long long> h(4 * (int64_t)std::max(v.n_tasks, 1));
+    std::vector<unsigned long long> h(4 * (int64_t)std::max(n_trace, 1));
     tbuf.download(h.data(), h.size(), st);
     SSYNC(st);
     if (FILE* f = fopen(trace_path, "ab")) {
-      const int hdr[6] = {v.n, v.n_coupled, v.n_tasks, grid, fifo ? v.n_part : -1, v.n_tasks - v.n_part - v.n_coupled};
+      const int hdr[6] = {v.n, v.n_coupled, n_trace, grid, fifo ? v.n_part : -1, v.n_tasks - v.n_part - v.n_coupled};
       fwrite(hdr, sizeof(int), 6, f);
       fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
       if (!fifo) {  // the flow items' codes (fseq): diagonal j < n, block n + b

@@ -299,7 +299,8 @@ struct Scene {
     DVec<int> ch_flags, ch_plan, ch_apos, ch_dep, ch_bleft, ch_queue, ch_dleft, ch_bgate;
     DVec<double> ch_scratch;  // partial sums of split factor tasks
     DVec<unsigned> ch_ctr;
-    DVec<int> ch_fl;   // k_chol_flow readiness flags (L blocks, then x)
+    DVec<int> ch_fl;   // k_chol_flow readiness flags (L blocks, x, parent-block sums)
+    DVec<double> ch_sbuf;  // k_chol_flow parent-block update sums (n x 144)
     int ch_epoch = 0;  // k_chol_flow launches so far (the flag value of the next one is + 1)
     DVec<double> ch_L, ch_dinv;
     HostPinned<int> h_plan, h_meta;
