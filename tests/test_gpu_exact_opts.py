@@ -13,6 +13,9 @@ and off, and the final states are compared bit for bit:
 * ABD_GMD_EXHAUSTIVE  -- end-of-step global minimum distance by the widened broad phase
 * ABD_MOLL_SERIAL     -- mollified EE pair blocks on a side stream beside the plain EE pairs
 
+The Cholesky's dataflow schedule (default) against the FIFO task graph with unsplit
+tasks (ABD_CHOL_FIFO + ABD_CHOL_NO_SPLIT) is compared the same way on the late pile.
+
 Speculative Cholesky analyses (of a rejected line-search trial's structure, or of a
 predicted next iterate right after the solve; ABD_CHOL_NO_SPECULATE) can change the
 elimination plan and so the rounding, like the step-local order reuse: they are held
@@ -179,3 +182,27 @@ def test_optimisations_are_bitwise_exact_on_the_full_pile(tmp_path):
     assert np.array_equal(res["on"]["its"], res["off"]["its"])
     assert np.array_equal(res["on"]["q"], res["off"]["q"])
     assert np.array_equal(res["on"]["q_dot"], res["off"]["q_dot"])
+
+
+def test_flow_schedule_equals_task_graph_on_the_deep_pile(tmp_path):
+    """The dataflow Cholesky schedule (k_chol_flow: owner-computes items with
+    readiness flags, a child's parent block finished by the parent's diagonal) sums
+    every update list in the same fixed order as the FIFO task graph with unsplit
+    tasks (ABD_CHOL_FIFO + ABD_CHOL_NO_SPLIT), so the two give the same bits.  Run on
+    the late pile (step-190 checkpoint: a 60-level elimination tree, 0.5 M
+    candidates), stepped resident as bench.py does."""
+    ckpt = os.path.join(ROOT, "bench_data", "pile_step190.npz")
+    res = {}
+    for tag, extra in (("flow", {}), ("fifo", {"ABD_CHOL_FIFO": "1", "ABD_CHOL_NO_SPLIT": "1"})):
+        out = str(tmp_path / f"pile190_{tag}.npz")
+        env = dict(os.environ)
+        for k in ("ABD_CHOL_FIFO", "ABD_CHOL_NO_SPLIT"):
+            env.pop(k, None)
+        env.update(extra)
+        r = subprocess.run([sys.executable, "-c", PILE_CHILD.format(root=ROOT, ckpt=ckpt), out, "3"], env=env,
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[tag] = np.load(out)
+    assert np.array_equal(res["flow"]["its"], res["fifo"]["its"])
+    assert np.array_equal(res["flow"]["q"], res["fifo"]["q"])
+    assert np.array_equal(res["flow"]["q_dot"], res["fifo"]["q_dot"])
