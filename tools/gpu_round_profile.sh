@@ -16,7 +16,7 @@ timeout 1200 python tools/measure_traffic.py --workload pile --steps 1 > $O/${TA
 cp profiles/fp64_peak.json $O/fp64_peak.json 2>/dev/null
 timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $O/${TAG}_bench_line.json 2> $O/${TAG}_bench.err
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launch_list.csv $ONE > $O/${TAG}_ncu_launch.log 2>&1
-for k in k_chol_sched k_prim_pairs2 k_ccd_hot k_energy_all; do
+for k in k_chol_flow k_prim_pairs2 k_ccd_hot k_energy_all; do
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"^${k}$" -s 20 -c 1 -o $O/${TAG}_${k} $ONE > $O/${TAG}_ncu_${k}.log 2>&1
 done
 timeout 1500 python bench.py --workload micro --steps 3 --warmup 1 > $O/${TAG}_bench_micro.json 2> $O/${TAG}_bench_micro.err
