@@ -372,14 +372,17 @@ constexpr int P2_THREADS = 256;
 constexpr int P2_VCAP = 256;
 constexpr int P2_HCAP = 1024;  // hits per (pair, product) sorted in shared memory
 
-// box of a primitive from packed local vertex ids (8 bits each, P2_VCAP = 256)
+// box of a primitive from packed local vertex ids (8 bits each, P2_VCAP = 256); vertex
+// boxes lie P2_VBS = 7 doubles apart in shared memory: the gathers of a half warp then
+// fall into distinct banks for 16 consecutive vertices (6 doubles apart they share 8)
+constexpr int P2_VBS = 7;
 __device__ __forceinline__ void box_from_packed(int kind, unsigned pk, const double* vb, double* bx) {
-  const double* s0 = vb + 6 * (pk & 0xffu);
+  const double* s0 = vb + P2_VBS * (pk & 0xffu);
 #pragma unroll
   for (int k = 0; k < 6; ++k) bx[k] = s0[k];
   const int nv = kind == 0 ? 1 : (kind == 1 ? 2 : 3);
   for (int m = 1; m < nv; ++m) {
-    const double* sm = vb + 6 * ((pk >> (8 * m)) & 0xffu);
+    const double* sm = vb + P2_VBS * ((pk >> (8 * m)) & 0xffu);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       bx[k] = fmin(bx[k], sm[k]);
@@ -458,8 +461,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
                   unsigned long long* work, const int* n_ov_dev) {
   if (n_ov_dev) n_ov = *n_ov_dev;  // deferred count (Verlet-list filter result, no host sync)
   extern __shared__ double p2_sm[];
-  double* vb = p2_sm;                   // [2][P2_VCAP][6] vertex boxes of i and j
-  double* obx = vb + 2 * 6 * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
+  double* vb = p2_sm;                        // [2][P2_VCAP][P2_VBS] vertex boxes of i and j
+  double* obx = vb + 2 * P2_VBS * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
   // survivor lists (list l = 3 side + kind) with per-kind capacities cap_k = (V, E, T)
   const int ltot = 2 * (cap_k.x + cap_k.y + cap_k.z);
   int* lists = reinterpret_cast<int*>(obx + 6 * (size_t)cap_list);  // [ltot] local ids
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   __shared__ int lcount[6];
   __shared__ double obox[6];
   __shared__ int gfirst[6], gcount[6], ghits;
+  __shared__ int glh[6];  // surviving groups per list
   __shared__ int hitg[256];
   // pairs are handed out dynamically (their costs vary by orders of magnitude);
   // multi-GPU (owner != null): this rank takes the overlap pairs of its slab -- the
@@ -520,26 +524,19 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       gfirst[l] = a;
       gcount[l] = gr.off[kind][body + 1] - a;
       nrun[l] = 0;
+      glh[l] = 0;
       if (l == 0) {
         ghits = 0;
         runs_ok = RUNS ? 1 : 0;
       }
     }
     __syncthreads();
-    // vertex boxes of both bodies
-    for (int t = threadIdx.x; t < 2 * P2_VCAP; t += P2_THREADS) {
-      const int side = t / P2_VCAP, lv = t % P2_VCAP;
-      if (lv < meta[6 + 3 * side]) {
-        const int body = side ? bj : bi;
-        vertex_box(g.rest, meta[3 * side] + lv, g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h,
-                   vb + 6 * (side * P2_VCAP + lv));
-      }
-    }
-    __syncthreads();
-    if (use_groups && gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5] <= 256) {
-      // cull in two stages: (a) the static groups of 32 primitives of the six lists
-      // against the overlap box (conservative swept boxes of their rest AABBs);
-      // (b) the primitives of the surviving groups, one warp per group
+    // cull in two stages: (a) the static groups of 32 primitives of the six lists
+    // against the overlap box (conservative swept boxes of their rest AABBs: no vertex
+    // box needed, so a pair none of whose products keeps a group on both sides ends
+    // here); (b) the primitives of the surviving groups, one warp per group
+    const bool grouped = use_groups && gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5] <= 256;
+    if (grouped) {
       const int gt = gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5];
       for (int t = threadIdx.x; t < gt; t += P2_THREADS) {
         int l = 0, r = t;
@@ -553,9 +550,28 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
                   g.q1 + 12 * (int64_t)body, g.h, gb);
         const bool hit = gb[0] <= obox[3] && obox[0] <= gb[3] && gb[1] <= obox[4] && obox[1] <= gb[4] &&
                          gb[2] <= obox[5] && obox[2] <= gb[5];
-        if (hit) hitg[atomicAdd(&ghits, 1)] = (l << 16) | r;
+        if (hit) {
+          hitg[atomicAdd(&ghits, 1)] = (l << 16) | r;
+          glh[l] = 1;
+        }
       }
       __syncthreads();
+      if (!((glh[0] && glh[5]) || (glh[3] && glh[2]) || (glh[1] && glh[4]))) {  // uniform
+        if (threadIdx.x < 3) tab[3 * pi + threadIdx.x] = make_int2(0, 0);
+        continue;  // pi is in registers and the shared state is rewritten after the next barrier
+      }
+    }
+    // vertex boxes of both bodies
+    for (int t = threadIdx.x; t < 2 * P2_VCAP; t += P2_THREADS) {
+      const int side = t / P2_VCAP, lv = t % P2_VCAP;
+      if (lv < meta[6 + 3 * side]) {
+        const int body = side ? bj : bi;
+        vertex_box(g.rest, meta[3 * side] + lv, g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h,
+                   vb + P2_VBS * (side * P2_VCAP + lv));
+      }
+    }
+    __syncthreads();
+    if (grouped) {
       const int lane = threadIdx.x & 31;
       for (int u = threadIdx.x >> 5; u < ghits; u += P2_THREADS / 32) {
         const int l = hitg[u] >> 16, r = hitg[u] & 0xffff;
@@ -569,7 +585,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
           const int64_t gi = (int64_t)meta[l] + i;  // prim offset of the body (grouped order)
           pk = gr.pk[kind][gi];
           id = gr.id[kind][gi];
-          box_from_packed(kind, pk, vb + 6 * side * P2_VCAP, bxs);
+          box_from_packed(kind, pk, vb + P2_VBS * side * P2_VCAP, bxs);
           keep = bxs[0] <= obox[3] && obox[0] <= bxs[3] && bxs[1] <= obox[4] && obox[1] <= bxs[4] &&
                  bxs[2] <= obox[5] && obox[2] <= bxs[5];
         }
@@ -652,7 +668,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
           if (lst[u] < 0) continue;
           const int l = lst[u], side = l / 3, kind = l % 3;
           double bx[6];
-          box_from_packed(kind, pk[u], vb + 6 * side * P2_VCAP, bx);
+          box_from_packed(kind, pk[u], vb + P2_VBS * side * P2_VCAP, bx);
           const bool keep = bx[0] <= obox[3] && obox[0] <= bx[3] && bx[1] <= obox[4] && obox[1] <= bx[4] &&
                             bx[2] <= obox[5] && obox[2] <= bx[5];
           if (keep) {
@@ -684,7 +700,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       if (threadIdx.x == 0) hcount = 0;
       // materialise the loop side's boxes
       for (int t = threadIdx.x; t < nl; t += P2_THREADS)
-        box_from_packed(kl, lpk[LOFF(ll) + t], vb + 6 * sl * P2_VCAP, obx + 6 * t);
+        box_from_packed(kl, lpk[LOFF(ll) + t], vb + P2_VBS * sl * P2_VCAP, obx + 6 * t);
       // run-pair mask: bit j of tmask[k] = run k of the thread side meets run j of the loop side
       // (only for large products: for small ones the plain warp-synchronous sweep wins)
       const bool use_runs = RUNS && runs_ok != 0 && nt * nl >= 4096;  // uniform
@@ -726,7 +742,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
               if (own >= run_s[lt][k] && own < run_s[lt][k] + run_n[lt][k]) kr = k;
             double ob[6];
             const int own_local = lists[LOFF(lt) + own];
-            box_from_packed(kt, lpk[LOFF(lt) + own], vb + 6 * st_ * P2_VCAP, ob);
+            box_from_packed(kt, lpk[LOFF(lt) + own], vb + P2_VBS * st_ * P2_VCAP, ob);
             unsigned mk = tmask[kr];
             int cyc = 0;  // position in this thread's filtered sequence mod G (chunks take every G-th)
             while (mk) {
@@ -755,15 +771,17 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
           const int own = live ? idx % nt : 0, chunk = idx / nt;
           double ob[6];
           const int own_local = live ? lists[LOFF(lt) + own] : 0;
-          if (live) box_from_packed(kt, lpk[LOFF(lt) + own], vb + 6 * st_ * P2_VCAP, ob);
+          if (live) box_from_packed(kt, lpk[LOFF(lt) + own], vb + P2_VBS * st_ * P2_VCAP, ob);
           const int y0 = chunk * Lc;
           for (int yy = 0; yy < Lc; ++yy) {
             const int y = y0 + yy;
             bool hit = false;
             if (live && y < nl) {
-              const double* b2 = obx + 6 * y;
-              hit = ob[0] <= b2[3] && b2[0] <= ob[3] && ob[1] <= b2[4] && b2[1] <= ob[4] && ob[2] <= b2[5] &&
-                    b2[2] <= ob[5];
+              // the box as three 16-byte broadcast loads: (lo0, lo1) (lo2, hi0) (hi1, hi2)
+              const double2* b2 = reinterpret_cast<const double2*>(obx + 6 * y);
+              const double2 u0 = b2[0], u1 = b2[1], u2 = b2[2];
+              hit = (ob[0] <= u1.y) & (u0.x <= ob[3]) & (ob[1] <= u2.x) & (u0.y <= ob[4]) & (ob[2] <= u2.y) &
+                    (u1.x <= ob[5]);
             }
             const unsigned m = __ballot_sync(0xffffffffu, hit);
             if (m) {
@@ -1328,7 +1346,7 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
     static bool attr = false;
     const int cap_list = std::max(s.max_v, std::max(s.max_e, s.max_t));
     const int3 cap_k = make_int3(s.max_v, s.max_e, s.max_t);
-    const size_t p2_smem = sizeof(double) * (2 * 6 * P2_VCAP + 6 * (size_t)cap_list) +
+    const size_t p2_smem = sizeof(double) * (2 * P2_VBS * P2_VCAP + 6 * (size_t)cap_list) +
                            2 * sizeof(int) * 2 * (size_t)(cap_k.x + cap_k.y + cap_k.z) + sizeof(unsigned) * P2_HCAP;
     const bool use2 = (s.max_v <= P2_VCAP && p2_smem <= 100 * 1024 && !getenv("ABD_BP_V1")) || s.comm.world > 1;
     if (s.comm.world > 1 && !(s.max_v <= P2_VCAP && p2_smem <= 100 * 1024))
