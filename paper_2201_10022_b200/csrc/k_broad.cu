@@ -490,11 +490,17 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   // slab of the lower body, or of the higher one when the lower is kinematic
   // (table rows of the other ranks' pairs stay 0)
   __shared__ long long next_k;
+  __shared__ int pcnt[2];              // merged products: hits of products 0 and 1
+  __shared__ unsigned long long hbase2;  // merged products: base of the EE chunk
+  // thread 0 takes the following pair's index while the current pair is processed (the
+  // atomic's round trip is off the per-pair chain)
+  long long ahead = threadIdx.x == 0 ? (long long)atomicAdd(work, 1ull) : 0;
   for (;;) {
-    if (threadIdx.x == 0) next_k = (long long)atomicAdd(work, 1ull);
+    if (threadIdx.x == 0) next_k = ahead;
     __syncthreads();
     const int64_t pi = next_k;
     if (pi >= n_ov) break;
+    if (threadIdx.x == 0) ahead = (long long)atomicAdd(work, 1ull);
     const int2 pr = ov[pi];
     const int bi = pr.x, bj = pr.y;
     if (owner) {
@@ -513,6 +519,11 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       meta[6 + 3 * side + kind] = b - a;
       lcount[threadIdx.x] = 0;
       if (threadIdx.x == 0 && !use_groups) runs_ok = 0;  // (thread 64 writes it otherwise)
+      if (threadIdx.x == 1) {  // merged products (hcount is dead: read before the last hbase barrier)
+        hcount = 0;
+        pcnt[0] = 0;
+        pcnt[1] = 0;
+      }
     } else if (threadIdx.x >= 32 && threadIdx.x < 35) {
       const int k = threadIdx.x - 32;
       obox[k] = fmax(bbox[6 * bi + k], bbox[6 * bj + k]);
@@ -681,6 +692,128 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
     }
     __syncthreads();
     // products: (verts i, tris j) -> vf(i,.,j,.); (verts j, tris i) -> vf(j,.,i,.); (edges i, edges j)
+    //
+    // Small pairs (the pile's common case: ~120 survivors, ~1,500 box tests) take the three
+    // products in ONE pass: every survivor's box is materialised once, the tests of the
+    // three products are dealt to the threads as one flat range, the hits carry their
+    // product in the key's top bits (so one sort gives the (product, prim_a, prim_b)
+    // order), and one pair of global atomics reserves the VF and EE chunks: 3 barriers
+    // and one atomic round trip per pair instead of 9 and 3.
+    bool merged = false;
+    {
+      const int c0 = lcount[0], c1 = lcount[1], c2 = lcount[2], c3 = lcount[3], c4 = lcount[4], c5 = lcount[5];
+      const int T0 = c0 * c5, T1 = c3 * c2, T2 = c1 * c4;  // (la, lb) = (0, 5), (3, 2), (1, 4)
+      const int nbox = c0 + c1 + c2 + c3 + c4 + c5, TT = T0 + T1 + T2;
+      const bool use_runs_any = RUNS && runs_ok != 0 && (T0 >= 4096 || T1 >= 4096 || T2 >= 4096);
+      if (TT > 0 && TT <= 32 * P2_THREADS && nbox <= cap_list && !use_runs_any && cap_k.y <= 16384 &&
+          cap_k.z <= 16384) {  // uniform
+        const int o1 = c0, o2 = o1 + c1, o3 = o2 + c2, o4 = o3 + c3, o5 = o4 + c4;
+        for (int t = threadIdx.x; t < nbox; t += P2_THREADS) {
+          const int l = t < o1 ? 0 : (t < o2 ? 1 : (t < o3 ? 2 : (t < o4 ? 3 : (t < o5 ? 4 : 5))));
+          const int ol = l == 0 ? 0 : (l == 1 ? o1 : (l == 2 ? o2 : (l == 3 ? o3 : (l == 4 ? o4 : o5))));
+          box_from_packed(l % 3, lpk[LOFF(l) + (t - ol)], vb + P2_VBS * (l / 3) * P2_VCAP, obx + 6 * t);
+        }
+        __syncthreads();
+        const int lane = threadIdx.x & 31;
+        for (int base = 0; base < TT; base += P2_THREADS) {
+          const int idx = base + threadIdx.x;
+          bool hit = false;
+          int pr_ = 0, a = 0, b = 0;
+          if (idx < TT) {
+            pr_ = idx < T0 ? 0 : (idx < T0 + T1 ? 1 : 2);
+            const int loc = idx - (pr_ == 0 ? 0 : (pr_ == 1 ? T0 : T0 + T1));
+            const int nb = pr_ == 0 ? c5 : (pr_ == 1 ? c2 : c4);
+            a = loc / nb;
+            b = loc - a * nb;
+            const double2* A = reinterpret_cast<const double2*>(obx + 6 * ((pr_ == 0 ? 0 : (pr_ == 1 ? o3 : o1)) + a));
+            const double2* B = reinterpret_cast<const double2*>(obx + 6 * ((pr_ == 0 ? o5 : (pr_ == 1 ? o2 : o4)) + b));
+            const double2 a0 = A[0], a1 = A[1], a2 = A[2], b0 = B[0], b1 = B[1], b2 = B[2];
+            hit = (a0.x <= b1.y) & (b0.x <= a1.y) & (a0.y <= b2.x) & (b0.y <= a2.x) & (a1.x <= b2.y) &
+                  (b1.x <= a2.y);
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, hit);
+          if (m) {  // warp-uniform
+            const unsigned m0 = __ballot_sync(0xffffffffu, hit && pr_ == 0);
+            const unsigned m1 = __ballot_sync(0xffffffffu, hit && pr_ == 1);
+            const int lead = __ffs(m) - 1;
+            int at0 = 0;
+            if (lane == lead) {
+              at0 = atomicAdd(&hcount, __popc(m));
+              if (m0) atomicAdd(&pcnt[0], __popc(m0));
+              if (m1) atomicAdd(&pcnt[1], __popc(m1));
+            }
+            at0 = __shfl_sync(0xffffffffu, at0, lead);
+            if (hit) {
+              const int at = at0 + __popc(m & ((1u << lane) - 1));
+              const int la = pr_ == 0 ? 0 : (pr_ == 1 ? 3 : 1), lb = pr_ == 0 ? 5 : (pr_ == 1 ? 2 : 4);
+              const unsigned pa = (unsigned)lists[LOFF(la) + a], pb = (unsigned)lists[LOFF(lb) + b];
+              if (at < P2_HCAP) hk[at] = ((unsigned)pr_ << 28) | (pa << 14) | pb;
+            }
+          }
+        }
+        __syncthreads();
+        const int cnt = hcount;
+        if (cnt <= P2_HCAP) {  // uniform
+          merged = true;
+          const int n0 = pcnt[0], n1 = pcnt[1], n01 = n0 + n1;
+          if (threadIdx.x == 0) {
+            const unsigned long long bv = n01 ? atomicAdd(counters + 0, (unsigned long long)n01) : 0ull;
+            const unsigned long long be = cnt - n01 ? atomicAdd(counters + 1, (unsigned long long)(cnt - n01)) : 0ull;
+            hbase = bv;
+            hbase2 = be;
+            tab[3 * pi + 0] = make_int2((int)bv, n0);
+            tab[3 * pi + 1] = make_int2((int)bv + n0, n1);
+            tab[3 * pi + 2] = make_int2((int)be, cnt - n01);
+          }
+          if (cnt > 256) {
+            // larger chunks: bitonic sort in shared memory
+            int P2 = 1;
+            while (P2 < cnt) P2 <<= 1;
+            for (int t = cnt + threadIdx.x; t < P2; t += P2_THREADS) hk[t] = 0xffffffffu;
+            __syncthreads();
+            for (int k = 2; k <= P2; k <<= 1)
+              for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                for (int t = threadIdx.x; t < P2; t += P2_THREADS) {
+                  const int u = t ^ jj;
+                  if (u > t) {
+                    const bool up = (t & k) == 0;
+                    const unsigned x = hk[t], y = hk[u];
+                    if ((x > y) == up) {
+                      hk[t] = y;
+                      hk[u] = x;
+                    }
+                  }
+                }
+                __syncthreads();
+              }
+          } else {
+            __syncthreads();  // hbase / hbase2 visible
+          }
+          const unsigned long long bv = hbase, be = hbase2;
+          for (int t = threadIdx.x; t < cnt; t += P2_THREADS) {
+            const unsigned key = hk[t];
+            int rank = t;
+            if (cnt <= 256) {  // order by rank (unique keys): one pass of broadcast reads
+              rank = 0;
+              for (int u = 0; u < cnt; ++u) rank += hk[u] < key;
+            }
+            const int pq = (int)(key >> 28), pa = (int)((key >> 14) & 0x3fffu), pb = (int)(key & 0x3fffu);
+            const int body_a = pq == 1 ? bj : bi, body_b = pq == 1 ? bi : bj;
+            if (pq < 2) {
+              const unsigned long long g2 = bv + (unsigned long long)rank;
+              if ((int64_t)g2 < cap_vf) out_vf[g2] = make_int4(body_a, pa, body_b, pb);
+            } else {
+              const unsigned long long g2 = be + (unsigned long long)(rank - n01);
+              if ((int64_t)g2 < cap_ee) out_ee[g2] = make_int4(body_a, pa, body_b, pb);
+            }
+          }
+          // no barrier: hk, hbase, pcnt and hcount are rewritten only after the next pair's barriers
+        } else {
+          __syncthreads();  // every thread has read hcount before the per-product path resets it
+        }
+      }
+    }
+    if (!merged)
     for (int prod = 0; prod < 3; ++prod) {
       const int la = prod == 0 ? 0 : (prod == 1 ? 3 : 1);  // list of side a
       const int lb = prod == 0 ? 5 : (prod == 1 ? 2 : 4);  // list of side b
