@@ -483,7 +483,6 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
   __shared__ int lcount[6];
   __shared__ double obox[6];
   __shared__ int gfirst[6], gcount[6], ghits;
-  __shared__ int glh[6];  // surviving groups per list
   __shared__ int hitg[256];
   // pairs are handed out dynamically (their costs vary by orders of magnitude);
   // multi-GPU (owner != null): this rank takes the overlap pairs of its slab -- the
@@ -535,7 +534,6 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       gfirst[l] = a;
       gcount[l] = gr.off[kind][body + 1] - a;
       nrun[l] = 0;
-      glh[l] = 0;
       if (l == 0) {
         ghits = 0;
         runs_ok = RUNS ? 1 : 0;
@@ -543,42 +541,34 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
     }
     __syncthreads();
     // cull in two stages: (a) the static groups of 32 primitives of the six lists
-    // against the overlap box (conservative swept boxes of their rest AABBs: no vertex
-    // box needed, so a pair none of whose products keeps a group on both sides ends
-    // here); (b) the primitives of the surviving groups, one warp per group
+    // against the overlap box (conservative swept boxes of their rest AABBs); (b) the
+    // primitives of the surviving groups, one warp per group.  Stage (a) needs no vertex
+    // box, so it shares one phase (one barrier) with the vertex boxes of both bodies: the
+    // work items are the nv_i + nv_j vertices followed by the groups.
     const bool grouped = use_groups && gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5] <= 256;
-    if (grouped) {
-      const int gt = gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5];
-      for (int t = threadIdx.x; t < gt; t += P2_THREADS) {
-        int l = 0, r = t;
-        while (r >= gcount[l]) {
-          r -= gcount[l];
-          ++l;
+    {
+      const int nvi = meta[6], nvj = meta[9];
+      const int gt = grouped ? gcount[0] + gcount[1] + gcount[2] + gcount[3] + gcount[4] + gcount[5] : 0;
+      for (int t = threadIdx.x; t < nvi + nvj + gt; t += P2_THREADS) {
+        if (t < nvi + nvj) {
+          const int side = t >= nvi, lv = side ? t - nvi : t;
+          const int body = side ? bj : bi;
+          vertex_box(g.rest, meta[3 * side] + lv, g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h,
+                     vb + P2_VBS * (side * P2_VCAP + lv));
+        } else {
+          int l = 0, r = t - nvi - nvj;
+          while (r >= gcount[l]) {
+            r -= gcount[l];
+            ++l;
+          }
+          const int side = l / 3, kind = l % 3, body = side ? bj : bi;
+          double gb[6];
+          group_box(gr.box[kind] + 6 * (int64_t)(gfirst[l] + r), g.q0 + 12 * (int64_t)body,
+                    g.q1 + 12 * (int64_t)body, g.h, gb);
+          const bool hit = gb[0] <= obox[3] && obox[0] <= gb[3] && gb[1] <= obox[4] && obox[1] <= gb[4] &&
+                           gb[2] <= obox[5] && obox[2] <= gb[5];
+          if (hit) hitg[atomicAdd(&ghits, 1)] = (l << 16) | r;
         }
-        const int side = l / 3, kind = l % 3, body = side ? bj : bi;
-        double gb[6];
-        group_box(gr.box[kind] + 6 * (int64_t)(gfirst[l] + r), g.q0 + 12 * (int64_t)body,
-                  g.q1 + 12 * (int64_t)body, g.h, gb);
-        const bool hit = gb[0] <= obox[3] && obox[0] <= gb[3] && gb[1] <= obox[4] && obox[1] <= gb[4] &&
-                         gb[2] <= obox[5] && obox[2] <= gb[5];
-        if (hit) {
-          hitg[atomicAdd(&ghits, 1)] = (l << 16) | r;
-          glh[l] = 1;
-        }
-      }
-      __syncthreads();
-      if (!((glh[0] && glh[5]) || (glh[3] && glh[2]) || (glh[1] && glh[4]))) {  // uniform
-        if (threadIdx.x < 3) tab[3 * pi + threadIdx.x] = make_int2(0, 0);
-        continue;  // pi is in registers and the shared state is rewritten after the next barrier
-      }
-    }
-    // vertex boxes of both bodies
-    for (int t = threadIdx.x; t < 2 * P2_VCAP; t += P2_THREADS) {
-      const int side = t / P2_VCAP, lv = t % P2_VCAP;
-      if (lv < meta[6 + 3 * side]) {
-        const int body = side ? bj : bi;
-        vertex_box(g.rest, meta[3 * side] + lv, g.q0 + 12 * (int64_t)body, g.q1 + 12 * (int64_t)body, g.h,
-                   vb + P2_VBS * (side * P2_VCAP + lv));
       }
     }
     __syncthreads();
