@@ -190,6 +190,12 @@ __global__ void __launch_bounds__(64) k_pair_blocks_act(SceneView sv, int kind_u
 // fixed orders: deterministic.
 constexpr int RUN_WARPS = 2;
 
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 template <int KIND>
 __device__ __forceinline__ int2 run_pair(const int4* __restrict__ rows, const int* __restrict__ act, int64_t cand_off,
                                          int64_t slot_off, int64_t count, const unsigned char* __restrict__ moll_flag,
@@ -233,6 +239,21 @@ __global__ void __launch_bounds__(32 * RUN_WARPS) k_pair_runs(SceneView sv, int6
                                                                int2* out_bodies, double* out_d2, double* run_part,
                                                                int2* run_bodies) {
   extern __shared__ double run_sm[];  // [RUN_WARPS][32][PB_STRIDE]
+  // run-sum read-out map: entry e of a run partial (aa | bb | ab, reference DOFs) ->
+  // (rho, sigma) of the 24-space in which the run is summed, rho <= sigma
+  __shared__ unsigned short emap[432];
+  for (int e = threadIdx.x; e < 432; e += 32 * RUN_WARPS) {
+    const int blk = e / 144, idx = e % 144, i = idx / 12, c = idx % 12;
+    const int R = blk == 1 ? 12 + i : i, C = blk == 0 ? c : 12 + c;
+    int rho = pb_rho(R / 12, R % 12), sg = pb_rho(C / 12, C % 12);
+    if (sg < rho) {
+      const int t = rho;
+      rho = sg;
+      sg = t;
+    }
+    emap[e] = (unsigned short)(rho * 32 + sg);
+  }
+  __syncthreads();
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * RUN_WARPS + wl;
   if (w >= n_win) return;
@@ -258,19 +279,68 @@ __global__ void __launch_bounds__(32 * RUN_WARPS) k_pair_runs(SceneView sv, int6
   __syncwarp();
   const int base = wbase[w];
   unsigned rem = starts;
+  // The run's Hessian sum_l Q_l M_l Q_l^T (fused pairs carry 5-column records) is
+  // accumulated in the affine 24-space on the FP64 tensor core: per pair the fragments of
+  // U = Q M (A operand) and Q (B operand) are formed from the record in shared memory --
+  // lane (g, tq) holds row 8 t + g, column 4 kk + tq; columns 5..7 are zero padding --
+  // and the six upper 8x8 tiles take two m8n8k4 steps each; pairs are added in lane
+  // order (deterministic).  ~110 warp instructions per pair instead of ~430 for the
+  // entry-by-entry expansion.
+  const int g8 = lane >> 2, tq = lane & 3;
   for (int k = 0; rem; ++k) {
     const int l0 = __ffs(rem) - 1;
     rem &= rem - 1;
     // the run ends at the next start or the next non-fused lane
     const unsigned stop = (starts | ~fused) & ~((2u << l0) - 1u);
     const int l1 = stop ? __ffs(stop) - 1 : 32;
+    double acc[6][2];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int l = l0; l < l1; ++l) {
+      const double* rec = recs + (size_t)l * PB_STRIDE;
+      const double* ch = rec + 25;
+      const double* f0 = rec + 33;
+      const double* f1 = rec + 57;
+      const double* M = rec + 81;
+      double ua[3][2], wb[3][2];
+#pragma unroll
+      for (int tt = 0; tt < 3; ++tt) {
+        const int rho = 8 * tt + g8, sj = rho / 3, a = rho - 3 * sj;
+        const double c_ = ch[sj], p0 = f0[rho], p1 = f1[rho];
+        ua[tt][0] = c_ * M[5 * a + tq] + p0 * M[15 + tq] + p1 * M[20 + tq];
+        ua[tt][1] = tq == 0 ? c_ * M[5 * a + 4] + p0 * M[19] + p1 * M[24] : 0.0;
+        wb[tt][0] = tq == 3 ? p0 : (a == tq ? c_ : 0.0);
+        wb[tt][1] = tq == 0 ? p1 : 0.0;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        dmma_f64(acc[0][0], acc[0][1], ua[0][kk], wb[0][kk]);
+        dmma_f64(acc[1][0], acc[1][1], ua[0][kk], wb[1][kk]);
+        dmma_f64(acc[2][0], acc[2][1], ua[0][kk], wb[2][kk]);
+        dmma_f64(acc[3][0], acc[3][1], ua[1][kk], wb[1][kk]);
+        dmma_f64(acc[4][0], acc[4][1], ua[1][kk], wb[2][kk]);
+        dmma_f64(acc[5][0], acc[5][1], ua[2][kk], wb[2][kk]);
+      }
+    }
+    // the 24 x 24 sum goes through the unused tails of records 0..23 (a 5-column record
+    // ends at 106 of PB_STRIDE = 136 doubles): row rho in record rho
+    __syncwarp();
+    {
+      constexpr int mi_of[6] = {0, 0, 0, 1, 1, 2}, ni_of[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        double* row = recs + (size_t)(8 * mi_of[i] + g8) * PB_STRIDE + 106 + 8 * ni_of[i] + 2 * tq;
+        row[0] = acc[i][0];
+        row[1] = acc[i][1];
+      }
+    }
+    __syncwarp();
     double* out = run_part + (int64_t)(base + k) * RUN_STRIDE;
     for (int e = lane; e < RUN_STRIDE; e += 32) {
       double a = 0.0;
       if (e < 432) {
-        const int blk = e / 144, idx = e % 144, i = idx / 12, c = idx % 12;
-        const int R = blk == 1 ? 12 + i : i, C = blk == 0 ? c : 12 + c;
-        for (int l = l0; l < l1; ++l) a += pb_entry(recs + (size_t)l * PB_STRIDE, R, C);
+        const int m = emap[e];
+        a = recs[(size_t)(m >> 5) * PB_STRIDE + 106 + (m & 31)];
       } else {
         for (int l = l0; l < l1; ++l) a += recs[(size_t)l * PB_STRIDE + (e - 432)];
       }
@@ -278,6 +348,7 @@ __global__ void __launch_bounds__(32 * RUN_WARPS) k_pair_runs(SceneView sv, int6
     }
     const int bx = __shfl_sync(0xffffffffu, bp.x, l0), by = __shfl_sync(0xffffffffu, bp.y, l0);
     if (lane == 0) run_bodies[base + k] = make_int2(bx, by);
+    __syncwarp();  // the next run rewrites the staging rows
   }
 }
 
