@@ -460,6 +460,8 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
                   int rank, const int* __restrict__ owner,
                   unsigned long long* work, const int* n_ov_dev) {
   if (n_ov_dev) n_ov = *n_ov_dev;  // deferred count (Verlet-list filter result, no host sync)
+  const bool no_merge = (use_groups & 2) != 0;  // ABD_BP_NO_MERGE: every pair takes the per-product path (tests)
+  use_groups &= 1;
   extern __shared__ double p2_sm[];
   double* vb = p2_sm;                        // [2][P2_VCAP][P2_VBS] vertex boxes of i and j
   double* obx = vb + 2 * P2_VBS * P2_VCAP;   // [cap_list][6] materialised boxes (one product at a time)
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(P2_THREADS, 3)
       const int T0 = c0 * c5, T1 = c3 * c2, T2 = c1 * c4;  // (la, lb) = (0, 5), (3, 2), (1, 4)
       const int nbox = c0 + c1 + c2 + c3 + c4 + c5, TT = T0 + T1 + T2;
       const bool use_runs_any = RUNS && runs_ok != 0 && (T0 >= 4096 || T1 >= 4096 || T2 >= 4096);
-      if (TT > 0 && TT <= 32 * P2_THREADS && nbox <= cap_list && !use_runs_any && cap_k.y <= 16384 &&
+      if (!no_merge && TT > 0 && TT <= 32 * P2_THREADS && nbox <= cap_list && !use_runs_any && cap_k.y <= 16384 &&
           cap_k.z <= 16384) {  // uniform
         const int o1 = c0, o2 = o1 + c1, o3 = o2 + c2, o4 = o3 + c3, o5 = o4 + c4;
         for (int t = threadIdx.x; t < nbox; t += P2_THREADS) {
@@ -1497,7 +1499,8 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
         gg.box[k] = s.grp_box[k].p;
         gg.off[k] = s.grp_off[k].p;
       }
-      const int ug = s.has_groups && !no_groups ? 1 : 0;
+      static const bool no_merge = getenv("ABD_BP_NO_MERGE") != nullptr;
+      const int ug = (s.has_groups && !no_groups ? 1 : 0) | (no_merge ? 2 : 0);
       // run-pair filtering of the products pays for large meshes (tori: 960 edges +
       // triangles per body, products of thousands of pairs); for the pile's
       // icospheres (800) the plain sweep is faster
