@@ -2168,7 +2168,13 @@ static Analysis chol_analyze(Scene& s) {
   std::copy(upd_ptr.begin(), upd_ptr.end(), hp + o[CH_UPDP]);
   std::copy(upd.begin(), upd.end(), hp + o[CH_UPD]);
   w.ch_plan.resize(total);
-  CK(cudaMemcpyAsync(w.ch_plan.p, hp, total * sizeof(int), cudaMemcpyHostToDevice, st));
+  // the plan goes up on the copy stream: every earlier use of the plan buffers has completed
+  // (the analysis starts from structure flags this thread has host-synchronised on, which
+  // the main stream produced after its last factorization), and the next factorization
+  // waits on plan_ev (plan_wait)
+  CK(cudaMemcpyAsync(w.ch_plan.p, hp, total * sizeof(int), cudaMemcpyHostToDevice, s.copy_stream));
+  CK(cudaEventRecord(s.plan_ev, s.copy_stream));
+  s.plan_pending = true;
   w.ch_L.resize(144 * std::max<int64_t>(an.n_blk, 1));
   w.ch_dinv.resize(12 * std::max<int64_t>(n, 1));
   w.ch_apos.resize(std::max<int64_t>(an.n_blk - n, 1));
@@ -2210,6 +2216,13 @@ static Analysis chol_analyze(Scene& s) {
 //   chol_finish : after a stream sync, pivot check, residual test, corrections
 // one factor (+ both substitutions) or one pair of substitutions over the task FIFO;
 // returns the grid size
+// the stream that is about to use the plan waits for its upload
+static void plan_wait(Scene& s, cudaStream_t st) {
+  if (!s.plan_pending) return;
+  CK(cudaStreamWaitEvent(st, s.plan_ev, 0));
+  s.plan_pending = false;
+}
+
 static int launch_sched(Scene& s, const CholView& v, const double* b, double* x, bool factor) {
   cudaStream_t st = s.stream;
   static int bps = 0;
@@ -2504,6 +2517,7 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
     kstat_flush(s, 0);
     CK(cudaEventRecord(ks.e0, st));
   }
+  plan_wait(s, st);
   k_chol_apos<<<grid_for(n, 128), 128, 0, st>>>(v);
   note_launch("k_chol_apos");
   run.n_cta = launch_sched(s, v, rhs, x, true);
@@ -2674,6 +2688,7 @@ int slab_pcg(Scene& s, const double* b, double* x, double rel_tol, int max_iters
     kstat_flush(s, 0);
     CK(cudaEventRecord(ks.e0, st));
   }
+  plan_wait(s, st);
   k_chol_apos<<<grid_for(n, 128), 128, 0, st>>>(v);
   note_launch("k_chol_apos");
   CK(cudaMemsetAsync(x, 0, N * sizeof(double), st));

@@ -45,6 +45,8 @@ Scene::Scene() {
   CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&side3, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&plan_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&moll_fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&moll_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&hot_fork_ev, cudaEventDisableTiming));
@@ -74,6 +76,8 @@ Scene::~Scene() {
   if (join_ev) cudaEventDestroy(join_ev);
   if (side2) cudaStreamDestroy(side2);
   if (side3) cudaStreamDestroy(side3);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (plan_ev) cudaEventDestroy(plan_ev);
   if (moll_fork_ev) cudaEventDestroy(moll_fork_ev);
   if (moll_ev) cudaEventDestroy(moll_ev);
   if (hot_fork_ev) cudaEventDestroy(hot_fork_ev);

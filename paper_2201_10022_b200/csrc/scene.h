@@ -185,6 +185,11 @@ struct Scene {
   cudaEvent_t hot_fork_ev = nullptr, hot_ev = nullptr;
   cudaEvent_t pb_fork_ev = nullptr, pb_ev = nullptr;  // VF pair blocks on side2
   cudaStream_t side3 = nullptr;  // mollified EE pair blocks beside the plain EE pairs
+  // Cholesky plan uploads (issued by the analysis worker): on their own stream, so the copy
+  // does not queue between the main stream's kernels; chol_begin waits on plan_ev
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t plan_ev = nullptr;
+  bool plan_pending = false;
   cudaStream_t side4 = nullptr;  // Cholesky: isolated nodes beside the coupled task graph
   cudaEvent_t ch_fork_ev = nullptr, ch_join_ev = nullptr;
   cudaEvent_t moll_fork_ev = nullptr, moll_ev = nullptr;
