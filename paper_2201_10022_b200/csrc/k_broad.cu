@@ -1016,6 +1016,74 @@ __global__ void k_ov_in_pattern(int64_t n, const int2* __restrict__ ov, const in
   *inside = 0;
 }
 
+// Chunks to their final offsets in ONE launch (chunk counts, the two prefix sums and the
+// two moves used to be nine launches of tiny kernels -- ~45 us of launch latency per broad
+// phase).  A CTA owns CG_PAIRS consecutive body pairs: it sums the chunk counts of all
+// pairs before its first one (the table is a few hundred KB in L2), scans its own pairs'
+// counts, and its warps copy the chunks.  Offsets = the exclusive prefix sums in (pair,
+// product) order, as before.
+constexpr int CG_PAIRS = 32, CG_THREADS = 256;
+__global__ void __launch_bounds__(CG_THREADS) k_chunk_gather(int n_ov, const int2* __restrict__ tab,
+                                                             const int4* __restrict__ src_vf, int4* dst_vf,
+                                                             const int4* __restrict__ src_ee, int4* dst_ee) {
+  __shared__ int red_vf[CG_THREADS / 32], red_ee[CG_THREADS / 32];
+  __shared__ int off_s[3 * CG_PAIRS];
+  const int p0 = blockIdx.x * CG_PAIRS;
+  const int np = min(CG_PAIRS, n_ov - p0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // counts before this CTA's first pair
+  int svf = 0, see = 0;
+  for (int i = threadIdx.x; i < 3 * p0; i += CG_THREADS) {
+    const int c = tab[i].y;
+    if (i % 3 == 2) see += c;
+    else svf += c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    svf += __shfl_xor_sync(0xffffffffu, svf, o);
+    see += __shfl_xor_sync(0xffffffffu, see, o);
+  }
+  if (lane == 0) {
+    red_vf[wid] = svf;
+    red_ee[wid] = see;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    // one warp: bases, then the exclusive scans over this CTA's pairs (lane = pair)
+    int bvf = 0, bee = 0;
+#pragma unroll
+    for (int k = 0; k < CG_THREADS / 32; ++k) {
+      bvf += red_vf[k];
+      bee += red_ee[k];
+    }
+    const int c0 = lane < np ? tab[3 * (p0 + lane)].y : 0;
+    const int c1 = lane < np ? tab[3 * (p0 + lane) + 1].y : 0;
+    const int c2 = lane < np ? tab[3 * (p0 + lane) + 2].y : 0;
+    int ivf = c0 + c1, iee = c2;  // inclusive scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, ivf, o), b = __shfl_up_sync(0xffffffffu, iee, o);
+      if (lane >= o) {
+        ivf += a;
+        iee += b;
+      }
+    }
+    off_s[3 * lane] = bvf + ivf - (c0 + c1);
+    off_s[3 * lane + 1] = bvf + ivf - c1;
+    off_s[3 * lane + 2] = bee + iee - c2;
+  }
+  __syncthreads();
+  for (int ch = wid; ch < 3 * np; ch += CG_THREADS / 32) {
+    const int2 e = tab[3 * p0 + ch];
+    const int d = off_s[ch];
+    if (ch % 3 == 2) {
+      for (int k = lane; k < e.y; k += 32) dst_ee[d + k] = src_ee[e.x + k];
+    } else {
+      for (int k = lane; k < e.y; k += 32) dst_vf[d + k] = src_vf[e.x + k];
+    }
+  }
+}
+
 // chunk table -> per-list counts in (pair, product) order
 __global__ void k_chunk_counts(int64_t n_ov, const int2* __restrict__ tab, int* cnt_vf, int* cnt_ee) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1558,6 +1626,27 @@ static void prim_pairs_run(Scene& s, const double* q0, const double* q1, double 
   // Deterministic order without a global sort: (overlap pair, product, prim_a, prim_b).
   // Each (pair, product) chunk was sorted in shared memory; chunks move to their
   // prefix-sum offsets in pair order.  (abd_get_candidates returns the canonical order.)
+  static const bool split = getenv("ABD_BP_CHUNK_SPLIT") != nullptr;  // the separate count / scan / move kernels
+  if (!split) {
+    w.rows_tmp.resize(std::max<int64_t>(n_vf, 1));
+    w.rows_tmp2.resize(std::max<int64_t>(n_ee, 1));
+    k_chunk_gather<<<(n_ov + CG_PAIRS - 1) / CG_PAIRS, CG_THREADS, 0, st>>>(n_ov, w.tab.p, vf.p, w.rows_tmp.p, ee.p,
+                                                                          w.rows_tmp2.p);
+    note_launch("k_chunk_gather");
+    if (n_vf) {
+      std::swap(vf.p, w.rows_tmp.p);
+      std::swap(vf.cap, w.rows_tmp.cap);
+      std::swap(vf.n, w.rows_tmp.n);
+      vf.n = n_vf;
+    }
+    if (n_ee) {
+      std::swap(ee.p, w.rows_tmp2.p);
+      std::swap(ee.cap, w.rows_tmp2.cap);
+      std::swap(ee.n, w.rows_tmp2.n);
+      ee.n = n_ee;
+    }
+    return;
+  }
   w.cnt.resize(2 * n_ov + 1);
   w.off.resize(2 * n_ov + 1);
   w.va.resize(n_ov + 1);

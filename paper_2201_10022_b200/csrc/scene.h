@@ -263,7 +263,7 @@ struct Scene {
     DVec<uint64_t> k0, k1, e0, e1;
     DVec<uint32_t> ka, kb;
     DVec<int> va, vb;
-    DVec<int4> rows_tmp;
+    DVec<int4> rows_tmp, rows_tmp2;
     DVec<int2> tab;  // broad phase (pair, product) -> (chunk start, count)
     // overlap list / friction generation of the resident BSR pattern (build_pattern reuse)
     DVec<int2> pat_ov;

@@ -11,6 +11,7 @@ and off, and the final states are compared bit for bit:
 * ABD_CONTRIB_SORT    -- counting placement of the system contributions
 * ABD_BP_NO_GROUPS    -- static primitive groups in the primitive cull
 * ABD_BP_NO_MERGE     -- the three products of a small body pair taken in one pass
+* ABD_BP_CHUNK_SPLIT  -- candidate chunks gathered by one kernel (off: counts, two scans, two moves)
 * ABD_GMD_EXHAUSTIVE  -- end-of-step global minimum distance by the widened broad phase
 * ABD_MOLL_SERIAL     -- mollified EE pair blocks on a side stream beside the plain EE pairs
 
@@ -56,7 +57,7 @@ np.savez(out, q=state.q, q_dot=state.q_dot, its=np.array(its), mind=np.array(min
 """
 
 OFF = {"ABD_CCD_NO_HOT": "1", "ABD_VL_MARGIN": "0", "ABD_CHOL_NO_EARLY": "1", "ABD_CHOL_SYNC_ANALYSIS": "1",
-       "ABD_CONTRIB_SORT": "1", "ABD_BP_NO_GROUPS": "1", "ABD_BP_NO_MERGE": "1", "ABD_GMD_EXHAUSTIVE": "1",
+       "ABD_CONTRIB_SORT": "1", "ABD_BP_NO_GROUPS": "1", "ABD_BP_NO_MERGE": "1", "ABD_BP_CHUNK_SPLIT": "1", "ABD_GMD_EXHAUSTIVE": "1",
        "ABD_MOLL_SERIAL": "1"}
 
 
@@ -116,7 +117,8 @@ def test_broad_phase_opts_exact_on_the_pile(tmp_path):
     ckpt = os.path.join(ROOT, "bench_data", "pile_step150.npz")
     outs = {}
     for tag, env_extra in (("default", {}), ("runs", {"ABD_BP_RUNS": "1"}),
-                           ("plain", {"ABD_VL_MARGIN": "0", "ABD_BP_NO_GROUPS": "1", "ABD_BP_NO_MERGE": "1", "ABD_BP_RUNS": "0"})):
+                           ("plain", {"ABD_VL_MARGIN": "0", "ABD_BP_NO_GROUPS": "1", "ABD_BP_NO_MERGE": "1", "ABD_BP_CHUNK_SPLIT": "1",
+                                      "ABD_BP_RUNS": "0"})):
         out = str(tmp_path / f"bp_{tag}.npz")
         env = dict(os.environ)
         env.update(env_extra)
