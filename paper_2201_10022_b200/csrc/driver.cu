@@ -704,7 +704,13 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
           pack_to_host(stream, s.h_pinned, {{am, 8, 0}, {s.w.scal.p, 8, 8}});
           SSYNC(stream);
         };
-        absmax_dot();
+        if (chol) {
+          // chol_begin's residual launch carried |dx|_inf and rhs . dx (rhs = -g) along
+          SSYNC(stream);
+          s.h_pinned[1] = -s.h_pinned[1];
+        } else {
+          absmax_dot();
+        }
         if (chol) {
           bool changed = false;
           pcg_it = chol_finish(s, P.pcg_rel_tol, rel, 3, changed);

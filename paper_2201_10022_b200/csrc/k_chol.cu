@@ -1320,9 +1320,29 @@ __global__ void k_block_nz(int64_t n_off, const int* __restrict__ upper_pos, con
 // r = b - A x and the partial sums of r.r and b.b (fixed order)
 __global__ void k_resid(int n, const int* __restrict__ row_ptr, const int* __restrict__ col,
                         const double* __restrict__ val, const double* __restrict__ x, const double* __restrict__ b,
-                        double* r, double* part) {
+                        double* r, double* part, unsigned long long* amax) {
   __shared__ double sr[RED_THREADS], sb[RED_THREADS];
   double ar = 0.0, ab = 0.0;
+  if (amax) {
+    // the Newton step's |x|_inf and b . x in the same launch (driver.cu reads them with the
+    // residual: b = -g, so g . dx = -(b . x)); same grid-stride order as k_absmax_dot
+    __shared__ double sd[RED_THREADS];
+    const int64_t Nx = 12 * (int64_t)n;
+    double m = 0.0, acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < Nx; i += (int64_t)gridDim.x * blockDim.x) {
+      m = fmax(m, fabs(x[i]));
+      acc += b[i] * x[i];
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax, (unsigned long long)__double_as_longlong(m));
+    sd[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) sd[threadIdx.x] += sd[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part[2 * gridDim.x + blockIdx.x] = sd[0];
+  }
   const int64_t N = 12 * (int64_t)n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
     int br = (int)(t / 12), rr = (int)(t % 12);
@@ -2307,13 +2327,25 @@ static int launch_sched(Scene& s, const CholView& v, const double* b, double* x,
   return grid;
 }
 
-static void launch_resid(Scene& s, const double* rhs, const double* x) {
+// with_step (chol_begin): |x|_inf and rhs . x ride along -- one launch, one reduction and
+// one pack for the residual check AND the Newton step's size / descent test (h_pinned[0] =
+// |x|_inf bits, h_pinned[1] = rhs . x), which advance_step reads after its sync
+static void launch_resid(Scene& s, const double* rhs, const double* x, bool with_step = false) {
   Scene::Work& w = s.w;
   cudaStream_t st = s.stream;
-  k_resid<<<RED_BLOCKS, RED_THREADS, 0, st>>>(s.H.n, s.H.row_ptr.p, s.H.col.p, s.H.val.p, x, rhs, w.r.p, w.part.p);
+  unsigned long long* am = w.ull.p + 2;
+  if (with_step) {
+    w.part.resize(3 * RED_BLOCKS);
+    CK(cudaMemsetAsync(am, 0, sizeof(unsigned long long), st));
+  }
+  k_resid<<<RED_BLOCKS, RED_THREADS, 0, st>>>(s.H.n, s.H.row_ptr.p, s.H.col.p, s.H.val.p, x, rhs, w.r.p, w.part.p,
+                                              with_step ? am : nullptr);
   note_launch("k_resid");
-  reduce_fixed_multi(st, w.part.p, RED_BLOCKS, 2, w.scal.p + 4);
-  pack_to_host(st, s.h_pinned + 24, {{w.scal.p + 4, 16, 0}, {w.bad.p, 4, 32}});
+  reduce_fixed_multi(st, w.part.p, RED_BLOCKS, with_step ? 3 : 2, w.scal.p + 4);
+  if (with_step)
+    pack_to_host(st, s.h_pinned, {{am, 8, 0}, {w.scal.p + 6, 8, 8}, {w.scal.p + 4, 16, 192}, {w.bad.p, 4, 224}});
+  else
+    pack_to_host(st, s.h_pinned + 24, {{w.scal.p + 4, 16, 0}, {w.bad.p, 4, 32}});
 }
 
 static void chol_verify_core(Scene& s, Analysis& an);
@@ -2524,9 +2556,9 @@ void chol_begin(Scene& s, const double* rhs, double* x) {
   if (s.instrument) CK(cudaEventRecord(ks.e1, st));
   w.r.resize(N);
   w.z.resize(N);
-  w.part.resize(2 * RED_BLOCKS);
+  w.part.resize(3 * RED_BLOCKS);
   w.scal.resize(8);
-  launch_resid(s, rhs, x);
+  launch_resid(s, rhs, x, /*with_step=*/true);
 }
 
 int chol_finish(Scene& s, double rel_tol, double& rel_res, int max_refine, bool& changed) {
