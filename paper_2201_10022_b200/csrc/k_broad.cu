@@ -58,7 +58,8 @@ __device__ __forceinline__ void vertex_box(const double* __restrict__ rest, int6
 // one warp per body: union of its swept vertex boxes (computed on the fly)
 __global__ void k_body_boxes(int B, const int* __restrict__ v_off, const double* __restrict__ rest,
                              const double* __restrict__ q0, const double* __restrict__ q1, double h,
-                             double* __restrict__ bbox) {
+                             double* __restrict__ bbox, const double* __restrict__ vl_box = nullptr,
+                             int* viol = nullptr) {
   int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (w >= B) return;
@@ -94,11 +95,18 @@ __global__ void k_body_boxes(int B, const int* __restrict__ v_off, const double*
       lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
       hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
     }
-  if (lane == 0)
+  if (lane == 0) {
     for (int k = 0; k < 3; ++k) {
       bbox[6 * w + k] = lo[k];
       bbox[6 * w + 3 + k] = hi[k];
     }
+    // Verlet list: the box must still lie inside its inflated box (k_vl_contain's test)
+    if (vl_box) {
+      const double* y = vl_box + 6 * w;
+      if (!(lo[0] >= y[0] && lo[1] >= y[1] && lo[2] >= y[2] && hi[0] <= y[3] && hi[1] <= y[4] && hi[2] <= y[5]))
+        atomicExch(viol, 1);
+    }
+  }
 }
 
 __device__ __forceinline__ uint64_t sortable_bits(double x) {
@@ -1762,8 +1770,10 @@ __global__ void k_vl_contain(int B, const double* __restrict__ bbox, const doubl
     atomicExch(viol, 1);
 }
 
-__global__ void k_vl_flags(int64_t n, const int2* __restrict__ sup, const double* __restrict__ bbox, int* flags) {
+__global__ void k_vl_flags(int64_t n, const int2* __restrict__ sup, const double* __restrict__ bbox, int* flags,
+                           int* set_one) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i == 0 && set_one) *set_one = 1;  // (the pattern check that follows clears it)
   if (i >= n) return;
   const int2 pr = sup[i];
   flags[i] = box_overlap(bbox + 6 * pr.x, bbox + 6 * pr.y);
@@ -1771,16 +1781,18 @@ __global__ void k_vl_flags(int64_t n, const int2* __restrict__ sup, const double
 
 // the Verlet-list filter over the whole GPU: containment flag, overlap flags and an
 // ordered (stable) compaction into c.ov; info = {count, violation} on the device
-static void vl_filter(Scene& s, int* info, bool zero_info) {
+static void vl_filter(Scene& s, int* info, bool zero_info, bool contain_done = false, int* set_one = nullptr) {
   cudaStream_t st = s.stream;
   Scene::Work& w = s.w;
   Cands& c = s.cands;
   if (zero_info) CK(cudaMemsetAsync(info, 0, 2 * sizeof(int), st));
-  k_vl_contain<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, info + 1);
-  note_launch("k_vl_contain");
+  if (!contain_done) {  // (the deferred path folds the containment test into k_body_boxes)
+    k_vl_contain<<<grid_for(s.B, 256), 256, 0, st>>>(s.B, s.bbox.p, w.vl_box.p, info + 1);
+    note_launch("k_vl_contain");
+  }
   if (w.vl_n == 0) return;
   w.flags.resize(w.vl_n);
-  k_vl_flags<<<grid_for(w.vl_n, 256), 256, 0, st>>>(w.vl_n, w.vl_pairs.p, s.bbox.p, w.flags.p);
+  k_vl_flags<<<grid_for(w.vl_n, 256), 256, 0, st>>>(w.vl_n, w.vl_pairs.p, s.bbox.p, w.flags.p, set_one);
   note_launch("k_vl_flags");
   size_t bytes = 0;
   CK(cub::DeviceSelect::Flagged(nullptr, bytes, w.vl_pairs.p, w.flags.p, c.ov.p, info, (int)w.vl_n, st));
@@ -1802,8 +1814,6 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   CK(cudaMemsetAsync(w.ull.p + 4, 0, 10 * sizeof(unsigned long long), st));
   if (s.B < 2) return;
   s.bbox.resize(6 * s.B);
-  k_body_boxes<<<grid_for((int64_t)s.B * 32, 256), 256, 0, st>>>(s.B, s.v_off.p, s.rest.p, q0, q1, h, s.bbox.p);
-  note_launch("k_body_boxes");
   // body pairs: filter the superset with the exact boxes (one CTA, one sync); rebuild
   // the superset on the uniform grid when a box left its inflated box
   static const double vl_frac = getenv("ABD_VL_MARGIN") ? atof(getenv("ABD_VL_MARGIN")) : 0.05;
@@ -1817,12 +1827,17 @@ void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat) {
   // counts (one sync less); a containment violation then restarts the broad phase
   static const bool no_defer = getenv("ABD_VL_SYNC") != nullptr;
   const bool defer = use_vl && w.vl_valid && !no_defer && s.max_v <= P2_VCAP && !getenv("ABD_BP_V1");
+  // (deferred path: the containment test rides in the body-box kernel; vl_info was zeroed above)
+  k_body_boxes<<<grid_for((int64_t)s.B * 32, 256), 256, 0, st>>>(s.B, s.v_off.p, s.rest.p, q0, q1, h, s.bbox.p,
+                                                                 defer ? w.vl_box.p : nullptr, vl_info + 1);
+  note_launch("k_body_boxes");
   if (defer) {
     if ((int64_t)c.ov.cap < std::max<int64_t>(w.vl_n, 1)) c.ov.resize(std::max<int64_t>(w.vl_n, 1));
-    vl_filter(s, vl_info, false);
     int* ov_same = reinterpret_cast<int*>(w.ull.p + 9);  // zeroed with the broad phase's scalars
-    if (w.pat_valid && s.H.n == s.n_dyn) {
-      dev_set_i32(st, ov_same, 1);
+    const bool check_pat = w.pat_valid && s.H.n == s.n_dyn;
+    vl_filter(s, vl_info, false, /*contain_done=*/true, check_pat && w.vl_n > 0 ? ov_same : nullptr);
+    if (check_pat) {
+      if (w.vl_n == 0) dev_set_i32(st, ov_same, 1);
       k_ov_in_pattern<<<grid_for(std::max<int64_t>(w.vl_n, 1), 256), 256, 0, st>>>(
           w.vl_n, c.ov.p, s.slot.p, s.H.n_off, s.H.upper_keys.p, ov_same, vl_info);
       note_launch("k_ov_in_pattern");
