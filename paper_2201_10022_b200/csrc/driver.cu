@@ -587,7 +587,8 @@ static void mark_structure(Scene& s) {
   chol_analysis_post(s);
 }
 
-void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v) {
+void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v,
+              double* neg_out) {
   int n = s.n_dyn;
   s.w.grad0.resize(std::max(12 * n, 1));
   s.w.diag0.resize(std::max(144 * n, 1));
@@ -617,7 +618,7 @@ void assemble(Scene& s, const double* q, const double* qt, double dt, double kap
   HMARK();
   append_friction_blocks(s, q, dt, eps_v, 1);
   if (body_forked) CK(cudaStreamWaitEvent(s.stream, s.join_ev, 0));
-  reduce_system(s, s.w.diag0.p, s.w.grad0.p);
+  reduce_system(s, s.w.diag0.p, s.w.grad0.p, s.comm.world > 1 ? nullptr : neg_out);
   HMARK();
   if (s.comm.world > 1) {
     // the replicated system: sum of the ranks' partial assemblies
@@ -676,14 +677,18 @@ void advance_step(Scene& s, const double* forces_host, const abd_step_params& P,
     bool converged = false;
     for (int it = 0; it < P.max_newton_iters; ++it) {
       t0 = clk::now();
-      assemble(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v);
+      // single rank with every dynamic body a row: the reduction writes -g as well
+      const bool fuse_neg = s.comm.world == 1 && ND > 0;
+      assemble(s, s.q.p, s.q_tilde.p, P.dt, P.kappa_barrier, P.d_hat, P.epsilon_v, fuse_neg ? s.w.neg.p : nullptr);
       st.t_assemble += ms(t0, clk::now());
       t0 = clk::now();
       double amax = 0.0, gd = 0.0, rel = 0.0;
       int pcg_it = 0;
       if (ND) {
-        k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
-        note_launch("k_neg");
+        if (!(fuse_neg && s.H.n == s.n_dyn)) {
+          k_neg<<<grid_for(ND, 256), 256, 0, stream>>>(ND, s.grad.p, s.w.neg.p);
+          note_launch("k_neg");
+        }
         const bool reduced = s.red_nu > 0;  // joints: dense T^T H T (k_reduced.cu)
         // multi-rank: distributed PCG over the slabs, slab-local Cholesky preconditioner
         const bool slab = !reduced && P.linear_solver != 1 && s.comm.world > 1;

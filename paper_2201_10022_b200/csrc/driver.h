@@ -8,7 +8,7 @@ namespace abd {
 void broad_phase(Scene& s, const double* q0, const double* q1, double d_hat);
 // k_solve.cu
 void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64_t n_f, bool from_cands = false);
-void reduce_system(Scene& s, const double* diag0, const double* grad0);
+void reduce_system(Scene& s, const double* diag0, const double* grad0, double* neg_out = nullptr);
 int pcg_solve(Scene& s, const double* rhs, double* x, double rel_tol, int max_iters, double& rel_res);
 // k_chol.cu: sparse block Cholesky + refinement; returns the number of triangular solves
 int chol_solve(Scene& s, const double* rhs, double* x, double rel_tol, double& rel_res, int max_refine = 3);
@@ -58,7 +58,9 @@ double body_energy(Scene& s, const double* q, const double* qt, double dt);
 double ip_value(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v);
 double step_filter(Scene& s, const double* q, const double* dq, double slack);
 double candidate_min_d2(Scene& s, const double* q);
-void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v);
+// neg_out: also write -gradient (12 n_dyn doubles; single rank only -- a partitioned system is summed afterwards)
+void assemble(Scene& s, const double* q, const double* qt, double dt, double kappa, double dh, double eps_v,
+              double* neg_out = nullptr);
 void advance_step(Scene& s, const double* forces_host, const abd_step_params& P, abd_step_stats& st, double* trace);
 
 }  // namespace abd

@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
                                                                  const double* __restrict__ grad0, double* val,
                                                                  double* grad, const int* __restrict__ row_of,
                                                                  int* sorted_out, int64_t n_rec,
-                                                                 const double* __restrict__ run_part) {
+                                                                 const double* __restrict__ run_part,
+                                                                 double* neg_out) {
   __shared__ double srec[RB_WARPS][RB_PER_LANE * 32];
   __shared__ double part[RB_WARPS][160];
   __shared__ double gpart[RB_WARPS][12];
@@ -291,7 +292,10 @@ __global__ void __launch_bounds__(32 * RB_WARPS) k_reduce_blocks(int n, const in
     if (idx < 144) out[idx] = acc[e];
   }
   if (is_diag) {
-    if (lane < 12) grad[12 * (int64_t)r + lane] = gacc;
+    if (lane < 12) {
+      grad[12 * (int64_t)r + lane] = gacc;
+      if (neg_out) neg_out[12 * (int64_t)r + lane] = -gacc;  // the Newton right-hand side (saves k_neg)
+    }
   } else {
     int lw = find_col(row_ptr, col, c, r);
     double* o2 = val + 144 * (int64_t)lw;
@@ -402,7 +406,7 @@ void build_pattern(Scene& s, const int2* ov, int64_t n_ov, const int2* fb, int64
 }
 
 // reduce resident pair blocks (s.pblk, n_pairs) + per-body diag0/grad0 into H, grad
-void reduce_system(Scene& s, const double* diag0, const double* grad0) {
+void reduce_system(Scene& s, const double* diag0, const double* grad0, double* neg_out) {
   Bsr& H = s.H;
   cudaStream_t st = s.stream;
   int n = H.n;
@@ -476,7 +480,7 @@ void reduce_system(Scene& s, const double* diag0, const double* grad0) {
   s.grad.resize(12 * (int64_t)n);
   k_reduce_blocks<<<grid_for(H.nnzb, RB_POS), 32 * RB_WARPS, 0, st>>>(n, H.row_ptr.p, H.col.p, sb, se, cv,
                                                               s.pblk.blk.p, diag0, grad0, H.val.p, s.grad.p,
-                                                              row_of.p, sorted_out, np, s.pblk.run_part.p);
+                                                              row_of.p, sorted_out, np, s.pblk.run_part.p, neg_out);
   note_launch("k_reduce_blocks");
 }
 
