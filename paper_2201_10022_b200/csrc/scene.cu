@@ -38,13 +38,18 @@ Scene::Scene() {
   int dev = 0;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  // the main stream carries the critical path: its pending CTAs are dispatched ahead of the
+  // side streams' (a 4-wave side kernel launched first -- k_body_derivs -- otherwise holds up
+  // the activity scan behind it for ~40 us per Newton iteration)
+  int prio_least = 0, prio_greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+  CK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_greatest));
   main_stream = stream;
-  CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio_least));
   CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
-  CK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&side3, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, prio_least));
+  CK(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, prio_least));
   CK(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&plan_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&moll_fork_ev, cudaEventDisableTiming));
